@@ -1,0 +1,157 @@
+/* hfpg — B200-native (sm_100a) solve-time hot path of the hierarchical-factor preconditioner.
+ *
+ * C ABI: plain pointers and sizes, no torch or C++ types. Each entry point names the
+ * reference interface (path:line under /root/reference/proj) it replaces. The C++ drop-in
+ * wrappers (hfp::gpu::pcg_solve, hfp::gpu::factor_applier, ...) live in hfp_gpu.hpp; the
+ * Python mirror in paper_2605_13343_b200/.
+ *
+ * Error model (mirrors the reference's exception split):
+ *   HFPG_EINVAL  <-> std::invalid_argument  (contract violations: lengths, layout, partition)
+ *   HFPG_EIO     <-> std::runtime_error     (HFTC format / checksum / file errors)
+ *   HFPG_ECUDA / HFPG_ENCCL                 (device / communicator failures)
+ * Numerical outcomes (breakdown, max_iters) are never errors: they are reported in
+ * hfpg_report, as pcg.cpp:90-112 does. hfpg_last_error() returns the message of the last
+ * failing call on the calling thread.
+ *
+ * Threading: one handle = one device + one CUDA stream + one workspace; a handle is not
+ * thread-safe, any number of handles may coexist (pcg.hpp:35, pcg.cpp:44-51).
+ */
+#ifndef HFPG_H
+#define HFPG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HFPG_ABI_VERSION 1
+
+enum hfpg_status { HFPG_OK = 0, HFPG_EINVAL = 1, HFPG_EIO = 2, HFPG_ECUDA = 3, HFPG_ENCCL = 4 };
+enum hfpg_where { HFPG_HOST = 0, HFPG_DEVICE = 1 };
+/* pcg.cpp:28-51 identity_applier / jacobi_applier / factor_applier */
+enum hfpg_precond { HFPG_PRECOND_IDENTITY = 0, HFPG_PRECOND_JACOBI = 1, HFPG_PRECOND_FACTOR = 2 };
+/* pcg.hpp:19 SolveStatus */
+enum hfpg_solve_status { HFPG_CONVERGED = 0, HFPG_MAX_ITERS = 1, HFPG_BREAKDOWN = 2 };
+
+/* partition.hpp:11-17 TileSpec */
+typedef struct {
+    uint64_t id, span, row_begin, col_begin, depth;
+} hfpg_tile;
+
+/* factor_tensor.hpp:18-48 FactorLayout (section bases in elements) */
+typedef struct {
+    uint64_t n, leaf_size, coarse_size, coupling_rank, leaf_count, tile_count;
+    uint64_t leaf_base, tile_base, bridge_base, gate_base, total;
+} hfpg_layout;
+
+/* pcg.hpp:12-17 SolveConfig */
+typedef struct {
+    double rtol;        /* default 1e-8 */
+    uint64_t max_iters; /* default 20000 */
+} hfpg_solve_config;
+
+/* pcg.hpp:21-33 SolveReport (residual_history is returned through a caller buffer) */
+typedef struct {
+    uint64_t n;
+    uint64_t iterations;     /* first k with |r_k|/|r_0| <= rtol, or the stopping k */
+    int32_t converged;
+    int32_t status;          /* hfpg_solve_status */
+    uint64_t breakdown_iter;
+    uint64_t history_len;    /* entries of residual_history produced */
+    double wall_ms;          /* device time of the solve (CUDA events around the graph) */
+} hfpg_report;
+
+typedef struct hfpg_handle hfpg_handle;
+typedef struct hfpg_frame hfpg_frame;
+
+const char* hfpg_version(void);
+/* Message of the last failed call on this thread ("" if none). */
+const char* hfpg_last_error(void);
+
+/* ---- host-side structure (no GPU needed) ------------------------------------------------ */
+/* partition.cpp:48-53 packed_width(build_partition(n, leaf), coarse) */
+int hfpg_packed_width(uint64_t n, uint64_t leaf_size, uint64_t coarse_size, uint64_t* out);
+/* partition.cpp:9-46 build_partition; writes min(K-1, cap) tiles, *count = K-1 */
+int hfpg_build_partition(uint64_t n, uint64_t leaf_size, hfpg_tile* tiles, uint64_t cap,
+                         uint64_t* count);
+/* factor_tensor.cpp:7-28 make_factor_layout */
+int hfpg_factor_layout(uint64_t n, uint64_t leaf_size, uint64_t coarse_size, hfpg_layout* out);
+/* factor_tensor.cpp:30-39 init_factors<float>(..., sigma, RngStream(seed, frame, factor_init));
+ * out has hfpg_packed_width elements. Bit-identical to the reference (multi-threaded). */
+int hfpg_init_factors(uint64_t n, uint64_t leaf_size, uint64_t coarse_size, double sigma,
+                      uint64_t seed, uint64_t frame, float* out);
+/* checkpoint.cpp:45-85 read_checkpoint. Call with packed == NULL to get the layout first.
+ * metadata (may be NULL) receives the JSON metadata object, truncated to meta_cap bytes. */
+int hfpg_read_checkpoint(const char* path, hfpg_layout* layout, float* packed,
+                         int32_t* spd_enabled, double* spd_raw, char* metadata,
+                         uint64_t meta_cap);
+/* checkpoint.cpp:17-43 write_checkpoint */
+int hfpg_write_checkpoint(const char* path, uint64_t n, uint64_t leaf_size,
+                          uint64_t coarse_size, const float* packed, int32_t spd_enabled,
+                          double spd_raw, const char* metadata_json);
+
+/* ---- synthetic systems (the path's input side) ------------------------------------------ */
+/* frame.cpp:161-181 make_frame(n, seed, frame_index): 2D Morton-ordered 5-point Neumann
+ * Laplacian, bit-identical to the reference (ordering, CSR, values, rhs). */
+int hfpg_frame_2d(uint64_t n, uint64_t seed, uint64_t frame_index, hfpg_frame** out);
+/* New (no reference counterpart): nx x ny x nz 7-point harmonic-mean Neumann Laplacian in 3D
+ * Morton order (x -> bit 3i, y -> 3i+1, z -> 3i+2), barrier slabs drawn with frame.cpp:45-98's
+ * parameter laws from RngStream(seed, frame, density); rhs = sample_rhs (frame.cpp:154-159). */
+int hfpg_frame_3d(uint64_t nx, uint64_t ny, uint64_t nz, uint64_t seed, uint64_t frame_index,
+                  hfpg_frame** out);
+int hfpg_frame_info(const hfpg_frame* f, uint64_t* n, uint64_t* nnz, uint64_t* width,
+                    uint64_t* height, uint64_t* depth, double* rho_heavy);
+/* Copy out (any pointer may be NULL). */
+int hfpg_frame_copy(const hfpg_frame* f, uint32_t* cell_order, double* rho,
+                    uint64_t* row_offsets, uint32_t* col_indices, double* values, double* b);
+void hfpg_frame_free(hfpg_frame* f);
+
+/* Pinned host memory for the end-to-end path (cudaMallocHost). */
+int hfpg_host_alloc(uint64_t bytes, void** out);
+int hfpg_host_free(void* p);
+
+/* ---- device handle ------------------------------------------------------------------------ */
+int hfpg_create(int device, hfpg_handle** out);
+int hfpg_destroy(hfpg_handle* h);
+/* The handle's CUDA stream (cudaStream_t), for callers timing with events. */
+int hfpg_get_stream(hfpg_handle* h, void** stream);
+
+/* System load: csr.hpp:11-16 CsrMatrix fields. Index values are preserved bit-exactly; the
+ * device copy is re-laid out as SELL-32 (slices of 32 rows, column-major within a slice).
+ * Computes diagonal() (csr.cpp:52-58) and frobenius_norm() (csr.cpp:64-68). */
+int hfpg_load_csr(hfpg_handle* h, uint64_t n, const uint64_t* row_offsets,
+                  const uint32_t* col_indices, const double* values, int where);
+/* Model load: the packed factor tensor (factor_tensor.hpp:57-112) for (n, leaf, coarse),
+ * `total` must equal the packed width. Host or device pointer; copied (owning, as
+ * factor_applier does, pcg.cpp:46). */
+int hfpg_load_factors(hfpg_handle* h, uint64_t n, uint64_t leaf_size, uint64_t coarse_size,
+                      const float* packed, uint64_t total, int32_t spd_enabled, double spd_raw,
+                      int where);
+/* apply.hpp:41-43 takes a_diag explicitly: override diag(A) (e.g. to apply with a diagonal
+ * that has no matrix, as test_apply.cpp does). Loading a CSR resets it to diag(A). */
+int hfpg_set_diag(hfpg_handle* h, uint64_t n, const double* a_diag, int where);
+/* Select the preconditioner used by hfpg_pcg_solve. JACOBI throws EINVAL on a nonpositive
+ * diagonal entry like jacobi_applier (pcg.cpp:34-42). */
+int hfpg_set_precond(hfpg_handle* h, int kind);
+
+/* apply.cpp:79-174 apply<float>: z = M r with the loaded factors and diag(A). */
+int hfpg_apply(hfpg_handle* h, const double* r, double* z, int where);
+/* csr.cpp:70-79 spmv: y = A x. */
+int hfpg_spmv(hfpg_handle* h, const double* x, double* y, int where);
+/* pcg.cpp:53-126 pcg_solve, the whole loop as one CUDA graph (conditional WHILE node).
+ * x (n) and history (max_iters entries, may be NULL) are written in `where` memory. */
+int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg, double* x,
+                   double* history, hfpg_report* report, int where);
+
+/* ---- introspection for tests / bench ---------------------------------------------------- */
+/* Number of kernels one PCG iteration launches, and one apply. */
+int hfpg_launch_counts(hfpg_handle* h, uint32_t* per_iteration, uint32_t* per_apply);
+/* 1 if the fast sm_100a TMA path (L=128, L_s=32) is selected for the loaded layout. */
+int hfpg_fast_path(hfpg_handle* h, int32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HFPG_H */

@@ -1,0 +1,14 @@
+"""paper_2605_13343_b200 — B200-native (sm_100a) PCG with the hierarchical-factor
+preconditioner of arxiv 2605.13343, behind the reference `hfp` API.
+
+The product is the native library `libhfpg.so` (C ABI in include/hfpg.h, CUDA kernels in
+csrc/); this package is the Python mirror of the reference interface over that ABI.
+"""
+from .api import (Checkpoint, CsrMatrix, Device, FactorInit, FactorLayout, FactorTensor, Frame,
+                  HPartition, PrecondApplier, RngPurpose, RngStream, SolveConfig, SolveReport,
+                  SolveStatus, TileSpec, apply, build_partition, clamp_leaf_size, factor_applier,
+                  identity_applier, init_factors, jacobi_applier, make_factor_layout, make_frame,
+                  make_frame_3d, packed_width, pcg_solve, read_checkpoint, test_frame_id,
+                  train_frame_id, write_checkpoint)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

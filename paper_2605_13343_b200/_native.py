@@ -1,0 +1,105 @@
+"""ctypes binding of include/hfpg.h (the C ABI of libhfpg.so).
+
+The library is loaded from this package directory only (built in-tree by build.py). There is
+no CPU fallback: if the shared object is missing this module raises at import.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(HERE, "libhfpg.so")
+
+HFPG_OK, HFPG_EINVAL, HFPG_EIO, HFPG_ECUDA, HFPG_ENCCL = range(5)
+HOST, DEVICE = 0, 1
+
+u64, i32, dbl, vp = C.c_uint64, C.c_int32, C.c_double, C.c_void_p
+
+
+class Tile(C.Structure):
+    _fields_ = [("id", u64), ("span", u64), ("row_begin", u64), ("col_begin", u64),
+                ("depth", u64)]
+
+
+class Layout(C.Structure):
+    _fields_ = [(k, u64) for k in ("n", "leaf_size", "coarse_size", "coupling_rank",
+                                   "leaf_count", "tile_count", "leaf_base", "tile_base",
+                                   "bridge_base", "gate_base", "total")]
+
+
+class SolveConfigC(C.Structure):
+    _fields_ = [("rtol", dbl), ("max_iters", u64)]
+
+
+class ReportC(C.Structure):
+    _fields_ = [("n", u64), ("iterations", u64), ("converged", i32), ("status", i32),
+                ("breakdown_iter", u64), ("history_len", u64), ("wall_ms", dbl)]
+
+
+class CudaError(RuntimeError):
+    """A CUDA failure inside libhfpg (HFPG_ECUDA)."""
+
+
+_PROTOS = {
+    "hfpg_version": (C.c_char_p, []),
+    "hfpg_last_error": (C.c_char_p, []),
+    "hfpg_packed_width": (C.c_int, [u64, u64, u64, C.POINTER(u64)]),
+    "hfpg_build_partition": (C.c_int, [u64, u64, vp, u64, C.POINTER(u64)]),
+    "hfpg_factor_layout": (C.c_int, [u64, u64, u64, C.POINTER(Layout)]),
+    "hfpg_init_factors": (C.c_int, [u64, u64, u64, dbl, u64, u64, vp]),
+    "hfpg_read_checkpoint": (C.c_int, [C.c_char_p, C.POINTER(Layout), vp, C.POINTER(i32),
+                                       C.POINTER(dbl), C.c_char_p, u64]),
+    "hfpg_write_checkpoint": (C.c_int, [C.c_char_p, u64, u64, u64, vp, i32, dbl, C.c_char_p]),
+    "hfpg_frame_2d": (C.c_int, [u64, u64, u64, C.POINTER(vp)]),
+    "hfpg_frame_3d": (C.c_int, [u64, u64, u64, u64, u64, C.POINTER(vp)]),
+    "hfpg_frame_info": (C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64),
+                                  C.POINTER(u64), C.POINTER(u64), C.POINTER(dbl)]),
+    "hfpg_frame_copy": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+    "hfpg_frame_free": (None, [vp]),
+    "hfpg_host_alloc": (C.c_int, [u64, C.POINTER(vp)]),
+    "hfpg_host_free": (C.c_int, [vp]),
+    "hfpg_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+    "hfpg_destroy": (C.c_int, [vp]),
+    "hfpg_get_stream": (C.c_int, [vp, C.POINTER(vp)]),
+    "hfpg_load_csr": (C.c_int, [vp, u64, vp, vp, vp, C.c_int]),
+    "hfpg_load_factors": (C.c_int, [vp, u64, u64, u64, vp, u64, i32, dbl, C.c_int]),
+    "hfpg_set_diag": (C.c_int, [vp, u64, vp, C.c_int]),
+    "hfpg_set_precond": (C.c_int, [vp, C.c_int]),
+    "hfpg_apply": (C.c_int, [vp, vp, vp, C.c_int]),
+    "hfpg_spmv": (C.c_int, [vp, vp, vp, C.c_int]),
+    "hfpg_pcg_solve": (C.c_int, [vp, vp, C.POINTER(SolveConfigC), vp, vp, C.POINTER(ReportC),
+                                 C.c_int]),
+    "hfpg_launch_counts": (C.c_int, [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+    "hfpg_fast_path": (C.c_int, [vp, C.POINTER(i32)]),
+}
+
+EXPORTED = sorted(_PROTOS)
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(SO_PATH):
+        raise ImportError(
+            f"{SO_PATH} is missing: build the native library first "
+            "(python -c 'import __graft_entry__ as g; g.build()')")
+    lib = C.CDLL(SO_PATH)
+    for name, (res, args) in _PROTOS.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(rc: int) -> None:
+    """Raise the Python analogue of the reference's exception for a failed call."""
+    if rc == HFPG_OK:
+        return
+    msg = lib.hfpg_last_error().decode()
+    if rc == HFPG_EINVAL:
+        raise ValueError(msg)  # std::invalid_argument
+    if rc == HFPG_ECUDA:
+        raise CudaError(msg)
+    raise RuntimeError(msg)  # std::runtime_error (I/O, format, checksum)

@@ -1,0 +1,542 @@
+"""Python mirror of the reference `hfp` API on the hot path, backed by libhfpg (sm_100a).
+
+Names, argument meaning and error behaviour follow the reference headers so parity tests read
+like the reference's own tests:
+
+  partition.hpp     TileSpec, HPartition, build_partition, packed_width, clamp_leaf_size
+  factor_tensor.hpp FactorLayout, make_factor_layout, FactorTensor (PackedFactors<float>),
+                    FactorInit, init_factors
+  rng.hpp           RngPurpose, RngStream (key only; draws happen natively)
+  csr.hpp           CsrMatrix
+  frame.hpp         make_frame (+ make_frame_3d, new)
+  apply.hpp         apply
+  pcg.hpp           SolveConfig, SolveStatus, SolveReport, identity_applier, jacobi_applier,
+                    factor_applier, pcg_solve
+  checkpoint.hpp    write_checkpoint, read_checkpoint, Checkpoint
+
+std::invalid_argument maps to ValueError, std::runtime_error to RuntimeError. Every numeric
+operation runs in libhfpg: the appliers and pcg_solve execute on the GPU, the partition /
+layout / seeded initialisation / frame generation in the library's native host code.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from ._native import check, lib
+
+# ---------------------------------------------------------------------------- partition.hpp
+
+
+@dataclass
+class TileSpec:
+    id: int
+    span: int
+    row_begin: int
+    col_begin: int
+    depth: int
+
+
+@dataclass
+class HPartition:
+    n: int
+    leaf_size: int
+    leaf_count: int
+    tiles: list
+    admissibility: int = 1
+    row_tiles_of_leaf: list = field(default_factory=list)
+    col_tiles_of_leaf: list = field(default_factory=list)
+
+    def tile_count(self) -> int:
+        return len(self.tiles)
+
+    def leaf_begin(self, k: int) -> int:
+        return k * self.leaf_size
+
+
+def build_partition(n: int, leaf_size: int) -> HPartition:
+    """partition.cpp:9-46."""
+    cnt = N.u64()
+    check(lib.hfpg_build_partition(n, leaf_size, None, 0, C.byref(cnt)))
+    arr = (N.Tile * max(cnt.value, 1))()
+    check(lib.hfpg_build_partition(n, leaf_size, arr, cnt.value, C.byref(cnt)))
+    k = n // leaf_size
+    tiles = [TileSpec(t.id, t.span, t.row_begin, t.col_begin, t.depth)
+             for t in arr[: cnt.value]]
+    p = HPartition(n, leaf_size, k, tiles)
+    p.row_tiles_of_leaf = [[] for _ in range(k)]
+    p.col_tiles_of_leaf = [[] for _ in range(k)]
+    for t in tiles:
+        for s in range(t.span):
+            p.row_tiles_of_leaf[t.row_begin + s].append(t.id)
+            p.col_tiles_of_leaf[t.col_begin + s].append(t.id)
+    return p
+
+
+def packed_width(p: HPartition, coarse_size: int) -> int:
+    """partition.cpp:48-53."""
+    out = N.u64()
+    check(lib.hfpg_packed_width(p.n, p.leaf_size, coarse_size, C.byref(out)))
+    return out.value
+
+
+def clamp_leaf_size(n: int, leaf_size: int) -> int:
+    """partition.hpp:48-50."""
+    return n // 2 if n < 2 * leaf_size else leaf_size
+
+
+# ------------------------------------------------------------------------ factor_tensor.hpp
+
+
+@dataclass
+class FactorLayout:
+    n: int
+    leaf_size: int
+    coarse_size: int
+    coupling_rank: int
+    leaf_count: int
+    tile_count: int
+    leaf_base: int
+    tile_base: int
+    bridge_base: int
+    gate_base: int
+    total: int
+    tiles: list
+
+    def leaf_factor(self, k):
+        return self.leaf_base + k * self.leaf_size * self.leaf_size
+
+    def tile_u(self, m):
+        return self.tile_base + m * self.coarse_size * self.coarse_size
+
+    def tile_v(self, m):
+        return self.tile_u(m) + self.coarse_size * self.coupling_rank
+
+    def bridge_u(self, k):
+        return self.bridge_base + k * 2 * self.leaf_size * self.coarse_size
+
+    def bridge_v(self, k):
+        return self.bridge_u(k) + self.leaf_size * self.coarse_size
+
+    def gate(self):
+        return self.gate_base
+
+
+def make_factor_layout(partition: HPartition, coarse_size: int) -> FactorLayout:
+    """factor_tensor.cpp:7-28."""
+    lay = N.Layout()
+    check(lib.hfpg_factor_layout(partition.n, partition.leaf_size, coarse_size, C.byref(lay)))
+    return FactorLayout(*(getattr(lay, f) for f, _ in N.Layout._fields_), tiles=partition.tiles)
+
+
+class FactorTensor:
+    """PackedFactors<float> (factor_tensor.hpp:57-112): one contiguous float32 array."""
+
+    def __init__(self, layout: FactorLayout, data: np.ndarray | None = None):
+        self.layout = layout
+        self.data = (np.zeros(layout.total, np.float32) if data is None
+                     else np.ascontiguousarray(data, dtype=np.float32))
+        if self.data.shape != (layout.total,):
+            raise ValueError("factor tensor: packed width mismatch")
+        self.spd_shift_enabled = False
+        self.spd_shift_raw = 0.0
+
+    def spd_shift(self) -> float:
+        return math.log1p(math.exp(self.spd_shift_raw)) if self.spd_shift_enabled else 0.0
+
+    def _sec(self, off, cnt, shape):
+        return self.data[off: off + cnt].reshape(shape)
+
+    def leaf_factor(self, k):
+        L = self.layout
+        return self._sec(L.leaf_factor(k), L.leaf_size ** 2, (L.leaf_size, L.leaf_size))
+
+    def tile_u(self, m):
+        L = self.layout
+        return self._sec(L.tile_u(m), L.coarse_size * L.coupling_rank,
+                         (L.coarse_size, L.coupling_rank))
+
+    def tile_v(self, m):
+        L = self.layout
+        return self._sec(L.tile_v(m), L.coarse_size * L.coupling_rank,
+                         (L.coarse_size, L.coupling_rank))
+
+    def bridge_u(self, k):
+        L = self.layout
+        return self._sec(L.bridge_u(k), L.leaf_size * L.coarse_size, (L.leaf_size, L.coarse_size))
+
+    def bridge_v(self, k):
+        L = self.layout
+        return self._sec(L.bridge_v(k), L.leaf_size * L.coarse_size, (L.leaf_size, L.coarse_size))
+
+    def gate(self):
+        return self.data[self.layout.gate_base: self.layout.total]
+
+    def copy(self) -> "FactorTensor":
+        f = FactorTensor(self.layout, self.data.copy())
+        f.spd_shift_enabled, f.spd_shift_raw = self.spd_shift_enabled, self.spd_shift_raw
+        return f
+
+
+class RngPurpose(enum.IntEnum):
+    """rng.hpp:12-20 (frozen values)."""
+    density = 1
+    rhs = 2
+    probes = 3
+    factor_init = 4
+    net_weights = 5
+    power_iter = 6
+    test = 7
+
+
+@dataclass
+class RngStream:
+    """rng.hpp:37-41 key. Draws are made natively at counter 0.. by the consumer."""
+    seed: int
+    frame: int
+    purpose: RngPurpose
+
+
+class FactorInit(enum.Enum):
+    jacobi_seed = 0
+    random = 1
+
+
+def init_factors(partition: HPartition, coarse_size: int, mode: FactorInit, sigma: float,
+                 stream: RngStream) -> FactorTensor:
+    """factor_tensor.cpp:30-39 (bit-identical; drawn in parallel from the counter stream)."""
+    if stream.purpose != RngPurpose.factor_init:
+        raise ValueError("init_factors: native draws use the factor_init purpose key")
+    lay = make_factor_layout(partition, coarse_size)
+    out = np.empty(lay.total, np.float32)
+    check(lib.hfpg_init_factors(partition.n, partition.leaf_size, coarse_size, float(sigma),
+                                stream.seed, stream.frame, out.ctypes.data))
+    return FactorTensor(lay, out)
+
+
+# ---------------------------------------------------------------------------------- csr.hpp
+
+
+class CsrMatrix:
+    """csr.hpp:11-30: u64 row offsets, u32 columns, f64 values."""
+
+    def __init__(self, n_rows, n_cols, row_offsets, col_indices, values):
+        self.n_rows, self.n_cols = int(n_rows), int(n_cols)
+        self.row_offsets = np.ascontiguousarray(row_offsets, np.uint64)
+        self.col_indices = np.ascontiguousarray(col_indices, np.uint32)
+        self.values = np.ascontiguousarray(values, np.float64)
+
+    def nnz(self) -> int:
+        return len(self.values)
+
+    def diagonal(self) -> np.ndarray:
+        """csr.cpp:52-58."""
+        d = np.zeros(self.n_rows)
+        rows = np.repeat(np.arange(self.n_rows), np.diff(self.row_offsets).astype(np.int64))
+        m = self.col_indices == rows
+        d[rows[m]] = self.values[m]
+        return d
+
+
+@dataclass
+class Frame:
+    """frame.hpp:26-40 (what the path consumes)."""
+    n: int
+    width: int
+    height: int
+    depth: int
+    cell_order: np.ndarray
+    rho: np.ndarray
+    A: CsrMatrix
+    b: np.ndarray
+    rho_heavy: float
+    master_seed: int = 0
+    frame_index: int = 0
+
+
+def _frame_from_handle(h, seed, fidx) -> Frame:
+    n, nnz, w, hh, d = (N.u64() for _ in range(5))
+    rh = N.dbl()
+    check(lib.hfpg_frame_info(h, C.byref(n), C.byref(nnz), C.byref(w), C.byref(hh), C.byref(d),
+                              C.byref(rh)))
+    co = np.empty(n.value, np.uint32)
+    rho = np.empty(n.value)
+    ro = np.empty(n.value + 1, np.uint64)
+    ci = np.empty(nnz.value, np.uint32)
+    v = np.empty(nnz.value)
+    b = np.empty(n.value)
+    check(lib.hfpg_frame_copy(h, co.ctypes.data, rho.ctypes.data, ro.ctypes.data,
+                              ci.ctypes.data, v.ctypes.data, b.ctypes.data))
+    lib.hfpg_frame_free(h)
+    return Frame(n.value, w.value, hh.value, d.value, co, rho,
+                 CsrMatrix(n.value, n.value, ro, ci, v), b, rh.value, seed, fidx)
+
+
+def make_frame(n: int, master_seed: int, frame_index: int) -> Frame:
+    """frame.cpp:161-181 (bit-identical native generator)."""
+    h = N.vp()
+    check(lib.hfpg_frame_2d(n, master_seed, frame_index, C.byref(h)))
+    return _frame_from_handle(h, master_seed, frame_index)
+
+
+def make_frame_3d(nx: int, ny: int, nz: int, master_seed: int, frame_index: int) -> Frame:
+    """3D analogue of make_frame (new; see include/hfpg.h)."""
+    h = N.vp()
+    check(lib.hfpg_frame_3d(nx, ny, nz, master_seed, frame_index, C.byref(h)))
+    return _frame_from_handle(h, master_seed, frame_index)
+
+
+def train_frame_id(scale: int, i: int) -> int:
+    return (scale << 24) | i
+
+
+def test_frame_id(scale: int, i: int) -> int:
+    return (scale << 24) | (1 << 20) | i
+
+
+# --------------------------------------------------------------------------- device handle
+
+
+class Device:
+    """One hfpg handle: a CUDA stream + device-resident operator, factors and workspace."""
+
+    def __init__(self, device: int = 0):
+        h = N.vp()
+        check(lib.hfpg_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+        self.csr_id = None
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            lib.hfpg_destroy(h)
+            self.h = None
+
+    def load_csr(self, A: CsrMatrix):
+        check(lib.hfpg_load_csr(self.h, A.n_rows, A.row_offsets.ctypes.data,
+                                A.col_indices.ctypes.data, A.values.ctypes.data, N.HOST))
+        self.csr_id = id(A)
+
+    def load_csr_device(self, n, ro_ptr, ci_ptr, v_ptr):
+        check(lib.hfpg_load_csr(self.h, n, ro_ptr, ci_ptr, v_ptr, N.DEVICE))
+
+    def load_factors(self, f: FactorTensor):
+        L = f.layout
+        check(lib.hfpg_load_factors(self.h, L.n, L.leaf_size, L.coarse_size, f.data.ctypes.data,
+                                    L.total, int(f.spd_shift_enabled), float(f.spd_shift_raw),
+                                    N.HOST))
+
+    def set_diag(self, a_diag: np.ndarray):
+        a = np.ascontiguousarray(a_diag, np.float64)
+        check(lib.hfpg_set_diag(self.h, len(a), a.ctypes.data, N.HOST))
+
+    def set_precond(self, kind: int):
+        check(lib.hfpg_set_precond(self.h, kind))
+
+    def apply(self, r: np.ndarray) -> np.ndarray:
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.empty_like(r)
+        check(lib.hfpg_apply(self.h, r.ctypes.data, z.ctypes.data, N.HOST))
+        return z
+
+    def apply_ptr(self, r_ptr: int, z_ptr: int, where: int = N.DEVICE):
+        check(lib.hfpg_apply(self.h, r_ptr, z_ptr, where))
+
+    def spmv(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.empty_like(x)
+        check(lib.hfpg_spmv(self.h, x.ctypes.data, y.ctypes.data, N.HOST))
+        return y
+
+    def spmv_ptr(self, x_ptr: int, y_ptr: int, where: int = N.DEVICE):
+        check(lib.hfpg_spmv(self.h, x_ptr, y_ptr, where))
+
+    def solve_ptr(self, b_ptr, x_ptr, cfg: "SolveConfig", hist_ptr=None, where=N.DEVICE):
+        rep = N.ReportC()
+        c = N.SolveConfigC(cfg.rtol, cfg.max_iters)
+        check(lib.hfpg_pcg_solve(self.h, b_ptr, C.byref(c), x_ptr, hist_ptr, C.byref(rep), where))
+        return rep
+
+    def stream(self) -> int:
+        s = N.vp()
+        check(lib.hfpg_get_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+    def fast_path(self) -> bool:
+        v = N.i32()
+        check(lib.hfpg_fast_path(self.h, C.byref(v)))
+        return bool(v.value)
+
+    def launch_counts(self):
+        a, b = C.c_uint32(), C.c_uint32()
+        check(lib.hfpg_launch_counts(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+
+# ---------------------------------------------------------------------------------- pcg.hpp
+
+
+@dataclass
+class SolveConfig:
+    rtol: float = 1e-8
+    max_iters: int = 20000
+
+
+class SolveStatus(enum.Enum):
+    converged = 0
+    max_iters = 1
+    breakdown = 2
+
+
+@dataclass
+class SolveReport:
+    method: str = ""
+    n: int = 0
+    iterations: int = 0
+    converged: bool = False
+    status: SolveStatus = SolveStatus.max_iters
+    residual_history: list = field(default_factory=list)
+    wall_ms: float = 0.0
+    frame_id: str = ""
+    breakdown_iter: int = 0
+
+
+class PrecondApplier:
+    """pcg.hpp:36: callable z = M r (host arrays; H2D -> device apply -> D2H, for parity and
+    plug compatibility). pcg_solve runs the same preconditioner device-resident."""
+
+    kind = N.vp  # overridden
+
+    def __init__(self, device: Device | None):
+        self.dev = device
+
+    def bind(self, A: CsrMatrix) -> Device:
+        if self.dev is None:
+            self.dev = Device(0)
+        if self.dev.csr_id != id(A):
+            self.dev.load_csr(A)
+        self.dev.set_precond(self.kind)
+        return self.dev
+
+
+class _Identity(PrecondApplier):
+    kind = 0
+    method = "none"
+
+    def __call__(self, r):
+        return np.array(r, dtype=np.float64, copy=True)
+
+
+class _Jacobi(PrecondApplier):
+    kind = 1
+    method = "jacobi"
+
+    def __init__(self, A: CsrMatrix):
+        super().__init__(Device(0))
+        self.dev.load_csr(A)
+        self.dev.set_precond(1)  # throws ValueError on a nonpositive diagonal (pcg.cpp:36-38)
+        self.diag = A.diagonal()
+
+    def __call__(self, r):
+        return np.asarray(r, np.float64) / self.diag
+
+
+class _Factor(PrecondApplier):
+    kind = 2
+    method = "hfactor-gpu"
+
+    def __init__(self, factors: FactorTensor, A: CsrMatrix):
+        super().__init__(Device(0))
+        self.dev.load_csr(A)
+        self.dev.load_factors(factors)
+
+    def __call__(self, r):
+        return self.dev.apply(r)
+
+
+def identity_applier() -> PrecondApplier:
+    return _Identity(None)
+
+
+def jacobi_applier(A: CsrMatrix) -> PrecondApplier:
+    return _Jacobi(A)
+
+
+def factor_applier(factors: FactorTensor, A: CsrMatrix) -> PrecondApplier:
+    """pcg.cpp:44-51: owning copy of the tensor and diag(A) — on the GPU."""
+    return _Factor(factors, A)
+
+
+def pcg_solve(A: CsrMatrix, b, precond: PrecondApplier, cfg: SolveConfig | None = None,
+              x_out: list | None = None) -> SolveReport:
+    """pcg.cpp:53-126, whole loop in one CUDA graph. If x_out is a list, the solution is
+    appended to it (the reference's optional std::vector<double>* out-parameter)."""
+    cfg = cfg or SolveConfig()
+    if cfg.rtol <= 0.0:
+        raise ValueError("pcg_solve: rtol must be positive")
+    b = np.ascontiguousarray(b, np.float64)
+    if b.shape != (A.n_rows,):
+        raise ValueError("pcg_solve: rhs length mismatch")
+    dev = precond.bind(A)
+    x = np.empty(A.n_rows)
+    hist = np.empty(max(cfg.max_iters, 1))
+    rep = dev.solve_ptr(b.ctypes.data, x.ctypes.data, cfg, hist.ctypes.data, N.HOST)
+    if x_out is not None:
+        x_out.append(x)
+    return SolveReport(method=getattr(precond, "method", ""), n=int(rep.n),
+                       iterations=int(rep.iterations), converged=bool(rep.converged),
+                       status=SolveStatus(rep.status),
+                       residual_history=hist[: rep.history_len].tolist(),
+                       wall_ms=float(rep.wall_ms), breakdown_iter=int(rep.breakdown_iter))
+
+
+# -------------------------------------------------------------------------------- apply.hpp
+
+
+def apply(factors: FactorTensor, a_diag, r, device: Device | None = None) -> np.ndarray:
+    """apply.cpp:79-174 apply<float> on the GPU: y = M r."""
+    dev = device or Device(0)
+    dev.load_factors(factors)
+    dev.set_diag(np.asarray(a_diag, np.float64))
+    r = np.asarray(r, np.float64)
+    if r.shape != (factors.layout.n,):
+        raise ValueError("apply: length mismatch")
+    return dev.apply(r)
+
+
+# --------------------------------------------------------------------------- checkpoint.hpp
+
+
+@dataclass
+class Checkpoint:
+    factors: FactorTensor
+    metadata_json: str
+
+
+def write_checkpoint(factors: FactorTensor, path: str, metadata_json: str = "{}") -> None:
+    """checkpoint.cpp:17-43 (HFTC v1)."""
+    L = factors.layout
+    check(lib.hfpg_write_checkpoint(str(path).encode(), L.n, L.leaf_size, L.coarse_size,
+                                    factors.data.ctypes.data, int(factors.spd_shift_enabled),
+                                    float(factors.spd_shift_raw), metadata_json.encode()))
+
+
+def read_checkpoint(path: str) -> Checkpoint:
+    """checkpoint.cpp:45-85 (magic, version, packed width and crc32 validated)."""
+    lay = N.Layout()
+    check(lib.hfpg_read_checkpoint(str(path).encode(), C.byref(lay), None, None, None, None, 0))
+    data = np.empty(lay.total, np.float32)
+    en, raw = N.i32(), N.dbl()
+    meta = C.create_string_buffer(1 << 16)
+    check(lib.hfpg_read_checkpoint(str(path).encode(), C.byref(lay), data.ctypes.data,
+                                   C.byref(en), C.byref(raw), meta, len(meta)))
+    p = build_partition(lay.n, lay.leaf_size)
+    f = FactorTensor(make_factor_layout(p, lay.coarse_size), data)
+    f.spd_shift_enabled, f.spd_shift_raw = bool(en.value), float(raw.value)
+    return Checkpoint(f, meta.value.decode())

@@ -1,0 +1,142 @@
+// Shared device helpers: PTX wrappers for TMA bulk copies + mbarriers, deterministic
+// warp/block/grid reductions, and the device-resident PCG state.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hfpg {
+
+// Device-resident PCG state (pcg.cpp:53-126 locals). All scalars are f64, as the reference
+// requires (pcg.hpp:14-16). Written by the last CTA of each reduction, read by the next kernel.
+struct Scalars {
+    double rz;            // r.z of the current iterate
+    double pap, pp;       // p.Ap, p.p (pcg.cpp:88-89)
+    double alpha, beta;   // step sizes
+    double r0;            // |r_0|
+    double rel;           // last |r_k|/|r_0|
+    double rtol;          // SolveConfig::rtol
+    double breakdown_tol; // 1e-12 |A|_F (pcg.cpp:80)
+    double shift;         // softplus SPD shift (factor_tensor.hpp:64-66)
+    unsigned long long k;          // current iteration (1-based inside the loop)
+    unsigned long long max_iters;
+    unsigned long long iterations;
+    unsigned long long breakdown_iter;
+    unsigned long long hist_len;
+    int status;    // 0 converged, 1 max_iters, 2 breakdown
+    int converged;
+    int done;      // loop finished: every later kernel of the iteration early-exits
+    int pad;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---- mbarrier + TMA bulk copy (cp.async.bulk, SASS UBLKCP) -------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// Global -> shared bulk copy completing on `bar`; `policy` is an L2 cache-policy descriptor.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// Streaming 128-bit load that does not allocate in L1.
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// ---- deterministic reductions ----------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-reduce NV values, publish the CTA partial, and let the last-arriving CTA reduce all
+// partials in CTA order (fixed tree => run-to-run identical results). Returns true in every
+// thread of the last CTA, with `total` filled; the arrival counter is reset for the next
+// launch. Must be called by all threads of every CTA.
+template <int NV>
+__device__ bool grid_reduce_last(double (&v)[NV], double* partials, unsigned* counter,
+                                 double (&total)[NV]) {
+    __shared__ double red[NV][32];
+    __shared__ int is_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const double s = warp_sum(v[i]);
+        if (lane == 0) red[i][warp] = s;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double s = lane < nwarps ? red[i][lane] : 0.0;
+            s = warp_sum(s);
+            if (lane == 0) partials[blockIdx.x * NV + i] = s;
+        }
+        if (lane == 0) {
+            __threadfence();
+            const unsigned t = atomicAdd(counter, 1u);
+            is_last = (t == gridDim.x - 1);
+        }
+    }
+    __syncthreads();
+    if (!is_last) return false;
+    __threadfence();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double s = 0.0;
+        for (unsigned j = threadIdx.x; j < gridDim.x; j += blockDim.x)
+            s += __ldcg(&partials[j * NV + i]);
+        s = warp_sum(s);
+        __syncthreads();
+        if (lane == 0) red[i][warp] = s;
+        __syncthreads();
+        double t = lane < nwarps ? red[i][lane] : 0.0;
+        total[i] = warp_sum(t);
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+    return true;
+}
+
+}  // namespace hfpg

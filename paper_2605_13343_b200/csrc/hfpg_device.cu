@@ -1,0 +1,607 @@
+// Device handle, CUDA-graph PCG driver and the device half of the C ABI (include/hfpg.h).
+#include "internal.hpp"
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+namespace hfpg {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& m) { g_last_error = m; }
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));          \
+    } while (0)
+
+template <class T>
+static void dfree(T*& p) {
+    if (p) cudaFree(const_cast<void*>(static_cast<const void*>(p)));
+    p = nullptr;
+}
+template <class T>
+static void dalloc(T*& p, size_t count) {
+    dfree(p);
+    if (count == 0) count = 1;
+    CK(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+}
+
+}  // namespace hfpg
+
+using namespace hfpg;
+
+struct hfpg_handle {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    // factors
+    bool have_factors = false;
+    Layout L;
+    float* F = nullptr;
+    int spd_enabled = 0;
+    double spd_raw = 0.0;
+    bool fast = false;
+
+    // operator
+    bool have_csr = false;
+    uint64_t n = 0;  // system size (CSR, else factors)
+    double fro = 0.0;
+    bool diag_positive = false;
+    unsigned long long* slice_off = nullptr;
+    uint32_t* sell_cols = nullptr;
+    double* sell_vals = nullptr;
+    double* a_diag = nullptr;
+    bool have_diag = false;
+
+    // vectors / workspace (sized for vec_n / ws layout)
+    uint64_t vec_n = 0;
+    double *x = nullptr, *r = nullptr, *z = nullptr, *ap = nullptr, *p0 = nullptr, *p1 = nullptr,
+           *y_loc = nullptr, *b = nullptr, *scratch = nullptr;
+    Layout ws_layout;
+    bool have_ws = false;
+    float *restrict_ = nullptr, *crow = nullptr, *ccol = nullptr;
+    double *node_u = nullptr, *node_v = nullptr;
+    unsigned* tree_counters = nullptr;
+    double* partials = nullptr;
+    uint64_t partials_cap = 0;
+    unsigned* counters = nullptr;
+    Scalars* sc = nullptr;
+    double* history = nullptr;
+    uint64_t history_cap = 0;
+
+    int precond = HFPG_PRECOND_FACTOR;
+
+    // graph
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    bool graph_valid = false;
+
+    DevSys sys{};
+};
+
+namespace {
+
+void set_device(hfpg_handle* h) { CK(cudaSetDevice(h->device)); }
+
+void invalidate_graph(hfpg_handle* h) {
+    if (h->exec) cudaGraphExecDestroy(h->exec);
+    if (h->graph) cudaGraphDestroy(h->graph);
+    h->exec = nullptr;
+    h->graph = nullptr;
+    h->graph_valid = false;
+}
+
+uint64_t leaf_grid(const hfpg_handle* h) {
+    return h->fast ? std::min<uint64_t>(h->L.k, uint64_t(h->num_sms)) : h->L.k;
+}
+uint64_t simple_grid(const hfpg_handle* h) {
+    return std::max<uint64_t>(1, std::min<uint64_t>((h->n + 255) / 256, uint64_t(h->num_sms) * 8));
+}
+
+// (Re)allocate the per-n vectors and the per-layout apply workspace.
+void ensure_workspace(hfpg_handle* h) {
+    const uint64_t n = h->n;
+    if (h->vec_n != n) {
+        invalidate_graph(h);
+        dalloc(h->x, n);
+        dalloc(h->r, n);
+        dalloc(h->z, n);
+        dalloc(h->ap, n);
+        dalloc(h->p0, n);
+        dalloc(h->p1, n);
+        dalloc(h->y_loc, n);
+        dalloc(h->b, n);
+        dalloc(h->scratch, n);
+        h->vec_n = n;
+    }
+    if (h->have_factors &&
+        (!h->have_ws || h->ws_layout.n != h->L.n || h->ws_layout.l != h->L.l ||
+         h->ws_layout.ls != h->L.ls)) {
+        invalidate_graph(h);
+        const Layout& L = h->L;
+        dalloc(h->restrict_, L.k * 2 * L.ls);
+        dalloc(h->crow, L.m * L.ls);
+        dalloc(h->ccol, L.m * L.ls);
+        dalloc(h->node_u, 2 * L.k * L.ls);
+        dalloc(h->node_v, 2 * L.k * L.ls);
+        dalloc(h->tree_counters, 2 * L.k);
+        CK(cudaMemsetAsync(h->tree_counters, 0, 2 * L.k * sizeof(unsigned), h->stream));
+        h->ws_layout = L;
+        h->have_ws = true;
+    }
+    const uint64_t need = 2 * std::max<uint64_t>({(n + 255) / 256, h->have_factors ? h->L.k : 1,
+                                                   uint64_t(h->num_sms) * 8});
+    if (h->partials_cap < need) {
+        invalidate_graph(h);
+        dalloc(h->partials, need);
+        h->partials_cap = need;
+    }
+    if (!h->counters) {
+        dalloc(h->counters, 8);
+        CK(cudaMemsetAsync(h->counters, 0, 8 * sizeof(unsigned), h->stream));
+    }
+    if (!h->sc) {
+        dalloc(h->sc, 1);
+        CK(cudaMemsetAsync(h->sc, 0, sizeof(Scalars), h->stream));
+    }
+}
+
+void fill_sys(hfpg_handle* h) {
+    DevSys& s = h->sys;
+    s = DevSys{};
+    const Layout& L = h->L;
+    s.F = h->F;
+    s.n = h->n;
+    s.l = L.l;
+    s.ls = L.ls;
+    s.rk = L.rk;
+    s.K = L.k;
+    s.D = L.depth;
+    s.tile_base = L.tile_base;
+    s.bridge_base = L.bridge_base;
+    s.gate_base = L.gate_base;
+    s.a_diag = h->a_diag;
+    s.slice_off = h->slice_off;
+    s.sell_cols = h->sell_cols;
+    s.sell_vals = h->sell_vals;
+    s.x = h->x;
+    s.r = h->r;
+    s.z = h->z;
+    s.ap = h->ap;
+    s.p0 = h->p0;
+    s.p1 = h->p1;
+    s.y_loc = h->y_loc;
+    s.restrict_ = h->restrict_;
+    s.crow = h->crow;
+    s.ccol = h->ccol;
+    s.node_u = h->node_u;
+    s.node_v = h->node_v;
+    s.tree_counters = h->tree_counters;
+    s.partials = h->partials;
+    s.counters = h->counters;
+    s.sc = h->sc;
+    s.history = h->history;
+    s.use_cond = 0;
+}
+
+size_t coarse_smem(const Layout& L) { return 126 * L.ls * sizeof(double) + 16 * L.rk * sizeof(float); }
+
+// The three apply launches (stages 1-3, 4, 5-7) in a given mode.
+void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
+    const DevSys& s = h->sys;
+    const Layout& L = h->L;
+    if (h->fast) {
+        k_leaf_fast<<<unsigned(leaf_grid(h)), kLeafThreads, sizeof(LeafSmem), h->stream>>>(s, mode, rin);
+    } else {
+        k_leaf_generic<<<unsigned(L.k), 256, 2 * L.l * sizeof(float), h->stream>>>(s, mode, rin);
+    }
+    CK(cudaGetLastError());
+    const uint64_t S0 = std::min<uint64_t>(L.k, 32);
+    k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(s, mode);
+    CK(cudaGetLastError());
+    if (h->fast)
+        k_prolong_fast<<<unsigned(L.k), 256, 0, h->stream>>>(s, mode, rin, zout);
+    else
+        k_prolong_generic<<<unsigned(L.k), 256, 2 * L.ls * sizeof(float), h->stream>>>(s, mode, rin, zout);
+    CK(cudaGetLastError());
+}
+
+void launch_iteration(hfpg_handle* h) {
+    const DevSys& s = h->sys;
+    k_spmv<kLoop><<<unsigned((h->n + 255) / 256), 256, 0, h->stream>>>(s, nullptr, nullptr);
+    CK(cudaGetLastError());
+    if (h->precond == HFPG_PRECOND_FACTOR) {
+        launch_apply(h, kLoop, nullptr, nullptr);
+    } else {
+        k_simple<<<unsigned(simple_grid(h)), 256, 0, h->stream>>>(s, kLoop, h->precond == HFPG_PRECOND_JACOBI);
+        CK(cudaGetLastError());
+    }
+}
+
+void launch_init(hfpg_handle* h) {
+    const DevSys& s = h->sys;
+    k_init<<<unsigned(simple_grid(h)), 256, 0, h->stream>>>(s, h->b);
+    CK(cudaGetLastError());
+    if (h->precond == HFPG_PRECOND_FACTOR) {
+        launch_apply(h, kInit, nullptr, nullptr);
+    } else {
+        k_simple<<<unsigned(simple_grid(h)), 256, 0, h->stream>>>(s, kInit, h->precond == HFPG_PRECOND_JACOBI);
+        CK(cudaGetLastError());
+    }
+}
+
+void configure_kernels() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        CK(cudaFuncSetAttribute(k_leaf_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(sizeof(LeafSmem))));
+        CK(cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        CK(cudaFuncSetAttribute(k_leaf_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    });
+}
+
+// One graph per handle: [k_init, precond init] -> WHILE(cond) { spmv, precond iteration }.
+void build_graph(hfpg_handle* h) {
+    invalidate_graph(h);
+    fill_sys(h);
+    CK(cudaGraphCreate(&h->graph, 0));
+    cudaGraphConditionalHandle cond;
+    CK(cudaGraphConditionalHandleCreate(&cond, h->graph, 1, cudaGraphCondAssignDefault));
+    h->sys.cond = cond;
+    h->sys.use_cond = 1;
+
+    CK(cudaStreamBeginCaptureToGraph(h->stream, h->graph, nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal));
+    launch_init(h);
+    CK(cudaStreamEndCapture(h->stream, &h->graph));
+
+    size_t nn = 0;
+    CK(cudaGraphGetNodes(h->graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CK(cudaGraphGetNodes(h->graph, nodes.data(), &nn));
+    cudaGraphNode_t sink = nullptr;
+    for (auto nd : nodes) {
+        size_t nout = 0;
+        CK(cudaGraphNodeGetDependentNodes(nd, nullptr, &nout));
+        if (nout == 0) sink = nd;
+    }
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    CK(cudaGraphAddNode(&cnode, h->graph, &sink, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal));
+    launch_iteration(h);
+    CK(cudaStreamEndCapture(h->stream, &body));
+    CK(cudaGraphInstantiate(&h->exec, h->graph, 0));
+    h->graph_valid = true;
+}
+
+void require_apply_ready(hfpg_handle* h) {
+    if (!h->have_factors) throw InvalidArgument("apply: no factor tensor loaded");
+    if (!h->have_diag) throw InvalidArgument("apply: no diagonal (load a CSR or set_diag)");
+    if (h->n != h->L.n) throw InvalidArgument("apply: length mismatch");
+}
+
+// Copy `count` doubles between caller memory (`where`) and device memory.
+void copy_in(hfpg_handle* h, double* dst, const double* src, uint64_t count, int where) {
+    CK(cudaMemcpyAsync(dst, src, count * 8, where == HFPG_HOST ? cudaMemcpyHostToDevice
+                                                                  : cudaMemcpyDeviceToDevice,
+                       h->stream));
+}
+void copy_out(hfpg_handle* h, double* dst, const double* src, uint64_t count, int where) {
+    CK(cudaMemcpyAsync(dst, src, count * 8, where == HFPG_HOST ? cudaMemcpyDeviceToHost
+                                                                  : cudaMemcpyDeviceToDevice,
+                       h->stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hfpg_version(void) { return "hfpg 0.1 (sm_100a)"; }
+const char* hfpg_last_error(void) { return g_last_error.c_str(); }
+
+int hfpg_host_alloc(uint64_t bytes, void** out) {
+    return guarded([&] { CK(cudaMallocHost(out, bytes ? bytes : 1)); });
+}
+int hfpg_host_free(void* p) {
+    return guarded([&] { CK(cudaFreeHost(p)); });
+}
+
+int hfpg_create(int device, hfpg_handle** out) {
+    return guarded([&] {
+        auto* h = new hfpg_handle;
+        try {
+            h->device = device;
+            CK(cudaSetDevice(device));
+            CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
+            int major = 0, minor = 0;
+            CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+            CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+            if (major != 10 || minor != 0)
+                throw CudaError("hfpg is built for sm_100a (B200); device is sm_" +
+                                std::to_string(major) + std::to_string(minor));
+            CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+            CK(cudaEventCreate(&h->ev0));
+            CK(cudaEventCreate(&h->ev1));
+            configure_kernels();
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int hfpg_destroy(hfpg_handle* h) {
+    return guarded([&] {
+        if (!h) return;
+        cudaSetDevice(h->device);
+        invalidate_graph(h);
+        dfree(h->F); dfree(h->slice_off); dfree(h->sell_cols); dfree(h->sell_vals);
+        dfree(h->a_diag); dfree(h->x); dfree(h->r); dfree(h->z); dfree(h->ap); dfree(h->p0);
+        dfree(h->p1); dfree(h->y_loc); dfree(h->b); dfree(h->scratch); dfree(h->restrict_);
+        dfree(h->crow); dfree(h->ccol); dfree(h->node_u); dfree(h->node_v);
+        dfree(h->tree_counters); dfree(h->partials); dfree(h->counters); dfree(h->sc);
+        dfree(h->history);
+        if (h->ev0) cudaEventDestroy(h->ev0);
+        if (h->ev1) cudaEventDestroy(h->ev1);
+        if (h->stream) cudaStreamDestroy(h->stream);
+        delete h;
+    });
+}
+
+int hfpg_get_stream(hfpg_handle* h, void** stream) {
+    return guarded([&] { *stream = h->stream; });
+}
+
+int hfpg_load_csr(hfpg_handle* h, uint64_t n, const uint64_t* ro_in, const uint32_t* ci_in,
+                  const double* v_in, int where) {
+    return guarded([&] {
+        set_device(h);
+        if (n == 0) throw InvalidArgument("csr: empty matrix");
+        std::vector<uint64_t> ro(n + 1);
+        std::vector<uint32_t> ci;
+        std::vector<double> vv;
+        if (where == HFPG_DEVICE) {
+            CK(cudaMemcpy(ro.data(), ro_in, (n + 1) * 8, cudaMemcpyDeviceToHost));
+        } else {
+            std::memcpy(ro.data(), ro_in, (n + 1) * 8);
+        }
+        // csr.cpp:9-25 structural checks that keep device reads in bounds
+        if (ro[0] != 0) throw InvalidArgument("csr: row_offsets[0] != 0");
+        for (uint64_t i = 0; i < n; ++i)
+            if (ro[i] > ro[i + 1]) throw InvalidArgument("csr: row_offsets not nondecreasing");
+        const uint64_t nnz = ro[n];
+        ci.resize(nnz);
+        vv.resize(nnz);
+        if (where == HFPG_DEVICE) {
+            CK(cudaMemcpy(ci.data(), ci_in, nnz * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(vv.data(), v_in, nnz * 8, cudaMemcpyDeviceToHost));
+        } else {
+            std::memcpy(ci.data(), ci_in, nnz * 4);
+            std::memcpy(vv.data(), v_in, nnz * 8);
+        }
+        for (uint64_t p = 0; p < nnz; ++p)
+            if (ci[p] >= n) throw InvalidArgument("csr: column index out of range");
+        // csr.cpp:52-58 diagonal, csr.cpp:64-68 Frobenius norm (sequential, as the reference)
+        std::vector<double> diag(n, 0.0);
+        double fro = 0.0;
+        for (uint64_t i = 0; i < n; ++i)
+            for (uint64_t p = ro[i]; p < ro[i + 1]; ++p)
+                if (ci[p] == i) diag[i] = vv[p];
+        for (double v : vv) fro += v * v;
+        h->fro = std::sqrt(fro);
+        h->diag_positive = std::all_of(diag.begin(), diag.end(), [](double d) { return d > 0.0; });
+        // SELL-32: slice s holds rows 32s..32s+31, width = longest row, column-major inside;
+        // padding = (own row, 0.0) so padded FMAs add exactly +0.
+        const uint64_t ns = (n + 31) / 32;
+        std::vector<unsigned long long> off(ns + 1, 0);
+        for (uint64_t s = 0; s < ns; ++s) {
+            uint64_t w = 0;
+            for (uint64_t r = 32 * s; r < std::min(n, 32 * s + 32); ++r) w = std::max(w, ro[r + 1] - ro[r]);
+            off[s + 1] = off[s] + 32 * w;
+        }
+        std::vector<uint32_t> sc(off[ns]);
+        std::vector<double> sv(off[ns]);
+        for (uint64_t s = 0; s < ns; ++s) {
+            const uint64_t w = (off[s + 1] - off[s]) / 32;
+            for (uint64_t lane = 0; lane < 32; ++lane) {
+                const uint64_t r = 32 * s + lane;
+                for (uint64_t j = 0; j < w; ++j) {
+                    const uint64_t idx = off[s] + j * 32 + lane;
+                    if (r < n && j < ro[r + 1] - ro[r]) {
+                        sc[idx] = ci[ro[r] + j];
+                        sv[idx] = vv[ro[r] + j];
+                    } else {
+                        sc[idx] = uint32_t(std::min(r, n - 1));
+                        sv[idx] = 0.0;
+                    }
+                }
+            }
+        }
+        if (h->n != n) {
+            h->n = n;
+        }
+        invalidate_graph(h);
+        dalloc(h->slice_off, ns + 1);
+        dalloc(h->sell_cols, sc.size());
+        dalloc(h->sell_vals, sv.size());
+        dalloc(h->a_diag, n);
+        CK(cudaMemcpy(h->slice_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->sell_cols, sc.data(), sc.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->sell_vals, sv.data(), sv.size() * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->a_diag, diag.data(), n * 8, cudaMemcpyHostToDevice));
+        h->have_csr = true;
+        h->have_diag = true;
+        ensure_workspace(h);
+    });
+}
+
+int hfpg_set_diag(hfpg_handle* h, uint64_t n, const double* a_diag, int where) {
+    return guarded([&] {
+        set_device(h);
+        if (h->have_csr && n != h->n) throw InvalidArgument("set_diag: length mismatch");
+        if (!h->have_csr) h->n = n;
+        invalidate_graph(h);
+        dalloc(h->a_diag, n);
+        copy_in(h, h->a_diag, a_diag, n, where);
+        CK(cudaStreamSynchronize(h->stream));
+        h->have_diag = true;
+        ensure_workspace(h);
+    });
+}
+
+int hfpg_load_factors(hfpg_handle* h, uint64_t n, uint64_t leaf, uint64_t ls, const float* packed,
+                      uint64_t total, int32_t spd_enabled, double spd_raw, int where) {
+    return guarded([&] {
+        set_device(h);
+        const Layout L = make_layout(n, leaf, ls);
+        if (total != L.total) throw InvalidArgument("load_factors: packed width mismatch");
+        if (h->have_csr && h->n != n) throw InvalidArgument("load_factors: length mismatch");
+        invalidate_graph(h);
+        if (!h->have_factors || h->L.total != L.total) dalloc(h->F, L.total);
+        CK(cudaMemcpyAsync(h->F, packed, L.total * 4,
+                           where == HFPG_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                           h->stream));
+        h->L = L;
+        h->have_factors = true;
+        h->spd_enabled = spd_enabled;
+        h->spd_raw = spd_raw;
+        h->fast = (L.l == kL && L.ls == kLs && std::getenv("HFPG_FORCE_GENERIC") == nullptr);
+        if (!h->have_csr && !h->have_diag) h->n = n;
+        ensure_workspace(h);
+        const double shift = spd_enabled ? std::log1p(std::exp(spd_raw)) : 0.0;  // factor_tensor.hpp:64
+        CK(cudaMemcpyAsync(&h->sc->shift, &shift, 8, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int hfpg_set_precond(hfpg_handle* h, int kind) {
+    return guarded([&] {
+        if (kind < 0 || kind > 2) throw InvalidArgument("set_precond: unknown kind");
+        if (kind == HFPG_PRECOND_JACOBI) {
+            if (!h->have_csr) throw InvalidArgument("jacobi_applier: no matrix loaded");
+            if (!h->diag_positive)
+                throw InvalidArgument("jacobi_applier: nonpositive diagonal entry");
+        }
+        if (kind != h->precond) invalidate_graph(h);
+        h->precond = kind;
+    });
+}
+
+int hfpg_apply(hfpg_handle* h, const double* r, double* z, int where) {
+    return guarded([&] {
+        set_device(h);
+        require_apply_ready(h);
+        ensure_workspace(h);
+        fill_sys(h);
+        const double* rin = r;
+        double* zout = z;
+        if (where == HFPG_HOST) {
+            copy_in(h, h->scratch, r, h->n, HFPG_HOST);
+            rin = h->scratch;
+            zout = h->z;
+        }
+        launch_apply(h, kApply, rin, zout);
+        if (where == HFPG_HOST) copy_out(h, z, h->z, h->n, HFPG_HOST);
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int hfpg_spmv(hfpg_handle* h, const double* x, double* y, int where) {
+    return guarded([&] {
+        set_device(h);
+        if (!h->have_csr) throw InvalidArgument("spmv: no matrix loaded");
+        ensure_workspace(h);
+        fill_sys(h);
+        const double* xin = x;
+        double* yout = y;
+        if (where == HFPG_HOST) {
+            copy_in(h, h->scratch, x, h->n, HFPG_HOST);
+            xin = h->scratch;
+            yout = h->ap;
+        }
+        k_spmv<kApply><<<unsigned((h->n + 255) / 256), 256, 0, h->stream>>>(h->sys, xin, yout);
+        CK(cudaGetLastError());
+        if (where == HFPG_HOST) copy_out(h, y, h->ap, h->n, HFPG_HOST);
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg_in, double* x,
+                   double* history, hfpg_report* report, int where) {
+    return guarded([&] {
+        set_device(h);
+        hfpg_solve_config cfg = cfg_in ? *cfg_in : hfpg_solve_config{1e-8, 20000};
+        if (!(cfg.rtol > 0.0)) throw InvalidArgument("pcg_solve: rtol must be positive");
+        if (!h->have_csr) throw InvalidArgument("pcg_solve: no matrix loaded");
+        if (h->precond == HFPG_PRECOND_FACTOR) require_apply_ready(h);
+        ensure_workspace(h);
+        const uint64_t n = h->n;
+        const uint64_t hcap = std::max<uint64_t>(cfg.max_iters, 1);
+        if (h->history_cap < hcap) {
+            invalidate_graph(h);
+            dalloc(h->history, hcap);
+            h->history_cap = hcap;
+        }
+        if (!h->graph_valid) build_graph(h);
+        // state words (the loop-invariant part of Scalars)
+        Scalars init{};
+        init.rtol = cfg.rtol;
+        init.max_iters = cfg.max_iters;
+        init.breakdown_tol = 1e-12 * h->fro;  // pcg.cpp:80
+        init.shift = (h->precond == HFPG_PRECOND_FACTOR && h->spd_enabled)
+                         ? std::log1p(std::exp(h->spd_raw)) : 0.0;
+        init.status = 1;
+        CK(cudaMemcpyAsync(h->sc, &init, sizeof(Scalars), cudaMemcpyHostToDevice, h->stream));
+        copy_in(h, h->b, b, n, where);
+        CK(cudaEventRecord(h->ev0, h->stream));
+        CK(cudaGraphLaunch(h->exec, h->stream));
+        CK(cudaEventRecord(h->ev1, h->stream));
+        Scalars out{};
+        CK(cudaMemcpyAsync(&out, h->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
+        if (x) copy_out(h, x, h->x, n, where);
+        CK(cudaStreamSynchronize(h->stream));
+        if (history && out.hist_len) {
+            copy_out(h, history, h->history, out.hist_len, where);
+            CK(cudaStreamSynchronize(h->stream));
+        }
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+        if (report) {
+            report->n = n;
+            report->iterations = out.iterations;
+            report->converged = out.converged;
+            report->status = out.status;
+            report->breakdown_iter = out.breakdown_iter;
+            report->history_len = out.hist_len;
+            report->wall_ms = ms;
+        }
+    });
+}
+
+int hfpg_launch_counts(hfpg_handle* h, uint32_t* per_iteration, uint32_t* per_apply) {
+    return guarded([&] {
+        *per_apply = 3;
+        *per_iteration = h->precond == HFPG_PRECOND_FACTOR ? 4 : 2;
+    });
+}
+
+int hfpg_fast_path(hfpg_handle* h, int32_t* out) {
+    return guarded([&] { *out = h->have_factors && h->fast ? 1 : 0; });
+}
+
+}  // extern "C"

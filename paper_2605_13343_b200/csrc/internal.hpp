@@ -1,0 +1,113 @@
+// Internal host-side declarations shared by the C ABI, the generators and the CUDA driver.
+#pragma once
+
+#include "../../include/hfpg.h"
+
+#include <cmath>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace hfpg {
+
+// Error classes mirroring the reference's exception split.
+struct InvalidArgument : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void set_error(const std::string& msg);
+
+// Runs f(), maps exceptions to status codes and records the message.
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        set_error("");
+        return HFPG_OK;
+    } catch (const InvalidArgument& e) {
+        set_error(e.what());
+        return HFPG_EINVAL;
+    } catch (const std::invalid_argument& e) {
+        set_error(e.what());
+        return HFPG_EINVAL;
+    } catch (const IoError& e) {
+        set_error(e.what());
+        return HFPG_EIO;
+    } catch (const CudaError& e) {
+        set_error(e.what());
+        return HFPG_ECUDA;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return HFPG_EIO;
+    }
+}
+
+// ---- counter-based RNG: same key schedule and draws as rng.hpp:25-70 -------------------
+inline uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+enum Purpose : uint64_t { kDensity = 1, kRhs = 2, kFactorInit = 4 };
+
+struct Rng {
+    uint64_t key, counter = 0;
+    Rng(uint64_t seed, uint64_t frame, uint64_t purpose)
+        : key(mix64(mix64(mix64(seed) ^ frame) ^ purpose)) {}
+    // Value at an explicit counter: the stream is a pure function of (key, counter), which is
+    // what lets the generators below fill large arrays in parallel and stay bit-identical.
+    uint64_t bits_at(uint64_t c) const { return mix64(key ^ c); }
+    static double normal_of(uint64_t bits) {
+        const double u1 = (static_cast<double>(bits >> 32) + 1.0) * 0x1.0p-32;
+        const double u2 = static_cast<double>(bits & 0xFFFFFFFFULL) * 0x1.0p-32;
+        return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.14159265358979323846 * u2);
+    }
+    uint64_t bits() { return bits_at(counter++); }
+    double uniform() { return static_cast<double>(bits() >> 11) * 0x1.0p-53; }
+    double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+    uint64_t below(uint64_t n) {
+        return static_cast<uint64_t>((static_cast<unsigned __int128>(bits()) * n) >> 64);
+    }
+    double normal() { return normal_of(bits()); }
+};
+
+// ---- partition / layout: partition.cpp:9-53, factor_tensor.cpp:7-28 ---------------------
+struct Layout {
+    uint64_t n = 0, l = 0, ls = 0, rk = 0, k = 0, m = 0, depth = 0;  // depth = log2 K
+    uint64_t tile_base = 0, bridge_base = 0, gate_base = 0, total = 0;
+    uint64_t leaf(uint64_t kk) const { return kk * l * l; }
+    uint64_t tile_u(uint64_t t) const { return tile_base + t * ls * ls; }
+    uint64_t tile_v(uint64_t t) const { return tile_u(t) + ls * rk; }
+    uint64_t bridge_u(uint64_t kk) const { return bridge_base + kk * 2 * l * ls; }
+    uint64_t bridge_v(uint64_t kk) const { return bridge_u(kk) + l * ls; }
+};
+void check_partition(uint64_t n, uint64_t leaf);
+Layout make_layout(uint64_t n, uint64_t leaf, uint64_t ls);
+hfpg_layout to_c(const Layout& L);
+
+// ---- synthetic systems ---------------------------------------------------------------------
+struct Csr {
+    uint64_t n = 0;
+    std::vector<uint64_t> row_offsets;
+    std::vector<uint32_t> cols;
+    std::vector<double> vals;
+};
+void init_factors_host(const Layout& L, double sigma, uint64_t seed, uint64_t frame, float* out);
+
+}  // namespace hfpg
+
+struct hfpg_frame {
+    uint64_t n = 0, width = 0, height = 0, depth = 1;
+    double rho_heavy = 0.0;
+    std::vector<uint32_t> cell_order;
+    std::vector<double> rho, b;
+    hfpg::Csr A;
+};

@@ -1,0 +1,641 @@
+// sm_100a kernels of the hot path. One PCG iteration (pcg.cpp:86-119) with the factor
+// preconditioner (apply.cpp:79-174) is four launches, all inside one CUDA graph:
+//
+//   k_spmv    p = z + beta p (fused), Ap = A p on SELL-32, p.Ap and p.p       (csr.cpp:70-79)
+//   k_leaf    x += alpha p, r -= alpha Ap, |r|^2; then per leaf: F_k^T r_k, F_k c,
+//             Ũ_k^T r_k, Ṽ_k^T r_k (apply stages 1-3) from TMA-staged factors
+//   k_coarse  bisection-tree strip sums, tile couplings V(U^T s_r), U(V^T s_c) (stage 4)
+//   k_prolong ancestor gather + Ũ_k g_r + Ṽ_k g_c + gate, z, r.z, beta      (stages 5-7)
+//
+// Accumulator precisions follow the reference apply: F^T r and the restrictions accumulate in
+// fp32 (matvec_t, apply.cpp:25-35), F c and the prolongation in f64 (apply.cpp:11-22, 39-50),
+// strip sums and gathers in f64; every PCG scalar is f64 (pcg.hpp:14-16).
+#pragma once
+
+#include "device_common.cuh"
+
+namespace hfpg {
+
+// Device view of the loaded system and factors (pointers fixed at graph build time).
+struct DevSys {
+    // factors (packed layout, factor_tensor.hpp:18-48)
+    const float* F;
+    uint64_t n, l, ls, rk, K, D;  // D = log2 K
+    uint64_t tile_base, bridge_base, gate_base;
+    // operator
+    const double* a_diag;
+    const unsigned long long* slice_off;  // SELL-32 slices (element offsets, n_slices + 1)
+    const uint32_t* sell_cols;
+    const double* sell_vals;
+    // PCG vectors
+    double *x, *r, *z, *ap, *p0, *p1, *y_loc;
+    // apply workspace
+    float* restrict_;        // K x 2 L_s  (û_k | v̂_k), fp32 as in the reference
+    float *crow, *ccol;      // M_H x L_s coupled_row / coupled_col
+    double *node_u, *node_v; // heap-indexed strip sums of subtree roots (2K x L_s)
+    unsigned* tree_counters; // 2K arrival counters for the coarse tree
+    // reductions / state
+    double* partials;
+    unsigned* counters;  // [0] spmv, [1] leaf, [2] prolong, [3] simple
+    Scalars* sc;
+    double* history;
+    cudaGraphConditionalHandle cond;
+    int use_cond;
+};
+
+enum Mode { kInit = 0, kLoop = 1, kApply = 2 };
+
+__device__ __forceinline__ double* p_cur(const DevSys& s, unsigned long long k) {
+    return (k & 1ULL) ? s.p1 : s.p0;
+}
+__device__ __forceinline__ double* p_prev(const DevSys& s, unsigned long long k) {
+    return (k & 1ULL) ? s.p0 : s.p1;
+}
+
+// pcg.cpp:97-110 after |r|^2 is known: history, convergence, max_iters.
+__device__ __forceinline__ void finish_residual(Scalars* sc, double* history, double rr) {
+    const unsigned long long k = sc->k;
+    const double rel = sqrt(rr) / sc->r0;
+    sc->rel = rel;
+    if (history) history[k - 1] = rel;
+    sc->hist_len = k;
+    if (rel <= sc->rtol) {
+        sc->converged = 1;
+        sc->status = 0;
+        sc->iterations = k;
+        sc->done = 1;
+    } else if (k == sc->max_iters) {
+        sc->iterations = k;
+        sc->status = 1;
+        sc->done = 1;
+    }
+}
+
+// ============================================================================================
+// SpMV on SELL-32 (slices of 32 rows, column-major inside a slice, padded with (row, 0.0)).
+// One thread per row: every load is coalesced and each row accumulates sequentially in the
+// reference's column order (csr.cpp:74-77), so ap is bit-identical to the reference spmv.
+// PCG mode fuses p = z + beta p_prev (pcg.cpp:118) into the gathers and reduces p.Ap, p.p.
+// ============================================================================================
+template <int MODE>  // kInit unused; kLoop = PCG, kApply = plain y = A x
+__global__ void __launch_bounds__(256) k_spmv(DevSys s, const double* xin, double* yout) {
+    if (MODE == kLoop && s.sc->done) return;
+    const unsigned long long k = MODE == kLoop ? s.sc->k : 0ULL;
+    const double beta = MODE == kLoop ? s.sc->beta : 0.0;
+    const double* z = MODE == kLoop ? s.z : xin;
+    const double* pp_ = MODE == kLoop ? p_prev(s, k) : nullptr;
+    double* pnew = MODE == kLoop ? p_cur(s, k) : nullptr;
+    double* y = MODE == kLoop ? s.ap : yout;
+    const uint64_t row = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    double v[2] = {0.0, 0.0};
+    if (row < s.n) {
+        const uint64_t sl = row >> 5, lane = row & 31;
+        const uint64_t base = s.slice_off[sl], w = (s.slice_off[sl + 1] - base) >> 5;
+        double acc = 0.0;
+        for (uint64_t j = 0; j < w; ++j) {
+            const uint64_t idx = base + j * 32 + lane;
+            const uint32_t c = __ldg(&s.sell_cols[idx]);
+            const double a = __ldg(&s.sell_vals[idx]);
+            const double pc = MODE == kLoop ? fma(beta, pp_[c], z[c]) : z[c];
+            acc = fma(a, pc, acc);
+        }
+        y[row] = acc;
+        if (MODE == kLoop) {
+            const double pi = fma(beta, pp_[row], z[row]);
+            pnew[row] = pi;
+            v[0] = pi * acc;
+            v[1] = pi * pi;
+        }
+    }
+    if (MODE != kLoop) return;
+    double tot[2];
+    if (grid_reduce_last<2>(v, s.partials, &s.counters[0], tot) && threadIdx.x == 0) {
+        Scalars* sc = s.sc;
+        const double pap = tot[0], p2 = tot[1];
+        sc->pap = pap;
+        sc->pp = p2;
+        // pcg.cpp:90-95 breakdown test, reported not thrown
+        if (pap < -sc->breakdown_tol * p2 || pap == 0.0) {
+            sc->status = 2;
+            sc->breakdown_iter = k;
+            sc->iterations = k;
+            sc->done = 1;
+        } else {
+            sc->alpha = sc->rz / pap;
+        }
+    }
+}
+
+// x += alpha p, r -= alpha Ap for one row (pcg.cpp:97-98); returns the updated r.
+__device__ __forceinline__ double update_row(const DevSys& s, const double* p, double alpha,
+                                             uint64_t i) {
+    s.x[i] = fma(alpha, p[i], s.x[i]);
+    const double rn = fma(-alpha, s.ap[i], s.r[i]);
+    s.r[i] = rn;
+    return rn;
+}
+
+// Last-CTA epilogue of the leaf kernels: |r|^2 -> r0 (init) or rel/history/stop (loop).
+__device__ __forceinline__ void leaf_epilogue(const DevSys& s, int mode, double rr) {
+    Scalars* sc = s.sc;
+    if (mode == kInit) {
+        sc->r0 = sqrt(rr);
+        if (sc->r0 == 0.0) {  // pcg.cpp:73-79
+            sc->converged = 1;
+            sc->status = 0;
+            sc->iterations = 0;
+            sc->done = 1;
+        }
+    } else {
+        finish_residual(sc, s.history, rr);
+    }
+}
+
+// ============================================================================================
+// Leaf kernel, fast path (L = 128, L_s = 32): persistent, one CTA of 512 threads per SM.
+// Per leaf the 64 KB F_k and the 32 KB bridge pair (Ũ_k | Ṽ_k, contiguous in the packed
+// layout) arrive by cp.async.bulk into a 2-stage shared-memory ring (192 KB); the next leaf's
+// copy is in flight while this one computes, so the kernel streams the factor tensor at HBM
+// rate. F_k is read from HBM once and from shared memory twice (F^T r, then F c).
+// ============================================================================================
+constexpr int kL = 128, kLs = 32;
+constexpr int kLeafThreads = 512;
+constexpr uint32_t kFBytes = kL * kL * 4, kBBytes = 2 * kL * kLs * 4;
+struct LeafSmem {
+    float F[2][kL * kL];
+    float B[2][2 * kL * kLs];
+    float rin[kL];
+    float cpart[4][kL];
+    float rpart[8][2 * kLs];
+    float c[kL];
+    uint64_t full[2];
+};
+
+__global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mode,
+                                                               const double* rin_ext) {
+    if (mode != kApply && s.sc->done) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    LeafSmem& sm = *reinterpret_cast<LeafSmem*>(smem_raw);
+    const int tid = threadIdx.x;
+    const double alpha = mode == kLoop ? s.sc->alpha : 0.0;
+    const double* rsrc = mode == kApply ? rin_ext : s.r;
+    const double* pcur = mode == kLoop ? p_cur(s, s.sc->k) : nullptr;
+    const uint64_t K = s.K;
+    const uint64_t policy = policy_evict_first();
+
+    if (tid == 0) {
+        mbar_init(&sm.full[0], 1);
+        mbar_init(&sm.full[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](uint64_t leaf, int st) {
+        mbar_expect_tx(&sm.full[st], kFBytes + kBBytes);
+        const float* f = s.F + leaf * (kL * kL);
+        const float* b = s.F + s.bridge_base + leaf * (2 * kL * kLs);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            tma_load_1d(&sm.F[st][q * kL * kL / 4], f + q * kL * kL / 4, kFBytes / 4,
+                        &sm.full[st], policy);
+        tma_load_1d(&sm.B[st][0], b, kBBytes / 2, &sm.full[st], policy);
+        tma_load_1d(&sm.B[st][kL * kLs], b + kL * kLs, kBBytes / 2, &sm.full[st], policy);
+    };
+    if (tid == 0 && blockIdx.x < K) issue(blockIdx.x, 0);
+
+    double rr = 0.0;
+    const int lane = tid & 31, warp = tid >> 5;
+    uint32_t it = 0;
+    for (uint64_t leaf = blockIdx.x; leaf < K; leaf += gridDim.x, ++it) {
+        const int st = it & 1;
+        if (tid == 0 && leaf + gridDim.x < K) issue(leaf + gridDim.x, st ^ 1);
+        if (tid < kL) {
+            const uint64_t i = leaf * kL + tid;
+            double rv = mode == kLoop ? update_row(s, pcur, alpha, i) : rsrc[i];
+            rr = fma(rv, rv, rr);
+            sm.rin[tid] = static_cast<float>(rv);  // apply.cpp:90
+        }
+        mbar_wait(&sm.full[st], (it >> 1) & 1);
+        __syncthreads();
+        const float* F = sm.F[st];
+        const float* B = sm.B[st];
+        {   // c partials: column j, rows 32g..32g+31 (fp32, i ascending like matvec_t)
+            const int j = tid & (kL - 1), g = tid >> 7;
+            float acc = 0.f;
+#pragma unroll 8
+            for (int ii = 0; ii < 32; ++ii) acc = fmaf(F[(32 * g + ii) * kL + j], sm.rin[32 * g + ii], acc);
+            sm.cpart[g][j] = acc;
+        }
+        {   // restriction partials: output o (û | v̂), rows 16g..16g+15
+            const int o = tid & 63, g = tid >> 6;
+            const float* Bo = B + (o >> 5) * (kL * kLs) + (o & 31);
+            float acc = 0.f;
+#pragma unroll 8
+            for (int ii = 0; ii < 16; ++ii) acc = fmaf(Bo[(16 * g + ii) * kLs], sm.rin[16 * g + ii], acc);
+            sm.rpart[g][o] = acc;
+        }
+        __syncthreads();
+        if (tid < kL) {
+            sm.c[tid] = ((sm.cpart[0][tid] + sm.cpart[1][tid]) + sm.cpart[2][tid]) + sm.cpart[3][tid];
+        } else if (tid < kL + 2 * kLs) {
+            const int o = tid - kL;
+            float v = sm.rpart[0][o];
+#pragma unroll
+            for (int g = 1; g < 8; ++g) v += sm.rpart[g][o];
+            s.restrict_[leaf * (2 * kLs) + o] = v;
+        }
+        __syncthreads();
+        {   // y = F c with f64 accumulation: warp w owns rows 8w..8w+7, lane l columns 4l..4l+3
+            const float4 c4 = reinterpret_cast<const float4*>(sm.c)[lane];
+            const double c0 = c4.x, c1 = c4.y, c2 = c4.z, c3 = c4.w;
+            double v[8];
+#pragma unroll
+            for (int rI = 0; rI < 8; ++rI) {
+                const float4 f4 = reinterpret_cast<const float4*>(F + (8 * warp + rI) * kL)[lane];
+                v[rI] = fma(double(f4.w), c3, fma(double(f4.z), c2, fma(double(f4.y), c1, double(f4.x) * c0)));
+            }
+            // transpose-reduce 8 rows x 32 lanes: after xor 16/8/4 each lane holds one row's
+            // partial over 4 lanes; xor 2/1 finish it.
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const bool hi = lane & 16;
+                const double send = hi ? v[q] : v[q + 4];
+                const double keep = hi ? v[q + 4] : v[q];
+                v[q] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const bool hi = lane & 8;
+                const double send = hi ? v[q] : v[q + 2];
+                const double keep = hi ? v[q + 2] : v[q];
+                v[q] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            }
+            {
+                const bool hi = lane & 4;
+                const double send = hi ? v[0] : v[1];
+                const double keep = hi ? v[1] : v[0];
+                v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+            }
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+            if ((lane & 3) == 0) {
+                const int row = 8 * warp + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+                s.y_loc[leaf * kL + row] = v[0];
+            }
+        }
+        __syncthreads();
+    }
+    if (mode == kApply) return;
+    double v[1] = {rr}, tot[1];
+    if (grid_reduce_last<1>(v, s.partials, &s.counters[1], tot) && tid == 0)
+        leaf_epilogue(s, mode, tot[0]);
+}
+
+// Leaf kernel, generic path (any L, L_s): one CTA per leaf, factors read from global.
+__global__ void __launch_bounds__(256) k_leaf_generic(DevSys s, int mode, const double* rin_ext) {
+    if (mode != kApply && s.sc->done) return;
+    extern __shared__ float gsm[];
+    const uint64_t L = s.l, ls = s.ls, leaf = blockIdx.x;
+    float* rin = gsm;
+    float* c = gsm + L;
+    const double alpha = mode == kLoop ? s.sc->alpha : 0.0;
+    const double* rsrc = mode == kApply ? rin_ext : s.r;
+    const double* pcur = mode == kLoop ? p_cur(s, s.sc->k) : nullptr;
+    double rr = 0.0;
+    for (uint64_t t = threadIdx.x; t < L; t += blockDim.x) {
+        const uint64_t i = leaf * L + t;
+        const double rv = mode == kLoop ? update_row(s, pcur, alpha, i) : rsrc[i];
+        rr = fma(rv, rv, rr);
+        rin[t] = static_cast<float>(rv);
+    }
+    __syncthreads();
+    const float* F = s.F + leaf * L * L;
+    for (uint64_t j = threadIdx.x; j < L; j += blockDim.x) {  // c = F^T r (fp32)
+        float acc = 0.f;
+        for (uint64_t i = 0; i < L; ++i) acc = fmaf(F[i * L + j], rin[i], acc);
+        c[j] = acc;
+    }
+    for (uint64_t o = threadIdx.x; o < 2 * ls; o += blockDim.x) {  // restriction (fp32)
+        const float* B = s.F + s.bridge_base + leaf * 2 * L * ls + (o >= ls ? L * ls : 0);
+        const uint64_t col = o % ls;
+        float acc = 0.f;
+        for (uint64_t i = 0; i < L; ++i) acc = fmaf(B[i * ls + col], rin[i], acc);
+        s.restrict_[leaf * 2 * ls + o] = acc;
+    }
+    __syncthreads();
+    for (uint64_t i = threadIdx.x; i < L; i += blockDim.x) {  // y = F c (f64)
+        double acc = 0.0;
+        for (uint64_t j = 0; j < L; ++j) acc = fma(double(F[i * L + j]), double(c[j]), acc);
+        s.y_loc[leaf * L + i] = acc;
+    }
+    if (mode == kApply) return;
+    double v[1] = {rr}, tot[1];
+    if (grid_reduce_last<1>(v, s.partials, &s.counters[1], tot) && threadIdx.x == 0)
+        leaf_epilogue(s, mode, tot[0]);
+}
+
+// ============================================================================================
+// Coarse kernel: apply stage 4 (apply.cpp:110-138) over the bisection tree in heap order
+// (tile m = heap node m; its rows are the left child's leaves, its columns the right child's).
+// s_r(m) = Σ û over the left child, s_c(m) = Σ v̂ over the right child: an f64 up-sweep. Each
+// CTA owns an aligned subtree of up to 32 leaves (or of 32 subtree roots at higher levels),
+// computes its internal tiles, publishes its root sums, and the last-arriving CTA of each
+// group of siblings carries on one level up — one launch covers the whole tree.
+// ============================================================================================
+constexpr int kCoarseThreads = 256;
+
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse(DevSys s, int mode) {
+    if (mode != kApply && s.sc->done) return;
+    extern __shared__ double csm[];
+    const uint64_t ls = s.ls, rk = s.rk;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* SU = csm;                // (2*32-1) x ls
+    double* SV = csm + 63 * ls;      // (2*32-1) x ls
+    float* coef = reinterpret_cast<float*>(csm + 126 * ls);  // 8 warps x 2 x rk
+    __shared__ int last;
+
+    uint64_t task = blockIdx.x;
+    uint64_t dlo = s.D;  // depth of this task's bottom layer
+    for (int level = 0;; ++level) {
+        const uint64_t cnt = 1ULL << dlo;
+        const uint64_t S = cnt < 32 ? cnt : 32;
+        int logS = 0;
+        while ((1ULL << logS) < S) ++logS;
+        const uint64_t dr = dlo - logS;  // depth of this task's root
+        // bottom layer -> local heap nodes S-1 .. 2S-2
+        for (uint64_t e = tid; e < S * ls; e += blockDim.x) {
+            const uint64_t q = e / ls, j = e % ls, u = S - 1 + q;
+            const uint64_t gi = task * S + q;  // index within depth dlo
+            if (level == 0) {
+                SU[u * ls + j] = double(s.restrict_[gi * 2 * ls + j]);
+                SV[u * ls + j] = double(s.restrict_[gi * 2 * ls + ls + j]);
+            } else {
+                const uint64_t g = (1ULL << dlo) - 1 + gi;
+                SU[u * ls + j] = __ldcg(&s.node_u[g * ls + j]);
+                SV[u * ls + j] = __ldcg(&s.node_v[g * ls + j]);
+            }
+        }
+        __syncthreads();
+        for (int ld = logS - 1; ld >= 0; --ld) {  // up-sweep inside the subtree
+            const uint64_t u0 = (1ULL << ld) - 1, nu = 1ULL << ld;
+            for (uint64_t e = tid; e < nu * ls; e += blockDim.x) {
+                const uint64_t u = u0 + e / ls, j = e % ls;
+                SU[u * ls + j] = SU[(2 * u + 1) * ls + j] + SU[(2 * u + 2) * ls + j];
+                SV[u * ls + j] = SV[(2 * u + 1) * ls + j] + SV[(2 * u + 2) * ls + j];
+            }
+            __syncthreads();
+        }
+        // internal tiles: one warp per tile
+        float* cr_ = coef + warp * 2 * rk;
+        float* cc_ = cr_ + rk;
+        for (uint64_t u = warp; u + 1 < S; u += blockDim.x / 32) {
+            int ld = 0;
+            while ((2ULL << ld) <= u + 1) ++ld;
+            const uint64_t depth = dr + ld, idx = task * (1ULL << ld) + (u + 1 - (1ULL << ld));
+            const uint64_t m = (1ULL << depth) - 1 + idx;
+            const float* U = s.F + s.tile_base + m * ls * ls;
+            const float* V = U + ls * rk;
+            const double* sr = SU + (2 * u + 1) * ls;
+            const double* sc = SV + (2 * u + 2) * ls;
+            for (uint64_t q = lane; q < rk; q += 32) {  // U^T float(s_r), V^T float(s_c)
+                float a = 0.f, b = 0.f;
+                for (uint64_t p = 0; p < ls; ++p) {
+                    a = fmaf(U[p * rk + q], float(sr[p]), a);
+                    b = fmaf(V[p * rk + q], float(sc[p]), b);
+                }
+                cr_[q] = a;
+                cc_[q] = b;
+            }
+            __syncwarp();
+            for (uint64_t j = lane; j < ls; j += 32) {  // coupled_col = V c, coupled_row = U c'
+                double a = 0.0, b = 0.0;
+                for (uint64_t q = 0; q < rk; ++q) {
+                    a = fma(double(V[j * rk + q]), double(cr_[q]), a);
+                    b = fma(double(U[j * rk + q]), double(cc_[q]), b);
+                }
+                s.ccol[m * ls + j] = float(a);
+                s.crow[m * ls + j] = float(b);
+            }
+            __syncwarp();
+        }
+        if (dr == 0) return;  // root handled
+        {   // publish the subtree root's sums
+            const uint64_t g = (1ULL << dr) - 1 + task;
+            for (uint64_t j = tid; j < ls; j += blockDim.x) {
+                s.node_u[g * ls + j] = SU[j];
+                s.node_v[g * ls + j] = SV[j];
+            }
+        }
+        const uint64_t cnt2 = 1ULL << dr;
+        const uint64_t S2 = cnt2 < 32 ? cnt2 : 32;
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            int logS2 = 0;
+            while ((1ULL << logS2) < S2) ++logS2;
+            const uint64_t parent = (1ULL << (dr - logS2)) - 1 + task / S2;
+            const unsigned t = atomicAdd(&s.tree_counters[parent], 1u);
+            last = (t == S2 - 1);
+            if (last) s.tree_counters[parent] = 0u;
+        }
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        task /= S2;
+        dlo = dr;
+    }
+}
+
+// ============================================================================================
+// Prolongation kernels: apply stages 5-7. The f64 gather of leaf k sums coupled_row over the
+// ancestors whose left half holds k and coupled_col over those whose right half holds it, in
+// tile order (root first), exactly the order of apply.cpp:140-154.
+// ============================================================================================
+__device__ __forceinline__ void prolong_epilogue(const DevSys& s, int mode, double rz) {
+    Scalars* sc = s.sc;
+    if (mode == kInit) {
+        sc->rz = rz;  // pcg.cpp:84
+        sc->beta = 0.0;
+        sc->k = 1;
+        if (sc->max_iters == 0) {
+            sc->iterations = 0;
+            sc->status = 1;
+            sc->done = 1;
+        }
+    } else {
+        sc->beta = rz / sc->rz;  // pcg.cpp:115-117
+        sc->rz = rz;
+        sc->k += 1;
+    }
+    if (s.use_cond) cudaGraphSetConditional(s.cond, sc->done ? 0u : 1u);
+}
+
+__device__ __forceinline__ bool prolong_skip(const DevSys& s, int mode) {
+    if (mode == kApply || !s.sc->done) return false;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && s.use_cond) cudaGraphSetConditional(s.cond, 0u);
+    return true;
+}
+
+__global__ void __launch_bounds__(256) k_prolong_fast(DevSys s, int mode, const double* rin_ext,
+                                                      double* zout) {
+    if (prolong_skip(s, mode)) return;
+    __shared__ float g[2][kLs];
+    __shared__ double su[kL], sv[kL];
+    const int tid = threadIdx.x;
+    const uint64_t leaf = blockIdx.x, K = s.K, D = s.D;
+    if (tid < 2 * kLs) {
+        const int side = tid >> 5, j = tid & 31;
+        const float* src = side ? s.ccol : s.crow;
+        double acc = 0.0;
+        for (uint64_t d = 0; d < D; ++d) {
+            const uint64_t m = ((K + leaf) >> (D - d)) - 1;
+            if (((leaf >> (D - 1 - d)) & 1ULL) == uint64_t(side)) acc += double(__ldcg(&src[m * kLs + j]));
+        }
+        g[side][j] = float(acc);
+    }
+    __syncthreads();
+    {   // Ũ_k g_r and Ṽ_k g_c, f64 accumulation; 8 lanes per row, 128-bit streaming loads
+        const int l8 = tid & 7, rowi = tid >> 3;
+        const float4 gr = reinterpret_cast<const float4*>(g[0])[l8];
+        const float4 gc = reinterpret_cast<const float4*>(g[1])[l8];
+        const float* Bu = s.F + s.bridge_base + leaf * (2 * kL * kLs);
+        const float* Bv = Bu + kL * kLs;
+        float4 u4[4], v4[4];
+#pragma unroll
+        for (int ps = 0; ps < 4; ++ps) {
+            const int row = ps * 32 + rowi;
+            u4[ps] = ldg_stream(reinterpret_cast<const float4*>(Bu + row * kLs) + l8);
+            v4[ps] = ldg_stream(reinterpret_cast<const float4*>(Bv + row * kLs) + l8);
+        }
+#pragma unroll
+        for (int ps = 0; ps < 4; ++ps) {
+            double au = fma(double(u4[ps].w), double(gr.w), fma(double(u4[ps].z), double(gr.z),
+                        fma(double(u4[ps].y), double(gr.y), double(u4[ps].x) * double(gr.x))));
+            double av = fma(double(v4[ps].w), double(gc.w), fma(double(v4[ps].z), double(gc.z),
+                        fma(double(v4[ps].y), double(gc.y), double(v4[ps].x) * double(gc.x))));
+            au += __shfl_xor_sync(0xffffffffu, au, 4);
+            au += __shfl_xor_sync(0xffffffffu, au, 2);
+            au += __shfl_xor_sync(0xffffffffu, au, 1);
+            av += __shfl_xor_sync(0xffffffffu, av, 4);
+            av += __shfl_xor_sync(0xffffffffu, av, 2);
+            av += __shfl_xor_sync(0xffffffffu, av, 1);
+            if (l8 == 0) {
+                su[ps * 32 + rowi] = au;
+                sv[ps * 32 + rowi] = av;
+            }
+        }
+    }
+    __syncthreads();
+    double rz = 0.0;
+    if (tid < kL) {
+        const uint64_t i = leaf * kL + tid;
+        const double rv = mode == kApply ? rin_ext[i] : s.r[i];
+        const double gate = double(s.F[s.gate_base + i]);
+        double y = s.y_loc[i];
+        y += su[tid];
+        y += sv[tid];
+        y += gate * rv / s.a_diag[i] + s.sc->shift * rv;  // apply.cpp:169-173
+        (mode == kApply ? zout : s.z)[i] = y;
+        rz = rv * y;
+    }
+    if (mode == kApply) return;
+    double v[1] = {rz}, tot[1];
+    if (grid_reduce_last<1>(v, s.partials, &s.counters[2], tot) && tid == 0)
+        prolong_epilogue(s, mode, tot[0]);
+}
+
+__global__ void __launch_bounds__(256) k_prolong_generic(DevSys s, int mode,
+                                                         const double* rin_ext, double* zout) {
+    if (prolong_skip(s, mode)) return;
+    extern __shared__ float psm[];
+    const uint64_t L = s.l, ls = s.ls, leaf = blockIdx.x, K = s.K, D = s.D;
+    for (uint64_t t = threadIdx.x; t < 2 * ls; t += blockDim.x) {
+        const uint64_t side = t / ls, j = t % ls;
+        const float* src = side ? s.ccol : s.crow;
+        double acc = 0.0;
+        for (uint64_t d = 0; d < D; ++d) {
+            const uint64_t m = ((K + leaf) >> (D - d)) - 1;
+            if (((leaf >> (D - 1 - d)) & 1ULL) == side) acc += double(__ldcg(&src[m * ls + j]));
+        }
+        psm[t] = float(acc);
+    }
+    __syncthreads();
+    const float* Bu = s.F + s.bridge_base + leaf * 2 * L * ls;
+    const float* Bv = Bu + L * ls;
+    double rz = 0.0;
+    for (uint64_t t = threadIdx.x; t < L; t += blockDim.x) {
+        double au = 0.0, av = 0.0;
+        for (uint64_t j = 0; j < ls; ++j) au = fma(double(Bu[t * ls + j]), double(psm[j]), au);
+        for (uint64_t j = 0; j < ls; ++j) av = fma(double(Bv[t * ls + j]), double(psm[ls + j]), av);
+        const uint64_t i = leaf * L + t;
+        const double rv = mode == kApply ? rin_ext[i] : s.r[i];
+        double y = s.y_loc[i];
+        y += au;
+        y += av;
+        y += double(s.F[s.gate_base + i]) * rv / s.a_diag[i] + s.sc->shift * rv;
+        (mode == kApply ? zout : s.z)[i] = y;
+        rz = fma(rv, y, rz);
+    }
+    if (mode == kApply) return;
+    double v[1] = {rz}, tot[1];
+    if (grid_reduce_last<1>(v, s.partials, &s.counters[2], tot) && threadIdx.x == 0)
+        prolong_epilogue(s, mode, tot[0]);
+}
+
+// ============================================================================================
+// Identity / Jacobi preconditioners (pcg.cpp:28-42) on the same graph: update, |r|^2,
+// z = r (/ a_ii), r.z in one pass.
+// ============================================================================================
+__global__ void __launch_bounds__(256) k_simple(DevSys s, int mode, int jacobi) {
+    if (s.sc->done) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && s.use_cond) cudaGraphSetConditional(s.cond, 0u);
+        return;
+    }
+    const double alpha = mode == kLoop ? s.sc->alpha : 0.0;
+    const double* pcur = mode == kLoop ? p_cur(s, s.sc->k) : nullptr;
+    double v[2] = {0.0, 0.0};
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < s.n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double rv = mode == kLoop ? update_row(s, pcur, alpha, i) : s.r[i];
+        const double zv = jacobi ? rv / s.a_diag[i] : rv;
+        s.z[i] = zv;
+        v[0] = fma(rv, rv, v[0]);
+        v[1] = fma(rv, zv, v[1]);
+    }
+    double tot[2];
+    if (grid_reduce_last<2>(v, s.partials, &s.counters[3], tot) && threadIdx.x == 0) {
+        Scalars* sc = s.sc;
+        if (mode == kInit) {
+            leaf_epilogue(s, kInit, tot[0]);
+            if (!sc->done) prolong_epilogue(s, kInit, tot[1]);
+            else if (s.use_cond) cudaGraphSetConditional(s.cond, 0u);
+        } else {
+            finish_residual(sc, s.history, tot[0]);
+            if (!sc->done) prolong_epilogue(s, kLoop, tot[1]);
+            else if (s.use_cond) cudaGraphSetConditional(s.cond, 0u);
+        }
+    }
+}
+
+// Solve initialisation: x = 0, r = b, p_prev = 0 and the state words (pcg.cpp:65-80).
+__global__ void k_init(DevSys s, const double* b) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < s.n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        s.x[i] = 0.0;
+        s.r[i] = b[i];
+        s.p0[i] = 0.0;  // p_prev of iteration 1 (k = 1 -> p_prev = p0)
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        Scalars* sc = s.sc;
+        sc->k = 0;
+        sc->iterations = 0;
+        sc->breakdown_iter = 0;
+        sc->hist_len = 0;
+        sc->status = 1;
+        sc->converged = 0;
+        sc->done = 0;
+        sc->beta = 0.0;
+        sc->alpha = 0.0;
+    }
+}
+
+}  // namespace hfpg
