@@ -148,6 +148,11 @@ int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg
 /* ---- introspection for tests / bench ---------------------------------------------------- */
 /* Number of kernels one PCG iteration launches, and one apply. */
 int hfpg_launch_counts(hfpg_handle* h, uint32_t* per_iteration, uint32_t* per_apply);
+/* Per-kernel device time of one factor-preconditioned PCG iteration, measured with CUDA events
+ * between standalone launches of the iteration's kernels on the handle's stream (state left by
+ * the last solve; alpha = beta = 0 so the traffic is a real iteration's but x, r stay fixed).
+ * ms_out[4] = {spmv, leaf, coarse, prolong}, averaged over `reps`. */
+int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out);
 /* 1 if the fast sm_100a TMA path (L=128, L_s=32) is selected for the loaded layout. */
 int hfpg_fast_path(hfpg_handle* h, int32_t* out);
 

@@ -72,6 +72,7 @@ _PROTOS = {
                                  C.c_int]),
     "hfpg_launch_counts": (C.c_int, [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "hfpg_fast_path": (C.c_int, [vp, C.POINTER(i32)]),
+    "hfpg_profile_iteration": (C.c_int, [vp, C.c_uint32, vp]),
 }
 
 EXPORTED = sorted(_PROTOS)

@@ -153,6 +153,14 @@ void ensure_workspace(hfpg_handle* h) {
     }
 }
 
+// Subtree width of k_coarse: 32 leaves when the staged tiles fit, else fewer.
+uint64_t coarse_width(const Layout& L) {
+    uint64_t S = 32;
+    while (S > 2 && coarse_smem_bytes(L.ls, S) > 200 * 1024) S /= 2;
+    return S;
+}
+size_t coarse_smem(const Layout& L) { return coarse_smem_bytes(L.ls, coarse_width(L)); }
+
 void fill_sys(hfpg_handle* h) {
     DevSys& s = h->sys;
     s = DevSys{};
@@ -184,6 +192,7 @@ void fill_sys(hfpg_handle* h) {
     s.node_u = h->node_u;
     s.node_v = h->node_v;
     s.tree_counters = h->tree_counters;
+    s.coarse_S = coarse_width(L);
     s.partials = h->partials;
     s.counters = h->counters;
     s.sc = h->sc;
@@ -191,7 +200,6 @@ void fill_sys(hfpg_handle* h) {
     s.use_cond = 0;
 }
 
-size_t coarse_smem(const Layout& L) { return 126 * L.ls * sizeof(double) + 16 * L.rk * sizeof(float); }
 
 // The three apply launches (stages 1-3, 4, 5-7) in a given mode.
 void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
@@ -203,7 +211,7 @@ void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
         k_leaf_generic<<<unsigned(L.k), 256, 2 * L.l * sizeof(float), h->stream>>>(s, mode, rin);
     }
     CK(cudaGetLastError());
-    const uint64_t S0 = std::min<uint64_t>(L.k, 32);
+    const uint64_t S0 = std::min<uint64_t>(L.k, coarse_width(L));
     k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(s, mode);
     CK(cudaGetLastError());
     if (h->fast)
@@ -242,7 +250,7 @@ void configure_kernels() {
     std::call_once(once, [] {
         CK(cudaFuncSetAttribute(k_leaf_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(sizeof(LeafSmem))));
-        CK(cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        CK(cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         CK(cudaFuncSetAttribute(k_leaf_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     });
 }
@@ -510,11 +518,12 @@ int hfpg_apply(hfpg_handle* h, const double* r, double* z, int where) {
         fill_sys(h);
         const double* rin = r;
         double* zout = z;
-        if (where == HFPG_HOST) {
-            copy_in(h, h->scratch, r, h->n, HFPG_HOST);
+        // the leaf kernel bulk-copies r slices: it needs a 16-byte aligned source
+        if (where == HFPG_HOST || (reinterpret_cast<uintptr_t>(r) & 15)) {
+            copy_in(h, h->scratch, r, h->n, where);
             rin = h->scratch;
-            zout = h->z;
         }
+        if (where == HFPG_HOST) zout = h->z;
         launch_apply(h, kApply, rin, zout);
         if (where == HFPG_HOST) copy_out(h, z, h->z, h->n, HFPG_HOST);
         CK(cudaStreamSynchronize(h->stream));
@@ -597,6 +606,56 @@ int hfpg_launch_counts(hfpg_handle* h, uint32_t* per_iteration, uint32_t* per_ap
     return guarded([&] {
         *per_apply = 3;
         *per_iteration = h->precond == HFPG_PRECOND_FACTOR ? 4 : 2;
+    });
+}
+
+int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out) {
+    return guarded([&] {
+        set_device(h);
+        if (h->precond != HFPG_PRECOND_FACTOR || !h->have_csr) throw InvalidArgument("profile: factor solve required");
+        require_apply_ready(h);
+        ensure_workspace(h);
+        fill_sys(h);
+        cudaEvent_t ev[5];
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        double acc[4] = {0, 0, 0, 0};
+        Scalars prof{};
+        prof.rtol = 0.0;
+        prof.max_iters = ~0ULL >> 1;
+        prof.rz = 1.0;
+        prof.r0 = 1.0;
+        prof.k = 1;
+        prof.breakdown_tol = 1e-12 * h->fro;
+        prof.shift = h->spd_enabled ? std::log1p(std::exp(h->spd_raw)) : 0.0;
+        const Layout& L = h->L;
+        const uint64_t S0 = std::min<uint64_t>(L.k, coarse_width(L));
+        for (uint32_t rep = 0; rep < std::max(reps, 1u); ++rep) {
+            CK(cudaMemcpyAsync(h->sc, &prof, sizeof(Scalars), cudaMemcpyHostToDevice, h->stream));
+            CK(cudaEventRecord(ev[0], h->stream));
+            k_spmv<kLoop><<<unsigned((h->n + 255) / 256), 256, 0, h->stream>>>(h->sys, nullptr, nullptr);
+            CK(cudaEventRecord(ev[1], h->stream));
+            if (h->fast)
+                k_leaf_fast<<<unsigned(leaf_grid(h)), kLeafThreads, sizeof(LeafSmem), h->stream>>>(h->sys, kLoop, nullptr);
+            else
+                k_leaf_generic<<<unsigned(L.k), 256, 2 * L.l * sizeof(float), h->stream>>>(h->sys, kLoop, nullptr);
+            CK(cudaEventRecord(ev[2], h->stream));
+            k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(h->sys, kLoop);
+            CK(cudaEventRecord(ev[3], h->stream));
+            if (h->fast)
+                k_prolong_fast<<<unsigned(L.k), 256, 0, h->stream>>>(h->sys, kLoop, nullptr, nullptr);
+            else
+                k_prolong_generic<<<unsigned(L.k), 256, 2 * L.ls * sizeof(float), h->stream>>>(h->sys, kLoop, nullptr, nullptr);
+            CK(cudaEventRecord(ev[4], h->stream));
+            CK(cudaGetLastError());
+            CK(cudaEventSynchronize(ev[4]));
+            for (int i = 0; i < 4; ++i) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+                acc[i] += ms;
+            }
+        }
+        for (int i = 0; i < 4; ++i) ms_out[i] = float(acc[i] / std::max(reps, 1u));
+        for (auto& e : ev) cudaEventDestroy(e);
     });
 }
 

@@ -34,6 +34,7 @@ struct DevSys {
     float *crow, *ccol;      // M_H x L_s coupled_row / coupled_col
     double *node_u, *node_v; // heap-indexed strip sums of subtree roots (2K x L_s)
     unsigned* tree_counters; // 2K arrival counters for the coarse tree
+    uint64_t coarse_S;       // subtree width per k_coarse task (power of two)
     // reductions / state
     double* partials;
     unsigned* counters;  // [0] spmv, [1] leaf, [2] prolong, [3] simple
@@ -92,12 +93,26 @@ __global__ void __launch_bounds__(256) k_spmv(DevSys s, const double* xin, doubl
         const uint64_t sl = row >> 5, lane = row & 31;
         const uint64_t base = s.slice_off[sl], w = (s.slice_off[sl + 1] - base) >> 5;
         double acc = 0.0;
-        for (uint64_t j = 0; j < w; ++j) {
-            const uint64_t idx = base + j * 32 + lane;
-            const uint32_t c = __ldg(&s.sell_cols[idx]);
-            const double a = __ldg(&s.sell_vals[idx]);
-            const double pc = MODE == kLoop ? fma(beta, pp_[c], z[c]) : z[c];
-            acc = fma(a, pc, acc);
+        // Batches of 8 slots: all index/value loads first, then the gathers, then the
+        // accumulation in slot order. The reference computes acc += a * x as a rounded
+        // product plus a rounded sum (its csr.cpp:76 loop is not FMA-contracted), so the
+        // products/sums are explicit __dmul_rn/__dadd_rn: ap is bit-identical to spmv().
+        for (uint64_t j0 = 0; j0 < w; j0 += 8) {
+            uint32_t c[8];
+            double a[8], pc[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (j0 + q < w) {
+                    const uint64_t idx = base + (j0 + q) * 32 + lane;
+                    c[q] = __ldg(&s.sell_cols[idx]);
+                    a[q] = __ldg(&s.sell_vals[idx]);
+                }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (j0 + q < w) pc[q] = MODE == kLoop ? fma(beta, pp_[c[q]], z[c[q]]) : z[c[q]];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (j0 + q < w) acc = __dadd_rn(acc, __dmul_rn(a[q], pc[q]));
         }
         y[row] = acc;
         if (MODE == kLoop) {
@@ -164,6 +179,7 @@ constexpr uint32_t kFBytes = kL * kL * 4, kBBytes = 2 * kL * kLs * 4;
 struct LeafSmem {
     float F[2][kL * kL];
     float B[2][2 * kL * kLs];
+    double vec[2][4][kL];  // r_k, Ap_k, p_k, x_k of the staged leaf (the fused PCG update)
     float rin[kL];
     float cpart[4][kL];
     float rpart[8][2 * kLs];
@@ -181,7 +197,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mod
     const double* rsrc = mode == kApply ? rin_ext : s.r;
     const double* pcur = mode == kLoop ? p_cur(s, s.sc->k) : nullptr;
     const uint64_t K = s.K;
-    const uint64_t policy = policy_evict_first();
+    const uint64_t pol_stream = policy_evict_first();
+    const int nvec = mode == kLoop ? 4 : 1;
+    const uint32_t stage_bytes = kFBytes + kBBytes + nvec * kL * 8;
 
     if (tid == 0) {
         mbar_init(&sm.full[0], 1);
@@ -189,16 +207,24 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mod
         fence_mbar_init();
     }
     __syncthreads();
+    // One elected thread streams a whole leaf: F_k (4 x 16 KB), Ũ_k|Ṽ_k (2 x 16 KB) and the
+    // leaf's slices of the PCG vectors, all completing on the stage's mbarrier.
     auto issue = [&](uint64_t leaf, int st) {
-        mbar_expect_tx(&sm.full[st], kFBytes + kBBytes);
+        mbar_expect_tx(&sm.full[st], stage_bytes);
         const float* f = s.F + leaf * (kL * kL);
         const float* b = s.F + s.bridge_base + leaf * (2 * kL * kLs);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
             tma_load_1d(&sm.F[st][q * kL * kL / 4], f + q * kL * kL / 4, kFBytes / 4,
-                        &sm.full[st], policy);
-        tma_load_1d(&sm.B[st][0], b, kBBytes / 2, &sm.full[st], policy);
-        tma_load_1d(&sm.B[st][kL * kLs], b + kL * kLs, kBBytes / 2, &sm.full[st], policy);
+                        &sm.full[st], pol_stream);
+        tma_load_1d(&sm.B[st][0], b, kBBytes / 2, &sm.full[st], pol_stream);
+        tma_load_1d(&sm.B[st][kL * kLs], b + kL * kLs, kBBytes / 2, &sm.full[st], pol_stream);
+        tma_load_1d(sm.vec[st][0], rsrc + leaf * kL, kL * 8, &sm.full[st], pol_stream);
+        if (mode == kLoop) {
+            tma_load_1d(sm.vec[st][1], s.ap + leaf * kL, kL * 8, &sm.full[st], pol_stream);
+            tma_load_1d(sm.vec[st][2], pcur + leaf * kL, kL * 8, &sm.full[st], pol_stream);
+            tma_load_1d(sm.vec[st][3], s.x + leaf * kL, kL * 8, &sm.full[st], pol_stream);
+        }
     };
     if (tid == 0 && blockIdx.x < K) issue(blockIdx.x, 0);
 
@@ -208,13 +234,18 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mod
     for (uint64_t leaf = blockIdx.x; leaf < K; leaf += gridDim.x, ++it) {
         const int st = it & 1;
         if (tid == 0 && leaf + gridDim.x < K) issue(leaf + gridDim.x, st ^ 1);
+        mbar_wait(&sm.full[st], (it >> 1) & 1);
         if (tid < kL) {
             const uint64_t i = leaf * kL + tid;
-            double rv = mode == kLoop ? update_row(s, pcur, alpha, i) : rsrc[i];
+            double rv = sm.vec[st][0][tid];
+            if (mode == kLoop) {  // pcg.cpp:97-98, fused
+                s.x[i] = fma(alpha, sm.vec[st][2][tid], sm.vec[st][3][tid]);
+                rv = fma(-alpha, sm.vec[st][1][tid], rv);
+                s.r[i] = rv;
+            }
             rr = fma(rv, rv, rr);
             sm.rin[tid] = static_cast<float>(rv);  // apply.cpp:90
         }
-        mbar_wait(&sm.full[st], (it >> 1) & 1);
         __syncthreads();
         const float* F = sm.F[st];
         const float* B = sm.B[st];
@@ -343,39 +374,80 @@ __global__ void __launch_bounds__(256) k_leaf_generic(DevSys s, int mode, const 
 // ============================================================================================
 constexpr int kCoarseThreads = 256;
 
+// Shared-memory bytes of k_coarse for a given L_s and subtree width Smax.
+__host__ __device__ inline size_t coarse_smem_bytes(uint64_t ls, uint64_t Smax) {
+    return (2 * (2 * Smax - 1) * ls) * sizeof(double) + (Smax - 1) * ls * ls * sizeof(float) +
+           Smax * 2 * ls * sizeof(float) + (kCoarseThreads / 32) * ls * sizeof(float);
+}
+
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse(DevSys s, int mode) {
     if (mode != kApply && s.sc->done) return;
-    extern __shared__ double csm[];
-    const uint64_t ls = s.ls, rk = s.rk;
+    extern __shared__ __align__(128) unsigned char craw[];
+    const uint64_t ls = s.ls, rk = s.rk, Smax = s.coarse_S;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double* SU = csm;                // (2*32-1) x ls
-    double* SV = csm + 63 * ls;      // (2*32-1) x ls
-    float* coef = reinterpret_cast<float*>(csm + 126 * ls);  // 8 warps x 2 x rk
+    double* SU = reinterpret_cast<double*>(craw);        // (2Smax-1) x ls, local heap order
+    double* SV = SU + (2 * Smax - 1) * ls;
+    float* T = reinterpret_cast<float*>(SV + (2 * Smax - 1) * ls);  // tile slot u: U|V
+    float* Rst = T + (Smax - 1) * ls * ls;                // bottom restrictions (level 0)
+    float* coef = Rst + Smax * 2 * ls;                    // per warp: rk + rk
+    __shared__ uint64_t bar;
     __shared__ int last;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint64_t pol_keep = policy_evict_last();  // tiles + restrictions are re-read every iteration
+    uint32_t phase = 0;
 
     uint64_t task = blockIdx.x;
     uint64_t dlo = s.D;  // depth of this task's bottom layer
     for (int level = 0;; ++level) {
         const uint64_t cnt = 1ULL << dlo;
-        const uint64_t S = cnt < 32 ? cnt : 32;
+        const uint64_t S = cnt < Smax ? cnt : Smax;
         int logS = 0;
         while ((1ULL << logS) < S) ++logS;
         const uint64_t dr = dlo - logS;  // depth of this task's root
-        // bottom layer -> local heap nodes S-1 .. 2S-2
-        for (uint64_t e = tid; e < S * ls; e += blockDim.x) {
-            const uint64_t q = e / ls, j = e % ls, u = S - 1 + q;
-            const uint64_t gi = task * S + q;  // index within depth dlo
+        const uint64_t g0 = (1ULL << dlo) - 1 + task * S;  // heap index of the first bottom node
+        // Stage the subtree's tile factors (one bulk copy per depth: the 2^ld tiles of a depth
+        // are contiguous in heap order) and its bottom layer, on one mbarrier.
+        const bool tiles_tma = (s.tile_base & 3) == 0;  // 16-byte aligned tile section
+        if (tid == 0) {
+            uint32_t bytes = 0;
+            if (tiles_tma)
+                for (int ld = 0; ld < logS; ++ld) bytes += (1u << ld) * uint32_t(ls * ls * 4);
+            bytes += level == 0 ? uint32_t(S * 2 * ls * 4) : uint32_t(2 * S * ls * 8);
+            mbar_expect_tx(&bar, bytes);
+            for (int ld = 0; tiles_tma && ld < logS; ++ld) {
+                const uint64_t m0 = (1ULL << (dr + ld)) - 1 + task * (1ULL << ld);
+                tma_load_1d(T + ((1ULL << ld) - 1) * ls * ls, s.F + s.tile_base + m0 * ls * ls,
+                            uint32_t((1ULL << ld) * ls * ls * 4), &bar, pol_keep);
+            }
             if (level == 0) {
-                SU[u * ls + j] = double(s.restrict_[gi * 2 * ls + j]);
-                SV[u * ls + j] = double(s.restrict_[gi * 2 * ls + ls + j]);
+                tma_load_1d(Rst, s.restrict_ + task * S * 2 * ls, uint32_t(S * 2 * ls * 4), &bar,
+                            pol_keep);
             } else {
-                const uint64_t g = (1ULL << dlo) - 1 + gi;
-                SU[u * ls + j] = __ldcg(&s.node_u[g * ls + j]);
-                SV[u * ls + j] = __ldcg(&s.node_v[g * ls + j]);
+                tma_load_1d(SU + (S - 1) * ls, s.node_u + g0 * ls, uint32_t(S * ls * 8), &bar, pol_keep);
+                tma_load_1d(SV + (S - 1) * ls, s.node_v + g0 * ls, uint32_t(S * ls * 8), &bar, pol_keep);
+            }
+        }
+        if (!tiles_tma)
+            for (int ld = 0; ld < logS; ++ld) {
+                const uint64_t m0 = (1ULL << (dr + ld)) - 1 + task * (1ULL << ld);
+                for (uint64_t e = tid; e < (1ULL << ld) * ls * ls; e += blockDim.x)
+                    T[((1ULL << ld) - 1) * ls * ls + e] = s.F[s.tile_base + m0 * ls * ls + e];
+            }
+        mbar_wait(&bar, phase);
+        phase ^= 1;
+        if (level == 0) {
+            for (uint64_t e = tid; e < S * ls; e += blockDim.x) {
+                const uint64_t q = e / ls, j = e % ls, u = S - 1 + q;
+                SU[u * ls + j] = double(Rst[q * 2 * ls + j]);
+                SV[u * ls + j] = double(Rst[q * 2 * ls + ls + j]);
             }
         }
         __syncthreads();
-        for (int ld = logS - 1; ld >= 0; --ld) {  // up-sweep inside the subtree
+        for (int ld = logS - 1; ld >= 0; --ld) {  // f64 up-sweep inside the subtree
             const uint64_t u0 = (1ULL << ld) - 1, nu = 1ULL << ld;
             for (uint64_t e = tid; e < nu * ls; e += blockDim.x) {
                 const uint64_t u = u0 + e / ls, j = e % ls;
@@ -384,19 +456,20 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse(DevSys s, int mode) {
             }
             __syncthreads();
         }
-        // internal tiles: one warp per tile
+        // Internal tiles, one warp each: coupled_col = V (U^T float(s_r)) and
+        // coupled_row = U (V^T float(s_c)); U^T / V^T accumulate in fp32 over p ascending
+        // (matvec_t), V c / U c' in f64 then cast (matvec), as apply.cpp:125-137.
         float* cr_ = coef + warp * 2 * rk;
         float* cc_ = cr_ + rk;
         for (uint64_t u = warp; u + 1 < S; u += blockDim.x / 32) {
             int ld = 0;
             while ((2ULL << ld) <= u + 1) ++ld;
-            const uint64_t depth = dr + ld, idx = task * (1ULL << ld) + (u + 1 - (1ULL << ld));
-            const uint64_t m = (1ULL << depth) - 1 + idx;
-            const float* U = s.F + s.tile_base + m * ls * ls;
+            const uint64_t m = (1ULL << (dr + ld)) - 1 + task * (1ULL << ld) + (u + 1 - (1ULL << ld));
+            const float* U = T + u * ls * ls;
             const float* V = U + ls * rk;
             const double* sr = SU + (2 * u + 1) * ls;
             const double* sc = SV + (2 * u + 2) * ls;
-            for (uint64_t q = lane; q < rk; q += 32) {  // U^T float(s_r), V^T float(s_c)
+            for (uint64_t q = lane; q < rk; q += 32) {
                 float a = 0.f, b = 0.f;
                 for (uint64_t p = 0; p < ls; ++p) {
                     a = fmaf(U[p * rk + q], float(sr[p]), a);
@@ -406,7 +479,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse(DevSys s, int mode) {
                 cc_[q] = b;
             }
             __syncwarp();
-            for (uint64_t j = lane; j < ls; j += 32) {  // coupled_col = V c, coupled_row = U c'
+            for (uint64_t j = lane; j < ls; j += 32) {
                 double a = 0.0, b = 0.0;
                 for (uint64_t q = 0; q < rk; ++q) {
                     a = fma(double(V[j * rk + q]), double(cr_[q]), a);
@@ -417,8 +490,8 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse(DevSys s, int mode) {
             }
             __syncwarp();
         }
-        if (dr == 0) return;  // root handled
-        {   // publish the subtree root's sums
+        if (dr == 0) return;  // the root tile is done
+        {   // publish the subtree root's sums for the next level
             const uint64_t g = (1ULL << dr) - 1 + task;
             for (uint64_t j = tid; j < ls; j += blockDim.x) {
                 s.node_u[g * ls + j] = SU[j];
@@ -426,7 +499,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse(DevSys s, int mode) {
             }
         }
         const uint64_t cnt2 = 1ULL << dr;
-        const uint64_t S2 = cnt2 < 32 ? cnt2 : 32;
+        const uint64_t S2 = cnt2 < Smax ? cnt2 : Smax;
         __threadfence();
         __syncthreads();
         if (tid == 0) {
@@ -440,6 +513,8 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse(DevSys s, int mode) {
         __syncthreads();
         if (!last) return;
         __threadfence();
+        // generic-proxy writes of other CTAs (node sums) must be visible to the async proxy
+        asm volatile("fence.proxy.async.global;" ::: "memory");
         task /= S2;
         dlo = dr;
     }
@@ -478,34 +553,56 @@ __device__ __forceinline__ bool prolong_skip(const DevSys& s, int mode) {
 __global__ void __launch_bounds__(256) k_prolong_fast(DevSys s, int mode, const double* rin_ext,
                                                       double* zout) {
     if (prolong_skip(s, mode)) return;
-    __shared__ float g[2][kLs];
+    __shared__ __align__(16) float g[2][kLs];
     __shared__ double su[kL], sv[kL];
     const int tid = threadIdx.x;
     const uint64_t leaf = blockIdx.x, K = s.K, D = s.D;
+    // Issue every independent load first: the 32 KB bridge pair (streamed once), then the
+    // epilogue operands, then the ancestor gather (L2-resident couplings).
+    const int l8 = tid & 7, rowi = tid >> 3;
+    const float* Bu = s.F + s.bridge_base + leaf * (2 * kL * kLs);
+    const float* Bv = Bu + kL * kLs;
+    float4 u4[4], v4[4];
+#pragma unroll
+    for (int ps = 0; ps < 4; ++ps) {
+        const int row = ps * 32 + rowi;
+        u4[ps] = ldg_stream(reinterpret_cast<const float4*>(Bu + row * kLs) + l8);
+        v4[ps] = ldg_stream(reinterpret_cast<const float4*>(Bv + row * kLs) + l8);
+    }
+    double yl = 0.0, rv = 0.0, ad = 1.0;
+    float gate = 0.f;
+    const uint64_t i = leaf * kL + (tid & (kL - 1));
+    if (tid < kL) {
+        yl = s.y_loc[i];
+        rv = mode == kApply ? rin_ext[i] : s.r[i];
+        ad = s.a_diag[i];
+        gate = s.F[s.gate_base + i];
+    }
     if (tid < 2 * kLs) {
         const int side = tid >> 5, j = tid & 31;
         const float* src = side ? s.ccol : s.crow;
         double acc = 0.0;
-        for (uint64_t d = 0; d < D; ++d) {
-            const uint64_t m = ((K + leaf) >> (D - d)) - 1;
-            if (((leaf >> (D - 1 - d)) & 1ULL) == uint64_t(side)) acc += double(__ldcg(&src[m * kLs + j]));
+        for (uint64_t d0 = 0; d0 < D; d0 += 8) {
+            float t[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint64_t d = d0 + q;
+                t[q] = 0.f;
+                if (d < D && ((leaf >> (D - 1 - d)) & 1ULL) == uint64_t(side))
+                    t[q] = __ldcg(&src[(((K + leaf) >> (D - d)) - 1) * kLs + j]);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint64_t d = d0 + q;
+                if (d < D && ((leaf >> (D - 1 - d)) & 1ULL) == uint64_t(side)) acc += double(t[q]);
+            }
         }
         g[side][j] = float(acc);
     }
     __syncthreads();
-    {   // Ũ_k g_r and Ṽ_k g_c, f64 accumulation; 8 lanes per row, 128-bit streaming loads
-        const int l8 = tid & 7, rowi = tid >> 3;
+    {   // Ũ_k g_r and Ṽ_k g_c, f64 accumulation; 8 lanes per row
         const float4 gr = reinterpret_cast<const float4*>(g[0])[l8];
         const float4 gc = reinterpret_cast<const float4*>(g[1])[l8];
-        const float* Bu = s.F + s.bridge_base + leaf * (2 * kL * kLs);
-        const float* Bv = Bu + kL * kLs;
-        float4 u4[4], v4[4];
-#pragma unroll
-        for (int ps = 0; ps < 4; ++ps) {
-            const int row = ps * 32 + rowi;
-            u4[ps] = ldg_stream(reinterpret_cast<const float4*>(Bu + row * kLs) + l8);
-            v4[ps] = ldg_stream(reinterpret_cast<const float4*>(Bv + row * kLs) + l8);
-        }
 #pragma unroll
         for (int ps = 0; ps < 4; ++ps) {
             double au = fma(double(u4[ps].w), double(gr.w), fma(double(u4[ps].z), double(gr.z),
@@ -527,13 +624,10 @@ __global__ void __launch_bounds__(256) k_prolong_fast(DevSys s, int mode, const 
     __syncthreads();
     double rz = 0.0;
     if (tid < kL) {
-        const uint64_t i = leaf * kL + tid;
-        const double rv = mode == kApply ? rin_ext[i] : s.r[i];
-        const double gate = double(s.F[s.gate_base + i]);
-        double y = s.y_loc[i];
+        double y = yl;
         y += su[tid];
         y += sv[tid];
-        y += gate * rv / s.a_diag[i] + s.sc->shift * rv;  // apply.cpp:169-173
+        y += double(gate) * rv / ad + s.sc->shift * rv;  // apply.cpp:169-173
         (mode == kApply ? zout : s.z)[i] = y;
         rz = rv * y;
     }

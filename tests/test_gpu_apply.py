@@ -1,0 +1,137 @@
+"""GPU parity of the preconditioner apply (apply.cpp:79-174) through the C ABI.
+
+Gate: relative l2 <= 1e-5 against apply<double> of the same float factors (the reference's
+own fp32 apply is itself up to ~7e-6 from it); the distance to apply<float> is
+checked at the same tolerance. Gate-only tensors must reproduce Jacobi bit-for-bit."""
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def dev(H):
+    return H.Device(0)
+
+
+def tensor(H, n, leaf, ls, sigma, seed, frame):
+    return H.init_factors(H.build_partition(n, leaf), ls, H.FactorInit.random, sigma,
+                          H.RngStream(seed, frame, H.RngPurpose.factor_init))
+
+
+@pytest.mark.parametrize("n,leaf,ls", [(256, 128, 32), (256, 64, 16), (32, 16, 4)])
+def test_gate_only_is_jacobi_bit_exact(H, n, leaf, ls):
+    # test_apply.cpp:40-66, test_pcg.cpp:154-167
+    f = tensor(H, n, leaf, ls, 0.0, 1, 0)
+    rng = np.random.default_rng(2)
+    diag = 1.0 + np.abs(rng.standard_normal(n))
+    r = rng.standard_normal(n)
+    d = dev(H)
+    y = H.apply(f, diag, r, device=d)
+    assert (y == r / diag).all()
+    assert (H.apply(f, diag, np.zeros(n), device=d) == 0.0).all()
+    g = f.copy()
+    g.spd_shift_enabled, g.spd_shift_raw = True, 0.0
+    ys = H.apply(g, diag, r, device=d)
+    np.testing.assert_allclose(ys, r / diag + np.log(2.0) * r, rtol=1e-12)
+
+
+CASES = [  # (n, leaf, ls, sigma) — fast path at (128, 32), generic elsewhere
+    (256, 128, 32, 1.0), (512, 128, 32, 1.0), (1024, 128, 32, 1.0), (8192, 128, 32, 1e-2),
+    (65536, 128, 32, 1e-2), (65536, 128, 32, 1.0), (262144, 128, 32, 1e-2),
+    (256, 64, 16, 1.0), (200, 100, 10, 0.5), (32, 16, 4, 1.0), (2048, 64, 32, 1.0),
+    (4096, 256, 16, 1.0), (128, 64, 64, 1.0),
+]
+
+
+@pytest.mark.parametrize("n,leaf,ls,sigma", CASES)
+def test_apply_matches_reference_f64(H, oracle, n, leaf, ls, sigma):
+    f = tensor(H, n, leaf, ls, sigma, 8, n)
+    rng = np.random.default_rng(n + leaf)
+    diag = 1.0 + np.abs(rng.standard_normal(n))
+    d = dev(H)
+    for t in range(2):
+        r = rng.standard_normal(n)
+        y = H.apply(f, diag, r, device=d)
+        y64 = oracle.apply_f64(n, leaf, ls, f.data.astype(np.float64), diag, r)
+        y32 = oracle.apply_f32(n, leaf, ls, f.data, diag, r)
+        assert rel_l2(y, y64) <= TOL, (rel_l2(y, y64), rel_l2(y32, y64))
+        assert rel_l2(y, y32) <= TOL
+    assert d.fast_path() == (leaf == 128 and ls == 32)
+
+
+def test_apply_golden_vector(H, golden):
+    f = tensor(H, 512, 128, 32, 1.0, 8, 512)
+    y = H.apply(f, golden["apply512_diag"], golden["apply512_r"])
+    assert rel_l2(y, golden["apply512_y_f64"]) <= TOL
+    assert rel_l2(y, golden["apply512_y_f32"]) <= TOL
+
+
+def test_apply_spd_shift_and_determinism(H, oracle):
+    n = 4096
+    f = tensor(H, n, 128, 32, 0.3, 5, 1)
+    f.spd_shift_enabled, f.spd_shift_raw = True, -0.7
+    rng = np.random.default_rng(9)
+    diag = 1.0 + np.abs(rng.standard_normal(n))
+    r = rng.standard_normal(n)
+    d = dev(H)
+    y1 = H.apply(f, diag, r, device=d)
+    y2 = d.apply(r)
+    assert (y1 == y2).all()  # run-to-run identical
+    y64 = oracle.apply_f64(n, 128, 32, f.data.astype(np.float64), diag, r, 1, -0.7)
+    assert rel_l2(y1, y64) <= TOL
+
+
+@pytest.mark.parametrize("n,leaf,ls", [(512, 128, 32), (256, 64, 16)])
+def test_symmetry_and_linearity(H, n, leaf, ls):
+    # test_apply.cpp:114-142 (r^T M s = s^T M r), :197-216 (linearity)
+    f = tensor(H, n, leaf, ls, 1.0, 11, 0)
+    rng = np.random.default_rng(12)
+    diag = 1.0 + np.abs(rng.standard_normal(n))
+    d = dev(H)
+    d.load_factors(f)
+    d.set_diag(diag)
+    for _ in range(5):
+        r, s = rng.standard_normal(n), rng.standard_normal(n)
+        Ms, Mr = d.apply(s), d.apply(r)
+        assert abs(r @ Ms - s @ Mr) <= 1e-5 * max(np.abs(r * Ms).sum(), 1.0)
+        a, b = 1.7, -0.3
+        lin = d.apply(a * r + b * s)
+        assert rel_l2(lin, a * Mr + b * Ms) <= 1e-5
+
+
+def test_apply_dense_oracle(H, ref):
+    # acceptance criterion 3 style: chain apply vs dense assembly (apply.cpp:184-260)
+    for n in (256, 512, 1024):
+        leaf = H.clamp_leaf_size(n, 128)
+        f = tensor(H, n, leaf, 32, 1.0, 2024, n * 100)
+        rng = np.random.default_rng(n)
+        diag = 1.0 + np.abs(rng.standard_normal(n))
+        M = ref.assemble_dense(n, leaf, 32, f.data, diag)
+        r = rng.standard_normal(n)
+        assert rel_l2(H.apply(f, diag, r), M @ r) <= TOL
+
+
+def test_contract_violations(H):
+    f = tensor(H, 256, 64, 16, 1.0, 81, 0)
+    d = dev(H)
+    d.load_factors(f)
+    d.set_diag(np.ones(256))
+    with pytest.raises(ValueError):
+        H.apply(f, np.ones(256), np.zeros(100), device=d)
+    with pytest.raises(ValueError):
+        d.set_diag(np.ones(100)) if False else H.apply(f, np.ones(100), np.zeros(256), device=H.Device(0))
+
+
+@pytest.mark.slow
+def test_apply_1m_3d_seeded(H, oracle):
+    fr = H.make_frame_3d(128, 128, 64, 2024, 0)
+    p = H.build_partition(fr.n, 128)
+    f = H.init_factors(p, 32, H.FactorInit.jacobi_seed, 1e-2, H.RngStream(2024, 0, H.RngPurpose.factor_init))
+    diag = fr.A.diagonal()
+    r = fr.b
+    y = H.apply(f, diag, r)
+    y64 = oracle.apply_f64(fr.n, 128, 32, f.data.astype(np.float64), diag, r)
+    assert rel_l2(y, y64) <= TOL
