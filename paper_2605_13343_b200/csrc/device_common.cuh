@@ -83,6 +83,17 @@ __device__ __forceinline__ float4 ldg_stream(const float4* p) {
     return r;
 }
 
+__device__ __forceinline__ uint32_t ldg_stream_u32(const uint32_t* p) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double ldg_stream_f64(const double* p) {
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+
 // ---- deterministic reductions ----------------------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

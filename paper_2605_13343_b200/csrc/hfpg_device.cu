@@ -101,6 +101,12 @@ void invalidate_graph(hfpg_handle* h) {
 uint64_t leaf_grid(const hfpg_handle* h) {
     return h->fast ? std::min<uint64_t>(h->L.k, uint64_t(h->num_sms)) : h->L.k;
 }
+uint64_t prolong_grid(const hfpg_handle* h) {
+    return h->fast ? std::min<uint64_t>(h->L.k, uint64_t(h->num_sms) * 2) : h->L.k;
+}
+uint64_t spmv_grid(const hfpg_handle* h) {
+    return std::max<uint64_t>(1, std::min<uint64_t>((h->n + 255) / 256, uint64_t(h->num_sms) * 4));
+}
 uint64_t simple_grid(const hfpg_handle* h) {
     return std::max<uint64_t>(1, std::min<uint64_t>((h->n + 255) / 256, uint64_t(h->num_sms) * 8));
 }
@@ -136,7 +142,7 @@ void ensure_workspace(hfpg_handle* h) {
         h->ws_layout = L;
         h->have_ws = true;
     }
-    const uint64_t need = 2 * std::max<uint64_t>({(n + 255) / 256, h->have_factors ? h->L.k : 1,
+    const uint64_t need = 2 * std::max<uint64_t>({(n + 255) / 256, h->have_factors ? 2 * h->L.k : 1,
                                                    uint64_t(h->num_sms) * 8});
     if (h->partials_cap < need) {
         invalidate_graph(h);
@@ -211,11 +217,15 @@ void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
         k_leaf_generic<<<unsigned(L.k), 256, 2 * L.l * sizeof(float), h->stream>>>(s, mode, rin);
     }
     CK(cudaGetLastError());
-    const uint64_t S0 = std::min<uint64_t>(L.k, coarse_width(L));
-    k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(s, mode);
+    if (h->fast) {
+        k_coarse_fast<<<unsigned(L.k / std::min<uint64_t>(L.k, 32)), 256, 0, h->stream>>>(s, mode);
+    } else {
+        const uint64_t S0 = std::min<uint64_t>(L.k, coarse_width(L));
+        k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(s, mode);
+    }
     CK(cudaGetLastError());
     if (h->fast)
-        k_prolong_fast<<<unsigned(L.k), 256, 0, h->stream>>>(s, mode, rin, zout);
+        k_prolong_fast<<<unsigned(prolong_grid(h)), 256, sizeof(ProlSmem), h->stream>>>(s, mode, rin, zout);
     else
         k_prolong_generic<<<unsigned(L.k), 256, 2 * L.ls * sizeof(float), h->stream>>>(s, mode, rin, zout);
     CK(cudaGetLastError());
@@ -223,7 +233,7 @@ void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
 
 void launch_iteration(hfpg_handle* h) {
     const DevSys& s = h->sys;
-    k_spmv<kLoop><<<unsigned((h->n + 255) / 256), 256, 0, h->stream>>>(s, nullptr, nullptr);
+    k_spmv<kLoop><<<unsigned(spmv_grid(h)), 256, 0, h->stream>>>(s, nullptr, nullptr);
     CK(cudaGetLastError());
     if (h->precond == HFPG_PRECOND_FACTOR) {
         launch_apply(h, kLoop, nullptr, nullptr);
@@ -251,6 +261,8 @@ void configure_kernels() {
         CK(cudaFuncSetAttribute(k_leaf_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(sizeof(LeafSmem))));
         CK(cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CK(cudaFuncSetAttribute(k_prolong_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(sizeof(ProlSmem))));
         CK(cudaFuncSetAttribute(k_leaf_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     });
 }
@@ -543,7 +555,7 @@ int hfpg_spmv(hfpg_handle* h, const double* x, double* y, int where) {
             xin = h->scratch;
             yout = h->ap;
         }
-        k_spmv<kApply><<<unsigned((h->n + 255) / 256), 256, 0, h->stream>>>(h->sys, xin, yout);
+        k_spmv<kApply><<<unsigned(spmv_grid(h)), 256, 0, h->stream>>>(h->sys, xin, yout);
         CK(cudaGetLastError());
         if (where == HFPG_HOST) copy_out(h, y, h->ap, h->n, HFPG_HOST);
         CK(cudaStreamSynchronize(h->stream));
@@ -632,17 +644,20 @@ int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out) {
         for (uint32_t rep = 0; rep < std::max(reps, 1u); ++rep) {
             CK(cudaMemcpyAsync(h->sc, &prof, sizeof(Scalars), cudaMemcpyHostToDevice, h->stream));
             CK(cudaEventRecord(ev[0], h->stream));
-            k_spmv<kLoop><<<unsigned((h->n + 255) / 256), 256, 0, h->stream>>>(h->sys, nullptr, nullptr);
+            k_spmv<kLoop><<<unsigned(spmv_grid(h)), 256, 0, h->stream>>>(h->sys, nullptr, nullptr);
             CK(cudaEventRecord(ev[1], h->stream));
             if (h->fast)
                 k_leaf_fast<<<unsigned(leaf_grid(h)), kLeafThreads, sizeof(LeafSmem), h->stream>>>(h->sys, kLoop, nullptr);
             else
                 k_leaf_generic<<<unsigned(L.k), 256, 2 * L.l * sizeof(float), h->stream>>>(h->sys, kLoop, nullptr);
             CK(cudaEventRecord(ev[2], h->stream));
-            k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(h->sys, kLoop);
+            if (h->fast)
+                k_coarse_fast<<<unsigned(L.k / std::min<uint64_t>(L.k, 32)), 256, 0, h->stream>>>(h->sys, kLoop);
+            else
+                k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(h->sys, kLoop);
             CK(cudaEventRecord(ev[3], h->stream));
             if (h->fast)
-                k_prolong_fast<<<unsigned(L.k), 256, 0, h->stream>>>(h->sys, kLoop, nullptr, nullptr);
+                k_prolong_fast<<<unsigned(prolong_grid(h)), 256, sizeof(ProlSmem), h->stream>>>(h->sys, kLoop, nullptr, nullptr);
             else
                 k_prolong_generic<<<unsigned(L.k), 256, 2 * L.ls * sizeof(float), h->stream>>>(h->sys, kLoop, nullptr, nullptr);
             CK(cudaEventRecord(ev[4], h->stream));

@@ -79,7 +79,7 @@ __device__ __forceinline__ void finish_residual(Scalars* sc, double* history, do
 // PCG mode fuses p = z + beta p_prev (pcg.cpp:118) into the gathers and reduces p.Ap, p.p.
 // ============================================================================================
 template <int MODE>  // kInit unused; kLoop = PCG, kApply = plain y = A x
-__global__ void __launch_bounds__(256) k_spmv(DevSys s, const double* xin, double* yout) {
+__global__ void __launch_bounds__(256, 4) k_spmv(DevSys s, const double* xin, double* yout) {
     if (MODE == kLoop && s.sc->done) return;
     const unsigned long long k = MODE == kLoop ? s.sc->k : 0ULL;
     const double beta = MODE == kLoop ? s.sc->beta : 0.0;
@@ -87,16 +87,17 @@ __global__ void __launch_bounds__(256) k_spmv(DevSys s, const double* xin, doubl
     const double* pp_ = MODE == kLoop ? p_prev(s, k) : nullptr;
     double* pnew = MODE == kLoop ? p_cur(s, k) : nullptr;
     double* y = MODE == kLoop ? s.ap : yout;
-    const uint64_t row = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     double v[2] = {0.0, 0.0};
-    if (row < s.n) {
+    // persistent grid-stride over rows: one CTA partial (and one fence) per CTA, not per row
+    for (uint64_t row = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < s.n;
+         row += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t sl = row >> 5, lane = row & 31;
         const uint64_t base = s.slice_off[sl], w = (s.slice_off[sl + 1] - base) >> 5;
         double acc = 0.0;
-        // Batches of 8 slots: all index/value loads first, then the gathers, then the
-        // accumulation in slot order. The reference computes acc += a * x as a rounded
-        // product plus a rounded sum (its csr.cpp:76 loop is not FMA-contracted), so the
-        // products/sums are explicit __dmul_rn/__dadd_rn: ap is bit-identical to spmv().
+        // Batches of 8 slots: the streamed index/value loads first (no L1 allocation), then
+        // the gathers (L1-cached: neighbours share Morton bricks), then the accumulation in
+        // slot order. The reference's csr.cpp:76 loop is not FMA-contracted, so products and
+        // sums are rounded separately (__dmul_rn/__dadd_rn): ap is bit-identical to spmv().
         for (uint64_t j0 = 0; j0 < w; j0 += 8) {
             uint32_t c[8];
             double a[8], pc[8];
@@ -104,8 +105,8 @@ __global__ void __launch_bounds__(256) k_spmv(DevSys s, const double* xin, doubl
             for (int q = 0; q < 8; ++q)
                 if (j0 + q < w) {
                     const uint64_t idx = base + (j0 + q) * 32 + lane;
-                    c[q] = __ldg(&s.sell_cols[idx]);
-                    a[q] = __ldg(&s.sell_vals[idx]);
+                    c[q] = ldg_stream_u32(&s.sell_cols[idx]);
+                    a[q] = ldg_stream_f64(&s.sell_vals[idx]);
                 }
 #pragma unroll
             for (int q = 0; q < 8; ++q)
@@ -118,8 +119,8 @@ __global__ void __launch_bounds__(256) k_spmv(DevSys s, const double* xin, doubl
         if (MODE == kLoop) {
             const double pi = fma(beta, pp_[row], z[row]);
             pnew[row] = pi;
-            v[0] = pi * acc;
-            v[1] = pi * pi;
+            v[0] = fma(pi, acc, v[0]);
+            v[1] = fma(pi, pi, v[1]);
         }
     }
     if (MODE != kLoop) return;
@@ -198,6 +199,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mod
     const double* pcur = mode == kLoop ? p_cur(s, s.sc->k) : nullptr;
     const uint64_t K = s.K;
     const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
     const int nvec = mode == kLoop ? 4 : 1;
     const uint32_t stage_bytes = kFBytes + kBBytes + nvec * kL * 8;
 
@@ -217,9 +219,11 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mod
         for (int q = 0; q < 4; ++q)
             tma_load_1d(&sm.F[st][q * kL * kL / 4], f + q * kL * kL / 4, kFBytes / 4,
                         &sm.full[st], pol_stream);
-        tma_load_1d(&sm.B[st][0], b, kBBytes / 2, &sm.full[st], pol_stream);
-        tma_load_1d(&sm.B[st][kL * kLs], b + kL * kLs, kBBytes / 2, &sm.full[st], pol_stream);
-        tma_load_1d(sm.vec[st][0], rsrc + leaf * kL, kL * 8, &sm.full[st], pol_stream);
+        // bridges: evict_last — the prolongation walks the leaves in reverse and finds the
+        // most recently streamed ones still in L2
+        tma_load_1d(&sm.B[st][0], b, kBBytes / 2, &sm.full[st], pol_keep);
+        tma_load_1d(&sm.B[st][kL * kLs], b + kL * kLs, kBBytes / 2, &sm.full[st], pol_keep);
+        tma_load_1d(sm.vec[st][0], rsrc + leaf * kL, kL * 8, &sm.full[st], pol_keep);
         if (mode == kLoop) {
             tma_load_1d(sm.vec[st][1], s.ap + leaf * kL, kL * 8, &sm.full[st], pol_stream);
             tma_load_1d(sm.vec[st][2], pcur + leaf * kL, kL * 8, &sm.full[st], pol_stream);
@@ -372,6 +376,150 @@ __global__ void __launch_bounds__(256) k_leaf_generic(DevSys s, int mode, const 
 // computes its internal tiles, publishes its root sums, and the last-arriving CTA of each
 // group of siblings carries on one level up — one launch covers the whole tree.
 // ============================================================================================
+// Sum 16 per-lane values over the warp: afterwards lane L holds the total of column L >> 1
+// (recursive halving; 16 shuffles instead of 16 x 5).
+__device__ __forceinline__ float transpose_reduce16(const float (&a)[16], int lane) {
+    float t8[8], t4[4], t2[2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const bool hi = lane & 16;
+        t8[i] = (hi ? a[i + 8] : a[i]) + __shfl_xor_sync(0xffffffffu, hi ? a[i] : a[i + 8], 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const bool hi = lane & 8;
+        t4[i] = (hi ? t8[i + 4] : t8[i]) + __shfl_xor_sync(0xffffffffu, hi ? t8[i] : t8[i + 4], 8);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const bool hi = lane & 4;
+        t2[i] = (hi ? t4[i + 2] : t4[i]) + __shfl_xor_sync(0xffffffffu, hi ? t4[i] : t4[i + 2], 4);
+    }
+    const bool hi = lane & 2;
+    float t1 = (hi ? t2[1] : t2[0]) + __shfl_xor_sync(0xffffffffu, hi ? t2[0] : t2[1], 2);
+    return t1 + __shfl_xor_sync(0xffffffffu, t1, 1);
+}
+
+// One tile (L_s = 32, rank 16) per warp, operands in registers: lane p holds row p of U_m and
+// V_m. coupled_col = V (U^T float(s_r)), coupled_row = U (V^T float(s_c)): the U^T / V^T
+// products accumulate in fp32 (as matvec_t), the V c / U c' products in f64 then round to
+// float (as matvec), apply.cpp:125-137.
+__device__ __forceinline__ void tile_warp32(const float4 (&u4)[4], const float4 (&v4)[4],
+                                            float sr, float sc, int lane, float* ccol,
+                                            float* crow) {
+    float u[16], v[16], a[16], b[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        u[4 * i] = u4[i].x; u[4 * i + 1] = u4[i].y; u[4 * i + 2] = u4[i].z; u[4 * i + 3] = u4[i].w;
+        v[4 * i] = v4[i].x; v[4 * i + 1] = v4[i].y; v[4 * i + 2] = v4[i].z; v[4 * i + 3] = v4[i].w;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        a[q] = u[q] * sr;
+        b[q] = v[q] * sc;
+    }
+    const float coef_r = transpose_reduce16(a, lane);  // (U^T s_r)[lane >> 1]
+    const float coef_c = transpose_reduce16(b, lane);  // (V^T s_c)[lane >> 1]
+    double acc_c = 0.0, acc_r = 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const float cr = __shfl_sync(0xffffffffu, coef_r, 2 * q);
+        const float cc = __shfl_sync(0xffffffffu, coef_c, 2 * q);
+        acc_c = fma(double(v[q]), double(cr), acc_c);
+        acc_r = fma(double(u[q]), double(cc), acc_r);
+    }
+    ccol[lane] = float(acc_c);
+    crow[lane] = float(acc_r);
+}
+
+__device__ __forceinline__ void load_tile32(const DevSys& s, uint64_t m, int lane, float4 (&u4)[4],
+                                            float4 (&v4)[4]) {
+    const float4* U = reinterpret_cast<const float4*>(s.F + s.tile_base + m * 1024) + lane * 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        u4[i] = __ldg(U + i);
+        v4[i] = __ldg(U + 128 + i);  // V_m = U_m + 32 x 16 floats
+    }
+}
+
+// Coarse stage, fast path (L_s = 32): the bisection tree in heap order; each CTA owns an
+// aligned subtree of up to 32 bottom nodes, runs the f64 up-sweep in shared memory, computes
+// its internal tiles a warp each, publishes the root sums, and the last CTA of each group of
+// 32 siblings continues one level up (no grid barrier, one launch for the whole tree).
+__global__ void __launch_bounds__(256) k_coarse_fast(DevSys s, int mode) {
+    if (mode != kApply && s.sc->done) return;
+    __shared__ double SU[63 * 32], SV[63 * 32];
+    __shared__ int last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint64_t task = blockIdx.x;
+    uint64_t dlo = s.D;
+    for (int level = 0;; ++level) {
+        const uint64_t cnt = 1ULL << dlo;
+        const uint64_t S = cnt < 32 ? cnt : 32;
+        int logS = 0;
+        while ((1ULL << logS) < S) ++logS;
+        const uint64_t dr = dlo - logS;
+        auto tile_id = [&](uint64_t u) {
+            int ld = 0;
+            while ((2ULL << ld) <= u + 1) ++ld;
+            return (1ULL << (dr + ld)) - 1 + task * (1ULL << ld) + (u + 1 - (1ULL << ld));
+        };
+        // this warp's first tile: issue its loads before the bottom layer / up-sweep
+        float4 u4[4], v4[4];
+        if (uint64_t(warp) + 1 < S) load_tile32(s, tile_id(warp), lane, u4, v4);
+        const uint64_t g0 = (1ULL << dlo) - 1 + task * S;
+        for (uint64_t e = tid; e < S * 32; e += blockDim.x) {
+            const uint64_t q = e >> 5, j = e & 31, u = S - 1 + q;
+            if (level == 0) {
+                SU[u * 32 + j] = double(__ldcg(&s.restrict_[(task * S + q) * 64 + j]));
+                SV[u * 32 + j] = double(__ldcg(&s.restrict_[(task * S + q) * 64 + 32 + j]));
+            } else {
+                SU[u * 32 + j] = __ldcg(&s.node_u[(g0 + q) * 32 + j]);
+                SV[u * 32 + j] = __ldcg(&s.node_v[(g0 + q) * 32 + j]);
+            }
+        }
+        __syncthreads();
+        for (int ld = logS - 1; ld >= 0; --ld) {  // f64 up-sweep
+            const uint64_t u0 = (1ULL << ld) - 1;
+            for (uint64_t e = tid; e < (1ULL << ld) * 32; e += blockDim.x) {
+                const uint64_t u = u0 + (e >> 5), j = e & 31;
+                SU[u * 32 + j] = SU[(2 * u + 1) * 32 + j] + SU[(2 * u + 2) * 32 + j];
+                SV[u * 32 + j] = SV[(2 * u + 1) * 32 + j] + SV[(2 * u + 2) * 32 + j];
+            }
+            __syncthreads();
+        }
+        for (uint64_t u = warp; u + 1 < S; u += 8) {
+            const uint64_t m = tile_id(u);
+            if (u != uint64_t(warp)) load_tile32(s, m, lane, u4, v4);
+            tile_warp32(u4, v4, float(SU[(2 * u + 1) * 32 + lane]), float(SV[(2 * u + 2) * 32 + lane]),
+                        lane, s.ccol + m * 32, s.crow + m * 32);
+        }
+        if (dr == 0) return;
+        if (tid < 32) {
+            const uint64_t g = (1ULL << dr) - 1 + task;
+            s.node_u[g * 32 + tid] = SU[tid];
+            s.node_v[g * 32 + tid] = SV[tid];
+        }
+        const uint64_t cnt2 = 1ULL << dr;
+        const uint64_t S2 = cnt2 < 32 ? cnt2 : 32;
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            int logS2 = 0;
+            while ((1ULL << logS2) < S2) ++logS2;
+            const uint64_t parent = (1ULL << (dr - logS2)) - 1 + task / S2;
+            const unsigned t = atomicAdd(&s.tree_counters[parent], 1u);
+            last = (t == S2 - 1);
+            if (last) s.tree_counters[parent] = 0u;
+        }
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        task /= S2;
+        dlo = dr;
+    }
+}
+
 constexpr int kCoarseThreads = 256;
 
 // Shared-memory bytes of k_coarse for a given L_s and subtree width Smax.
@@ -550,86 +698,120 @@ __device__ __forceinline__ bool prolong_skip(const DevSys& s, int mode) {
     return true;
 }
 
-__global__ void __launch_bounds__(256) k_prolong_fast(DevSys s, int mode, const double* rin_ext,
-                                                      double* zout) {
+// Prolongation, fast path: persistent, 2 CTAs x 256 threads per SM, a 3-stage TMA ring of
+// {Ũ_k|Ṽ_k (32 KB), y_loc_k, r_k, a_diag_k, gate_k}. Leaves are walked in REVERSE order: the
+// leaf kernel streamed the bridges with an evict_last policy, so the last ~100 MB it read are
+// still in L2 when this kernel starts. The ancestor gather of the next leaf is prefetched into
+// registers while the current one computes.
+constexpr int kProlStages = 3;
+constexpr int kMaxDepth = 24;
+struct ProlSmem {
+    float B[kProlStages][2 * kL * kLs];
+    double vec[kProlStages][3][kL];  // y_loc, r, a_diag
+    float gate[kProlStages][kL];
+    float g[2][kLs];
+    double su[kL], sv[kL];
+    uint64_t full[kProlStages];
+};
+
+__global__ void __launch_bounds__(256, 2) k_prolong_fast(DevSys s, int mode, const double* rin_ext,
+                                                         double* zout) {
     if (prolong_skip(s, mode)) return;
-    __shared__ __align__(16) float g[2][kLs];
-    __shared__ double su[kL], sv[kL];
+    extern __shared__ __align__(128) unsigned char praw[];
+    ProlSmem& sm = *reinterpret_cast<ProlSmem*>(praw);
     const int tid = threadIdx.x;
-    const uint64_t leaf = blockIdx.x, K = s.K, D = s.D;
-    // Issue every independent load first: the 32 KB bridge pair (streamed once), then the
-    // epilogue operands, then the ancestor gather (L2-resident couplings).
-    const int l8 = tid & 7, rowi = tid >> 3;
-    const float* Bu = s.F + s.bridge_base + leaf * (2 * kL * kLs);
-    const float* Bv = Bu + kL * kLs;
-    float4 u4[4], v4[4];
-#pragma unroll
-    for (int ps = 0; ps < 4; ++ps) {
-        const int row = ps * 32 + rowi;
-        u4[ps] = ldg_stream(reinterpret_cast<const float4*>(Bu + row * kLs) + l8);
-        v4[ps] = ldg_stream(reinterpret_cast<const float4*>(Bv + row * kLs) + l8);
+    const uint64_t K = s.K, D = s.D;
+    const double* rsrc = mode == kApply ? rin_ext : s.r;
+    double* zdst = mode == kApply ? zout : s.z;
+    const double shift = s.sc->shift;
+    const uint64_t pol = policy_evict_first();
+    const uint64_t nl = K > blockIdx.x ? (K - 1 - blockIdx.x) / gridDim.x + 1 : 0;  // my leaves
+    auto leaf_of = [&](uint64_t i) { return K - 1 - (blockIdx.x + i * gridDim.x); };
+    if (tid == 0) {
+        for (int q = 0; q < kProlStages; ++q) mbar_init(&sm.full[q], 1);
+        fence_mbar_init();
     }
-    double yl = 0.0, rv = 0.0, ad = 1.0;
-    float gate = 0.f;
-    const uint64_t i = leaf * kL + (tid & (kL - 1));
-    if (tid < kL) {
-        yl = s.y_loc[i];
-        rv = mode == kApply ? rin_ext[i] : s.r[i];
-        ad = s.a_diag[i];
-        gate = s.F[s.gate_base + i];
-    }
-    if (tid < 2 * kLs) {
-        const int side = tid >> 5, j = tid & 31;
+    __syncthreads();
+    auto issue = [&](uint64_t i) {
+        const int st = int(i % kProlStages);
+        const uint64_t leaf = leaf_of(i);
+        mbar_expect_tx(&sm.full[st], 2 * kL * kLs * 4 + 3 * kL * 8 + kL * 4);
+        const float* b = s.F + s.bridge_base + leaf * (2 * kL * kLs);
+        tma_load_1d(&sm.B[st][0], b, kL * kLs * 4, &sm.full[st], pol);
+        tma_load_1d(&sm.B[st][kL * kLs], b + kL * kLs, kL * kLs * 4, &sm.full[st], pol);
+        tma_load_1d(sm.vec[st][0], s.y_loc + leaf * kL, kL * 8, &sm.full[st], pol);
+        tma_load_1d(sm.vec[st][1], rsrc + leaf * kL, kL * 8, &sm.full[st], pol);
+        tma_load_1d(sm.vec[st][2], s.a_diag + leaf * kL, kL * 8, &sm.full[st], pol);
+        tma_load_1d(sm.gate[st], s.F + s.gate_base + leaf * kL, kL * 4, &sm.full[st], pol);
+    };
+    if (tid == 0)
+        for (uint64_t i = 0; i < nl && i < kProlStages; ++i) issue(i);
+    // ancestor gather operands of leaf i -> registers (side 0: coupled_row where the leaf is in
+    // the tile's row half; side 1: coupled_col where it is in the column half)
+    const int side = tid >> 5, j = tid & 31;
+    float t[kMaxDepth];
+    auto gather_load = [&](uint64_t leaf) {
         const float* src = side ? s.ccol : s.crow;
-        double acc = 0.0;
-        for (uint64_t d0 = 0; d0 < D; d0 += 8) {
-            float t[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const uint64_t d = d0 + q;
-                t[q] = 0.f;
-                if (d < D && ((leaf >> (D - 1 - d)) & 1ULL) == uint64_t(side))
-                    t[q] = __ldcg(&src[(((K + leaf) >> (D - d)) - 1) * kLs + j]);
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const uint64_t d = d0 + q;
-                if (d < D && ((leaf >> (D - 1 - d)) & 1ULL) == uint64_t(side)) acc += double(t[q]);
-            }
+        for (int d = 0; d < kMaxDepth; ++d) {
+            t[d] = 0.f;
+            if (uint64_t(d) < D && ((leaf >> (D - 1 - d)) & 1ULL) == uint64_t(side))
+                t[d] = __ldcg(&src[(((K + leaf) >> (D - d)) - 1) * kLs + j]);
         }
-        g[side][j] = float(acc);
-    }
-    __syncthreads();
-    {   // Ũ_k g_r and Ṽ_k g_c, f64 accumulation; 8 lanes per row
-        const float4 gr = reinterpret_cast<const float4*>(g[0])[l8];
-        const float4 gc = reinterpret_cast<const float4*>(g[1])[l8];
-#pragma unroll
-        for (int ps = 0; ps < 4; ++ps) {
-            double au = fma(double(u4[ps].w), double(gr.w), fma(double(u4[ps].z), double(gr.z),
-                        fma(double(u4[ps].y), double(gr.y), double(u4[ps].x) * double(gr.x))));
-            double av = fma(double(v4[ps].w), double(gc.w), fma(double(v4[ps].z), double(gc.z),
-                        fma(double(v4[ps].y), double(gc.y), double(v4[ps].x) * double(gc.x))));
-            au += __shfl_xor_sync(0xffffffffu, au, 4);
-            au += __shfl_xor_sync(0xffffffffu, au, 2);
-            au += __shfl_xor_sync(0xffffffffu, au, 1);
-            av += __shfl_xor_sync(0xffffffffu, av, 4);
-            av += __shfl_xor_sync(0xffffffffu, av, 2);
-            av += __shfl_xor_sync(0xffffffffu, av, 1);
-            if (l8 == 0) {
-                su[ps * 32 + rowi] = au;
-                sv[ps * 32 + rowi] = av;
-            }
-        }
-    }
-    __syncthreads();
+    };
+    if (tid < 2 * kLs && nl) gather_load(leaf_of(0));
     double rz = 0.0;
-    if (tid < kL) {
-        double y = yl;
-        y += su[tid];
-        y += sv[tid];
-        y += double(gate) * rv / ad + s.sc->shift * rv;  // apply.cpp:169-173
-        (mode == kApply ? zout : s.z)[i] = y;
-        rz = rv * y;
+    const int l8 = tid & 7, rowi = tid >> 3;
+    for (uint64_t i = 0; i < nl; ++i) {
+        const int st = int(i % kProlStages);
+        const uint64_t leaf = leaf_of(i);
+        if (tid < 2 * kLs) {  // f64 gather in tile order (root first), apply.cpp:140-154
+            double acc = 0.0;
+#pragma unroll
+            for (int d = 0; d < kMaxDepth; ++d)
+                if (uint64_t(d) < D && ((leaf >> (D - 1 - d)) & 1ULL) == uint64_t(side))
+                    acc += double(t[d]);
+            sm.g[side][j] = float(acc);
+            if (i + 1 < nl) gather_load(leaf_of(i + 1));
+        }
+        mbar_wait(&sm.full[st], uint32_t((i / kProlStages) & 1));
+        __syncthreads();
+        {   // Ũ_k g_r and Ṽ_k g_c (f64 accumulation), 8 lanes per 32-float row
+            const float4 gr = reinterpret_cast<const float4*>(sm.g[0])[l8];
+            const float4 gc = reinterpret_cast<const float4*>(sm.g[1])[l8];
+#pragma unroll
+            for (int ps = 0; ps < 4; ++ps) {
+                const int row = ps * 32 + rowi;
+                const float4 u4 = reinterpret_cast<const float4*>(&sm.B[st][row * kLs])[l8];
+                const float4 v4 = reinterpret_cast<const float4*>(&sm.B[st][kL * kLs + row * kLs])[l8];
+                double au = fma(double(u4.w), double(gr.w), fma(double(u4.z), double(gr.z),
+                            fma(double(u4.y), double(gr.y), double(u4.x) * double(gr.x))));
+                double av = fma(double(v4.w), double(gc.w), fma(double(v4.z), double(gc.z),
+                            fma(double(v4.y), double(gc.y), double(v4.x) * double(gc.x))));
+                au += __shfl_xor_sync(0xffffffffu, au, 4);
+                au += __shfl_xor_sync(0xffffffffu, au, 2);
+                au += __shfl_xor_sync(0xffffffffu, au, 1);
+                av += __shfl_xor_sync(0xffffffffu, av, 4);
+                av += __shfl_xor_sync(0xffffffffu, av, 2);
+                av += __shfl_xor_sync(0xffffffffu, av, 1);
+                if (l8 == 0) {
+                    sm.su[row] = au;
+                    sm.sv[row] = av;
+                }
+            }
+        }
+        __syncthreads();
+        if (tid < kL) {
+            const double rv = sm.vec[st][1][tid];
+            double y = sm.vec[st][0][tid];
+            y += sm.su[tid];
+            y += sm.sv[tid];
+            y += double(sm.gate[st][tid]) * rv / sm.vec[st][2][tid] + shift * rv;  // apply.cpp:169-173
+            zdst[leaf * kL + tid] = y;
+            rz = fma(rv, y, rz);
+        }
+        __syncthreads();  // stage st and g/su/sv are free again
+        if (tid == 0 && i + kProlStages < nl) issue(i + kProlStages);
     }
     if (mode == kApply) return;
     double v[1] = {rz}, tot[1];
