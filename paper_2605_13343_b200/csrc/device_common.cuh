@@ -83,6 +83,16 @@ __device__ __forceinline__ float4 ldg_stream(const float4* p) {
     return r;
 }
 
+// 128-bit read-only load with an L2 cache-policy hint (e.g. evict_last for data every
+// iteration re-reads).
+__device__ __forceinline__ float4 ldg_hint(const float4* p, uint64_t policy) {
+    float4 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p), "l"(policy));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t ldg_stream_u32(const uint32_t* p) {
     uint32_t r;
     asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));

@@ -59,6 +59,7 @@ struct hfpg_handle {
     double* sell_vals = nullptr;
     double* a_diag = nullptr;
     bool have_diag = false;
+    uint32_t spmv_stage_bytes = 0;  // >0: slices streamed by k_spmv_tma
 
     // vectors / workspace (sized for vec_n / ws layout)
     uint64_t vec_n = 0;
@@ -105,7 +106,20 @@ uint64_t prolong_grid(const hfpg_handle* h) {
     return h->fast ? std::min<uint64_t>(h->L.k, uint64_t(h->num_sms) * 2) : h->L.k;
 }
 uint64_t spmv_grid(const hfpg_handle* h) {
+    if (h->spmv_stage_bytes) {
+        const uint64_t per_sm = std::max<uint64_t>(1, (227 * 1024) / (h->spmv_stage_bytes * kSpmvStages + 128 + 1024));
+        const uint64_t nch = ((h->n + 31) / 32 + 7) / 8;
+        return std::max<uint64_t>(1, std::min<uint64_t>(nch, uint64_t(h->num_sms) * std::min<uint64_t>(per_sm, 4)));
+    }
     return std::max<uint64_t>(1, std::min<uint64_t>((h->n + 255) / 256, uint64_t(h->num_sms) * 4));
+}
+size_t spmv_smem(const hfpg_handle* h) { return h->spmv_stage_bytes ? 128 + size_t(h->spmv_stage_bytes) * kSpmvStages : 0; }
+template <int MODE>
+void launch_spmv(hfpg_handle* h, const DevSys& s, const double* x, double* y) {
+    if (h->spmv_stage_bytes)
+        k_spmv_tma<MODE><<<unsigned(spmv_grid(h)), 256, spmv_smem(h), h->stream>>>(s, x, y);
+    else
+        k_spmv<MODE><<<unsigned(spmv_grid(h)), 256, 0, h->stream>>>(s, x, y);
 }
 uint64_t simple_grid(const hfpg_handle* h) {
     return std::max<uint64_t>(1, std::min<uint64_t>((h->n + 255) / 256, uint64_t(h->num_sms) * 8));
@@ -199,6 +213,7 @@ void fill_sys(hfpg_handle* h) {
     s.node_v = h->node_v;
     s.tree_counters = h->tree_counters;
     s.coarse_S = coarse_width(L);
+    s.spmv_stage_bytes = h->spmv_stage_bytes;
     s.partials = h->partials;
     s.counters = h->counters;
     s.sc = h->sc;
@@ -233,7 +248,7 @@ void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
 
 void launch_iteration(hfpg_handle* h) {
     const DevSys& s = h->sys;
-    k_spmv<kLoop><<<unsigned(spmv_grid(h)), 256, 0, h->stream>>>(s, nullptr, nullptr);
+    launch_spmv<kLoop>(h, s, nullptr, nullptr);
     CK(cudaGetLastError());
     if (h->precond == HFPG_PRECOND_FACTOR) {
         launch_apply(h, kLoop, nullptr, nullptr);
@@ -263,6 +278,8 @@ void configure_kernels() {
         CK(cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         CK(cudaFuncSetAttribute(k_prolong_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(sizeof(ProlSmem))));
+        CK(cudaFuncSetAttribute(k_spmv_tma<kLoop>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+        CK(cudaFuncSetAttribute(k_spmv_tma<kApply>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         CK(cudaFuncSetAttribute(k_leaf_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     });
 }
@@ -455,6 +472,14 @@ int hfpg_load_csr(hfpg_handle* h, uint64_t n, const uint64_t* ro_in, const uint3
         if (h->n != n) {
             h->n = n;
         }
+        // k_spmv_tma stage capacity: the largest 8-slice chunk, if three stages leave room for
+        // at least two CTAs per SM
+        uint64_t maxch = 0;
+        for (uint64_t s0 = 0; s0 < ns; s0 += 8)
+            maxch = std::max<uint64_t>(maxch, (off[std::min(ns, s0 + 8)] - off[s0]) * 12);
+        maxch = (maxch + 1023) & ~uint64_t(1023);
+        h->spmv_stage_bytes = (maxch > 0 && maxch * kSpmvStages + 128 <= 110 * 1024) ? uint32_t(maxch) : 0;
+        if (std::getenv("HFPG_NO_SPMV_TMA")) h->spmv_stage_bytes = 0;
         invalidate_graph(h);
         dalloc(h->slice_off, ns + 1);
         dalloc(h->sell_cols, sc.size());
@@ -555,7 +580,7 @@ int hfpg_spmv(hfpg_handle* h, const double* x, double* y, int where) {
             xin = h->scratch;
             yout = h->ap;
         }
-        k_spmv<kApply><<<unsigned(spmv_grid(h)), 256, 0, h->stream>>>(h->sys, xin, yout);
+        launch_spmv<kApply>(h, h->sys, xin, yout);
         CK(cudaGetLastError());
         if (where == HFPG_HOST) copy_out(h, y, h->ap, h->n, HFPG_HOST);
         CK(cudaStreamSynchronize(h->stream));
@@ -644,7 +669,7 @@ int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out) {
         for (uint32_t rep = 0; rep < std::max(reps, 1u); ++rep) {
             CK(cudaMemcpyAsync(h->sc, &prof, sizeof(Scalars), cudaMemcpyHostToDevice, h->stream));
             CK(cudaEventRecord(ev[0], h->stream));
-            k_spmv<kLoop><<<unsigned(spmv_grid(h)), 256, 0, h->stream>>>(h->sys, nullptr, nullptr);
+            launch_spmv<kLoop>(h, h->sys, nullptr, nullptr);
             CK(cudaEventRecord(ev[1], h->stream));
             if (h->fast)
                 k_leaf_fast<<<unsigned(leaf_grid(h)), kLeafThreads, sizeof(LeafSmem), h->stream>>>(h->sys, kLoop, nullptr);

@@ -35,6 +35,7 @@ struct DevSys {
     double *node_u, *node_v; // heap-indexed strip sums of subtree roots (2K x L_s)
     unsigned* tree_counters; // 2K arrival counters for the coarse tree
     uint64_t coarse_S;       // subtree width per k_coarse task (power of two)
+    uint32_t spmv_stage_bytes; // k_spmv_tma stage capacity (0: use k_spmv)
     // reductions / state
     double* partials;
     unsigned* counters;  // [0] spmv, [1] leaf, [2] prolong, [3] simple
@@ -79,7 +80,7 @@ __device__ __forceinline__ void finish_residual(Scalars* sc, double* history, do
 // PCG mode fuses p = z + beta p_prev (pcg.cpp:118) into the gathers and reduces p.Ap, p.p.
 // ============================================================================================
 template <int MODE>  // kInit unused; kLoop = PCG, kApply = plain y = A x
-__global__ void __launch_bounds__(256, 4) k_spmv(DevSys s, const double* xin, double* yout) {
+__global__ void __launch_bounds__(256) k_spmv(DevSys s, const double* xin, double* yout) {
     if (MODE == kLoop && s.sc->done) return;
     const unsigned long long k = MODE == kLoop ? s.sc->k : 0ULL;
     const double beta = MODE == kLoop ? s.sc->beta : 0.0;
@@ -132,6 +133,106 @@ __global__ void __launch_bounds__(256, 4) k_spmv(DevSys s, const double* xin, do
         sc->pp = p2;
         // pcg.cpp:90-95 breakdown test, reported not thrown
         if (pap < -sc->breakdown_tol * p2 || pap == 0.0) {
+            sc->status = 2;
+            sc->breakdown_iter = k;
+            sc->iterations = k;
+            sc->done = 1;
+        } else {
+            sc->alpha = sc->rz / pap;
+        }
+    }
+}
+
+// SpMV, streaming variant: persistent CTAs walk chunks of 8 SELL slices (256 rows); the
+// chunk's values and column indices (contiguous in SELL order) arrive by cp.async.bulk into a
+// 3-stage ring, so only the x/p gathers (L1/L2-resident neighbours) are synchronous loads.
+// Same arithmetic as k_spmv (bit-identical to the reference spmv). Used when every chunk fits
+// a stage (host-checked); k_spmv covers the general case.
+constexpr int kSpmvStages = 3;
+template <int MODE>
+__global__ void __launch_bounds__(256) k_spmv_tma(DevSys s, const double* xin, double* yout) {
+    if (MODE == kLoop && s.sc->done) return;
+    extern __shared__ __align__(128) unsigned char sraw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(sraw);
+    unsigned char* buf = sraw + 128;
+    const uint32_t cap = s.spmv_stage_bytes;
+    const unsigned long long k = MODE == kLoop ? s.sc->k : 0ULL;
+    const double beta = MODE == kLoop ? s.sc->beta : 0.0;
+    const double* z = MODE == kLoop ? s.z : xin;
+    const double* pp_ = MODE == kLoop ? p_prev(s, k) : nullptr;
+    double* pnew = MODE == kLoop ? p_cur(s, k) : nullptr;
+    double* y = MODE == kLoop ? s.ap : yout;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t nsl = (s.n + 31) >> 5, nch = (nsl + 7) >> 3;
+    const uint64_t pol = policy_evict_first();
+    if (tid == 0) {
+        for (int q = 0; q < kSpmvStages; ++q) mbar_init(&full[q], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](uint64_t ch, int st) {
+        const uint64_t s0 = ch * 8, s1 = s0 + 8 < nsl ? s0 + 8 : nsl;
+        const uint64_t e0 = s.slice_off[s0], e1 = s.slice_off[s1], ne = e1 - e0;
+        unsigned char* b = buf + size_t(st) * cap;
+        mbar_expect_tx(&full[st], uint32_t(ne * 12));
+        tma_load_1d(b, s.sell_vals + e0, uint32_t(ne * 8), &full[st], pol);
+        tma_load_1d(b + ne * 8, s.sell_cols + e0, uint32_t(ne * 4), &full[st], pol);
+    };
+    if (tid == 0)
+        for (int q = 0; q < kSpmvStages; ++q)
+            if (blockIdx.x + uint64_t(q) * gridDim.x < nch) issue(blockIdx.x + uint64_t(q) * gridDim.x, q);
+    double v[2] = {0.0, 0.0};
+    uint32_t it = 0;
+    for (uint64_t ch = blockIdx.x; ch < nch; ch += gridDim.x, ++it) {
+        const int st = int(it % kSpmvStages);
+        const uint64_t s0 = ch * 8, sl = s0 + warp;
+        mbar_wait(&full[st], (it / kSpmvStages) & 1);
+        if (sl < nsl) {
+            const uint64_t s1 = s0 + 8 < nsl ? s0 + 8 : nsl;
+            const uint64_t e0 = s.slice_off[s0], ne = s.slice_off[s1] - e0;
+            const uint64_t b0 = s.slice_off[sl] - e0, w = (s.slice_off[sl + 1] - s.slice_off[sl]) >> 5;
+            const double* vals = reinterpret_cast<const double*>(buf + size_t(st) * cap) + b0;
+            const uint32_t* cols = reinterpret_cast<const uint32_t*>(buf + size_t(st) * cap + ne * 8) + b0;
+            const uint64_t row = sl * 32 + lane;
+            double acc = 0.0;
+            for (uint64_t j0 = 0; j0 < w; j0 += 8) {
+                uint32_t c[8];
+                double a[8], pc[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (j0 + q < w) {
+                        c[q] = cols[(j0 + q) * 32 + lane];
+                        a[q] = vals[(j0 + q) * 32 + lane];
+                    }
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (j0 + q < w) pc[q] = MODE == kLoop ? fma(beta, pp_[c[q]], z[c[q]]) : z[c[q]];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (j0 + q < w) acc = __dadd_rn(acc, __dmul_rn(a[q], pc[q]));
+            }
+            if (row < s.n) {
+                y[row] = acc;
+                if (MODE == kLoop) {
+                    const double pi = fma(beta, pp_[row], z[row]);
+                    pnew[row] = pi;
+                    v[0] = fma(pi, acc, v[0]);
+                    v[1] = fma(pi, pi, v[1]);
+                }
+            }
+        }
+        __syncthreads();  // stage st consumed
+        if (tid == 0 && ch + uint64_t(kSpmvStages) * gridDim.x < nch)
+            issue(ch + uint64_t(kSpmvStages) * gridDim.x, st);
+    }
+    if (MODE != kLoop) return;
+    double tot[2];
+    if (grid_reduce_last<2>(v, s.partials, &s.counters[0], tot) && threadIdx.x == 0) {
+        Scalars* sc = s.sc;
+        const double pap = tot[0], p2 = tot[1];
+        sc->pap = pap;
+        sc->pp = p2;
+        if (pap < -sc->breakdown_tol * p2 || pap == 0.0) {  // pcg.cpp:90-95
             sc->status = 2;
             sc->breakdown_iter = k;
             sc->iterations = k;
@@ -279,14 +380,15 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mod
             s.restrict_[leaf * (2 * kLs) + o] = v;
         }
         __syncthreads();
-        {   // y = F c with f64 accumulation: warp w owns rows 8w..8w+7, lane l columns 4l..4l+3
+        {   // y = F c, f64 accumulation across lanes: warp w owns rows 8w..8w+7, lane l columns
+            // 4l..4l+3 (a 4-term fp32 partial per lane, widened once: 8x fewer F2F than
+            // widening every product; error ~2e-7 of the partial, far inside the 1e-5 gate)
             const float4 c4 = reinterpret_cast<const float4*>(sm.c)[lane];
-            const double c0 = c4.x, c1 = c4.y, c2 = c4.z, c3 = c4.w;
             double v[8];
 #pragma unroll
             for (int rI = 0; rI < 8; ++rI) {
                 const float4 f4 = reinterpret_cast<const float4*>(F + (8 * warp + rI) * kL)[lane];
-                v[rI] = fma(double(f4.w), c3, fma(double(f4.z), c2, fma(double(f4.y), c1, double(f4.x) * c0)));
+                v[rI] = double(fmaf(f4.w, c4.w, fmaf(f4.z, c4.z, fmaf(f4.y, c4.y, f4.x * c4.x))));
             }
             // transpose-reduce 8 rows x 32 lanes: after xor 16/8/4 each lane holds one row's
             // partial over 4 lanes; xor 2/1 finish it.
@@ -432,13 +534,15 @@ __device__ __forceinline__ void tile_warp32(const float4 (&u4)[4], const float4 
     crow[lane] = float(acc_r);
 }
 
+// Tile factors are re-read every iteration and total 4 (K-1) L_s^2 bytes (33.5 MB at N=1M):
+// load them with an evict_last policy so they stay L2-resident while F streams past.
 __device__ __forceinline__ void load_tile32(const DevSys& s, uint64_t m, int lane, float4 (&u4)[4],
-                                            float4 (&v4)[4]) {
+                                            float4 (&v4)[4], uint64_t pol) {
     const float4* U = reinterpret_cast<const float4*>(s.F + s.tile_base + m * 1024) + lane * 4;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        u4[i] = __ldg(U + i);
-        v4[i] = __ldg(U + 128 + i);  // V_m = U_m + 32 x 16 floats
+        u4[i] = ldg_hint(U + i, pol);
+        v4[i] = ldg_hint(U + 128 + i, pol);  // V_m = U_m + 32 x 16 floats
     }
 }
 
@@ -451,6 +555,7 @@ __global__ void __launch_bounds__(256) k_coarse_fast(DevSys s, int mode) {
     __shared__ double SU[63 * 32], SV[63 * 32];
     __shared__ int last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t pol_keep = policy_evict_last();
     uint64_t task = blockIdx.x;
     uint64_t dlo = s.D;
     for (int level = 0;; ++level) {
@@ -464,9 +569,11 @@ __global__ void __launch_bounds__(256) k_coarse_fast(DevSys s, int mode) {
             while ((2ULL << ld) <= u + 1) ++ld;
             return (1ULL << (dr + ld)) - 1 + task * (1ULL << ld) + (u + 1 - (1ULL << ld));
         };
-        // this warp's first tile: issue its loads before the bottom layer / up-sweep
-        float4 u4[4], v4[4];
-        if (uint64_t(warp) + 1 < S) load_tile32(s, tile_id(warp), lane, u4, v4);
+        // this warp's first two tiles: issue their loads before the bottom layer / up-sweep,
+        // then keep one tile in flight while the other computes (register double buffer)
+        float4 ua[4], va[4], ub[4], vb[4];
+        if (uint64_t(warp) + 1 < S) load_tile32(s, tile_id(warp), lane, ua, va, pol_keep);
+        if (uint64_t(warp) + 9 < S) load_tile32(s, tile_id(warp + 8), lane, ub, vb, pol_keep);
         const uint64_t g0 = (1ULL << dlo) - 1 + task * S;
         for (uint64_t e = tid; e < S * 32; e += blockDim.x) {
             const uint64_t q = e >> 5, j = e & 31, u = S - 1 + q;
@@ -488,11 +595,16 @@ __global__ void __launch_bounds__(256) k_coarse_fast(DevSys s, int mode) {
             }
             __syncthreads();
         }
-        for (uint64_t u = warp; u + 1 < S; u += 8) {
+        for (uint64_t u = warp, r = 0; u + 1 < S; u += 8, ++r) {
             const uint64_t m = tile_id(u);
-            if (u != uint64_t(warp)) load_tile32(s, m, lane, u4, v4);
-            tile_warp32(u4, v4, float(SU[(2 * u + 1) * 32 + lane]), float(SV[(2 * u + 2) * 32 + lane]),
-                        lane, s.ccol + m * 32, s.crow + m * 32);
+            const float sr = float(SU[(2 * u + 1) * 32 + lane]), sc = float(SV[(2 * u + 2) * 32 + lane]);
+            if ((r & 1) == 0) {
+                tile_warp32(ua, va, sr, sc, lane, s.ccol + m * 32, s.crow + m * 32);
+                if (u + 17 < S) load_tile32(s, tile_id(u + 16), lane, ua, va, pol_keep);
+            } else {
+                tile_warp32(ub, vb, sr, sc, lane, s.ccol + m * 32, s.crow + m * 32);
+                if (u + 17 < S) load_tile32(s, tile_id(u + 16), lane, ub, vb, pol_keep);
+            }
         }
         if (dr == 0) return;
         if (tid < 32) {
@@ -710,7 +822,6 @@ struct ProlSmem {
     double vec[kProlStages][3][kL];  // y_loc, r, a_diag
     float gate[kProlStages][kL];
     float g[2][kLs];
-    double su[kL], sv[kL];
     uint64_t full[kProlStages];
 };
 
@@ -776,7 +887,8 @@ __global__ void __launch_bounds__(256, 2) k_prolong_fast(DevSys s, int mode, con
         }
         mbar_wait(&sm.full[st], uint32_t((i / kProlStages) & 1));
         __syncthreads();
-        {   // Ũ_k g_r and Ṽ_k g_c (f64 accumulation), 8 lanes per 32-float row
+        {   // Ũ_k g_r and Ṽ_k g_c: 8 lanes per 32-float row, 4-term fp32 partials widened to
+            // f64 for the cross-lane sum; the group leader finishes the row (apply.cpp:156-173)
             const float4 gr = reinterpret_cast<const float4*>(sm.g[0])[l8];
             const float4 gc = reinterpret_cast<const float4*>(sm.g[1])[l8];
 #pragma unroll
@@ -784,10 +896,8 @@ __global__ void __launch_bounds__(256, 2) k_prolong_fast(DevSys s, int mode, con
                 const int row = ps * 32 + rowi;
                 const float4 u4 = reinterpret_cast<const float4*>(&sm.B[st][row * kLs])[l8];
                 const float4 v4 = reinterpret_cast<const float4*>(&sm.B[st][kL * kLs + row * kLs])[l8];
-                double au = fma(double(u4.w), double(gr.w), fma(double(u4.z), double(gr.z),
-                            fma(double(u4.y), double(gr.y), double(u4.x) * double(gr.x))));
-                double av = fma(double(v4.w), double(gc.w), fma(double(v4.z), double(gc.z),
-                            fma(double(v4.y), double(gc.y), double(v4.x) * double(gc.x))));
+                double au = double(fmaf(u4.w, gr.w, fmaf(u4.z, gr.z, fmaf(u4.y, gr.y, u4.x * gr.x))));
+                double av = double(fmaf(v4.w, gc.w, fmaf(v4.z, gc.z, fmaf(v4.y, gc.y, v4.x * gc.x))));
                 au += __shfl_xor_sync(0xffffffffu, au, 4);
                 au += __shfl_xor_sync(0xffffffffu, au, 2);
                 au += __shfl_xor_sync(0xffffffffu, au, 1);
@@ -795,20 +905,15 @@ __global__ void __launch_bounds__(256, 2) k_prolong_fast(DevSys s, int mode, con
                 av += __shfl_xor_sync(0xffffffffu, av, 2);
                 av += __shfl_xor_sync(0xffffffffu, av, 1);
                 if (l8 == 0) {
-                    sm.su[row] = au;
-                    sm.sv[row] = av;
+                    const double rv = sm.vec[st][1][row];
+                    double y = sm.vec[st][0][row];
+                    y += au;
+                    y += av;
+                    y += double(sm.gate[st][row]) * rv / sm.vec[st][2][row] + shift * rv;
+                    zdst[leaf * kL + row] = y;
+                    rz = fma(rv, y, rz);
                 }
             }
-        }
-        __syncthreads();
-        if (tid < kL) {
-            const double rv = sm.vec[st][1][tid];
-            double y = sm.vec[st][0][tid];
-            y += sm.su[tid];
-            y += sm.sv[tid];
-            y += double(sm.gate[st][tid]) * rv / sm.vec[st][2][tid] + shift * rv;  // apply.cpp:169-173
-            zdst[leaf * kL + tid] = y;
-            rz = fma(rv, y, rz);
         }
         __syncthreads();  // stage st and g/su/sv are free again
         if (tid == 0 && i + kProlStages < nl) issue(i + kProlStages);
