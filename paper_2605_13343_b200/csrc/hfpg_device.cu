@@ -233,7 +233,7 @@ void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
     }
     CK(cudaGetLastError());
     if (h->fast) {
-        k_coarse_fast<<<unsigned(L.k / std::min<uint64_t>(L.k, 32)), 256, 0, h->stream>>>(s, mode);
+        k_coarse_fast<<<unsigned(L.k / std::min<uint64_t>(L.k, 32)), 256, kCoarseFastSmem, h->stream>>>(s, mode);
     } else {
         const uint64_t S0 = std::min<uint64_t>(L.k, coarse_width(L));
         k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(s, mode);
@@ -278,6 +278,7 @@ void configure_kernels() {
         CK(cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         CK(cudaFuncSetAttribute(k_prolong_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(sizeof(ProlSmem))));
+        CK(cudaFuncSetAttribute(k_coarse_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCoarseFastSmem)));
         CK(cudaFuncSetAttribute(k_spmv_tma<kLoop>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         CK(cudaFuncSetAttribute(k_spmv_tma<kApply>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         CK(cudaFuncSetAttribute(k_leaf_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
@@ -677,7 +678,7 @@ int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out) {
                 k_leaf_generic<<<unsigned(L.k), 256, 2 * L.l * sizeof(float), h->stream>>>(h->sys, kLoop, nullptr);
             CK(cudaEventRecord(ev[2], h->stream));
             if (h->fast)
-                k_coarse_fast<<<unsigned(L.k / std::min<uint64_t>(L.k, 32)), 256, 0, h->stream>>>(h->sys, kLoop);
+                k_coarse_fast<<<unsigned(L.k / std::min<uint64_t>(L.k, 32)), 256, kCoarseFastSmem, h->stream>>>(h->sys, kLoop);
             else
                 k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(h->sys, kLoop);
             CK(cudaEventRecord(ev[3], h->stream));

@@ -283,8 +283,6 @@ struct LeafSmem {
     float B[2][2 * kL * kLs];
     double vec[2][4][kL];  // r_k, Ap_k, p_k, x_k of the staged leaf (the fused PCG update)
     float rin[kL];
-    float cpart[4][kL];
-    float rpart[8][2 * kLs];
     float c[kL];
     uint64_t full[2];
 };
@@ -354,41 +352,35 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mod
         __syncthreads();
         const float* F = sm.F[st];
         const float* B = sm.B[st];
-        {   // c partials: column j, rows 32g..32g+31 (fp32, i ascending like matvec_t)
-            const int j = tid & (kL - 1), g = tid >> 7;
-            float acc = 0.f;
-#pragma unroll 8
-            for (int ii = 0; ii < 32; ++ii) acc = fmaf(F[(32 * g + ii) * kL + j], sm.rin[32 * g + ii], acc);
-            sm.cpart[g][j] = acc;
-        }
-        {   // restriction partials: output o (û | v̂), rows 16g..16g+15
-            const int o = tid & 63, g = tid >> 6;
-            const float* Bo = B + (o >> 5) * (kL * kLs) + (o & 31);
-            float acc = 0.f;
-#pragma unroll 8
-            for (int ii = 0; ii < 16; ++ii) acc = fmaf(Bo[(16 * g + ii) * kLs], sm.rin[16 * g + ii], acc);
-            sm.rpart[g][o] = acc;
-        }
-        __syncthreads();
+        // c = F^T r and the restrictions Ũ^T r, Ṽ^T r: one thread per output, a sequential
+        // fp32 FMA chain over the 128 rows — the exact operation order of the reference's
+        // vectorised matvec_t (apply.cpp:25-35), so c and û, v̂ are bit-identical to it.
         if (tid < kL) {
-            sm.c[tid] = ((sm.cpart[0][tid] + sm.cpart[1][tid]) + sm.cpart[2][tid]) + sm.cpart[3][tid];
+            const int j = tid;
+            float acc = 0.f;
+#pragma unroll 16
+            for (int i = 0; i < kL; ++i) acc = fmaf(F[i * kL + j], sm.rin[i], acc);
+            sm.c[j] = acc;
         } else if (tid < kL + 2 * kLs) {
             const int o = tid - kL;
-            float v = sm.rpart[0][o];
-#pragma unroll
-            for (int g = 1; g < 8; ++g) v += sm.rpart[g][o];
-            s.restrict_[leaf * (2 * kLs) + o] = v;
+            const float* Bo = B + (o >> 5) * (kL * kLs) + (o & 31);
+            float acc = 0.f;
+#pragma unroll 16
+            for (int i = 0; i < kL; ++i) acc = fmaf(Bo[i * kLs], sm.rin[i], acc);
+            s.restrict_[leaf * (2 * kLs) + o] = acc;
         }
         __syncthreads();
-        {   // y = F c, f64 accumulation across lanes: warp w owns rows 8w..8w+7, lane l columns
-            // 4l..4l+3 (a 4-term fp32 partial per lane, widened once: 8x fewer F2F than
-            // widening every product; error ~2e-7 of the partial, far inside the 1e-5 gate)
+        {   // y = F c: products of two floats are exact in f64 and the reference accumulates
+            // them in f64 (matvec_add_double, apply.cpp:39-50); warp w owns rows 8w..8w+7, lane
+            // l columns 4l..4l+3, then a transpose-reduce across lanes (order differs only at
+            // the f64 rounding level)
             const float4 c4 = reinterpret_cast<const float4*>(sm.c)[lane];
+            const double c0 = c4.x, c1 = c4.y, c2 = c4.z, c3 = c4.w;
             double v[8];
 #pragma unroll
             for (int rI = 0; rI < 8; ++rI) {
                 const float4 f4 = reinterpret_cast<const float4*>(F + (8 * warp + rI) * kL)[lane];
-                v[rI] = double(fmaf(f4.w, c4.w, fmaf(f4.z, c4.z, fmaf(f4.y, c4.y, f4.x * c4.x))));
+                v[rI] = fma(double(f4.w), c3, fma(double(f4.z), c2, fma(double(f4.y), c1, double(f4.x) * c0)));
             }
             // transpose-reduce 8 rows x 32 lanes: after xor 16/8/4 each lane holds one row's
             // partial over 4 lanes; xor 2/1 finish it.
@@ -502,36 +494,44 @@ __device__ __forceinline__ float transpose_reduce16(const float (&a)[16], int la
     return t1 + __shfl_xor_sync(0xffffffffu, t1, 1);
 }
 
-// One tile (L_s = 32, rank 16) per warp, operands in registers: lane p holds row p of U_m and
-// V_m. coupled_col = V (U^T float(s_r)), coupled_row = U (V^T float(s_c)): the U^T / V^T
-// products accumulate in fp32 (as matvec_t), the V c / U c' products in f64 then round to
-// float (as matvec), apply.cpp:125-137.
+// One tile (L_s = 32, rank 16) per warp. Lane p holds row p of U_m and V_m (registers) and
+// stages them in the warp's shared scratch; lanes q < 16 then run the fp32 chain
+// coef_r[q] = sum_p U[p][q] float(s_r[p]) and lanes 16 + q the chain for V^T float(s_c), in
+// p order exactly like matvec_t; lane j finishes coupled_col[j] = float(sum_q V[j][q] coef_r[q])
+// and coupled_row[j] = float(sum_q U[j][q] coef_c[q]) in f64 like matvec (apply.cpp:125-137).
 __device__ __forceinline__ void tile_warp32(const float4 (&u4)[4], const float4 (&v4)[4],
-                                            float sr, float sc, int lane, float* ccol,
-                                            float* crow) {
-    float u[16], v[16], a[16], b[16];
+                                            const double* sr, const double* sc, int lane,
+                                            float* scratch, float* ccol, float* crow) {
+    float4* T4 = reinterpret_cast<float4*>(scratch);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        u[4 * i] = u4[i].x; u[4 * i + 1] = u4[i].y; u[4 * i + 2] = u4[i].z; u[4 * i + 3] = u4[i].w;
-        v[4 * i] = v4[i].x; v[4 * i + 1] = v4[i].y; v[4 * i + 2] = v4[i].z; v[4 * i + 3] = v4[i].w;
+        T4[lane * 4 + i] = u4[i];
+        T4[128 + lane * 4 + i] = v4[i];
     }
+    __syncwarp();
+    const int q = lane & 15;
+    const float* col = scratch + (lane < 16 ? 0 : 512) + q;
+    const double* st = lane < 16 ? sr : sc;
+    float coef = 0.f;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        a[q] = u[q] * sr;
-        b[q] = v[q] * sc;
-    }
-    const float coef_r = transpose_reduce16(a, lane);  // (U^T s_r)[lane >> 1]
-    const float coef_c = transpose_reduce16(b, lane);  // (V^T s_c)[lane >> 1]
+    for (int p = 0; p < 32; ++p) coef = fmaf(col[p * 16], float(st[p]), coef);
     double acc_c = 0.0, acc_r = 0.0;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        const float cr = __shfl_sync(0xffffffffu, coef_r, 2 * q);
-        const float cc = __shfl_sync(0xffffffffu, coef_c, 2 * q);
-        acc_c = fma(double(v[q]), double(cr), acc_c);
-        acc_r = fma(double(u[q]), double(cc), acc_r);
+    for (int i = 0; i < 4; ++i) {
+        const float uu[4] = {u4[i].x, u4[i].y, u4[i].z, u4[i].w};
+        const float vv[4] = {v4[i].x, v4[i].y, v4[i].z, v4[i].w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int qq = 4 * i + t;
+            const float cr = __shfl_sync(0xffffffffu, coef, qq);       // (U^T s_r)[qq]
+            const float cc = __shfl_sync(0xffffffffu, coef, 16 + qq);  // (V^T s_c)[qq]
+            acc_c += double(vv[t]) * double(cr);
+            acc_r += double(uu[t]) * double(cc);
+        }
     }
     ccol[lane] = float(acc_c);
     crow[lane] = float(acc_r);
+    __syncwarp();
 }
 
 // Tile factors are re-read every iteration and total 4 (K-1) L_s^2 bytes (33.5 MB at N=1M):
@@ -546,13 +546,18 @@ __device__ __forceinline__ void load_tile32(const DevSys& s, uint64_t m, int lan
     }
 }
 
+constexpr size_t kCoarseFastSmem = 2 * 63 * 32 * sizeof(double) + 8 * 1024 * sizeof(float);
+
 // Coarse stage, fast path (L_s = 32): the bisection tree in heap order; each CTA owns an
 // aligned subtree of up to 32 bottom nodes, runs the f64 up-sweep in shared memory, computes
 // its internal tiles a warp each, publishes the root sums, and the last CTA of each group of
 // 32 siblings continues one level up (no grid barrier, one launch for the whole tree).
 __global__ void __launch_bounds__(256) k_coarse_fast(DevSys s, int mode) {
     if (mode != kApply && s.sc->done) return;
-    __shared__ double SU[63 * 32], SV[63 * 32];
+    extern __shared__ __align__(128) unsigned char cfraw[];
+    double* SU = reinterpret_cast<double*>(cfraw);                 // 63 x 32
+    double* SV = SU + 63 * 32;                                      // 63 x 32
+    float (*scratch)[1024] = reinterpret_cast<float (*)[1024]>(SV + 63 * 32);  // per warp
     __shared__ int last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t pol_keep = policy_evict_last();
@@ -575,14 +580,28 @@ __global__ void __launch_bounds__(256) k_coarse_fast(DevSys s, int mode) {
         if (uint64_t(warp) + 1 < S) load_tile32(s, tile_id(warp), lane, ua, va, pol_keep);
         if (uint64_t(warp) + 9 < S) load_tile32(s, tile_id(warp + 8), lane, ub, vb, pol_keep);
         const uint64_t g0 = (1ULL << dlo) - 1 + task * S;
-        for (uint64_t e = tid; e < S * 32; e += blockDim.x) {
-            const uint64_t q = e >> 5, j = e & 31, u = S - 1 + q;
-            if (level == 0) {
-                SU[u * 32 + j] = double(__ldcg(&s.restrict_[(task * S + q) * 64 + j]));
-                SV[u * 32 + j] = double(__ldcg(&s.restrict_[(task * S + q) * 64 + 32 + j]));
-            } else {
-                SU[u * 32 + j] = __ldcg(&s.node_u[(g0 + q) * 32 + j]);
-                SV[u * 32 + j] = __ldcg(&s.node_v[(g0 + q) * 32 + j]);
+        {   // bottom layer: up to 4 + 4 values per thread, all loads issued before any store
+            double bu[4], bv[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint64_t e = uint64_t(tid) + 256u * t, q = e >> 5, j = e & 31;
+                if (e < S * 32) {
+                    if (level == 0) {
+                        bu[t] = double(__ldcg(&s.restrict_[(task * S + q) * 64 + j]));
+                        bv[t] = double(__ldcg(&s.restrict_[(task * S + q) * 64 + 32 + j]));
+                    } else {
+                        bu[t] = __ldcg(&s.node_u[(g0 + q) * 32 + j]);
+                        bv[t] = __ldcg(&s.node_v[(g0 + q) * 32 + j]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint64_t e = uint64_t(tid) + 256u * t;
+                if (e < S * 32) {
+                    SU[(S - 1) * 32 + e] = bu[t];
+                    SV[(S - 1) * 32 + e] = bv[t];
+                }
             }
         }
         __syncthreads();
@@ -597,24 +616,25 @@ __global__ void __launch_bounds__(256) k_coarse_fast(DevSys s, int mode) {
         }
         for (uint64_t u = warp, r = 0; u + 1 < S; u += 8, ++r) {
             const uint64_t m = tile_id(u);
-            const float sr = float(SU[(2 * u + 1) * 32 + lane]), sc = float(SV[(2 * u + 2) * 32 + lane]);
+            const double* sr = SU + (2 * u + 1) * 32;
+            const double* sc = SV + (2 * u + 2) * 32;
             if ((r & 1) == 0) {
-                tile_warp32(ua, va, sr, sc, lane, s.ccol + m * 32, s.crow + m * 32);
+                tile_warp32(ua, va, sr, sc, lane, scratch[warp], s.ccol + m * 32, s.crow + m * 32);
                 if (u + 17 < S) load_tile32(s, tile_id(u + 16), lane, ua, va, pol_keep);
             } else {
-                tile_warp32(ub, vb, sr, sc, lane, s.ccol + m * 32, s.crow + m * 32);
+                tile_warp32(ub, vb, sr, sc, lane, scratch[warp], s.ccol + m * 32, s.crow + m * 32);
                 if (u + 17 < S) load_tile32(s, tile_id(u + 16), lane, ub, vb, pol_keep);
             }
         }
         if (dr == 0) return;
-        if (tid < 32) {
+        const uint64_t cnt2 = 1ULL << dr;
+        const uint64_t S2 = cnt2 < 32 ? cnt2 : 32;
+        if (tid < 32) {  // publish the root sums (only these must be visible to the next level)
             const uint64_t g = (1ULL << dr) - 1 + task;
             s.node_u[g * 32 + tid] = SU[tid];
             s.node_v[g * 32 + tid] = SV[tid];
+            __threadfence();
         }
-        const uint64_t cnt2 = 1ULL << dr;
-        const uint64_t S2 = cnt2 < 32 ? cnt2 : 32;
-        __threadfence();
         __syncthreads();
         if (tid == 0) {
             int logS2 = 0;
@@ -887,24 +907,28 @@ __global__ void __launch_bounds__(256, 2) k_prolong_fast(DevSys s, int mode, con
         }
         mbar_wait(&sm.full[st], uint32_t((i / kProlStages) & 1));
         __syncthreads();
-        {   // Ũ_k g_r and Ṽ_k g_c: 8 lanes per 32-float row, 4-term fp32 partials widened to
-            // f64 for the cross-lane sum; the group leader finishes the row (apply.cpp:156-173)
+        {   // Ũ_k g_r and Ṽ_k g_c: 8 lanes per 32-float row, exact f64 products, f64 sums
+            // (matvec_add_double, apply.cpp:156-166); after the xor-reduce every lane of the
+            // group holds the row sums, so lane l8 = ps finishes the row of pass ps (one f64
+            // division per lane instead of four on one lane)
             const float4 gr = reinterpret_cast<const float4*>(sm.g[0])[l8];
             const float4 gc = reinterpret_cast<const float4*>(sm.g[1])[l8];
+            const double g0 = gr.x, g1 = gr.y, g2 = gr.z, g3 = gr.w;
+            const double h0 = gc.x, h1 = gc.y, h2 = gc.z, h3 = gc.w;
 #pragma unroll
             for (int ps = 0; ps < 4; ++ps) {
                 const int row = ps * 32 + rowi;
                 const float4 u4 = reinterpret_cast<const float4*>(&sm.B[st][row * kLs])[l8];
                 const float4 v4 = reinterpret_cast<const float4*>(&sm.B[st][kL * kLs + row * kLs])[l8];
-                double au = double(fmaf(u4.w, gr.w, fmaf(u4.z, gr.z, fmaf(u4.y, gr.y, u4.x * gr.x))));
-                double av = double(fmaf(v4.w, gc.w, fmaf(v4.z, gc.z, fmaf(v4.y, gc.y, v4.x * gc.x))));
+                double au = fma(double(u4.w), g3, fma(double(u4.z), g2, fma(double(u4.y), g1, double(u4.x) * g0)));
+                double av = fma(double(v4.w), h3, fma(double(v4.z), h2, fma(double(v4.y), h1, double(v4.x) * h0)));
                 au += __shfl_xor_sync(0xffffffffu, au, 4);
                 au += __shfl_xor_sync(0xffffffffu, au, 2);
                 au += __shfl_xor_sync(0xffffffffu, au, 1);
                 av += __shfl_xor_sync(0xffffffffu, av, 4);
                 av += __shfl_xor_sync(0xffffffffu, av, 2);
                 av += __shfl_xor_sync(0xffffffffu, av, 1);
-                if (l8 == 0) {
+                if (l8 == ps) {
                     const double rv = sm.vec[st][1][row];
                     double y = sm.vec[st][0][row];
                     y += au;

@@ -135,3 +135,19 @@ def test_apply_1m_3d_seeded(H, oracle):
     y = H.apply(f, diag, r)
     y64 = oracle.apply_f64(fr.n, 128, 32, f.data.astype(np.float64), diag, r)
     assert rel_l2(y, y64) <= TOL
+
+
+@pytest.mark.parametrize("n,sigma", [(512, 1.0), (8192, 1e-2), (65536, 1e-2), (65536, 1.0)])
+def test_fast_path_reproduces_reference_fp32_rounding(H, oracle, n, sigma):
+    """The fast kernels run the reference's fp32 accumulation chains in its exact order
+    (F^T r, restrictions, tile couplings) and form every f64-accumulated product exactly, so
+    the output tracks apply<float> to f64 rounding, far inside the 1e-5 gate. (The PCG
+    iteration count is sensitive to these fp32 roundings: the reference's own apply<double>
+    needs 224 instead of 240 iterations on make_frame(1024, 7, 3).)"""
+    f = tensor(H, n, 128, 32, sigma, 17, n)
+    rng = np.random.default_rng(3)
+    diag = 1.0 + np.abs(rng.standard_normal(n))
+    r = rng.standard_normal(n)
+    y = H.apply(f, diag, r)
+    y32 = oracle.apply_f32(n, 128, 32, f.data, diag, r)
+    assert rel_l2(y, y32) <= 1e-9, rel_l2(y, y32)
