@@ -67,7 +67,7 @@ struct hfpg_handle {
            *y_loc = nullptr, *b = nullptr, *scratch = nullptr;
     Layout ws_layout;
     bool have_ws = false;
-    float *restrict_ = nullptr, *crow = nullptr, *ccol = nullptr;
+    float *restrict_ = nullptr, *coupled = nullptr;
     double *node_u = nullptr, *node_v = nullptr;
     unsigned* tree_counters = nullptr;
     double* partials = nullptr;
@@ -103,7 +103,8 @@ uint64_t leaf_grid(const hfpg_handle* h) {
     return h->fast ? std::min<uint64_t>(h->L.k, uint64_t(h->num_sms)) : h->L.k;
 }
 uint64_t prolong_grid(const hfpg_handle* h) {
-    return h->fast ? std::min<uint64_t>(h->L.k, uint64_t(h->num_sms) * 2) : h->L.k;
+    return h->fast ? std::min<uint64_t>((h->L.k + kProlWarps - 1) / kProlWarps, uint64_t(h->num_sms) * 2)
+                   : h->L.k;
 }
 uint64_t spmv_grid(const hfpg_handle* h) {
     if (h->spmv_stage_bytes) {
@@ -147,8 +148,7 @@ void ensure_workspace(hfpg_handle* h) {
         invalidate_graph(h);
         const Layout& L = h->L;
         dalloc(h->restrict_, L.k * 2 * L.ls);
-        dalloc(h->crow, L.m * L.ls);
-        dalloc(h->ccol, L.m * L.ls);
+        dalloc(h->coupled, L.m * 2 * L.ls);
         dalloc(h->node_u, 2 * L.k * L.ls);
         dalloc(h->node_v, 2 * L.k * L.ls);
         dalloc(h->tree_counters, 2 * L.k);
@@ -207,8 +207,7 @@ void fill_sys(hfpg_handle* h) {
     s.p1 = h->p1;
     s.y_loc = h->y_loc;
     s.restrict_ = h->restrict_;
-    s.crow = h->crow;
-    s.ccol = h->ccol;
+    s.coupled = h->coupled;
     s.node_u = h->node_u;
     s.node_v = h->node_v;
     s.tree_counters = h->tree_counters;
@@ -233,14 +232,14 @@ void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
     }
     CK(cudaGetLastError());
     if (h->fast) {
-        k_coarse_fast<<<unsigned(L.k / std::min<uint64_t>(L.k, 32)), 256, kCoarseFastSmem, h->stream>>>(s, mode);
+        k_coarse_fast<<<unsigned(L.k / std::min<uint64_t>(L.k, kCoarseS0)), 256, kCoarseFastSmem, h->stream>>>(s, mode);
     } else {
         const uint64_t S0 = std::min<uint64_t>(L.k, coarse_width(L));
         k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(s, mode);
     }
     CK(cudaGetLastError());
     if (h->fast)
-        k_prolong_fast<<<unsigned(prolong_grid(h)), 256, sizeof(ProlSmem), h->stream>>>(s, mode, rin, zout);
+        k_prolong_fast<<<unsigned(prolong_grid(h)), 256, 0, h->stream>>>(s, mode, rin, zout);
     else
         k_prolong_generic<<<unsigned(L.k), 256, 2 * L.ls * sizeof(float), h->stream>>>(s, mode, rin, zout);
     CK(cudaGetLastError());
@@ -276,8 +275,6 @@ void configure_kernels() {
         CK(cudaFuncSetAttribute(k_leaf_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(sizeof(LeafSmem))));
         CK(cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        CK(cudaFuncSetAttribute(k_prolong_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(sizeof(ProlSmem))));
         CK(cudaFuncSetAttribute(k_coarse_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCoarseFastSmem)));
         CK(cudaFuncSetAttribute(k_spmv_tma<kLoop>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         CK(cudaFuncSetAttribute(k_spmv_tma<kApply>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
@@ -391,7 +388,7 @@ int hfpg_destroy(hfpg_handle* h) {
         dfree(h->F); dfree(h->slice_off); dfree(h->sell_cols); dfree(h->sell_vals);
         dfree(h->a_diag); dfree(h->x); dfree(h->r); dfree(h->z); dfree(h->ap); dfree(h->p0);
         dfree(h->p1); dfree(h->y_loc); dfree(h->b); dfree(h->scratch); dfree(h->restrict_);
-        dfree(h->crow); dfree(h->ccol); dfree(h->node_u); dfree(h->node_v);
+        dfree(h->coupled); dfree(h->node_u); dfree(h->node_v);
         dfree(h->tree_counters); dfree(h->partials); dfree(h->counters); dfree(h->sc);
         dfree(h->history);
         if (h->ev0) cudaEventDestroy(h->ev0);
@@ -678,12 +675,12 @@ int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out) {
                 k_leaf_generic<<<unsigned(L.k), 256, 2 * L.l * sizeof(float), h->stream>>>(h->sys, kLoop, nullptr);
             CK(cudaEventRecord(ev[2], h->stream));
             if (h->fast)
-                k_coarse_fast<<<unsigned(L.k / std::min<uint64_t>(L.k, 32)), 256, kCoarseFastSmem, h->stream>>>(h->sys, kLoop);
+                k_coarse_fast<<<unsigned(L.k / std::min<uint64_t>(L.k, kCoarseS0)), 256, kCoarseFastSmem, h->stream>>>(h->sys, kLoop);
             else
                 k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(h->sys, kLoop);
             CK(cudaEventRecord(ev[3], h->stream));
             if (h->fast)
-                k_prolong_fast<<<unsigned(prolong_grid(h)), 256, sizeof(ProlSmem), h->stream>>>(h->sys, kLoop, nullptr, nullptr);
+                k_prolong_fast<<<unsigned(prolong_grid(h)), 256, 0, h->stream>>>(h->sys, kLoop, nullptr, nullptr);
             else
                 k_prolong_generic<<<unsigned(L.k), 256, 2 * L.ls * sizeof(float), h->stream>>>(h->sys, kLoop, nullptr, nullptr);
             CK(cudaEventRecord(ev[4], h->stream));

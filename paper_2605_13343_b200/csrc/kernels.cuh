@@ -31,7 +31,7 @@ struct DevSys {
     double *x, *r, *z, *ap, *p0, *p1, *y_loc;
     // apply workspace
     float* restrict_;        // K x 2 L_s  (û_k | v̂_k), fp32 as in the reference
-    float *crow, *ccol;      // M_H x L_s coupled_row / coupled_col
+    float* coupled;          // M_H x 2 L_s: tile m = [coupled_row (L_s) | coupled_col (L_s)]
     double *node_u, *node_v; // heap-indexed strip sums of subtree roots (2K x L_s)
     unsigned* tree_counters; // 2K arrival counters for the coarse tree
     uint64_t coarse_S;       // subtree width per k_coarse task (power of two)
@@ -506,11 +506,11 @@ __device__ __forceinline__ void tile_warp32(const float4 (&u4)[4], const float4 
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         T4[lane * 4 + i] = u4[i];
-        T4[128 + lane * 4 + i] = v4[i];
+        T4[132 + lane * 4 + i] = v4[i];  // V at +528 floats: the two half-warps hit disjoint banks
     }
     __syncwarp();
     const int q = lane & 15;
-    const float* col = scratch + (lane < 16 ? 0 : 512) + q;
+    const float* col = scratch + (lane < 16 ? 0 : 528) + q;
     const double* st = lane < 16 ? sr : sc;
     float coef = 0.f;
 #pragma unroll
@@ -546,7 +546,8 @@ __device__ __forceinline__ void load_tile32(const DevSys& s, uint64_t m, int lan
     }
 }
 
-constexpr size_t kCoarseFastSmem = 2 * 63 * 32 * sizeof(double) + 8 * 1024 * sizeof(float);
+constexpr uint64_t kCoarseS0 = 16;
+constexpr size_t kCoarseFastSmem = 2 * 63 * 32 * sizeof(double) + 8 * 1056 * sizeof(float);
 
 // Coarse stage, fast path (L_s = 32): the bisection tree in heap order; each CTA owns an
 // aligned subtree of up to 32 bottom nodes, runs the f64 up-sweep in shared memory, computes
@@ -557,15 +558,17 @@ __global__ void __launch_bounds__(256) k_coarse_fast(DevSys s, int mode) {
     extern __shared__ __align__(128) unsigned char cfraw[];
     double* SU = reinterpret_cast<double*>(cfraw);                 // 63 x 32
     double* SV = SU + 63 * 32;                                      // 63 x 32
-    float (*scratch)[1024] = reinterpret_cast<float (*)[1024]>(SV + 63 * 32);  // per warp
+    float (*scratch)[1056] = reinterpret_cast<float (*)[1056]>(SV + 63 * 32);  // per warp
     __shared__ int last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t pol_keep = policy_evict_last();
     uint64_t task = blockIdx.x;
     uint64_t dlo = s.D;
     for (int level = 0;; ++level) {
-        const uint64_t cnt = 1ULL << dlo;
-        const uint64_t S = cnt < 32 ? cnt : 32;
+        // bottom level: 16-leaf subtrees (one wave of CTAs, two tile rounds per warp); above:
+        // 32-node subtrees (fewer serial levels)
+        const uint64_t cnt = 1ULL << dlo, Smax = level == 0 ? kCoarseS0 : 32;
+        const uint64_t S = cnt < Smax ? cnt : Smax;
         int logS = 0;
         while ((1ULL << logS) < S) ++logS;
         const uint64_t dr = dlo - logS;
@@ -619,10 +622,10 @@ __global__ void __launch_bounds__(256) k_coarse_fast(DevSys s, int mode) {
             const double* sr = SU + (2 * u + 1) * 32;
             const double* sc = SV + (2 * u + 2) * 32;
             if ((r & 1) == 0) {
-                tile_warp32(ua, va, sr, sc, lane, scratch[warp], s.ccol + m * 32, s.crow + m * 32);
+                tile_warp32(ua, va, sr, sc, lane, scratch[warp], s.coupled + m * 64 + 32, s.coupled + m * 64);
                 if (u + 17 < S) load_tile32(s, tile_id(u + 16), lane, ua, va, pol_keep);
             } else {
-                tile_warp32(ub, vb, sr, sc, lane, scratch[warp], s.ccol + m * 32, s.crow + m * 32);
+                tile_warp32(ub, vb, sr, sc, lane, scratch[warp], s.coupled + m * 64 + 32, s.coupled + m * 64);
                 if (u + 17 < S) load_tile32(s, tile_id(u + 16), lane, ub, vb, pol_keep);
             }
         }
@@ -765,8 +768,8 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse(DevSys s, int mode) {
                     a = fma(double(V[j * rk + q]), double(cr_[q]), a);
                     b = fma(double(U[j * rk + q]), double(cc_[q]), b);
                 }
-                s.ccol[m * ls + j] = float(a);
-                s.crow[m * ls + j] = float(b);
+                s.coupled[m * 2 * ls + ls + j] = float(a);
+                s.coupled[m * 2 * ls + j] = float(b);
             }
             __syncwarp();
         }
@@ -830,121 +833,127 @@ __device__ __forceinline__ bool prolong_skip(const DevSys& s, int mode) {
     return true;
 }
 
-// Prolongation, fast path: persistent, 2 CTAs x 256 threads per SM, a 3-stage TMA ring of
-// {Ũ_k|Ṽ_k (32 KB), y_loc_k, r_k, a_diag_k, gate_k}. Leaves are walked in REVERSE order: the
-// leaf kernel streamed the bridges with an evict_last policy, so the last ~100 MB it read are
-// still in L2 when this kernel starts. The ancestor gather of the next leaf is prefetched into
-// registers while the current one computes.
-constexpr int kProlStages = 3;
-constexpr int kMaxDepth = 24;
-struct ProlSmem {
-    float B[kProlStages][2 * kL * kLs];
-    double vec[kProlStages][3][kL];  // y_loc, r, a_diag
-    float gate[kProlStages][kL];
-    float g[2][kLs];
-    uint64_t full[kProlStages];
-};
+// Prolongation, fast path: one warp per leaf, no shared-memory staging and no block
+// barriers. Leaves are walked in REVERSE order: the leaf kernel streamed the bridges with an
+// evict_last policy, so the ones it read last are still in L2 here. Per leaf a warp
+//   1. loads the epilogue operands of its 128 rows (lane L: rows L + 32t) and the ancestor
+//      gather (lane j: coupled_row / coupled_col component j of every ancestor),
+//   2. streams Ũ_k | Ṽ_k as 128-bit loads, two 16-row chunks in flight, 8 lanes per row,
+//      exact f64 products summed in f64 (matvec_add_double, apply.cpp:156-166),
+//   3. finishes z = y_loc + Ũ g_r + Ṽ g_c + gate r / a + shift r (apply.cpp:169-173).
+constexpr int kMaxDepth = 20;  // K <= 2^20 leaves (N <= 134M at L = 128)
+constexpr int kProlWarps = 8;
 
 __global__ void __launch_bounds__(256, 2) k_prolong_fast(DevSys s, int mode, const double* rin_ext,
                                                          double* zout) {
     if (prolong_skip(s, mode)) return;
-    extern __shared__ __align__(128) unsigned char praw[];
-    ProlSmem& sm = *reinterpret_cast<ProlSmem*>(praw);
-    const int tid = threadIdx.x;
+    __shared__ double su[kProlWarps][kL], sv[kProlWarps][kL];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t K = s.K, D = s.D;
     const double* rsrc = mode == kApply ? rin_ext : s.r;
     double* zdst = mode == kApply ? zout : s.z;
     const double shift = s.sc->shift;
-    const uint64_t pol = policy_evict_first();
-    const uint64_t nl = K > blockIdx.x ? (K - 1 - blockIdx.x) / gridDim.x + 1 : 0;  // my leaves
-    auto leaf_of = [&](uint64_t i) { return K - 1 - (blockIdx.x + i * gridDim.x); };
-    if (tid == 0) {
-        for (int q = 0; q < kProlStages; ++q) mbar_init(&sm.full[q], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    auto issue = [&](uint64_t i) {
-        const int st = int(i % kProlStages);
-        const uint64_t leaf = leaf_of(i);
-        mbar_expect_tx(&sm.full[st], 2 * kL * kLs * 4 + 3 * kL * 8 + kL * 4);
-        const float* b = s.F + s.bridge_base + leaf * (2 * kL * kLs);
-        tma_load_1d(&sm.B[st][0], b, kL * kLs * 4, &sm.full[st], pol);
-        tma_load_1d(&sm.B[st][kL * kLs], b + kL * kLs, kL * kLs * 4, &sm.full[st], pol);
-        tma_load_1d(sm.vec[st][0], s.y_loc + leaf * kL, kL * 8, &sm.full[st], pol);
-        tma_load_1d(sm.vec[st][1], rsrc + leaf * kL, kL * 8, &sm.full[st], pol);
-        tma_load_1d(sm.vec[st][2], s.a_diag + leaf * kL, kL * 8, &sm.full[st], pol);
-        tma_load_1d(sm.gate[st], s.F + s.gate_base + leaf * kL, kL * 4, &sm.full[st], pol);
-    };
-    if (tid == 0)
-        for (uint64_t i = 0; i < nl && i < kProlStages; ++i) issue(i);
-    // ancestor gather operands of leaf i -> registers (side 0: coupled_row where the leaf is in
-    // the tile's row half; side 1: coupled_col where it is in the column half)
-    const int side = tid >> 5, j = tid & 31;
-    float t[kMaxDepth];
-    auto gather_load = [&](uint64_t leaf) {
-        const float* src = side ? s.ccol : s.crow;
+    const int l8 = lane & 7, rsub = lane >> 3;
+    double rz = 0.0;
+    for (uint64_t w = uint64_t(blockIdx.x) * kProlWarps + wid; w < K; w += uint64_t(gridDim.x) * kProlWarps) {
+        const uint64_t leaf = K - 1 - w;
+        const uint64_t base = leaf * kL;
+        // (1) ancestor gather, all loads issued up front
+        // ancestor at depth d: heap node (K + leaf) >> (D - d), minus one; the leaf sits in its
+        // column half iff bit D-1-d of the leaf index is set -> offset 32 in the tile's pair
+        const uint32_t hl = uint32_t(K + leaf), lf = uint32_t(leaf), Du = uint32_t(D);
+        float ga[kMaxDepth];
 #pragma unroll
         for (int d = 0; d < kMaxDepth; ++d) {
-            t[d] = 0.f;
-            if (uint64_t(d) < D && ((leaf >> (D - 1 - d)) & 1ULL) == uint64_t(side))
-                t[d] = __ldcg(&src[(((K + leaf) >> (D - d)) - 1) * kLs + j]);
+            ga[d] = 0.f;
+            if (uint32_t(d) < Du) {
+                const uint32_t m = (hl >> (Du - d)) - 1u, right = (lf >> (Du - 1 - d)) & 1u;
+                ga[d] = __ldcg(&s.coupled[m * 64u + right * 32u + lane]);
+            }
         }
-    };
-    if (tid < 2 * kLs && nl) gather_load(leaf_of(0));
-    double rz = 0.0;
-    const int l8 = tid & 7, rowi = tid >> 3;
-    for (uint64_t i = 0; i < nl; ++i) {
-        const int st = int(i % kProlStages);
-        const uint64_t leaf = leaf_of(i);
-        if (tid < 2 * kLs) {  // f64 gather in tile order (root first), apply.cpp:140-154
-            double acc = 0.0;
+        // f64 gathers in tile order, root first (apply.cpp:140-154): lane j ends with
+        // g_r[j] (rows halves) and g_c[j] (column halves)
+        double gr = 0.0, gc = 0.0;
 #pragma unroll
-            for (int d = 0; d < kMaxDepth; ++d)
-                if (uint64_t(d) < D && ((leaf >> (D - 1 - d)) & 1ULL) == uint64_t(side))
-                    acc += double(t[d]);
-            sm.g[side][j] = float(acc);
-            if (i + 1 < nl) gather_load(leaf_of(i + 1));
+        for (int d = 0; d < kMaxDepth; ++d)
+            if (uint32_t(d) < Du) {
+                if ((lf >> (Du - 1 - d)) & 1u) gc += double(ga[d]);
+                else gr += double(ga[d]);
+            }
+        const float grf = float(gr), gcf = float(gc);
+        double g4[4], h4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            g4[q] = double(__shfl_sync(0xffffffffu, grf, 4 * l8 + q));
+            h4[q] = double(__shfl_sync(0xffffffffu, gcf, 4 * l8 + q));
         }
-        mbar_wait(&sm.full[st], uint32_t((i / kProlStages) & 1));
-        __syncthreads();
-        {   // Ũ_k g_r and Ṽ_k g_c: 8 lanes per 32-float row, exact f64 products, f64 sums
-            // (matvec_add_double, apply.cpp:156-166); after the xor-reduce every lane of the
-            // group holds the row sums, so lane l8 = ps finishes the row of pass ps (one f64
-            // division per lane instead of four on one lane)
-            const float4 gr = reinterpret_cast<const float4*>(sm.g[0])[l8];
-            const float4 gc = reinterpret_cast<const float4*>(sm.g[1])[l8];
-            const double g0 = gr.x, g1 = gr.y, g2 = gr.z, g3 = gr.w;
-            const double h0 = gc.x, h1 = gc.y, h2 = gc.z, h3 = gc.w;
+        // (2) bridges: chunk c = rows 16c..16c+15; lane (rsub, l8) covers rows 16c + 4i + rsub;
+        //     two chunks (8 KB per warp) in flight
+        const float4* Bu = reinterpret_cast<const float4*>(s.F + s.bridge_base + leaf * (2 * kL * kLs));
+        const float4* Bv = Bu + kL * kLs / 4;
+        float4 ua[4], va[4], ub[4], vb[4];
+        auto load_chunk = [&](int c, float4 (&u)[4], float4 (&v)[4]) {
 #pragma unroll
-            for (int ps = 0; ps < 4; ++ps) {
-                const int row = ps * 32 + rowi;
-                const float4 u4 = reinterpret_cast<const float4*>(&sm.B[st][row * kLs])[l8];
-                const float4 v4 = reinterpret_cast<const float4*>(&sm.B[st][kL * kLs + row * kLs])[l8];
-                double au = fma(double(u4.w), g3, fma(double(u4.z), g2, fma(double(u4.y), g1, double(u4.x) * g0)));
-                double av = fma(double(v4.w), h3, fma(double(v4.z), h2, fma(double(v4.y), h1, double(v4.x) * h0)));
+            for (int i = 0; i < 4; ++i) {
+                const int row = 16 * c + 4 * i + rsub;
+                u[i] = ldg_stream(Bu + row * (kLs / 4) + l8);
+                v[i] = ldg_stream(Bv + row * (kLs / 4) + l8);
+            }
+        };
+        auto do_chunk = [&](int c, const float4 (&u)[4], const float4 (&v)[4]) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                double au = fma(double(u[i].w), g4[3], fma(double(u[i].z), g4[2],
+                            fma(double(u[i].y), g4[1], double(u[i].x) * g4[0])));
+                double av = fma(double(v[i].w), h4[3], fma(double(v[i].z), h4[2],
+                            fma(double(v[i].y), h4[1], double(v[i].x) * h4[0])));
                 au += __shfl_xor_sync(0xffffffffu, au, 4);
                 au += __shfl_xor_sync(0xffffffffu, au, 2);
                 au += __shfl_xor_sync(0xffffffffu, au, 1);
                 av += __shfl_xor_sync(0xffffffffu, av, 4);
                 av += __shfl_xor_sync(0xffffffffu, av, 2);
                 av += __shfl_xor_sync(0xffffffffu, av, 1);
-                if (l8 == ps) {
-                    const double rv = sm.vec[st][1][row];
-                    double y = sm.vec[st][0][row];
-                    y += au;
-                    y += av;
-                    y += double(sm.gate[st][row]) * rv / sm.vec[st][2][row] + shift * rv;
-                    zdst[leaf * kL + row] = y;
-                    rz = fma(rv, y, rz);
+                if (l8 == 0) {
+                    su[wid][16 * c + 4 * i + rsub] = au;
+                    sv[wid][16 * c + 4 * i + rsub] = av;
                 }
             }
+        };
+        load_chunk(0, ua, va);
+#pragma unroll 1
+        for (int c = 0; c < 8; c += 2) {
+            load_chunk(c + 1, ub, vb);
+            do_chunk(c, ua, va);
+            if (c + 2 < 8) load_chunk(c + 2, ua, va);
+            do_chunk(c + 1, ub, vb);
         }
-        __syncthreads();  // stage st and g/su/sv are free again
-        if (tid == 0 && i + kProlStages < nl) issue(i + kProlStages);
+        double yl[4], rv[4], ad[4];
+        float gt[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const uint64_t i = base + lane + 32 * t;
+            yl[t] = __ldcg(&s.y_loc[i]);
+            rv[t] = __ldcg(&rsrc[i]);
+            ad[t] = __ldg(&s.a_diag[i]);
+            gt[t] = __ldg(&s.F[s.gate_base + i]);
+        }
+        __syncwarp();
+        // (3) epilogue, lane L owns rows L + 32t (coalesced)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int row = lane + 32 * t;
+            double y = yl[t];
+            y += su[wid][row];
+            y += sv[wid][row];
+            y += double(gt[t]) * rv[t] / ad[t] + shift * rv[t];
+            zdst[base + row] = y;
+            rz = fma(rv[t], y, rz);
+        }
+        __syncwarp();
     }
     if (mode == kApply) return;
     double v[1] = {rz}, tot[1];
-    if (grid_reduce_last<1>(v, s.partials, &s.counters[2], tot) && tid == 0)
+    if (grid_reduce_last<1>(v, s.partials, &s.counters[2], tot) && threadIdx.x == 0)
         prolong_epilogue(s, mode, tot[0]);
 }
 
@@ -955,11 +964,11 @@ __global__ void __launch_bounds__(256) k_prolong_generic(DevSys s, int mode,
     const uint64_t L = s.l, ls = s.ls, leaf = blockIdx.x, K = s.K, D = s.D;
     for (uint64_t t = threadIdx.x; t < 2 * ls; t += blockDim.x) {
         const uint64_t side = t / ls, j = t % ls;
-        const float* src = side ? s.ccol : s.crow;
+        const float* src = s.coupled + side * ls;
         double acc = 0.0;
         for (uint64_t d = 0; d < D; ++d) {
             const uint64_t m = ((K + leaf) >> (D - d)) - 1;
-            if (((leaf >> (D - 1 - d)) & 1ULL) == side) acc += double(__ldcg(&src[m * ls + j]));
+            if (((leaf >> (D - 1 - d)) & 1ULL) == side) acc += double(__ldcg(&src[m * 2 * ls + j]));
         }
         psm[t] = float(acc);
     }
