@@ -251,6 +251,7 @@ def run_ours(args, cfg):
     N.lib.hfpg_host_free(hb)
     N.lib.hfpg_host_free(hx)
 
+    per_iter, per_apply = dev.launch_counts()
     # per-kernel device times (standalone launches of the iteration's kernels, CUDA events on
     # the library stream) -> roofline of the dominant kernel
     ms4 = np.zeros(4, np.float32)
@@ -296,7 +297,7 @@ def run_ours(args, cfg):
                      "solve_ms_per_iteration": (t_max / args.steps) / max(iters[-1], 1)},
         "e2e": {"value": e2e_max / (e2e_steps * world), "unit": UNIT,
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 96},
-        "gpu_launches": args.steps * (4 + 4 * iters[-1]),
+        "gpu_launches": args.steps * (1 + per_apply + per_iter * iters[-1]),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -221,7 +221,24 @@ void fill_sys(hfpg_handle* h) {
 }
 
 
-// The three apply launches (stages 1-3, 4, 5-7) in a given mode.
+// Apply stage 4: subtree kernel + (above 32 leaves) the parallel top-of-tree kernel.
+void launch_coarse(hfpg_handle* h, const DevSys& s, int mode) {
+    const Layout& L = h->L;
+    if (h->fast) {
+        k_coarse_fast<<<unsigned(L.k / std::min<uint64_t>(L.k, kCoarseS0)), 256, kCoarseFastSmem, h->stream>>>(s, mode);
+        if (L.k > kCoarseS0) {
+            CK(cudaGetLastError());
+            const uint64_t top = L.k / kCoarseS0 - 1;
+            k_coarse_top<<<unsigned((top + kTopWarps - 1) / kTopWarps), 32 * kTopWarps, 0, h->stream>>>(s, mode);
+        }
+    } else {
+        const uint64_t S0 = std::min<uint64_t>(L.k, coarse_width(L));
+        k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(s, mode);
+    }
+    CK(cudaGetLastError());
+}
+
+// The apply launches (stages 1-3, 4, 5-7) in a given mode.
 void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
     const DevSys& s = h->sys;
     const Layout& L = h->L;
@@ -231,13 +248,7 @@ void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
         k_leaf_generic<<<unsigned(L.k), 256, 2 * L.l * sizeof(float), h->stream>>>(s, mode, rin);
     }
     CK(cudaGetLastError());
-    if (h->fast) {
-        k_coarse_fast<<<unsigned(L.k / std::min<uint64_t>(L.k, kCoarseS0)), 256, kCoarseFastSmem, h->stream>>>(s, mode);
-    } else {
-        const uint64_t S0 = std::min<uint64_t>(L.k, coarse_width(L));
-        k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(s, mode);
-    }
-    CK(cudaGetLastError());
+    launch_coarse(h, s, mode);
     if (h->fast)
         k_prolong_fast<<<unsigned(prolong_grid(h)), 256, 0, h->stream>>>(s, mode, rin, zout);
     else
@@ -639,8 +650,9 @@ int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg
 
 int hfpg_launch_counts(hfpg_handle* h, uint32_t* per_iteration, uint32_t* per_apply) {
     return guarded([&] {
-        *per_apply = 3;
-        *per_iteration = h->precond == HFPG_PRECOND_FACTOR ? 4 : 2;
+        const uint32_t apply = (h->have_factors && h->fast && h->L.k > kCoarseS0) ? 4 : 3;
+        *per_apply = apply;
+        *per_iteration = h->precond == HFPG_PRECOND_FACTOR ? apply + 1 : 2;
     });
 }
 
@@ -674,10 +686,7 @@ int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out) {
             else
                 k_leaf_generic<<<unsigned(L.k), 256, 2 * L.l * sizeof(float), h->stream>>>(h->sys, kLoop, nullptr);
             CK(cudaEventRecord(ev[2], h->stream));
-            if (h->fast)
-                k_coarse_fast<<<unsigned(L.k / std::min<uint64_t>(L.k, kCoarseS0)), 256, kCoarseFastSmem, h->stream>>>(h->sys, kLoop);
-            else
-                k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(h->sys, kLoop);
+            launch_coarse(h, h->sys, kLoop);
             CK(cudaEventRecord(ev[3], h->stream));
             if (h->fast)
                 k_prolong_fast<<<unsigned(prolong_grid(h)), 256, 0, h->stream>>>(h->sys, kLoop, nullptr, nullptr);
