@@ -6,5 +6,5 @@ timeout 300 python bench.py --steps 3 --warmup 1 --no-cpu-baseline > gpurun_out/
 timeout 300 python bench.py --steps 3 --warmup 1 --no-cpu-baseline --config 2d_65536 > gpurun_out/bench65k.log 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_3d.csv python tools/iter_driver.py --reps 3 > gpurun_out/ncu_launch.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_leaf_fast -s 1 -c 1 -o gpurun_out/prof_leaf python tools/iter_driver.py --reps 3 > gpurun_out/ncu_full.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_prolong_fast|k_spmv_tma|k_coarse_fast" -s 3 -c 3 -o gpurun_out/prof_other python tools/iter_driver.py --reps 3 > gpurun_out/ncu_full2.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_prolong_fast|k_spmv_tma|k_coarse" -s 4 -c 4 -o gpurun_out/prof_other python tools/iter_driver.py --reps 3 > gpurun_out/ncu_full2.log 2>&1
 tail -2 gpurun_out/smoke.log; tail -6 gpurun_out/pytest.log; cut -c1-300 gpurun_out/bench.log; tail -3 gpurun_out/ncu_launch.log; tail -3 gpurun_out/ncu_full.log

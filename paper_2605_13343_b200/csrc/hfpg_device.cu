@@ -225,12 +225,13 @@ void fill_sys(hfpg_handle* h) {
 void launch_coarse(hfpg_handle* h, const DevSys& s, int mode) {
     const Layout& L = h->L;
     if (h->fast) {
-        k_coarse_fast<<<unsigned(L.k / std::min<uint64_t>(L.k, kCoarseS0)), 256, kCoarseFastSmem, h->stream>>>(s, mode);
-        if (L.k > kCoarseS0) {
+        const uint64_t S = std::min<uint64_t>(L.k, kCoarseS0), R = L.k / S;
+        if (S > 1) {
+            k_coarse_sums<<<unsigned(R), 256, 0, h->stream>>>(s, mode);
             CK(cudaGetLastError());
-            const uint64_t top = L.k / kCoarseS0 - 1;
-            k_coarse_top<<<unsigned((top + kTopWarps - 1) / kTopWarps), 32 * kTopWarps, 0, h->stream>>>(s, mode);
         }
+        const uint64_t grid = (R - 1) + ((L.k - 1) - (R - 1) + kTileWarps - 1) / kTileWarps;
+        k_coarse_tiles<<<unsigned(grid), 32 * kTileWarps, 0, h->stream>>>(s, mode);
     } else {
         const uint64_t S0 = std::min<uint64_t>(L.k, coarse_width(L));
         k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(s, mode);
@@ -286,7 +287,6 @@ void configure_kernels() {
         CK(cudaFuncSetAttribute(k_leaf_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(sizeof(LeafSmem))));
         CK(cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        CK(cudaFuncSetAttribute(k_coarse_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCoarseFastSmem)));
         CK(cudaFuncSetAttribute(k_spmv_tma<kLoop>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         CK(cudaFuncSetAttribute(k_spmv_tma<kApply>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         CK(cudaFuncSetAttribute(k_leaf_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
@@ -650,7 +650,7 @@ int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg
 
 int hfpg_launch_counts(hfpg_handle* h, uint32_t* per_iteration, uint32_t* per_apply) {
     return guarded([&] {
-        const uint32_t apply = (h->have_factors && h->fast && h->L.k > kCoarseS0) ? 4 : 3;
+        const uint32_t apply = (h->have_factors && h->fast) ? 4 : 3;
         *per_apply = apply;
         *per_iteration = h->precond == HFPG_PRECOND_FACTOR ? apply + 1 : 2;
     });

@@ -547,43 +547,27 @@ __device__ __forceinline__ void load_tile32(const DevSys& s, uint64_t m, int lan
 }
 
 constexpr uint64_t kCoarseS0 = 32;
-constexpr size_t kCoarseFastSmem = 2 * 63 * 32 * sizeof(double) + 8 * 1056 * sizeof(float);
 
-// Coarse stage, fast path (L_s = 32), part 1: each CTA owns an aligned subtree of up to 32
-// leaves, runs the f64 up-sweep of its restrictions in shared memory, computes the subtree's
-// internal tiles (one warp each) and publishes the subtree-root sums. No inter-CTA chaining:
-// one wave of independent CTAs.
-__global__ void __launch_bounds__(256) k_coarse_fast(DevSys s, int mode) {
+// Coarse stage, fast path (L_s = 32), part 1 — strip sums. Each CTA owns an aligned subtree of
+// up to 32 leaves, loads their restrictions (û | v̂, fp32) and runs the f64 up-sweep in shared
+// memory; every internal node's sums (root included) go to the heap-indexed node arrays.
+__global__ void __launch_bounds__(256) k_coarse_sums(DevSys s, int mode) {
     if (mode != kApply && s.sc->done) return;
-    extern __shared__ __align__(128) unsigned char cfraw[];
-    double* SU = reinterpret_cast<double*>(cfraw);  // 63 x 32, local heap order
-    double* SV = SU + 63 * 32;
-    float (*scratch)[1056] = reinterpret_cast<float (*)[1056]>(SV + 63 * 32);  // per warp
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t pol_keep = policy_evict_last();
+    __shared__ double SU[63 * 32], SV[63 * 32];
+    const int tid = threadIdx.x;
     const uint64_t task = blockIdx.x, D = s.D;
     const uint64_t S = s.K < kCoarseS0 ? s.K : kCoarseS0;
     int logS = 0;
     while ((1ULL << logS) < S) ++logS;
-    const uint64_t dr = D - logS;  // depth of this subtree's root
-    auto tile_id = [&](uint64_t u) {
-        int ld = 0;
-        while ((2ULL << ld) <= u + 1) ++ld;
-        return (1ULL << (dr + ld)) - 1 + task * (1ULL << ld) + (u + 1 - (1ULL << ld));
-    };
-    // this warp's first two tiles: issue their loads before the bottom layer / up-sweep, then
-    // keep one tile in flight while the other computes (register double buffer)
-    float4 ua[4], va[4], ub[4], vb[4];
-    if (uint64_t(warp) + 1 < S) load_tile32(s, tile_id(warp), lane, ua, va, pol_keep);
-    if (uint64_t(warp) + 9 < S) load_tile32(s, tile_id(warp + 8), lane, ub, vb, pol_keep);
-    {   // bottom layer: the subtree's restrictions (f32 -> f64), all loads issued first
+    const uint64_t dr = D - logS;
+    {   // all loads issued before any store
         double bu[4], bv[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             const uint64_t e = uint64_t(tid) + 256u * t, q = e >> 5, j = e & 31;
             if (e < S * 32) {
-                bu[t] = double(__ldcg(&s.restrict_[(task * S + q) * 64 + j]));
-                bv[t] = double(__ldcg(&s.restrict_[(task * S + q) * 64 + 32 + j]));
+                bu[t] = double(__ldg(&s.restrict_[(task * S + q) * 64 + j]));
+                bv[t] = double(__ldg(&s.restrict_[(task * S + q) * 64 + 32 + j]));
             }
         }
 #pragma unroll
@@ -596,60 +580,82 @@ __global__ void __launch_bounds__(256) k_coarse_fast(DevSys s, int mode) {
         }
     }
     __syncthreads();
-    for (int ld = logS - 1; ld >= 0; --ld) {  // f64 up-sweep
+    for (int ld = logS - 1; ld >= 0; --ld) {
         const uint64_t u0 = (1ULL << ld) - 1;
         for (uint64_t e = tid; e < (1ULL << ld) * 32; e += blockDim.x) {
             const uint64_t u = u0 + (e >> 5), j = e & 31;
-            SU[u * 32 + j] = SU[(2 * u + 1) * 32 + j] + SU[(2 * u + 2) * 32 + j];
-            SV[u * 32 + j] = SV[(2 * u + 1) * 32 + j] + SV[(2 * u + 2) * 32 + j];
+            const double a = SU[(2 * u + 1) * 32 + j] + SU[(2 * u + 2) * 32 + j];
+            const double b = SV[(2 * u + 1) * 32 + j] + SV[(2 * u + 2) * 32 + j];
+            SU[u * 32 + j] = a;
+            SV[u * 32 + j] = b;
+            const uint64_t g = (1ULL << (dr + ld)) - 1 + task * (1ULL << ld) + (u - u0);
+            s.node_u[g * 32 + j] = a;
+            s.node_v[g * 32 + j] = b;
         }
         __syncthreads();
     }
-    for (uint64_t u = warp, r = 0; u + 1 < S; u += 8, ++r) {
-        const uint64_t m = tile_id(u);
-        const double* sr = SU + (2 * u + 1) * 32;
-        const double* sc = SV + (2 * u + 2) * 32;
-        if ((r & 1) == 0) {
-            tile_warp32(ua, va, sr, sc, lane, scratch[warp], s.coupled + m * 64 + 32, s.coupled + m * 64);
-            if (u + 17 < S) load_tile32(s, tile_id(u + 16), lane, ua, va, pol_keep);
-        } else {
-            tile_warp32(ub, vb, sr, sc, lane, scratch[warp], s.coupled + m * 64 + 32, s.coupled + m * 64);
-            if (u + 17 < S) load_tile32(s, tile_id(u + 16), lane, ub, vb, pol_keep);
-        }
-    }
-    if (dr > 0 && tid < 32) {  // subtree-root sums for part 2
-        const uint64_t g = (1ULL << dr) - 1 + task;
-        s.node_u[g * 32 + tid] = SU[tid];
-        s.node_v[g * 32 + tid] = SV[tid];
-    }
 }
 
-// Coarse stage, fast path, part 2: every tile above the 32-leaf subtrees, one warp each, in
-// parallel. A tile at depth d spans w = R / 2^d subtree roots (R = K / 32); its strip sums are
-// the f64 sums of the left half's root û-sums and the right half's root v̂-sums.
-constexpr int kTopWarps = 8;
-__global__ void __launch_bounds__(32 * kTopWarps) k_coarse_top(DevSys s, int mode) {
+// Coarse stage, fast path, part 2 — every tile in parallel. Tiles whose children lie inside the
+// 32-leaf subtrees take one warp each and read the children's sums directly (leaf children:
+// the restrictions themselves); each tile above them takes a whole CTA whose 8 warps split the
+// sum over the subtree roots of its halves. Then the exact-order tile chain (tile_warp32).
+constexpr int kTileWarps = 8;
+__global__ void __launch_bounds__(32 * kTileWarps) k_coarse_tiles(DevSys s, int mode) {
     if (mode != kApply && s.sc->done) return;
-    __shared__ __align__(16) float scratch[kTopWarps][1056];
-    __shared__ double sr[kTopWarps][32], sc[kTopWarps][32];
+    __shared__ __align__(16) float scratch[kTileWarps][1056];
+    __shared__ double sr[kTileWarps][32], sc[kTileWarps][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t m = uint64_t(blockIdx.x) * kTopWarps + warp;
-    const uint64_t R = s.K / kCoarseS0;  // subtree roots (nodes at depth D - 5)
-    if (m >= R - 1) return;
+    const uint64_t K = s.K, D = s.D;
+    const uint64_t S = K < kCoarseS0 ? K : kCoarseS0;
+    const uint64_t R = K / S;            // subtree roots, at depth dr
+    const uint64_t upper = R - 1;        // tiles above the roots: one CTA each
     const uint64_t pol_keep = policy_evict_last();
+    uint64_t m;
+    if (blockIdx.x < upper) {
+        m = blockIdx.x;
+        int d = 0;
+        while ((2ULL << d) <= m + 1) ++d;
+        const uint64_t w = R >> d, a = (m + 1 - (1ULL << d)) * w, g0 = R - 1;
+        double pu = 0.0, pv = 0.0;
+        for (uint64_t t = warp; t < w / 2; t += kTileWarps) {
+            pu += __ldg(&s.node_u[(g0 + a + t) * 32 + lane]);
+            pv += __ldg(&s.node_v[(g0 + a + w / 2 + t) * 32 + lane]);
+        }
+        sr[warp][lane] = pu;
+        sc[warp][lane] = pv;
+        __syncthreads();
+        if (warp != 0) return;
+        float4 u4[4], v4[4];
+        load_tile32(s, m, lane, u4, v4, pol_keep);
+        double tu = 0.0, tv = 0.0;
+#pragma unroll
+        for (int q = 0; q < kTileWarps; ++q) {
+            tu += sr[q][lane];
+            tv += sc[q][lane];
+        }
+        __syncwarp();
+        sr[0][lane] = tu;
+        sc[0][lane] = tv;
+        __syncwarp();
+        tile_warp32(u4, v4, sr[0], sc[0], lane, scratch[0], s.coupled + m * 64 + 32, s.coupled + m * 64);
+        return;
+    }
+    m = upper + (uint64_t(blockIdx.x) - upper) * kTileWarps + warp;
+    if (m >= K - 1) return;
     float4 u4[4], v4[4];
     load_tile32(s, m, lane, u4, v4, pol_keep);
-    int d = 0;
-    while ((2ULL << d) <= m + 1) ++d;
-    const uint64_t i = m + 1 - (1ULL << d), w = R >> d, a = i * w;
-    const uint64_t g0 = R - 1;  // heap index of root 0
-    double su_ = 0.0, sv_ = 0.0;
-    for (uint64_t t = 0; t < w / 2; ++t) {
-        su_ += __ldcg(&s.node_u[(g0 + a + t) * 32 + lane]);
-        sv_ += __ldcg(&s.node_v[(g0 + a + w / 2 + t) * 32 + lane]);
+    const uint64_t l = 2 * m + 1, r = 2 * m + 2;  // children (heap)
+    double a, b;
+    if (l >= K - 1) {  // leaf children: their restrictions
+        a = double(__ldg(&s.restrict_[(l - (K - 1)) * 64 + lane]));
+        b = double(__ldg(&s.restrict_[(r - (K - 1)) * 64 + 32 + lane]));
+    } else {
+        a = __ldg(&s.node_u[l * 32 + lane]);
+        b = __ldg(&s.node_v[r * 32 + lane]);
     }
-    sr[warp][lane] = su_;
-    sc[warp][lane] = sv_;
+    sr[warp][lane] = a;
+    sc[warp][lane] = b;
     __syncwarp();
     tile_warp32(u4, v4, sr[warp], sc[warp], lane, scratch[warp], s.coupled + m * 64 + 32, s.coupled + m * 64);
 }
