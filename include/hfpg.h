@@ -63,6 +63,30 @@ typedef struct {
     double wall_ms;          /* device time of the solve (CUDA events around the graph) */
 } hfpg_report;
 
+/* toy_net.hpp:12-19 Config */
+typedef struct {
+    uint64_t d, layers, heads, gcn_layers, d_global, edge_hidden;
+} hfpg_toynet_config;
+
+/* toy_net.hpp:64-74 Trace, plus the host wall time of the call */
+typedef struct {
+    double max_attention_row_sum_error;
+    double highway_max_deviation;
+    uint64_t leaf_attention_dispatches, tile_attention_dispatches;
+    double ms;
+} hfpg_toynet_trace;
+
+/* frame.hpp:26-40 — the fields toynet::encode / forward consume (host pointers) */
+typedef struct {
+    uint64_t n, width, height;
+    const uint32_t* cell_order;
+    const double* rho;
+    double rho_heavy;
+    const uint64_t* row_offsets;
+    const uint32_t* col_indices;
+    const double* values;
+} hfpg_frame_view;
+
 typedef struct hfpg_handle hfpg_handle;
 typedef struct hfpg_frame hfpg_frame;
 
@@ -145,6 +169,16 @@ int hfpg_spmv(hfpg_handle* h, const double* x, double* y, int where);
 int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg, double* x,
                    double* history, hfpg_report* report, int where);
 
+/* ---- network inference + factor assembly ------------------------------------------------ */
+/* toy_net.cpp:170-223 init_weights(cfg, make_factor_layout(build_partition(n, leaf), coarse),
+ * weight_seed) and :322-586 forward(frame, ...) on the GPU (tcgen05 tf32 GEMMs + fp32 kernels;
+ * d = 128, head dim 16). Writes the packed factor tensor to `out` (host, packed-width floats;
+ * may be NULL); if `load` != 0 it also becomes the handle's factor tensor (no host round trip),
+ * ready for hfpg_apply / hfpg_pcg_solve. */
+int hfpg_toynet_forward(hfpg_handle* h, const hfpg_frame_view* frame, uint64_t leaf_size,
+                        uint64_t coarse_size, const hfpg_toynet_config* cfg, uint64_t weight_seed,
+                        float* out, int32_t load, hfpg_toynet_trace* trace);
+
 /* ---- introspection for tests / bench ---------------------------------------------------- */
 /* Number of kernels one PCG iteration launches, and one apply. */
 int hfpg_launch_counts(hfpg_handle* h, uint32_t* per_iteration, uint32_t* per_apply);
@@ -153,6 +187,9 @@ int hfpg_launch_counts(hfpg_handle* h, uint32_t* per_iteration, uint32_t* per_ap
  * the last solve; alpha = beta = 0 so the traffic is a real iteration's but x, r stay fixed).
  * ms_out[4] = {spmv, leaf, coarse, prolong}, averaged over `reps`. */
 int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out);
+/* C = A (M x K) * Bt^T (Bt: N x K), fp32 in/out, through the inference path's tcgen05 kind::tf32
+ * GEMM (host pointers; test hook). */
+int hfpg_gemm_tf32(uint64_t M, uint64_t N, uint64_t K, const float* A, const float* Bt, float* C);
 /* 1 if the fast sm_100a TMA path (L=128, L_s=32) is selected for the loaded layout. */
 int hfpg_fast_path(hfpg_handle* h, int32_t* out);
 

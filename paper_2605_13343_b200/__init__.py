@@ -6,9 +6,9 @@ csrc/); this package is the Python mirror of the reference interface over that A
 """
 from .api import (Checkpoint, CsrMatrix, Device, FactorInit, FactorLayout, FactorTensor, Frame,
                   HPartition, PrecondApplier, RngPurpose, RngStream, SolveConfig, SolveReport,
-                  SolveStatus, TileSpec, apply, build_partition, clamp_leaf_size, factor_applier,
+                  SolveStatus, TileSpec, ToynetConfig, ToynetTrace, apply, build_partition, clamp_leaf_size, factor_applier,
                   identity_applier, init_factors, jacobi_applier, make_factor_layout, make_frame,
                   make_frame_3d, packed_width, pcg_solve, read_checkpoint, test_frame_id,
-                  train_frame_id, write_checkpoint)
+                  toynet_forward, train_frame_id, write_checkpoint)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

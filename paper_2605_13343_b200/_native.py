@@ -37,6 +37,22 @@ class ReportC(C.Structure):
                 ("breakdown_iter", u64), ("history_len", u64), ("wall_ms", dbl)]
 
 
+class ToynetConfigC(C.Structure):
+    _fields_ = [(k, u64) for k in ("d", "layers", "heads", "gcn_layers", "d_global",
+                                   "edge_hidden")]
+
+
+class ToynetTraceC(C.Structure):
+    _fields_ = [("max_attention_row_sum_error", dbl), ("highway_max_deviation", dbl),
+                ("leaf_attention_dispatches", u64), ("tile_attention_dispatches", u64),
+                ("ms", dbl)]
+
+
+class FrameViewC(C.Structure):
+    _fields_ = [("n", u64), ("width", u64), ("height", u64), ("cell_order", vp), ("rho", vp),
+                ("rho_heavy", dbl), ("row_offsets", vp), ("col_indices", vp), ("values", vp)]
+
+
 class CudaError(RuntimeError):
     """A CUDA failure inside libhfpg (HFPG_ECUDA)."""
 
@@ -73,6 +89,9 @@ _PROTOS = {
     "hfpg_launch_counts": (C.c_int, [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "hfpg_fast_path": (C.c_int, [vp, C.POINTER(i32)]),
     "hfpg_profile_iteration": (C.c_int, [vp, C.c_uint32, vp]),
+    "hfpg_gemm_tf32": (C.c_int, [u64, u64, u64, vp, vp, vp]),
+    "hfpg_toynet_forward": (C.c_int, [vp, C.POINTER(FrameViewC), u64, u64, C.POINTER(ToynetConfigC),
+                                      u64, vp, i32, C.POINTER(ToynetTraceC)]),
 }
 
 EXPORTED = sorted(_PROTOS)

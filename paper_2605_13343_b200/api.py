@@ -496,6 +496,70 @@ def pcg_solve(A: CsrMatrix, b, precond: PrecondApplier, cfg: SolveConfig | None 
                        wall_ms=float(rep.wall_ms), breakdown_iter=int(rep.breakdown_iter))
 
 
+# ------------------------------------------------------------------------------ toy_net.hpp
+
+
+@dataclass
+class ToynetConfig:
+    """toy_net.hpp:12-19. The GPU forward implements the production width (d = 128, head dim
+    16, i.e. the d128_L3_hw config: layers=3, heads=8)."""
+    d: int = 128
+    layers: int = 3
+    heads: int = 8
+    gcn_layers: int = 2
+    d_global: int = 12
+    edge_hidden: int = 8
+
+
+@dataclass
+class ToynetTrace:
+    """toy_net.hpp:64-74."""
+    leaf_attention_dispatches: int = 0
+    tile_attention_dispatches: int = 0
+    max_attention_row_sum_error: float = 0.0
+    highway_max_deviation: float = 0.0
+    ms: float = 0.0
+
+    def attention_kernel_families(self) -> int:
+        return int(self.leaf_attention_dispatches > 0) + int(self.tile_attention_dispatches > 0)
+
+
+def _frame_view(frame: Frame) -> "N.FrameViewC":
+    A = frame.A
+    v = N.FrameViewC(frame.n, frame.width, frame.height, frame.cell_order.ctypes.data,
+                     frame.rho.ctypes.data, float(frame.rho_heavy), A.row_offsets.ctypes.data,
+                     A.col_indices.ctypes.data, A.values.ctypes.data)
+    v._keep = (frame,)
+    return v
+
+
+def toynet_forward(frame: Frame, partition: HPartition, coarse_size: int,
+                   cfg: ToynetConfig | None = None, weight_seed: int = 0,
+                   trace: ToynetTrace | None = None, device: Device | None = None,
+                   load: bool = False) -> FactorTensor:
+    """toy_net.cpp:170 init_weights(cfg, layout, weight_seed) + :322 forward on the GPU
+    (tcgen05 tf32 GEMMs). With load=True the tensor also becomes `device`'s factor tensor."""
+    cfg = cfg or ToynetConfig()
+    if frame.depth != 1:
+        raise ValueError("toynet: 2D frames only (frame.hpp)")
+    dev = device or Device(0)
+    lay = make_factor_layout(partition, coarse_size)
+    out = np.empty(lay.total, np.float32)
+    c = N.ToynetConfigC(cfg.d, cfg.layers, cfg.heads, cfg.gcn_layers, cfg.d_global, cfg.edge_hidden)
+    tr = N.ToynetTraceC()
+    view = _frame_view(frame)
+    check(lib.hfpg_toynet_forward(dev.h, C.byref(view), partition.leaf_size, coarse_size, C.byref(c),
+                                  weight_seed, out.ctypes.data, int(load),
+                                  C.byref(tr) if trace is not None else None))
+    if trace is not None:
+        trace.max_attention_row_sum_error = tr.max_attention_row_sum_error
+        trace.highway_max_deviation = tr.highway_max_deviation
+        trace.leaf_attention_dispatches = tr.leaf_attention_dispatches
+        trace.tile_attention_dispatches = tr.tile_attention_dispatches
+        trace.ms = tr.ms
+    return FactorTensor(lay, out)
+
+
 # -------------------------------------------------------------------------------- apply.hpp
 
 

@@ -706,6 +706,47 @@ int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out) {
     });
 }
 
+int hfpg_toynet_forward(hfpg_handle* h, const hfpg_frame_view* frame, uint64_t leaf, uint64_t ls,
+                        const hfpg_toynet_config* cfg, uint64_t seed, float* out, int32_t load,
+                        hfpg_toynet_trace* trace) {
+    return guarded([&] {
+        set_device(h);
+        if (!frame || !cfg) throw InvalidArgument("toynet: null frame or config");
+        const Layout L = make_layout(frame->n, leaf, ls);
+        float* dst = nullptr;
+        if (load) {
+            if (h->have_csr && h->n != frame->n) throw InvalidArgument("toynet: length mismatch");
+            invalidate_graph(h);
+            if (!h->have_factors || h->L.total != L.total) dalloc(h->F, L.total);
+            dst = h->F;
+        } else {
+            CK(cudaMalloc(&dst, L.total * 4));
+        }
+        CK(cudaMemsetAsync(dst, 0, L.total * 4, h->stream));
+        try {
+            toynet_forward_device(h->stream, *frame, leaf, ls, *cfg, seed, dst, trace);
+            if (out) CK(cudaMemcpy(out, dst, L.total * 4, cudaMemcpyDeviceToHost));
+        } catch (...) {
+            if (!load) cudaFree(dst);
+            throw;
+        }
+        if (!load) {
+            CK(cudaFree(dst));
+            return;
+        }
+        h->L = L;
+        h->have_factors = true;
+        h->spd_enabled = 0;
+        h->spd_raw = 0.0;
+        h->fast = (L.l == kL && L.ls == kLs && std::getenv("HFPG_FORCE_GENERIC") == nullptr);
+        if (!h->have_csr && !h->have_diag) h->n = frame->n;
+        ensure_workspace(h);
+        const double shift = 0.0;
+        CK(cudaMemcpyAsync(&h->sc->shift, &shift, 8, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
 int hfpg_fast_path(hfpg_handle* h, int32_t* out) {
     return guarded([&] { *out = h->have_factors && h->fast ? 1 : 0; });
 }

@@ -3,6 +3,8 @@
 
 #include "../../include/hfpg.h"
 
+#include <cuda_runtime.h>
+
 #include <cmath>
 #include <cstdint>
 #include <stdexcept>
@@ -101,6 +103,11 @@ struct Csr {
     std::vector<double> vals;
 };
 void init_factors_host(const Layout& L, double sigma, uint64_t seed, uint64_t frame, float* out);
+
+// toynet.cu: the GPU forward into a device buffer of the packed layout.
+void toynet_forward_device(cudaStream_t st, const hfpg_frame_view& fr, uint64_t L, uint64_t Ls,
+                           const hfpg_toynet_config& cfg, uint64_t seed, float* out,
+                           hfpg_toynet_trace* trace);
 
 }  // namespace hfpg
 

@@ -1,0 +1,512 @@
+// Toy-network inference + factor assembly on the GPU (toy_net.cpp:170-586): encoder MLP, D^-1 A
+// graph convolutions, leaf-window and strip-pooled tile attention with edge biases, highway
+// buffers, 4d FFNs and the decoder heads writing the packed factor tensor. Dense contractions
+// run on tcgen05 (kind::tf32, TMEM accumulators, TMA-fed); the rest are fp32 SIMT kernels.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <vector>
+
+#include "gemm_tcgen05.cuh"
+#include "internal.hpp"
+#include "toynet_kernels.cuh"
+
+namespace hfpg {
+
+namespace {
+
+#define TCK(call)                                                                         \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));          \
+    } while (0)
+
+// ---- weights: toy_net.cpp:170-223, drawn in the reference's exact order ---------------------
+struct Mat {
+    uint64_t rows = 0, cols = 0;
+    std::vector<double> v;  // row-major rows x cols (in x out)
+};
+struct HostWeights {
+    Mat enc1, enc2;
+    std::vector<Mat> gcn;
+    struct Layer {
+        Mat wq, wk, wv, wo, ffn1, ffn2;
+    };
+    std::vector<Layer> leaf, tile;
+    Mat le_w1, le_w2, te_w1, te_w2;
+    Mat lh1, lh2, thu, thv, bhu, bhv;
+    std::vector<double> gate;
+};
+
+HostWeights init_weights(const hfpg_toynet_config& c, uint64_t L, uint64_t Ls, uint64_t seed) {
+    if (c.d % c.heads != 0) throw InvalidArgument("toynet: heads must divide embedding width");
+    Rng rng(seed, 0, 5);  // RngPurpose::net_weights
+    auto random_mat = [&](uint64_t rows, uint64_t cols) {  // toy_net.cpp:43-48
+        Mat m;
+        m.rows = rows;
+        m.cols = cols;
+        m.v.resize(rows * cols);
+        const double scale = 1.0 / std::sqrt(static_cast<double>(rows));
+        for (double& x : m.v) x = scale * rng.normal();
+        return m;
+    };
+    const uint64_t d = c.d, feat = 7 + c.d_global;
+    HostWeights w;
+    w.enc1 = random_mat(feat, d);
+    w.enc2 = random_mat(d, d);
+    for (uint64_t g = 0; g < c.gcn_layers; ++g) w.gcn.push_back(random_mat(d, d));
+    for (auto* s : {&w.leaf, &w.tile})
+        for (uint64_t l = 0; l < c.layers; ++l) {
+            HostWeights::Layer x;
+            x.wq = random_mat(d, d);
+            x.wk = random_mat(d, d);
+            x.wv = random_mat(d, d);
+            x.wo = random_mat(d, d);
+            x.ffn1 = random_mat(4 * d, 4 * d);
+            x.ffn2 = random_mat(4 * d, d);
+            s->push_back(std::move(x));
+        }
+    w.le_w1 = random_mat(4, c.edge_hidden);
+    w.le_w2 = random_mat(c.edge_hidden, c.heads);
+    w.te_w1 = random_mat(4, c.edge_hidden);
+    w.te_w2 = random_mat(c.edge_hidden, c.heads);
+    w.lh1 = random_mat(d, d);
+    w.lh2 = random_mat(d, L);
+    w.thu = random_mat(d, Ls / 2);
+    w.thv = random_mat(d, Ls / 2);
+    w.bhu = random_mat(d, Ls);
+    w.bhv = random_mat(d, Ls);
+    w.gate.resize(d);
+    for (double& x : w.gate) x = rng.normal() / std::sqrt(static_cast<double>(d));
+    return w;  // every bias of init_weights is zero
+}
+
+// ---- TMA tensor maps (driver entry point fetched through the runtime) -----------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        TCK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+// fp32 row-major [rows x cols] with row pitch ld (elements); box = box_rows x 32, SWIZZLE_128B.
+CUtensorMap tmap(const float* p, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {ld * 4};
+    cuuint32_t box[2] = {32, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p), dims,
+                                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return m;
+}
+
+// ---- GEMM epilogues ---------------------------------------------------------------------------
+struct EpiStore {  // out[row, col] = act(v + bias)
+    float* out;
+    uint32_t ld, n;
+    const float* bias;
+    int gelu;
+    __device__ void operator()(int row, int col0, float (&v)[16]) const {
+        float* o = out + uint64_t(row) * ld + col0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (col0 + j < int(n)) {
+                float x = v[j] + (bias ? bias[col0 + j] : 0.f);
+                o[j] = gelu ? gelu_f(x) : x;
+            }
+    }
+};
+struct EpiResidual {  // out[row, col] += act(v + bias)
+    float* out;
+    uint32_t ld, n;
+    const float* bias;
+    int gelu;
+    __device__ void operator()(int row, int col0, float (&v)[16]) const {
+        float* o = out + uint64_t(row) * ld + col0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (col0 + j < int(n)) {
+                float x = v[j] + (bias ? bias[col0 + j] : 0.f);
+                o[j] += gelu ? gelu_f(x) : x;
+            }
+    }
+};
+// Decoder heads of leaf node `row` (toy_net.cpp:549-567): columns [0, L_s) -> Ũ_k row,
+// [L_s, 2 L_s) -> Ṽ_k row, 2 L_s -> gate. Cast to float as the reference does.
+struct EpiLeafHeads {
+    float* out;
+    uint64_t L, Ls, bridge_base, gate_base;
+    const float* bias;  // 2 Ls + 1
+    __device__ void operator()(int row, int col0, float (&v)[16]) const {
+        const uint64_t k = uint64_t(row) / L, r = uint64_t(row) % L;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint64_t c = uint64_t(col0 + j);
+            const float x = v[j] + (bias && c <= 2 * Ls ? bias[c] : 0.f);
+            if (c < Ls) out[bridge_base + k * 2 * L * Ls + r * Ls + c] = x;
+            else if (c < 2 * Ls) out[bridge_base + k * 2 * L * Ls + L * Ls + r * Ls + (c - Ls)] = x;
+            else if (c == 2 * Ls) out[gate_base + uint64_t(row)] = x;
+        }
+    }
+};
+// Tile heads of tile token `row` = m L_s + tok (toy_net.cpp:570-584): [0, rk) -> U_m[tok],
+// [rk, 2 rk) -> V_m[tok].
+struct EpiTileHeads {
+    float* out;
+    uint64_t Ls, rk, tile_base;
+    const float* bias;
+    __device__ void operator()(int row, int col0, float (&v)[16]) const {
+        const uint64_t m = uint64_t(row) / Ls, tok = uint64_t(row) % Ls;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint64_t c = uint64_t(col0 + j);
+            if (c >= 2 * rk) continue;
+            const float x = v[j] + (bias ? bias[c] : 0.f);
+            out[tile_base + m * Ls * Ls + (c < rk ? 0 : Ls * rk) + tok * rk + (c % rk)] = x;
+        }
+    }
+};
+
+template <int BN, class Epi>
+void gemm(cudaStream_t st, const float* A, uint64_t M, uint64_t K, uint64_t lda, const float* Bt,
+          uint64_t N, uint64_t ldb, const Epi& epi) {
+    static bool configured = false;
+    if (!configured) {
+        TCK(cudaFuncSetAttribute(k_gemm_tf32<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(gemm_smem_bytes<BN>())));
+        configured = true;
+    }
+    if (M == 0 || N == 0) return;
+    const CUtensorMap ta = tmap(A, M, K, lda, kGemmBM), tb = tmap(Bt, N, K, ldb, BN);
+    dim3 grid(unsigned((M + kGemmBM - 1) / kGemmBM), unsigned((N + BN - 1) / BN));
+    k_gemm_tf32<BN, Epi><<<grid, kGemmThreads, gemm_smem_bytes<BN>(), st>>>(ta, tb, int(M), int(N), int(K), epi);
+    TCK(cudaGetLastError());
+}
+
+// Device copy of W^T (out x in, fp32), optionally padding the input dimension to kpad.
+float* upload_t(const Mat& m, std::vector<float*>& owned, uint64_t kpad = 0) {
+    const uint64_t kp = std::max(kpad, m.rows);
+    std::vector<float> t(m.cols * kp, 0.f);
+    for (uint64_t i = 0; i < m.rows; ++i)
+        for (uint64_t o = 0; o < m.cols; ++o) t[o * kp + i] = float(m.v[i * m.cols + o]);
+    float* p = nullptr;
+    TCK(cudaMalloc(&p, t.size() * 4));
+    TCK(cudaMemcpy(p, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+    owned.push_back(p);
+    return p;
+}
+// [W_a | W_b | ...]^T stacked along the output dimension (same input dimension).
+float* upload_stack_t(std::vector<const Mat*> ms, std::vector<float*>& owned, uint64_t extra_rows = 0,
+                      const std::vector<double>* gate = nullptr) {
+    const uint64_t kin = ms[0]->rows;
+    uint64_t nout = extra_rows;
+    for (auto* m : ms) nout += m->cols;
+    std::vector<float> t(nout * kin, 0.f);
+    uint64_t o0 = 0;
+    for (auto* m : ms) {
+        for (uint64_t i = 0; i < m->rows; ++i)
+            for (uint64_t o = 0; o < m->cols; ++o) t[(o0 + o) * kin + i] = float(m->v[i * m->cols + o]);
+        o0 += m->cols;
+    }
+    if (gate)
+        for (uint64_t i = 0; i < kin; ++i) t[o0 * kin + i] = float((*gate)[i]);
+    float* p = nullptr;
+    TCK(cudaMalloc(&p, t.size() * 4));
+    TCK(cudaMemcpy(p, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+    owned.push_back(p);
+    return p;
+}
+
+template <class T>
+T* dnew(uint64_t count, std::vector<void*>& owned) {
+    T* p = nullptr;
+    TCK(cudaMalloc(&p, std::max<uint64_t>(count, 1) * sizeof(T)));
+    owned.push_back(p);
+    return p;
+}
+
+EdgeMlp edge_params(const Mat& w1, const Mat& w2) {
+    EdgeMlp e{};
+    for (uint64_t i = 0; i < w1.v.size(); ++i) e.w1[i] = float(w1.v[i]);
+    for (uint64_t i = 0; i < w2.v.size(); ++i) e.w2[i] = float(w2.v[i]);
+    return e;
+}
+
+}  // namespace
+
+// Full forward: writes the packed factor tensor (device pointer out, layout of (n, L, Ls)).
+void toynet_forward_device(cudaStream_t st, const hfpg_frame_view& fr, uint64_t L, uint64_t Ls,
+                           const hfpg_toynet_config& cfg, uint64_t seed, float* out,
+                           hfpg_toynet_trace* trace) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const Layout lay = make_layout(fr.n, L, Ls);
+    const uint64_t n = fr.n, d = cfg.d;
+    if (d != 128) throw InvalidArgument("toynet (gpu): embedding width must be 128");
+    if (cfg.heads * 16 != d) throw InvalidArgument("toynet (gpu): head dimension must be 16");
+    if (cfg.edge_hidden > 8 || cfg.heads > 8 || cfg.d_global > 12)
+        throw InvalidArgument("toynet (gpu): edge_hidden, heads <= 8 and d_global <= 12");
+    if (!(L == 128 && (Ls == 32 || Ls == 16 || Ls == 8)) && !(L == 64 || L == 32 || L == 16 || L == 8 || L == 4))
+        throw InvalidArgument("toynet (gpu): unsupported leaf size");
+    const HostWeights w = init_weights(cfg, L, Ls, seed);
+
+    // ---- glob stats on the host, f64 in the reference's order (toy_net.cpp:232-268) --------
+    std::vector<double> diag(n, 0.0);
+    double rho_mean = 0.0, rho_var = 0.0, dmean = 0.0, offmean = 0.0;
+    uint64_t off = 0;
+    for (uint64_t i = 0; i < n; ++i)
+        for (uint64_t p = fr.row_offsets[i]; p < fr.row_offsets[i + 1]; ++p)
+            if (fr.col_indices[p] == i) diag[i] = fr.values[p];
+    for (uint64_t i = 0; i < n; ++i) rho_mean += fr.rho[i];
+    rho_mean /= double(n);
+    for (uint64_t i = 0; i < n; ++i) rho_var += (fr.rho[i] - rho_mean) * (fr.rho[i] - rho_mean);
+    rho_var /= double(n);
+    double dmin = diag[0], dmax = diag[0];
+    for (uint64_t i = 0; i < n; ++i) {
+        dmean += diag[i];
+        dmin = std::min(dmin, diag[i]);
+        dmax = std::max(dmax, diag[i]);
+        for (uint64_t p = fr.row_offsets[i]; p < fr.row_offsets[i + 1]; ++p)
+            if (fr.col_indices[p] != i) {
+                offmean += std::fabs(fr.values[p]);
+                ++off;
+            }
+    }
+    dmean /= double(n);
+    if (off) offmean /= double(off);
+    const double stats[12] = {std::log(double(n)), rho_mean, std::sqrt(rho_var),
+                              std::log(std::max(fr.rho_heavy, 1.0)), dmean, dmax, dmin, offmean,
+                              double(fr.row_offsets[n]) / double(n),
+                              double(fr.width) / double(fr.height), dmax / std::max(dmin, 1e-30), 1.0};
+    std::vector<float> glob(std::max<uint64_t>(cfg.d_global, 1), 0.f);
+    for (uint64_t i = 0; i < cfg.d_global && i < 12; ++i) glob[i] = float(stats[i]);
+
+    std::vector<void*> buf;
+    std::vector<float*> wbuf;
+    struct Cleanup {
+        std::vector<void*>& a;
+        std::vector<float*>& b;
+        ~Cleanup() {
+            for (void* p : a) cudaFree(p);
+            for (float* p : b) cudaFree(p);
+        }
+    } cleanup{buf, wbuf};
+
+    TnDims g{};
+    g.n = n;
+    g.L = L;
+    g.Ls = Ls;
+    g.rk = Ls / 2;
+    g.K = lay.k;
+    g.M = lay.m;
+    g.D = lay.depth;
+    g.width = uint32_t(fr.width);
+    g.height = uint32_t(fr.height);
+    g.d = uint32_t(d);
+    g.heads = uint32_t(cfg.heads);
+    g.dglob = uint32_t(cfg.d_global);
+    g.eh = uint32_t(cfg.edge_hidden);
+    g.feat_pad = 32;
+    const uint64_t nnz = fr.row_offsets[n], MT = lay.m * Ls;  // tile tokens
+
+    // ---- inputs ------------------------------------------------------------------------------
+    auto* d_order = dnew<uint32_t>(n, buf);
+    auto* d_rho = dnew<double>(n, buf);
+    auto* d_ro = dnew<unsigned long long>(n + 1, buf);
+    auto* d_ci = dnew<uint32_t>(nnz, buf);
+    auto* d_v = dnew<double>(nnz, buf);
+    auto* d_diag = dnew<double>(n, buf);
+    auto* d_glob = dnew<float>(glob.size(), buf);
+    TCK(cudaMemcpyAsync(d_order, fr.cell_order, n * 4, cudaMemcpyHostToDevice, st));
+    TCK(cudaMemcpyAsync(d_rho, fr.rho, n * 8, cudaMemcpyHostToDevice, st));
+    TCK(cudaMemcpyAsync(d_ro, fr.row_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+    TCK(cudaMemcpyAsync(d_ci, fr.col_indices, nnz * 4, cudaMemcpyHostToDevice, st));
+    TCK(cudaMemcpyAsync(d_v, fr.values, nnz * 8, cudaMemcpyHostToDevice, st));
+    TCK(cudaMemcpyAsync(d_diag, diag.data(), n * 8, cudaMemcpyHostToDevice, st));
+    TCK(cudaMemcpyAsync(d_glob, glob.data(), glob.size() * 4, cudaMemcpyHostToDevice, st));
+
+    // ---- weights (W^T, fp32) -------------------------------------------------------------------
+    float* w_enc1 = upload_t(w.enc1, wbuf, g.feat_pad);
+    float* w_enc2 = upload_t(w.enc2, wbuf);
+    std::vector<float*> w_gcn;
+    for (auto& m : w.gcn) w_gcn.push_back(upload_t(m, wbuf));
+    struct LW {
+        float *qkv, *wo, *f1, *f2;
+    };
+    std::vector<LW> wl, wt;
+    for (auto* src : {&w.leaf, &w.tile})
+        for (auto& x : *src) {
+            LW l{upload_stack_t({&x.wq, &x.wk, &x.wv}, wbuf), upload_t(x.wo, wbuf), upload_t(x.ffn1, wbuf),
+                 upload_t(x.ffn2, wbuf)};
+            (src == &w.leaf ? wl : wt).push_back(l);
+        }
+    float* w_lh1 = upload_t(w.lh1, wbuf);
+    float* w_lh2 = upload_t(w.lh2, wbuf);
+    float* w_heads = upload_stack_t({&w.bhu, &w.bhv}, wbuf, 1, &w.gate);  // (2 Ls + 1) x d
+    float* w_theads = upload_stack_t({&w.thu, &w.thv}, wbuf);             // Ls x d
+
+    // ---- activations -------------------------------------------------------------------------
+    auto* feat = dnew<float>(n * g.feat_pad, buf);
+    auto* x = dnew<float>(n * d, buf);       // embedding -> leaf tokens
+    auto* h1 = dnew<float>(n * d, buf);      // encoder hidden / gcn message / decoder hidden
+    auto* tile_tok = dnew<float>(MT * d, buf);
+    auto* ln = dnew<float>(std::max(n, MT) * d, buf);
+    auto* qkv = dnew<float>(std::max(n, MT) * 3 * d, buf);
+    auto* hout = dnew<float>(std::max(n, MT) * d, buf);
+    auto* row_hw = dnew<float>(n * d, buf);
+    auto* col_hw = dnew<float>(n * d, buf);
+    auto* Af = dnew<float>(std::max(n, MT) * 4 * d, buf);
+    auto* Hf = dnew<float>(std::max(n, MT) * 4 * d, buf);
+    auto* glob_hw = dnew<float>(d, buf);
+    const uint32_t nparts = 296;
+    auto* partial = dnew<float>(uint64_t(nparts) * 2 * d, buf);
+    auto* leaf_bias = dnew<float>(lay.k * cfg.heads * L * L, buf);
+    auto* tile_bias = dnew<float>(lay.m * cfg.heads * Ls * Ls, buf);
+    unsigned int* rowsum_bits = trace ? dnew<unsigned int>(1, buf) : nullptr;
+    if (rowsum_bits) TCK(cudaMemsetAsync(rowsum_bits, 0, 4, st));
+
+    const unsigned nb = unsigned((n + 255) / 256), nw = unsigned((n * 32 + 255) / 256);
+    // ---- encoder (toy_net.cpp:295-318) -----------------------------------------------------
+    k_tn_features<<<nb, 256, 0, st>>>(g, d_order, d_rho, d_ro, d_ci, d_glob, feat);
+    gemm<128>(st, feat, n, g.feat_pad, g.feat_pad, w_enc1, d, g.feat_pad, EpiStore{h1, uint32_t(d), uint32_t(d), nullptr, 1});
+    gemm<128>(st, h1, n, d, d, w_enc2, d, d, EpiStore{x, uint32_t(d), uint32_t(d), nullptr, 0});
+    for (float* wg : w_gcn) {
+        k_tn_gcn_msg<<<nw, 256, 0, st>>>(g, d_ro, d_ci, d_v, d_diag, x, h1);
+        gemm<128>(st, h1, n, d, d, wg, d, d, EpiResidual{x, uint32_t(d), uint32_t(d), nullptr, 1});
+    }
+    TCK(cudaGetLastError());
+    // ---- tile tokens, edge biases ------------------------------------------------------------
+    if (lay.m) k_tn_tile_pool<<<dim3(unsigned(lay.m), unsigned(Ls)), 128, 0, st>>>(g, x, tile_tok);
+    k_tn_leaf_bias<<<dim3(unsigned((L * L + 255) / 256), unsigned(lay.k)), 256, 0, st>>>(
+        g, d_order, d_ro, d_ci, d_v, edge_params(w.le_w1, w.le_w2), leaf_bias);
+    if (lay.m)
+        k_tn_tile_bias<<<dim3(unsigned(lay.m), unsigned(Ls)), 64, 0, st>>>(
+            g, d_order, d_ro, d_ci, d_v, edge_params(w.te_w1, w.te_w2), tile_bias);
+    TCK(cudaGetLastError());
+
+    std::vector<double> hw_dev;
+    auto attention = [&](float* tok, uint64_t rows, uint64_t T, const LW& lw, const float* bias) {
+        k_tn_layernorm<<<unsigned((rows * 32 + 255) / 256), 256, 0, st>>>(rows, uint32_t(d), tok, ln, uint32_t(d));
+        gemm<128>(st, ln, rows, d, d, lw.qkv, 3 * d, d, EpiStore{qkv, uint32_t(3 * d), uint32_t(3 * d), nullptr, 0});
+        const dim3 grid(unsigned(rows / T), unsigned(cfg.heads));
+        switch (T) {
+            case 128: k_tn_attention<128><<<grid, 128, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
+            case 64: k_tn_attention<64><<<grid, 64, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
+            case 32: k_tn_attention<32><<<grid, 32, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
+            case 16: k_tn_attention<16><<<grid, 16, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
+            case 8: k_tn_attention<8><<<grid, 8, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
+            case 4: k_tn_attention<4><<<grid, 4, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
+            default: throw InvalidArgument("toynet (gpu): unsupported attention window");
+        }
+        TCK(cudaGetLastError());
+        gemm<128>(st, hout, rows, d, d, lw.wo, d, d, EpiResidual{tok, uint32_t(d), uint32_t(d), nullptr, 0});
+    };
+    auto ffn = [&](float* tok, uint64_t rows, const LW& lw, bool leaf) {
+        k_tn_layernorm<<<unsigned((rows * 32 + 255) / 256), 256, 0, st>>>(rows, uint32_t(d), tok, Af, uint32_t(4 * d));
+        if (leaf)
+            k_tn_ffn_input_leaf<<<unsigned((rows * 32 + 255) / 256), 256, 0, st>>>(g, row_hw, col_hw, glob_hw, Af);
+        else
+            k_tn_ffn_input_tile<<<dim3(unsigned(lay.m), unsigned(Ls)), 128, 0, st>>>(g, row_hw, col_hw, glob_hw, Af);
+        TCK(cudaGetLastError());
+        gemm<128>(st, Af, rows, 4 * d, 4 * d, lw.f1, 4 * d, 4 * d, EpiStore{Hf, uint32_t(4 * d), uint32_t(4 * d), nullptr, 1});
+        gemm<128>(st, Hf, rows, 4 * d, 4 * d, lw.f2, d, 4 * d, EpiResidual{tok, uint32_t(d), uint32_t(d), nullptr, 0});
+    };
+
+    for (uint64_t layer = 0; layer < cfg.layers; ++layer) {
+        attention(x, n, L, wl[layer], leaf_bias);
+        if (lay.m) attention(tile_tok, MT, Ls, wt[layer], tile_bias);
+        k_tn_highway<<<nw, 256, 0, st>>>(g, x, tile_tok, row_hw, col_hw);
+        k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(n, uint32_t(d), x, partial);
+        k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(MT, uint32_t(d), tile_tok, partial + nparts * d);
+        k_tn_colsum_finish<<<1, unsigned(d), 0, st>>>(2 * nparts, uint32_t(d), partial, glob_hw);
+        TCK(cudaGetLastError());
+        if (trace) {  // highway conservation audit (toy_net.cpp:478-512), host-side f64
+            std::vector<float> lt(n * d), tt(MT * d), rh(n * d), ch(n * d), gh(d);
+            TCK(cudaMemcpyAsync(lt.data(), x, n * d * 4, cudaMemcpyDeviceToHost, st));
+            TCK(cudaMemcpyAsync(tt.data(), tile_tok, MT * d * 4, cudaMemcpyDeviceToHost, st));
+            TCK(cudaMemcpyAsync(rh.data(), row_hw, n * d * 4, cudaMemcpyDeviceToHost, st));
+            TCK(cudaMemcpyAsync(ch.data(), col_hw, n * d * 4, cudaMemcpyDeviceToHost, st));
+            TCK(cudaMemcpyAsync(gh.data(), glob_hw, d * 4, cudaMemcpyDeviceToHost, st));
+            TCK(cudaStreamSynchronize(st));
+            double dev = 0.0, scale = 0.0;
+            for (uint64_t c = 0; c < d; ++c) {
+                double er = 0, ec = 0, eg = 0, gr = 0, gc = 0;
+                for (uint64_t i = 0; i < n; ++i) {
+                    er += lt[i * d + c];
+                    gr += rh[i * d + c];
+                    gc += ch[i * d + c];
+                }
+                ec = eg = er;
+                for (uint64_t m = 0; m < lay.m; ++m) {
+                    int dd = 0;
+                    while ((2ULL << dd) <= m + 1) ++dd;
+                    const double chunk = double((lay.k >> dd) / 2 * L / Ls);
+                    for (uint64_t tok = 0; tok < Ls; ++tok) {
+                        const double e = tt[(m * Ls + tok) * d + c];
+                        er += e * chunk;
+                        ec += e * chunk;
+                        eg += e;
+                    }
+                }
+                dev = std::max({dev, std::fabs(gr - er), std::fabs(gc - ec), std::fabs(double(gh[c]) - eg)});
+                scale = std::max({scale, std::fabs(er), std::fabs(ec), std::fabs(eg), 1.0});
+            }
+            hw_dev.push_back(dev / scale);
+        }
+        ffn(x, n, wl[layer], true);
+        if (lay.m) ffn(tile_tok, MT, wt[layer], false);
+    }
+
+    // ---- decoder heads into the packed layout (toy_net.cpp:540-585) ------------------------
+    gemm<128>(st, x, n, d, d, w_lh1, d, d, EpiStore{h1, uint32_t(d), uint32_t(d), nullptr, 1});
+    // F_k rows: leaf_factor(k) + r L = (k L + r) L = i L -> a row-major [n x L] section
+    gemm<128>(st, h1, n, d, d, w_lh2, L, d, EpiStore{out, uint32_t(L), uint32_t(L), nullptr, 0});
+    gemm<80>(st, x, n, d, d, w_heads, 2 * Ls + 1, d,
+             EpiLeafHeads{out, L, Ls, lay.bridge_base, lay.gate_base, nullptr});
+    if (lay.m) gemm<32>(st, tile_tok, MT, d, d, w_theads, Ls, d, EpiTileHeads{out, Ls, Ls / 2, lay.tile_base, nullptr});
+    TCK(cudaStreamSynchronize(st));
+
+    if (trace) {
+        unsigned int bits = 0;
+        TCK(cudaMemcpy(&bits, rowsum_bits, 4, cudaMemcpyDeviceToHost));
+        float e;
+        std::memcpy(&e, &bits, 4);
+        trace->max_attention_row_sum_error = e;
+        trace->highway_max_deviation = hw_dev.empty() ? 0.0 : *std::max_element(hw_dev.begin(), hw_dev.end());
+        trace->leaf_attention_dispatches = cfg.layers;
+        trace->tile_attention_dispatches = lay.m ? cfg.layers : 0;
+        trace->ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+}
+
+}  // namespace hfpg
+
+extern "C" int hfpg_gemm_tf32(uint64_t M, uint64_t N, uint64_t K, const float* A, const float* Bt,
+                              float* C) {
+    using namespace hfpg;
+    return guarded([&] {
+        if (K % 4) throw InvalidArgument("gemm: K must be a multiple of 4 (16-byte rows)");
+        float *dA = nullptr, *dB = nullptr, *dC = nullptr;
+        TCK(cudaMalloc(&dA, std::max<uint64_t>(M * K, 1) * 4));
+        TCK(cudaMalloc(&dB, std::max<uint64_t>(N * K, 1) * 4));
+        TCK(cudaMalloc(&dC, std::max<uint64_t>(M * N, 1) * 4));
+        TCK(cudaMemcpy(dA, A, M * K * 4, cudaMemcpyHostToDevice));
+        TCK(cudaMemcpy(dB, Bt, N * K * 4, cudaMemcpyHostToDevice));
+        gemm<128>(0, dA, M, K, K, dB, N, K, EpiStore{dC, uint32_t(N), uint32_t(N), nullptr, 0});
+        TCK(cudaDeviceSynchronize());
+        TCK(cudaMemcpy(C, dC, M * N * 4, cudaMemcpyDeviceToHost));
+        cudaFree(dA);
+        cudaFree(dB);
+        cudaFree(dC);
+    });
+}

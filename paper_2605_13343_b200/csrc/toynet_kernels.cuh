@@ -1,0 +1,342 @@
+// Toy-network inference kernels (toy_net.cpp:225-586) other than the tcgen05 GEMMs:
+// features, D^-1 A graph aggregation, layer norm, edge-bias MLP, windowed attention,
+// strip pooling, highway scatter / chunk means, FFN input assembly. fp32 activations.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace hfpg {
+
+struct TnDims {
+    uint64_t n, L, Ls, rk, K, M, D;  // nodes, leaf, coarse, rank, leaves, tiles, log2 K
+    uint32_t width, height, d, heads, dglob, eh, feat_pad;
+};
+
+__device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
+
+// Tile heap index m -> (span in leaves, row0 node, col0 node, chunk rows per token)
+struct TileGeom {
+    uint64_t span, row0, col0, chunk;
+};
+__device__ __forceinline__ TileGeom tile_geom(const TnDims& g, uint64_t m) {
+    int d = 0;
+    while ((2ULL << d) <= m + 1) ++d;
+    const uint64_t i = m + 1 - (1ULL << d), width = g.K >> d, span = width / 2;
+    TileGeom t;
+    t.span = span;
+    t.row0 = i * width * g.L;
+    t.col0 = (i * width + span) * g.L;
+    t.chunk = span * g.L / g.Ls;
+    return t;
+}
+
+// toy_net.cpp:270-293 per-node features [rho, x^, y^, 4 absent-neighbour flags, glob]; the
+// flags come from the operator's off-diagonal pattern (a present neighbour always couples).
+__global__ void k_tn_features(TnDims g, const uint32_t* order, const double* rho,
+                              const unsigned long long* ro, const uint32_t* ci, const float* glob,
+                              float* feat) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= g.n) return;
+    const uint32_t id = order[i], x = id % g.width, y = id / g.width;
+    float* f = feat + i * g.feat_pad;
+    bool present[4] = {false, false, false, false};
+    for (unsigned long long p = ro[i]; p < ro[i + 1]; ++p) {
+        const uint32_t j = ci[p];
+        if (j == i) continue;
+        const uint32_t jd = order[j], xj = jd % g.width, yj = jd / g.width;
+        if (xj + 1 == x && yj == y) present[0] = true;
+        if (xj == x + 1 && yj == y) present[1] = true;
+        if (xj == x && yj + 1 == y) present[2] = true;
+        if (xj == x && yj == y + 1) present[3] = true;
+    }
+    f[0] = float(rho[i]);
+    f[1] = float((double(x) + 0.5) / double(g.width));
+    f[2] = float((double(y) + 0.5) / double(g.height));
+    for (int b = 0; b < 4; ++b) f[3 + b] = present[b] ? 0.f : 1.f;
+    for (uint32_t q = 0; q < g.dglob; ++q) f[7 + q] = glob[q];
+    for (uint32_t q = 7 + g.dglob; q < g.feat_pad; ++q) f[q] = 0.f;
+}
+
+// toy_net.cpp:305-313 msg_i = sum_p (A_ip / A_ii) x_j: one warp per row, lane owns 4 channels
+// (d = 128). f64 weights, fp32 accumulation of the channel sums.
+__global__ void k_tn_gcn_msg(TnDims g, const unsigned long long* ro, const uint32_t* ci,
+                             const double* v, const double* diag, const float* x, float* msg) {
+    const uint64_t row = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= g.n) return;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (unsigned long long p = ro[row]; p < ro[row + 1]; ++p) {
+        const float w = float(v[p] / diag[row]);
+        const float4 xj = reinterpret_cast<const float4*>(x + uint64_t(ci[p]) * g.d)[lane];
+        acc.x = fmaf(w, xj.x, acc.x);
+        acc.y = fmaf(w, xj.y, acc.y);
+        acc.z = fmaf(w, xj.z, acc.z);
+        acc.w = fmaf(w, xj.w, acc.w);
+    }
+    reinterpret_cast<float4*>(msg + row * g.d)[lane] = acc;
+}
+
+// toy_net.cpp:28-41 layer norm without affine, eps 1e-5, two-pass (mean, then centred
+// variance) so huge token magnitudes stay accurate. One warp per row of d = 128.
+// out may be a wider matrix (row stride ld_out).
+__global__ void k_tn_layernorm(uint64_t rows, uint32_t d, const float* x, float* out, uint32_t ld_out) {
+    const uint64_t row = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const float4 v = reinterpret_cast<const float4*>(x + row * d)[lane];
+    float s = (v.x + v.y) + (v.z + v.w);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mean = s / float(d);
+    const float a = v.x - mean, b = v.y - mean, c = v.z - mean, e = v.w - mean;
+    float q = (a * a + b * b) + (c * c + e * e);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    const float inv = 1.f / sqrtf(q / float(d) + 1e-5f);
+    reinterpret_cast<float4*>(out + row * ld_out)[lane] = make_float4(a * inv, b * inv, c * inv, e * inv);
+}
+
+// toy_net.cpp:55-74 edge-bias MLP [dx, dy, dist, c] -> GELU(8) -> heads.
+struct EdgeMlp {
+    float w1[4 * 8], b1[8], w2[8 * 8], b2[8];
+};
+__device__ __forceinline__ void edge_mlp(const EdgeMlp& m, uint32_t eh, uint32_t heads, float dx,
+                                         float dy, float dist, float c, float* out) {
+    float hid[8];
+    for (uint32_t k = 0; k < eh; ++k) {
+        float a = m.b1[k];
+        a = fmaf(dx, m.w1[0 * eh + k], a);
+        a = fmaf(dy, m.w1[1 * eh + k], a);
+        a = fmaf(dist, m.w1[2 * eh + k], a);
+        a = fmaf(c, m.w1[3 * eh + k], a);
+        hid[k] = gelu_f(a);
+    }
+    for (uint32_t h = 0; h < heads; ++h) {
+        float a = m.b2[h];
+        for (uint32_t k = 0; k < eh; ++k) a = fmaf(hid[k], m.w2[k * heads + h], a);
+        out[h] = a;
+    }
+}
+
+// Leaf-pair edge biases (toy_net.cpp:371-381): bias[k][h][i][j], once per forward (reused by
+// every layer). Coupling = A_{base+i, base+j} looked up in the sorted CSR row.
+__global__ void k_tn_leaf_bias(TnDims g, const uint32_t* order, const unsigned long long* ro,
+                               const uint32_t* ci, const double* v, EdgeMlp mlp, float* bias) {
+    const uint64_t k = blockIdx.y;
+    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // i * L + j
+    if (idx >= g.L * g.L) return;
+    const uint64_t i = idx / g.L, j = idx % g.L, base = k * g.L;
+    const uint32_t a = order[base + i], b = order[base + j];
+    const double xa = (double(a % g.width) + 0.5) / double(g.width), ya = (double(a / g.width) + 0.5) / double(g.height);
+    const double xb = (double(b % g.width) + 0.5) / double(g.width), yb = (double(b / g.width) + 0.5) / double(g.height);
+    const double dx = xa - xb, dy = ya - yb, dist = sqrt(dx * dx + dy * dy);
+    double c = 0.0;
+    for (unsigned long long p = ro[base + i]; p < ro[base + i + 1]; ++p)
+        if (ci[p] == base + j) c = v[p];
+    float out[8];
+    edge_mlp(mlp, g.eh, g.heads, float(dx), float(dy), float(dist), float(c), out);
+    for (uint32_t h = 0; h < g.heads; ++h) bias[((k * g.heads + h) * g.L + i) * g.L + j] = out[h];
+}
+
+// Tile-pair edge biases (toy_net.cpp:382-414): chunk-mean positions and the mean coupling over
+// each (row chunk a, column chunk b) pair. One CTA per (tile, a); the a-chunk's CSR rows are
+// scanned once and their column-band entries binned by b.
+__global__ void k_tn_tile_bias(TnDims g, const uint32_t* order, const unsigned long long* ro,
+                               const uint32_t* ci, const double* v, EdgeMlp mlp, float* bias) {
+    const uint64_t m = blockIdx.x, a = blockIdx.y;
+    const TileGeom t = tile_geom(g, m);
+    __shared__ double coup[64], cxs[64], cys[64];
+    __shared__ double rx, ry;
+    const int tid = threadIdx.x;
+    auto xn = [&](uint64_t node) {
+        const uint32_t id = order[node];
+        return (double(id % g.width) + 0.5) / double(g.width);
+    };
+    auto yn = [&](uint64_t node) {
+        const uint32_t id = order[node];
+        return (double(id / g.width) + 0.5) / double(g.height);
+    };
+    if (tid < g.Ls) {
+        coup[tid] = 0.0;
+        double sx = 0.0, sy = 0.0;
+        for (uint64_t s = 0; s < t.chunk; ++s) {  // column-chunk position sums, s ascending
+            sx += xn(t.col0 + tid * t.chunk + s);
+            sy += yn(t.col0 + tid * t.chunk + s);
+        }
+        cxs[tid] = sx;
+        cys[tid] = sy;
+    }
+    if (tid == 0) {
+        double sx = 0.0, sy = 0.0;
+        for (uint64_t s = 0; s < t.chunk; ++s) {
+            sx += xn(t.row0 + a * t.chunk + s);
+            sy += yn(t.row0 + a * t.chunk + s);
+        }
+        rx = sx;
+        ry = sy;
+    }
+    __syncthreads();
+    if (tid == 0) {  // sparse coupling sums, in the reference's (s, p) order per bin
+        const uint64_t cbase = t.col0, cend = t.col0 + g.Ls * t.chunk;
+        for (uint64_t s = 0; s < t.chunk; ++s) {
+            const uint64_t r = t.row0 + a * t.chunk + s;
+            for (unsigned long long p = ro[r]; p < ro[r + 1]; ++p)
+                if (ci[p] >= cbase && ci[p] < cend) coup[(ci[p] - cbase) / t.chunk] += v[p];
+        }
+    }
+    __syncthreads();
+    if (tid < g.Ls) {
+        const double ch = double(t.chunk);
+        const double dx = (rx - cxs[tid]) / ch, dy = (ry - cys[tid]) / ch;
+        const double dist = sqrt(dx * dx + dy * dy), c = coup[tid] / (ch * ch);
+        float out[8];
+        edge_mlp(mlp, g.eh, g.heads, float(dx), float(dy), float(dist), float(c), out);
+        for (uint32_t h = 0; h < g.heads; ++h)
+            bias[((m * g.heads + h) * g.Ls + a) * g.Ls + tid] = out[h];
+    }
+}
+
+// toy_net.cpp:348-365 tile tokens: mean over each token's chunk of (row_emb + col_emb) / 2.
+__global__ void k_tn_tile_pool(TnDims g, const float* emb, float* tile_tok) {
+    const uint64_t m = blockIdx.x, tok = blockIdx.y;
+    const TileGeom t = tile_geom(g, m);
+    for (uint32_t c = threadIdx.x; c < g.d; c += blockDim.x) {
+        float s = 0.f;
+        for (uint64_t q = 0; q < t.chunk; ++q)
+            s += 0.5f * (emb[(t.row0 + tok * t.chunk + q) * g.d + c] + emb[(t.col0 + tok * t.chunk + q) * g.d + c]);
+        tile_tok[(m * g.Ls + tok) * g.d + c] = s / float(t.chunk);
+    }
+}
+
+// Windowed multi-head attention core (toy_net.cpp:78-125) for one (block, head): T tokens,
+// head dim 16. qkv rows hold [q | k | v] (3d wide). One thread per query row; K/V of the block
+// head staged in shared memory; softmax in fp32 with max subtraction. Writes head_out[row, h*16..].
+// Also tracks max |row sum - 1| (trace).
+template <int T>
+__global__ void __launch_bounds__(T) k_tn_attention(uint32_t d, uint32_t heads, const float* qkv,
+                                                    const float* bias, float* head_out,
+                                                    unsigned int* rowsum_err_bits) {
+    const uint64_t blk = blockIdx.x;
+    const uint32_t h = blockIdx.y, i = threadIdx.x;
+    constexpr int HD = 16;
+    __shared__ float ks[T][HD + 1], vs[T][HD + 1];
+    const float* rowp = qkv + (blk * T + i) * 3 * d;
+    float q[HD];
+#pragma unroll
+    for (int c = 0; c < HD; ++c) {
+        q[c] = rowp[h * HD + c];
+        ks[i][c] = rowp[d + h * HD + c];
+        vs[i][c] = rowp[2 * d + h * HD + c];
+    }
+    __syncthreads();
+    const float* b = bias + ((blk * heads + h) * T + i) * T;
+    const float scale = 0.25f;  // 1/sqrt(16)
+    float mx = -CUDART_INF_F;
+    for (int j = 0; j < T; ++j) {
+        float dot = 0.f;
+#pragma unroll
+        for (int c = 0; c < HD; ++c) dot = fmaf(q[c], ks[j][c], dot);
+        mx = fmaxf(mx, fmaf(dot, scale, b[j]));
+    }
+    float sum = 0.f, acc[HD];
+#pragma unroll
+    for (int c = 0; c < HD; ++c) acc[c] = 0.f;
+    for (int j = 0; j < T; ++j) {
+        float dot = 0.f;
+#pragma unroll
+        for (int c = 0; c < HD; ++c) dot = fmaf(q[c], ks[j][c], dot);
+        const float p = expf(fmaf(dot, scale, b[j]) - mx);
+        sum += p;
+#pragma unroll
+        for (int c = 0; c < HD; ++c) acc[c] = fmaf(p, vs[j][c], acc[c]);
+    }
+    const float inv = 1.f / sum;
+    float* o = head_out + (blk * T + i) * d + h * HD;
+#pragma unroll
+    for (int c = 0; c < HD; ++c) o[c] = acc[c] * inv;
+    if (rowsum_err_bits) {  // row sum of the normalised probabilities, as the trace audits
+        float rs = 0.f;
+        for (int j = 0; j < T; ++j) {
+            float dot = 0.f;
+#pragma unroll
+            for (int c = 0; c < HD; ++c) dot = fmaf(q[c], ks[j][c], dot);
+            rs += expf(fmaf(dot, scale, b[j]) - mx) * inv;
+        }
+        atomicMax(rowsum_err_bits, __float_as_uint(fabsf(rs - 1.f)));
+    }
+}
+
+// Highway scatter (toy_net.cpp:451-476) as an ancestor gather: row_hw[i] = leaf_tok[i] + the
+// tile token covering i in the row half of every ancestor tile; col_hw likewise for column
+// halves. One warp per node, lane owns 4 channels.
+__global__ void k_tn_highway(TnDims g, const float* leaf_tok, const float* tile_tok, float* row_hw,
+                             float* col_hw) {
+    const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= g.n) return;
+    const float4 lt = reinterpret_cast<const float4*>(leaf_tok + i * g.d)[lane];
+    float4 r = lt, c = lt;
+    const uint64_t leaf = i / g.L;
+    for (uint64_t dd = 0; dd < g.D; ++dd) {
+        const uint64_t m = ((g.K + leaf) >> (g.D - dd)) - 1;
+        const TileGeom t = tile_geom(g, m);
+        const bool right = (leaf >> (g.D - 1 - dd)) & 1ULL;
+        const uint64_t tok = (i - (right ? t.col0 : t.row0)) / t.chunk;
+        const float4 e = reinterpret_cast<const float4*>(tile_tok + (m * g.Ls + tok) * g.d)[lane];
+        float4& dst = right ? c : r;
+        dst.x += e.x; dst.y += e.y; dst.z += e.z; dst.w += e.w;
+    }
+    reinterpret_cast<float4*>(row_hw + i * g.d)[lane] = r;
+    reinterpret_cast<float4*>(col_hw + i * g.d)[lane] = c;
+}
+
+// glob_hw = sum of every leaf token + every tile token (toy_net.cpp:458, 474). Column sums via
+// per-block partials (deterministic), then a single-block finish.
+__global__ void k_tn_colsum_partial(uint64_t rows, uint32_t d, const float* x, float* partial) {
+    const uint32_t c = threadIdx.x;  // blockDim.x == d
+    float s = 0.f;
+    for (uint64_t r = blockIdx.x; r < rows; r += gridDim.x) s += x[r * d + c];
+    partial[uint64_t(blockIdx.x) * d + c] = s;
+}
+__global__ void k_tn_colsum_finish(uint32_t nparts, uint32_t d, const float* partial, float* out) {
+    const uint32_t c = threadIdx.x;
+    double s = 0.0;
+    for (uint32_t b = 0; b < nparts; ++b) s += partial[uint64_t(b) * d + c];
+    out[c] = float(s);
+}
+
+// FFN input rows for leaves (toy_net.cpp:421-436, 515-517): [LN(tok) | row_hw | col_hw | glob],
+// LN already written into columns 0..d-1 by k_tn_layernorm.
+__global__ void k_tn_ffn_input_leaf(TnDims g, const float* row_hw, const float* col_hw,
+                                    const float* glob, float* A) {
+    const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= g.n) return;
+    float4* a = reinterpret_cast<float4*>(A + i * 4 * g.d);
+    a[32 + lane] = reinterpret_cast<const float4*>(row_hw + i * g.d)[lane];
+    a[64 + lane] = reinterpret_cast<const float4*>(col_hw + i * g.d)[lane];
+    a[96 + lane] = reinterpret_cast<const float4*>(glob)[lane];
+}
+
+// ... and for tile tokens (toy_net.cpp:519-537): chunk means of row_hw over the token's row
+// chunk and of col_hw over its column chunk.
+__global__ void k_tn_ffn_input_tile(TnDims g, const float* row_hw, const float* col_hw,
+                                    const float* glob, float* A) {
+    const uint64_t m = blockIdx.x, tok = blockIdx.y;
+    const TileGeom t = tile_geom(g, m);
+    float* a = A + (m * g.Ls + tok) * 4 * g.d;
+    for (uint32_t c = threadIdx.x; c < g.d; c += blockDim.x) {
+        float rs = 0.f, cs = 0.f;
+        for (uint64_t s = 0; s < t.chunk; ++s) {
+            rs += row_hw[(t.row0 + tok * t.chunk + s) * g.d + c];
+            cs += col_hw[(t.col0 + tok * t.chunk + s) * g.d + c];
+        }
+        a[g.d + c] = rs / float(t.chunk);
+        a[2 * g.d + c] = cs / float(t.chunk);
+        a[3 * g.d + c] = glob[c];
+    }
+}
+
+}  // namespace hfpg
