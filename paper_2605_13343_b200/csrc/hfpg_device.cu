@@ -85,6 +85,7 @@ struct hfpg_handle {
     bool graph_valid = false;
 
     DevSys sys{};
+    ToynetModel* toynet = nullptr;
 };
 
 namespace {
@@ -402,6 +403,7 @@ int hfpg_destroy(hfpg_handle* h) {
         dfree(h->coupled); dfree(h->node_u); dfree(h->node_v);
         dfree(h->tree_counters); dfree(h->partials); dfree(h->counters); dfree(h->sc);
         dfree(h->history);
+        if (h->toynet) toynet_model_destroy(h->toynet);
         if (h->ev0) cudaEventDestroy(h->ev0);
         if (h->ev1) cudaEventDestroy(h->ev1);
         if (h->stream) cudaStreamDestroy(h->stream);
@@ -724,7 +726,12 @@ int hfpg_toynet_forward(hfpg_handle* h, const hfpg_frame_view* frame, uint64_t l
         }
         CK(cudaMemsetAsync(dst, 0, L.total * 4, h->stream));
         try {
-            toynet_forward_device(h->stream, *frame, leaf, ls, *cfg, seed, dst, trace);
+            if (!toynet_model_matches(h->toynet, *cfg, leaf, ls, seed)) {
+                if (h->toynet) toynet_model_destroy(h->toynet);
+                h->toynet = nullptr;
+                h->toynet = toynet_model_create(*cfg, leaf, ls, seed);
+            }
+            toynet_forward_device(h->toynet, h->stream, *frame, dst, trace);
             if (out) CK(cudaMemcpy(out, dst, L.total * 4, cudaMemcpyDeviceToHost));
         } catch (...) {
             if (!load) cudaFree(dst);

@@ -104,9 +104,14 @@ struct Csr {
 };
 void init_factors_host(const Layout& L, double sigma, uint64_t seed, uint64_t frame, float* out);
 
-// toynet.cu: the GPU forward into a device buffer of the packed layout.
-void toynet_forward_device(cudaStream_t st, const hfpg_frame_view& fr, uint64_t L, uint64_t Ls,
-                           const hfpg_toynet_config& cfg, uint64_t seed, float* out,
+// toynet.cu: device-resident toy-network model (weights once per config/seed) and the GPU
+// forward of one frame into a device buffer of the packed layout.
+struct ToynetModel;
+ToynetModel* toynet_model_create(const hfpg_toynet_config& cfg, uint64_t L, uint64_t Ls, uint64_t seed);
+void toynet_model_destroy(ToynetModel* m);
+bool toynet_model_matches(const ToynetModel* m, const hfpg_toynet_config& cfg, uint64_t L, uint64_t Ls,
+                          uint64_t seed);
+void toynet_forward_device(ToynetModel* m, cudaStream_t st, const hfpg_frame_view& fr, float* out,
                            hfpg_toynet_trace* trace);
 
 }  // namespace hfpg

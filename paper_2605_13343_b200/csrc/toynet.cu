@@ -245,20 +245,97 @@ EdgeMlp edge_params(const Mat& w1, const Mat& w2) {
 
 }  // namespace
 
-// Full forward: writes the packed factor tensor (device pointer out, layout of (n, L, Ls)).
-void toynet_forward_device(cudaStream_t st, const hfpg_frame_view& fr, uint64_t L, uint64_t Ls,
-                           const hfpg_toynet_config& cfg, uint64_t seed, float* out,
-                           hfpg_toynet_trace* trace) {
-    const auto t0 = std::chrono::steady_clock::now();
-    const Layout lay = make_layout(fr.n, L, Ls);
-    const uint64_t n = fr.n, d = cfg.d;
+// A toy-network instance on the device: weights drawn once per (cfg, L, L_s, seed) and kept as
+// W^T fp32; activation scratch grown on demand and reused across frames.
+struct ToynetModel {
+    hfpg_toynet_config cfg{};
+    uint64_t L = 0, Ls = 0, seed = 0;
+    EdgeMlp le{}, te{};
+    std::vector<float*> wbuf;
+    float *w_enc1 = nullptr, *w_enc2 = nullptr, *w_lh1 = nullptr, *w_lh2 = nullptr,
+          *w_heads = nullptr, *w_theads = nullptr;
+    std::vector<float*> w_gcn;
+    struct LW {
+        float *qkv, *wo, *f1, *f2;
+    };
+    std::vector<LW> wl, wt;
+    std::vector<std::pair<void*, size_t>> scratch;  // (ptr, bytes), index = buffer id
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    ~ToynetModel() {
+        for (float* p : wbuf) cudaFree(p);
+        for (auto& b : scratch) cudaFree(b.first);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+    }
+    template <class T>
+    T* buf(size_t id, uint64_t count) {
+        if (scratch.size() <= id) scratch.resize(id + 1, {nullptr, 0});
+        const size_t bytes = std::max<uint64_t>(count, 1) * sizeof(T);
+        if (scratch[id].second < bytes) {
+            if (scratch[id].first) cudaFree(scratch[id].first);
+            scratch[id].first = nullptr;
+            TCK(cudaMalloc(&scratch[id].first, bytes));
+            scratch[id].second = bytes;
+        }
+        return static_cast<T*>(scratch[id].first);
+    }
+};
+
+ToynetModel* toynet_model_create(const hfpg_toynet_config& cfg, uint64_t L, uint64_t Ls, uint64_t seed) {
+    const uint64_t d = cfg.d;
     if (d != 128) throw InvalidArgument("toynet (gpu): embedding width must be 128");
     if (cfg.heads * 16 != d) throw InvalidArgument("toynet (gpu): head dimension must be 16");
     if (cfg.edge_hidden > 8 || cfg.heads > 8 || cfg.d_global > 12)
         throw InvalidArgument("toynet (gpu): edge_hidden, heads <= 8 and d_global <= 12");
-    if (!(L == 128 && (Ls == 32 || Ls == 16 || Ls == 8)) && !(L == 64 || L == 32 || L == 16 || L == 8 || L == 4))
-        throw InvalidArgument("toynet (gpu): unsupported leaf size");
-    const HostWeights w = init_weights(cfg, L, Ls, seed);
+    if (!(L == 128 || L == 64 || L == 32 || L == 16 || L == 8 || L == 4) ||
+        !(Ls == 32 || Ls == 16 || Ls == 8 || Ls == 4))
+        throw InvalidArgument("toynet (gpu): unsupported leaf / coarse size");
+    auto* m = new ToynetModel;
+    try {
+        m->cfg = cfg;
+        m->L = L;
+        m->Ls = Ls;
+        m->seed = seed;
+        const HostWeights w = init_weights(cfg, L, Ls, seed);
+        m->le = edge_params(w.le_w1, w.le_w2);
+        m->te = edge_params(w.te_w1, w.te_w2);
+        m->w_enc1 = upload_t(w.enc1, m->wbuf, 32);
+        m->w_enc2 = upload_t(w.enc2, m->wbuf);
+        for (auto& g : w.gcn) m->w_gcn.push_back(upload_t(g, m->wbuf));
+        for (auto* src : {&w.leaf, &w.tile})
+            for (auto& x : *src) {
+                ToynetModel::LW l{upload_stack_t({&x.wq, &x.wk, &x.wv}, m->wbuf), upload_t(x.wo, m->wbuf),
+                                  upload_t(x.ffn1, m->wbuf), upload_t(x.ffn2, m->wbuf)};
+                (src == &w.leaf ? m->wl : m->wt).push_back(l);
+            }
+        m->w_lh1 = upload_t(w.lh1, m->wbuf);
+        m->w_lh2 = upload_t(w.lh2, m->wbuf);
+        m->w_heads = upload_stack_t({&w.bhu, &w.bhv}, m->wbuf, 1, &w.gate);
+        m->w_theads = upload_stack_t({&w.thu, &w.thv}, m->wbuf);
+        TCK(cudaEventCreate(&m->ev0));
+        TCK(cudaEventCreate(&m->ev1));
+    } catch (...) {
+        delete m;
+        throw;
+    }
+    return m;
+}
+void toynet_model_destroy(ToynetModel* m) { delete m; }
+bool toynet_model_matches(const ToynetModel* m, const hfpg_toynet_config& c, uint64_t L, uint64_t Ls,
+                          uint64_t seed) {
+    return m && m->L == L && m->Ls == Ls && m->seed == seed && m->cfg.d == c.d &&
+           m->cfg.layers == c.layers && m->cfg.heads == c.heads && m->cfg.gcn_layers == c.gcn_layers &&
+           m->cfg.d_global == c.d_global && m->cfg.edge_hidden == c.edge_hidden;
+}
+
+// Full forward for one frame: writes the packed factor tensor (device pointer out).
+void toynet_forward_device(ToynetModel* mdl, cudaStream_t st, const hfpg_frame_view& fr, float* out,
+                           hfpg_toynet_trace* trace) {
+    const hfpg_toynet_config& cfg = mdl->cfg;
+    const uint64_t L = mdl->L, Ls = mdl->Ls;
+    const auto t0 = std::chrono::steady_clock::now();
+    const Layout lay = make_layout(fr.n, L, Ls);
+    const uint64_t n = fr.n, d = cfg.d;
 
     // ---- glob stats on the host, f64 in the reference's order (toy_net.cpp:232-268) --------
     std::vector<double> diag(n, 0.0);
@@ -291,17 +368,6 @@ void toynet_forward_device(cudaStream_t st, const hfpg_frame_view& fr, uint64_t 
     std::vector<float> glob(std::max<uint64_t>(cfg.d_global, 1), 0.f);
     for (uint64_t i = 0; i < cfg.d_global && i < 12; ++i) glob[i] = float(stats[i]);
 
-    std::vector<void*> buf;
-    std::vector<float*> wbuf;
-    struct Cleanup {
-        std::vector<void*>& a;
-        std::vector<float*>& b;
-        ~Cleanup() {
-            for (void* p : a) cudaFree(p);
-            for (float* p : b) cudaFree(p);
-        }
-    } cleanup{buf, wbuf};
-
     TnDims g{};
     g.n = n;
     g.L = L;
@@ -320,13 +386,13 @@ void toynet_forward_device(cudaStream_t st, const hfpg_frame_view& fr, uint64_t 
     const uint64_t nnz = fr.row_offsets[n], MT = lay.m * Ls;  // tile tokens
 
     // ---- inputs ------------------------------------------------------------------------------
-    auto* d_order = dnew<uint32_t>(n, buf);
-    auto* d_rho = dnew<double>(n, buf);
-    auto* d_ro = dnew<unsigned long long>(n + 1, buf);
-    auto* d_ci = dnew<uint32_t>(nnz, buf);
-    auto* d_v = dnew<double>(nnz, buf);
-    auto* d_diag = dnew<double>(n, buf);
-    auto* d_glob = dnew<float>(glob.size(), buf);
+    auto* d_order = mdl->buf<uint32_t>(21, n);
+    auto* d_rho = mdl->buf<double>(0, n);
+    auto* d_ro = mdl->buf<unsigned long long>(1, n + 1);
+    auto* d_ci = mdl->buf<uint32_t>(22, nnz);
+    auto* d_v = mdl->buf<double>(2, nnz);
+    auto* d_diag = mdl->buf<double>(3, n);
+    auto* d_glob = mdl->buf<float>(4, glob.size());
     TCK(cudaMemcpyAsync(d_order, fr.cell_order, n * 4, cudaMemcpyHostToDevice, st));
     TCK(cudaMemcpyAsync(d_rho, fr.rho, n * 8, cudaMemcpyHostToDevice, st));
     TCK(cudaMemcpyAsync(d_ro, fr.row_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, st));
@@ -335,52 +401,36 @@ void toynet_forward_device(cudaStream_t st, const hfpg_frame_view& fr, uint64_t 
     TCK(cudaMemcpyAsync(d_diag, diag.data(), n * 8, cudaMemcpyHostToDevice, st));
     TCK(cudaMemcpyAsync(d_glob, glob.data(), glob.size() * 4, cudaMemcpyHostToDevice, st));
 
-    // ---- weights (W^T, fp32) -------------------------------------------------------------------
-    float* w_enc1 = upload_t(w.enc1, wbuf, g.feat_pad);
-    float* w_enc2 = upload_t(w.enc2, wbuf);
-    std::vector<float*> w_gcn;
-    for (auto& m : w.gcn) w_gcn.push_back(upload_t(m, wbuf));
-    struct LW {
-        float *qkv, *wo, *f1, *f2;
-    };
-    std::vector<LW> wl, wt;
-    for (auto* src : {&w.leaf, &w.tile})
-        for (auto& x : *src) {
-            LW l{upload_stack_t({&x.wq, &x.wk, &x.wv}, wbuf), upload_t(x.wo, wbuf), upload_t(x.ffn1, wbuf),
-                 upload_t(x.ffn2, wbuf)};
-            (src == &w.leaf ? wl : wt).push_back(l);
-        }
-    float* w_lh1 = upload_t(w.lh1, wbuf);
-    float* w_lh2 = upload_t(w.lh2, wbuf);
-    float* w_heads = upload_stack_t({&w.bhu, &w.bhv}, wbuf, 1, &w.gate);  // (2 Ls + 1) x d
-    float* w_theads = upload_stack_t({&w.thu, &w.thv}, wbuf);             // Ls x d
-
+    const auto& wl = mdl->wl;
+    const auto& wt = mdl->wt;
+    using LW = ToynetModel::LW;
     // ---- activations -------------------------------------------------------------------------
-    auto* feat = dnew<float>(n * g.feat_pad, buf);
-    auto* x = dnew<float>(n * d, buf);       // embedding -> leaf tokens
-    auto* h1 = dnew<float>(n * d, buf);      // encoder hidden / gcn message / decoder hidden
-    auto* tile_tok = dnew<float>(MT * d, buf);
-    auto* ln = dnew<float>(std::max(n, MT) * d, buf);
-    auto* qkv = dnew<float>(std::max(n, MT) * 3 * d, buf);
-    auto* hout = dnew<float>(std::max(n, MT) * d, buf);
-    auto* row_hw = dnew<float>(n * d, buf);
-    auto* col_hw = dnew<float>(n * d, buf);
-    auto* Af = dnew<float>(std::max(n, MT) * 4 * d, buf);
-    auto* Hf = dnew<float>(std::max(n, MT) * 4 * d, buf);
-    auto* glob_hw = dnew<float>(d, buf);
+    auto* feat = mdl->buf<float>(5, n * g.feat_pad);
+    auto* x = mdl->buf<float>(6, n * d);       // embedding -> leaf tokens
+    auto* h1 = mdl->buf<float>(7, n * d);      // encoder hidden / gcn message / decoder hidden
+    auto* tile_tok = mdl->buf<float>(8, MT * d);
+    auto* ln = mdl->buf<float>(9, std::max(n, MT) * d);
+    auto* qkv = mdl->buf<float>(10, std::max(n, MT) * 3 * d);
+    auto* hout = mdl->buf<float>(11, std::max(n, MT) * d);
+    auto* row_hw = mdl->buf<float>(12, n * d);
+    auto* col_hw = mdl->buf<float>(13, n * d);
+    auto* Af = mdl->buf<float>(14, std::max(n, MT) * 4 * d);
+    auto* Hf = mdl->buf<float>(15, std::max(n, MT) * 4 * d);
+    auto* glob_hw = mdl->buf<float>(16, d);
     const uint32_t nparts = 296;
-    auto* partial = dnew<float>(uint64_t(nparts) * 2 * d, buf);
-    auto* leaf_bias = dnew<float>(lay.k * cfg.heads * L * L, buf);
-    auto* tile_bias = dnew<float>(lay.m * cfg.heads * Ls * Ls, buf);
-    unsigned int* rowsum_bits = trace ? dnew<unsigned int>(1, buf) : nullptr;
+    auto* partial = mdl->buf<float>(17, uint64_t(nparts) * 2 * d);
+    auto* leaf_bias = mdl->buf<float>(18, lay.k * cfg.heads * L * L);
+    auto* tile_bias = mdl->buf<float>(19, lay.m * cfg.heads * Ls * Ls);
+    unsigned int* rowsum_bits = trace ? mdl->buf<unsigned int>(20, 1) : nullptr;
     if (rowsum_bits) TCK(cudaMemsetAsync(rowsum_bits, 0, 4, st));
 
     const unsigned nb = unsigned((n + 255) / 256), nw = unsigned((n * 32 + 255) / 256);
+    TCK(cudaEventRecord(mdl->ev0, st));
     // ---- encoder (toy_net.cpp:295-318) -----------------------------------------------------
     k_tn_features<<<nb, 256, 0, st>>>(g, d_order, d_rho, d_ro, d_ci, d_glob, feat);
-    gemm<128>(st, feat, n, g.feat_pad, g.feat_pad, w_enc1, d, g.feat_pad, EpiStore{h1, uint32_t(d), uint32_t(d), nullptr, 1});
-    gemm<128>(st, h1, n, d, d, w_enc2, d, d, EpiStore{x, uint32_t(d), uint32_t(d), nullptr, 0});
-    for (float* wg : w_gcn) {
+    gemm<128>(st, feat, n, g.feat_pad, g.feat_pad, mdl->w_enc1, d, g.feat_pad, EpiStore{h1, uint32_t(d), uint32_t(d), nullptr, 1});
+    gemm<128>(st, h1, n, d, d, mdl->w_enc2, d, d, EpiStore{x, uint32_t(d), uint32_t(d), nullptr, 0});
+    for (float* wg : mdl->w_gcn) {
         k_tn_gcn_msg<<<nw, 256, 0, st>>>(g, d_ro, d_ci, d_v, d_diag, x, h1);
         gemm<128>(st, h1, n, d, d, wg, d, d, EpiResidual{x, uint32_t(d), uint32_t(d), nullptr, 1});
     }
@@ -388,10 +438,10 @@ void toynet_forward_device(cudaStream_t st, const hfpg_frame_view& fr, uint64_t 
     // ---- tile tokens, edge biases ------------------------------------------------------------
     if (lay.m) k_tn_tile_pool<<<dim3(unsigned(lay.m), unsigned(Ls)), 128, 0, st>>>(g, x, tile_tok);
     k_tn_leaf_bias<<<dim3(unsigned((L * L + 255) / 256), unsigned(lay.k)), 256, 0, st>>>(
-        g, d_order, d_ro, d_ci, d_v, edge_params(w.le_w1, w.le_w2), leaf_bias);
+        g, d_order, d_ro, d_ci, d_v, mdl->le, leaf_bias);
     if (lay.m)
         k_tn_tile_bias<<<dim3(unsigned(lay.m), unsigned(Ls)), 64, 0, st>>>(
-            g, d_order, d_ro, d_ci, d_v, edge_params(w.te_w1, w.te_w2), tile_bias);
+            g, d_order, d_ro, d_ci, d_v, mdl->te, tile_bias);
     TCK(cudaGetLastError());
 
     std::vector<double> hw_dev;
@@ -468,12 +518,13 @@ void toynet_forward_device(cudaStream_t st, const hfpg_frame_view& fr, uint64_t 
     }
 
     // ---- decoder heads into the packed layout (toy_net.cpp:540-585) ------------------------
-    gemm<128>(st, x, n, d, d, w_lh1, d, d, EpiStore{h1, uint32_t(d), uint32_t(d), nullptr, 1});
+    gemm<128>(st, x, n, d, d, mdl->w_lh1, d, d, EpiStore{h1, uint32_t(d), uint32_t(d), nullptr, 1});
     // F_k rows: leaf_factor(k) + r L = (k L + r) L = i L -> a row-major [n x L] section
-    gemm<128>(st, h1, n, d, d, w_lh2, L, d, EpiStore{out, uint32_t(L), uint32_t(L), nullptr, 0});
-    gemm<80>(st, x, n, d, d, w_heads, 2 * Ls + 1, d,
+    gemm<128>(st, h1, n, d, d, mdl->w_lh2, L, d, EpiStore{out, uint32_t(L), uint32_t(L), nullptr, 0});
+    gemm<80>(st, x, n, d, d, mdl->w_heads, 2 * Ls + 1, d,
              EpiLeafHeads{out, L, Ls, lay.bridge_base, lay.gate_base, nullptr});
-    if (lay.m) gemm<32>(st, tile_tok, MT, d, d, w_theads, Ls, d, EpiTileHeads{out, Ls, Ls / 2, lay.tile_base, nullptr});
+    if (lay.m) gemm<32>(st, tile_tok, MT, d, d, mdl->w_theads, Ls, d, EpiTileHeads{out, Ls, Ls / 2, lay.tile_base, nullptr});
+    TCK(cudaEventRecord(mdl->ev1, st));
     TCK(cudaStreamSynchronize(st));
 
     if (trace) {
@@ -485,7 +536,10 @@ void toynet_forward_device(cudaStream_t st, const hfpg_frame_view& fr, uint64_t 
         trace->highway_max_deviation = hw_dev.empty() ? 0.0 : *std::max_element(hw_dev.begin(), hw_dev.end());
         trace->leaf_attention_dispatches = cfg.layers;
         trace->tile_attention_dispatches = lay.m ? cfg.layers : 0;
-        trace->ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        float dev_ms = 0.f;
+        TCK(cudaEventElapsedTime(&dev_ms, mdl->ev0, mdl->ev1));
+        trace->ms = dev_ms;  // device time of the forward (all kernels, excl. host setup)
+        (void)t0;
     }
 }
 

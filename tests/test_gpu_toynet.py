@@ -59,11 +59,15 @@ def test_forward_deterministic_and_loads_into_solver(H, oracle):
     dev.load_csr(fr.A)
     f2 = H.toynet_forward(fr, p, 32, weight_seed=3, device=dev, load=True)
     assert (f1.data.view(np.uint32) == f2.data.view(np.uint32)).all()
-    # the tensor now lives on the handle: apply it there and check against the oracle
+    # the tensor now lives on the handle: apply it there. Seeded-weight factors reach ~1e38
+    # (SURVEY.md §0 fact 2), where even the reference's own apply<float> drifts from
+    # apply<double>; the fast path reproduces the reference's fp32 rounding, so gate on that.
     r = np.random.default_rng(1).standard_normal(n)
     z = dev.apply(r)
+    z32 = oracle.apply_f32(n, 128, 32, f2.data, fr.A.diagonal(), r)
     z64 = oracle.apply_f64(n, 128, 32, f2.data.astype(np.float64), fr.A.diagonal(), r)
-    assert rel_l2(z, z64) <= 1e-5
+    assert rel_l2(z, z32) <= 1e-6, (rel_l2(z, z32), rel_l2(z32, z64))
+    assert rel_l2(z, z64) <= 1e-4
 
 
 def test_toynet_tensor_pcg_is_non_convergent_like_reference(H):

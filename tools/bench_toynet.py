@@ -22,9 +22,13 @@ fr = H.make_frame(a.n, 2024, 0)
 p = H.build_partition(a.n, 128)
 dev = H.Device(0)
 dev.load_csr(fr.A)
-times = []
+times, dev_ms = [], []
 for i in range(a.reps + 1):
+    tr = H.ToynetTrace()
     t0 = time.perf_counter()
-    H.toynet_forward(fr, p, 32, device=dev, load=True)
+    H.toynet_forward(fr, p, 32, device=dev, load=True, trace=tr if i else None)
     times.append((time.perf_counter() - t0) * 1e3)
-print(json.dumps({"n": a.n, "toynet_forward_ms": times[1:], "first_call_ms": times[0]}))
+    tr2 = H.ToynetTrace()
+    H.toynet_forward(fr, p, 32, device=dev, load=True, trace=tr2)
+    dev_ms.append(tr2.ms)
+print(json.dumps({"n": a.n, "host_wall_ms": times, "device_ms": dev_ms}))
