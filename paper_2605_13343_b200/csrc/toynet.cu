@@ -422,6 +422,9 @@ void toynet_forward_device(ToynetModel* mdl, cudaStream_t st, const hfpg_frame_v
     auto* leaf_bias = mdl->buf<float>(18, lay.k * cfg.heads * L * L);
     auto* tile_bias = mdl->buf<float>(19, lay.m * cfg.heads * Ls * Ls);
     unsigned int* rowsum_bits = trace ? mdl->buf<unsigned int>(20, 1) : nullptr;
+    float* audit_part = trace ? mdl->buf<float>(23, uint64_t(nparts) * d) : nullptr;
+    float* audit_sums = trace ? mdl->buf<float>(24, 6 * d) : nullptr;
+    float* audit_dev = trace ? mdl->buf<float>(25, cfg.layers) : nullptr;
     if (rowsum_bits) TCK(cudaMemsetAsync(rowsum_bits, 0, 4, st));
 
     const unsigned nb = unsigned((n + 255) / 256), nw = unsigned((n * 32 + 255) / 256);
@@ -444,7 +447,6 @@ void toynet_forward_device(ToynetModel* mdl, cudaStream_t st, const hfpg_frame_v
             g, d_order, d_ro, d_ci, d_v, mdl->te, tile_bias);
     TCK(cudaGetLastError());
 
-    std::vector<double> hw_dev;
     auto attention = [&](float* tok, uint64_t rows, uint64_t T, const LW& lw, const float* bias) {
         k_tn_layernorm<<<unsigned((rows * 32 + 255) / 256), 256, 0, st>>>(rows, uint32_t(d), tok, ln, uint32_t(d));
         gemm<128>(st, ln, rows, d, d, lw.qkv, 3 * d, d, EpiStore{qkv, uint32_t(3 * d), uint32_t(3 * d), nullptr, 0});
@@ -480,38 +482,20 @@ void toynet_forward_device(ToynetModel* mdl, cudaStream_t st, const hfpg_frame_v
         k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(MT, uint32_t(d), tile_tok, partial + nparts * d);
         k_tn_colsum_finish<<<1, unsigned(d), 0, st>>>(2 * nparts, uint32_t(d), partial, glob_hw);
         TCK(cudaGetLastError());
-        if (trace) {  // highway conservation audit (toy_net.cpp:478-512), host-side f64
-            std::vector<float> lt(n * d), tt(MT * d), rh(n * d), ch(n * d), gh(d);
-            TCK(cudaMemcpyAsync(lt.data(), x, n * d * 4, cudaMemcpyDeviceToHost, st));
-            TCK(cudaMemcpyAsync(tt.data(), tile_tok, MT * d * 4, cudaMemcpyDeviceToHost, st));
-            TCK(cudaMemcpyAsync(rh.data(), row_hw, n * d * 4, cudaMemcpyDeviceToHost, st));
-            TCK(cudaMemcpyAsync(ch.data(), col_hw, n * d * 4, cudaMemcpyDeviceToHost, st));
-            TCK(cudaMemcpyAsync(gh.data(), glob_hw, d * 4, cudaMemcpyDeviceToHost, st));
-            TCK(cudaStreamSynchronize(st));
-            double dev = 0.0, scale = 0.0;
-            for (uint64_t c = 0; c < d; ++c) {
-                double er = 0, ec = 0, eg = 0, gr = 0, gc = 0;
-                for (uint64_t i = 0; i < n; ++i) {
-                    er += lt[i * d + c];
-                    gr += rh[i * d + c];
-                    gc += ch[i * d + c];
-                }
-                ec = eg = er;
-                for (uint64_t m = 0; m < lay.m; ++m) {
-                    int dd = 0;
-                    while ((2ULL << dd) <= m + 1) ++dd;
-                    const double chunk = double((lay.k >> dd) / 2 * L / Ls);
-                    for (uint64_t tok = 0; tok < Ls; ++tok) {
-                        const double e = tt[(m * Ls + tok) * d + c];
-                        er += e * chunk;
-                        ec += e * chunk;
-                        eg += e;
-                    }
-                }
-                dev = std::max({dev, std::fabs(gr - er), std::fabs(gc - ec), std::fabs(double(gh[c]) - eg)});
-                scale = std::max({scale, std::fabs(er), std::fabs(ec), std::fabs(eg), 1.0});
-            }
-            hw_dev.push_back(dev / scale);
+        if (trace) {  // highway conservation audit (toy_net.cpp:478-512), on device
+            k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(n, uint32_t(d), row_hw, audit_part);
+            k_tn_colsum_finish<<<1, unsigned(d), 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums);
+            k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(n, uint32_t(d), col_hw, audit_part);
+            k_tn_colsum_finish<<<1, unsigned(d), 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums + d);
+            k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(n, uint32_t(d), x, audit_part);
+            k_tn_colsum_finish<<<1, unsigned(d), 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums + 2 * d);
+            k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(MT, uint32_t(d), tile_tok, audit_part);
+            k_tn_colsum_finish<<<1, unsigned(d), 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums + 3 * d);
+            k_tn_colsum_tiles_weighted<<<nparts, unsigned(d), 0, st>>>(g, tile_tok, audit_part);
+            k_tn_colsum_finish<<<1, unsigned(d), 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums + 4 * d);
+            TCK(cudaMemcpyAsync(audit_sums + 5 * d, glob_hw, d * 4, cudaMemcpyDeviceToDevice, st));
+            k_tn_highway_audit<<<1, unsigned(d), 0, st>>>(uint32_t(d), audit_sums, audit_dev + layer);
+            TCK(cudaGetLastError());
         }
         ffn(x, n, wl[layer], true);
         if (lay.m) ffn(tile_tok, MT, wt[layer], false);
@@ -533,7 +517,9 @@ void toynet_forward_device(ToynetModel* mdl, cudaStream_t st, const hfpg_frame_v
         float e;
         std::memcpy(&e, &bits, 4);
         trace->max_attention_row_sum_error = e;
-        trace->highway_max_deviation = hw_dev.empty() ? 0.0 : *std::max_element(hw_dev.begin(), hw_dev.end());
+        std::vector<float> hw(cfg.layers, 0.f);
+        TCK(cudaMemcpy(hw.data(), audit_dev, cfg.layers * 4, cudaMemcpyDeviceToHost));
+        trace->highway_max_deviation = hw.empty() ? 0.0 : *std::max_element(hw.begin(), hw.end());
         trace->leaf_attention_dispatches = cfg.layers;
         trace->tile_attention_dispatches = lay.m ? cfg.layers : 0;
         float dev_ms = 0.f;

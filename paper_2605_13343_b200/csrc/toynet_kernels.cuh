@@ -300,6 +300,36 @@ __global__ void k_tn_colsum_partial(uint64_t rows, uint32_t d, const float* x, f
     for (uint64_t r = blockIdx.x; r < rows; r += gridDim.x) s += x[r * d + c];
     partial[uint64_t(blockIdx.x) * d + c] = s;
 }
+// Tile-token column sums weighted by each token's chunk length (the number of highway rows it
+// is scattered to), for the conservation audit.
+__global__ void k_tn_colsum_tiles_weighted(TnDims g, const float* tile_tok, float* partial) {
+    const uint32_t c = threadIdx.x;
+    float s = 0.f;
+    for (uint64_t r = blockIdx.x; r < g.M * g.Ls; r += gridDim.x)
+        s += tile_tok[r * g.d + c] * float(tile_geom(g, r / g.Ls).chunk);
+    partial[uint64_t(blockIdx.x) * g.d + c] = s;
+}
+// Highway conservation (toy_net.cpp:478-512) from column sums: sums[0..5] = row_hw, col_hw,
+// leaf tokens, tile tokens, chunk-weighted tile tokens, glob_hw -> dev / scale.
+__global__ void k_tn_highway_audit(uint32_t d, const float* sums, float* out_layer) {
+    __shared__ float dev[128], sc[128];
+    const uint32_t c = threadIdx.x;
+    const float gr = sums[c], gc = sums[d + c], lt = sums[2 * d + c], tt = sums[3 * d + c],
+                ttw = sums[4 * d + c], gg = sums[5 * d + c];
+    const float er = lt + ttw, eg = lt + tt;
+    dev[c] = fmaxf(fmaxf(fabsf(gr - er), fabsf(gc - er)), fabsf(gg - eg));
+    sc[c] = fmaxf(fmaxf(fabsf(er), fabsf(eg)), 1.f);
+    __syncthreads();
+    if (c == 0) {
+        float dm = 0.f, sm = 0.f;
+        for (uint32_t i = 0; i < d; ++i) {
+            dm = fmaxf(dm, dev[i]);
+            sm = fmaxf(sm, sc[i]);
+        }
+        *out_layer = dm / sm;
+    }
+}
+
 __global__ void k_tn_colsum_finish(uint32_t nparts, uint32_t d, const float* partial, float* out) {
     const uint32_t c = threadIdx.x;
     double s = 0.0;

@@ -80,6 +80,6 @@ def test_toynet_tensor_pcg_is_non_convergent_like_reference(H):
     dev.load_csr(fr.A)
     H.toynet_forward(fr, H.build_partition(n, 128), 32, device=dev, load=True)
     dev.set_precond(2)
-    rep = dev.solve_ptr(fr.b.ctypes.data, np.empty(n).ctypes.data, H.SolveConfig(max_iters=2000),
-                        None, 0)
+    x = np.empty(n)
+    rep = dev.solve_ptr(fr.b.ctypes.data, x.ctypes.data, H.SolveConfig(max_iters=2000), None, 0)
     assert rep.status == 1 and rep.iterations == 2000
