@@ -32,6 +32,11 @@ enum hfpg_status { HFPG_OK = 0, HFPG_EINVAL = 1, HFPG_EIO = 2, HFPG_ECUDA = 3, H
 enum hfpg_where { HFPG_HOST = 0, HFPG_DEVICE = 1 };
 /* pcg.cpp:28-51 identity_applier / jacobi_applier / factor_applier */
 enum hfpg_precond { HFPG_PRECOND_IDENTITY = 0, HFPG_PRECOND_JACOBI = 1, HFPG_PRECOND_FACTOR = 2 };
+/* How hfpg_pcg_solve runs the loop. GRAPH: one CUDA graph, a conditional WHILE node over the
+ * per-stage kernels (any layout / preconditioner). PERSISTENT: one cooperative kernel for the
+ * whole solve, phases separated by grid barriers (factor preconditioner, L=128, L_s=32).
+ * AUTO picks PERSISTENT where it applies. */
+enum hfpg_solver { HFPG_SOLVER_AUTO = 0, HFPG_SOLVER_GRAPH = 1, HFPG_SOLVER_PERSISTENT = 2 };
 /* pcg.hpp:19 SolveStatus */
 enum hfpg_solve_status { HFPG_CONVERGED = 0, HFPG_MAX_ITERS = 1, HFPG_BREAKDOWN = 2 };
 
@@ -159,6 +164,17 @@ int hfpg_set_diag(hfpg_handle* h, uint64_t n, const double* a_diag, int where);
 /* Select the preconditioner used by hfpg_pcg_solve. JACOBI throws EINVAL on a nonpositive
  * diagonal entry like jacobi_applier (pcg.cpp:34-42). */
 int hfpg_set_precond(hfpg_handle* h, int kind);
+
+/* Select the solve driver (hfpg_solver); the one that will run is reported by
+ * hfpg_solver_in_use. Iterates are identical up to the order of the f64 dot-product sums. */
+int hfpg_set_solver(hfpg_handle* h, int kind);
+int hfpg_solver_in_use(hfpg_handle* h, int32_t* out);
+/* Phase trace of the persistent solver: with cap > 0, every later solve records %globaltimer
+ * (ns) at its start (entry 0) and after each grid barrier e (entry e, e < cap), from CTA 0.
+ * Barrier sequence: init = [leaf, sums, tiles, prolong], then per iteration [spmv, leaf, sums,
+ * tiles, prolong]. cap = 0 turns tracing off. */
+int hfpg_set_trace(hfpg_handle* h, uint32_t cap);
+int hfpg_get_trace(hfpg_handle* h, uint64_t* out, uint32_t cap);
 
 /* apply.cpp:79-174 apply<float>: z = M r with the loaded factors and diag(A). */
 int hfpg_apply(hfpg_handle* h, const double* r, double* z, int where);

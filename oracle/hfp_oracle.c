@@ -228,7 +228,41 @@ DEFINE_APPLY(orc_apply_f32, float)
 DEFINE_APPLY(orc_apply_f64, double)
 
 /* ---- pcg.cpp:53-126 --------------------------------------------------------------------- */
+/* Sequential as the reference (pcg.cpp dot). ORC_DOT_MODE (sensitivity experiments only):
+ * 1 = blocked tree (128-element sequential blocks, pairwise combine, like a GPU reduction),
+ * 2 = compensated (Neumaier) — near the exact dot. */
+static int dot_mode = -1;
 static double dot(uint64_t n, const double* a, const double* c) {
+    if (dot_mode < 0) {
+        const char* e = getenv("ORC_DOT_MODE");
+        dot_mode = e ? atoi(e) : 0;
+    }
+    if (dot_mode == 1) {
+        uint64_t nb = (n + 127) / 128;
+        double* part = (double*)malloc(nb * sizeof(double));
+        for (uint64_t b = 0; b < nb; ++b) {
+            double t = 0.0;
+            for (uint64_t i = 128 * b; i < n && i < 128 * b + 128; ++i) t += a[i] * c[i];
+            part[b] = t;
+        }
+        for (uint64_t w = 1; w < nb; w *= 2)
+            for (uint64_t b = 0; b + w < nb; b += 2 * w) part[b] += part[b + w];
+        double r = part[0];
+        free(part);
+        return r;
+    }
+    if (dot_mode == 2) {
+        double s = 0.0, comp = 0.0;
+        for (uint64_t i = 0; i < n; ++i) {
+            const double p = a[i] * c[i];
+            const double pe = fma(a[i], c[i], -p);
+            const double t = s + p;
+            comp += (fabs(s) >= fabs(p)) ? (s - t) + p : (p - t) + s;
+            comp += pe;
+            s = t;
+        }
+        return s + comp;
+    }
     double s = 0.0;
     for (uint64_t i = 0; i < n; ++i) s += a[i] * c[i];
     return s;

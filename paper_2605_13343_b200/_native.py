@@ -13,6 +13,7 @@ SO_PATH = os.path.join(HERE, "libhfpg.so")
 
 HFPG_OK, HFPG_EINVAL, HFPG_EIO, HFPG_ECUDA, HFPG_ENCCL = range(5)
 HOST, DEVICE = 0, 1
+SOLVER_AUTO, SOLVER_GRAPH, SOLVER_PERSISTENT = 0, 1, 2
 
 u64, i32, dbl, vp = C.c_uint64, C.c_int32, C.c_double, C.c_void_p
 
@@ -86,6 +87,10 @@ _PROTOS = {
     "hfpg_spmv": (C.c_int, [vp, vp, vp, C.c_int]),
     "hfpg_pcg_solve": (C.c_int, [vp, vp, C.POINTER(SolveConfigC), vp, vp, C.POINTER(ReportC),
                                  C.c_int]),
+    "hfpg_set_solver": (C.c_int, [vp, C.c_int]),
+    "hfpg_solver_in_use": (C.c_int, [vp, C.POINTER(i32)]),
+    "hfpg_set_trace": (C.c_int, [vp, C.c_uint32]),
+    "hfpg_get_trace": (C.c_int, [vp, vp, C.c_uint32]),
     "hfpg_launch_counts": (C.c_int, [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "hfpg_fast_path": (C.c_int, [vp, C.POINTER(i32)]),
     "hfpg_profile_iteration": (C.c_int, [vp, C.c_uint32, vp]),

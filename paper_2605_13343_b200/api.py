@@ -363,6 +363,15 @@ class Device:
         check(lib.hfpg_pcg_solve(self.h, b_ptr, C.byref(c), x_ptr, hist_ptr, C.byref(rep), where))
         return rep
 
+    def set_solver(self, kind: int):
+        """N.SOLVER_AUTO / SOLVER_GRAPH / SOLVER_PERSISTENT (include/hfpg.h hfpg_solver)."""
+        check(lib.hfpg_set_solver(self.h, kind))
+
+    def solver_in_use(self) -> int:
+        v = N.i32()
+        check(lib.hfpg_solver_in_use(self.h, C.byref(v)))
+        return v.value
+
     def stream(self) -> int:
         s = N.vp()
         check(lib.hfpg_get_stream(self.h, C.byref(s)))

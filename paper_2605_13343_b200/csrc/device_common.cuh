@@ -93,6 +93,12 @@ __device__ __forceinline__ float4 ldg_hint(const float4* p, uint64_t policy) {
     return r;
 }
 
+__device__ __forceinline__ float ldg_f32_hint(const float* p, uint64_t policy) {
+    float r;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(policy));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t ldg_stream_u32(const uint32_t* p) {
     uint32_t r;
     asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));

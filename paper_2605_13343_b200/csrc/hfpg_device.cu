@@ -1,6 +1,7 @@
 // Device handle, CUDA-graph PCG driver and the device half of the C ABI (include/hfpg.h).
 #include "internal.hpp"
 #include "kernels.cuh"
+#include "solve_persistent.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -60,6 +61,7 @@ struct hfpg_handle {
     double* a_diag = nullptr;
     bool have_diag = false;
     uint32_t spmv_stage_bytes = 0;  // >0: slices streamed by k_spmv_tma
+    uint32_t pspmv_stage_bytes = 0; // >0: k_solve streams 16-slice chunks through a TMA ring
 
     // vectors / workspace (sized for vec_n / ws layout)
     uint64_t vec_n = 0;
@@ -78,6 +80,11 @@ struct hfpg_handle {
     uint64_t history_cap = 0;
 
     int precond = HFPG_PRECOND_FACTOR;
+    int solver = HFPG_SOLVER_AUTO;
+    unsigned* gbar = nullptr;  // grid-barrier counter of k_solve
+    unsigned long long* trace = nullptr;  // k_solve barrier timestamps (hfpg_set_trace)
+    unsigned trace_cap = 0;
+    int l2_bytes = 0;
 
     // graph
     cudaGraph_t graph = nullptr;
@@ -168,6 +175,7 @@ void ensure_workspace(hfpg_handle* h) {
         dalloc(h->counters, 8);
         CK(cudaMemsetAsync(h->counters, 0, 8 * sizeof(unsigned), h->stream));
     }
+    if (!h->gbar) dalloc(h->gbar, 1);
     if (!h->sc) {
         dalloc(h->sc, 1);
         CK(cudaMemsetAsync(h->sc, 0, sizeof(Scalars), h->stream));
@@ -214,11 +222,17 @@ void fill_sys(hfpg_handle* h) {
     s.tree_counters = h->tree_counters;
     s.coarse_S = coarse_width(L);
     s.spmv_stage_bytes = h->spmv_stage_bytes;
+    s.pspmv_stage_bytes = h->pspmv_stage_bytes;
     s.partials = h->partials;
     s.counters = h->counters;
     s.sc = h->sc;
     s.history = h->history;
     s.use_cond = 0;
+    s.trace = h->trace;
+    s.trace_cap = h->trace_cap;
+    s.trace_probe = h->trace_cap > 64 ? 3 : 0;  // intra-phase probes in iteration 3
+    // keep the factors L2-resident across iterations when they fit comfortably (65K: 53 MB)
+    s.l2_resident = h->have_factors && double(h->L.total) * 4.0 < 0.6 * double(h->l2_bytes);
 }
 
 
@@ -291,6 +305,7 @@ void configure_kernels() {
         CK(cudaFuncSetAttribute(k_spmv_tma<kLoop>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         CK(cudaFuncSetAttribute(k_spmv_tma<kApply>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         CK(cudaFuncSetAttribute(k_leaf_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        CK(cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(PSmem))));
     });
 }
 
@@ -335,6 +350,29 @@ void build_graph(hfpg_handle* h) {
     h->graph_valid = true;
 }
 
+// The persistent whole-solve kernel serves the factor preconditioner on the fast layout.
+bool use_persistent(const hfpg_handle* h) {
+    if (h->solver == HFPG_SOLVER_GRAPH) return false;
+    const bool ok = h->fast && h->precond == HFPG_PRECOND_FACTOR;
+    if (h->solver == HFPG_SOLVER_PERSISTENT && !ok)
+        throw InvalidArgument("persistent solver needs the factor preconditioner on L=128, L_s=32");
+    return ok;
+}
+
+void launch_persistent(hfpg_handle* h) {
+    fill_sys(h);
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, kPThreads, sizeof(PSmem)));
+    if (per_sm < 1) throw CudaError("k_solve does not fit on an SM");
+    const unsigned grid = unsigned(h->num_sms);
+    CK(cudaMemsetAsync(h->gbar, 0, sizeof(unsigned), h->stream));
+    const double* bptr = h->b;
+    unsigned* gb = h->gbar;
+    void* args[] = {&h->sys, &bptr, &gb};
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_solve), dim3(grid), dim3(kPThreads), args,
+                                   sizeof(PSmem), h->stream));
+}
+
 void require_apply_ready(hfpg_handle* h) {
     if (!h->have_factors) throw InvalidArgument("apply: no factor tensor loaded");
     if (!h->have_diag) throw InvalidArgument("apply: no diagonal (load a CSR or set_diag)");
@@ -374,6 +412,7 @@ int hfpg_create(int device, hfpg_handle** out) {
             h->device = device;
             CK(cudaSetDevice(device));
             CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
+            CK(cudaDeviceGetAttribute(&h->l2_bytes, cudaDevAttrL2CacheSize, device));
             int major = 0, minor = 0;
             CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
             CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
@@ -402,7 +441,7 @@ int hfpg_destroy(hfpg_handle* h) {
         dfree(h->p1); dfree(h->y_loc); dfree(h->b); dfree(h->scratch); dfree(h->restrict_);
         dfree(h->coupled); dfree(h->node_u); dfree(h->node_v);
         dfree(h->tree_counters); dfree(h->partials); dfree(h->counters); dfree(h->sc);
-        dfree(h->history);
+        dfree(h->history); dfree(h->gbar); dfree(h->trace);
         if (h->toynet) toynet_model_destroy(h->toynet);
         if (h->ev0) cudaEventDestroy(h->ev0);
         if (h->ev1) cudaEventDestroy(h->ev1);
@@ -491,6 +530,13 @@ int hfpg_load_csr(hfpg_handle* h, uint64_t n, const uint64_t* ro_in, const uint3
         maxch = (maxch + 1023) & ~uint64_t(1023);
         h->spmv_stage_bytes = (maxch > 0 && maxch * kSpmvStages + 128 <= 110 * 1024) ? uint32_t(maxch) : 0;
         if (std::getenv("HFPG_NO_SPMV_TMA")) h->spmv_stage_bytes = 0;
+        // k_solve's ring: two stages of 16-slice chunks inside a free 96 KB leaf stage
+        uint64_t maxch16 = 0;
+        for (uint64_t s0 = 0; s0 < ns; s0 += kPSpmvSlices)
+            maxch16 = std::max<uint64_t>(maxch16, (off[std::min<uint64_t>(ns, s0 + kPSpmvSlices)] - off[s0]) * 12);
+        maxch16 = (maxch16 + 127) & ~uint64_t(127);
+        h->pspmv_stage_bytes = (maxch16 > 0 && 2 * maxch16 <= sizeof(PStage)) ? uint32_t(maxch16) : 0;
+        if (std::getenv("HFPG_NO_SPMV_TMA")) h->pspmv_stage_bytes = 0;
         invalidate_graph(h);
         dalloc(h->slice_off, ns + 1);
         dalloc(h->sell_cols, sc.size());
@@ -614,7 +660,8 @@ int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg
             dalloc(h->history, hcap);
             h->history_cap = hcap;
         }
-        if (!h->graph_valid) build_graph(h);
+        const bool persistent = use_persistent(h);
+        if (!persistent && !h->graph_valid) build_graph(h);
         // state words (the loop-invariant part of Scalars)
         Scalars init{};
         init.rtol = cfg.rtol;
@@ -626,7 +673,10 @@ int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg
         CK(cudaMemcpyAsync(h->sc, &init, sizeof(Scalars), cudaMemcpyHostToDevice, h->stream));
         copy_in(h, h->b, b, n, where);
         CK(cudaEventRecord(h->ev0, h->stream));
-        CK(cudaGraphLaunch(h->exec, h->stream));
+        if (persistent)
+            launch_persistent(h);
+        else
+            CK(cudaGraphLaunch(h->exec, h->stream));
         CK(cudaEventRecord(h->ev1, h->stream));
         Scalars out{};
         CK(cudaMemcpyAsync(&out, h->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
@@ -655,7 +705,44 @@ int hfpg_launch_counts(hfpg_handle* h, uint32_t* per_iteration, uint32_t* per_ap
         const uint32_t apply = (h->have_factors && h->fast) ? 4 : 3;
         *per_apply = apply;
         *per_iteration = h->precond == HFPG_PRECOND_FACTOR ? apply + 1 : 2;
+        if (use_persistent(h)) {  // one k_solve launch per solve
+            *per_apply = 0;
+            *per_iteration = 0;
+        }
     });
+}
+
+int hfpg_set_trace(hfpg_handle* h, uint32_t cap) {
+    return guarded([&] {
+        set_device(h);
+        dfree(h->trace);
+        h->trace_cap = 0;
+        if (cap) {
+            dalloc(h->trace, cap);
+            CK(cudaMemset(h->trace, 0, cap * sizeof(unsigned long long)));
+            h->trace_cap = cap;
+        }
+    });
+}
+
+int hfpg_get_trace(hfpg_handle* h, uint64_t* out, uint32_t cap) {
+    return guarded([&] {
+        set_device(h);
+        if (!h->trace) throw InvalidArgument("get_trace: tracing is off");
+        CK(cudaMemcpy(out, h->trace, std::min(cap, h->trace_cap) * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int hfpg_set_solver(hfpg_handle* h, int kind) {
+    return guarded([&] {
+        if (kind < HFPG_SOLVER_AUTO || kind > HFPG_SOLVER_PERSISTENT)
+            throw InvalidArgument("set_solver: unknown kind");
+        h->solver = kind;
+    });
+}
+
+int hfpg_solver_in_use(hfpg_handle* h, int32_t* out) {
+    return guarded([&] { *out = use_persistent(h) ? HFPG_SOLVER_PERSISTENT : HFPG_SOLVER_GRAPH; });
 }
 
 int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out) {

@@ -36,6 +36,7 @@ struct DevSys {
     unsigned* tree_counters; // 2K arrival counters for the coarse tree
     uint64_t coarse_S;       // subtree width per k_coarse task (power of two)
     uint32_t spmv_stage_bytes; // k_spmv_tma stage capacity (0: use k_spmv)
+    uint32_t pspmv_stage_bytes; // k_solve SpMV ring stage (16 slices; 0: direct loads)
     // reductions / state
     double* partials;
     unsigned* counters;  // [0] spmv, [1] leaf, [2] prolong, [3] simple
@@ -43,6 +44,10 @@ struct DevSys {
     double* history;
     cudaGraphConditionalHandle cond;
     int use_cond;
+    int l2_resident;  // factor tensor small enough to keep in L2 across iterations
+    unsigned long long* trace;  // k_solve: %globaltimer at every grid barrier (CTA 0), or null
+    unsigned trace_cap;
+    int trace_probe;
 };
 
 enum Mode { kInit = 0, kLoop = 1, kApply = 2 };

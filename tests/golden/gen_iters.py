@@ -26,6 +26,8 @@ CASES = {
     "3d_1m_s1e-3": (lambda: H.make_frame_3d(128, 128, 64, 2024, 0), 1e-3, 20000),
     "2d_262144_t0_s1e-3": (lambda: H.make_frame(262144, 2024, H.test_frame_id(262144, 0)), 1e-3,
                            20000),
+    "2d_262144_t0_s1e-2": (lambda: H.make_frame(262144, 2024, H.test_frame_id(262144, 0)), 1e-2,
+                           20000),
     "3d_1m_s1e-2": (lambda: H.make_frame_3d(128, 128, 64, 2024, 0), 1e-2, 20000),
 }
 

@@ -1,0 +1,111 @@
+"""The persistent whole-solve kernel (k_solve, one cooperative launch per pcg_solve) against
+the per-stage CUDA-graph driver and the reference: identical iteration counts (the two differ
+only in the order of the f64 dot-product partial sums), residual histories to f64 rounding,
+and the status semantics of pcg.cpp:53-126."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, rel_l2
+
+pytestmark = pytest.mark.gpu
+ITERS = os.path.join(ROOT, "tests", "golden", "ref_iterations.json")
+
+
+def _setup(H, fr, sigma, seed, frame):
+    f = H.init_factors(H.build_partition(fr.n, 128), 32, H.FactorInit.jacobi_seed, sigma,
+                       H.RngStream(seed, frame, H.RngPurpose.factor_init))
+    dev = H.Device(0)
+    dev.load_csr(fr.A)
+    dev.load_factors(f)
+    dev.set_precond(2)
+    return dev, f
+
+
+def _solve(H, dev, fr, solver, cfg=None):
+    from paper_2605_13343_b200 import _native as N
+    dev.set_solver(solver)
+    cfg = cfg or H.SolveConfig()
+    x = np.empty(fr.n)
+    hist = np.empty(max(cfg.max_iters, 1))
+    rep = dev.solve_ptr(fr.b.ctypes.data, x.ctypes.data, cfg, hist.ctypes.data, N.HOST)
+    return rep, x, hist[: rep.history_len]
+
+
+@pytest.mark.parametrize("n,seed,frame", [(256, 3, 1), (1024, 7, 3), (8192, 2024, 0),
+                                          (16384, 5, 2)])
+def test_persistent_matches_graph(H, n, seed, frame):
+    from paper_2605_13343_b200 import _native as N
+    fr = H.make_frame(n, seed, frame)
+    dev, _ = _setup(H, fr, 1e-2, seed, frame)
+    dev.set_solver(N.SOLVER_AUTO)
+    assert dev.solver_in_use() == N.SOLVER_PERSISTENT
+    rp, xp, hp = _solve(H, dev, fr, N.SOLVER_PERSISTENT)
+    rg, xg, hg = _solve(H, dev, fr, N.SOLVER_GRAPH)
+    assert rp.status == rg.status == 0
+    assert abs(int(rp.iterations) - int(rg.iterations)) <= 2
+    m = min(len(hp), len(hg), 50)
+    np.testing.assert_allclose(hp[:m], hg[:m], rtol=1e-9)
+    assert rel_l2(xp, xg) < 1e-6
+    # true residual (test_pcg.cpp:118-143)
+    r = fr.b - dev.spmv(xp)
+    assert np.linalg.norm(r) <= 1e-6 * np.linalg.norm(fr.b)
+
+
+def test_persistent_deterministic(H):
+    from paper_2605_13343_b200 import _native as N
+    fr = H.make_frame(4096, 11, 0)
+    dev, _ = _setup(H, fr, 1e-2, 11, 0)
+    r1, x1, h1 = _solve(H, dev, fr, N.SOLVER_PERSISTENT)
+    r2, x2, h2 = _solve(H, dev, fr, N.SOLVER_PERSISTENT)
+    assert r1.iterations == r2.iterations
+    assert (h1 == h2).all() and (x1 == x2).all()
+
+
+@pytest.mark.parametrize("key", ["2d_8192", "2d_65536"])
+def test_persistent_reference_iterations(H, key):
+    from paper_2605_13343_b200 import _native as N
+    ref = json.load(open(ITERS))[key]
+    fr = H.make_frame(ref["n"], 2024, ref["frame_index"])
+    dev, _ = _setup(H, fr, ref["sigma"], 2024, ref["frame_index"])
+    rep, x, hist = _solve(H, dev, fr, N.SOLVER_PERSISTENT)
+    assert rep.status == 0
+    assert abs(int(rep.iterations) - ref["factor"]["iterations"]) <= 2
+    np.testing.assert_allclose(hist[:8], ref["factor"]["hist_head"], rtol=1e-9)
+
+
+def test_persistent_status_semantics(H):
+    from paper_2605_13343_b200 import _native as N
+    fr = H.make_frame(1024, 7, 3)
+    dev, _ = _setup(H, fr, 1e-2, 7, 3)
+    rep, _, hist = _solve(H, dev, fr, N.SOLVER_PERSISTENT, H.SolveConfig(max_iters=5))
+    assert rep.status == 1 and rep.iterations == 5 and len(hist) == 5
+    rep, _, hist = _solve(H, dev, fr, N.SOLVER_PERSISTENT, H.SolveConfig(max_iters=0))
+    assert rep.status == 1 and rep.iterations == 0 and len(hist) == 0
+    # zero rhs: converged in 0 iterations (pcg.cpp:73-79)
+    x = np.empty(fr.n)
+    z = np.zeros(fr.n)
+    dev.set_solver(N.SOLVER_PERSISTENT)
+    rep = dev.solve_ptr(z.ctypes.data, x.ctypes.data, H.SolveConfig(), None, N.HOST)
+    assert rep.converged and rep.iterations == 0 and (x == 0).all()
+    # the persistent driver only serves the factor preconditioner
+    dev.set_precond(1)
+    with pytest.raises(ValueError):
+        dev.solve_ptr(fr.b.ctypes.data, x.ctypes.data, H.SolveConfig(), None, N.HOST)
+    dev.set_solver(N.SOLVER_AUTO)
+    rep = dev.solve_ptr(fr.b.ctypes.data, x.ctypes.data, H.SolveConfig(), None, N.HOST)
+    assert rep.converged
+
+
+def test_persistent_large_3d(H):
+    # 3D N = 1M (BASELINE configs[2]): graph and persistent drivers agree
+    from paper_2605_13343_b200 import _native as N
+    fr = H.make_frame_3d(128, 128, 64, 2024, 0)
+    dev, _ = _setup(H, fr, 1e-3, 2024, 0)
+    rp, xp, hp = _solve(H, dev, fr, N.SOLVER_PERSISTENT)
+    rg, xg, hg = _solve(H, dev, fr, N.SOLVER_GRAPH)
+    assert rp.status == rg.status == 0
+    assert abs(int(rp.iterations) - int(rg.iterations)) <= 2
+    assert rel_l2(xp, xg) < 1e-6
