@@ -185,6 +185,53 @@ int hfpg_spmv(hfpg_handle* h, const double* x, double* y, int where);
 int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg, double* x,
                    double* history, hfpg_report* report, int where);
 
+/* ---- row-partitioned solve (north star: N=16.7M over 8 GPUs) ------------------------------
+ * The system is split along the bisection tree (partition.cpp:9-46): rank r of G (a power of
+ * two, <= 16, >= 2 leaves per rank) owns leaves [r K/G, (r+1) K/G) and rows [r N/G, (r+1) N/G),
+ * with every tile inside its subtree; the G-1 tiles above the rank subtrees are recomputed by
+ * every rank from the exchanged subtree-root strip sums. Per iteration each rank sends three
+ * small f64 messages to every rank (p.Ap/p.p, |r|^2 + root sums, r.z after pushing its z halo
+ * rows into the peers' ghost slots) through device mailboxes over peer memory, and reduces
+ * them in rank order, so all ranks take identical decisions. A partitioned handle solves with
+ * hfpg_pcg_solve on its local slices (b, x: n/G entries) once connected; hfpg_apply /
+ * hfpg_spmv are refused (use hfpg_group_apply). */
+/* Rank `rank`'s share of the GLOBAL system (host pointers): local CSR with ghost columns,
+ * halo lists, and the factor slice — sliced from `packed` (the global packed tensor) or, when
+ * packed == NULL, drawn directly as init_factors(sigma, RngStream(seed, frame, factor_init))
+ * would draw those elements (factor_tensor.cpp:30-39). L = 128, L_s = 32 required. */
+int hfpg_part_load(hfpg_handle* h, uint32_t G, uint32_t rank, uint64_t n, const uint64_t* row_offsets,
+                   const uint32_t* col_indices, const double* values, uint64_t leaf_size,
+                   uint64_t coarse_size, const float* packed, double sigma, uint64_t seed,
+                   uint64_t frame, int32_t spd_enabled, double spd_raw);
+/* out[6] = {n_local, row_begin, n_ghost, halo rows sent, G, rank} */
+int hfpg_part_info(hfpg_handle* h, uint64_t* out);
+/* Device addresses peers write into (mailbox, z) — for ranks sharing a process. */
+int hfpg_part_mailbox(hfpg_handle* h, void** mailbox, void** z);
+/* Peer tables: G device pointers each, valid in h's context (own slot = own buffers). */
+int hfpg_part_connect(hfpg_handle* h, void* const* mailboxes, void* const* zs);
+/* Multi-process: 128 bytes of CUDA IPC handles (mailbox, z) to all-gather, then connect with
+ * the G x 128-byte table (own entry ignored). */
+int hfpg_part_ipc_get(hfpg_handle* h, void* out);
+int hfpg_part_ipc_connect(hfpg_handle* h, const void* all);
+/* All G ranks in this process on one device (e.g. to check a partitioning on one GPU): one
+ * graph over every rank, b / x / r / z are GLOBAL host vectors. */
+int hfpg_group_pcg_solve(hfpg_handle* const* hs, uint32_t G, const double* b,
+                         const hfpg_solve_config* cfg, double* x, double* history,
+                         hfpg_report* report);
+int hfpg_group_apply(hfpg_handle* const* hs, uint32_t G, const double* r, double* z);
+/* Host-only: the partition plan (no GPU). counts[4] = {n_local, n_ghost, halo rows sent,
+ * local nnz}; any array may be NULL (ghost_cols: n_ghost, send_rows/send_slot: halo rows,
+ * send_off: G+1, local_cols: local nnz). */
+int hfpg_part_plan(uint64_t n, const uint64_t* row_offsets, const uint32_t* col_indices,
+                   const double* values, uint64_t leaf_size, uint32_t G, uint32_t rank,
+                   uint64_t* counts, uint32_t* ghost_cols, uint32_t* send_rows, uint32_t* send_slot,
+                   uint64_t* send_off, uint32_t* local_cols);
+/* Host-only: rank's factor slice (local packed tensor of size n/G + (G-1) x L_s^2 top tiles),
+ * sliced from `packed` or drawn from (sigma, seed, frame) when packed == NULL. */
+int hfpg_part_factors(uint64_t n, uint64_t leaf_size, uint64_t coarse_size, uint32_t G, uint32_t rank,
+                      const float* packed, double sigma, uint64_t seed, uint64_t frame,
+                      float* local, float* top);
+
 /* ---- network inference + factor assembly ------------------------------------------------ */
 /* toy_net.cpp:170-223 init_weights(cfg, make_factor_layout(build_partition(n, leaf), coarse),
  * weight_seed) and :322-586 forward(frame, ...) on the GPU (tcgen05 tf32 GEMMs + fp32 kernels;

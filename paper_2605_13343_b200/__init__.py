@@ -11,4 +11,6 @@ from .api import (Checkpoint, CsrMatrix, Device, FactorInit, FactorLayout, Facto
                   make_frame_3d, packed_width, pcg_solve, read_checkpoint, test_frame_id,
                   toynet_forward, train_frame_id, write_checkpoint)
 
+from .partition import PartitionGroup, RankSolver  # noqa: E402
+
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -91,6 +91,20 @@ _PROTOS = {
     "hfpg_solver_in_use": (C.c_int, [vp, C.POINTER(i32)]),
     "hfpg_set_trace": (C.c_int, [vp, C.c_uint32]),
     "hfpg_get_trace": (C.c_int, [vp, vp, C.c_uint32]),
+    "hfpg_part_load": (C.c_int, [vp, C.c_uint32, C.c_uint32, u64, vp, vp, vp, u64, u64, vp, dbl, u64,
+                                 u64, i32, dbl]),
+    "hfpg_part_info": (C.c_int, [vp, vp]),
+    "hfpg_part_mailbox": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp)]),
+    "hfpg_part_connect": (C.c_int, [vp, vp, vp]),
+    "hfpg_part_ipc_get": (C.c_int, [vp, vp]),
+    "hfpg_part_ipc_connect": (C.c_int, [vp, vp]),
+    "hfpg_group_pcg_solve": (C.c_int, [vp, C.c_uint32, vp, C.POINTER(SolveConfigC), vp, vp,
+                                       C.POINTER(ReportC)]),
+    "hfpg_group_apply": (C.c_int, [vp, C.c_uint32, vp, vp]),
+    "hfpg_part_plan": (C.c_int, [u64, vp, vp, vp, u64, C.c_uint32, C.c_uint32, vp, vp, vp, vp, vp,
+                                 vp]),
+    "hfpg_part_factors": (C.c_int, [u64, u64, u64, C.c_uint32, C.c_uint32, vp, dbl, u64, u64, vp,
+                                    vp]),
     "hfpg_launch_counts": (C.c_int, [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "hfpg_fast_path": (C.c_int, [vp, C.POINTER(i32)]),
     "hfpg_profile_iteration": (C.c_int, [vp, C.c_uint32, vp]),

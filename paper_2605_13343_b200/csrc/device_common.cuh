@@ -27,6 +27,7 @@ struct Scalars {
     int converged;
     int done;      // loop finished: every later kernel of the iteration early-exits
     int pad;
+    double rr_loc; // row partition: this rank's |r|^2 partial (leaf -> strip-sum kernel)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

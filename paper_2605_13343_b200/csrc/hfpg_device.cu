@@ -2,6 +2,7 @@
 #include "internal.hpp"
 #include "kernels.cuh"
 #include "solve_persistent.cuh"
+#include "partition_host.hpp"
 
 #include <algorithm>
 #include <cstdlib>
@@ -40,6 +41,7 @@ struct hfpg_handle {
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t lstream = nullptr;  // stream the launch_* helpers use (a group capture redirects it)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
     // factors
@@ -93,6 +95,23 @@ struct hfpg_handle {
 
     DevSys sys{};
     ToynetModel* toynet = nullptr;
+
+    // row partition (G > 1): this handle holds rank `rank`'s share of a system
+    struct Part {
+        uint32_t G = 1, rank = 0, glog = 0;
+        uint64_t n_ghost = 0, row0 = 0, n_global = 0, halo_send = 0;
+        float* top_tiles = nullptr;
+        float* top_coupled = nullptr;
+        Mailbox* mbox = nullptr;
+        Mailbox** peer_mbox = nullptr;  // device array of G
+        double** peer_z = nullptr;      // device array of G
+        uint32_t *send_rows = nullptr, *send_slot = nullptr;
+        unsigned long long* send_off = nullptr;
+        unsigned long long* seq = nullptr;
+        bool connected = false;
+        std::vector<void*> ipc_opened;
+    } part;
+    uint64_t vec_ng = 0;  // ghost entries the z/p vectors were sized for
 };
 
 namespace {
@@ -126,9 +145,9 @@ size_t spmv_smem(const hfpg_handle* h) { return h->spmv_stage_bytes ? 128 + size
 template <int MODE>
 void launch_spmv(hfpg_handle* h, const DevSys& s, const double* x, double* y) {
     if (h->spmv_stage_bytes)
-        k_spmv_tma<MODE><<<unsigned(spmv_grid(h)), 256, spmv_smem(h), h->stream>>>(s, x, y);
+        k_spmv_tma<MODE><<<unsigned(spmv_grid(h)), 256, spmv_smem(h), h->lstream>>>(s, x, y);
     else
-        k_spmv<MODE><<<unsigned(spmv_grid(h)), 256, 0, h->stream>>>(s, x, y);
+        k_spmv<MODE><<<unsigned(spmv_grid(h)), 256, 0, h->lstream>>>(s, x, y);
 }
 uint64_t simple_grid(const hfpg_handle* h) {
     return std::max<uint64_t>(1, std::min<uint64_t>((h->n + 255) / 256, uint64_t(h->num_sms) * 8));
@@ -137,14 +156,20 @@ uint64_t simple_grid(const hfpg_handle* h) {
 // (Re)allocate the per-n vectors and the per-layout apply workspace.
 void ensure_workspace(hfpg_handle* h) {
     const uint64_t n = h->n;
-    if (h->vec_n != n) {
+    if (h->vec_n != n || h->vec_ng != h->part.n_ghost) {
         invalidate_graph(h);
+        const uint64_t ng = h->part.n_ghost;  // peers' rows read by this rank's SpMV
         dalloc(h->x, n);
         dalloc(h->r, n);
-        dalloc(h->z, n);
+        dalloc(h->z, n + ng);
         dalloc(h->ap, n);
-        dalloc(h->p0, n);
-        dalloc(h->p1, n);
+        dalloc(h->p0, n + ng);
+        dalloc(h->p1, n + ng);
+        h->vec_ng = ng;
+        if (ng) {
+            CK(cudaMemset(h->z, 0, (n + ng) * 8));
+            CK(cudaMemset(h->p1, 0, (n + ng) * 8));
+        }
         dalloc(h->y_loc, n);
         dalloc(h->b, n);
         dalloc(h->scratch, n);
@@ -230,6 +255,19 @@ void fill_sys(hfpg_handle* h) {
     s.use_cond = 0;
     s.trace = h->trace;
     s.trace_cap = h->trace_cap;
+    s.G = h->part.G;
+    s.rank = h->part.rank;
+    s.glog = h->part.glog;
+    s.n_ghost = h->part.n_ghost;
+    s.top_tiles = h->part.top_tiles;
+    s.top_coupled = h->part.top_coupled;
+    s.mbox = h->part.mbox;
+    s.peer_mbox = h->part.peer_mbox;
+    s.peer_z = h->part.peer_z;
+    s.send_rows = h->part.send_rows;
+    s.send_slot = h->part.send_slot;
+    s.send_off = h->part.send_off;
+    s.seq = h->part.seq;
     s.trace_probe = h->trace_cap > 64 ? 3 : 0;  // intra-phase probes in iteration 3
     // keep the factors L2-resident across iterations when they fit comfortably (65K: 53 MB)
     s.l2_resident = h->have_factors && double(h->L.total) * 4.0 < 0.6 * double(h->l2_bytes);
@@ -240,16 +278,14 @@ void fill_sys(hfpg_handle* h) {
 void launch_coarse(hfpg_handle* h, const DevSys& s, int mode) {
     const Layout& L = h->L;
     if (h->fast) {
-        const uint64_t S = std::min<uint64_t>(L.k, kCoarseS0), R = L.k / S;
-        if (S > 1) {
-            k_coarse_sums<<<unsigned(R), 256, 0, h->stream>>>(s, mode);
-            CK(cudaGetLastError());
-        }
-        const uint64_t grid = (R - 1) + ((L.k - 1) - (R - 1) + kTileWarps - 1) / kTileWarps;
-        k_coarse_tiles<<<unsigned(grid), 32 * kTileWarps, 0, h->stream>>>(s, mode);
+        const uint64_t R = L.k / std::min<uint64_t>(L.k, kCoarseS0);
+        k_sums_tree<<<unsigned(std::min<uint64_t>(R, uint64_t(h->num_sms))), kSumsThreads, 0, h->lstream>>>(s, mode);
+        CK(cudaGetLastError());
+        const uint64_t tw = (L.k - 1 + kTilesThreads / 32 - 1) / (kTilesThreads / 32);
+        k_tiles_all<<<unsigned(std::max<uint64_t>(1, std::min<uint64_t>(tw, uint64_t(h->num_sms) * 2))), kTilesThreads, 0, h->lstream>>>(s, mode);
     } else {
         const uint64_t S0 = std::min<uint64_t>(L.k, coarse_width(L));
-        k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->stream>>>(s, mode);
+        k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->lstream>>>(s, mode);
     }
     CK(cudaGetLastError());
 }
@@ -259,16 +295,16 @@ void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
     const DevSys& s = h->sys;
     const Layout& L = h->L;
     if (h->fast) {
-        k_leaf_fast<<<unsigned(leaf_grid(h)), kLeafThreads, sizeof(LeafSmem), h->stream>>>(s, mode, rin);
+        k_leaf_fast<<<unsigned(leaf_grid(h)), kLeafThreads, sizeof(LeafSmem), h->lstream>>>(s, mode, rin);
     } else {
-        k_leaf_generic<<<unsigned(L.k), 256, 2 * L.l * sizeof(float), h->stream>>>(s, mode, rin);
+        k_leaf_generic<<<unsigned(L.k), 256, 2 * L.l * sizeof(float), h->lstream>>>(s, mode, rin);
     }
     CK(cudaGetLastError());
     launch_coarse(h, s, mode);
     if (h->fast)
-        k_prolong_fast<<<unsigned(prolong_grid(h)), 256, 0, h->stream>>>(s, mode, rin, zout);
+        k_prolong_fast<<<unsigned(prolong_grid(h)), 256, 0, h->lstream>>>(s, mode, rin, zout);
     else
-        k_prolong_generic<<<unsigned(L.k), 256, 2 * L.ls * sizeof(float), h->stream>>>(s, mode, rin, zout);
+        k_prolong_generic<<<unsigned(L.k), 256, 2 * L.ls * sizeof(float), h->lstream>>>(s, mode, rin, zout);
     CK(cudaGetLastError());
 }
 
@@ -279,19 +315,19 @@ void launch_iteration(hfpg_handle* h) {
     if (h->precond == HFPG_PRECOND_FACTOR) {
         launch_apply(h, kLoop, nullptr, nullptr);
     } else {
-        k_simple<<<unsigned(simple_grid(h)), 256, 0, h->stream>>>(s, kLoop, h->precond == HFPG_PRECOND_JACOBI);
+        k_simple<<<unsigned(simple_grid(h)), 256, 0, h->lstream>>>(s, kLoop, h->precond == HFPG_PRECOND_JACOBI);
         CK(cudaGetLastError());
     }
 }
 
 void launch_init(hfpg_handle* h) {
     const DevSys& s = h->sys;
-    k_init<<<unsigned(simple_grid(h)), 256, 0, h->stream>>>(s, h->b);
+    k_init<<<unsigned(simple_grid(h)), 256, 0, h->lstream>>>(s, h->b);
     CK(cudaGetLastError());
     if (h->precond == HFPG_PRECOND_FACTOR) {
         launch_apply(h, kInit, nullptr, nullptr);
     } else {
-        k_simple<<<unsigned(simple_grid(h)), 256, 0, h->stream>>>(s, kInit, h->precond == HFPG_PRECOND_JACOBI);
+        k_simple<<<unsigned(simple_grid(h)), 256, 0, h->lstream>>>(s, kInit, h->precond == HFPG_PRECOND_JACOBI);
         CK(cudaGetLastError());
     }
 }
@@ -353,7 +389,7 @@ void build_graph(hfpg_handle* h) {
 // The persistent whole-solve kernel serves the factor preconditioner on the fast layout.
 bool use_persistent(const hfpg_handle* h) {
     if (h->solver == HFPG_SOLVER_GRAPH) return false;
-    const bool ok = h->fast && h->precond == HFPG_PRECOND_FACTOR;
+    const bool ok = h->fast && h->precond == HFPG_PRECOND_FACTOR && h->part.G == 1;
     if (h->solver == HFPG_SOLVER_PERSISTENT && !ok)
         throw InvalidArgument("persistent solver needs the factor preconditioner on L=128, L_s=32");
     return ok;
@@ -391,6 +427,139 @@ void copy_out(hfpg_handle* h, double* dst, const double* src, uint64_t count, in
                        h->stream));
 }
 
+// Device copy of a (local) CSR with n rows: diagonal, |A|_F (fro < 0: computed here, else the
+// global value of a partitioned system), SELL-32 layout. Columns are < n + n_ghost.
+void upload_csr(hfpg_handle* h, uint64_t n, const std::vector<uint64_t>& ro,
+                const std::vector<uint32_t>& ci, const std::vector<double>& vv, double fro_in) {
+        // csr.cpp:52-58 diagonal, csr.cpp:64-68 Frobenius norm (sequential, as the reference)
+    std::vector<double> diag(n, 0.0);
+    double fro = 0.0;
+    for (uint64_t i = 0; i < n; ++i)
+        for (uint64_t p = ro[i]; p < ro[i + 1]; ++p)
+            if (ci[p] == i) diag[i] = vv[p];
+    for (double v : vv) fro += v * v;
+    h->fro = fro_in < 0.0 ? std::sqrt(fro) : fro_in;
+    h->diag_positive = std::all_of(diag.begin(), diag.end(), [](double d) { return d > 0.0; });
+    // SELL-32: slice s holds rows 32s..32s+31, width = longest row, column-major inside;
+    // padding = (own row, 0.0) so padded FMAs add exactly +0.
+    const uint64_t ns = (n + 31) / 32;
+    std::vector<unsigned long long> off(ns + 1, 0);
+    for (uint64_t s = 0; s < ns; ++s) {
+        uint64_t w = 0;
+        for (uint64_t r = 32 * s; r < std::min(n, 32 * s + 32); ++r) w = std::max(w, ro[r + 1] - ro[r]);
+        off[s + 1] = off[s] + 32 * w;
+    }
+    std::vector<uint32_t> sc(off[ns]);
+    std::vector<double> sv(off[ns]);
+    for (uint64_t s = 0; s < ns; ++s) {
+        const uint64_t w = (off[s + 1] - off[s]) / 32;
+        for (uint64_t lane = 0; lane < 32; ++lane) {
+            const uint64_t r = 32 * s + lane;
+            for (uint64_t j = 0; j < w; ++j) {
+                const uint64_t idx = off[s] + j * 32 + lane;
+                if (r < n && j < ro[r + 1] - ro[r]) {
+                    sc[idx] = ci[ro[r] + j];
+                    sv[idx] = vv[ro[r] + j];
+                } else {
+                    sc[idx] = uint32_t(std::min(r, n - 1));
+                    sv[idx] = 0.0;
+                }
+            }
+        }
+    }
+    if (h->n != n) {
+        h->n = n;
+    }
+    // k_spmv_tma stage capacity: the largest 8-slice chunk, if three stages leave room for
+    // at least two CTAs per SM
+    uint64_t maxch = 0;
+    for (uint64_t s0 = 0; s0 < ns; s0 += 8)
+        maxch = std::max<uint64_t>(maxch, (off[std::min(ns, s0 + 8)] - off[s0]) * 12);
+    maxch = (maxch + 1023) & ~uint64_t(1023);
+    h->spmv_stage_bytes = (maxch > 0 && maxch * kSpmvStages + 128 <= 110 * 1024) ? uint32_t(maxch) : 0;
+    if (std::getenv("HFPG_NO_SPMV_TMA")) h->spmv_stage_bytes = 0;
+    // k_solve's ring: two stages of 16-slice chunks inside a free 96 KB leaf stage
+    uint64_t maxch16 = 0;
+    for (uint64_t s0 = 0; s0 < ns; s0 += kPSpmvSlices)
+        maxch16 = std::max<uint64_t>(maxch16, (off[std::min<uint64_t>(ns, s0 + kPSpmvSlices)] - off[s0]) * 12);
+    maxch16 = (maxch16 + 127) & ~uint64_t(127);
+    h->pspmv_stage_bytes = (maxch16 > 0 && 2 * maxch16 <= sizeof(PStage)) ? uint32_t(maxch16) : 0;
+    if (std::getenv("HFPG_NO_SPMV_TMA")) h->pspmv_stage_bytes = 0;
+    invalidate_graph(h);
+    dalloc(h->slice_off, ns + 1);
+    dalloc(h->sell_cols, sc.size());
+    dalloc(h->sell_vals, sv.size());
+    dalloc(h->a_diag, n);
+    CK(cudaMemcpy(h->slice_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->sell_cols, sc.data(), sc.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->sell_vals, sv.data(), sv.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->a_diag, diag.data(), n * 8, cudaMemcpyHostToDevice));
+    h->have_csr = true;
+    h->have_diag = true;
+    ensure_workspace(h);
+}
+
+
+
+// ---- row partition (G > 1) ---------------------------------------------------------------
+void reset_partition(hfpg_handle* h) {
+    auto& P = h->part;
+    for (void* q : P.ipc_opened) cudaIpcCloseMemHandle(q);
+    P.ipc_opened.clear();
+    dfree(P.top_tiles); dfree(P.top_coupled); dfree(P.mbox); dfree(P.peer_mbox); dfree(P.peer_z);
+    dfree(P.send_rows); dfree(P.send_slot); dfree(P.send_off); dfree(P.seq);
+    P = hfpg_handle::Part{};
+    invalidate_graph(h);
+}
+
+void require_part_ready(hfpg_handle* h) {
+    if (h->part.G > 1 && !h->part.connected)
+        throw InvalidArgument("partition: rank not connected to its peers (hfpg_part_connect)");
+}
+
+// The apply's stages for stage-ordered multi-rank launches (one stream, rank after rank).
+void stage_leaf(hfpg_handle* h, int mode, const double* rin) {
+    k_leaf_fast<<<unsigned(leaf_grid(h)), kLeafThreads, sizeof(LeafSmem), h->lstream>>>(h->sys, mode, rin);
+    CK(cudaGetLastError());
+}
+void stage_prolong(hfpg_handle* h, int mode, const double* rin, double* zout) {
+    k_prolong_fast<<<unsigned(prolong_grid(h)), 256, 0, h->lstream>>>(h->sys, mode, rin, zout);
+    CK(cudaGetLastError());
+}
+void stage_sums(hfpg_handle* h, int mode) {
+    const uint64_t R = h->L.k / std::min<uint64_t>(h->L.k, kCoarseS0);
+    k_sums_tree<<<unsigned(std::min<uint64_t>(R, uint64_t(h->num_sms))), kSumsThreads, 0, h->lstream>>>(h->sys, mode);
+    CK(cudaGetLastError());
+}
+void stage_tiles(hfpg_handle* h, int mode) {
+    const uint64_t tw = (h->L.k - 1 + kTilesThreads / 32 - 1) / (kTilesThreads / 32);
+    k_tiles_all<<<unsigned(std::max<uint64_t>(1, std::min<uint64_t>(tw, uint64_t(h->num_sms) * 2))), kTilesThreads, 0, h->lstream>>>(h->sys, mode);
+    CK(cudaGetLastError());
+}
+
+// Per-solve state words (the loop-invariant part of Scalars).
+Scalars solve_scalars(const hfpg_handle* h, const hfpg_solve_config& cfg) {
+    Scalars init{};
+    init.rtol = cfg.rtol;
+    init.max_iters = cfg.max_iters;
+    init.breakdown_tol = 1e-12 * h->fro;  // pcg.cpp:80
+    init.shift = (h->precond == HFPG_PRECOND_FACTOR && h->spd_enabled) ? std::log1p(std::exp(h->spd_raw)) : 0.0;
+    init.status = 1;
+    return init;
+}
+
+void check_group(hfpg_handle* const* hs, uint32_t G) {
+    if (G < 2 || G > kMaxRanks) throw InvalidArgument("group: rank count must be in [2, 16]");
+    for (uint32_t r = 0; r < G; ++r) {
+        hfpg_handle* h = hs[r];
+        if (!h || h->part.G != G || h->part.rank != r)
+            throw InvalidArgument("group: handle " + std::to_string(r) + " is not rank " + std::to_string(r) + " of " + std::to_string(G));
+        if (h->device != hs[0]->device) throw InvalidArgument("group: all ranks must share a device");
+        require_part_ready(h);
+        require_apply_ready(h);
+        if (!h->fast) throw InvalidArgument("group: fast layout (L=128, L_s=32) required");
+    }
+}
 }  // namespace
 
 extern "C" {
@@ -420,6 +589,7 @@ int hfpg_create(int device, hfpg_handle** out) {
                 throw CudaError("hfpg is built for sm_100a (B200); device is sm_" +
                                 std::to_string(major) + std::to_string(minor));
             CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+            h->lstream = h->stream;
             CK(cudaEventCreate(&h->ev0));
             CK(cudaEventCreate(&h->ev1));
             configure_kernels();
@@ -442,6 +612,7 @@ int hfpg_destroy(hfpg_handle* h) {
         dfree(h->coupled); dfree(h->node_u); dfree(h->node_v);
         dfree(h->tree_counters); dfree(h->partials); dfree(h->counters); dfree(h->sc);
         dfree(h->history); dfree(h->gbar); dfree(h->trace);
+        reset_partition(h);
         if (h->toynet) toynet_model_destroy(h->toynet);
         if (h->ev0) cudaEventDestroy(h->ev0);
         if (h->ev1) cudaEventDestroy(h->ev1);
@@ -483,72 +654,8 @@ int hfpg_load_csr(hfpg_handle* h, uint64_t n, const uint64_t* ro_in, const uint3
         }
         for (uint64_t p = 0; p < nnz; ++p)
             if (ci[p] >= n) throw InvalidArgument("csr: column index out of range");
-        // csr.cpp:52-58 diagonal, csr.cpp:64-68 Frobenius norm (sequential, as the reference)
-        std::vector<double> diag(n, 0.0);
-        double fro = 0.0;
-        for (uint64_t i = 0; i < n; ++i)
-            for (uint64_t p = ro[i]; p < ro[i + 1]; ++p)
-                if (ci[p] == i) diag[i] = vv[p];
-        for (double v : vv) fro += v * v;
-        h->fro = std::sqrt(fro);
-        h->diag_positive = std::all_of(diag.begin(), diag.end(), [](double d) { return d > 0.0; });
-        // SELL-32: slice s holds rows 32s..32s+31, width = longest row, column-major inside;
-        // padding = (own row, 0.0) so padded FMAs add exactly +0.
-        const uint64_t ns = (n + 31) / 32;
-        std::vector<unsigned long long> off(ns + 1, 0);
-        for (uint64_t s = 0; s < ns; ++s) {
-            uint64_t w = 0;
-            for (uint64_t r = 32 * s; r < std::min(n, 32 * s + 32); ++r) w = std::max(w, ro[r + 1] - ro[r]);
-            off[s + 1] = off[s] + 32 * w;
-        }
-        std::vector<uint32_t> sc(off[ns]);
-        std::vector<double> sv(off[ns]);
-        for (uint64_t s = 0; s < ns; ++s) {
-            const uint64_t w = (off[s + 1] - off[s]) / 32;
-            for (uint64_t lane = 0; lane < 32; ++lane) {
-                const uint64_t r = 32 * s + lane;
-                for (uint64_t j = 0; j < w; ++j) {
-                    const uint64_t idx = off[s] + j * 32 + lane;
-                    if (r < n && j < ro[r + 1] - ro[r]) {
-                        sc[idx] = ci[ro[r] + j];
-                        sv[idx] = vv[ro[r] + j];
-                    } else {
-                        sc[idx] = uint32_t(std::min(r, n - 1));
-                        sv[idx] = 0.0;
-                    }
-                }
-            }
-        }
-        if (h->n != n) {
-            h->n = n;
-        }
-        // k_spmv_tma stage capacity: the largest 8-slice chunk, if three stages leave room for
-        // at least two CTAs per SM
-        uint64_t maxch = 0;
-        for (uint64_t s0 = 0; s0 < ns; s0 += 8)
-            maxch = std::max<uint64_t>(maxch, (off[std::min(ns, s0 + 8)] - off[s0]) * 12);
-        maxch = (maxch + 1023) & ~uint64_t(1023);
-        h->spmv_stage_bytes = (maxch > 0 && maxch * kSpmvStages + 128 <= 110 * 1024) ? uint32_t(maxch) : 0;
-        if (std::getenv("HFPG_NO_SPMV_TMA")) h->spmv_stage_bytes = 0;
-        // k_solve's ring: two stages of 16-slice chunks inside a free 96 KB leaf stage
-        uint64_t maxch16 = 0;
-        for (uint64_t s0 = 0; s0 < ns; s0 += kPSpmvSlices)
-            maxch16 = std::max<uint64_t>(maxch16, (off[std::min<uint64_t>(ns, s0 + kPSpmvSlices)] - off[s0]) * 12);
-        maxch16 = (maxch16 + 127) & ~uint64_t(127);
-        h->pspmv_stage_bytes = (maxch16 > 0 && 2 * maxch16 <= sizeof(PStage)) ? uint32_t(maxch16) : 0;
-        if (std::getenv("HFPG_NO_SPMV_TMA")) h->pspmv_stage_bytes = 0;
-        invalidate_graph(h);
-        dalloc(h->slice_off, ns + 1);
-        dalloc(h->sell_cols, sc.size());
-        dalloc(h->sell_vals, sv.size());
-        dalloc(h->a_diag, n);
-        CK(cudaMemcpy(h->slice_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(h->sell_cols, sc.data(), sc.size() * 4, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(h->sell_vals, sv.data(), sv.size() * 8, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(h->a_diag, diag.data(), n * 8, cudaMemcpyHostToDevice));
-        h->have_csr = true;
-        h->have_diag = true;
-        ensure_workspace(h);
+        if (h->part.G > 1) reset_partition(h);
+        upload_csr(h, n, ro, ci, vv, -1.0);
     });
 }
 
@@ -607,6 +714,7 @@ int hfpg_set_precond(hfpg_handle* h, int kind) {
 int hfpg_apply(hfpg_handle* h, const double* r, double* z, int where) {
     return guarded([&] {
         set_device(h);
+        if (h->part.G > 1) throw InvalidArgument("apply: partitioned handle (use hfpg_group_apply)");
         require_apply_ready(h);
         ensure_workspace(h);
         fill_sys(h);
@@ -627,6 +735,7 @@ int hfpg_apply(hfpg_handle* h, const double* r, double* z, int where) {
 int hfpg_spmv(hfpg_handle* h, const double* x, double* y, int where) {
     return guarded([&] {
         set_device(h);
+        if (h->part.G > 1) throw InvalidArgument("spmv: partitioned handle");
         if (!h->have_csr) throw InvalidArgument("spmv: no matrix loaded");
         ensure_workspace(h);
         fill_sys(h);
@@ -652,6 +761,7 @@ int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg
         if (!(cfg.rtol > 0.0)) throw InvalidArgument("pcg_solve: rtol must be positive");
         if (!h->have_csr) throw InvalidArgument("pcg_solve: no matrix loaded");
         if (h->precond == HFPG_PRECOND_FACTOR) require_apply_ready(h);
+        require_part_ready(h);
         ensure_workspace(h);
         const uint64_t n = h->n;
         const uint64_t hcap = std::max<uint64_t>(cfg.max_iters, 1);
@@ -662,14 +772,7 @@ int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg
         }
         const bool persistent = use_persistent(h);
         if (!persistent && !h->graph_valid) build_graph(h);
-        // state words (the loop-invariant part of Scalars)
-        Scalars init{};
-        init.rtol = cfg.rtol;
-        init.max_iters = cfg.max_iters;
-        init.breakdown_tol = 1e-12 * h->fro;  // pcg.cpp:80
-        init.shift = (h->precond == HFPG_PRECOND_FACTOR && h->spd_enabled)
-                         ? std::log1p(std::exp(h->spd_raw)) : 0.0;
-        init.status = 1;
+        const Scalars init = solve_scalars(h, cfg);
         CK(cudaMemcpyAsync(h->sc, &init, sizeof(Scalars), cudaMemcpyHostToDevice, h->stream));
         copy_in(h, h->b, b, n, where);
         CK(cudaEventRecord(h->ev0, h->stream));
@@ -843,6 +946,260 @@ int hfpg_toynet_forward(hfpg_handle* h, const hfpg_frame_view* frame, uint64_t l
 
 int hfpg_fast_path(hfpg_handle* h, int32_t* out) {
     return guarded([&] { *out = h->have_factors && h->fast ? 1 : 0; });
+}
+
+
+// ---- row partition ------------------------------------------------------------------------
+int hfpg_part_load(hfpg_handle* h, uint32_t G, uint32_t rank, uint64_t n, const uint64_t* ro,
+                   const uint32_t* ci, const double* v, uint64_t leaf, uint64_t ls,
+                   const float* packed, double sigma, uint64_t seed, uint64_t frame,
+                   int32_t spd_enabled, double spd_raw) {
+    return guarded([&] {
+        set_device(h);
+        if (leaf != uint64_t(kL) || ls != uint64_t(kLs))
+            throw InvalidArgument("partition: fast layout (L=128, L_s=32) required");
+        PartPlan P = plan_partition(n, ro, ci, v, leaf, G, rank);
+        reset_partition(h);
+        auto& S = h->part;
+        S.G = G;
+        S.rank = rank;
+        S.glog = uint32_t(P.glog);
+        S.n_ghost = P.ghost_cols.size();
+        S.row0 = P.row0;
+        S.n_global = n;
+        S.halo_send = P.send_rows.size();
+        h->have_factors = false;
+        h->n = 0;
+        upload_csr(h, P.n_loc, P.local.row_offsets, P.local.cols, P.local.vals, P.fro);
+        // factor slice: the rank's leaves, subtree tiles, bridges and gate + the G-1 top tiles
+        const Layout Lg = make_layout(n, leaf, ls), Ll = make_layout(P.n_loc, leaf, ls);
+        std::vector<float> loc(Ll.total), top((G - 1) * ls * ls);
+        if (packed) slice_factors(Lg, packed, G, rank, loc.data(), top.data());
+        else init_factors_slice(Lg, G, rank, sigma, seed, frame, loc.data(), top.data());
+        dalloc(h->F, Ll.total);
+        CK(cudaMemcpy(h->F, loc.data(), Ll.total * 4, cudaMemcpyHostToDevice));
+        h->L = Ll;
+        h->have_factors = true;
+        h->spd_enabled = spd_enabled;
+        h->spd_raw = spd_raw;
+        h->fast = true;
+        h->precond = HFPG_PRECOND_FACTOR;
+        ensure_workspace(h);
+        dalloc(S.top_tiles, top.size());
+        CK(cudaMemcpy(S.top_tiles, top.data(), top.size() * 4, cudaMemcpyHostToDevice));
+        dalloc(S.top_coupled, (G - 1) * 64);
+        dalloc(S.send_rows, P.send_rows.size());
+        dalloc(S.send_slot, P.send_slot.size());
+        dalloc(S.send_off, G + 1);
+        if (!P.send_rows.empty()) {
+            CK(cudaMemcpy(S.send_rows, P.send_rows.data(), P.send_rows.size() * 4, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(S.send_slot, P.send_slot.data(), P.send_slot.size() * 4, cudaMemcpyHostToDevice));
+        }
+        std::vector<unsigned long long> so(P.send_off.begin(), P.send_off.end());
+        CK(cudaMemcpy(S.send_off, so.data(), so.size() * 8, cudaMemcpyHostToDevice));
+        dalloc(S.mbox, 1);
+        CK(cudaMemset(S.mbox, 0, sizeof(Mailbox)));
+        dalloc(S.seq, 3);
+        CK(cudaMemset(S.seq, 0, 3 * 8));
+        dalloc(S.peer_mbox, G);
+        dalloc(S.peer_z, G);
+        const double shift = spd_enabled ? std::log1p(std::exp(spd_raw)) : 0.0;
+        CK(cudaMemcpy(&h->sc->shift, &shift, 8, cudaMemcpyHostToDevice));
+        CK(cudaDeviceSynchronize());
+    });
+}
+
+int hfpg_part_info(hfpg_handle* h, uint64_t* out) {
+    return guarded([&] {
+        out[0] = h->part.G > 1 ? h->n : h->n;
+        out[1] = h->part.row0;
+        out[2] = h->part.n_ghost;
+        out[3] = h->part.halo_send;
+        out[4] = h->part.G;
+        out[5] = h->part.rank;
+    });
+}
+
+int hfpg_part_mailbox(hfpg_handle* h, void** mailbox, void** z) {
+    return guarded([&] {
+        if (h->part.G < 2) throw InvalidArgument("partition: handle holds no partition");
+        *mailbox = h->part.mbox;
+        *z = h->z;
+    });
+}
+
+int hfpg_part_connect(hfpg_handle* h, void* const* mailboxes, void* const* zs) {
+    return guarded([&] {
+        set_device(h);
+        auto& S = h->part;
+        if (S.G < 2) throw InvalidArgument("partition: handle holds no partition");
+        if (mailboxes[S.rank] != S.mbox || zs[S.rank] != h->z)
+            throw InvalidArgument("partition: own slot of the peer table is not this rank");
+        CK(cudaMemcpy(S.peer_mbox, mailboxes, S.G * sizeof(void*), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(S.peer_z, zs, S.G * sizeof(void*), cudaMemcpyHostToDevice));
+        S.connected = true;
+        invalidate_graph(h);
+    });
+}
+
+int hfpg_part_ipc_get(hfpg_handle* h, void* out) {
+    return guarded([&] {
+        set_device(h);
+        if (h->part.G < 2) throw InvalidArgument("partition: handle holds no partition");
+        cudaIpcMemHandle_t a, b;
+        CK(cudaIpcGetMemHandle(&a, h->part.mbox));
+        CK(cudaIpcGetMemHandle(&b, h->z));
+        std::memcpy(out, &a, sizeof(a));
+        std::memcpy(static_cast<char*>(out) + 64, &b, sizeof(b));
+    });
+}
+
+int hfpg_part_ipc_connect(hfpg_handle* h, const void* all) {
+    return guarded([&] {
+        set_device(h);
+        auto& S = h->part;
+        if (S.G < 2) throw InvalidArgument("partition: handle holds no partition");
+        std::vector<void*> mb(S.G), zz(S.G);
+        for (uint32_t q = 0; q < S.G; ++q) {
+            if (q == S.rank) {
+                mb[q] = S.mbox;
+                zz[q] = h->z;
+                continue;
+            }
+            cudaIpcMemHandle_t a, b;
+            std::memcpy(&a, static_cast<const char*>(all) + 128 * q, sizeof(a));
+            std::memcpy(&b, static_cast<const char*>(all) + 128 * q + 64, sizeof(b));
+            CK(cudaIpcOpenMemHandle(&mb[q], a, cudaIpcMemLazyEnablePeerAccess));
+            S.ipc_opened.push_back(mb[q]);
+            CK(cudaIpcOpenMemHandle(&zz[q], b, cudaIpcMemLazyEnablePeerAccess));
+            S.ipc_opened.push_back(zz[q]);
+        }
+        CK(cudaMemcpy(S.peer_mbox, mb.data(), S.G * sizeof(void*), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(S.peer_z, zz.data(), S.G * sizeof(void*), cudaMemcpyHostToDevice));
+        S.connected = true;
+        invalidate_graph(h);
+    });
+}
+
+// In-process group: every rank's kernels in ONE graph on rank 0's stream, stage by stage, so a
+// stage's messages are complete before any rank's next stage waits on them.
+int hfpg_group_pcg_solve(hfpg_handle* const* hs, uint32_t G, const double* b,
+                         const hfpg_solve_config* cfg_in, double* x, double* history,
+                         hfpg_report* report) {
+    return guarded([&] {
+        check_group(hs, G);
+        hfpg_handle* h0 = hs[0];
+        set_device(h0);
+        hfpg_solve_config cfg = cfg_in ? *cfg_in : hfpg_solve_config{1e-8, 20000};
+        if (!(cfg.rtol > 0.0)) throw InvalidArgument("pcg_solve: rtol must be positive");
+        const uint64_t nl = h0->n, hcap = std::max<uint64_t>(cfg.max_iters, 1);
+        for (uint32_t r = 0; r < G; ++r) {
+            hfpg_handle* h = hs[r];
+            ensure_workspace(h);
+            if (h->history_cap < hcap) {
+                dalloc(h->history, hcap);
+                h->history_cap = hcap;
+            }
+            const Scalars init = solve_scalars(h, cfg);
+            CK(cudaMemcpyAsync(h->sc, &init, sizeof(Scalars), cudaMemcpyHostToDevice, h0->stream));
+            CK(cudaMemcpyAsync(h->b, b + r * nl, nl * 8, cudaMemcpyHostToDevice, h0->stream));
+        }
+        cudaGraph_t graph;
+        CK(cudaGraphCreate(&graph, 0));
+        cudaGraphConditionalHandle cond;
+        CK(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+        for (uint32_t r = 0; r < G; ++r) {
+            fill_sys(hs[r]);
+            hs[r]->sys.cond = cond;
+            hs[r]->sys.use_cond = 1;
+            hs[r]->lstream = h0->stream;
+        }
+        auto each = [&](auto&& fn) { for (uint32_t r = 0; r < G; ++r) fn(hs[r]); };
+        CK(cudaStreamBeginCaptureToGraph(h0->stream, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        each([&](hfpg_handle* h) { k_init<<<unsigned(simple_grid(h)), 256, 0, h0->stream>>>(h->sys, h->b); });
+        each([&](hfpg_handle* h) { stage_leaf(h, kInit, nullptr); });
+        each([&](hfpg_handle* h) { stage_sums(h, kInit); });
+        each([&](hfpg_handle* h) { stage_tiles(h, kInit); });
+        each([&](hfpg_handle* h) { stage_prolong(h, kInit, nullptr, nullptr); });
+        CK(cudaStreamEndCapture(h0->stream, &graph));
+        size_t nn = 0;
+        CK(cudaGraphGetNodes(graph, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+        cudaGraphNode_t sink = nullptr;
+        for (auto nd : nodes) {
+            size_t nout = 0;
+            CK(cudaGraphNodeGetDependentNodes(nd, nullptr, &nout));
+            if (nout == 0) sink = nd;
+        }
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = cond;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cnode;
+        CK(cudaGraphAddNode(&cnode, graph, &sink, 1, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        CK(cudaStreamBeginCaptureToGraph(h0->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        each([&](hfpg_handle* h) { launch_spmv<kLoop>(h, h->sys, nullptr, nullptr); CK(cudaGetLastError()); });
+        each([&](hfpg_handle* h) { stage_leaf(h, kLoop, nullptr); });
+        each([&](hfpg_handle* h) { stage_sums(h, kLoop); });
+        each([&](hfpg_handle* h) { stage_tiles(h, kLoop); });
+        each([&](hfpg_handle* h) { stage_prolong(h, kLoop, nullptr, nullptr); });
+        CK(cudaStreamEndCapture(h0->stream, &body));
+        for (uint32_t r = 0; r < G; ++r) hs[r]->lstream = hs[r]->stream;
+        cudaGraphExec_t exec;
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+        CK(cudaEventRecord(h0->ev0, h0->stream));
+        CK(cudaGraphLaunch(exec, h0->stream));
+        CK(cudaEventRecord(h0->ev1, h0->stream));
+        Scalars out{};
+        CK(cudaMemcpyAsync(&out, h0->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h0->stream));
+        if (x)
+            for (uint32_t r = 0; r < G; ++r)
+                CK(cudaMemcpyAsync(x + r * nl, hs[r]->x, nl * 8, cudaMemcpyDeviceToHost, h0->stream));
+        CK(cudaStreamSynchronize(h0->stream));
+        if (history && out.hist_len) {
+            CK(cudaMemcpy(history, h0->history, out.hist_len * 8, cudaMemcpyDeviceToHost));
+        }
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h0->ev0, h0->ev1));
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
+        if (report) {
+            report->n = nl * G;
+            report->iterations = out.iterations;
+            report->converged = out.converged;
+            report->status = out.status;
+            report->breakdown_iter = out.breakdown_iter;
+            report->history_len = out.hist_len;
+            report->wall_ms = ms;
+        }
+    });
+}
+
+int hfpg_group_apply(hfpg_handle* const* hs, uint32_t G, const double* r_in, double* z_out) {
+    return guarded([&] {
+        check_group(hs, G);
+        hfpg_handle* h0 = hs[0];
+        set_device(h0);
+        const uint64_t nl = h0->n;
+        for (uint32_t r = 0; r < G; ++r) {
+            ensure_workspace(hs[r]);
+            fill_sys(hs[r]);
+            hs[r]->lstream = h0->stream;
+            CK(cudaMemcpyAsync(hs[r]->scratch, r_in + r * nl, nl * 8, cudaMemcpyHostToDevice, h0->stream));
+        }
+        for (uint32_t r = 0; r < G; ++r) stage_leaf(hs[r], kApply, hs[r]->scratch);
+        for (uint32_t r = 0; r < G; ++r) stage_sums(hs[r], kApply);
+        for (uint32_t r = 0; r < G; ++r) stage_tiles(hs[r], kApply);
+        for (uint32_t r = 0; r < G; ++r) stage_prolong(hs[r], kApply, hs[r]->scratch, hs[r]->z);
+        for (uint32_t r = 0; r < G; ++r) {
+            hs[r]->lstream = hs[r]->stream;
+            CK(cudaMemcpyAsync(z_out + r * nl, hs[r]->z, nl * 8, cudaMemcpyDeviceToHost, h0->stream));
+        }
+        CK(cudaStreamSynchronize(h0->stream));
+    });
 }
 
 }  // extern "C"

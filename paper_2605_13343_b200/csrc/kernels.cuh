@@ -13,6 +13,7 @@
 #pragma once
 
 #include "device_common.cuh"
+#include "comm.cuh"
 
 namespace hfpg {
 
@@ -48,6 +49,18 @@ struct DevSys {
     unsigned long long* trace;  // k_solve: %globaltimer at every grid barrier (CTA 0), or null
     unsigned trace_cap;
     int trace_probe;
+    // row partition over G ranks (G == 1: the whole system). n, K, D above are this rank's.
+    uint32_t G, rank, glog;
+    uint64_t n_ghost;               // ghost entries of z, p0, p1 after the n owned rows
+    const float* top_tiles;         // the G-1 tiles above the rank subtrees (global heap order)
+    float* top_coupled;             // (G-1) x 64: [coupled_row | coupled_col]
+    Mailbox* mbox;                  // this rank's mailbox
+    Mailbox* const* peer_mbox;      // G mailboxes (device array of pointers)
+    double* const* peer_z;          // G z vectors (their ghost regions start at n)
+    const uint32_t* send_rows;      // halo: local rows pushed to peers, grouped by peer
+    const uint32_t* send_slot;      //       destination ghost slot in that peer
+    const unsigned long long* send_off;  // G + 1
+    unsigned long long* seq;        // 3 message sequence counters (monotonic across solves)
 };
 
 enum Mode { kInit = 0, kLoop = 1, kApply = 2 };
@@ -78,6 +91,61 @@ __device__ __forceinline__ void finish_residual(Scalars* sc, double* history, do
     }
 }
 
+
+// ---- row partition (G > 1) helpers -------------------------------------------------------
+// SpMV prologue: beta = rz_{k-1} / rz_{k-2} from the last M3 (k >= 2; beta = 0 at k = 1) —
+// the same division the single-rank prolong epilogue does (pcg.cpp:115-117) — and the ghost
+// entries of the new p (peers' rows this rank reads), p = z + beta p_prev like owned rows.
+__device__ __forceinline__ double part_spmv_beta(const DevSys& s, unsigned long long k, const double* pprev,
+                                                 double* pnew) {
+    __shared__ double sb;
+    if (threadIdx.x == 0) {
+        double beta = 0.0;
+        if (k >= 2) {
+            const unsigned long long q3 = s.seq[2];
+            mb_wait<2>(s.mbox, s.G, q3);
+            beta = mb_sum<2>(s.mbox, s.G, q3, 0) / s.sc->rz;
+        }
+        sb = beta;
+    }
+    __syncthreads();
+    const double beta = sb;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < s.n_ghost;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        pnew[s.n + i] = fma(beta, pprev[s.n + i], s.z[s.n + i]);
+    return beta;
+}
+
+// The last CTA of a partitioned SpMV: send M1 = {p.Ap, p.p} partials (warp 0).
+__device__ __forceinline__ void part_send_m1(const DevSys& s, double pap, double pp) {
+    if (threadIdx.x >= 32) return;
+    __shared__ double pay[2];
+    unsigned long long seq = 0;
+    if (threadIdx.x == 0) {
+        seq = ++s.seq[0];
+        pay[0] = pap;
+        pay[1] = pp;
+    }
+    seq = __shfl_sync(0xffffffffu, seq, 0);
+    __syncwarp();
+    mb_send<0>(s.peer_mbox, s.G, s.rank, seq, pay, 2);
+}
+
+// Single-rank SpMV epilogue (last CTA, thread 0): breakdown test and alpha (pcg.cpp:88-96).
+__device__ __forceinline__ void spmv_epilogue(const DevSys& s, unsigned long long k, double pap, double p2) {
+    Scalars* sc = s.sc;
+    sc->pap = pap;
+    sc->pp = p2;
+    if (pap < -sc->breakdown_tol * p2 || pap == 0.0) {  // pcg.cpp:90-95
+        sc->status = 2;
+        sc->breakdown_iter = k;
+        sc->iterations = k;
+        sc->done = 1;
+    } else {
+        sc->alpha = sc->rz / pap;
+    }
+}
+
 // ============================================================================================
 // SpMV on SELL-32 (slices of 32 rows, column-major inside a slice, padded with (row, 0.0)).
 // One thread per row: every load is coalesced and each row accumulates sequentially in the
@@ -88,11 +156,11 @@ template <int MODE>  // kInit unused; kLoop = PCG, kApply = plain y = A x
 __global__ void __launch_bounds__(256) k_spmv(DevSys s, const double* xin, double* yout) {
     if (MODE == kLoop && s.sc->done) return;
     const unsigned long long k = MODE == kLoop ? s.sc->k : 0ULL;
-    const double beta = MODE == kLoop ? s.sc->beta : 0.0;
     const double* z = MODE == kLoop ? s.z : xin;
     const double* pp_ = MODE == kLoop ? p_prev(s, k) : nullptr;
     double* pnew = MODE == kLoop ? p_cur(s, k) : nullptr;
     double* y = MODE == kLoop ? s.ap : yout;
+    const double beta = MODE != kLoop ? 0.0 : s.G > 1 ? part_spmv_beta(s, k, pp_, pnew) : s.sc->beta;
     double v[2] = {0.0, 0.0};
     // persistent grid-stride over rows: one CTA partial (and one fence) per CTA, not per row
     for (uint64_t row = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < s.n;
@@ -131,20 +199,9 @@ __global__ void __launch_bounds__(256) k_spmv(DevSys s, const double* xin, doubl
     }
     if (MODE != kLoop) return;
     double tot[2];
-    if (grid_reduce_last<2>(v, s.partials, &s.counters[0], tot) && threadIdx.x == 0) {
-        Scalars* sc = s.sc;
-        const double pap = tot[0], p2 = tot[1];
-        sc->pap = pap;
-        sc->pp = p2;
-        // pcg.cpp:90-95 breakdown test, reported not thrown
-        if (pap < -sc->breakdown_tol * p2 || pap == 0.0) {
-            sc->status = 2;
-            sc->breakdown_iter = k;
-            sc->iterations = k;
-            sc->done = 1;
-        } else {
-            sc->alpha = sc->rz / pap;
-        }
+    if (grid_reduce_last<2>(v, s.partials, &s.counters[0], tot)) {
+        if (s.G > 1) part_send_m1(s, tot[0], tot[1]);
+        else if (threadIdx.x == 0) spmv_epilogue(s, k, tot[0], tot[1]);
     }
 }
 
@@ -162,11 +219,11 @@ __global__ void __launch_bounds__(256) k_spmv_tma(DevSys s, const double* xin, d
     unsigned char* buf = sraw + 128;
     const uint32_t cap = s.spmv_stage_bytes;
     const unsigned long long k = MODE == kLoop ? s.sc->k : 0ULL;
-    const double beta = MODE == kLoop ? s.sc->beta : 0.0;
     const double* z = MODE == kLoop ? s.z : xin;
     const double* pp_ = MODE == kLoop ? p_prev(s, k) : nullptr;
     double* pnew = MODE == kLoop ? p_cur(s, k) : nullptr;
     double* y = MODE == kLoop ? s.ap : yout;
+    const double beta = MODE != kLoop ? 0.0 : s.G > 1 ? part_spmv_beta(s, k, pp_, pnew) : s.sc->beta;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t nsl = (s.n + 31) >> 5, nch = (nsl + 7) >> 3;
     const uint64_t pol = policy_evict_first();
@@ -232,19 +289,9 @@ __global__ void __launch_bounds__(256) k_spmv_tma(DevSys s, const double* xin, d
     }
     if (MODE != kLoop) return;
     double tot[2];
-    if (grid_reduce_last<2>(v, s.partials, &s.counters[0], tot) && threadIdx.x == 0) {
-        Scalars* sc = s.sc;
-        const double pap = tot[0], p2 = tot[1];
-        sc->pap = pap;
-        sc->pp = p2;
-        if (pap < -sc->breakdown_tol * p2 || pap == 0.0) {  // pcg.cpp:90-95
-            sc->status = 2;
-            sc->breakdown_iter = k;
-            sc->iterations = k;
-            sc->done = 1;
-        } else {
-            sc->alpha = sc->rz / pap;
-        }
+    if (grid_reduce_last<2>(v, s.partials, &s.counters[0], tot)) {
+        if (s.G > 1) part_send_m1(s, tot[0], tot[1]);
+        else if (threadIdx.x == 0) spmv_epilogue(s, k, tot[0], tot[1]);
     }
 }
 
@@ -292,13 +339,48 @@ struct LeafSmem {
     uint64_t full[2];
 };
 
+
+// Partitioned leaf prologue: wait for every rank's M1, alpha = rz_{k-1} / p.Ap with the rank-
+// ordered totals, breakdown test (pcg.cpp:88-96). Every CTA computes the same; CTA 0 records
+// the scalars. Returns false (all CTAs) on breakdown.
+__device__ __forceinline__ bool part_leaf_alpha(const DevSys& s, double& alpha) {
+    __shared__ double sa;
+    __shared__ int sok;
+    if (threadIdx.x == 0) {
+        const unsigned long long q1 = s.seq[0], q3 = s.seq[2];
+        mb_wait<0>(s.mbox, s.G, q1);
+        const double pap = mb_sum<0>(s.mbox, s.G, q1, 0), p2 = mb_sum<0>(s.mbox, s.G, q1, 1);
+        const double rz = mb_sum<2>(s.mbox, s.G, q3, 0);  // rz_{k-1}: awaited by the SpMV
+        Scalars* sc = s.sc;
+        const bool brk = pap < -sc->breakdown_tol * p2 || pap == 0.0;
+        sok = !brk;
+        sa = rz / pap;
+        if (blockIdx.x == 0) {
+            sc->pap = pap;
+            sc->pp = p2;
+            sc->alpha = sa;
+            sc->rz = rz;  // the next SpMV's beta denominator
+            if (brk) {
+                sc->status = 2;
+                sc->breakdown_iter = sc->k;
+                sc->iterations = sc->k;
+                sc->done = 1;
+            }
+        }
+    }
+    __syncthreads();
+    alpha = sa;
+    return sok != 0;
+}
+
 __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mode,
                                                                const double* rin_ext) {
     if (mode != kApply && s.sc->done) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     LeafSmem& sm = *reinterpret_cast<LeafSmem*>(smem_raw);
     const int tid = threadIdx.x;
-    const double alpha = mode == kLoop ? s.sc->alpha : 0.0;
+    double alpha = mode == kLoop ? s.sc->alpha : 0.0;
+    if (s.G > 1 && mode == kLoop && !part_leaf_alpha(s, alpha)) return;
     const double* rsrc = mode == kApply ? rin_ext : s.r;
     const double* pcur = mode == kLoop ? p_cur(s, s.sc->k) : nullptr;
     const uint64_t K = s.K;
@@ -420,8 +502,10 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mod
     }
     if (mode == kApply) return;
     double v[1] = {rr}, tot[1];
-    if (grid_reduce_last<1>(v, s.partials, &s.counters[1], tot) && tid == 0)
-        leaf_epilogue(s, mode, tot[0]);
+    if (grid_reduce_last<1>(v, s.partials, &s.counters[1], tot) && tid == 0) {
+        if (s.G > 1) s.sc->rr_loc = tot[0];  // reduced across ranks after the strip sums (M2)
+        else leaf_epilogue(s, mode, tot[0]);
+    }
 }
 
 // Leaf kernel, generic path (any L, L_s): one CTA per leaf, factors read from global.
@@ -665,6 +749,222 @@ __global__ void __launch_bounds__(32 * kTileWarps) k_coarse_tiles(DevSys s, int 
     tile_warp32(u4, v4, sr[warp], sc[warp], lane, scratch[warp], s.coupled + m * 64 + 32, s.coupled + m * 64);
 }
 
+
+// ============================================================================================
+// Coarse stage, graph path (also the row-partitioned solve): strip sums, then every tile.
+// ============================================================================================
+// One tile (L_s = 32, rank 16) per warp, without shared staging of the factors: lanes q < 16
+// read column q of U (lanes 16 + q: of V) from L2 and run the fp32 chain
+// coef = sum_p U[p][q] float(s_r[p]) in p order (matvec_t); lane j then forms
+// coupled_col[j] = float(sum_q V[j][q] coef_r[q]) and coupled_row[j] = float(sum_q U[j][q]
+// coef_c[q]) with exact f64 products summed in q order (matvec, apply.cpp:121-138) — bit-
+// identical to the reference. f32<->f64 conversions run at 15.6/clk/SM (measured), so the strip
+// sums are cast once per tile and each coefficient is converted once and broadcast through
+// shared memory. T = the tile's U (V = T + 512); out = [coupled_row (32) | coupled_col (32)].
+struct TileScratch {
+    float fr[32], fc[32];
+    double coef[32];
+};
+__device__ __forceinline__ void tile_couple(const float* T, double sr_p, double sc_p, TileScratch& ws,
+                                            int lane, uint64_t pol, float* out) {
+    const float* colp = T + (lane < 16 ? 0 : kLs * 16) + (lane & 15);
+    float cv[32];
+#pragma unroll
+    for (int p = 0; p < 32; ++p) cv[p] = ldg_f32_hint(colp + p * 16, pol);
+    float4 u4[4], v4[4];
+    const float4* U = reinterpret_cast<const float4*>(T) + lane * 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        u4[i] = ldg_hint(U + i, pol);
+        v4[i] = ldg_hint(U + 128 + i, pol);
+    }
+    ws.fr[lane] = float(sr_p);  // apply.cpp:121-124 (strip sums cast to T)
+    ws.fc[lane] = float(sc_p);
+    __syncwarp();
+    const float4* st4 = reinterpret_cast<const float4*>(lane < 16 ? ws.fr : ws.fc);
+    float coef = 0.f;
+#pragma unroll
+    for (int p4 = 0; p4 < 8; ++p4) {
+        const float4 sv = st4[p4];
+        coef = fmaf(cv[4 * p4 + 0], sv.x, coef);
+        coef = fmaf(cv[4 * p4 + 1], sv.y, coef);
+        coef = fmaf(cv[4 * p4 + 2], sv.z, coef);
+        coef = fmaf(cv[4 * p4 + 3], sv.w, coef);
+    }
+    ws.coef[lane] = double(coef);  // [0,16): U^T s_r, [16,32): V^T s_c
+    __syncwarp();
+    double acc_c = 0.0, acc_r = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float uu[4] = {u4[i].x, u4[i].y, u4[i].z, u4[i].w};
+        const float vv[4] = {v4[i].x, v4[i].y, v4[i].z, v4[i].w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int qq = 4 * i + t;
+            acc_c += double(vv[t]) * ws.coef[qq];
+            acc_r += double(uu[t]) * ws.coef[16 + qq];
+        }
+    }
+    __stcg(&out[32 + lane], float(acc_c));
+    __stcg(&out[lane], float(acc_r));
+    __syncwarp();
+}
+
+// Strip sums (apply.cpp:110-120) over this rank's bisection tree in one launch. A CTA takes an
+// aligned subtree of S <= 32 leaves: warp w owns 4 of the 64 sum columns (u: 0-31, v: 32-63),
+// lane q holds leaf q, and a shuffle butterfly builds the pairwise f64 up-sweep (after the step
+// of distance d every lane holds its (2d)-group's sum = left + right child, the heap sums
+// node[u] = node[2u+1] + node[2u+2]); the first lane of each group writes the node. The last
+// CTA to finish among S2 sibling subtrees (arrival counter) continues one level up with their
+// roots as its leaves, up to the root. Partitioned: the CTA that finishes the rank's root sends
+// M2 = {|r|^2 partial, root sums}.
+constexpr int kSumsThreads = 512;
+__global__ void __launch_bounds__(kSumsThreads) k_sums_tree(DevSys s, int mode) {
+    if (mode != kApply && s.sc->done) return;
+    __shared__ int last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t K = s.K, D = s.D;
+    const uint64_t S0 = K < kCoarseS0 ? K : kCoarseS0, R = K / S0;
+    const int side = warp >> 3, c0 = 4 * (warp & 7);  // side 0: u columns, 1: v columns
+    double* node = side ? s.node_v : s.node_u;
+    for (uint64_t task0 = blockIdx.x; task0 < R; task0 += gridDim.x) {
+        uint64_t task = task0, dlo = D;
+        for (int level = 0;; ++level) {
+            const uint64_t cnt = 1ULL << dlo;
+            const uint64_t S = cnt < kCoarseS0 ? cnt : kCoarseS0;
+            int logS = 0;
+            while ((1ULL << logS) < S) ++logS;
+            const uint64_t dr = dlo - logS;
+            double v[4] = {0.0, 0.0, 0.0, 0.0};
+            if (uint64_t(lane) < S) {
+                if (level == 0) {
+                    const float4 f = __ldcg(reinterpret_cast<const float4*>(
+                        &s.restrict_[(task * S + lane) * 64 + 32 * side + c0]));
+                    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+                } else {
+                    const uint64_t g = (1ULL << dlo) - 1 + task * S + lane;
+                    const double2 a = __ldcg(reinterpret_cast<const double2*>(&node[g * 32 + c0]));
+                    const double2 bb = __ldcg(reinterpret_cast<const double2*>(&node[g * 32 + c0 + 2]));
+                    v[0] = a.x; v[1] = a.y; v[2] = bb.x; v[3] = bb.y;
+                }
+            }
+            for (int l2 = 0; l2 < logS; ++l2) {  // step 2^l2 -> nodes at local depth logS-1-l2
+                const int d = 1 << l2;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) v[c] += __shfl_xor_sync(0xffffffffu, v[c], d);
+                const int ld = logS - 1 - l2;
+                if (uint64_t(lane) < S && (lane & (2 * d - 1)) == 0) {
+                    const uint64_t g = (1ULL << (dr + ld)) - 1 + task * (1ULL << ld) + uint64_t(lane >> (l2 + 1));
+                    __stcg(reinterpret_cast<double2*>(&node[g * 32 + c0]), make_double2(v[0], v[1]));
+                    __stcg(reinterpret_cast<double2*>(&node[g * 32 + c0 + 2]), make_double2(v[2], v[3]));
+                }
+            }
+            if (dr == 0) {  // the rank's root: node 0
+                if (s.G > 1) {
+                    __syncthreads();
+                    if (warp == 0) {
+                        __shared__ double pay[kM2Len];
+                        unsigned long long seq = 0;
+                        if (lane == 0) {
+                            seq = ++s.seq[1];
+                            pay[0] = mode == kApply ? 0.0 : s.sc->rr_loc;
+                            pay[1] = 0.0;
+                        }
+                        pay[2 + lane] = __ldcg(&s.node_u[lane]);
+                        pay[34 + lane] = __ldcg(&s.node_v[lane]);
+                        seq = __shfl_sync(0xffffffffu, seq, 0);
+                        __syncwarp();
+                        mb_send<1>(s.peer_mbox, s.G, s.rank, seq, pay, kM2Len);
+                    }
+                }
+                break;
+            }
+            __threadfence();
+            __syncthreads();
+            const uint64_t cnt2 = 1ULL << dr;
+            const uint64_t S2 = cnt2 < kCoarseS0 ? cnt2 : kCoarseS0;
+            int logS2 = 0;
+            while ((1ULL << logS2) < S2) ++logS2;
+            if (tid == 0) {
+                const uint64_t parent = (1ULL << (dr - logS2)) - 1 + task / S2;
+                const unsigned t = atomicAdd(&s.tree_counters[parent], 1u);
+                last = (t == S2 - 1);
+                if (last) s.tree_counters[parent] = 0u;
+            }
+            __syncthreads();
+            if (!last) break;
+            __threadfence();
+            task /= S2;
+            dlo = dr;
+        }
+    }
+}
+
+// Tile couplings (apply.cpp:121-138): every tile of the rank's tree in parallel, one warp each,
+// dealt across CTAs first (tile t -> CTA t mod grid); children sums from the node arrays (leaf
+// children: the restrictions). Partitioned: CTA 0 first waits for every rank's M2, finishes the
+// residual bookkeeping with the rank-ordered |r|^2 (r0 at init, rel / history / stop in the
+// loop — pcg.cpp:73-112) and computes the G-1 top tiles from the rank-root sums (same pairwise
+// order as a single-rank up-sweep), identically on every rank.
+constexpr int kTilesThreads = 512;
+__global__ void __launch_bounds__(kTilesThreads) k_tiles_all(DevSys s, int mode) {
+    if (mode != kApply && s.sc->done) return;
+    __shared__ TileScratch ws[kTilesThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint64_t pol = policy_evict_last();
+    if (s.G > 1 && blockIdx.x == 0) {
+        __shared__ int stop;
+        __shared__ unsigned long long q2s;
+        if (threadIdx.x == 0) {
+            const unsigned long long q2 = s.seq[1];
+            mb_wait<1>(s.mbox, s.G, q2);
+            q2s = q2;
+            stop = 0;
+            if (mode != kApply) {
+                const double rr = mb_sum<1>(s.mbox, s.G, q2, 0);
+                if (mode == kInit) leaf_epilogue(s, kInit, rr);
+                else finish_residual(s.sc, s.history, rr);
+                stop = s.sc->done;
+            }
+        }
+        __syncthreads();
+        if (!stop && wid < int(s.G) - 1) {
+            // top tile t = wid over the rank-root tree (its leaves: heap nodes G-1 .. 2G-2 =
+            // ranks); strip sums of its children: pairwise sums of the covered ranks' roots
+            const unsigned G = s.G, t = unsigned(wid);
+            const int par = int(q2s & 1);
+            double sum[2];
+#pragma unroll
+            for (int sd = 0; sd < 2; ++sd) {
+                const unsigned c = 2 * t + 1 + sd;  // left child (u sums) / right child (v sums)
+                unsigned dc = 0;
+                while ((2u << dc) <= c + 1) ++dc;
+                const unsigned span = G >> dc, a = (c + 1 - (1u << dc)) * span;
+                double acc[kMaxRanksDev];
+                for (unsigned i = 0; i < span; ++i) acc[i] = __ldcg(&s.mbox->m2[par][a + i][2 + 32 * sd + lane]);
+                for (unsigned w2 = 1; w2 < span; w2 *= 2)
+                    for (unsigned i = 0; i + w2 < span; i += 2 * w2) acc[i] += acc[i + w2];
+                sum[sd] = acc[0];
+            }
+            tile_couple(s.top_tiles + uint64_t(t) * (kLs * kLs), sum[0], sum[1], ws[wid], lane, pol,
+                        s.top_coupled + uint64_t(t) * 64);
+        }
+    }
+    const uint64_t K = s.K, G = gridDim.x;
+    for (uint64_t m = uint64_t(wid) * G + blockIdx.x; m < K - 1; m += G * (kTilesThreads / 32)) {
+        const uint64_t l = 2 * m + 1, r = 2 * m + 2;  // children (heap)
+        double a, bb;
+        if (l >= K - 1) {
+            a = double(__ldcg(&s.restrict_[(l - (K - 1)) * 64 + lane]));
+            bb = double(__ldcg(&s.restrict_[(r - (K - 1)) * 64 + 32 + lane]));
+        } else {
+            a = __ldcg(&s.node_u[l * 32 + lane]);
+            bb = __ldcg(&s.node_v[r * 32 + lane]);
+        }
+        tile_couple(s.F + s.tile_base + m * (kLs * kLs), a, bb, ws[wid], lane, pol, s.coupled + m * 64);
+    }
+}
+
 constexpr int kCoarseThreads = 256;
 
 // Shared-memory bytes of k_coarse for a given L_s and subtree width Smax.
@@ -843,6 +1143,48 @@ __device__ __forceinline__ bool prolong_skip(const DevSys& s, int mode) {
     return true;
 }
 
+
+// Partitioned prolong epilogue (last CTA, all threads): push the halo rows of z into the
+// peers' ghost slots, send M3 = {r.z partial}, then the iteration bookkeeping (beta is formed by
+// the next SpMV from the rank-ordered r.z totals).
+__device__ __forceinline__ void part_prolong_epilogue(const DevSys& s, int mode, double rz_loc) {
+    const uint64_t nsend = s.send_off[s.G];
+    for (uint64_t i = threadIdx.x; i < nsend; i += blockDim.x) {
+        unsigned q = 0;
+        while (s.send_off[q + 1] <= i) ++q;
+        s.peer_z[q][s.n + s.send_slot[i]] = __ldcg(&s.z[s.send_rows[i]]);
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        __shared__ double pay[2];
+        unsigned long long seq = 0;
+        if (threadIdx.x == 0) {
+            seq = ++s.seq[2];
+            pay[0] = rz_loc;
+            pay[1] = 0.0;
+        }
+        seq = __shfl_sync(0xffffffffu, seq, 0);
+        __syncwarp();
+        mb_send<2>(s.peer_mbox, s.G, s.rank, seq, pay, 2);
+    }
+    if (threadIdx.x == 0) {
+        Scalars* sc = s.sc;
+        if (mode == kInit) {
+            sc->beta = 0.0;
+            sc->k = 1;
+            if (sc->max_iters == 0) {
+                sc->iterations = 0;
+                sc->status = 1;
+                sc->done = 1;
+            }
+        } else {
+            sc->k += 1;
+        }
+        if (s.use_cond) cudaGraphSetConditional(s.cond, sc->done ? 0u : 1u);
+    }
+}
+
 // Prolongation, fast path: one warp per leaf, no shared-memory staging and no block
 // barriers. Leaves are walked in REVERSE order: the leaf kernel streamed the bridges with an
 // evict_last policy, so the ones it read last are still in L2 here. Per leaf a warp
@@ -882,8 +1224,15 @@ __global__ void __launch_bounds__(256, 2) k_prolong_fast(DevSys s, int mode, con
             }
         }
         // f64 gathers in tile order, root first (apply.cpp:140-154): lane j ends with
-        // g_r[j] (rows halves) and g_c[j] (column halves)
+        // g_r[j] (rows halves) and g_c[j] (column halves). Partitioned: the top tiles (depth <
+        // log2 G) come first and are the same for every leaf of the rank.
         double gr = 0.0, gc = 0.0;
+        for (uint32_t d = 0; d < s.glog; ++d) {
+            const uint32_t t = ((s.G + s.rank) >> (s.glog - d)) - 1u, right = (s.rank >> (s.glog - 1 - d)) & 1u;
+            const double gv = double(__ldcg(&s.top_coupled[t * 64u + right * 32u + lane]));
+            if (right) gc += gv;
+            else gr += gv;
+        }
 #pragma unroll
         for (int d = 0; d < kMaxDepth; ++d)
             if (uint32_t(d) < Du) {
@@ -963,8 +1312,10 @@ __global__ void __launch_bounds__(256, 2) k_prolong_fast(DevSys s, int mode, con
     }
     if (mode == kApply) return;
     double v[1] = {rz}, tot[1];
-    if (grid_reduce_last<1>(v, s.partials, &s.counters[2], tot) && threadIdx.x == 0)
-        prolong_epilogue(s, mode, tot[0]);
+    if (grid_reduce_last<1>(v, s.partials, &s.counters[2], tot)) {
+        if (s.G > 1) part_prolong_epilogue(s, mode, tot[0]);
+        else if (threadIdx.x == 0) prolong_epilogue(s, mode, tot[0]);
+    }
 }
 
 __global__ void __launch_bounds__(256) k_prolong_generic(DevSys s, int mode,
@@ -1048,6 +1399,9 @@ __global__ void k_init(DevSys s, const double* b) {
         s.r[i] = b[i];
         s.p0[i] = 0.0;  // p_prev of iteration 1 (k = 1 -> p_prev = p0)
     }
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < s.n_ghost;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        s.p0[s.n + i] = 0.0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         Scalars* sc = s.sc;
         sc->k = 0;
