@@ -93,20 +93,19 @@ __device__ __forceinline__ void finish_residual(Scalars* sc, double* history, do
 
 
 // ---- row partition (G > 1) helpers -------------------------------------------------------
-// SpMV prologue: beta = rz_{k-1} / rz_{k-2} from the last M3 (k >= 2; beta = 0 at k = 1) —
+// SpMV prologue: wait for the last M3 (its z halo rows), beta = rz_{k-1} / rz_{k-2} (k >= 2;
+// beta = 0 at k = 1) —
 // the same division the single-rank prolong epilogue does (pcg.cpp:115-117) — and the ghost
 // entries of the new p (peers' rows this rank reads), p = z + beta p_prev like owned rows.
 __device__ __forceinline__ double part_spmv_beta(const DevSys& s, unsigned long long k, const double* pprev,
                                                  double* pnew) {
     __shared__ double sb;
     if (threadIdx.x == 0) {
-        double beta = 0.0;
-        if (k >= 2) {
-            const unsigned long long q3 = s.seq[2];
-            mb_wait<2>(s.mbox, s.G, q3);
-            beta = mb_sum<2>(s.mbox, s.G, q3, 0) / s.sc->rz;
-        }
-        sb = beta;
+        // always wait: even at k = 1 (beta = 0) the SpMV reads the z halo rows the peers pushed
+        // before their M3 (the init apply's)
+        const unsigned long long q3 = s.seq[2];
+        mb_wait<2>(s.mbox, s.G, q3);
+        sb = k >= 2 ? mb_sum<2>(s.mbox, s.G, q3, 0) / s.sc->rz : 0.0;
     }
     __syncthreads();
     const double beta = sb;
