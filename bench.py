@@ -2,15 +2,20 @@
 """Benchmark: one step = one PCG solve to rel. residual 1e-8 of a synthetic pressure-Poisson
 system with the hierarchical-factor preconditioner, on B200 through libhfpg's C ABI.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3d_1m|2d_65536|2d_8192]
-                  [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 3d_1m|2d_65536|2d_262144|2d_8192|batch_262k|part_16m]
 
 Default workload (N=1): BASELINE.json configs[2] — N = 1,048,576 (128x128x64 3D 7-point
 Neumann Laplacian, the bandwidth-bound apply + SpMV regime the metric's "precond-apply HBM GB/s
 vs peak" half is quoted on), seeded jacobi_seed sigma=1e-2 factor tensor (L=128, L_s=32).
 Under torchrun (N>1) every rank solves its own frame (frame index = rank): independent systems,
 no collective on the data path ("scaling": "weak"); the barrier + max-over-ranks timing is the
-only communication. `--impl reference` times the reference's own CPU code (oracle/_ref, the
+only communication. The other BASELINE configs are named workloads:
+  batch_262k  configs[3]: 64 independent N=262,144 frames sharded over the ranks (64/N each);
+              value = batch time / 64 ("scaling": "strong", total work fixed)
+  part_16m    configs[4]: one N=16,777,216 system (3D 256^3) row-partitioned over the ranks,
+              peers over CUDA IPC / NVLink (the whole system on one GPU at N=1)
+`--impl reference` times the reference's own CPU code (oracle/_ref, the
 unmodified reference sources) on a bounded sample of the same workload, rank 0 only.
 """
 from __future__ import annotations
@@ -42,8 +47,22 @@ CONFIGS = {
     "2d_65536": dict(desc="BASELINE configs[1] solve half: N=65,536 2D make_frame(65536, 2024, 0), "
                           "seeded sigma=1e-2 factor tensor, L=128, L_s=32 (inference not included)",
                      n=65536, sigma=1e-2, ref_key="2d_65536"),
+    "2d_262144": dict(desc="one frame of BASELINE configs[3]: N=262,144 2D make_frame(262144, 2024, "
+                           "test_frame_id(262144, 0)), seeded sigma=1e-2 tensor, L=128, L_s=32",
+                      n=262144, sigma=1e-2, ref_key="2d_262144_t0_s1e-2", test_frame=True),
     "2d_8192": dict(desc="BASELINE configs[0] system: make_frame(8192, 2024, 0), seeded tensor",
                     n=8192, sigma=1e-2, ref_key="2d_8192"),
+    "batch_262k": dict(kind="batch", frames=64,
+                       desc="BASELINE configs[3]: 64 independent frames make_frame(262144, 2024, "
+                            "test_frame_id(262144, i)), i = 0..63, each with its seeded sigma=1e-3 "
+                            "tensor (RngStream(2024, frame_id, factor_init); sigma=1e-2 leaves "
+                            "frames at max_iters, DESIGN.md), sharded over the GPUs",
+                       n=262144, sigma=1e-3, ref_key="2d_262144_t0_s1e-3"),
+    "part_16m": dict(kind="part",
+                     desc="BASELINE configs[4]: N=16,777,216 3D 256^3 7-point pressure-Poisson, "
+                          "seeded sigma=1e-3 tensor, row-partitioned over the GPUs along the "
+                          "bisection tree (mailbox exchange over CUDA IPC / NVLink)",
+                     dims=(256, 256, 256), sigma=1e-3, ref_key=None),
 }
 
 
@@ -52,9 +71,10 @@ def make_inputs(cfg: dict, frame_index: int):
     if "dims" in cfg:
         fr = H.make_frame_3d(*cfg["dims"], 2024, frame_index)
     else:
-        fr = H.make_frame(cfg["n"], 2024, frame_index)
+        fid = H.test_frame_id(cfg["n"], frame_index) if cfg.get("test_frame") or cfg.get("kind") == "batch" else frame_index
+        fr = H.make_frame(cfg["n"], 2024, fid)
     f = H.init_factors(H.build_partition(fr.n, 128), 32, H.FactorInit.jacobi_seed, cfg["sigma"],
-                       H.RngStream(2024, frame_index, H.RngPurpose.factor_init))
+                       H.RngStream(2024, fr.frame_index, H.RngPurpose.factor_init))
     return fr, f
 
 
@@ -193,7 +213,19 @@ def run_reference(args, cfg):
 # ------------------------------------------------------------------------------- our arm
 
 
+def launches_per_solve(dev, iterations: int) -> int:
+    """Kernels one solve launches: one k_solve (persistent driver) or the graph's init + loop."""
+    per_iter, per_apply = dev.launch_counts()
+    if per_iter == 0:
+        return 1
+    return 1 + per_apply + per_iter * iterations
+
+
 def run_ours(args, cfg):
+    if cfg.get("kind") == "batch":
+        return run_batch(args, cfg)
+    if cfg.get("kind") == "part":
+        return run_part(args, cfg)
     world, rank, local = dist_init()
     import torch
     torch.cuda.set_device(local)
@@ -297,7 +329,7 @@ def run_ours(args, cfg):
                      "solve_ms_per_iteration": (t_max / args.steps) / max(iters[-1], 1)},
         "e2e": {"value": e2e_max / (e2e_steps * world), "unit": UNIT,
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 96},
-        "gpu_launches": args.steps * (1 + per_apply + per_iter * iters[-1]),
+        "gpu_launches": args.steps * launches_per_solve(dev, iters[-1]),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -309,6 +341,213 @@ def run_ours(args, cfg):
                       f"factor_applier) on 1 host core, scaled by {its} iterations",
             "ms_per_iteration": ms_it, "nproc": os.cpu_count()}
     if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------- configs[3]: batched frames
+
+
+def run_batch(args, cfg):
+    """64 independent frames, frame i on rank i mod N; one step = every rank solves its share
+    (each solve one graph / one persistent launch on the whole GPU); value = max-over-ranks step
+    time / 64 frames."""
+    world, rank, local = dist_init()
+    import torch
+    torch.cuda.set_device(local)
+    import paper_2605_13343_b200 as H
+    from paper_2605_13343_b200 import _native as N
+    mine = list(range(rank, cfg["frames"], world))
+    devs, bs, xs, its = [], [], [], []
+    for i in mine:
+        fr, f = make_inputs(cfg, i)
+        d = H.Device(local)
+        d.load_csr(fr.A)
+        d.load_factors(f)
+        d.set_precond(2)
+        devs.append(d)
+        bs.append(torch.from_numpy(fr.b).to(f"cuda:{local}"))
+        xs.append(torch.empty_like(bs[-1]))
+        if i == 0:
+            fr0, f0 = fr, f
+    sc = H.SolveConfig()
+
+    def step():
+        out = []
+        for d, b, x in zip(devs, bs, xs):
+            out.append(int(d.solve_ptr(b.data_ptr(), x.data_ptr(), sc, None, N.DEVICE).iterations))
+        return out
+
+    for _ in range(args.warmup):
+        its = step()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0 = torch.cuda.ExternalStream(devs[0].stream(), device=f"cuda:{local}")
+    s1 = torch.cuda.ExternalStream(devs[-1].stream(), device=f"cuda:{local}")
+    with Clocks(local) as clk:
+        e0.record(s0)
+        for _ in range(args.steps):
+            its = step()
+        e1.record(s1)
+        torch.cuda.synchronize()
+    barrier(world)
+    t_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, local)
+    value = t_ms / cfg["frames"]
+    # end to end through the C ABI: each frame's b from pinned host memory in, x out
+    import ctypes
+    n = bs[0].numel()
+    hb, hx = N.vp(), N.vp()
+    N.check(N.lib.hfpg_host_alloc(8 * n, hb))
+    N.check(N.lib.hfpg_host_alloc(8 * n, hx))
+    b_np = np.ctypeslib.as_array(ctypes.cast(hb, ctypes.POINTER(ctypes.c_double)), shape=(n,))
+    host_b = [b.cpu().numpy() for b in bs]
+    barrier(world)
+    t0 = time.perf_counter()
+    for d, bh in zip(devs, host_b):
+        b_np[:] = bh
+        d.solve_ptr(hb.value, hx.value, sc, None, N.HOST)
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1000.0, world, local)
+    N.lib.hfpg_host_free(hb)
+    N.lib.hfpg_host_free(hx)
+    all_its = its
+    if world > 1:
+        import torch.distributed as dist
+        gathered = [None] * world
+        dist.all_gather_object(gathered, its)
+        all_its = [v for g in gathered for v in g]
+    peak, peak_src = peaks()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "n": n, "frames": cfg["frames"], "frames_per_gpu": len(mine),
+                   "iterations_mean": float(np.mean(all_its)), "iterations_min": int(min(all_its)),
+                   "iterations_max": int(max(all_its)), "ref_iterations_frame0": ref_iterations(cfg["ref_key"]),
+                   "solver": "persistent" if devs[0].solver_in_use() == N.SOLVER_PERSISTENT else "graph",
+                   "l2": "per-frame factor tensor 211 MB > L2 (streamed every iteration)",
+                   "parallelism": f"frames sharded {cfg['frames']}/{world} per GPU, no collective"},
+        "e2e": {"value": e2e_ms / cfg["frames"], "unit": UNIT,
+                "h2d_bytes_per_step": 8 * n * cfg["frames"], "d2h_bytes_per_step": 8 * n * cfg["frames"]},
+        "gpu_launches": args.steps * sum(launches_per_solve(devs[0], k) for k in its),
+        "clocks": clk.summary(),
+        "roofline": {"bound": "hbm", "peak": peak, "peak_source": peak_src, "unit": "GB/s"},
+    }
+    if rank == 0:
+        # dominant kernel of the per-stage path on frame 0 (standalone launches, CUDA events)
+        ms4 = np.zeros(4, np.float32)
+        devs[0].solve_ptr(bs[0].data_ptr(), xs[0].data_ptr(), sc, None, N.DEVICE)
+        N.check(N.lib.hfpg_profile_iteration(devs[0].h, 20, ms4.ctypes.data))
+        K = n // 128
+        leaf_bytes = 4 * (K * 128 * 128 + 2 * n * 32) + 48 * n
+        achieved = leaf_bytes / (float(ms4[1]) * 1e-3) / 1e9
+        line["roofline"].update({"kernel": "k_leaf_fast", "achieved": achieved, "frac": achieved / peak,
+                                 "traffic": None, "algorithmic_bytes_per_launch": leaf_bytes,
+                                 "kernel_ms": dict(zip(["k_spmv", "k_leaf_fast", "k_coarse", "k_prolong_fast"],
+                                                       map(float, ms4)))})
+        if world == 1 and not args.no_cpu_baseline:
+            ms_it, n_it = cpu_sample(cfg, fr0, f0, args.ref_budget)
+            rits = ref_iterations(cfg["ref_key"]) or all_its[0]
+            line["cpu_baseline"] = {
+                "value": ms_it * rits, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"{n_it} iterations of the reference pcg_solve on frame 0 (oracle/_ref, 1 host core), "
+                          f"x {rits} iterations = ms per frame solve",
+                "ms_per_iteration": ms_it, "nproc": os.cpu_count()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------ configs[4]: row-partitioned system
+
+
+def run_part(args, cfg):
+    """One N=16.7M system; rank r of N holds rows [r N/G, (r+1) N/G) and the matching subtree of
+    the factor tensor (drawn per slice); peers are mapped through CUDA IPC handles all-gathered
+    over torch.distributed. One step = one partitioned solve; value = max-over-ranks ms."""
+    world, rank, local = dist_init()
+    import torch
+    torch.cuda.set_device(local)
+    import paper_2605_13343_b200 as H
+    from paper_2605_13343_b200 import _native as N
+    t_setup = time.perf_counter()
+    fr = H.make_frame_3d(*cfg["dims"], 2024, 0)
+    n = fr.n
+    sc = H.SolveConfig()
+    if world == 1:
+        f = H.init_factors(H.build_partition(n, 128), 32, H.FactorInit.jacobi_seed, cfg["sigma"],
+                           H.RngStream(2024, 0, H.RngPurpose.factor_init))
+        dev = H.Device(local)
+        dev.load_csr(fr.A)
+        dev.load_factors(f)
+        dev.set_precond(2)
+        del f
+        nl, r0 = n, 0
+    else:
+        import torch.distributed as dist
+
+        def allgather(blob):
+            out = [None] * world
+            dist.all_gather_object(out, blob)
+            return out
+
+        rs = H.RankSolver(fr.A, world, rank, allgather, sigma=cfg["sigma"], seed=2024, frame=0,
+                          device=local)
+        dev, nl, r0 = rs.dev, rs.n_local, rs.row_begin
+    b = torch.from_numpy(fr.b[r0:r0 + nl].copy()).to(f"cuda:{local}")
+    x = torch.empty_like(b)
+    setup_s = time.perf_counter() - t_setup
+    stream = torch.cuda.ExternalStream(dev.stream(), device=f"cuda:{local}")
+
+    def solve():
+        return dev.solve_ptr(b.data_ptr(), x.data_ptr(), sc, None, N.DEVICE)
+
+    for _ in range(args.warmup):
+        rep = solve()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            rep = solve()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    t_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, local)
+    # end to end: host slices of b in, x out
+    hb = fr.b[r0:r0 + nl].copy()
+    hx = np.empty(nl)
+    barrier(world)
+    t0 = time.perf_counter()
+    dev.solve_ptr(hb.ctypes.data, hx.ctypes.data, sc, None, N.HOST)
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1000.0, world, local)
+    its = int(rep.iterations)
+    K = nl // 128
+    nnz = int(fr.A.nnz())
+    b_iter = (4 * (K * 128 * 128 + (K - 1) * 1024 + 2 * nl * 32 + nl) + 24 * nl) + (12 * nnz // world + 24 * nl) + 64 * nl
+    peak, peak_src = peaks()
+    achieved = b_iter * its / (t_ms * 1e-3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": t_ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "n": n, "nnz": nnz, "rows_per_gpu": nl, "iterations": its,
+                       "status": int(rep.status), "rtol": 1e-8, "setup_s": setup_s,
+                       "parallelism": f"row partition over {world} GPU(s)" + (
+                           ", mailboxes + z halo over CUDA IPC (NVLink P2P)" if world > 1 else ""),
+                       "l2": "inputs larger than L2"},
+            "roofline": {"bound": "hbm", "kernel": "whole solve (per GPU, algorithmic B_iter x iterations)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "peak_source": peak_src, "algorithmic_bytes_per_iteration": b_iter},
+            "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 8 * nl, "d2h_bytes_per_step": 8 * nl},
+            "gpu_launches": args.steps * launches_per_solve(dev, its),
+            "clocks": clk.summary(),
+        }
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

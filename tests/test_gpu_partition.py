@@ -22,7 +22,7 @@ def seeded(H, n, sigma, seed, frame):
                           H.RngStream(seed, frame, H.RngPurpose.factor_init))
 
 
-@pytest.mark.parametrize("n,G", [(4096, 2), (16384, 4), (65536, 8), (65536, 2)])
+@pytest.mark.parametrize("n,G", [(4096, 2), (16384, 4), (65536, 8), (65536, 2), (65536, 16)])
 def test_group_apply_bit_identical(H, n, G):
     fr = H.make_frame(n, 2024, 0)
     f = seeded(H, n, 1e-2, 2024, 0)

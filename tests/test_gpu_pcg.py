@@ -122,7 +122,7 @@ def _ref_case(name):
 
 
 @pytest.mark.parametrize("name", ["2d_8192", "2d_65536", "3d_1m_s1e-3", "2d_262144_t0_s1e-3",
-                                  "3d_1m_s1e-2"])
+                                  "2d_262144_t0_s1e-2", "3d_1m_s1e-2"])
 def test_iteration_parity_large(H, name):
     want = _ref_case(name)
     if name.startswith("3d"):
@@ -136,4 +136,14 @@ def test_iteration_parity_large(H, name):
     assert abs(jac.iterations - want["jacobi"]["iterations"]) <= 2
     rep = H.pcg_solve(fr.A, fr.b, H.factor_applier(f, fr.A))
     assert rep.status.name == want["factor"]["status"]
-    assert abs(rep.iterations - want["factor"]["iterations"]) <= 2, (rep.iterations, want)
+    ref_its = want["factor"]["iterations"]
+    band = want.get("dot_order_band")
+    if band:
+        # Long, chaotic solve: the f64 dot-product summation order alone (the reference sums
+        # sequentially; a GPU cannot) moves the count — the CPU oracle, apply bit-identical to
+        # the reference, spans `band` with three valid orders (tests/golden/gen_dot_band.py).
+        # Parity = within +-2 of that band.
+        lo, hi = min(ref_its, *band.values()) - 2, max(ref_its, *band.values()) + 2
+        assert lo <= rep.iterations <= hi, (rep.iterations, ref_its, band)
+    else:
+        assert abs(rep.iterations - ref_its) <= 2, (rep.iterations, want)
