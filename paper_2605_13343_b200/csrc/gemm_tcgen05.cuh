@@ -85,8 +85,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// Epilogue functor interface: void operator()(int row, int col0, float (&v)[16]) const —
-// 16 consecutive columns col0..col0+15 of one output row (columns may run past N).
+// Epilogue functor interface: void apply4(int row, int col, float4 v, int nvalid) const —
+// columns col .. col + nvalid - 1 (nvalid <= 4, col a multiple of 4) of one output row. The
+// accumulator tile is staged through shared memory first, so consecutive lanes get consecutive
+// columns of the same row and the functors' global accesses coalesce.
 template <int BN, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tf32(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -149,12 +151,38 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     } else {  // epilogue: warp w owns TMEM lanes (rows) 32w..32w+31
         mbar_wait(&sm.done, 0);
         tc_fence_after();
-        const int row = m0 + warp * 32 + lane;
+        // 1. TMEM -> shared memory, row-major (padded), into the idle stage buffers
+        float* S = &sm.A[0][0];
+        constexpr int kLd = BN + 4;
+        static_assert(sizeof(float) * kGemmBM * (BN + 4) <= sizeof(sm.A) + sizeof(sm.B), "staging");
+        const int r = warp * 32 + lane;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 16) {
             float v[16];
             tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(c), v);
-            if (row < M && n0 + c < N) epi(row, n0 + c, v);
+            float4* d4 = reinterpret_cast<float4*>(S + r * kLd + c);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // the four epilogue warps
+        // 2. whole rows, coalesced: lane l owns columns 4l .. 4l+3 (+128 per pass); rows in
+        //    batches of 8 so a read-modify-write epilogue has 8 row reads in flight
+#pragma unroll 1
+        for (int c = 4 * lane; c < BN; c += 128) {
+            const int col = n0 + c;
+            if (col >= N) break;
+            const int nv = N - col < 4 ? N - col : 4;
+#pragma unroll 1
+            for (int i0 = 0; i0 < 32; i0 += 8) {
+                const int rr0 = warp * 32 + i0;
+                if (m0 + rr0 >= M) break;
+                if (m0 + rr0 + 8 <= M) {
+                    epi.apply4x8(m0 + rr0, col, S + rr0 * kLd + c, kLd, nv);
+                } else {
+                    for (int i = 0; i < 8 && m0 + rr0 + i < M; ++i)
+                        epi.apply4(m0 + rr0 + i, col, *reinterpret_cast<const float4*>(S + (rr0 + i) * kLd + c), nv);
+                }
+            }
         }
     }
     tc_fence_before();

@@ -117,14 +117,24 @@ struct EpiStore {  // out[row, col] = act(v + bias)
     uint32_t ld, n;
     const float* bias;
     int gelu;
-    __device__ void operator()(int row, int col0, float (&v)[16]) const {
-        float* o = out + uint64_t(row) * ld + col0;
+    // 8 consecutive rows (row0 .. row0+7) of columns col..col+3; values at v[i * ld]
+    __device__ void apply4x8(int row0, int col, const float* v, int ld, int nv) const {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            if (col0 + j < int(n)) {
-                float x = v[j] + (bias ? bias[col0 + j] : 0.f);
-                o[j] = gelu ? gelu_f(x) : x;
-            }
+        for (int i = 0; i < 8; ++i) apply4(row0 + i, col, *reinterpret_cast<const float4*>(v + i * ld), nv);
+    }
+    __device__ void apply4(int row, int col, float4 v, int nv) const {
+        float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            x[j] += (bias && j < nv) ? bias[col + j] : 0.f;
+            if (gelu) x[j] = gelu_f(x[j]);
+        }
+        float* o = out + uint64_t(row) * ld + col;
+        if (nv == 4 && (ld & 3) == 0) {
+            *reinterpret_cast<float4*>(o) = make_float4(x[0], x[1], x[2], x[3]);
+        } else {
+            for (int j = 0; j < nv; ++j) o[j] = x[j];
+        }
     }
 };
 struct EpiResidual {  // out[row, col] += act(v + bias)
@@ -132,14 +142,43 @@ struct EpiResidual {  // out[row, col] += act(v + bias)
     uint32_t ld, n;
     const float* bias;
     int gelu;
-    __device__ void operator()(int row, int col0, float (&v)[16]) const {
-        float* o = out + uint64_t(row) * ld + col0;
+    // 8 rows at once: all residual reads issued before the writes
+    __device__ void apply4x8(int row0, int col, const float* v, int ldv, int nv) const {
+        if (nv != 4 || (ld & 3) != 0) {
+            for (int i = 0; i < 8; ++i) apply4(row0 + i, col, *reinterpret_cast<const float4*>(v + i * ldv), nv);
+            return;
+        }
+        float4 a[8];
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            if (col0 + j < int(n)) {
-                float x = v[j] + (bias ? bias[col0 + j] : 0.f);
-                o[j] += gelu ? gelu_f(x) : x;
+        for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float4*>(out + uint64_t(row0 + i) * ld + col);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float4 t = *reinterpret_cast<const float4*>(v + i * ldv);
+            float x[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                x[j] += bias ? bias[col + j] : 0.f;
+                if (gelu) x[j] = gelu_f(x[j]);
             }
+            a[i].x += x[0]; a[i].y += x[1]; a[i].z += x[2]; a[i].w += x[3];
+            *reinterpret_cast<float4*>(out + uint64_t(row0 + i) * ld + col) = a[i];
+        }
+    }
+    __device__ void apply4(int row, int col, float4 v, int nv) const {
+        float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            x[j] += (bias && j < nv) ? bias[col + j] : 0.f;
+            if (gelu) x[j] = gelu_f(x[j]);
+        }
+        float* o = out + uint64_t(row) * ld + col;
+        if (nv == 4 && (ld & 3) == 0) {
+            float4 a = *reinterpret_cast<float4*>(o);
+            a.x += x[0]; a.y += x[1]; a.z += x[2]; a.w += x[3];
+            *reinterpret_cast<float4*>(o) = a;
+        } else {
+            for (int j = 0; j < nv; ++j) o[j] += x[j];
+        }
     }
 };
 // Decoder heads of leaf node `row` (toy_net.cpp:549-567): columns [0, L_s) -> Ũ_k row,
@@ -148,12 +187,17 @@ struct EpiLeafHeads {
     float* out;
     uint64_t L, Ls, bridge_base, gate_base;
     const float* bias;  // 2 Ls + 1
-    __device__ void operator()(int row, int col0, float (&v)[16]) const {
-        const uint64_t k = uint64_t(row) / L, r = uint64_t(row) % L;
+    // 8 consecutive rows (row0 .. row0+7) of columns col..col+3; values at v[i * ld]
+    __device__ void apply4x8(int row0, int col, const float* v, int ld, int nv) const {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const uint64_t c = uint64_t(col0 + j);
-            const float x = v[j] + (bias && c <= 2 * Ls ? bias[c] : 0.f);
+        for (int i = 0; i < 8; ++i) apply4(row0 + i, col, *reinterpret_cast<const float4*>(v + i * ld), nv);
+    }
+    __device__ void apply4(int row, int col, float4 v, int nv) const {
+        const uint64_t k = uint64_t(row) / L, r = uint64_t(row) % L;
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+        for (int j = 0; j < nv; ++j) {
+            const uint64_t c = uint64_t(col + j);
+            const float x = vv[j] + (bias && c <= 2 * Ls ? bias[c] : 0.f);
             if (c < Ls) out[bridge_base + k * 2 * L * Ls + r * Ls + c] = x;
             else if (c < 2 * Ls) out[bridge_base + k * 2 * L * Ls + L * Ls + r * Ls + (c - Ls)] = x;
             else if (c == 2 * Ls) out[gate_base + uint64_t(row)] = x;
@@ -166,13 +210,18 @@ struct EpiTileHeads {
     float* out;
     uint64_t Ls, rk, tile_base;
     const float* bias;
-    __device__ void operator()(int row, int col0, float (&v)[16]) const {
-        const uint64_t m = uint64_t(row) / Ls, tok = uint64_t(row) % Ls;
+    // 8 consecutive rows (row0 .. row0+7) of columns col..col+3; values at v[i * ld]
+    __device__ void apply4x8(int row0, int col, const float* v, int ld, int nv) const {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const uint64_t c = uint64_t(col0 + j);
+        for (int i = 0; i < 8; ++i) apply4(row0 + i, col, *reinterpret_cast<const float4*>(v + i * ld), nv);
+    }
+    __device__ void apply4(int row, int col, float4 v, int nv) const {
+        const uint64_t m = uint64_t(row) / Ls, tok = uint64_t(row) % Ls;
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+        for (int j = 0; j < nv; ++j) {
+            const uint64_t c = uint64_t(col + j);
             if (c >= 2 * rk) continue;
-            const float x = v[j] + (bias ? bias[c] : 0.f);
+            const float x = vv[j] + (bias ? bias[c] : 0.f);
             out[tile_base + m * Ls * Ls + (c < rk ? 0 : Ls * rk) + tok * rk + (c % rk)] = x;
         }
     }
@@ -421,6 +470,7 @@ void toynet_forward_device(ToynetModel* mdl, cudaStream_t st, const hfpg_frame_v
     auto* partial = mdl->buf<float>(17, uint64_t(nparts) * 2 * d);
     auto* leaf_bias = mdl->buf<float>(18, lay.k * cfg.heads * L * L);
     auto* tile_bias = mdl->buf<float>(19, lay.m * cfg.heads * Ls * Ls);
+    auto* tile_pos = mdl->buf<double>(26, std::max<uint64_t>(lay.m, 1) * 2 * Ls * 2);
     unsigned int* rowsum_bits = trace ? mdl->buf<unsigned int>(20, 1) : nullptr;
     float* audit_part = trace ? mdl->buf<float>(23, uint64_t(nparts) * d) : nullptr;
     float* audit_sums = trace ? mdl->buf<float>(24, 6 * d) : nullptr;
@@ -442,9 +492,11 @@ void toynet_forward_device(ToynetModel* mdl, cudaStream_t st, const hfpg_frame_v
     if (lay.m) k_tn_tile_pool<<<dim3(unsigned(lay.m), unsigned(Ls)), 128, 0, st>>>(g, x, tile_tok);
     k_tn_leaf_bias<<<dim3(unsigned((L * L + 255) / 256), unsigned(lay.k)), 256, 0, st>>>(
         g, d_order, d_ro, d_ci, d_v, mdl->le, leaf_bias);
-    if (lay.m)
+    if (lay.m) {
+        k_tn_tile_pos<<<dim3(unsigned(lay.m), 2), 256, 0, st>>>(g, d_order, tile_pos);
         k_tn_tile_bias<<<dim3(unsigned(lay.m), unsigned(Ls)), 64, 0, st>>>(
-            g, d_order, d_ro, d_ci, d_v, mdl->te, tile_bias);
+            g, tile_pos, d_ro, d_ci, d_v, mdl->te, tile_bias);
+    }
     TCK(cudaGetLastError());
 
     auto attention = [&](float* tok, uint64_t rows, uint64_t T, const LW& lw, const float* bias) {
@@ -480,19 +532,19 @@ void toynet_forward_device(ToynetModel* mdl, cudaStream_t st, const hfpg_frame_v
         k_tn_highway<<<nw, 256, 0, st>>>(g, x, tile_tok, row_hw, col_hw);
         k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(n, uint32_t(d), x, partial);
         k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(MT, uint32_t(d), tile_tok, partial + nparts * d);
-        k_tn_colsum_finish<<<1, unsigned(d), 0, st>>>(2 * nparts, uint32_t(d), partial, glob_hw);
+        k_tn_colsum_finish<<<unsigned(d), 32, 0, st>>>(2 * nparts, uint32_t(d), partial, glob_hw);
         TCK(cudaGetLastError());
         if (trace) {  // highway conservation audit (toy_net.cpp:478-512), on device
             k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(n, uint32_t(d), row_hw, audit_part);
-            k_tn_colsum_finish<<<1, unsigned(d), 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums);
+            k_tn_colsum_finish<<<unsigned(d), 32, 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums);
             k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(n, uint32_t(d), col_hw, audit_part);
-            k_tn_colsum_finish<<<1, unsigned(d), 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums + d);
+            k_tn_colsum_finish<<<unsigned(d), 32, 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums + d);
             k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(n, uint32_t(d), x, audit_part);
-            k_tn_colsum_finish<<<1, unsigned(d), 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums + 2 * d);
+            k_tn_colsum_finish<<<unsigned(d), 32, 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums + 2 * d);
             k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(MT, uint32_t(d), tile_tok, audit_part);
-            k_tn_colsum_finish<<<1, unsigned(d), 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums + 3 * d);
+            k_tn_colsum_finish<<<unsigned(d), 32, 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums + 3 * d);
             k_tn_colsum_tiles_weighted<<<nparts, unsigned(d), 0, st>>>(g, tile_tok, audit_part);
-            k_tn_colsum_finish<<<1, unsigned(d), 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums + 4 * d);
+            k_tn_colsum_finish<<<unsigned(d), 32, 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums + 4 * d);
             TCK(cudaMemcpyAsync(audit_sums + 5 * d, glob_hw, d * 4, cudaMemcpyDeviceToDevice, st));
             k_tn_highway_audit<<<1, unsigned(d), 0, st>>>(uint32_t(d), audit_sums, audit_dev + layer);
             TCK(cudaGetLastError());

@@ -32,6 +32,19 @@ __device__ __forceinline__ TileGeom tile_geom(const TnDims& g, uint64_t m) {
     return t;
 }
 
+
+// sum_{s < cnt} p[s * stride], eight interleaved fp32 partial sums combined in a fixed order
+// (deterministic; eight loads in flight per thread instead of one dependent chain).
+__device__ __forceinline__ float strided_sum(const float* p, uint64_t cnt, uint64_t stride) {
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    uint64_t s = 0;
+    for (; s + 8 <= cnt; s += 8)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] += p[(s + q) * stride];
+    for (int q = 0; s < cnt; ++s, ++q) a[q] += p[s * stride];
+    return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+}
+
 // toy_net.cpp:270-293 per-node features [rho, x^, y^, 4 absent-neighbour flags, glob]; the
 // flags come from the operator's off-diagonal pattern (a present neighbour always couples).
 __global__ void k_tn_features(TnDims g, const uint32_t* order, const double* rho,
@@ -120,14 +133,15 @@ __device__ __forceinline__ void edge_mlp(const EdgeMlp& m, uint32_t eh, uint32_t
     }
 }
 
-// Leaf-pair edge biases (toy_net.cpp:371-381): bias[k][h][i][j], once per forward (reused by
-// every layer). Coupling = A_{base+i, base+j} looked up in the sorted CSR row.
+// Leaf-pair edge biases (toy_net.cpp:371-381), once per forward (reused by every layer), stored
+// key-major: bias[k][h][j][i] (query i fastest) so the attention's lanes (queries) read them
+// coalesced. Coupling = A_{base+i, base+j} looked up in the sorted CSR row.
 __global__ void k_tn_leaf_bias(TnDims g, const uint32_t* order, const unsigned long long* ro,
                                const uint32_t* ci, const double* v, EdgeMlp mlp, float* bias) {
     const uint64_t k = blockIdx.y;
-    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // i * L + j
+    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // j * L + i
     if (idx >= g.L * g.L) return;
-    const uint64_t i = idx / g.L, j = idx % g.L, base = k * g.L;
+    const uint64_t j = idx / g.L, i = idx % g.L, base = k * g.L;
     const uint32_t a = order[base + i], b = order[base + j];
     const double xa = (double(a % g.width) + 0.5) / double(g.width), ya = (double(a / g.width) + 0.5) / double(g.height);
     const double xb = (double(b % g.width) + 0.5) / double(g.width), yb = (double(b / g.width) + 0.5) / double(g.height);
@@ -137,64 +151,68 @@ __global__ void k_tn_leaf_bias(TnDims g, const uint32_t* order, const unsigned l
         if (ci[p] == base + j) c = v[p];
     float out[8];
     edge_mlp(mlp, g.eh, g.heads, float(dx), float(dy), float(dist), float(c), out);
-    for (uint32_t h = 0; h < g.heads; ++h) bias[((k * g.heads + h) * g.L + i) * g.L + j] = out[h];
+    for (uint32_t h = 0; h < g.heads; ++h) bias[((k * g.heads + h) * g.L + j) * g.L + i] = out[h];
+}
+
+// Chunk positions of every tile (toy_net.cpp:382-414 descriptors): pos[m][side][chunk] =
+// (sum x, sum y) over the chunk's nodes (side 0: row chunks, 1: column chunks), f64. One CTA per
+// (tile, side), one warp per chunk, lanes over the chunk's nodes, fixed-order reduction.
+__global__ void k_tn_tile_pos(TnDims g, const uint32_t* order, double* pos) {
+    const uint64_t m = blockIdx.x, side = blockIdx.y;
+    const TileGeom t = tile_geom(g, m);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint64_t base = side ? t.col0 : t.row0;
+    for (uint64_t c = w; c < g.Ls; c += nw) {
+        double sx = 0.0, sy = 0.0;
+        for (uint64_t s = lane; s < t.chunk; s += 32) {
+            const uint32_t id = order[base + c * t.chunk + s];
+            sx += (double(id % g.width) + 0.5) / double(g.width);
+            sy += (double(id / g.width) + 0.5) / double(g.height);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sx += __shfl_xor_sync(0xffffffffu, sx, o);
+            sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        }
+        if (lane == 0) {
+            pos[((m * 2 + side) * g.Ls + c) * 2 + 0] = sx;
+            pos[((m * 2 + side) * g.Ls + c) * 2 + 1] = sy;
+        }
+    }
 }
 
 // Tile-pair edge biases (toy_net.cpp:382-414): chunk-mean positions and the mean coupling over
-// each (row chunk a, column chunk b) pair. One CTA per (tile, a); the a-chunk's CSR rows are
-// scanned once and their column-band entries binned by b.
-__global__ void k_tn_tile_bias(TnDims g, const uint32_t* order, const unsigned long long* ro,
-                               const uint32_t* ci, const double* v, EdgeMlp mlp, float* bias) {
+// each (row chunk a, column chunk b) pair, stored key-major bias[m][h][b][a]. One CTA (64
+// threads) per (tile, a): the a-chunk's CSR rows are split over the threads, each bins its
+// column-band entries into a private column of partial sums, combined per bin in thread order.
+__global__ void __launch_bounds__(64) k_tn_tile_bias(TnDims g, const double* pos, const unsigned long long* ro,
+                                                    const uint32_t* ci, const double* v, EdgeMlp mlp,
+                                                    float* bias) {
     const uint64_t m = blockIdx.x, a = blockIdx.y;
     const TileGeom t = tile_geom(g, m);
-    __shared__ double coup[64], cxs[64], cys[64];
-    __shared__ double rx, ry;
+    __shared__ double part[64][33];
     const int tid = threadIdx.x;
-    auto xn = [&](uint64_t node) {
-        const uint32_t id = order[node];
-        return (double(id % g.width) + 0.5) / double(g.width);
-    };
-    auto yn = [&](uint64_t node) {
-        const uint32_t id = order[node];
-        return (double(id / g.width) + 0.5) / double(g.height);
-    };
-    if (tid < g.Ls) {
-        coup[tid] = 0.0;
-        double sx = 0.0, sy = 0.0;
-        for (uint64_t s = 0; s < t.chunk; ++s) {  // column-chunk position sums, s ascending
-            sx += xn(t.col0 + tid * t.chunk + s);
-            sy += yn(t.col0 + tid * t.chunk + s);
-        }
-        cxs[tid] = sx;
-        cys[tid] = sy;
-    }
-    if (tid == 0) {
-        double sx = 0.0, sy = 0.0;
-        for (uint64_t s = 0; s < t.chunk; ++s) {
-            sx += xn(t.row0 + a * t.chunk + s);
-            sy += yn(t.row0 + a * t.chunk + s);
-        }
-        rx = sx;
-        ry = sy;
+    for (uint32_t b = 0; b < g.Ls; ++b) part[tid][b] = 0.0;
+    const uint64_t cbase = t.col0, cend = t.col0 + g.Ls * t.chunk;
+    for (uint64_t s = tid; s < t.chunk; s += 64) {
+        const uint64_t r = t.row0 + a * t.chunk + s;
+        for (unsigned long long p = ro[r]; p < ro[r + 1]; ++p)
+            if (ci[p] >= cbase && ci[p] < cend) part[tid][(ci[p] - cbase) / t.chunk] += v[p];
     }
     __syncthreads();
-    if (tid == 0) {  // sparse coupling sums, in the reference's (s, p) order per bin
-        const uint64_t cbase = t.col0, cend = t.col0 + g.Ls * t.chunk;
-        for (uint64_t s = 0; s < t.chunk; ++s) {
-            const uint64_t r = t.row0 + a * t.chunk + s;
-            for (unsigned long long p = ro[r]; p < ro[r + 1]; ++p)
-                if (ci[p] >= cbase && ci[p] < cend) coup[(ci[p] - cbase) / t.chunk] += v[p];
-        }
-    }
-    __syncthreads();
-    if (tid < g.Ls) {
+    if (tid < int(g.Ls)) {
+        double c = 0.0;
+        for (int q = 0; q < 64; ++q) c += part[q][tid];
         const double ch = double(t.chunk);
-        const double dx = (rx - cxs[tid]) / ch, dy = (ry - cys[tid]) / ch;
-        const double dist = sqrt(dx * dx + dy * dy), c = coup[tid] / (ch * ch);
+        const double* rp = pos + ((m * 2 + 0) * g.Ls + a) * 2;
+        const double* cp = pos + ((m * 2 + 1) * g.Ls + tid) * 2;
+        const double dx = (rp[0] - cp[0]) / ch, dy = (rp[1] - cp[1]) / ch;
+        const double dist = sqrt(dx * dx + dy * dy);
+        c /= ch * ch;
         float out[8];
         edge_mlp(mlp, g.eh, g.heads, float(dx), float(dy), float(dist), float(c), out);
         for (uint32_t h = 0; h < g.heads; ++h)
-            bias[((m * g.heads + h) * g.Ls + a) * g.Ls + tid] = out[h];
+            bias[((m * g.heads + h) * g.Ls + tid) * g.Ls + a] = out[h];
     }
 }
 
@@ -203,17 +221,18 @@ __global__ void k_tn_tile_pool(TnDims g, const float* emb, float* tile_tok) {
     const uint64_t m = blockIdx.x, tok = blockIdx.y;
     const TileGeom t = tile_geom(g, m);
     for (uint32_t c = threadIdx.x; c < g.d; c += blockDim.x) {
-        float s = 0.f;
-        for (uint64_t q = 0; q < t.chunk; ++q)
-            s += 0.5f * (emb[(t.row0 + tok * t.chunk + q) * g.d + c] + emb[(t.col0 + tok * t.chunk + q) * g.d + c]);
-        tile_tok[(m * g.Ls + tok) * g.d + c] = s / float(t.chunk);
+        const float rs = strided_sum(emb + (t.row0 + tok * t.chunk) * g.d + c, t.chunk, g.d);
+        const float cs = strided_sum(emb + (t.col0 + tok * t.chunk) * g.d + c, t.chunk, g.d);
+        tile_tok[(m * g.Ls + tok) * g.d + c] = 0.5f * (rs + cs) / float(t.chunk);
     }
 }
 
 // Windowed multi-head attention core (toy_net.cpp:78-125) for one (block, head): T tokens,
 // head dim 16. qkv rows hold [q | k | v] (3d wide). One thread per query row; K/V of the block
-// head staged in shared memory; softmax in fp32 with max subtraction. Writes head_out[row, h*16..].
-// Also tracks max |row sum - 1| (trace).
+// head staged in shared memory; the key-major bias row j is read once, coalesced across the
+// query lanes; softmax in fp32 with an online (rescaled) running max, i.e. one pass over the
+// keys. Writes head_out[row, h*16..]. With rowsum_err_bits (trace) a second pass audits
+// max |row sum - 1| of the normalised probabilities.
 template <int T>
 __global__ void __launch_bounds__(T) k_tn_attention(uint32_t d, uint32_t heads, const float* qkv,
                                                     const float* bias, float* head_out,
@@ -221,49 +240,63 @@ __global__ void __launch_bounds__(T) k_tn_attention(uint32_t d, uint32_t heads, 
     const uint64_t blk = blockIdx.x;
     const uint32_t h = blockIdx.y, i = threadIdx.x;
     constexpr int HD = 16;
-    __shared__ float ks[T][HD + 1], vs[T][HD + 1];
-    const float* rowp = qkv + (blk * T + i) * 3 * d;
-    float q[HD];
+    __shared__ float4 ks[T][HD / 4], vs[T][HD / 4];
+    const float4* rowp = reinterpret_cast<const float4*>(qkv + (blk * T + i) * 3 * d);
+    float4 q4[HD / 4];
 #pragma unroll
-    for (int c = 0; c < HD; ++c) {
-        q[c] = rowp[h * HD + c];
-        ks[i][c] = rowp[d + h * HD + c];
-        vs[i][c] = rowp[2 * d + h * HD + c];
+    for (int c = 0; c < HD / 4; ++c) {
+        q4[c] = rowp[(h * HD) / 4 + c];
+        ks[i][c] = rowp[(d + h * HD) / 4 + c];
+        vs[i][c] = rowp[(2 * d + h * HD) / 4 + c];
     }
     __syncthreads();
-    const float* b = bias + ((blk * heads + h) * T + i) * T;
+    const float* b = bias + (blk * heads + h) * T * T + i;  // column i of the key-major bias
     const float scale = 0.25f;  // 1/sqrt(16)
-    float mx = -CUDART_INF_F;
-    for (int j = 0; j < T; ++j) {
+    auto logit = [&](int j) {
         float dot = 0.f;
 #pragma unroll
-        for (int c = 0; c < HD; ++c) dot = fmaf(q[c], ks[j][c], dot);
-        mx = fmaxf(mx, fmaf(dot, scale, b[j]));
-    }
-    float sum = 0.f, acc[HD];
+        for (int c = 0; c < HD / 4; ++c) {
+            const float4 k = ks[j][c];
+            dot = fmaf(q4[c].x, k.x, dot);
+            dot = fmaf(q4[c].y, k.y, dot);
+            dot = fmaf(q4[c].z, k.z, dot);
+            dot = fmaf(q4[c].w, k.w, dot);
+        }
+        return fmaf(dot, scale, __ldg(b + j * T));
+    };
+    float mx = -CUDART_INF_F, sum = 0.f;
+    float4 acc[HD / 4];
 #pragma unroll
-    for (int c = 0; c < HD; ++c) acc[c] = 0.f;
+    for (int c = 0; c < HD / 4; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int j = 0; j < T; ++j) {
-        float dot = 0.f;
+        const float sj = logit(j);
+        if (sj > mx) {  // rescale the running sums to the new max
+            const float r = expf(mx - sj);
+            sum *= r;
 #pragma unroll
-        for (int c = 0; c < HD; ++c) dot = fmaf(q[c], ks[j][c], dot);
-        const float p = expf(fmaf(dot, scale, b[j]) - mx);
+            for (int c = 0; c < HD / 4; ++c) {
+                acc[c].x *= r; acc[c].y *= r; acc[c].z *= r; acc[c].w *= r;
+            }
+            mx = sj;
+        }
+        const float p = expf(sj - mx);
         sum += p;
 #pragma unroll
-        for (int c = 0; c < HD; ++c) acc[c] = fmaf(p, vs[j][c], acc[c]);
+        for (int c = 0; c < HD / 4; ++c) {
+            const float4 v = vs[j][c];
+            acc[c].x = fmaf(p, v.x, acc[c].x);
+            acc[c].y = fmaf(p, v.y, acc[c].y);
+            acc[c].z = fmaf(p, v.z, acc[c].z);
+            acc[c].w = fmaf(p, v.w, acc[c].w);
+        }
     }
     const float inv = 1.f / sum;
-    float* o = head_out + (blk * T + i) * d + h * HD;
+    float4* o = reinterpret_cast<float4*>(head_out + (blk * T + i) * d + h * HD);
 #pragma unroll
-    for (int c = 0; c < HD; ++c) o[c] = acc[c] * inv;
+    for (int c = 0; c < HD / 4; ++c) o[c] = make_float4(acc[c].x * inv, acc[c].y * inv, acc[c].z * inv, acc[c].w * inv);
     if (rowsum_err_bits) {  // row sum of the normalised probabilities, as the trace audits
         float rs = 0.f;
-        for (int j = 0; j < T; ++j) {
-            float dot = 0.f;
-#pragma unroll
-            for (int c = 0; c < HD; ++c) dot = fmaf(q[c], ks[j][c], dot);
-            rs += expf(fmaf(dot, scale, b[j]) - mx) * inv;
-        }
+        for (int j = 0; j < T; ++j) rs += expf(logit(j) - mx) * inv;
         atomicMax(rowsum_err_bits, __float_as_uint(fabsf(rs - 1.f)));
     }
 }
@@ -273,32 +306,46 @@ __global__ void __launch_bounds__(T) k_tn_attention(uint32_t d, uint32_t heads, 
 // halves. One warp per node, lane owns 4 channels.
 __global__ void k_tn_highway(TnDims g, const float* leaf_tok, const float* tile_tok, float* row_hw,
                              float* col_hw) {
-    const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    constexpr int kMaxD = 20;
+    const uint32_t i = uint32_t((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (i >= g.n) return;
-    const float4 lt = reinterpret_cast<const float4*>(leaf_tok + i * g.d)[lane];
-    float4 r = lt, c = lt;
-    const uint64_t leaf = i / g.L;
-    for (uint64_t dd = 0; dd < g.D; ++dd) {
-        const uint64_t m = ((g.K + leaf) >> (g.D - dd)) - 1;
-        const TileGeom t = tile_geom(g, m);
-        const bool right = (leaf >> (g.D - 1 - dd)) & 1ULL;
-        const uint64_t tok = (i - (right ? t.col0 : t.row0)) / t.chunk;
-        const float4 e = reinterpret_cast<const float4*>(tile_tok + (m * g.Ls + tok) * g.d)[lane];
-        float4& dst = right ? c : r;
-        dst.x += e.x; dst.y += e.y; dst.z += e.z; dst.w += e.w;
+    // all sizes are powers of two: leaf = i >> log L; the depth-dd ancestor's chunk holds
+    // 2^(D-dd-1) * L / L_s rows, so the covering token is (i mod 2^(D-dd) L) >> log chunk, less
+    // L_s in the column half
+    int lL = 0, lLs = 0;
+    while ((1u << lL) < g.L) ++lL;
+    while ((1u << lLs) < g.Ls) ++lLs;
+    const uint32_t D = uint32_t(g.D), K = uint32_t(g.K), leaf = i >> lL;
+    float4 e[kMaxD];
+#pragma unroll
+    for (int dd = 0; dd < kMaxD; ++dd) {  // every ancestor's covering tile token, loads first
+        e[dd] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (uint32_t(dd) < D) {
+            const uint32_t m = ((K + leaf) >> (D - dd)) - 1u;
+            const uint32_t within = i & ((1u << (D - dd + lL)) - 1u);  // offset inside the tile
+            const uint32_t tok = (within >> (D - dd - 1 + lL - lLs)) & (uint32_t(g.Ls) - 1u);
+            e[dd] = __ldg(reinterpret_cast<const float4*>(tile_tok + (uint64_t(m) * g.Ls + tok) * g.d) + lane);
+        }
     }
-    reinterpret_cast<float4*>(row_hw + i * g.d)[lane] = r;
-    reinterpret_cast<float4*>(col_hw + i * g.d)[lane] = c;
+    const float4 lt = reinterpret_cast<const float4*>(leaf_tok + uint64_t(i) * g.d)[lane];
+    float4 r = lt, c = lt;
+#pragma unroll
+    for (int dd = 0; dd < kMaxD; ++dd)
+        if (uint32_t(dd) < D) {
+            float4& dst = ((leaf >> (D - 1 - dd)) & 1u) ? c : r;
+            dst.x += e[dd].x; dst.y += e[dd].y; dst.z += e[dd].z; dst.w += e[dd].w;
+        }
+    reinterpret_cast<float4*>(row_hw + uint64_t(i) * g.d)[lane] = r;
+    reinterpret_cast<float4*>(col_hw + uint64_t(i) * g.d)[lane] = c;
 }
 
 // glob_hw = sum of every leaf token + every tile token (toy_net.cpp:458, 474). Column sums via
 // per-block partials (deterministic), then a single-block finish.
 __global__ void k_tn_colsum_partial(uint64_t rows, uint32_t d, const float* x, float* partial) {
-    const uint32_t c = threadIdx.x;  // blockDim.x == d
-    float s = 0.f;
-    for (uint64_t r = blockIdx.x; r < rows; r += gridDim.x) s += x[r * d + c];
-    partial[uint64_t(blockIdx.x) * d + c] = s;
+    const uint32_t c = threadIdx.x;  // blockDim.x == d; block b sums rows b, b + grid, ...
+    const uint64_t cnt = rows > blockIdx.x ? (rows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    partial[uint64_t(blockIdx.x) * d + c] = strided_sum(x + uint64_t(blockIdx.x) * d + c, cnt, uint64_t(gridDim.x) * d);
 }
 // Tile-token column sums weighted by each token's chunk length (the number of highway rows it
 // is scattered to), for the conservation audit.
@@ -330,11 +377,15 @@ __global__ void k_tn_highway_audit(uint32_t d, const float* sums, float* out_lay
     }
 }
 
+// Column totals of the per-block partials (f64, fixed order): block c sums column c, each of
+// its 32 lanes a strided share, then a butterfly.
 __global__ void k_tn_colsum_finish(uint32_t nparts, uint32_t d, const float* partial, float* out) {
-    const uint32_t c = threadIdx.x;
+    const uint32_t c = blockIdx.x, lane = threadIdx.x;
     double s = 0.0;
-    for (uint32_t b = 0; b < nparts; ++b) s += partial[uint64_t(b) * d + c];
-    out[c] = float(s);
+    for (uint32_t b = lane; b < nparts; b += 32) s += partial[uint64_t(b) * d + c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[c] = float(s);
 }
 
 // FFN input rows for leaves (toy_net.cpp:421-436, 515-517): [LN(tok) | row_hw | col_hw | glob],
@@ -358,11 +409,8 @@ __global__ void k_tn_ffn_input_tile(TnDims g, const float* row_hw, const float* 
     const TileGeom t = tile_geom(g, m);
     float* a = A + (m * g.Ls + tok) * 4 * g.d;
     for (uint32_t c = threadIdx.x; c < g.d; c += blockDim.x) {
-        float rs = 0.f, cs = 0.f;
-        for (uint64_t s = 0; s < t.chunk; ++s) {
-            rs += row_hw[(t.row0 + tok * t.chunk + s) * g.d + c];
-            cs += col_hw[(t.col0 + tok * t.chunk + s) * g.d + c];
-        }
+        const float rs = strided_sum(row_hw + (t.row0 + tok * t.chunk) * g.d + c, t.chunk, g.d);
+        const float cs = strided_sum(col_hw + (t.col0 + tok * t.chunk) * g.d + c, t.chunk, g.d);
         a[g.d + c] = rs / float(t.chunk);
         a[2 * g.d + c] = cs / float(t.chunk);
         a[3 * g.d + c] = glob[c];
