@@ -7,8 +7,10 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <cstdlib>
 #include <vector>
 
+#include "attention_tcgen05.cuh"
 #include "gemm_tcgen05.cuh"
 #include "internal.hpp"
 #include "toynet_kernels.cuh"
@@ -503,6 +505,19 @@ void toynet_forward_device(ToynetModel* mdl, cudaStream_t st, const hfpg_frame_v
         k_tn_layernorm<<<unsigned((rows * 32 + 255) / 256), 256, 0, st>>>(rows, uint32_t(d), tok, ln, uint32_t(d));
         gemm<128>(st, ln, rows, d, d, lw.qkv, 3 * d, d, EpiStore{qkv, uint32_t(3 * d), uint32_t(3 * d), nullptr, 0});
         const dim3 grid(unsigned(rows / T), unsigned(cfg.heads));
+        static const bool simt128 = std::getenv("HFPG_ATTENTION_SIMT") != nullptr;  // A/B checks only
+        if (T == 128 && !simt128) {  // tensor-core path (attention_tcgen05.cuh)
+            static bool configured = false;
+            if (!configured) {
+                TCK(cudaFuncSetAttribute(k_tn_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(att_smem_bytes())));
+                configured = true;
+            }
+            k_tn_attention_tc<<<unsigned(rows / T), kAttThreads, att_smem_bytes(), st>>>(
+                uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits);
+            TCK(cudaGetLastError());
+            gemm<128>(st, hout, rows, d, d, lw.wo, d, d, EpiResidual{tok, uint32_t(d), uint32_t(d), nullptr, 0});
+            return;
+        }
         switch (T) {
             case 128: k_tn_attention<128><<<grid, 128, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
             case 64: k_tn_attention<64><<<grid, 64, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
