@@ -20,7 +20,7 @@
 
 namespace hfpg {
 
-constexpr int kGemmBM = 128, kGemmBK = 32, kGemmStages = 4;
+constexpr int kGemmBM = 128, kGemmBK = 32, kGemmStages = 3;  // 3 stages: two CTAs per SM
 constexpr int kGemmThreads = 192;  // warps 0-3 epilogue, warp 4 TMA, warp 5 MMA + TMEM
 
 template <int BN>
@@ -90,7 +90,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 // accumulator tile is staged through shared memory first, so consecutive lanes get consecutive
 // columns of the same row and the functors' global accesses coalesce.
 template <int BN, class Epi>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kGemmThreads, 2)
     k_gemm_tf32(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 int M, int N, int K, Epi epi) {
     extern __shared__ __align__(1024) unsigned char graw[];
