@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) k_coarse_tiles(DevSys s, int 
 // identical to the reference. f32<->f64 conversions run at 15.6/clk/SM (measured), so the strip
 // sums are cast once per tile and each coefficient is converted once and broadcast through
 // shared memory. T = the tile's U (V = T + 512); out = [coupled_row (32) | coupled_col (32)].
-struct TileScratch {
+struct alignas(16) TileScratch {
     float fr[32], fc[32];
     double coef[32];
 };

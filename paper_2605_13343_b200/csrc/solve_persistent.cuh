@@ -353,7 +353,7 @@ __device__ __forceinline__ double p_leaf_phase(const DevSys& s, PSmem& sm, PLeaf
 // (matvec, apply.cpp:121-138) — bit-identical to the reference. f32<->f64 conversions run at
 // 15.6/clk/SM (measured), so the strip sums are cast once per tile (lane p casts s_r[p],
 // s_c[p]) and each lane converts its coefficient once and broadcasts it through shared memory.
-struct PTileScratch {
+struct alignas(16) PTileScratch {
     float fr[32], fc[32];
     double coef[32];
 };
