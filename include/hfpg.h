@@ -232,6 +232,14 @@ int hfpg_part_factors(uint64_t n, uint64_t leaf_size, uint64_t coarse_size, uint
                       const float* packed, double sigma, uint64_t seed, uint64_t frame,
                       float* local, float* top);
 
+/* Asynchronous form of hfpg_pcg_solve: enqueue on the handle's stream and return; wait for it
+ * (and fill history / report) with hfpg_pcg_solve_wait. Lets independent systems on separate
+ * handles run concurrently on one GPU (the batched-frames configuration). With HFPG_HOST
+ * buffers the copies are only asynchronous for pinned memory (hfpg_host_alloc). */
+int hfpg_pcg_solve_async(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg, double* x,
+                         int where);
+int hfpg_pcg_solve_wait(hfpg_handle* h, double* history, hfpg_report* report, int where);
+
 /* ---- network inference + factor assembly ------------------------------------------------ */
 /* toy_net.cpp:170-223 init_weights(cfg, make_factor_layout(build_partition(n, leaf), coarse),
  * weight_seed) and :322-586 forward(frame, ...) on the GPU (tcgen05 tf32 GEMMs + fp32 kernels;

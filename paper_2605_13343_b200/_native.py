@@ -105,6 +105,8 @@ _PROTOS = {
                                  vp]),
     "hfpg_part_factors": (C.c_int, [u64, u64, u64, C.c_uint32, C.c_uint32, vp, dbl, u64, u64, vp,
                                     vp]),
+    "hfpg_pcg_solve_async": (C.c_int, [vp, vp, C.POINTER(SolveConfigC), vp, C.c_int]),
+    "hfpg_pcg_solve_wait": (C.c_int, [vp, vp, C.POINTER(ReportC), C.c_int]),
     "hfpg_launch_counts": (C.c_int, [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "hfpg_fast_path": (C.c_int, [vp, C.POINTER(i32)]),
     "hfpg_profile_iteration": (C.c_int, [vp, C.c_uint32, vp]),

@@ -363,6 +363,16 @@ class Device:
         check(lib.hfpg_pcg_solve(self.h, b_ptr, C.byref(c), x_ptr, hist_ptr, C.byref(rep), where))
         return rep
 
+    def solve_async(self, b_ptr, x_ptr, cfg: "SolveConfig", where=N.DEVICE):
+        """Enqueue a solve on this handle's stream (hfpg_pcg_solve_async); finish with wait()."""
+        c = N.SolveConfigC(cfg.rtol, cfg.max_iters)
+        check(lib.hfpg_pcg_solve_async(self.h, b_ptr, C.byref(c), x_ptr, where))
+
+    def wait(self, hist_ptr=None, where=N.DEVICE):
+        rep = N.ReportC()
+        check(lib.hfpg_pcg_solve_wait(self.h, hist_ptr, C.byref(rep), where))
+        return rep
+
     def set_solver(self, kind: int):
         """N.SOLVER_AUTO / SOLVER_GRAPH / SOLVER_PERSISTENT (include/hfpg.h hfpg_solver)."""
         check(lib.hfpg_set_solver(self.h, kind))

@@ -83,6 +83,8 @@ struct hfpg_handle {
 
     int precond = HFPG_PRECOND_FACTOR;
     int solver = HFPG_SOLVER_AUTO;
+    Scalars* sc_host = nullptr;  // pinned copy of the solve's scalars (async solves)
+    bool pending = false;
     unsigned* gbar = nullptr;  // grid-barrier counter of k_solve
     unsigned long long* trace = nullptr;  // k_solve barrier timestamps (hfpg_set_trace)
     unsigned trace_cap = 0;
@@ -622,6 +624,7 @@ int hfpg_destroy(hfpg_handle* h) {
         dfree(h->coupled); dfree(h->node_u); dfree(h->node_v);
         dfree(h->tree_counters); dfree(h->partials); dfree(h->counters); dfree(h->sc);
         dfree(h->history); dfree(h->gbar); dfree(h->trace);
+        if (h->sc_host) cudaFreeHost(h->sc_host);
         reset_partition(h);
         if (h->toynet) toynet_model_destroy(h->toynet);
         if (h->ev0) cudaEventDestroy(h->ev0);
@@ -763,54 +766,77 @@ int hfpg_spmv(hfpg_handle* h, const double* x, double* y, int where) {
     });
 }
 
+// Enqueue a solve on the handle's stream (no host synchronisation). The scalars land in the
+// handle's pinned report buffer; x (n) is copied to `where` memory.
+static void solve_enqueue(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg_in, double* x, int where) {
+    set_device(h);
+    hfpg_solve_config cfg = cfg_in ? *cfg_in : hfpg_solve_config{1e-8, 20000};
+    if (!(cfg.rtol > 0.0)) throw InvalidArgument("pcg_solve: rtol must be positive");
+    if (!h->have_csr) throw InvalidArgument("pcg_solve: no matrix loaded");
+    if (h->precond == HFPG_PRECOND_FACTOR) require_apply_ready(h);
+    require_part_ready(h);
+    ensure_workspace(h);
+    const uint64_t n = h->n;
+    const uint64_t hcap = std::max<uint64_t>(cfg.max_iters, 1);
+    if (h->history_cap < hcap) {
+        invalidate_graph(h);
+        dalloc(h->history, hcap);
+        h->history_cap = hcap;
+    }
+    if (!h->sc_host) CK(cudaMallocHost(reinterpret_cast<void**>(&h->sc_host), sizeof(Scalars)));
+    const bool persistent = use_persistent(h);
+    if (!persistent && !h->graph_valid) build_graph(h);
+    *h->sc_host = solve_scalars(h, cfg);
+    CK(cudaMemcpyAsync(h->sc, h->sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, h->stream));
+    copy_in(h, h->b, b, n, where);
+    CK(cudaEventRecord(h->ev0, h->stream));
+    if (persistent)
+        launch_persistent(h);
+    else
+        CK(cudaGraphLaunch(h->exec, h->stream));
+    CK(cudaEventRecord(h->ev1, h->stream));
+    CK(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
+    if (x) copy_out(h, x, h->x, n, where);
+    h->pending = true;
+}
+
+static void solve_finish(hfpg_handle* h, double* history, hfpg_report* report, int where) {
+    set_device(h);
+    if (!h->pending) throw InvalidArgument("pcg_solve_wait: no solve in flight");
+    h->pending = false;
+    CK(cudaStreamSynchronize(h->stream));
+    const Scalars out = *h->sc_host;
+    if (history && out.hist_len) {
+        copy_out(h, history, h->history, out.hist_len, where);
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    if (report) {
+        report->n = h->n;
+        report->iterations = out.iterations;
+        report->converged = out.converged;
+        report->status = out.status;
+        report->breakdown_iter = out.breakdown_iter;
+        report->history_len = out.hist_len;
+        report->wall_ms = ms;
+    }
+}
+
 int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg_in, double* x,
                    double* history, hfpg_report* report, int where) {
     return guarded([&] {
-        set_device(h);
-        hfpg_solve_config cfg = cfg_in ? *cfg_in : hfpg_solve_config{1e-8, 20000};
-        if (!(cfg.rtol > 0.0)) throw InvalidArgument("pcg_solve: rtol must be positive");
-        if (!h->have_csr) throw InvalidArgument("pcg_solve: no matrix loaded");
-        if (h->precond == HFPG_PRECOND_FACTOR) require_apply_ready(h);
-        require_part_ready(h);
-        ensure_workspace(h);
-        const uint64_t n = h->n;
-        const uint64_t hcap = std::max<uint64_t>(cfg.max_iters, 1);
-        if (h->history_cap < hcap) {
-            invalidate_graph(h);
-            dalloc(h->history, hcap);
-            h->history_cap = hcap;
-        }
-        const bool persistent = use_persistent(h);
-        if (!persistent && !h->graph_valid) build_graph(h);
-        const Scalars init = solve_scalars(h, cfg);
-        CK(cudaMemcpyAsync(h->sc, &init, sizeof(Scalars), cudaMemcpyHostToDevice, h->stream));
-        copy_in(h, h->b, b, n, where);
-        CK(cudaEventRecord(h->ev0, h->stream));
-        if (persistent)
-            launch_persistent(h);
-        else
-            CK(cudaGraphLaunch(h->exec, h->stream));
-        CK(cudaEventRecord(h->ev1, h->stream));
-        Scalars out{};
-        CK(cudaMemcpyAsync(&out, h->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
-        if (x) copy_out(h, x, h->x, n, where);
-        CK(cudaStreamSynchronize(h->stream));
-        if (history && out.hist_len) {
-            copy_out(h, history, h->history, out.hist_len, where);
-            CK(cudaStreamSynchronize(h->stream));
-        }
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
-        if (report) {
-            report->n = n;
-            report->iterations = out.iterations;
-            report->converged = out.converged;
-            report->status = out.status;
-            report->breakdown_iter = out.breakdown_iter;
-            report->history_len = out.hist_len;
-            report->wall_ms = ms;
-        }
+        solve_enqueue(h, b, cfg_in, x, where);
+        solve_finish(h, history, report, where);
     });
+}
+
+int hfpg_pcg_solve_async(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg, double* x, int where) {
+    return guarded([&] { solve_enqueue(h, b, cfg, x, where); });
+}
+
+int hfpg_pcg_solve_wait(hfpg_handle* h, double* history, hfpg_report* report, int where) {
+    return guarded([&] { solve_finish(h, history, report, where); });
 }
 
 int hfpg_launch_counts(hfpg_handle* h, uint32_t* per_iteration, uint32_t* per_apply) {
