@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(kAttThreads, 2)
                 dst[c] = make_float4(o[4 * c] * inv, o[4 * c + 1] * inv, o[4 * c + 2] * inv, o[4 * c + 3] * inv);
         }
         if (rowsum_err_bits) {
+            __syncthreads();  // both quads have read part[] for the row total
             sm.part[quad][row] = rs_trace * inv;
             __syncthreads();
             if (quad == 0) atomicMax(rowsum_err_bits, __float_as_uint(fabsf(sm.part[0][row] + sm.part[1][row] - 1.f)));
