@@ -137,6 +137,32 @@ int hfpg_frame_copy(const hfpg_frame* f, uint32_t* cell_order, double* rho,
                     uint64_t* row_offsets, uint32_t* col_indices, double* values, double* b);
 void hfpg_frame_free(hfpg_frame* f);
 
+/* ---- GPU frame generator (new; framegen.cuh) ---------------------------------------------
+ * make_frame (frame.cpp:161-181) / hfpg_frame_3d generated on the handle's device and loaded as
+ * its system (operator, diagonal, |A|_F): no host round trip. Morton order and CSR structure
+ * are bit-identical to hfpg_frame_2d/3d; floating values are bit-identical to them under
+ * HFPG_FRAME_CRMATH=1 (correctly rounded log/cos) and within one ulp of the glibc draws on the
+ * ~0.16% of normals glibc rounds incorrectly. The arrays stay valid until the next frame. */
+typedef struct {
+    uint64_t n, nnz, width, height, depth;
+    double rho_heavy;
+    const uint32_t* cell_order; /* device pointers */
+    const double* rho;
+    const uint64_t* row_offsets;
+    const uint32_t* col_indices;
+    const double* values;
+    const double* b;
+    const double* a_diag;
+    float generate_ms; /* device time of the generation (events on the handle's stream) */
+} hfpg_frame_device;
+int hfpg_frame_gpu_2d(hfpg_handle* h, uint64_t n, uint64_t seed, uint64_t frame_index);
+int hfpg_frame_gpu_3d(hfpg_handle* h, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t seed,
+                      uint64_t frame_index);
+int hfpg_frame_gpu_view(hfpg_handle* h, hfpg_frame_device* out);
+/* Copy the GPU frame to host arrays (any pointer may be NULL). */
+int hfpg_frame_gpu_copy(hfpg_handle* h, uint32_t* cell_order, double* rho, uint64_t* row_offsets,
+                        uint32_t* col_indices, double* values, double* b);
+
 /* Pinned host memory for the end-to-end path (cudaMallocHost). */
 int hfpg_host_alloc(uint64_t bytes, void** out);
 int hfpg_host_free(void* p);

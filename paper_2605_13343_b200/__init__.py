@@ -4,7 +4,7 @@ preconditioner of arxiv 2605.13343, behind the reference `hfp` API.
 The product is the native library `libhfpg.so` (C ABI in include/hfpg.h, CUDA kernels in
 csrc/); this package is the Python mirror of the reference interface over that ABI.
 """
-from .api import (Checkpoint, CsrMatrix, Device, FactorInit, FactorLayout, FactorTensor, Frame,
+from .api import (Checkpoint, CsrMatrix, Device, FactorInit, FactorLayout, FactorTensor, Frame, GpuFrame,
                   HPartition, PrecondApplier, RngPurpose, RngStream, SolveConfig, SolveReport,
                   SolveStatus, TileSpec, ToynetConfig, ToynetTrace, apply, build_partition, clamp_leaf_size, factor_applier,
                   identity_applier, init_factors, jacobi_applier, make_factor_layout, make_frame,

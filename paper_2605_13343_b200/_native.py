@@ -54,6 +54,13 @@ class FrameViewC(C.Structure):
                 ("rho_heavy", dbl), ("row_offsets", vp), ("col_indices", vp), ("values", vp)]
 
 
+class FrameDeviceC(C.Structure):
+    _fields_ = [("n", u64), ("nnz", u64), ("width", u64), ("height", u64), ("depth", u64),
+                ("rho_heavy", dbl), ("cell_order", vp), ("rho", vp), ("row_offsets", vp),
+                ("col_indices", vp), ("values", vp), ("b", vp), ("a_diag", vp),
+                ("generate_ms", C.c_float)]
+
+
 class CudaError(RuntimeError):
     """A CUDA failure inside libhfpg (HFPG_ECUDA)."""
 
@@ -73,6 +80,10 @@ _PROTOS = {
     "hfpg_frame_info": (C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64),
                                   C.POINTER(u64), C.POINTER(u64), C.POINTER(dbl)]),
     "hfpg_frame_copy": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+    "hfpg_frame_gpu_2d": (C.c_int, [vp, u64, u64, u64]),
+    "hfpg_frame_gpu_3d": (C.c_int, [vp, u64, u64, u64, u64, u64]),
+    "hfpg_frame_gpu_view": (C.c_int, [vp, C.POINTER(FrameDeviceC)]),
+    "hfpg_frame_gpu_copy": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
     "hfpg_frame_free": (None, [vp]),
     "hfpg_host_alloc": (C.c_int, [u64, C.POINTER(vp)]),
     "hfpg_host_free": (C.c_int, [vp]),

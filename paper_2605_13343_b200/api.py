@@ -302,6 +302,43 @@ def test_frame_id(scale: int, i: int) -> int:
 # --------------------------------------------------------------------------- device handle
 
 
+@dataclass
+class GpuFrame:
+    """A frame generated on the device (Device.frame_gpu / frame_gpu_3d) and loaded as that
+    device's system; `b`, `rho`, ... are device pointers, valid until the next frame."""
+    n: int
+    nnz: int
+    width: int
+    height: int
+    depth: int
+    rho_heavy: float
+    cell_order: int
+    rho: int
+    row_offsets: int
+    col_indices: int
+    values: int
+    b: int
+    a_diag: int
+    generate_ms: float
+    master_seed: int
+    frame_index: int
+    device: "Device"
+
+    def to_host(self) -> Frame:
+        """Download as a host Frame (same fields as make_frame / make_frame_3d)."""
+        co = np.empty(self.n, np.uint32)
+        rho = np.empty(self.n)
+        ro = np.empty(self.n + 1, np.uint64)
+        ci = np.empty(self.nnz, np.uint32)
+        v = np.empty(self.nnz)
+        b = np.empty(self.n)
+        check(lib.hfpg_frame_gpu_copy(self.device.h, co.ctypes.data, rho.ctypes.data, ro.ctypes.data,
+                                      ci.ctypes.data, v.ctypes.data, b.ctypes.data))
+        return Frame(self.n, self.width, self.height, self.depth, co, rho,
+                     CsrMatrix(self.n, self.n, ro, ci, v), b, self.rho_heavy, self.master_seed,
+                     self.frame_index)
+
+
 class Device:
     """One hfpg handle: a CUDA stream + device-resident operator, factors and workspace."""
 
@@ -322,6 +359,24 @@ class Device:
         check(lib.hfpg_load_csr(self.h, A.n_rows, A.row_offsets.ctypes.data,
                                 A.col_indices.ctypes.data, A.values.ctypes.data, N.HOST))
         self.csr_id = id(A)
+
+    def _gpu_frame(self, seed, fidx) -> GpuFrame:
+        v = N.FrameDeviceC()
+        check(lib.hfpg_frame_gpu_view(self.h, C.byref(v)))
+        self.csr_id = ("gpu_frame", seed, fidx)
+        return GpuFrame(v.n, v.nnz, v.width, v.height, v.depth, v.rho_heavy, v.cell_order or 0,
+                        v.rho or 0, v.row_offsets or 0, v.col_indices or 0, v.values or 0, v.b or 0,
+                        v.a_diag or 0, float(v.generate_ms), seed, fidx, self)
+
+    def frame_gpu(self, n: int, master_seed: int, frame_index: int) -> GpuFrame:
+        """make_frame (frame.cpp:161-181) generated on this device and loaded as its system."""
+        check(lib.hfpg_frame_gpu_2d(self.h, n, master_seed, frame_index))
+        return self._gpu_frame(master_seed, frame_index)
+
+    def frame_gpu_3d(self, nx: int, ny: int, nz: int, master_seed: int, frame_index: int) -> GpuFrame:
+        """make_frame_3d generated on this device and loaded as its system."""
+        check(lib.hfpg_frame_gpu_3d(self.h, nx, ny, nz, master_seed, frame_index))
+        return self._gpu_frame(master_seed, frame_index)
 
     def load_csr_device(self, n, ro_ptr, ci_ptr, v_ptr):
         check(lib.hfpg_load_csr(self.h, n, ro_ptr, ci_ptr, v_ptr, N.DEVICE))

@@ -3,6 +3,7 @@
 #include "kernels.cuh"
 #include "solve_persistent.cuh"
 #include "partition_host.hpp"
+#include "framegen.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -114,6 +115,23 @@ struct hfpg_handle {
         std::vector<void*> ipc_opened;
     } part;
     uint64_t vec_ng = 0;  // ghost entries the z/p vectors were sized for
+
+    // operator storage capacities (a GPU frame per step reuses them)
+    uint64_t sell_cap = 0, slice_cap = 0, diag_cap = 0;
+
+    // GPU-generated frame (framegen.cuh), resident and loaded as the system
+    struct FrameDev {
+        bool valid = false;
+        FgParams P{};
+        uint64_t nnz = 0, cap_cells = 0, cap_n = 0, cap_nnz = 0;
+        uint32_t *order = nullptr, *rank_of = nullptr, *len = nullptr, *ci = nullptr, *slice_len = nullptr;
+        double *rho = nullptr, *b = nullptr, *vals = nullptr, *sums = nullptr;
+        unsigned long long *ro = nullptr, *tot = nullptr, *tail = nullptr;  // tail: nnz, nonpos, maxch8, maxch16
+        unsigned long long* tail_host = nullptr;
+        cudaStream_t side[2] = {nullptr, nullptr};
+        cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+        float gen_ms = 0.f;
+    } fr;
 };
 
 namespace {
@@ -502,6 +520,9 @@ void upload_csr(hfpg_handle* h, uint64_t n, const std::vector<uint64_t>& ro,
     dalloc(h->sell_cols, sc.size());
     dalloc(h->sell_vals, sv.size());
     dalloc(h->a_diag, n);
+    h->sell_cap = sc.size();
+    h->slice_cap = ns + 1;
+    h->diag_cap = n;
     CK(cudaMemcpy(h->slice_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->sell_cols, sc.data(), sc.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->sell_vals, sv.data(), sv.size() * 8, cudaMemcpyHostToDevice));
@@ -572,6 +593,149 @@ void check_group(hfpg_handle* const* hs, uint32_t G) {
         if (!h->fast) throw InvalidArgument("group: fast layout (L=128, L_s=32) required");
     }
 }
+
+unsigned fg_blocks(const hfpg_handle* h, uint64_t items) {
+    return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((items + 255) / 256, uint64_t(h->num_sms) * 16)));
+}
+
+// u32 counts -> u64 exclusive offsets, out[n] = total (three passes, framegen.cuh).
+void scan_counts(hfpg_handle* h, cudaStream_t st, const uint32_t* in, uint64_t n, unsigned long long* out) {
+    auto& F = h->fr;
+    const uint64_t tiles = std::max<uint64_t>(1, (n + kScanTile - 1) / kScanTile);
+    k_scan_tiles<<<unsigned(tiles), kScanThreads, 0, st>>>(in, n, out, F.tot);
+    k_scan_totals<<<1, kScanThreads, 0, st>>>(F.tot, tiles, out + n);
+    k_scan_add<<<unsigned(tiles), kScanThreads, 0, st>>>(out, n, F.tot);
+    CK(cudaGetLastError());
+}
+
+// make_frame / frame_3d on the GPU, loaded as the handle's system (framegen.cuh).
+void frame_gpu(hfpg_handle* h, const FrameParams& FP) {
+    set_device(h);
+    if (h->part.G > 1) reset_partition(h);
+    auto& F = h->fr;
+    FgParams P{};
+    P.dims = FP.dims;
+    P.nb = int(FP.bars.size());
+    P.n = FP.n;
+    P.W = FP.W;
+    P.H = FP.H;
+    P.D = FP.D;
+    P.rho_heavy = FP.rho_heavy;
+    P.density_key = FP.density_key;
+    P.c0 = FP.c0;
+    P.rhs_key = FP.rhs_key;
+    for (int k = 0; k < P.nb; ++k)
+        P.bars[k] = {int(FP.bars[k].axis), int(FP.bars[k].gap), FP.bars[k].center, FP.bars[k].thickness};
+    const uint64_t big = std::max(P.W, std::max(P.H, P.D));
+    P.levels = 0;
+    while ((1ULL << P.levels) < big) ++P.levels;
+    const uint64_t n = P.n, cells = P.W * P.H * P.D, ns = (n + 31) / 32;
+    const uint64_t nnz_max = n * uint64_t(1 + 2 * P.dims), sell_max = ns * 32 * uint64_t(1 + 2 * P.dims);
+
+    if (!F.side[0]) {
+        for (auto& st : F.side) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        for (auto& e : F.ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaMallocHost(reinterpret_cast<void**>(&F.tail_host), 8 * sizeof(unsigned long long)));
+        dalloc(F.sums, 2);
+        dalloc(F.tail, 8);
+    }
+    // per-frame arrays: every per-row array is sized n + 1, every per-entry array nnz_max
+    if (cells > F.cap_cells || !F.rank_of) {
+        dalloc(F.rank_of, cells);
+        F.cap_cells = cells;
+    }
+    if (n + 1 > F.cap_n || !F.order) {
+        for (uint32_t** p : {&F.order, &F.len, &F.slice_len}) dalloc(*p, n + 1);
+        for (double** p : {&F.rho, &F.b}) dalloc(*p, n + 1);
+        for (unsigned long long** p : {&F.ro, &F.tot}) dalloc(*p, n + 1);
+        F.cap_n = n + 1;
+    }
+    if (nnz_max > F.cap_nnz || !F.ci) {
+        dalloc(F.ci, nnz_max);
+        dalloc(F.vals, nnz_max);
+        F.cap_nnz = nnz_max;
+    }
+    F.valid = false;
+
+    // the handle's operator arrays: reuse when large enough (pointers stay put -> graph stays valid)
+    const bool realloc_op = sell_max > h->sell_cap || ns + 1 > h->slice_cap || n > h->diag_cap ||
+                            !h->sell_cols || !h->slice_off || !h->a_diag;
+    if (realloc_op) {
+        invalidate_graph(h);
+        dalloc(h->sell_cols, sell_max);
+        dalloc(h->sell_vals, sell_max);
+        dalloc(h->slice_off, ns + 1);
+        dalloc(h->a_diag, n);
+        h->sell_cap = sell_max;
+        h->slice_cap = ns + 1;
+        h->diag_cap = n;
+    }
+
+    cudaStream_t st = h->stream;
+    cudaEvent_t t0 = h->ev0, t1 = h->ev1;
+    CK(cudaEventRecord(t0, st));
+    CK(cudaMemsetAsync(F.tail, 0, 8 * sizeof(unsigned long long), st));
+    k_fg_rank<<<fg_blocks(h, cells), 256, 0, st>>>(P, F.order, F.rank_of);
+    k_fg_cells<<<fg_blocks(h, n), 256, 0, st>>>(P, F.order, F.rank_of, F.rho, F.len, F.b);
+    CK(cudaGetLastError());
+    // sum of b on side stream 0 (overlaps assembly and SELL), then b -= mean
+    CK(cudaEventRecord(F.ev[0], st));
+    CK(cudaStreamWaitEvent(F.side[0], F.ev[0], 0));
+    k_fg_chain<<<1, kFgChainThreads, 0, F.side[0]>>>(F.b, n, nullptr, 0, F.sums);
+    k_fg_center<<<fg_blocks(h, n), 256, 0, F.side[0]>>>(F.b, n, F.sums);
+    CK(cudaGetLastError());
+    scan_counts(h, st, F.len, n, F.ro);
+    k_fg_assemble<<<fg_blocks(h, n), 256, 0, st>>>(P, F.order, F.rank_of, F.rho, F.ro, F.ci, F.vals,
+                                                   h->a_diag, reinterpret_cast<unsigned*>(F.tail + 1));
+    CK(cudaGetLastError());
+    // sum of v^2 on side stream 1
+    CK(cudaEventRecord(F.ev[1], st));
+    CK(cudaStreamWaitEvent(F.side[1], F.ev[1], 0));
+    k_fg_chain<<<1, kFgChainThreads, 0, F.side[1]>>>(F.vals, 0, F.ro + n, 1, F.sums + 1);
+    CK(cudaGetLastError());
+    // SELL-32
+    k_sell_widths<<<unsigned((ns + 7) / 8), 256, 0, st>>>(F.len, n, ns, F.slice_len);
+    scan_counts(h, st, F.slice_len, ns, h->slice_off);
+    k_sell_fill<<<unsigned((ns + 7) / 8), 256, 0, st>>>(F.ro, F.ci, F.vals, n, ns, h->slice_off,
+                                                         h->sell_cols, h->sell_vals);
+    k_sell_chunks<<<unsigned((ns + 8 * 256 - 1) / (8 * 256)), 256, 0, st>>>(h->slice_off, ns, F.tail + 2);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(F.ev[0], F.side[0]));
+    CK(cudaEventRecord(F.ev[1], F.side[1]));
+    CK(cudaStreamWaitEvent(st, F.ev[0], 0));
+    CK(cudaStreamWaitEvent(st, F.ev[1], 0));
+    CK(cudaMemcpyAsync(F.tail, F.ro + n, 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(F.tail + 4, F.sums, 16, cudaMemcpyDeviceToDevice, st));
+    CK(cudaEventRecord(t1, st));
+    CK(cudaMemcpyAsync(F.tail_host, F.tail, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaEventElapsedTime(&F.gen_ms, t0, t1));
+
+    const unsigned long long* T = F.tail_host;
+    F.nnz = T[0];
+    double sums[2];
+    std::memcpy(sums, T + 4, 16);
+    F.P = P;
+    F.valid = true;
+
+    // the state upload_csr leaves (csr.cpp:52-68; stage sizes as upload_csr computes them)
+    h->fro = std::sqrt(sums[1]);
+    h->diag_positive = (T[1] & 0xFFFFFFFFULL) == 0;
+    uint64_t maxch = (T[2] + 1023) & ~uint64_t(1023);
+    const uint32_t sb = (maxch > 0 && maxch * kSpmvStages + 128 <= 110 * 1024) ? uint32_t(maxch) : 0;
+    const uint64_t maxch16 = (T[3] + 127) & ~uint64_t(127);
+    const uint32_t psb = (maxch16 > 0 && 2 * maxch16 <= sizeof(PStage)) ? uint32_t(maxch16) : 0;
+    const bool no_tma = std::getenv("HFPG_NO_SPMV_TMA") != nullptr;
+    const uint32_t sb2 = no_tma ? 0 : sb, psb2 = no_tma ? 0 : psb;
+    if (h->n != n || sb2 != h->spmv_stage_bytes || psb2 != h->pspmv_stage_bytes) invalidate_graph(h);
+    h->spmv_stage_bytes = sb2;
+    h->pspmv_stage_bytes = psb2;
+    h->n = n;
+    h->have_csr = true;
+    h->have_diag = true;
+    ensure_workspace(h);
+}
+
 }  // namespace
 
 extern "C" {
@@ -625,6 +789,14 @@ int hfpg_destroy(hfpg_handle* h) {
         dfree(h->tree_counters); dfree(h->partials); dfree(h->counters); dfree(h->sc);
         dfree(h->history); dfree(h->gbar); dfree(h->trace);
         if (h->sc_host) cudaFreeHost(h->sc_host);
+        {
+            auto& F = h->fr;
+            dfree(F.order); dfree(F.rank_of); dfree(F.len); dfree(F.ci); dfree(F.slice_len);
+            dfree(F.rho); dfree(F.b); dfree(F.vals); dfree(F.sums); dfree(F.ro); dfree(F.tot); dfree(F.tail);
+            if (F.tail_host) cudaFreeHost(F.tail_host);
+            for (auto& st : F.side) if (st) cudaStreamDestroy(st);
+            for (auto& e : F.ev) if (e) cudaEventDestroy(e);
+        }
         reset_partition(h);
         if (h->toynet) toynet_model_destroy(h->toynet);
         if (h->ev0) cudaEventDestroy(h->ev0);
@@ -672,6 +844,56 @@ int hfpg_load_csr(hfpg_handle* h, uint64_t n, const uint64_t* ro_in, const uint3
     });
 }
 
+int hfpg_frame_gpu_2d(hfpg_handle* h, uint64_t n, uint64_t seed, uint64_t frame_index) {
+    return guarded([&] { frame_gpu(h, frame_params_2d(n, seed, frame_index)); });
+}
+
+int hfpg_frame_gpu_3d(hfpg_handle* h, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t seed,
+                      uint64_t frame_index) {
+    return guarded([&] { frame_gpu(h, frame_params_3d(nx, ny, nz, seed, frame_index)); });
+}
+
+int hfpg_frame_gpu_view(hfpg_handle* h, hfpg_frame_device* out) {
+    return guarded([&] {
+        const auto& F = h->fr;
+        if (!F.valid) throw InvalidArgument("frame_gpu: no GPU frame generated on this handle");
+        out->n = F.P.n;
+        out->nnz = F.nnz;
+        out->width = F.P.W;
+        out->height = F.P.H;
+        out->depth = F.P.D;
+        out->rho_heavy = F.P.rho_heavy;
+        out->cell_order = F.order;
+        out->rho = F.rho;
+        out->row_offsets = reinterpret_cast<uint64_t*>(F.ro);
+        out->col_indices = F.ci;
+        out->values = F.vals;
+        out->b = F.b;
+        out->a_diag = h->a_diag;
+        out->generate_ms = F.gen_ms;
+    });
+}
+
+int hfpg_frame_gpu_copy(hfpg_handle* h, uint32_t* cell_order, double* rho, uint64_t* row_offsets,
+                        uint32_t* col_indices, double* values, double* b) {
+    return guarded([&] {
+        set_device(h);
+        const auto& F = h->fr;
+        if (!F.valid) throw InvalidArgument("frame_gpu: no GPU frame generated on this handle");
+        const uint64_t n = F.P.n;
+        auto d2h = [&](void* dst, const void* src, size_t bytes) {
+            if (dst) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->stream));
+        };
+        d2h(cell_order, F.order, n * 4);
+        d2h(rho, F.rho, n * 8);
+        d2h(row_offsets, F.ro, (n + 1) * 8);
+        d2h(col_indices, F.ci, F.nnz * 4);
+        d2h(values, F.vals, F.nnz * 8);
+        d2h(b, F.b, n * 8);
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
 int hfpg_set_diag(hfpg_handle* h, uint64_t n, const double* a_diag, int where) {
     return guarded([&] {
         set_device(h);
@@ -679,6 +901,7 @@ int hfpg_set_diag(hfpg_handle* h, uint64_t n, const double* a_diag, int where) {
         if (!h->have_csr) h->n = n;
         invalidate_graph(h);
         dalloc(h->a_diag, n);
+        h->diag_cap = n;
         copy_in(h, h->a_diag, a_diag, n, where);
         CK(cudaStreamSynchronize(h->stream));
         h->have_diag = true;

@@ -4,6 +4,7 @@
 // Native C++, multi-threaded where the reference is a sequential loop over a counter-based
 // stream, and bit-identical to it (tests/test_host.py pins this against oracle/_ref).
 #include "internal.hpp"
+#include "crmath.cuh"
 
 #include <zlib.h>
 
@@ -108,12 +109,7 @@ static uint64_t spread3(uint64_t v) {  // 21 bits -> every third bit
 }
 
 // frame.cpp:60-79 in_heavy_region, generalised to an axis triple (2D: cross/along = x|y).
-struct Barrier {
-    uint64_t axis = 0;  // 2D: 0 vertical (cross = x), 1 horizontal (cross = y); 3D: slab normal
-    double center = 0.5, thickness = 0.1;
-    uint64_t gap = 3;   // frame.hpp:15 top/bottom/middle_hole/closed
-};
-static bool heavy_at(double cross, double along, const Barrier& b) {
+static bool heavy_at(double cross, double along, const FrameBarrier& b) {
     if (std::fabs(cross - b.center) > 0.5 * b.thickness) return false;
     switch (b.gap) {
         case 0: return along < 0.8;
@@ -124,12 +120,12 @@ static bool heavy_at(double cross, double along, const Barrier& b) {
 }
 
 // frame.cpp:81-98 sample_density: rho_heavy ~ loguniform[5,100], 1-3 barriers.
-static std::vector<Barrier> sample_barriers(Rng& s, uint64_t n_axes, double& rho_heavy) {
+static std::vector<FrameBarrier> sample_barriers(Rng& s, uint64_t n_axes, double& rho_heavy) {
     rho_heavy = std::exp(s.uniform(std::log(5.0), std::log(100.0)));
     const uint64_t nb = 1 + s.below(3);
-    std::vector<Barrier> bars;
+    std::vector<FrameBarrier> bars;
     for (uint64_t i = 0; i < nb; ++i) {
-        Barrier b;
+        FrameBarrier b;
         b.axis = s.below(n_axes);
         b.center = s.uniform(0.2, 0.8);
         b.thickness = s.uniform(0.05, 0.20);
@@ -139,12 +135,60 @@ static std::vector<Barrier> sample_barriers(Rng& s, uint64_t n_axes, double& rho
     return bars;
 }
 
+bool frame_crmath() {
+    const char* e = std::getenv("HFPG_FRAME_CRMATH");
+    return e && e[0] == '1';
+}
+static double frame_normal(bool cr, uint64_t bits) {
+    return cr ? crm::normal_of_cr(bits) : Rng::normal_of(bits);
+}
+
+// frame.cpp:161-166 grid_dims and the density/rhs streams of make_frame.
+FrameParams frame_params_2d(uint64_t n, uint64_t seed, uint64_t fidx) {
+    if (n < 4) throw InvalidArgument("grid_dims: need at least 4 cells");
+    uint64_t w = static_cast<uint64_t>(std::ceil(std::sqrt(static_cast<double>(n))));
+    while (w * w < n) ++w;
+    const uint64_t h = (n + w - 1) / w;
+    if (w >= (1u << 16) || h >= (1u << 16))
+        throw InvalidArgument("morton_cell_order: grid dimension >= 2^16");
+    FrameParams P;
+    P.dims = 2;
+    P.n = n;
+    P.W = w;
+    P.H = h;
+    Rng s(seed, fidx, kDensity);
+    P.bars = sample_barriers(s, 2, P.rho_heavy);
+    P.density_key = s.key;
+    P.c0 = s.counter;  // one normal per retained cell follows, in Morton order
+    P.rhs_key = Rng(seed, fidx, kRhs).key;
+    return P;
+}
+
+FrameParams frame_params_3d(uint64_t nx, uint64_t ny, uint64_t nz, uint64_t seed, uint64_t fidx) {
+    if (nx < 2 || ny < 2 || nz < 2) throw InvalidArgument("frame_3d: each dimension must be >= 2");
+    if (nx > (1u << 21) || ny > (1u << 21) || nz > (1u << 21) || nx * ny * nz > (1ULL << 32))
+        throw InvalidArgument("frame_3d: grid too large");
+    FrameParams P;
+    P.dims = 3;
+    P.n = nx * ny * nz;
+    P.W = nx;
+    P.H = ny;
+    P.D = nz;
+    Rng s(seed, fidx, kDensity);
+    P.bars = sample_barriers(s, 3, P.rho_heavy);
+    P.density_key = s.key;
+    P.c0 = s.counter;
+    P.rhs_key = Rng(seed, fidx, kRhs).key;
+    return P;
+}
+
 // frame.cpp:154-159 sample_rhs: normals, then b -= mean (sequential mean, :147-152).
 static std::vector<double> sample_rhs(uint64_t n, uint64_t seed, uint64_t frame) {
     const Rng s(seed, frame, kRhs);
+    const bool cr = frame_crmath();
     std::vector<double> b(n);
     parallel_for(n, [&](uint64_t lo, uint64_t hi) {
-        for (uint64_t i = lo; i < hi; ++i) b[i] = Rng::normal_of(s.bits_at(i));
+        for (uint64_t i = lo; i < hi; ++i) b[i] = frame_normal(cr, s.bits_at(i));
     });
     double mean = 0.0;
     for (double v : b) mean += v;
@@ -222,16 +266,13 @@ static Csr assemble(const std::vector<double>& rho, const std::vector<uint32_t>&
 // frame.cpp:161-181 make_frame (2D): W = ceil(sqrt N), H = ceil(N/W); Morton-sorted cells
 // truncated to N; barrier density with multiplicative noise; Neumann Laplacian; projected rhs.
 static hfpg_frame* frame_2d(uint64_t n, uint64_t seed, uint64_t fidx) {
-    if (n < 4) throw InvalidArgument("grid_dims: need at least 4 cells");
-    uint64_t w = static_cast<uint64_t>(std::ceil(std::sqrt(static_cast<double>(n))));
-    while (w * w < n) ++w;
-    const uint64_t h = (n + w - 1) / w;
-    if (w >= (1u << 16) || h >= (1u << 16))
-        throw InvalidArgument("morton_cell_order: grid dimension >= 2^16");
+    const FrameParams P = frame_params_2d(n, seed, fidx);
+    const uint64_t w = P.W, h = P.H;
     auto* f = new hfpg_frame;
     f->n = n;
     f->width = w;
     f->height = h;
+    f->rho_heavy = P.rho_heavy;
     // frame.cpp:24-41: Morton codes are unique per cell, so a key sort equals the reference's
     // comparator sort.
     std::vector<std::pair<uint32_t, uint32_t>> keyed(w * h);
@@ -243,9 +284,8 @@ static hfpg_frame* frame_2d(uint64_t n, uint64_t seed, uint64_t fidx) {
     f->cell_order.resize(n);
     for (uint64_t i = 0; i < n; ++i) f->cell_order[i] = keyed[i].second;
 
-    Rng s(seed, fidx, kDensity);
-    auto bars = sample_barriers(s, 2, f->rho_heavy);
-    const uint64_t c0 = s.counter;  // one normal per retained cell follows, in Morton order
+    const Rng s(seed, fidx, kDensity);
+    const bool cr = frame_crmath();
     f->rho.resize(n);
     parallel_for(n, [&](uint64_t lo, uint64_t hi) {
         for (uint64_t i = lo; i < hi; ++i) {
@@ -253,14 +293,14 @@ static hfpg_frame* frame_2d(uint64_t n, uint64_t seed, uint64_t fidx) {
             const double xn = (static_cast<double>(id % w) + 0.5) / static_cast<double>(w);
             const double yn = (static_cast<double>(id / w) + 0.5) / static_cast<double>(h);
             bool heavy = false;
-            for (const Barrier& b : bars) {
+            for (const FrameBarrier& b : P.bars) {
                 const double cross = b.axis == 0 ? xn : yn, along = b.axis == 0 ? yn : xn;
                 if (heavy_at(cross, along, b)) {
                     heavy = true;
                     break;
                 }
             }
-            const double noise = std::max(0.5, 1.0 + 0.05 * Rng::normal_of(s.bits_at(c0 + i)));
+            const double noise = std::max(0.5, 1.0 + 0.05 * frame_normal(cr, s.bits_at(P.c0 + i)));
             f->rho[i] = (heavy ? f->rho_heavy : 1.0) * noise;
         }
     });
@@ -274,15 +314,14 @@ static hfpg_frame* frame_2d(uint64_t n, uint64_t seed, uint64_t fidx) {
 // running along the next axis; 7-point harmonic-mean Neumann Laplacian; projected rhs.
 static hfpg_frame* frame_3d(uint64_t nx, uint64_t ny, uint64_t nz, uint64_t seed,
                             uint64_t fidx) {
-    if (nx < 2 || ny < 2 || nz < 2) throw InvalidArgument("frame_3d: each dimension must be >= 2");
-    if (nx > (1u << 21) || ny > (1u << 21) || nz > (1u << 21) || nx * ny * nz > (1ULL << 32))
-        throw InvalidArgument("frame_3d: grid too large");
+    const FrameParams P = frame_params_3d(nx, ny, nz, seed, fidx);
     auto* f = new hfpg_frame;
-    const uint64_t n = nx * ny * nz;
+    const uint64_t n = P.n;
     f->n = n;
     f->width = nx;
     f->height = ny;
     f->depth = nz;
+    f->rho_heavy = P.rho_heavy;
     std::vector<std::pair<uint64_t, uint32_t>> keyed(n);
     parallel_for(n, [&](uint64_t lo, uint64_t hi) {
         for (uint64_t id = lo; id < hi; ++id) {
@@ -294,9 +333,8 @@ static hfpg_frame* frame_3d(uint64_t nx, uint64_t ny, uint64_t nz, uint64_t seed
     f->cell_order.resize(n);
     for (uint64_t i = 0; i < n; ++i) f->cell_order[i] = keyed[i].second;
 
-    Rng s(seed, fidx, kDensity);
-    auto bars = sample_barriers(s, 3, f->rho_heavy);
-    const uint64_t c0 = s.counter;
+    const Rng s(seed, fidx, kDensity);
+    const bool cr = frame_crmath();
     f->rho.resize(n);
     parallel_for(n, [&](uint64_t lo, uint64_t hi) {
         for (uint64_t i = lo; i < hi; ++i) {
@@ -305,12 +343,12 @@ static hfpg_frame* frame_3d(uint64_t nx, uint64_t ny, uint64_t nz, uint64_t seed
                                  (double((id / nx) % ny) + 0.5) / double(ny),
                                  (double(id / (nx * ny)) + 0.5) / double(nz)};
             bool heavy = false;
-            for (const Barrier& b : bars)
+            for (const FrameBarrier& b : P.bars)
                 if (heavy_at(c[b.axis], c[(b.axis + 1) % 3], b)) {
                     heavy = true;
                     break;
                 }
-            const double noise = std::max(0.5, 1.0 + 0.05 * Rng::normal_of(s.bits_at(c0 + i)));
+            const double noise = std::max(0.5, 1.0 + 0.05 * frame_normal(cr, s.bits_at(P.c0 + i)));
             f->rho[i] = (heavy ? f->rho_heavy : 1.0) * noise;
         }
     });

@@ -81,6 +81,27 @@ struct Rng {
     double normal() { return normal_of(bits()); }
 };
 
+// ---- frame parameters (frame.cpp:45-98, :161-181): everything a frame draws before its
+// per-cell arrays, shared by the host generator and the GPU generator (framegen.cuh) ----------
+struct FrameBarrier {
+    uint64_t axis = 0;  // 2D: 0 vertical (cross = x), 1 horizontal (cross = y); 3D: slab normal
+    double center = 0.5, thickness = 0.1;
+    uint64_t gap = 3;   // frame.hpp:15 top/bottom/middle_hole/closed
+};
+struct FrameParams {
+    int dims = 2;
+    uint64_t n = 0, W = 0, H = 0, D = 1;  // 2D: the first n cells of W x H in Morton order
+    double rho_heavy = 0.0;
+    uint64_t density_key = 0, c0 = 0;  // noise of retained cell i = normal(density stream @ c0+i)
+    uint64_t rhs_key = 0;              // b_i = normal(rhs stream @ i) before centring
+    std::vector<FrameBarrier> bars;
+};
+FrameParams frame_params_2d(uint64_t n, uint64_t seed, uint64_t fidx);
+FrameParams frame_params_3d(uint64_t nx, uint64_t ny, uint64_t nz, uint64_t seed, uint64_t fidx);
+// HFPG_FRAME_CRMATH=1: the host generator draws its normals with crmath.cuh's correctly
+// rounded log/cos (what the GPU generator computes) instead of libm's.
+bool frame_crmath();
+
 // ---- partition / layout: partition.cpp:9-53, factor_tensor.cpp:7-28 ---------------------
 struct Layout {
     uint64_t n = 0, l = 0, ls = 0, rk = 0, k = 0, m = 0, depth = 0;  // depth = log2 K
