@@ -154,11 +154,17 @@ typedef struct {
     const double* b;
     const double* a_diag;
     float generate_ms; /* device time of the generation (events on the handle's stream) */
+    double frobenius;  /* |A|_F = sqrt of the sequential fused sum of squares (csr.cpp:64-68) */
 } hfpg_frame_device;
 int hfpg_frame_gpu_2d(hfpg_handle* h, uint64_t n, uint64_t seed, uint64_t frame_index);
 int hfpg_frame_gpu_3d(hfpg_handle* h, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t seed,
                       uint64_t frame_index);
 int hfpg_frame_gpu_view(hfpg_handle* h, hfpg_frame_device* out);
+/* The generator's sequential sums as a primitive: *out = (((0 + x0) + x1) + ...) in exactly the
+ * rounding order of the one-thread loop (squares != 0: s = fma(x_i, x_i, s), csr.cpp:64-68 as the
+ * host build contracts it), computed by the exact parallel emulation (framegen.cuh k_seq_sum).
+ * x is a host (HFPG_HOST) or device pointer. */
+int hfpg_seq_sum(hfpg_handle* h, const double* x, uint64_t n, int32_t squares, int where, double* out);
 /* Copy the GPU frame to host arrays (any pointer may be NULL). */
 int hfpg_frame_gpu_copy(hfpg_handle* h, uint32_t* cell_order, double* rho, uint64_t* row_offsets,
                         uint32_t* col_indices, double* values, double* b);

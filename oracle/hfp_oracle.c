@@ -352,3 +352,15 @@ int orc_pcg_solve(uint64_t n, const uint64_t* ro, const uint32_t* ci, const doub
     free(diag); free(x); free(r); free(z); free(p); free(q);
     return 0;
 }
+
+/* frame.cpp:147-152 (the rhs mean's sum) and csr.cpp:64-68 (|A|_F^2, one fused multiply-add per
+ * entry as the reference's -march=native build contracts `fro += v * v`): the sequential sums the
+ * GPU frame generator reproduces bit for bit. */
+double orc_seq_sum(const double* x, uint64_t n, int squares) {
+    double s = 0.0;
+    if (squares)
+        for (uint64_t i = 0; i < n; ++i) s = fma(x[i], x[i], s);
+    else
+        for (uint64_t i = 0; i < n; ++i) s = s + x[i];
+    return s;
+}

@@ -55,6 +55,9 @@ int orc_pcg_solve(uint64_t n, const uint64_t* ro, const uint32_t* ci, const doub
                   int spd_enabled, double spd_raw, double rtol, uint64_t max_iters,
                   double* x_out, double* history_out, double* report_out);
 
+/* frame.cpp:147-152 / csr.cpp:64-68 sequential sums (squares: s = fma(x, x, s)) */
+double orc_seq_sum(const double* x, uint64_t n, int squares);
+
 #ifdef __cplusplus
 }
 #endif

@@ -123,6 +123,12 @@ class Oracle(_Base):
                self.lib, "apply_f64")
         return y
 
+    def seq_sum(self, x, squares: bool) -> float:
+        x = np.ascontiguousarray(x, np.float64)
+        self.lib.orc_seq_sum.restype = C.c_double
+        self.lib.orc_seq_sum.argtypes = [_p, _u64, C.c_int]
+        return float(self.lib.orc_seq_sum(_ptr(x), len(x), int(squares)))
+
     def rng(self, seed, frame, purpose, count):
         class S(C.Structure):
             _fields_ = [("key", _u64), ("counter", _u64)]

@@ -58,7 +58,7 @@ class FrameDeviceC(C.Structure):
     _fields_ = [("n", u64), ("nnz", u64), ("width", u64), ("height", u64), ("depth", u64),
                 ("rho_heavy", dbl), ("cell_order", vp), ("rho", vp), ("row_offsets", vp),
                 ("col_indices", vp), ("values", vp), ("b", vp), ("a_diag", vp),
-                ("generate_ms", C.c_float)]
+                ("generate_ms", C.c_float), ("frobenius", dbl)]
 
 
 class CudaError(RuntimeError):
@@ -83,6 +83,7 @@ _PROTOS = {
     "hfpg_frame_gpu_2d": (C.c_int, [vp, u64, u64, u64]),
     "hfpg_frame_gpu_3d": (C.c_int, [vp, u64, u64, u64, u64, u64]),
     "hfpg_frame_gpu_view": (C.c_int, [vp, C.POINTER(FrameDeviceC)]),
+    "hfpg_seq_sum": (C.c_int, [vp, vp, u64, i32, C.c_int, C.POINTER(dbl)]),
     "hfpg_frame_gpu_copy": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
     "hfpg_frame_free": (None, [vp]),
     "hfpg_host_alloc": (C.c_int, [u64, C.POINTER(vp)]),

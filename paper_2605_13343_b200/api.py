@@ -320,6 +320,7 @@ class GpuFrame:
     b: int
     a_diag: int
     generate_ms: float
+    frobenius: float
     master_seed: int
     frame_index: int
     device: "Device"
@@ -366,7 +367,7 @@ class Device:
         self.csr_id = ("gpu_frame", seed, fidx)
         return GpuFrame(v.n, v.nnz, v.width, v.height, v.depth, v.rho_heavy, v.cell_order or 0,
                         v.rho or 0, v.row_offsets or 0, v.col_indices or 0, v.values or 0, v.b or 0,
-                        v.a_diag or 0, float(v.generate_ms), seed, fidx, self)
+                        v.a_diag or 0, float(v.generate_ms), float(v.frobenius), seed, fidx, self)
 
     def frame_gpu(self, n: int, master_seed: int, frame_index: int) -> GpuFrame:
         """make_frame (frame.cpp:161-181) generated on this device and loaded as its system."""

@@ -34,6 +34,28 @@ static void dalloc(T*& p, size_t count) {
     CK(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
 }
 
+
+// Scratch of one exact sequential sum (per-tile approximate sums, guesses, summaries).
+struct SeqScratch {
+    double* tsum = nullptr;
+    int* guess = nullptr;
+    SeqTile* tiles = nullptr;
+    uint64_t cap = 0;
+    void reserve(uint64_t tiles_max) {
+        if (tiles_max <= cap && tsum) return;
+        dalloc(tsum, tiles_max);
+        dalloc(guess, tiles_max);
+        dalloc(tiles, tiles_max);
+        cap = tiles_max;
+    }
+    void release() {
+        dfree(tsum);
+        dfree(guess);
+        dfree(tiles);
+        cap = 0;
+    }
+};
+
 }  // namespace hfpg
 
 using namespace hfpg;
@@ -131,6 +153,7 @@ struct hfpg_handle {
         cudaStream_t side[2] = {nullptr, nullptr};
         cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
         float gen_ms = 0.f;
+        SeqScratch seq[2];  // the two sequential sums' scratch
     } fr;
 };
 
@@ -608,6 +631,39 @@ void scan_counts(hfpg_handle* h, cudaStream_t st, const uint32_t* in, uint64_t n
     CK(cudaGetLastError());
 }
 
+// One of the reference's sequential sums on `st` (cnt elements, or *cnt_dev when given, at most
+// cnt_max): the exact parallel emulation (framegen.cuh), HFPG_FG_SERIAL=1 the literal one-thread
+// loop, HFPG_FG_NOSUMM=1 the emulation without tile summaries (A/B checks).
+void seq_sum(cudaStream_t st, const double* src, uint64_t cnt, const unsigned long long* cnt_dev,
+             uint64_t cnt_max, bool squares, double* out, SeqScratch& sc) {
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(k_seq_sum<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSeqSmem)));
+        CK(cudaFuncSetAttribute(k_seq_sum<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSeqSmem)));
+        attr = true;
+    }
+    if (std::getenv("HFPG_FG_SERIAL")) {
+        k_fg_chain<<<1, kFgChainThreads, 0, st>>>(src, cnt, cnt_dev, squares ? 1 : 0, out);
+        CK(cudaGetLastError());
+        return;
+    }
+    const uint64_t tiles_max = std::max<uint64_t>(1, (cnt_max + kSeqW - 1) / kSeqW);
+    const bool summ = std::getenv("HFPG_FG_NOSUMM") == nullptr;
+    if (summ) {
+        sc.reserve(tiles_max);
+        const unsigned g = unsigned(tiles_max);
+        if (squares) k_seq_tsum<true><<<g, kSeqSumThreads, 0, st>>>(src, cnt, cnt_dev, sc.tsum);
+        else k_seq_tsum<false><<<g, kSeqSumThreads, 0, st>>>(src, cnt, cnt_dev, sc.tsum);
+        k_seq_guess<<<1, 1024, 0, st>>>(sc.tsum, tiles_max, cnt, cnt_dev, sc.guess);
+        if (squares) k_seq_summ<true><<<g, kSeqSumThreads, 0, st>>>(src, cnt, cnt_dev, sc.guess, sc.tiles);
+        else k_seq_summ<false><<<g, kSeqSumThreads, 0, st>>>(src, cnt, cnt_dev, sc.guess, sc.tiles);
+    }
+    const SeqTile* tl = summ ? sc.tiles : nullptr;
+    if (squares) k_seq_sum<true><<<1, kSeqThreads, kSeqSmem, st>>>(src, cnt, cnt_dev, tl, out);
+    else k_seq_sum<false><<<1, kSeqThreads, kSeqSmem, st>>>(src, cnt, cnt_dev, tl, out);
+    CK(cudaGetLastError());
+}
+
 // make_frame / frame_3d on the GPU, loaded as the handle's system (framegen.cuh).
 void frame_gpu(hfpg_handle* h, const FrameParams& FP) {
     set_device(h);
@@ -681,7 +737,7 @@ void frame_gpu(hfpg_handle* h, const FrameParams& FP) {
     // sum of b on side stream 0 (overlaps assembly and SELL), then b -= mean
     CK(cudaEventRecord(F.ev[0], st));
     CK(cudaStreamWaitEvent(F.side[0], F.ev[0], 0));
-    k_fg_chain<<<1, kFgChainThreads, 0, F.side[0]>>>(F.b, n, nullptr, 0, F.sums);
+    seq_sum(F.side[0], F.b, n, nullptr, n, false, F.sums, F.seq[0]);
     k_fg_center<<<fg_blocks(h, n), 256, 0, F.side[0]>>>(F.b, n, F.sums);
     CK(cudaGetLastError());
     scan_counts(h, st, F.len, n, F.ro);
@@ -691,7 +747,7 @@ void frame_gpu(hfpg_handle* h, const FrameParams& FP) {
     // sum of v^2 on side stream 1
     CK(cudaEventRecord(F.ev[1], st));
     CK(cudaStreamWaitEvent(F.side[1], F.ev[1], 0));
-    k_fg_chain<<<1, kFgChainThreads, 0, F.side[1]>>>(F.vals, 0, F.ro + n, 1, F.sums + 1);
+    seq_sum(F.side[1], F.vals, 0, F.ro + n, nnz_max, true, F.sums + 1, F.seq[1]);
     CK(cudaGetLastError());
     // SELL-32
     k_sell_widths<<<unsigned((ns + 7) / 8), 256, 0, st>>>(F.len, n, ns, F.slice_len);
@@ -796,6 +852,7 @@ int hfpg_destroy(hfpg_handle* h) {
             if (F.tail_host) cudaFreeHost(F.tail_host);
             for (auto& st : F.side) if (st) cudaStreamDestroy(st);
             for (auto& e : F.ev) if (e) cudaEventDestroy(e);
+            for (auto& q : F.seq) q.release();
         }
         reset_partition(h);
         if (h->toynet) toynet_model_destroy(h->toynet);
@@ -853,6 +910,24 @@ int hfpg_frame_gpu_3d(hfpg_handle* h, uint64_t nx, uint64_t ny, uint64_t nz, uin
     return guarded([&] { frame_gpu(h, frame_params_3d(nx, ny, nz, seed, frame_index)); });
 }
 
+int hfpg_seq_sum(hfpg_handle* h, const double* x, uint64_t n, int32_t squares, int where, double* out) {
+    return guarded([&] {
+        set_device(h);
+        double* d = nullptr;
+        dalloc(d, n + 2);  // k_seq_sum may read to the next 16-byte boundary
+        if (n) CK(cudaMemcpyAsync(d, x, n * 8, where == HFPG_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, h->stream));
+        double* r = nullptr;
+        dalloc(r, 1);
+        SeqScratch sc;
+        seq_sum(h->stream, d, n, nullptr, n, squares != 0, r, sc);
+        CK(cudaMemcpyAsync(out, r, 8, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        dfree(d);
+        dfree(r);
+        sc.release();
+    });
+}
+
 int hfpg_frame_gpu_view(hfpg_handle* h, hfpg_frame_device* out) {
     return guarded([&] {
         const auto& F = h->fr;
@@ -871,6 +946,7 @@ int hfpg_frame_gpu_view(hfpg_handle* h, hfpg_frame_device* out) {
         out->b = F.b;
         out->a_diag = h->a_diag;
         out->generate_ms = F.gen_ms;
+        out->frobenius = h->fro;
     });
 }
 

@@ -47,7 +47,7 @@ def arrays(f):
 
 
 @pytest.mark.parametrize("spec", CASES_2D + CASES_3D, ids=str)
-def test_bit_identical_to_crmath_host(H, spec):
+def test_bit_identical_to_crmath_host(H, oracle, spec):
     dev = H.Device(0)
     for seed, fidx in [(0, 1), (2024, (3 << 24) | 17)]:
         g = gpu_frame(dev, spec, seed, fidx)
@@ -55,6 +55,8 @@ def test_bit_identical_to_crmath_host(H, spec):
         assert (g.n, g.width, g.height, g.depth) == (h.n, h.width, h.height, h.depth)
         assert g.rho_heavy == h.rho_heavy
         got = arrays(g.to_host())
+        # |A|_F from the sequential fused sum of squares (csr.cpp:64-68), bit for bit
+        assert g.frobenius == np.sqrt(oracle.seq_sum(h.A.values, True))
         for k, want in arrays(h).items():
             assert got[k].dtype == want.dtype and got[k].shape == want.shape, k
             bad = np.flatnonzero(got[k] != want)
@@ -110,9 +112,9 @@ def test_regenerate_on_one_handle(H):
     import torch
     from paper_2605_13343_b200 import _native as N
     dev = H.Device(0)
-    dev.set_precond(1)  # Jacobi: no factors needed
     for n, fidx in [(65536, 0), (4096, 1), (65536, 2), (1 << 18, 3), (65536, 0)]:
         g = dev.frame_gpu(n, 3, fidx)
+        dev.set_precond(1)  # Jacobi: no factors needed
         x = torch.empty(n, dtype=torch.float64, device="cuda")
         rep = dev.solve_ptr(g.b, x.data_ptr(), H.SolveConfig(), None, N.DEVICE)
         h = host_frame(H, n, 3, fidx, True)
@@ -130,3 +132,42 @@ def test_errors(H):
     from paper_2605_13343_b200 import _native as N
     with pytest.raises(ValueError):
         N.check(N.lib.hfpg_frame_gpu_view(H.Device(0).h, None))
+
+
+def _seq_inputs():
+    g = np.random.default_rng(42)
+    yield "normals", g.standard_normal(1 << 20), False
+    yield "normals_odd_len", g.standard_normal((1 << 16) + 4097), False
+    yield "drift", g.standard_normal(300000) + 0.01, False
+    yield "halves_ties", g.integers(-50, 50, 200000) / 2.0, False
+    yield "mixed_scales", g.standard_normal(100000) * 10.0 ** g.integers(-12, 12, 100000), False
+    yield "cancel", np.repeat([1e16, 1.0, -1e16], 20000), False
+    yield "zeros_tiny", np.where(g.random(50000) < 0.5, 0.0, 1e-310), False
+    yield "overflow", np.full(10000, 1e305), False
+    yield "weights_sq", g.random(5 << 20) * 200.0 + 0.1, True
+    yield "ints_sq_ties", g.integers(1, 64, 300000).astype(np.float64) * 2.0 ** -20, True
+    yield "mixed_sq", g.standard_normal(200000) * 10.0 ** g.integers(-6, 6, 200000), True
+    for n in (0, 1, 5, 4095, 4096, 4097, 8193):
+        yield f"len{n}", g.standard_normal(n), False
+        yield f"len{n}_sq", g.standard_normal(n), True
+
+
+@pytest.mark.parametrize("mode", ["summaries", "HFPG_FG_NOSUMM", "HFPG_FG_SERIAL"])
+@pytest.mark.parametrize("name,x,squares", list(_seq_inputs()), ids=lambda v: v if isinstance(v, str) else "")
+def test_seq_sum_bit_identical_to_serial(H, oracle, name, x, squares, mode):
+    """hfpg_seq_sum (the generator's exact parallel emulation of a sequential sum: tile summaries
+    + detailed scans; detailed scans only; the literal loop) equals the one-thread loop bit for
+    bit — including ties, binade crossings, sign changes and overflow."""
+    import ctypes as C
+    from paper_2605_13343_b200 import _native as N
+    dev = H.Device(0)
+    x = np.ascontiguousarray(x, np.float64)
+    out = C.c_double()
+    if mode != "summaries":
+        os.environ[mode] = "1"
+    try:
+        N.check(N.lib.hfpg_seq_sum(dev.h, x.ctypes.data, len(x), int(squares), N.HOST, C.byref(out)))
+    finally:
+        os.environ.pop(mode, None)
+    want = oracle.seq_sum(x, squares)
+    assert np.array_equal(np.float64(out.value), np.float64(want), equal_nan=True), (out.value, want)
