@@ -281,6 +281,12 @@ int hfpg_pcg_solve_wait(hfpg_handle* h, double* history, hfpg_report* report, in
 int hfpg_toynet_forward(hfpg_handle* h, const hfpg_frame_view* frame, uint64_t leaf_size,
                         uint64_t coarse_size, const hfpg_toynet_config* cfg, uint64_t weight_seed,
                         float* out, int32_t load, hfpg_toynet_trace* trace);
+/* The same forward from the handle's GPU frame (hfpg_frame_gpu_2d): inputs stay on the device,
+ * the global statistics (toy_net.cpp:232-268) are reduced on the device. With load, the factors
+ * go straight into the handle: generate -> infer -> solve without a host round trip. */
+int hfpg_toynet_forward_gpu_frame(hfpg_handle* h, uint64_t leaf_size, uint64_t coarse_size,
+                                  const hfpg_toynet_config* cfg, uint64_t weight_seed, float* out,
+                                  int32_t load, hfpg_toynet_trace* trace);
 
 /* ---- introspection for tests / bench ---------------------------------------------------- */
 /* Number of kernels one PCG iteration launches, and one apply. */

@@ -9,7 +9,7 @@ from .api import (Checkpoint, CsrMatrix, Device, FactorInit, FactorLayout, Facto
                   SolveStatus, TileSpec, ToynetConfig, ToynetTrace, apply, build_partition, clamp_leaf_size, factor_applier,
                   identity_applier, init_factors, jacobi_applier, make_factor_layout, make_frame,
                   make_frame_3d, packed_width, pcg_solve, read_checkpoint, test_frame_id,
-                  toynet_forward, train_frame_id, write_checkpoint)
+                  toynet_forward, toynet_forward_gpu_frame, train_frame_id, write_checkpoint)
 
 from .partition import PartitionGroup, RankSolver  # noqa: E402
 

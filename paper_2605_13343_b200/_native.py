@@ -125,6 +125,8 @@ _PROTOS = {
     "hfpg_gemm_tf32": (C.c_int, [u64, u64, u64, vp, vp, vp]),
     "hfpg_toynet_forward": (C.c_int, [vp, C.POINTER(FrameViewC), u64, u64, C.POINTER(ToynetConfigC),
                                       u64, vp, i32, C.POINTER(ToynetTraceC)]),
+    "hfpg_toynet_forward_gpu_frame": (C.c_int, [vp, u64, u64, C.POINTER(ToynetConfigC), u64, vp, i32,
+                                                vp]),
 }
 
 EXPORTED = sorted(_PROTOS)

@@ -635,6 +635,32 @@ def toynet_forward(frame: Frame, partition: HPartition, coarse_size: int,
     return FactorTensor(lay, out)
 
 
+def toynet_forward_gpu_frame(frame: "GpuFrame", coarse_size: int, cfg: ToynetConfig | None = None,
+                             weight_seed: int = 0, trace: ToynetTrace | None = None,
+                             leaf_size: int = 128, load: bool = True,
+                             copy_out: bool = False) -> FactorTensor | None:
+    """toynet forward from a GPU frame (Device.frame_gpu): inputs never leave the device. With
+    load=True the factors become the frame's device's factor tensor (generate -> infer -> solve
+    on the GPU); copy_out=True also returns them as a host FactorTensor."""
+    cfg = cfg or ToynetConfig()
+    if frame.depth != 1:
+        raise ValueError("toynet: 2D frames only (frame.hpp)")
+    lay = make_factor_layout(build_partition(frame.n, leaf_size), coarse_size)
+    out = np.empty(lay.total, np.float32) if copy_out else None
+    c = N.ToynetConfigC(cfg.d, cfg.layers, cfg.heads, cfg.gcn_layers, cfg.d_global, cfg.edge_hidden)
+    tr = N.ToynetTraceC()
+    check(lib.hfpg_toynet_forward_gpu_frame(frame.device.h, leaf_size, coarse_size, C.byref(c), weight_seed,
+                                            out.ctypes.data if copy_out else None, int(load),
+                                            C.byref(tr) if trace is not None else None))
+    if trace is not None:
+        trace.max_attention_row_sum_error = tr.max_attention_row_sum_error
+        trace.highway_max_deviation = tr.highway_max_deviation
+        trace.leaf_attention_dispatches = tr.leaf_attention_dispatches
+        trace.tile_attention_dispatches = tr.tile_attention_dispatches
+        trace.ms = tr.ms
+    return FactorTensor(lay, out) if copy_out else None
+
+
 # -------------------------------------------------------------------------------- apply.hpp
 
 

@@ -1233,49 +1233,77 @@ int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out) {
     });
 }
 
+}  // extern "C"
+
+namespace {
+// toynet forward of an n-node frame into a fresh buffer (out != NULL: copied to the host) or,
+// with load, straight into the handle's factor tensor. `run(dst)` launches the forward.
+template <class Run>
+void toynet_into(hfpg_handle* h, uint64_t n, uint64_t leaf, uint64_t ls, const hfpg_toynet_config& cfg,
+                 uint64_t seed, float* out, int32_t load, Run&& run) {
+    set_device(h);
+    const Layout L = make_layout(n, leaf, ls);
+    float* dst = nullptr;
+    if (load) {
+        if (h->have_csr && h->n != n) throw InvalidArgument("toynet: length mismatch");
+        invalidate_graph(h);
+        if (!h->have_factors || h->L.total != L.total) dalloc(h->F, L.total);
+        dst = h->F;
+    } else {
+        CK(cudaMalloc(&dst, L.total * 4));
+    }
+    CK(cudaMemsetAsync(dst, 0, L.total * 4, h->stream));
+    try {
+        if (!toynet_model_matches(h->toynet, cfg, leaf, ls, seed)) {
+            if (h->toynet) toynet_model_destroy(h->toynet);
+            h->toynet = nullptr;
+            h->toynet = toynet_model_create(cfg, leaf, ls, seed);
+        }
+        run(dst);
+        if (out) CK(cudaMemcpy(out, dst, L.total * 4, cudaMemcpyDeviceToHost));
+    } catch (...) {
+        if (!load) cudaFree(dst);
+        throw;
+    }
+    if (!load) {
+        CK(cudaFree(dst));
+        return;
+    }
+    h->L = L;
+    h->have_factors = true;
+    h->spd_enabled = 0;
+    h->spd_raw = 0.0;
+    h->fast = (L.l == kL && L.ls == kLs && std::getenv("HFPG_FORCE_GENERIC") == nullptr);
+    if (!h->have_csr && !h->have_diag) h->n = n;
+    ensure_workspace(h);
+    const double shift = 0.0;
+    CK(cudaMemcpyAsync(&h->sc->shift, &shift, 8, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+}
+}  // namespace
+
+extern "C" {
+
 int hfpg_toynet_forward(hfpg_handle* h, const hfpg_frame_view* frame, uint64_t leaf, uint64_t ls,
                         const hfpg_toynet_config* cfg, uint64_t seed, float* out, int32_t load,
                         hfpg_toynet_trace* trace) {
     return guarded([&] {
-        set_device(h);
         if (!frame || !cfg) throw InvalidArgument("toynet: null frame or config");
-        const Layout L = make_layout(frame->n, leaf, ls);
-        float* dst = nullptr;
-        if (load) {
-            if (h->have_csr && h->n != frame->n) throw InvalidArgument("toynet: length mismatch");
-            invalidate_graph(h);
-            if (!h->have_factors || h->L.total != L.total) dalloc(h->F, L.total);
-            dst = h->F;
-        } else {
-            CK(cudaMalloc(&dst, L.total * 4));
-        }
-        CK(cudaMemsetAsync(dst, 0, L.total * 4, h->stream));
-        try {
-            if (!toynet_model_matches(h->toynet, *cfg, leaf, ls, seed)) {
-                if (h->toynet) toynet_model_destroy(h->toynet);
-                h->toynet = nullptr;
-                h->toynet = toynet_model_create(*cfg, leaf, ls, seed);
-            }
-            toynet_forward_device(h->toynet, h->stream, *frame, dst, trace);
-            if (out) CK(cudaMemcpy(out, dst, L.total * 4, cudaMemcpyDeviceToHost));
-        } catch (...) {
-            if (!load) cudaFree(dst);
-            throw;
-        }
-        if (!load) {
-            CK(cudaFree(dst));
-            return;
-        }
-        h->L = L;
-        h->have_factors = true;
-        h->spd_enabled = 0;
-        h->spd_raw = 0.0;
-        h->fast = (L.l == kL && L.ls == kLs && std::getenv("HFPG_FORCE_GENERIC") == nullptr);
-        if (!h->have_csr && !h->have_diag) h->n = frame->n;
-        ensure_workspace(h);
-        const double shift = 0.0;
-        CK(cudaMemcpyAsync(&h->sc->shift, &shift, 8, cudaMemcpyHostToDevice, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        toynet_into(h, frame->n, leaf, ls, *cfg, seed, out, load,
+                    [&](float* dst) { toynet_forward_device(h->toynet, h->stream, *frame, dst, trace); });
+    });
+}
+
+int hfpg_toynet_forward_gpu_frame(hfpg_handle* h, uint64_t leaf, uint64_t ls, const hfpg_toynet_config* cfg,
+                                  uint64_t seed, float* out, int32_t load, hfpg_toynet_trace* trace) {
+    return guarded([&] {
+        if (!cfg) throw InvalidArgument("toynet: null config");
+        const auto& F = h->fr;
+        if (!F.valid) throw InvalidArgument("toynet: no GPU frame generated on this handle");
+        if (F.P.dims != 2) throw InvalidArgument("toynet: 2D frames only (frame.hpp)");
+        const ToynetDeviceFrame df{F.P.n, F.P.W, F.P.H, F.nnz, F.P.rho_heavy, F.order, F.rho, F.ro, F.ci, F.vals, h->a_diag};
+        toynet_into(h, F.P.n, leaf, ls, *cfg, seed, out, load,
+                    [&](float* dst) { toynet_forward_device_frame(h->toynet, h->stream, df, dst, trace); });
     });
 }
 

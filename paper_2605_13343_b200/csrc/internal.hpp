@@ -134,6 +134,19 @@ bool toynet_model_matches(const ToynetModel* m, const hfpg_toynet_config& cfg, u
                           uint64_t seed);
 void toynet_forward_device(ToynetModel* m, cudaStream_t st, const hfpg_frame_view& fr, float* out,
                            hfpg_toynet_trace* trace);
+// A frame resident on the device (the GPU frame generator's arrays).
+struct ToynetDeviceFrame {
+    uint64_t n, width, height, nnz;
+    double rho_heavy;
+    const uint32_t* order;
+    const double* rho;
+    const unsigned long long* ro;
+    const uint32_t* ci;
+    const double* v;
+    const double* diag;
+};
+void toynet_forward_device_frame(ToynetModel* m, cudaStream_t st, const ToynetDeviceFrame& f, float* out,
+                                 hfpg_toynet_trace* trace);
 
 }  // namespace hfpg
 

@@ -379,46 +379,16 @@ bool toynet_model_matches(const ToynetModel* m, const hfpg_toynet_config& c, uin
            m->cfg.d_global == c.d_global && m->cfg.edge_hidden == c.edge_hidden;
 }
 
-// Full forward for one frame: writes the packed factor tensor (device pointer out).
-void toynet_forward_device(ToynetModel* mdl, cudaStream_t st, const hfpg_frame_view& fr, float* out,
-                           hfpg_toynet_trace* trace) {
+// The forward proper, from device-resident inputs (the frame's order / rho / CSR / diagonal
+// and the global feature vector).
+static void toynet_run(ToynetModel* mdl, cudaStream_t st, uint64_t n, uint64_t width, uint64_t height,
+                       uint64_t nnz, const uint32_t* d_order, const double* d_rho,
+                       const unsigned long long* d_ro, const uint32_t* d_ci, const double* d_v,
+                       const double* d_diag, const float* d_glob, float* out, hfpg_toynet_trace* trace) {
     const hfpg_toynet_config& cfg = mdl->cfg;
     const uint64_t L = mdl->L, Ls = mdl->Ls;
-    const auto t0 = std::chrono::steady_clock::now();
-    const Layout lay = make_layout(fr.n, L, Ls);
-    const uint64_t n = fr.n, d = cfg.d;
-
-    // ---- glob stats on the host, f64 in the reference's order (toy_net.cpp:232-268) --------
-    std::vector<double> diag(n, 0.0);
-    double rho_mean = 0.0, rho_var = 0.0, dmean = 0.0, offmean = 0.0;
-    uint64_t off = 0;
-    for (uint64_t i = 0; i < n; ++i)
-        for (uint64_t p = fr.row_offsets[i]; p < fr.row_offsets[i + 1]; ++p)
-            if (fr.col_indices[p] == i) diag[i] = fr.values[p];
-    for (uint64_t i = 0; i < n; ++i) rho_mean += fr.rho[i];
-    rho_mean /= double(n);
-    for (uint64_t i = 0; i < n; ++i) rho_var += (fr.rho[i] - rho_mean) * (fr.rho[i] - rho_mean);
-    rho_var /= double(n);
-    double dmin = diag[0], dmax = diag[0];
-    for (uint64_t i = 0; i < n; ++i) {
-        dmean += diag[i];
-        dmin = std::min(dmin, diag[i]);
-        dmax = std::max(dmax, diag[i]);
-        for (uint64_t p = fr.row_offsets[i]; p < fr.row_offsets[i + 1]; ++p)
-            if (fr.col_indices[p] != i) {
-                offmean += std::fabs(fr.values[p]);
-                ++off;
-            }
-    }
-    dmean /= double(n);
-    if (off) offmean /= double(off);
-    const double stats[12] = {std::log(double(n)), rho_mean, std::sqrt(rho_var),
-                              std::log(std::max(fr.rho_heavy, 1.0)), dmean, dmax, dmin, offmean,
-                              double(fr.row_offsets[n]) / double(n),
-                              double(fr.width) / double(fr.height), dmax / std::max(dmin, 1e-30), 1.0};
-    std::vector<float> glob(std::max<uint64_t>(cfg.d_global, 1), 0.f);
-    for (uint64_t i = 0; i < cfg.d_global && i < 12; ++i) glob[i] = float(stats[i]);
-
+    const Layout lay = make_layout(n, L, Ls);
+    const uint64_t d = cfg.d;
     TnDims g{};
     g.n = n;
     g.L = L;
@@ -427,30 +397,15 @@ void toynet_forward_device(ToynetModel* mdl, cudaStream_t st, const hfpg_frame_v
     g.K = lay.k;
     g.M = lay.m;
     g.D = lay.depth;
-    g.width = uint32_t(fr.width);
-    g.height = uint32_t(fr.height);
+    g.width = uint32_t(width);
+    g.height = uint32_t(height);
     g.d = uint32_t(d);
     g.heads = uint32_t(cfg.heads);
     g.dglob = uint32_t(cfg.d_global);
     g.eh = uint32_t(cfg.edge_hidden);
     g.feat_pad = 32;
-    const uint64_t nnz = fr.row_offsets[n], MT = lay.m * Ls;  // tile tokens
-
-    // ---- inputs ------------------------------------------------------------------------------
-    auto* d_order = mdl->buf<uint32_t>(21, n);
-    auto* d_rho = mdl->buf<double>(0, n);
-    auto* d_ro = mdl->buf<unsigned long long>(1, n + 1);
-    auto* d_ci = mdl->buf<uint32_t>(22, nnz);
-    auto* d_v = mdl->buf<double>(2, nnz);
-    auto* d_diag = mdl->buf<double>(3, n);
-    auto* d_glob = mdl->buf<float>(4, glob.size());
-    TCK(cudaMemcpyAsync(d_order, fr.cell_order, n * 4, cudaMemcpyHostToDevice, st));
-    TCK(cudaMemcpyAsync(d_rho, fr.rho, n * 8, cudaMemcpyHostToDevice, st));
-    TCK(cudaMemcpyAsync(d_ro, fr.row_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, st));
-    TCK(cudaMemcpyAsync(d_ci, fr.col_indices, nnz * 4, cudaMemcpyHostToDevice, st));
-    TCK(cudaMemcpyAsync(d_v, fr.values, nnz * 8, cudaMemcpyHostToDevice, st));
-    TCK(cudaMemcpyAsync(d_diag, diag.data(), n * 8, cudaMemcpyHostToDevice, st));
-    TCK(cudaMemcpyAsync(d_glob, glob.data(), glob.size() * 4, cudaMemcpyHostToDevice, st));
+    const uint64_t MT = lay.m * Ls;  // tile tokens
+    (void)nnz;
 
     const auto& wl = mdl->wl;
     const auto& wt = mdl->wt;
@@ -592,8 +547,83 @@ void toynet_forward_device(ToynetModel* mdl, cudaStream_t st, const hfpg_frame_v
         float dev_ms = 0.f;
         TCK(cudaEventElapsedTime(&dev_ms, mdl->ev0, mdl->ev1));
         trace->ms = dev_ms;  // device time of the forward (all kernels, excl. host setup)
-        (void)t0;
     }
+}
+
+// Full forward for one frame: writes the packed factor tensor (device pointer out).
+void toynet_forward_device(ToynetModel* mdl, cudaStream_t st, const hfpg_frame_view& fr, float* out,
+                           hfpg_toynet_trace* trace) {
+    const hfpg_toynet_config& cfg = mdl->cfg;
+    const uint64_t L = mdl->L, Ls = mdl->Ls;
+    const Layout lay = make_layout(fr.n, L, Ls);
+    const uint64_t n = fr.n, d = cfg.d;
+
+    // ---- glob stats on the host, f64 in the reference's order (toy_net.cpp:232-268) --------
+    std::vector<double> diag(n, 0.0);
+    double rho_mean = 0.0, rho_var = 0.0, dmean = 0.0, offmean = 0.0;
+    uint64_t off = 0;
+    for (uint64_t i = 0; i < n; ++i)
+        for (uint64_t p = fr.row_offsets[i]; p < fr.row_offsets[i + 1]; ++p)
+            if (fr.col_indices[p] == i) diag[i] = fr.values[p];
+    for (uint64_t i = 0; i < n; ++i) rho_mean += fr.rho[i];
+    rho_mean /= double(n);
+    for (uint64_t i = 0; i < n; ++i) rho_var += (fr.rho[i] - rho_mean) * (fr.rho[i] - rho_mean);
+    rho_var /= double(n);
+    double dmin = diag[0], dmax = diag[0];
+    for (uint64_t i = 0; i < n; ++i) {
+        dmean += diag[i];
+        dmin = std::min(dmin, diag[i]);
+        dmax = std::max(dmax, diag[i]);
+        for (uint64_t p = fr.row_offsets[i]; p < fr.row_offsets[i + 1]; ++p)
+            if (fr.col_indices[p] != i) {
+                offmean += std::fabs(fr.values[p]);
+                ++off;
+            }
+    }
+    dmean /= double(n);
+    if (off) offmean /= double(off);
+    const double stats[12] = {std::log(double(n)), rho_mean, std::sqrt(rho_var),
+                              std::log(std::max(fr.rho_heavy, 1.0)), dmean, dmax, dmin, offmean,
+                              double(fr.row_offsets[n]) / double(n),
+                              double(fr.width) / double(fr.height), dmax / std::max(dmin, 1e-30), 1.0};
+    std::vector<float> glob(std::max<uint64_t>(cfg.d_global, 1), 0.f);
+    for (uint64_t i = 0; i < cfg.d_global && i < 12; ++i) glob[i] = float(stats[i]);
+
+    // ---- inputs ------------------------------------------------------------------------------
+    const uint64_t nnz = fr.row_offsets[n];
+    auto* d_order = mdl->buf<uint32_t>(21, n);
+    auto* d_rho = mdl->buf<double>(0, n);
+    auto* d_ro = mdl->buf<unsigned long long>(1, n + 1);
+    auto* d_ci = mdl->buf<uint32_t>(22, nnz);
+    auto* d_v = mdl->buf<double>(2, nnz);
+    auto* d_diag = mdl->buf<double>(3, n);
+    auto* d_glob = mdl->buf<float>(4, glob.size());
+    TCK(cudaMemcpyAsync(d_order, fr.cell_order, n * 4, cudaMemcpyHostToDevice, st));
+    TCK(cudaMemcpyAsync(d_rho, fr.rho, n * 8, cudaMemcpyHostToDevice, st));
+    TCK(cudaMemcpyAsync(d_ro, fr.row_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+    TCK(cudaMemcpyAsync(d_ci, fr.col_indices, nnz * 4, cudaMemcpyHostToDevice, st));
+    TCK(cudaMemcpyAsync(d_v, fr.values, nnz * 8, cudaMemcpyHostToDevice, st));
+    TCK(cudaMemcpyAsync(d_diag, diag.data(), n * 8, cudaMemcpyHostToDevice, st));
+    TCK(cudaMemcpyAsync(d_glob, glob.data(), glob.size() * 4, cudaMemcpyHostToDevice, st));
+
+    toynet_run(mdl, st, n, fr.width, fr.height, nnz, d_order, d_rho, d_ro, d_ci, d_v, d_diag, d_glob, out, trace);
+}
+
+// The same forward from a frame already on the device (the GPU frame generator): the global
+// statistics (toy_net.cpp:232-268) are reduced on the device (k_tn_frame_stats, fixed-order
+// partial sums — float features, so the order does not matter at the 1e-5 parity bar).
+void toynet_forward_device_frame(ToynetModel* mdl, cudaStream_t st, const ToynetDeviceFrame& f, float* out,
+                                 hfpg_toynet_trace* trace) {
+    const hfpg_toynet_config& cfg = mdl->cfg;
+    const uint64_t nglob = std::max<uint64_t>(cfg.d_global, 1);
+    auto* d_glob = mdl->buf<float>(4, nglob);
+    auto* part = mdl->buf<double>(27, uint64_t(kStatParts) * kStatFields);
+    k_tn_frame_stats<<<kStatParts, 256, 0, st>>>(f.n, f.rho, f.ro, f.ci, f.v, f.diag, part);
+    k_tn_frame_var<<<kStatParts, 256, 0, st>>>(f.n, f.rho, part);
+    k_tn_frame_finish<<<1, 32, 0, st>>>(f.n, f.nnz, f.width, f.height, f.rho_heavy, part,
+                                        uint32_t(cfg.d_global), d_glob);
+    TCK(cudaGetLastError());
+    toynet_run(mdl, st, f.n, f.width, f.height, f.nnz, f.order, f.rho, f.ro, f.ci, f.v, f.diag, d_glob, out, trace);
 }
 
 }  // namespace hfpg

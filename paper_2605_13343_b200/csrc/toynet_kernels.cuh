@@ -417,4 +417,86 @@ __global__ void k_tn_ffn_input_tile(TnDims g, const float* row_hw, const float* 
     }
 }
 
+// ---- global statistics of a device frame (toy_net.cpp:232-268) --------------------------
+// Fixed partition into kStatParts blocks, fixed-order combination: deterministic.
+constexpr int kStatParts = 296, kStatFields = 7;  // rho sum, diag sum/min/max, |offdiag| sum/count, rho sq dev
+__device__ __forceinline__ double block_reduce_d(double v, int op, double* sh) {  // op 0 sum, 1 min, 2 max
+    for (int o = 16; o; o >>= 1) {
+        const double t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = op == 0 ? v + t : (op == 1 ? fmin(v, t) : fmax(v, t));
+    }
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double r = sh[0];
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) r = op == 0 ? r + sh[w] : (op == 1 ? fmin(r, sh[w]) : fmax(r, sh[w]));
+    __syncthreads();
+    return r;
+}
+__global__ void __launch_bounds__(256) k_tn_frame_stats(uint64_t n, const double* __restrict__ rho,
+                                                        const unsigned long long* __restrict__ ro,
+                                                        const uint32_t* __restrict__ ci, const double* __restrict__ v,
+                                                        const double* __restrict__ diag, double* __restrict__ part) {
+    __shared__ double sh[8];
+    const uint64_t per = (n + kStatParts - 1) / kStatParts, r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+    double rs = 0.0, ds = 0.0, dmn = INFINITY, dmx = -INFINITY, os = 0.0, oc = 0.0;
+    for (uint64_t i = r0 + threadIdx.x; i < r1; i += 256) {
+        rs += rho[i];
+        const double dd = diag[i];
+        ds += dd;
+        dmn = fmin(dmn, dd);
+        dmx = fmax(dmx, dd);
+        for (unsigned long long p = ro[i]; p < ro[i + 1]; ++p)
+            if (ci[p] != i) {
+                os += fabs(v[p]);
+                oc += 1.0;
+            }
+    }
+    double* o = part + uint64_t(blockIdx.x) * kStatFields;
+    rs = block_reduce_d(rs, 0, sh);
+    ds = block_reduce_d(ds, 0, sh);
+    dmn = block_reduce_d(dmn, 1, sh);
+    dmx = block_reduce_d(dmx, 2, sh);
+    os = block_reduce_d(os, 0, sh);
+    oc = block_reduce_d(oc, 0, sh);
+    if (threadIdx.x == 0) {
+        o[0] = rs;
+        o[1] = ds;
+        o[2] = dmn;
+        o[3] = dmx;
+        o[4] = os;
+        o[5] = oc;
+    }
+}
+__global__ void __launch_bounds__(256) k_tn_frame_var(uint64_t n, const double* __restrict__ rho, double* __restrict__ part) {
+    __shared__ double sh[8];
+    double tot = 0.0;  // every block recombines the rho partial sums in the same order
+    for (int b = 0; b < kStatParts; ++b) tot += part[uint64_t(b) * kStatFields];
+    const double mean = tot / double(n);
+    const uint64_t per = (n + kStatParts - 1) / kStatParts, r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+    double q = 0.0;
+    for (uint64_t i = r0 + threadIdx.x; i < r1; i += 256) q += (rho[i] - mean) * (rho[i] - mean);
+    q = block_reduce_d(q, 0, sh);
+    if (threadIdx.x == 0) part[uint64_t(blockIdx.x) * kStatFields + 6] = q;
+}
+__global__ void k_tn_frame_finish(uint64_t n, uint64_t nnz, uint64_t width, uint64_t height, double rho_heavy,
+                                  const double* __restrict__ part, uint32_t dglob, float* __restrict__ glob) {
+    if (threadIdx.x != 0) return;
+    double a[kStatFields] = {0, 0, INFINITY, -INFINITY, 0, 0, 0};
+    for (int b = 0; b < kStatParts; ++b) {
+        const double* o = part + uint64_t(b) * kStatFields;
+        a[0] += o[0];
+        a[1] += o[1];
+        a[2] = fmin(a[2], o[2]);
+        a[3] = fmax(a[3], o[3]);
+        a[4] += o[4];
+        a[5] += o[5];
+        a[6] += o[6];
+    }
+    const double dn = double(n);
+    const double stats[12] = {log(dn), a[0] / dn, sqrt(a[6] / dn), log(fmax(rho_heavy, 1.0)), a[1] / dn, a[3], a[2],
+                              a[5] > 0.0 ? a[4] / a[5] : 0.0, double(nnz) / dn, double(width) / double(height),
+                              a[3] / fmax(a[2], 1e-30), 1.0};
+    for (uint32_t i = 0; i < (dglob > 0 ? dglob : 1u); ++i) glob[i] = i < 12 && i < dglob ? float(stats[i]) : 0.f;
+}
+
 }  // namespace hfpg

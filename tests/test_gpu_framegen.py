@@ -171,3 +171,45 @@ def test_seq_sum_bit_identical_to_serial(H, oracle, name, x, squares, mode):
         os.environ.pop(mode, None)
     want = oracle.seq_sum(x, squares)
     assert np.array_equal(np.float64(out.value), np.float64(want), equal_nan=True), (out.value, want)
+
+
+@pytest.mark.parametrize("n", [1024, 4096, 65536])
+def test_toynet_from_gpu_frame_matches_host_path(H, n):
+    """toynet_forward_gpu_frame (inputs on the device, global statistics reduced there) equals
+    the host-frame forward (tests/test_gpu_toynet.py pins that one to the reference) on the same
+    frame: the CR-math host frame is bit-identical to the GPU frame, so only the order of the
+    f64 statistic sums differs before their rounding to f32 features."""
+    from conftest import rel_l2
+    dev = H.Device(0)
+    g = dev.frame_gpu(n, 2024, 0)
+    h = host_frame(H, n, 2024, 0, True)
+    p = H.build_partition(n, 128)
+    want = H.toynet_forward(h, p, 32, weight_seed=0)
+    tr = H.ToynetTrace()
+    got = H.toynet_forward_gpu_frame(g, 32, weight_seed=0, trace=tr, load=False, copy_out=True)
+    assert got.data.shape == want.data.shape
+    assert np.isfinite(got.data).all()
+    assert rel_l2(got.data.astype(np.float64), want.data.astype(np.float64)) <= 1e-5
+    assert tr.attention_kernel_families() == 2 and tr.max_attention_row_sum_error <= 1e-5
+
+
+def test_generate_infer_solve_on_device(H):
+    """frame -> toynet factors -> PCG without a host round trip (the handle owns all three);
+    the seeded-weight tensor is the reference's non-convergent preconditioner (SURVEY.md §0
+    fact 2), so the pipeline must report max_iters exactly as the host-input path does."""
+    import torch
+    from paper_2605_13343_b200 import _native as N
+    n = 8192
+    dev = H.Device(0)
+    g = dev.frame_gpu(n, 2024, 0)
+    H.toynet_forward_gpu_frame(g, 32, load=True)
+    dev.set_precond(2)
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    rep = dev.solve_ptr(g.b, x.data_ptr(), H.SolveConfig(max_iters=2000), None, N.DEVICE)
+    assert rep.status == 1 and rep.iterations == 2000
+    # and with init_factors instead of the network: converges like the host-loaded system
+    f = H.init_factors(H.build_partition(n, 128), 32, H.FactorInit.jacobi_seed, 1e-2,
+                       H.RngStream(2024, 0, H.RngPurpose.factor_init))
+    dev.load_factors(f)
+    rep = dev.solve_ptr(g.b, x.data_ptr(), H.SolveConfig(), None, N.DEVICE)
+    assert rep.converged
