@@ -46,6 +46,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
+// Arrival counters with release / acquire semantics at GPU scope (no SC fence: MEMBAR.SC.GPU
+// waits for the issuing warp's in-flight memory operations, TMA bulk copies included).
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -142,15 +152,13 @@ __device__ bool grid_reduce_last(double (&v)[NV], double* partials, unsigned* co
             s = warp_sum(s);
             if (lane == 0) partials[blockIdx.x * NV + i] = s;
         }
-        if (lane == 0) {
-            __threadfence();
-            const unsigned t = atomicAdd(counter, 1u);
+        if (lane == 0) {  // release this CTA's partial, acquire the others' (acq_rel, no SC fence)
+            const unsigned t = atom_add_acq_rel_gpu(counter, 1u);
             is_last = (t == gridDim.x - 1);
         }
     }
     __syncthreads();
     if (!is_last) return false;
-    __threadfence();
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
         double s = 0.0;

@@ -176,19 +176,21 @@ uint64_t prolong_grid(const hfpg_handle* h) {
     return h->fast ? std::min<uint64_t>((h->L.k + kProlWarps - 1) / kProlWarps, uint64_t(h->num_sms) * 2)
                    : h->L.k;
 }
+size_t spmv_smem(const hfpg_handle* h) {
+    return h->spmv_stage_bytes ? 128 + size_t(h->spmv_stage_bytes + kSpmvHdr) * kSpmvStages : 0;
+}
 uint64_t spmv_grid(const hfpg_handle* h) {
     if (h->spmv_stage_bytes) {
-        const uint64_t per_sm = std::max<uint64_t>(1, (227 * 1024) / (h->spmv_stage_bytes * kSpmvStages + 128 + 1024));
+        const uint64_t per_sm = std::max<uint64_t>(1, (227 * 1024) / (spmv_smem(h) + 1024));
         const uint64_t nch = ((h->n + 31) / 32 + 7) / 8;
         return std::max<uint64_t>(1, std::min<uint64_t>(nch, uint64_t(h->num_sms) * std::min<uint64_t>(per_sm, 4)));
     }
     return std::max<uint64_t>(1, std::min<uint64_t>((h->n + 255) / 256, uint64_t(h->num_sms) * 4));
 }
-size_t spmv_smem(const hfpg_handle* h) { return h->spmv_stage_bytes ? 128 + size_t(h->spmv_stage_bytes) * kSpmvStages : 0; }
 template <int MODE>
 void launch_spmv(hfpg_handle* h, const DevSys& s, const double* x, double* y) {
     if (h->spmv_stage_bytes)
-        k_spmv_tma<MODE><<<unsigned(spmv_grid(h)), 256, spmv_smem(h), h->lstream>>>(s, x, y);
+        k_spmv_tma<MODE><<<unsigned(spmv_grid(h)), kSpmvThreads, spmv_smem(h), h->lstream>>>(s, x, y);
     else
         k_spmv<MODE><<<unsigned(spmv_grid(h)), 256, 0, h->lstream>>>(s, x, y);
 }
@@ -529,7 +531,7 @@ void upload_csr(hfpg_handle* h, uint64_t n, const std::vector<uint64_t>& ro,
     for (uint64_t s0 = 0; s0 < ns; s0 += 8)
         maxch = std::max<uint64_t>(maxch, (off[std::min(ns, s0 + 8)] - off[s0]) * 12);
     maxch = (maxch + 1023) & ~uint64_t(1023);
-    h->spmv_stage_bytes = (maxch > 0 && maxch * kSpmvStages + 128 <= 110 * 1024) ? uint32_t(maxch) : 0;
+    h->spmv_stage_bytes = (maxch > 0 && (maxch + kSpmvHdr) * kSpmvStages + 128 <= 110 * 1024) ? uint32_t(maxch) : 0;
     if (std::getenv("HFPG_NO_SPMV_TMA")) h->spmv_stage_bytes = 0;
     // k_solve's ring: two stages of 16-slice chunks inside a free 96 KB leaf stage
     uint64_t maxch16 = 0;
@@ -778,7 +780,7 @@ void frame_gpu(hfpg_handle* h, const FrameParams& FP) {
     h->fro = std::sqrt(sums[1]);
     h->diag_positive = (T[1] & 0xFFFFFFFFULL) == 0;
     uint64_t maxch = (T[2] + 1023) & ~uint64_t(1023);
-    const uint32_t sb = (maxch > 0 && maxch * kSpmvStages + 128 <= 110 * 1024) ? uint32_t(maxch) : 0;
+    const uint32_t sb = (maxch > 0 && (maxch + kSpmvHdr) * kSpmvStages + 128 <= 110 * 1024) ? uint32_t(maxch) : 0;
     const uint64_t maxch16 = (T[3] + 127) & ~uint64_t(127);
     const uint32_t psb = (maxch16 > 0 && 2 * maxch16 <= sizeof(PStage)) ? uint32_t(maxch16) : 0;
     const bool no_tma = std::getenv("HFPG_NO_SPMV_TMA") != nullptr;

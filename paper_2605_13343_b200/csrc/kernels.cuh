@@ -145,6 +145,53 @@ __device__ __forceinline__ void spmv_epilogue(const DevSys& s, unsigned long lon
     }
 }
 
+// One SELL-32 row: acc += a_q * p(c_q) over W slots in slot (= the reference's column) order,
+// products and sums rounded separately (csr.cpp:76 is not FMA-contracted). p(c) = z[c] or, in
+// PCG mode, fma(beta, p_prev[c], z[c]) (pcg.cpp:118 recomputed at the gather). Every load of the
+// W slots is issued before the first arithmetic, with a fixed trip count: with predicated slots
+// ptxas reused one register pair for every gather and serialised the row into W dependent round
+// trips to L2 (ncu: 40 us for the 3D 1M SpMV, DFMA stalls on each gather in turn).
+template <int W, bool LOOP, bool CG>
+__device__ __forceinline__ double sell_row_w(const double* vals, const uint32_t* cols, int lane, const double* z,
+                                             const double* pprev, double beta, double acc) {
+    uint32_t c[W];
+    double zv[W], pv[W], a[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) c[q] = cols[q * 32 + lane];
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        zv[q] = CG ? __ldcg(&z[c[q]]) : z[c[q]];
+        if (LOOP) pv[q] = CG ? __ldcg(&pprev[c[q]]) : pprev[c[q]];
+    }
+#pragma unroll
+    for (int q = 0; q < W; ++q) a[q] = vals[q * 32 + lane];
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        const double pc = LOOP ? fma(beta, pv[q], zv[q]) : zv[q];
+        acc = __dadd_rn(acc, __dmul_rn(a[q], pc));
+    }
+    return acc;
+}
+template <bool LOOP, bool CG>
+__device__ __forceinline__ double sell_row(const double* vals, const uint32_t* cols, uint64_t w, int lane,
+                                           const double* z, const double* pprev, double beta) {
+    double acc = 0.0;
+    uint64_t j = 0;
+    for (; j + 8 <= w; j += 8) acc = sell_row_w<8, LOOP, CG>(vals + j * 32, cols + j * 32, lane, z, pprev, beta, acc);
+    vals += j * 32;
+    cols += j * 32;
+    switch (w - j) {  // uniform per slice
+        case 1: return sell_row_w<1, LOOP, CG>(vals, cols, lane, z, pprev, beta, acc);
+        case 2: return sell_row_w<2, LOOP, CG>(vals, cols, lane, z, pprev, beta, acc);
+        case 3: return sell_row_w<3, LOOP, CG>(vals, cols, lane, z, pprev, beta, acc);
+        case 4: return sell_row_w<4, LOOP, CG>(vals, cols, lane, z, pprev, beta, acc);
+        case 5: return sell_row_w<5, LOOP, CG>(vals, cols, lane, z, pprev, beta, acc);
+        case 6: return sell_row_w<6, LOOP, CG>(vals, cols, lane, z, pprev, beta, acc);
+        case 7: return sell_row_w<7, LOOP, CG>(vals, cols, lane, z, pprev, beta, acc);
+        default: return acc;
+    }
+}
+
 // ============================================================================================
 // SpMV on SELL-32 (slices of 32 rows, column-major inside a slice, padded with (row, 0.0)).
 // One thread per row: every load is coalesced and each row accumulates sequentially in the
@@ -166,31 +213,16 @@ __global__ void __launch_bounds__(256) k_spmv(DevSys s, const double* xin, doubl
          row += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t sl = row >> 5, lane = row & 31;
         const uint64_t base = s.slice_off[sl], w = (s.slice_off[sl + 1] - base) >> 5;
-        double acc = 0.0;
-        // Batches of 8 slots: the streamed index/value loads first (no L1 allocation), then
-        // the gathers (L1-cached: neighbours share Morton bricks), then the accumulation in
-        // slot order. The reference's csr.cpp:76 loop is not FMA-contracted, so products and
-        // sums are rounded separately (__dmul_rn/__dadd_rn): ap is bit-identical to spmv().
-        for (uint64_t j0 = 0; j0 < w; j0 += 8) {
-            uint32_t c[8];
-            double a[8], pc[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (j0 + q < w) {
-                    const uint64_t idx = base + (j0 + q) * 32 + lane;
-                    c[q] = ldg_stream_u32(&s.sell_cols[idx]);
-                    a[q] = ldg_stream_f64(&s.sell_vals[idx]);
-                }
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (j0 + q < w) pc[q] = MODE == kLoop ? fma(beta, pp_[c[q]], z[c[q]]) : z[c[q]];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (j0 + q < w) acc = __dadd_rn(acc, __dmul_rn(a[q], pc[q]));
+        double zr = 0.0, pr = 0.0;
+        if (MODE == kLoop) {
+            zr = z[row];
+            pr = pp_[row];
         }
+        const double acc = sell_row<MODE == kLoop, false>(s.sell_vals + base, s.sell_cols + base, w, int(lane), z,
+                                                          pp_, beta);
         y[row] = acc;
         if (MODE == kLoop) {
-            const double pi = fma(beta, pp_[row], z[row]);
+            const double pi = fma(beta, pr, zr);
             pnew[row] = pi;
             v[0] = fma(pi, acc, v[0]);
             v[1] = fma(pi, pi, v[1]);
@@ -204,19 +236,55 @@ __global__ void __launch_bounds__(256) k_spmv(DevSys s, const double* xin, doubl
     }
 }
 
-// SpMV, streaming variant: persistent CTAs walk chunks of 8 SELL slices (256 rows); the
-// chunk's values and column indices (contiguous in SELL order) arrive by cp.async.bulk into a
-// 3-stage ring, so only the x/p gathers (L1/L2-resident neighbours) are synchronous loads.
-// Same arithmetic as k_spmv (bit-identical to the reference spmv). Used when every chunk fits
-// a stage (host-checked); k_spmv covers the general case.
+// SpMV, streaming variant: persistent CTAs walk chunks of 8 SELL slices (256 rows), warp-
+// specialised. Warp 8 (the producer) reads the chunk's 9 slice offsets into the stage header and
+// bulk-copies the chunk's values and column indices (contiguous in SELL order) into a 3-stage
+// ring; warps 0-7 (one slice each) copy their slots from the stage into registers, release the
+// stage (mbarrier arrive, so the next chunk's copy starts while this one's gathers are still in
+// flight), then gather z / p_prev (L1/L2-resident neighbours) and accumulate. No CTA-wide
+// barrier inside the loop. Same arithmetic as k_spmv (bit-identical to the reference spmv).
+// Used when every chunk fits a stage (host-checked); k_spmv covers the general case.
 constexpr int kSpmvStages = 3;
+constexpr int kSpmvThreads = 288;  // 8 consumer warps + 1 producer warp
+constexpr uint32_t kSpmvHdr = 128; // per stage: 9 slice offsets (u64)
+
+// Consumer half of a fixed-width row: slots from the stage into registers, release the stage,
+// then the gathers (all issued before the first product) and the exact-order accumulation.
+template <int W, bool LOOP>
+__device__ __forceinline__ double sell_row_release(const double* vals, const uint32_t* cols, int lane,
+                                                   const double* z, const double* pprev, double beta,
+                                                   uint64_t* empty) {
+    uint32_t c[W];
+    double a[W], zv[W], pv[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        c[q] = cols[q * 32 + lane];
+        a[q] = vals[q * 32 + lane];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty);
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        zv[q] = z[c[q]];
+        if (LOOP) pv[q] = pprev[c[q]];
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        const double pc = LOOP ? fma(beta, pv[q], zv[q]) : zv[q];
+        acc = __dadd_rn(acc, __dmul_rn(a[q], pc));
+    }
+    return acc;
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(256) k_spmv_tma(DevSys s, const double* xin, double* yout) {
+__global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv_tma(DevSys s, const double* xin, double* yout) {
     if (MODE == kLoop && s.sc->done) return;
     extern __shared__ __align__(128) unsigned char sraw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(sraw);
-    unsigned char* buf = sraw + 128;
-    const uint32_t cap = s.spmv_stage_bytes;
+    uint64_t* empty = full + kSpmvStages;
+    unsigned char* ring = sraw + 128;
+    const uint32_t cap = s.spmv_stage_bytes, stride = cap + kSpmvHdr;
     const unsigned long long k = MODE == kLoop ? s.sc->k : 0ULL;
     const double* z = MODE == kLoop ? s.z : xin;
     const double* pp_ = MODE == kLoop ? p_prev(s, k) : nullptr;
@@ -225,66 +293,83 @@ __global__ void __launch_bounds__(256) k_spmv_tma(DevSys s, const double* xin, d
     const double beta = MODE != kLoop ? 0.0 : s.G > 1 ? part_spmv_beta(s, k, pp_, pnew) : s.sc->beta;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t nsl = (s.n + 31) >> 5, nch = (nsl + 7) >> 3;
-    const uint64_t pol = policy_evict_first();
     if (tid == 0) {
-        for (int q = 0; q < kSpmvStages; ++q) mbar_init(&full[q], 1);
+        for (int q = 0; q < kSpmvStages; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], 8);
+        }
         fence_mbar_init();
     }
     __syncthreads();
-    auto issue = [&](uint64_t ch, int st) {
-        const uint64_t s0 = ch * 8, s1 = s0 + 8 < nsl ? s0 + 8 : nsl;
-        const uint64_t e0 = s.slice_off[s0], e1 = s.slice_off[s1], ne = e1 - e0;
-        unsigned char* b = buf + size_t(st) * cap;
-        mbar_expect_tx(&full[st], uint32_t(ne * 12));
-        tma_load_1d(b, s.sell_vals + e0, uint32_t(ne * 8), &full[st], pol);
-        tma_load_1d(b + ne * 8, s.sell_cols + e0, uint32_t(ne * 4), &full[st], pol);
-    };
-    if (tid == 0)
-        for (int q = 0; q < kSpmvStages; ++q)
-            if (blockIdx.x + uint64_t(q) * gridDim.x < nch) issue(blockIdx.x + uint64_t(q) * gridDim.x, q);
     double v[2] = {0.0, 0.0};
-    uint32_t it = 0;
-    for (uint64_t ch = blockIdx.x; ch < nch; ch += gridDim.x, ++it) {
-        const int st = int(it % kSpmvStages);
-        const uint64_t s0 = ch * 8, sl = s0 + warp;
-        mbar_wait(&full[st], (it / kSpmvStages) & 1);
-        if (sl < nsl) {
-            const uint64_t s1 = s0 + 8 < nsl ? s0 + 8 : nsl;
-            const uint64_t e0 = s.slice_off[s0], ne = s.slice_off[s1] - e0;
-            const uint64_t b0 = s.slice_off[sl] - e0, w = (s.slice_off[sl + 1] - s.slice_off[sl]) >> 5;
-            const double* vals = reinterpret_cast<const double*>(buf + size_t(st) * cap) + b0;
-            const uint32_t* cols = reinterpret_cast<const uint32_t*>(buf + size_t(st) * cap + ne * 8) + b0;
-            const uint64_t row = sl * 32 + lane;
+    if (warp == 8) {  // producer
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            uint32_t it = 0;
+            for (uint64_t ch = blockIdx.x; ch < nch; ch += gridDim.x, ++it) {
+                const int st = int(it % kSpmvStages);
+                if (it >= uint32_t(kSpmvStages)) mbar_wait(&empty[st], ((it / kSpmvStages) - 1) & 1);
+                unsigned char* b = ring + size_t(st) * stride;
+                unsigned long long* off = reinterpret_cast<unsigned long long*>(b);
+                const uint64_t s0 = ch * 8;
+                unsigned long long o[9];
+#pragma unroll
+                for (int q = 0; q < 9; ++q) o[q] = __ldg(&s.slice_off[s0 + q < nsl ? s0 + q : nsl]);
+#pragma unroll
+                for (int q = 0; q < 9; ++q) off[q] = o[q];
+                const uint64_t ne = o[8] - o[0];
+                mbar_expect_tx(&full[st], uint32_t(ne * 12));
+                tma_load_1d(b + kSpmvHdr, s.sell_vals + o[0], uint32_t(ne * 8), &full[st], pol);
+                tma_load_1d(b + kSpmvHdr + ne * 8, s.sell_cols + o[0], uint32_t(ne * 4), &full[st], pol);
+            }
+        }
+    } else {  // consumers: warp w takes slice 8 ch + w
+        uint32_t it = 0;
+        for (uint64_t ch = blockIdx.x; ch < nch; ch += gridDim.x, ++it) {
+            const int st = int(it % kSpmvStages);
+            const uint64_t sl = ch * 8 + warp, row = sl * 32 + lane;
+            double zr = 0.0, pr = 0.0;
+            if (MODE == kLoop && row < s.n) {
+                zr = z[row];
+                pr = pp_[row];
+            }
+            mbar_wait(&full[st], (it / kSpmvStages) & 1);
+            const unsigned char* b = ring + size_t(st) * stride;
+            const unsigned long long* off = reinterpret_cast<const unsigned long long*>(b);
             double acc = 0.0;
-            for (uint64_t j0 = 0; j0 < w; j0 += 8) {
-                uint32_t c[8];
-                double a[8], pc[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    if (j0 + q < w) {
-                        c[q] = cols[(j0 + q) * 32 + lane];
-                        a[q] = vals[(j0 + q) * 32 + lane];
-                    }
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    if (j0 + q < w) pc[q] = MODE == kLoop ? fma(beta, pp_[c[q]], z[c[q]]) : z[c[q]];
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    if (j0 + q < w) acc = __dadd_rn(acc, __dmul_rn(a[q], pc[q]));
+            if (sl < nsl) {
+                const uint64_t e0 = off[0], ne = off[8] - e0, b0 = off[warp] - e0, w = (off[warp + 1] - off[warp]) >> 5;
+                const double* vals = reinterpret_cast<const double*>(b + kSpmvHdr) + b0;
+                const uint32_t* cols = reinterpret_cast<const uint32_t*>(b + kSpmvHdr + ne * 8) + b0;
+                constexpr bool LP = MODE == kLoop;
+                switch (w) {  // uniform per slice
+                    case 1: acc = sell_row_release<1, LP>(vals, cols, lane, z, pp_, beta, &empty[st]); break;
+                    case 2: acc = sell_row_release<2, LP>(vals, cols, lane, z, pp_, beta, &empty[st]); break;
+                    case 3: acc = sell_row_release<3, LP>(vals, cols, lane, z, pp_, beta, &empty[st]); break;
+                    case 4: acc = sell_row_release<4, LP>(vals, cols, lane, z, pp_, beta, &empty[st]); break;
+                    case 5: acc = sell_row_release<5, LP>(vals, cols, lane, z, pp_, beta, &empty[st]); break;
+                    case 6: acc = sell_row_release<6, LP>(vals, cols, lane, z, pp_, beta, &empty[st]); break;
+                    case 7: acc = sell_row_release<7, LP>(vals, cols, lane, z, pp_, beta, &empty[st]); break;
+                    case 8: acc = sell_row_release<8, LP>(vals, cols, lane, z, pp_, beta, &empty[st]); break;
+                    default:
+                        acc = sell_row<LP, false>(vals, cols, w, lane, z, pp_, beta);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&empty[st]);
+                }
+            } else {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
             }
             if (row < s.n) {
                 y[row] = acc;
                 if (MODE == kLoop) {
-                    const double pi = fma(beta, pp_[row], z[row]);
+                    const double pi = fma(beta, pr, zr);
                     pnew[row] = pi;
                     v[0] = fma(pi, acc, v[0]);
                     v[1] = fma(pi, pi, v[1]);
                 }
             }
         }
-        __syncthreads();  // stage st consumed
-        if (tid == 0 && ch + uint64_t(kSpmvStages) * gridDim.x < nch)
-            issue(ch + uint64_t(kSpmvStages) * gridDim.x, st);
     }
     if (MODE != kLoop) return;
     double tot[2];
@@ -372,6 +457,8 @@ __device__ __forceinline__ bool part_leaf_alpha(const DevSys& s, double& alpha) 
     return sok != 0;
 }
 
+constexpr uint64_t kCoarseS0 = 32;  // leaves per bottom subtree (group) of the up-sweep
+
 __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mode,
                                                                const double* rin_ext) {
     if (mode != kApply && s.sc->done) return;
@@ -405,7 +492,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mod
             tma_load_1d(&sm.F[st][q * kL * kL / 4], f + q * kL * kL / 4, kFBytes / 4,
                         &sm.full[st], pol_stream);
         // bridges: evict_last — the prolongation walks the leaves in reverse and finds the
-        // most recently streamed ones still in L2
+        // most recently streamed ones still in L2 (measured: evict_first makes it 10% slower)
         tma_load_1d(&sm.B[st][0], b, kBBytes / 2, &sm.full[st], pol_keep);
         tma_load_1d(&sm.B[st][kL * kLs], b + kL * kLs, kBBytes / 2, &sm.full[st], pol_keep);
         tma_load_1d(sm.vec[st][0], rsrc + leaf * kL, kL * 8, &sm.full[st], pol_keep);
@@ -634,8 +721,6 @@ __device__ __forceinline__ void load_tile32(const DevSys& s, uint64_t m, int lan
     }
 }
 
-constexpr uint64_t kCoarseS0 = 32;
-
 // Coarse stage, fast path (L_s = 32), part 1 — strip sums. Each CTA owns an aligned subtree of
 // up to 32 leaves, loads their restrictions (û | v̂, fp32) and runs the f64 up-sweep in shared
 // memory; every internal node's sums (root included) go to the heap-indexed node arrays.
@@ -849,67 +934,72 @@ __device__ __forceinline__ void sweep_leaves(const DevSys& s, uint64_t dlo, uint
     }
 }
 
-template <int V>
-__device__ __forceinline__ void sweep_group_v(const DevSys& s, uint64_t dlo, uint64_t t, uint64_t M, int level0) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int side = warp >> 3, c0 = 4 * (warp & 7);
-    double* node = side ? s.node_v : s.node_u;
-    constexpr int logV = V == 1 ? 0 : V == 2 ? 1 : V == 4 ? 2 : V == 8 ? 3 : 4;
-    const int lanes = int(M >= 32 ? 32 : M);
-    const uint64_t pos0 = t * M + uint64_t(lane) * V;  // first node position of this lane
+// Upper levels, coalesced: lane = column (256-byte rows of node sums per load / store). A block
+// of B consecutive nodes is summed pairwise in one lane's registers, one column per lane;
+// the <= 16 block roots of a group meet in shared memory for the last levels. (The previous
+// lane-per-node layout issued 32-sector loads and stores and took 10 us for 256 roots on the
+// single SM that runs the upper levels.)
+template <int B>
+__device__ __forceinline__ double sweep_block(double* node, uint64_t dlo, uint64_t p0, int lane) {
+    double v[B];
 #pragma unroll
-    for (int cp = 0; cp < 4; cp += 2) {  // two columns at a time (register budget)
-        double v0[V], v1[V];
-        if (lane < lanes) {
+    for (int i = 0; i < B; ++i) v[i] = __ldcg(&node[((1ULL << dlo) - 1 + p0 + i) * 32 + lane]);
 #pragma unroll
-            for (int i = 0; i < V; ++i) {
-                if (level0) {
-                    const float2 f = __ldcg(reinterpret_cast<const float2*>(
-                        &s.restrict_[(pos0 + i) * 64 + 32 * side + c0 + cp]));
-                    v0[i] = f.x;
-                    v1[i] = f.y;
-                } else {
-                    const double2 a = __ldcg(reinterpret_cast<const double2*>(
-                        &node[((1ULL << dlo) - 1 + pos0 + i) * 32 + c0 + cp]));
-                    v0[i] = a.x;
-                    v1[i] = a.y;
-                }
-            }
+    for (int l2 = 0; (1 << l2) < B; ++l2) {
 #pragma unroll
-            for (int l2 = 0; l2 < logV; ++l2) {  // in-lane pairwise levels
-#pragma unroll
-                for (int i = 0; i < (V >> (l2 + 1)); ++i) {
-                    v0[i] = v0[2 * i] + v0[2 * i + 1];
-                    v1[i] = v1[2 * i] + v1[2 * i + 1];
-                    const uint64_t d = dlo - (l2 + 1), p = (pos0 >> (l2 + 1)) + i;
-                    __stcg(reinterpret_cast<double2*>(&node[((1ULL << d) - 1 + p) * 32 + c0 + cp]),
-                           make_double2(v0[i], v1[i]));
-                }
-            }
-        } else {
-            v0[0] = v1[0] = 0.0;
-        }
-        for (int l2 = 0; (1 << l2) < lanes; ++l2) {  // butterfly: step 2^l2
-            const int d = 1 << l2;
-            v0[0] += __shfl_xor_sync(0xffffffffu, v0[0], d);
-            v1[0] += __shfl_xor_sync(0xffffffffu, v1[0], d);
-            if (lane < lanes && (lane & (2 * d - 1)) == 0) {
-                const uint64_t dd = dlo - logV - (l2 + 1);
-                const uint64_t p = ((t * M) >> (logV + l2 + 1)) + uint64_t(lane >> (l2 + 1));
-                __stcg(reinterpret_cast<double2*>(&node[((1ULL << dd) - 1 + p) * 32 + c0 + cp]),
-                       make_double2(v0[0], v1[0]));
-            }
+        for (int i = 0; i < (B >> (l2 + 1)); ++i) {
+            v[i] = v[2 * i] + v[2 * i + 1];  // heap sum: left child + right child
+            const uint64_t d = dlo - (l2 + 1), pos = (p0 >> (l2 + 1)) + i;
+            __stcg(&node[((1ULL << d) - 1 + pos) * 32 + lane], v[i]);
         }
     }
+    return v[0];
 }
-__device__ __forceinline__ void sweep_group(const DevSys& s, uint64_t dlo, uint64_t t, uint64_t M, int level0) {
-    switch (M >= 32 ? M / 32 : 1) {
-        case 1: sweep_group_v<1>(s, dlo, t, M, level0); break;
-        case 2: sweep_group_v<2>(s, dlo, t, M, level0); break;
-        case 4: sweep_group_v<4>(s, dlo, t, M, level0); break;
-        case 8: sweep_group_v<8>(s, dlo, t, M, level0); break;
-        default: sweep_group_v<16>(s, dlo, t, M, level0); break;
+// All internal nodes above M (a power of two <= kSumsGroup) nodes at depth dlo, positions
+// [t M, (t+1) M). Called by every thread of a kSumsThreads CTA: warps 0-7 the u sums, 8-15 v.
+__device__ __forceinline__ void sweep_group(const DevSys& s, uint64_t dlo, uint64_t t, uint64_t M) {
+    __shared__ double roots[2][16][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int side = warp >> 3, j = warp & 7;
+    double* node = side ? s.node_v : s.node_u;
+    const uint64_t B = M >= 256 ? 32 : (M >= 8 ? M / 8 : 1), nb = M / B;
+    int logB = 0;
+    while ((1ULL << logB) < B) ++logB;
+    for (uint64_t b = j; b < nb; b += 8) {
+        const uint64_t p0 = t * M + b * B;
+        double r;
+        switch (B) {
+            case 1: r = sweep_block<1>(node, dlo, p0, lane); break;
+            case 2: r = sweep_block<2>(node, dlo, p0, lane); break;
+            case 4: r = sweep_block<4>(node, dlo, p0, lane); break;
+            case 8: r = sweep_block<8>(node, dlo, p0, lane); break;
+            case 16: r = sweep_block<16>(node, dlo, p0, lane); break;
+            default: r = sweep_block<32>(node, dlo, p0, lane); break;
+        }
+        roots[side][b][lane] = r;
     }
+    __syncthreads();
+    if (j == 0 && nb > 1) {  // the levels above the blocks (nb <= 16 block roots)
+        double v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = uint64_t(i) < nb ? roots[side][i][lane] : 0.0;
+        const uint64_t dblk = dlo - logB, q0 = t * nb;  // block roots: depth dblk, positions q0 + i
+        uint64_t cnt = nb;
+#pragma unroll
+        for (int l2 = 0; l2 < 4; ++l2) {
+            if (cnt < 2) break;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (uint64_t(i) < cnt / 2) {
+                    v[i] = v[2 * i] + v[2 * i + 1];
+                    const uint64_t d = dblk - (l2 + 1), pos = (q0 >> (l2 + 1)) + i;
+                    __stcg(&node[((1ULL << d) - 1 + pos) * 32 + lane], v[i]);
+                }
+            }
+            cnt /= 2;
+        }
+    }
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(kSumsThreads) k_sums_tree(DevSys s, int mode) {
@@ -928,23 +1018,24 @@ __global__ void __launch_bounds__(kSumsThreads) k_sums_tree(DevSys s, int mode) 
     unsigned arrivals = gridDim.x;  // CTAs that report into this level's counter
     uint64_t t = blockIdx.x;
     while (true) {
-        __threadfence();
+        // the CTA's node writes are ordered before thread 0's release by the barrier; thread 0's
+        // acq_rel arrival also acquires the other CTAs' writes for the whole CTA (no SC fences:
+        // MEMBAR.SC.GPU from every warp cost more than the sweep itself)
         __syncthreads();
         if (dlo == 0) break;  // the rank's root is done
         if (tid == 0) {
-            const unsigned old = atomicAdd(counter, 1u);
+            const unsigned old = atom_add_acq_rel_gpu(counter, 1u);
             last = (old == arrivals - 1);
             if (last) *counter = 0u;
         }
         __syncthreads();
         if (!last) return;
-        __threadfence();
         // this CTA is the last of its level: sweep the next level's groups (all of them if
         // they fit one group, else chain once more per group of 512)
         const uint64_t M = cnt < kSumsGroup ? cnt : kSumsGroup, ng = cnt / M;
         int logM = 0;
         while ((1ULL << logM) < M) ++logM;
-        for (uint64_t g = 0; g < ng; ++g) sweep_group(s, dlo, g, M, 0);
+        for (uint64_t g = 0; g < ng; ++g) sweep_group(s, dlo, g, M);
         dlo -= logM;
         cnt = ng;
         ++counter;

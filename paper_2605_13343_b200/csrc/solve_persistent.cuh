@@ -621,26 +621,15 @@ __device__ __forceinline__ void p_spmv_phase(const DevSys& s, PSmem& sm, unsigne
     const uint32_t cap = s.pspmv_stage_bytes;
     auto row_work = [&](uint64_t sl, const double* vals, const uint32_t* cols, uint64_t w) {
         const uint64_t row = sl * 32 + lane;
-        double acc = 0.0;
-        for (uint64_t j0 = 0; j0 < w; j0 += 8) {
-            uint32_t c[8];
-            double a[8], pc[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (j0 + q < w) {
-                    c[q] = cols[(j0 + q) * 32 + lane];
-                    a[q] = vals[(j0 + q) * 32 + lane];
-                }
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (j0 + q < w) pc[q] = fma(beta, __ldcg(&pprev[c[q]]), __ldcg(&z[c[q]]));
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (j0 + q < w) acc = __dadd_rn(acc, __dmul_rn(a[q], pc[q]));
+        double zr = 0.0, pr = 0.0;
+        if (row < s.n) {
+            zr = __ldcg(&z[row]);
+            pr = __ldcg(&pprev[row]);
         }
+        const double acc = sell_row<true, true>(vals, cols, w, lane, z, pprev, beta);
         if (row < s.n) {
             s.ap[row] = acc;
-            const double pi = fma(beta, __ldcg(&pprev[row]), __ldcg(&z[row]));
+            const double pi = fma(beta, pr, zr);
             pcur[row] = pi;
             v[0] = fma(pi, acc, v[0]);
             v[1] = fma(pi, pi, v[1]);
