@@ -28,6 +28,7 @@ struct Scalars {
     int done;      // loop finished: every later kernel of the iteration early-exits
     int pad;
     double rr_loc; // row partition: this rank's |r|^2 partial (leaf -> strip-sum kernel)
+    double rzs[2]; // deferred reductions: r.z of iteration k-1, by parity of k (SpMV writes)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -126,6 +127,45 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
+}
+
+// Deferred grid reductions: the producing kernel only publishes one partial per CTA (block
+// reduce, no arrival counter, no fence, no last-CTA tail); every CTA of the consuming kernel sums
+// all partials itself in one fixed order (one warp: lane-strided sums, then an xor butterfly,
+// whose result is bit-identical in every lane — a + b = b + a — and so in every CTA).
+template <int NV>
+__device__ __forceinline__ void publish_partials(const double (&v)[NV], double* dst) {
+    __shared__ double red[NV][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const double s = warp_sum(v[i]);
+        if (lane == 0) red[i][warp] = s;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double s = lane < nwarps ? red[i][lane] : 0.0;
+            s = warp_sum(s);
+            if (lane == 0) dst[blockIdx.x * NV + i] = s;
+        }
+    }
+}
+// Called by one whole warp.
+template <int NV>
+__device__ __forceinline__ void sum_partials(const double* src, uint32_t n, double (&out)[NV]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double acc = 0.0;
+        for (uint32_t j = lane; j < n; j += 32) acc += __ldcg(&src[j * NV + i]);
+        out[i] = warp_sum(acc);
+    }
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // Block-reduce NV values, publish the CTA partial, and let the last-arriving CTA reduce all

@@ -98,6 +98,7 @@ struct hfpg_handle {
     double *node_u = nullptr, *node_v = nullptr;
     unsigned* tree_counters = nullptr;
     double* partials = nullptr;
+    double* dpart = nullptr;  // deferred-reduction partials (kPartLen)
     uint64_t partials_cap = 0;
     unsigned* counters = nullptr;
     Scalars* sc = nullptr;
@@ -176,8 +177,16 @@ uint64_t prolong_grid(const hfpg_handle* h) {
     return h->fast ? std::min<uint64_t>((h->L.k + kProlWarps - 1) / kProlWarps, uint64_t(h->num_sms) * 2)
                    : h->L.k;
 }
+uint32_t spmv_stages() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("HFPG_SPMV_STAGES");
+        const int n = e ? std::atoi(e) : kSpmvStages;
+        return uint32_t(n >= 2 && n <= 8 ? n : kSpmvStages);
+    }();
+    return v;
+}
 size_t spmv_smem(const hfpg_handle* h) {
-    return h->spmv_stage_bytes ? 128 + size_t(h->spmv_stage_bytes + kSpmvHdr) * kSpmvStages : 0;
+    return h->spmv_stage_bytes ? 128 + size_t(h->spmv_stage_bytes + kSpmvHdr) * spmv_stages() : 0;
 }
 uint64_t spmv_grid(const hfpg_handle* h) {
     if (h->spmv_stage_bytes) {
@@ -241,6 +250,10 @@ void ensure_workspace(hfpg_handle* h) {
         dalloc(h->partials, need);
         h->partials_cap = need;
     }
+    if (!h->dpart) {
+        dalloc(h->dpart, kPartLen);
+        CK(cudaMemsetAsync(h->dpart, 0, kPartLen * sizeof(double), h->stream));
+    }
     if (!h->counters) {
         dalloc(h->counters, 8);
         CK(cudaMemsetAsync(h->counters, 0, 8 * sizeof(unsigned), h->stream));
@@ -293,8 +306,16 @@ void fill_sys(hfpg_handle* h) {
     s.coarse_S = coarse_width(L);
     s.spmv_stage_bytes = h->spmv_stage_bytes;
     s.pspmv_stage_bytes = h->pspmv_stage_bytes;
+    s.spmv_stages = spmv_stages();
     s.partials = h->partials;
     s.counters = h->counters;
+    s.dpart = h->dpart;
+    s.grid_spmv = uint32_t(spmv_grid(h));
+    s.grid_leaf = uint32_t(leaf_grid(h));
+    s.grid_prol = uint32_t(prolong_grid(h));
+    // deferred reductions on the single-rank factor fast path (HFPG_NO_DEFER=1: last-CTA tails)
+    s.defer = h->part.G == 1 && h->precond == HFPG_PRECOND_FACTOR && h->fast && h->have_factors &&
+              !std::getenv("HFPG_NO_DEFER");
     s.sc = h->sc;
     s.history = h->history;
     s.use_cond = 0;
@@ -531,7 +552,7 @@ void upload_csr(hfpg_handle* h, uint64_t n, const std::vector<uint64_t>& ro,
     for (uint64_t s0 = 0; s0 < ns; s0 += 8)
         maxch = std::max<uint64_t>(maxch, (off[std::min(ns, s0 + 8)] - off[s0]) * 12);
     maxch = (maxch + 1023) & ~uint64_t(1023);
-    h->spmv_stage_bytes = (maxch > 0 && (maxch + kSpmvHdr) * kSpmvStages + 128 <= 110 * 1024) ? uint32_t(maxch) : 0;
+    h->spmv_stage_bytes = (maxch > 0 && (maxch + kSpmvHdr) * spmv_stages() + 128 <= 110 * 1024) ? uint32_t(maxch) : 0;
     if (std::getenv("HFPG_NO_SPMV_TMA")) h->spmv_stage_bytes = 0;
     // k_solve's ring: two stages of 16-slice chunks inside a free 96 KB leaf stage
     uint64_t maxch16 = 0;
@@ -780,7 +801,7 @@ void frame_gpu(hfpg_handle* h, const FrameParams& FP) {
     h->fro = std::sqrt(sums[1]);
     h->diag_positive = (T[1] & 0xFFFFFFFFULL) == 0;
     uint64_t maxch = (T[2] + 1023) & ~uint64_t(1023);
-    const uint32_t sb = (maxch > 0 && (maxch + kSpmvHdr) * kSpmvStages + 128 <= 110 * 1024) ? uint32_t(maxch) : 0;
+    const uint32_t sb = (maxch > 0 && (maxch + kSpmvHdr) * spmv_stages() + 128 <= 110 * 1024) ? uint32_t(maxch) : 0;
     const uint64_t maxch16 = (T[3] + 127) & ~uint64_t(127);
     const uint32_t psb = (maxch16 > 0 && 2 * maxch16 <= sizeof(PStage)) ? uint32_t(maxch16) : 0;
     const bool no_tma = std::getenv("HFPG_NO_SPMV_TMA") != nullptr;
@@ -844,7 +865,7 @@ int hfpg_destroy(hfpg_handle* h) {
         dfree(h->a_diag); dfree(h->x); dfree(h->r); dfree(h->z); dfree(h->ap); dfree(h->p0);
         dfree(h->p1); dfree(h->y_loc); dfree(h->b); dfree(h->scratch); dfree(h->restrict_);
         dfree(h->coupled); dfree(h->node_u); dfree(h->node_v);
-        dfree(h->tree_counters); dfree(h->partials); dfree(h->counters); dfree(h->sc);
+        dfree(h->tree_counters); dfree(h->partials); dfree(h->dpart); dfree(h->counters); dfree(h->sc);
         dfree(h->history); dfree(h->gbar); dfree(h->trace);
         if (h->sc_host) cudaFreeHost(h->sc_host);
         {

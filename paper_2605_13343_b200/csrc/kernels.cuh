@@ -38,6 +38,7 @@ struct DevSys {
     uint64_t coarse_S;       // subtree width per k_coarse task (power of two)
     uint32_t spmv_stage_bytes; // k_spmv_tma stage capacity (0: use k_spmv)
     uint32_t pspmv_stage_bytes; // k_solve SpMV ring stage (16 slices; 0: direct loads)
+    uint32_t spmv_stages;      // k_spmv_tma ring depth (<= 8)
     // reductions / state
     double* partials;
     unsigned* counters;  // [0] spmv, [1] leaf, [2] prolong, [3] simple
@@ -61,7 +62,13 @@ struct DevSys {
     const uint32_t* send_slot;      //       destination ghost slot in that peer
     const unsigned long long* send_off;  // G + 1
     unsigned long long* seq;        // 3 message sequence counters (monotonic across solves)
+    // deferred reductions (single-rank factor path): per-CTA partials of the SpMV (p.Ap, p.p),
+    // the leaf kernel (|r|^2) and the prolongation (r.z), summed by the next kernel
+    int defer;
+    double* dpart;
+    uint32_t grid_spmv, grid_leaf, grid_prol;
 };
+constexpr uint32_t kPartSpmv = 0, kPartLeaf = 2048, kPartProl = 3072, kPartLen = 4096;
 
 enum Mode { kInit = 0, kLoop = 1, kApply = 2 };
 
@@ -192,6 +199,21 @@ __device__ __forceinline__ double sell_row(const double* vals, const uint32_t* c
     }
 }
 
+// Deferred: beta_k = rz_{k-1} / rz_{k-2} (pcg.cpp:115-117; 0 at k = 1) from the previous
+// prolongation's r.z partials. One warp; CTA 0 records rz_{k-1} in the parity slot k & 1 (the
+// slot this iteration's leaf kernel reads for alpha, while slot (k-1) & 1 stays readable).
+__device__ __forceinline__ double defer_beta(const DevSys& s, unsigned long long k) {
+    double rz[1];
+    sum_partials<1>(s.dpart + kPartProl, s.grid_prol, rz);
+    const double beta = k >= 2 ? rz[0] / s.sc->rzs[(k - 1) & 1] : 0.0;
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) {
+        s.sc->rzs[k & 1] = rz[0];
+        s.sc->rz = rz[0];
+        s.sc->beta = beta;
+    }
+    return beta;
+}
+
 // ============================================================================================
 // SpMV on SELL-32 (slices of 32 rows, column-major inside a slice, padded with (row, 0.0)).
 // One thread per row: every load is coalesced and each row accumulates sequentially in the
@@ -206,7 +228,13 @@ __global__ void __launch_bounds__(256) k_spmv(DevSys s, const double* xin, doubl
     const double* pp_ = MODE == kLoop ? p_prev(s, k) : nullptr;
     double* pnew = MODE == kLoop ? p_cur(s, k) : nullptr;
     double* y = MODE == kLoop ? s.ap : yout;
-    const double beta = MODE != kLoop ? 0.0 : s.G > 1 ? part_spmv_beta(s, k, pp_, pnew) : s.sc->beta;
+    double beta = MODE != kLoop ? 0.0 : s.G > 1 ? part_spmv_beta(s, k, pp_, pnew) : s.sc->beta;
+    if (MODE == kLoop && s.defer) {
+        __shared__ double sb;
+        if (threadIdx.x < 32) sb = defer_beta(s, k);
+        __syncthreads();
+        beta = sb;
+    }
     double v[2] = {0.0, 0.0};
     // persistent grid-stride over rows: one CTA partial (and one fence) per CTA, not per row
     for (uint64_t row = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < s.n;
@@ -229,6 +257,10 @@ __global__ void __launch_bounds__(256) k_spmv(DevSys s, const double* xin, doubl
         }
     }
     if (MODE != kLoop) return;
+    if (s.defer) {
+        publish_partials<2>(v, s.dpart + kPartSpmv);
+        return;
+    }
     double tot[2];
     if (grid_reduce_last<2>(v, s.partials, &s.counters[0], tot)) {
         if (s.G > 1) part_send_m1(s, tot[0], tot[1]);
@@ -282,7 +314,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv_tma(DevSys s, const do
     if (MODE == kLoop && s.sc->done) return;
     extern __shared__ __align__(128) unsigned char sraw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(sraw);
-    uint64_t* empty = full + kSpmvStages;
+    const uint32_t NS = s.spmv_stages;
+    uint64_t* empty = full + NS;
     unsigned char* ring = sraw + 128;
     const uint32_t cap = s.spmv_stage_bytes, stride = cap + kSpmvHdr;
     const unsigned long long k = MODE == kLoop ? s.sc->k : 0ULL;
@@ -290,11 +323,12 @@ __global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv_tma(DevSys s, const do
     const double* pp_ = MODE == kLoop ? p_prev(s, k) : nullptr;
     double* pnew = MODE == kLoop ? p_cur(s, k) : nullptr;
     double* y = MODE == kLoop ? s.ap : yout;
-    const double beta = MODE != kLoop ? 0.0 : s.G > 1 ? part_spmv_beta(s, k, pp_, pnew) : s.sc->beta;
+    const bool defer = MODE == kLoop && s.defer;
+    double beta = MODE != kLoop || defer ? 0.0 : s.G > 1 ? part_spmv_beta(s, k, pp_, pnew) : s.sc->beta;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t nsl = (s.n + 31) >> 5, nch = (nsl + 7) >> 3;
     if (tid == 0) {
-        for (int q = 0; q < kSpmvStages; ++q) {
+        for (uint32_t q = 0; q < NS; ++q) {
             mbar_init(&full[q], 1);
             mbar_init(&empty[q], 8);
         }
@@ -307,8 +341,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv_tma(DevSys s, const do
             const uint64_t pol = policy_evict_first();
             uint32_t it = 0;
             for (uint64_t ch = blockIdx.x; ch < nch; ch += gridDim.x, ++it) {
-                const int st = int(it % kSpmvStages);
-                if (it >= uint32_t(kSpmvStages)) mbar_wait(&empty[st], ((it / kSpmvStages) - 1) & 1);
+                const int st = int(it % NS);
+                if (it >= NS) mbar_wait(&empty[st], ((it / NS) - 1) & 1);
                 unsigned char* b = ring + size_t(st) * stride;
                 unsigned long long* off = reinterpret_cast<unsigned long long*>(b);
                 const uint64_t s0 = ch * 8;
@@ -324,16 +358,22 @@ __global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv_tma(DevSys s, const do
             }
         }
     } else {  // consumers: warp w takes slice 8 ch + w
+        if (defer) {  // beta from the previous prolongation's r.z partials, while the producer streams
+            __shared__ double sb;
+            if (warp == 0) sb = defer_beta(s, k);
+            named_bar_sync(1, 256);
+            beta = sb;
+        }
         uint32_t it = 0;
         for (uint64_t ch = blockIdx.x; ch < nch; ch += gridDim.x, ++it) {
-            const int st = int(it % kSpmvStages);
+            const int st = int(it % NS);
             const uint64_t sl = ch * 8 + warp, row = sl * 32 + lane;
             double zr = 0.0, pr = 0.0;
             if (MODE == kLoop && row < s.n) {
                 zr = z[row];
                 pr = pp_[row];
             }
-            mbar_wait(&full[st], (it / kSpmvStages) & 1);
+            mbar_wait(&full[st], (it / NS) & 1);
             const unsigned char* b = ring + size_t(st) * stride;
             const unsigned long long* off = reinterpret_cast<const unsigned long long*>(b);
             double acc = 0.0;
@@ -372,6 +412,10 @@ __global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv_tma(DevSys s, const do
         }
     }
     if (MODE != kLoop) return;
+    if (s.defer) {
+        publish_partials<2>(v, s.dpart + kPartSpmv);
+        return;
+    }
     double tot[2];
     if (grid_reduce_last<2>(v, s.partials, &s.counters[0], tot)) {
         if (s.G > 1) part_send_m1(s, tot[0], tot[1]);
@@ -465,7 +509,8 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mod
     extern __shared__ __align__(128) unsigned char smem_raw[];
     LeafSmem& sm = *reinterpret_cast<LeafSmem*>(smem_raw);
     const int tid = threadIdx.x;
-    double alpha = mode == kLoop ? s.sc->alpha : 0.0;
+    const bool defer = mode == kLoop && s.defer;
+    double alpha = mode == kLoop && !defer ? s.sc->alpha : 0.0;
     if (s.G > 1 && mode == kLoop && !part_leaf_alpha(s, alpha)) return;
     const double* rsrc = mode == kApply ? rin_ext : s.r;
     const double* pcur = mode == kLoop ? p_cur(s, s.sc->k) : nullptr;
@@ -503,6 +548,38 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mod
         }
     };
     if (tid == 0 && blockIdx.x < K) issue(blockIdx.x, 0);
+    if (defer) {  // alpha from the SpMV's partials while the first leaf streams in
+        __shared__ double sa;
+        __shared__ int sbrk;
+        if (tid >= 32 && tid < 64) {
+            double t[2];
+            sum_partials<2>(s.dpart + kPartSpmv, s.grid_spmv, t);
+            if (tid == 32) {
+                Scalars* sc = s.sc;
+                const unsigned long long k = sc->k;
+                const bool brk = t[0] < -sc->breakdown_tol * t[1] || t[0] == 0.0;  // pcg.cpp:90-95
+                sa = sc->rzs[k & 1] / t[0];
+                sbrk = brk;
+                if (blockIdx.x == 0) {
+                    sc->pap = t[0];
+                    sc->pp = t[1];
+                    sc->alpha = sa;
+                    if (brk) {
+                        sc->status = 2;
+                        sc->breakdown_iter = k;
+                        sc->iterations = k;
+                        sc->done = 1;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        alpha = sa;
+        if (sbrk) {  // no update; let the issued copy land before the CTA exits
+            if (blockIdx.x < K) mbar_wait(&sm.full[0], 0);
+            return;
+        }
+    }
 
     double rr = 0.0;
     const int lane = tid & 31, warp = tid >> 5;
@@ -588,6 +665,10 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mod
     }
     if (mode == kApply) return;
     double v[1] = {rr}, tot[1];
+    if (s.defer) {  // |r|^2 is finished by k_tiles_all's CTA 0 (rel, history, stop)
+        publish_partials<1>(v, s.dpart + kPartLeaf);
+        return;
+    }
     if (grid_reduce_last<1>(v, s.partials, &s.counters[1], tot) && tid == 0) {
         if (s.G > 1) s.sc->rr_loc = tot[0];  // reduced across ranks after the strip sums (M2)
         else leaf_epilogue(s, mode, tot[0]);
@@ -1074,6 +1155,11 @@ __global__ void __launch_bounds__(kTilesThreads) k_tiles_all(DevSys s, int mode)
     __shared__ TileScratch ws[kTilesThreads / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t pol = policy_evict_last();
+    if (s.defer && mode != kApply && blockIdx.x == 0 && wid == 0) {  // |r|^2 of the leaf kernel
+        double rr[1];
+        sum_partials<1>(s.dpart + kPartLeaf, s.grid_leaf, rr);
+        if (lane == 0) leaf_epilogue(s, mode, rr[0]);  // r0 (init) or rel / history / stop
+    }
     if (s.G > 1 && blockIdx.x == 0) {
         __shared__ int stop;
         __shared__ unsigned long long q2s;
@@ -1474,6 +1560,25 @@ __global__ void __launch_bounds__(256, 2) k_prolong_fast(DevSys s, int mode, con
     }
     if (mode == kApply) return;
     double v[1] = {rz}, tot[1];
+    if (s.defer) {  // r.z is summed by the next SpMV (beta); CTA 0 keeps the books
+        publish_partials<1>(v, s.dpart + kPartProl);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            Scalars* sc = s.sc;
+            if (mode == kInit) {
+                sc->beta = 0.0;
+                sc->k = 1;
+                if (sc->max_iters == 0) {
+                    sc->iterations = 0;
+                    sc->status = 1;
+                    sc->done = 1;
+                }
+            } else {
+                sc->k += 1;
+            }
+            if (s.use_cond) cudaGraphSetConditional(s.cond, sc->done ? 0u : 1u);
+        }
+        return;
+    }
     if (grid_reduce_last<1>(v, s.partials, &s.counters[2], tot)) {
         if (s.G > 1) part_prolong_epilogue(s, mode, tot[0]);
         else if (threadIdx.x == 0) prolong_epilogue(s, mode, tot[0]);
