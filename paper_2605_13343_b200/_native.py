@@ -10,6 +10,10 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(HERE, "libhfpg.so")
+# development A/B only: HFPG_SO_VARIANT=<name> loads the in-tree variants/libhfpg_<name>.so built
+# by tools/build_variant.sh (same sources, different compile-time constants)
+if os.environ.get("HFPG_SO_VARIANT"):
+    SO_PATH = os.path.join(HERE, "variants", "libhfpg_%s.so" % os.environ["HFPG_SO_VARIANT"])
 
 HFPG_OK, HFPG_EINVAL, HFPG_EIO, HFPG_ECUDA, HFPG_ENCCL = range(5)
 HOST, DEVICE = 0, 1
