@@ -31,7 +31,8 @@ extern "C" {
 enum hfpg_status { HFPG_OK = 0, HFPG_EINVAL = 1, HFPG_EIO = 2, HFPG_ECUDA = 3, HFPG_ENCCL = 4 };
 enum hfpg_where { HFPG_HOST = 0, HFPG_DEVICE = 1 };
 /* pcg.cpp:28-51 identity_applier / jacobi_applier / factor_applier */
-enum hfpg_precond { HFPG_PRECOND_IDENTITY = 0, HFPG_PRECOND_JACOBI = 1, HFPG_PRECOND_FACTOR = 2 };
+enum hfpg_precond { HFPG_PRECOND_IDENTITY = 0, HFPG_PRECOND_JACOBI = 1, HFPG_PRECOND_FACTOR = 2,
+                     HFPG_PRECOND_IC0 = 3 };
 /* How hfpg_pcg_solve runs the loop. GRAPH: one CUDA graph, a conditional WHILE node over the
  * per-stage kernels (any layout / preconditioner). PERSISTENT: one cooperative kernel for the
  * whole solve, phases separated by grid barriers (factor preconditioner, L=128, L_s=32).
@@ -210,6 +211,21 @@ int hfpg_get_trace(hfpg_handle* h, uint64_t* out, uint32_t cap);
 
 /* apply.cpp:79-174 apply<float>: z = M r with the loaded factors and diag(A). */
 int hfpg_apply(hfpg_handle* h, const double* r, double* z, int where);
+/* ---- IC(0) baseline (ic0.hpp / ic0.cpp) ----
+ * ic0.cpp:10-69 ic0_factorize on the host (no device needed): the lower factor L of A (pattern =
+ * lower triangle of A, diagonal last; policy 0 = Ic0Shift::none, 1 = Ic0Shift::scaled, shift
+ * 1e-8 max diag), bit-identical to the reference. lro: n + 1, lci / lv: cap >= nnz(A) + n
+ * entries; *nnz_out = nnz(L). A nonpositive pivot is HFPG_EIO (std::runtime_error). */
+int hfpg_ic0_factor_host(uint64_t n, const uint64_t* row_offsets, const uint32_t* col_indices,
+                         const double* values, int32_t policy, uint64_t* lro, uint32_t* lci, double* lv,
+                         uint64_t cap, uint64_t* nnz_out, double* shift_out);
+/* ic0.cpp:72 ic0_applier: loads the factor (host pointers) for hfpg_ic0_apply and for
+ * hfpg_pcg_solve with HFPG_PRECOND_IC0. */
+int hfpg_load_ic0(hfpg_handle* h, uint64_t n, const uint64_t* lro, const uint32_t* lci, const double* lv);
+/* ic0.cpp:75-98: z = (L L^T)^{-1} r by two sync-free triangular sweeps on the device,
+ * bit-identical to the reference applier. */
+int hfpg_ic0_apply(hfpg_handle* h, const double* r, double* z, int where);
+
 /* csr.cpp:70-79 spmv: y = A x. */
 int hfpg_spmv(hfpg_handle* h, const double* x, double* y, int where);
 /* pcg.cpp:53-126 pcg_solve, the whole loop as one CUDA graph (conditional WHILE node).

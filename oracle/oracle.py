@@ -87,7 +87,7 @@ class _Base:
 
     def pcg_solve(self, csr, b, kind: int, leaf=0, ls=0, packed=None, rtol=1e-8,
                   max_iters=20000, spd_enabled=0, spd_raw=0.0):
-        """kind: 0 identity, 1 jacobi, 2 factor. Returns (report dict, x, history)."""
+        """kind: 0 identity, 1 jacobi, 2 factor, 3 ic0 (Ref only). Returns (report dict, x, history)."""
         ro, ci, v = csr
         n = len(ro) - 1
         x = np.empty(n, np.float64)
@@ -147,6 +147,33 @@ class Ref(_Base):
     """The reference itself, compiled from /root/reference by oracle/Makefile."""
 
     prefix = "ref_"
+
+    def ic0_factorize(self, csr, policy=1):
+        """ic0.cpp:10 -> (lro u64[n+1], lci u32[nnz], lv f64[nnz], shift)."""
+        ro, ci, v = csr
+        n = len(ro) - 1
+        cap = int(ro[-1]) + n
+        lro = np.empty(n + 1, np.uint64)
+        lci = np.empty(cap, np.uint32)
+        lv = np.empty(cap, np.float64)
+        nnz = C.c_uint64()
+        shift = C.c_double()
+        f = self._f("ic0_factorize")
+        f.argtypes = [_u64, _p, _p, _p, C.c_int, _p, _p, _p, _u64, _p, _p]
+        _check(f(n, _ptr(ro), _ptr(ci), _ptr(v), policy, _ptr(lro), _ptr(lci), _ptr(lv), cap,
+                 C.byref(nnz), C.byref(shift)), self.lib, "ic0_factorize")
+        return lro, lci[: nnz.value].copy(), lv[: nnz.value].copy(), shift.value
+
+    def ic0_apply(self, csr, r, policy=1):
+        """ic0_applier(ic0_factorize(A)) on r (ic0.cpp:72-99)."""
+        ro, ci, v = csr
+        n = len(ro) - 1
+        z = np.empty(n, np.float64)
+        f = self._f("ic0_apply")
+        f.argtypes = [_u64, _p, _p, _p, C.c_int, _p, _p]
+        _check(f(n, _ptr(ro), _ptr(ci), _ptr(v), policy, _ptr(np.ascontiguousarray(r, np.float64)),
+                 _ptr(z)), self.lib, "ic0_apply")
+        return z
 
     def __init__(self):
         super().__init__(REF_SO)

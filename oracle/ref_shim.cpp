@@ -14,6 +14,7 @@
 #include "hfp/csr.hpp"
 #include "hfp/factor_tensor.hpp"
 #include "hfp/frame.hpp"
+#include "hfp/ic0.hpp"
 #include "hfp/morton.hpp"
 #include "hfp/partition.hpp"
 #include "hfp/pcg.hpp"
@@ -213,7 +214,33 @@ int ref_assemble_dense_f32(uint64_t n, uint64_t leaf, uint64_t ls, const float* 
     });
 }
 
-// pcg.cpp:53 pcg_solve with identity (0) / jacobi (1) / factor (2) applier (pcg.cpp:28-51).
+// ic0.cpp:10 ic0_factorize (policy 0 none, 1 scaled) -> the lower factor as CSR.
+int ref_ic0_factorize(uint64_t n, const uint64_t* ro, const uint32_t* ci, const double* v, int policy,
+                      uint64_t* lro, uint32_t* lci, double* lv, uint64_t cap, uint64_t* nnz_out,
+                      double* shift_out) {
+    return guard([&] {
+        Ic0Factor f = ic0_factorize(make_csr(n, ro, ci, v), policy ? Ic0Shift::scaled : Ic0Shift::none);
+        *nnz_out = f.lower.col_indices.size();
+        *shift_out = f.shift;
+        if (cap < *nnz_out) throw std::invalid_argument("ref_ic0_factorize: capacity");
+        std::memcpy(lro, f.lower.row_offsets.data(), (n + 1) * 8);
+        std::memcpy(lci, f.lower.col_indices.data(), *nnz_out * 4);
+        std::memcpy(lv, f.lower.values.data(), *nnz_out * 8);
+    });
+}
+
+// ic0.cpp:72 ic0_applier(ic0_factorize(A, policy)) applied to r.
+int ref_ic0_apply(uint64_t n, const uint64_t* ro, const uint32_t* ci, const double* v, int policy,
+                  const double* r, double* z) {
+    return guard([&] {
+        PrecondApplier pa = ic0_applier(ic0_factorize(make_csr(n, ro, ci, v),
+                                                      policy ? Ic0Shift::scaled : Ic0Shift::none));
+        pa(std::span<const double>(r, n), std::span<double>(z, n));
+    });
+}
+
+// pcg.cpp:53 pcg_solve with identity (0) / jacobi (1) / factor (2) applier (pcg.cpp:28-51),
+// or (3) ic0_applier(ic0_factorize(A)) as hfp solve --method ic0 (hfp_cli.cpp:80).
 // report_out: {iterations, converged, status(0 conv,1 max,2 breakdown), breakdown_iter,
 //              history_len, wall_ms}
 int ref_pcg_solve(uint64_t n, const uint64_t* ro, const uint32_t* ci, const double* v,
@@ -225,6 +252,7 @@ int ref_pcg_solve(uint64_t n, const uint64_t* ro, const uint32_t* ci, const doub
         PrecondApplier pa;
         if (kind == 0) pa = identity_applier();
         else if (kind == 1) pa = jacobi_applier(A);
+        else if (kind == 3) pa = ic0_applier(ic0_factorize(A));
         else pa = factor_applier(make_factors<float>(n, leaf, ls, packed, spd_enabled, spd_raw), A);
         SolveConfig cfg;
         cfg.rtol = rtol;

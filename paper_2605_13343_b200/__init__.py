@@ -5,9 +5,9 @@ The product is the native library `libhfpg.so` (C ABI in include/hfpg.h, CUDA ke
 csrc/); this package is the Python mirror of the reference interface over that ABI.
 """
 from .api import (Checkpoint, CsrMatrix, Device, FactorInit, FactorLayout, FactorTensor, Frame, GpuFrame,
-                  HPartition, PrecondApplier, RngPurpose, RngStream, SolveConfig, SolveReport,
+                  HPartition, Ic0Factor, Ic0Shift, PrecondApplier, RngPurpose, RngStream, SolveConfig, SolveReport,
                   SolveStatus, TileSpec, ToynetConfig, ToynetTrace, apply, build_partition, clamp_leaf_size, factor_applier,
-                  identity_applier, init_factors, jacobi_applier, make_factor_layout, make_frame,
+                  ic0_applier, ic0_factorize, identity_applier, init_factors, jacobi_applier, make_factor_layout, make_frame,
                   make_frame_3d, packed_width, pcg_solve, read_checkpoint, test_frame_id,
                   toynet_forward, toynet_forward_gpu_frame, train_frame_id, write_checkpoint)
 

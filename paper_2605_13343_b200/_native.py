@@ -101,6 +101,10 @@ _PROTOS = {
     "hfpg_set_precond": (C.c_int, [vp, C.c_int]),
     "hfpg_apply": (C.c_int, [vp, vp, vp, C.c_int]),
     "hfpg_spmv": (C.c_int, [vp, vp, vp, C.c_int]),
+    "hfpg_ic0_factor_host": (C.c_int, [u64, vp, vp, vp, i32, vp, vp, vp, u64, C.POINTER(u64),
+                                       C.POINTER(dbl)]),
+    "hfpg_load_ic0": (C.c_int, [vp, u64, vp, vp, vp]),
+    "hfpg_ic0_apply": (C.c_int, [vp, vp, vp, C.c_int]),
     "hfpg_pcg_solve": (C.c_int, [vp, vp, C.POINTER(SolveConfigC), vp, vp, C.POINTER(ReportC),
                                  C.c_int]),
     "hfpg_set_solver": (C.c_int, [vp, C.c_int]),

@@ -535,6 +535,80 @@ class _Factor(PrecondApplier):
         return self.dev.apply(r)
 
 
+class Ic0Shift(enum.IntEnum):
+    """ic0.hpp:7: scaled factors A + 1e-8 max(diag) I."""
+    none = 0
+    scaled = 1
+
+
+@dataclass
+class Ic0Factor:
+    """ic0.hpp:10-13: the lower factor (pattern = lower triangle of A, diagonal last) + shift."""
+    lower: "CsrMatrix"
+    shift: float = 0.0
+
+
+def ic0_factorize(A: "CsrMatrix", policy: Ic0Shift = Ic0Shift.scaled) -> Ic0Factor:
+    """ic0.cpp:10-69 (host C++ in libhfpg, bit-identical to the reference). Raises ValueError on
+    a non-square matrix and RuntimeError on a nonpositive pivot, like the reference's
+    std::invalid_argument / std::runtime_error."""
+    if A.n_rows != A.n_cols:
+        raise ValueError("ic0_factorize: matrix not square")
+    n = A.n_rows
+    ro = np.ascontiguousarray(A.row_offsets, np.uint64)
+    ci = np.ascontiguousarray(A.col_indices, np.uint32)
+    v = np.ascontiguousarray(A.values, np.float64)
+    cap = int(ro[-1]) + n
+    lro = np.empty(n + 1, np.uint64)
+    lci = np.empty(max(cap, 1), np.uint32)
+    lv = np.empty(max(cap, 1), np.float64)
+    nnz = N.u64()
+    shift = N.dbl()
+    rc = N.lib.hfpg_ic0_factor_host(n, ro.ctypes.data, ci.ctypes.data, v.ctypes.data, int(policy),
+                                    lro.ctypes.data, lci.ctypes.data, lv.ctypes.data, cap,
+                                    N.C.byref(nnz), N.C.byref(shift))
+    N.check(rc)
+    k = int(nnz.value)
+    return Ic0Factor(CsrMatrix(n, n, lro, lci[:k].copy(), lv[:k].copy()), float(shift.value))
+
+
+class _Ic0(PrecondApplier):
+    kind = 3
+    method = "ic0"
+
+    def __init__(self, factor: Ic0Factor, A: "CsrMatrix | None" = None):
+        super().__init__(Device(0))
+        self.factor = factor
+        if A is not None:
+            self.bind(A)
+
+    def bind(self, A: "CsrMatrix") -> Device:
+        if self.dev.csr_id != id(A):
+            self.dev.load_csr(A)
+        L = self.factor.lower
+        lro = np.ascontiguousarray(L.row_offsets, np.uint64)
+        lci = np.ascontiguousarray(L.col_indices, np.uint32)
+        lv = np.ascontiguousarray(L.values, np.float64)
+        N.check(N.lib.hfpg_load_ic0(self.dev.h, L.n_rows, lro.ctypes.data, lci.ctypes.data, lv.ctypes.data))
+        self.dev.set_precond(self.kind)
+        return self.dev
+
+    def __call__(self, r):
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.empty_like(r)
+        if self.dev.csr_id is None:  # a bare applier: the factor alone defines the operator
+            L = self.factor.lower
+            self.bind(CsrMatrix(L.n_rows, L.n_cols, L.row_offsets, L.col_indices, L.values))
+        N.check(N.lib.hfpg_ic0_apply(self.dev.h, r.ctypes.data, z.ctypes.data, N.HOST))
+        return z
+
+
+def ic0_applier(factor: Ic0Factor) -> PrecondApplier:
+    """ic0.cpp:72-99: z = (L L^T)^{-1} r — two sync-free triangular sweeps on the GPU. Bind it
+    to the system (pcg_solve does) to run the device-resident IC(0)-PCG."""
+    return _Ic0(factor)
+
+
 def identity_applier() -> PrecondApplier:
     return _Identity(None)
 

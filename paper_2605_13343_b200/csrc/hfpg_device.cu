@@ -4,6 +4,7 @@
 #include "solve_persistent.cuh"
 #include "partition_host.hpp"
 #include "framegen.cuh"
+#include "ic0.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -80,6 +81,15 @@ struct hfpg_handle {
     uint64_t n = 0;  // system size (CSR, else factors)
     double fro = 0.0;
     bool diag_positive = false;
+    // IC(0) preconditioner (hfpg_load_ic0): lower factor, its transpose, sweep state
+    struct Ic0 {
+        bool have = false;
+        uint64_t n = 0;
+        unsigned long long *lro = nullptr, *tro = nullptr;
+        uint32_t *lci = nullptr, *tci = nullptr;
+        double *lv = nullptr, *tv = nullptr, *y = nullptr;
+        unsigned *fflag = nullptr, *bflag = nullptr, *epoch = nullptr;
+    } ic0;
     unsigned long long* slice_off = nullptr;
     uint32_t* sell_cols = nullptr;
     double* sell_vals = nullptr;
@@ -374,12 +384,33 @@ void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
     CK(cudaGetLastError());
 }
 
+Ic0Dev ic0_dev(const hfpg_handle* h) {
+    const auto& c = h->ic0;
+    return Ic0Dev{c.lro, c.lci, c.lv, c.tro, c.tci, c.tv, c.y, c.fflag, c.bflag, c.epoch};
+}
+// The two sync-free sweeps (ic0.cuh): z = (L L^T)^{-1} rin; mode kApply leaves the scalars alone.
+void launch_ic0_sweeps(hfpg_handle* h, const DevSys& s, int mode, const double* rin, double* zout) {
+    const unsigned g = unsigned((h->n + kIc0Threads - 1) / kIc0Threads);
+    const Ic0Dev d = ic0_dev(h);
+    k_ic0_forward<<<g, kIc0Threads, 0, h->lstream>>>(s, d, rin, mode);
+    CK(cudaGetLastError());
+    k_ic0_backward<<<g, kIc0Threads, 0, h->lstream>>>(s, d, rin, zout, mode);
+    CK(cudaGetLastError());
+}
+void launch_ic0_step(hfpg_handle* h, const DevSys& s, int mode) {
+    k_ic0_update<<<unsigned(simple_grid(h)), 256, 0, h->lstream>>>(s, ic0_dev(h), mode);
+    CK(cudaGetLastError());
+    launch_ic0_sweeps(h, s, mode, h->r, h->z);
+}
+
 void launch_iteration(hfpg_handle* h) {
     const DevSys& s = h->sys;
     launch_spmv<kLoop>(h, s, nullptr, nullptr);
     CK(cudaGetLastError());
     if (h->precond == HFPG_PRECOND_FACTOR) {
         launch_apply(h, kLoop, nullptr, nullptr);
+    } else if (h->precond == HFPG_PRECOND_IC0) {
+        launch_ic0_step(h, s, kLoop);
     } else {
         k_simple<<<unsigned(simple_grid(h)), 256, 0, h->lstream>>>(s, kLoop, h->precond == HFPG_PRECOND_JACOBI);
         CK(cudaGetLastError());
@@ -392,6 +423,8 @@ void launch_init(hfpg_handle* h) {
     CK(cudaGetLastError());
     if (h->precond == HFPG_PRECOND_FACTOR) {
         launch_apply(h, kInit, nullptr, nullptr);
+    } else if (h->precond == HFPG_PRECOND_IC0) {
+        launch_ic0_step(h, s, kInit);
     } else {
         k_simple<<<unsigned(simple_grid(h)), 256, 0, h->lstream>>>(s, kInit, h->precond == HFPG_PRECOND_JACOBI);
         CK(cudaGetLastError());
@@ -867,6 +900,8 @@ int hfpg_destroy(hfpg_handle* h) {
         dfree(h->coupled); dfree(h->node_u); dfree(h->node_v);
         dfree(h->tree_counters); dfree(h->partials); dfree(h->dpart); dfree(h->counters); dfree(h->sc);
         dfree(h->history); dfree(h->gbar); dfree(h->trace);
+        dfree(h->ic0.lro); dfree(h->ic0.lci); dfree(h->ic0.lv); dfree(h->ic0.tro); dfree(h->ic0.tci);
+        dfree(h->ic0.tv); dfree(h->ic0.y); dfree(h->ic0.fflag); dfree(h->ic0.bflag); dfree(h->ic0.epoch);
         if (h->sc_host) cudaFreeHost(h->sc_host);
         {
             auto& F = h->fr;
@@ -1035,7 +1070,9 @@ int hfpg_load_factors(hfpg_handle* h, uint64_t n, uint64_t leaf, uint64_t ls, co
 
 int hfpg_set_precond(hfpg_handle* h, int kind) {
     return guarded([&] {
-        if (kind < 0 || kind > 2) throw InvalidArgument("set_precond: unknown kind");
+        if (kind < 0 || kind > 3) throw InvalidArgument("set_precond: unknown kind");
+        if (kind == HFPG_PRECOND_IC0 && (!h->ic0.have || h->ic0.n != h->n || !h->have_csr))
+            throw InvalidArgument("ic0_applier: no IC(0) factor of the loaded matrix (hfpg_load_ic0)");
         if (kind == HFPG_PRECOND_JACOBI) {
             if (!h->have_csr) throw InvalidArgument("jacobi_applier: no matrix loaded");
             if (!h->diag_positive)
@@ -1165,7 +1202,7 @@ int hfpg_launch_counts(hfpg_handle* h, uint32_t* per_iteration, uint32_t* per_ap
     return guarded([&] {
         const uint32_t apply = (h->have_factors && h->fast) ? 4 : 3;
         *per_apply = apply;
-        *per_iteration = h->precond == HFPG_PRECOND_FACTOR ? apply + 1 : 2;
+        *per_iteration = h->precond == HFPG_PRECOND_FACTOR ? apply + 1 : h->precond == HFPG_PRECOND_IC0 ? 4 : 2;
         if (use_persistent(h)) {  // one k_solve launch per solve
             *per_apply = 0;
             *per_iteration = 0;
@@ -1585,6 +1622,92 @@ int hfpg_group_apply(hfpg_handle* const* hs, uint32_t G, const double* r_in, dou
             CK(cudaMemcpyAsync(z_out + r * nl, hs[r]->z, nl * 8, cudaMemcpyDeviceToHost, h0->stream));
         }
         CK(cudaStreamSynchronize(h0->stream));
+    });
+}
+
+
+// ---- IC(0) (ic0.cpp) ------------------------------------------------------------------------
+int hfpg_ic0_factor_host(uint64_t n, const uint64_t* ro, const uint32_t* ci, const double* v, int32_t policy,
+                         uint64_t* lro, uint32_t* lci, double* lv, uint64_t cap, uint64_t* nnz_out,
+                         double* shift_out) {
+    return guarded([&] {
+        std::vector<uint64_t> r;
+        std::vector<uint32_t> c;
+        std::vector<double> x;
+        double shift = 0.0;
+        ic0_factorize_host(n, ro, ci, v, policy, r, c, x, shift);
+        *nnz_out = c.size();
+        if (shift_out) *shift_out = shift;
+        if (cap < c.size()) throw InvalidArgument("ic0_factor_host: output capacity below nnz(L)");
+        std::memcpy(lro, r.data(), (n + 1) * 8);
+        std::memcpy(lci, c.data(), c.size() * 4);
+        std::memcpy(lv, x.data(), x.size() * 8);
+    });
+}
+
+int hfpg_load_ic0(hfpg_handle* h, uint64_t n, const uint64_t* lro, const uint32_t* lci, const double* lv) {
+    return guarded([&] {
+        set_device(h);
+        if (h->part.G > 1) throw InvalidArgument("load_ic0: partitioned handle");
+        if (n == 0 || lro[0] != 0) throw InvalidArgument("load_ic0: bad lower factor");
+        for (uint64_t i = 0; i < n; ++i)  // rows nonempty, diagonal last, strictly lower before it
+            if (lro[i + 1] <= lro[i] || lci[lro[i + 1] - 1] != i)
+                throw InvalidArgument("load_ic0: row " + std::to_string(i) + " does not end with its diagonal");
+        const uint64_t nnz = lro[n];
+        for (uint64_t i = 0; i < n; ++i)
+            for (uint64_t p = lro[i]; p + 1 < lro[i + 1]; ++p)
+                if (lci[p] >= i) throw InvalidArgument("load_ic0: entry above the diagonal");
+        std::vector<uint64_t> vr(lro, lro + n + 1), tro;
+        std::vector<uint32_t> vc(lci, lci + nnz), tci;
+        std::vector<double> vv(lv, lv + nnz), tv;
+        ic0_transpose_host(n, vr, vc, vv, tro, tci, tv);
+        invalidate_graph(h);
+        auto& c = h->ic0;
+        dalloc(c.lro, n + 1);
+        dalloc(c.lci, nnz);
+        dalloc(c.lv, nnz);
+        dalloc(c.tro, n + 1);
+        dalloc(c.tci, std::max<uint64_t>(tci.size(), 1));
+        dalloc(c.tv, std::max<uint64_t>(tv.size(), 1));
+        dalloc(c.y, n);
+        dalloc(c.fflag, n);
+        dalloc(c.bflag, n);
+        dalloc(c.epoch, 1);
+        CK(cudaMemcpy(c.lro, vr.data(), (n + 1) * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c.lci, vc.data(), nnz * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c.lv, vv.data(), nnz * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c.tro, tro.data(), (n + 1) * 8, cudaMemcpyHostToDevice));
+        if (!tci.empty()) {
+            CK(cudaMemcpy(c.tci, tci.data(), tci.size() * 4, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(c.tv, tv.data(), tv.size() * 8, cudaMemcpyHostToDevice));
+        }
+        CK(cudaMemset(c.fflag, 0, n * 4));
+        CK(cudaMemset(c.bflag, 0, n * 4));
+        CK(cudaMemset(c.epoch, 0, 4));
+        c.n = n;
+        c.have = true;
+    });
+}
+
+int hfpg_ic0_apply(hfpg_handle* h, const double* r, double* z, int where) {
+    return guarded([&] {
+        set_device(h);
+        if (!h->ic0.have || !h->have_csr || h->ic0.n != h->n) throw InvalidArgument("ic0_apply: no IC(0) factor loaded");
+        ensure_workspace(h);
+        fill_sys(h);
+        const double* rin = r;
+        double* zout = z;
+        if (where == HFPG_HOST) {
+            copy_in(h, h->scratch, r, h->n, HFPG_HOST);
+            rin = h->scratch;
+            zout = h->z;
+        }
+        h->lstream = h->stream;
+        k_ic0_bump<<<1, 1, 0, h->stream>>>(ic0_dev(h));
+        CK(cudaGetLastError());
+        launch_ic0_sweeps(h, h->sys, kApply, rin, zout);
+        if (where == HFPG_HOST) copy_out(h, z, h->z, h->n, HFPG_HOST);
+        CK(cudaStreamSynchronize(h->stream));
     });
 }
 

@@ -26,6 +26,14 @@ struct CudaError : std::runtime_error {
 
 void set_error(const std::string& msg);
 
+// ic0_host.cpp (ic0.cpp:10-69): lower IC(0) factor of A (policy 0 none, 1 scaled); its transpose.
+void ic0_factorize_host(uint64_t n, const uint64_t* ro, const uint32_t* ci, const double* v, int policy,
+                        std::vector<uint64_t>& lro, std::vector<uint32_t>& lci, std::vector<double>& lv,
+                        double& shift);
+void ic0_transpose_host(uint64_t n, const std::vector<uint64_t>& lro, const std::vector<uint32_t>& lci,
+                        const std::vector<double>& lv, std::vector<uint64_t>& tro, std::vector<uint32_t>& tci,
+                        std::vector<double>& tv);
+
 // Runs f(), maps exceptions to status codes and records the message.
 template <class F>
 int guarded(F&& f) {
