@@ -88,7 +88,8 @@ struct hfpg_handle {
         unsigned long long *lro = nullptr, *tro = nullptr;
         uint32_t *lci = nullptr, *tci = nullptr;
         double *lv = nullptr, *tv = nullptr, *y = nullptr;
-        unsigned *fflag = nullptr, *bflag = nullptr, *epoch = nullptr;
+        uint32_t *fperm = nullptr, *bperm = nullptr;
+        uint32_t flevels = 0, blevels = 0;
     } ic0;
     unsigned long long* slice_off = nullptr;
     uint32_t* sell_cols = nullptr;
@@ -386,7 +387,7 @@ void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
 
 Ic0Dev ic0_dev(const hfpg_handle* h) {
     const auto& c = h->ic0;
-    return Ic0Dev{c.lro, c.lci, c.lv, c.tro, c.tci, c.tv, c.y, c.fflag, c.bflag, c.epoch};
+    return Ic0Dev{c.lro, c.lci, c.lv, c.tro, c.tci, c.tv, c.y, c.fperm, c.bperm};
 }
 // The two sync-free sweeps (ic0.cuh): z = (L L^T)^{-1} rin; mode kApply leaves the scalars alone.
 void launch_ic0_sweeps(hfpg_handle* h, const DevSys& s, int mode, const double* rin, double* zout) {
@@ -901,7 +902,8 @@ int hfpg_destroy(hfpg_handle* h) {
         dfree(h->tree_counters); dfree(h->partials); dfree(h->dpart); dfree(h->counters); dfree(h->sc);
         dfree(h->history); dfree(h->gbar); dfree(h->trace);
         dfree(h->ic0.lro); dfree(h->ic0.lci); dfree(h->ic0.lv); dfree(h->ic0.tro); dfree(h->ic0.tci);
-        dfree(h->ic0.tv); dfree(h->ic0.y); dfree(h->ic0.fflag); dfree(h->ic0.bflag); dfree(h->ic0.epoch);
+        dfree(h->ic0.tv); dfree(h->ic0.y);
+        dfree(h->ic0.fperm); dfree(h->ic0.bperm);
         if (h->sc_host) cudaFreeHost(h->sc_host);
         {
             auto& F = h->fr;
@@ -1661,6 +1663,9 @@ int hfpg_load_ic0(hfpg_handle* h, uint64_t n, const uint64_t* lro, const uint32_
         std::vector<uint32_t> vc(lci, lci + nnz), tci;
         std::vector<double> vv(lv, lv + nnz), tv;
         ic0_transpose_host(n, vr, vc, vv, tro, tci, tv);
+        std::vector<uint32_t> fperm, bperm;
+        uint32_t fl = 0, bl = 0;
+        ic0_levels_host(n, vr, vc, tro, tci, fperm, bperm, fl, bl);
         invalidate_graph(h);
         auto& c = h->ic0;
         dalloc(c.lro, n + 1);
@@ -1670,9 +1675,12 @@ int hfpg_load_ic0(hfpg_handle* h, uint64_t n, const uint64_t* lro, const uint32_
         dalloc(c.tci, std::max<uint64_t>(tci.size(), 1));
         dalloc(c.tv, std::max<uint64_t>(tv.size(), 1));
         dalloc(c.y, n);
-        dalloc(c.fflag, n);
-        dalloc(c.bflag, n);
-        dalloc(c.epoch, 1);
+        dalloc(c.fperm, n);
+        dalloc(c.bperm, n);
+        CK(cudaMemcpy(c.fperm, fperm.data(), n * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c.bperm, bperm.data(), n * 4, cudaMemcpyHostToDevice));
+        c.flevels = fl;
+        c.blevels = bl;
         CK(cudaMemcpy(c.lro, vr.data(), (n + 1) * 8, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(c.lci, vc.data(), nnz * 4, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(c.lv, vv.data(), nnz * 8, cudaMemcpyHostToDevice));
@@ -1681,9 +1689,6 @@ int hfpg_load_ic0(hfpg_handle* h, uint64_t n, const uint64_t* lro, const uint32_
             CK(cudaMemcpy(c.tci, tci.data(), tci.size() * 4, cudaMemcpyHostToDevice));
             CK(cudaMemcpy(c.tv, tv.data(), tv.size() * 8, cudaMemcpyHostToDevice));
         }
-        CK(cudaMemset(c.fflag, 0, n * 4));
-        CK(cudaMemset(c.bflag, 0, n * 4));
-        CK(cudaMemset(c.epoch, 0, 4));
         c.n = n;
         c.have = true;
     });
@@ -1703,7 +1708,7 @@ int hfpg_ic0_apply(hfpg_handle* h, const double* r, double* z, int where) {
             zout = h->z;
         }
         h->lstream = h->stream;
-        k_ic0_bump<<<1, 1, 0, h->stream>>>(ic0_dev(h));
+        k_ic0_pending<<<unsigned(simple_grid(h)), 256, 0, h->stream>>>(ic0_dev(h), zout, h->n);
         CK(cudaGetLastError());
         launch_ic0_sweeps(h, h->sys, kApply, rin, zout);
         if (where == HFPG_HOST) copy_out(h, z, h->z, h->n, HFPG_HOST);

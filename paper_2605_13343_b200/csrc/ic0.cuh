@@ -1,15 +1,15 @@
 // IC(0) preconditioner apply on sm_100a (ic0.cpp:72-99, ic0_applier): z = (L L^T)^{-1} r by a
 // forward sweep L y = r and a backward sweep L^T z = y, each a sync-free triangular solve.
 //
-// One thread per row. A row waits, per dependency, for that row's ready flag (ld.acquire, the
-// writer publishes value then flag with st.release), then accumulates exactly as the reference:
+// One thread per row, rows handed out in dependency-level order (fperm / bperm,
+// ic0_levels_host). A row polls its dependencies' values until they are no longer pending (the
+// value word is the ready flag, see kIc0Pending), then accumulates exactly as the reference:
 //   forward   y_i = (r_i - sum_p L_ip y_p) / L_ii, p ascending          (ic0.cpp:80-86)
 //   backward  z_j = (y_j - sum_i L_ij z_i) / L_jj, i DESCENDING          (ic0.cpp:88-95)
-// with the reference build's rounding of each product and difference and IEEE division, so y and z are
-// bit-identical to the reference's (the pinned reference build, oracle/_ref: vmulsd + vsubsd in
-// the forward loop, vfnmadd in the backward scatter). Flags carry an epoch (bumped once per apply), so they are
-// never reset. Deadlock freedom: every dependency of a row lives in a CTA of lower index (the
-// backward sweep numbers its CTAs from the last row), and CTAs are dispatched in index order.
+// with the pinned reference build's rounding (oracle/_ref: vmulsd + vsubsd in the forward loop,
+// vfnmadd in the backward scatter) and IEEE division, so y and z are bit-identical to it.
+// Deadlock freedom: every dependency of a row sits earlier in the level order, so in a CTA of
+// lower (or the same) index, and CTAs are dispatched in index order.
 // For a 7-point stencil in Morton order the dependency depth is nx + ny + nz - 2 levels.
 #pragma once
 
@@ -24,57 +24,89 @@ struct Ic0Dev {
     const unsigned long long* tro;  // strictly-lower L transposed, rows in decreasing order
     const uint32_t* tci;
     const double* tv;
-    double* y;         // forward-sweep result
-    unsigned* fflag;   // per-row ready epochs, forward / backward
-    unsigned* bflag;
-    unsigned* epoch;   // current apply's epoch (device word)
+    double* y;                      // forward-sweep result
+    const uint32_t* fperm;          // rows in forward / backward dependency-level order
+    const uint32_t* bperm;
 };
 constexpr int kIc0Threads = 128;
+// "Not yet computed": a NaN payload no arithmetic produces (a computed value with these bits is
+// stored as the canonical NaN instead). The value word is its own ready flag: one relaxed 64-bit
+// store publishes it, one polled load receives it — no separate flag, fence or second load.
+constexpr unsigned long long kIc0Pending = 0x7FF4DEAD0C0FFEE1ULL;
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const double* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_f64(double* p, double x) {
+    unsigned long long v = __double_as_longlong(x);
+    if (v == kIc0Pending) v = 0x7FFFFFFFFFFFFFFFULL;
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void ic0_wait(const unsigned* flag, unsigned e) {
-    while (ld_acquire_u32(flag) != e) __nanosleep(20);
+__device__ __forceinline__ double ic0_get(const double* p) {
+    unsigned long long v = ld_relaxed_u64(p);
+    while (v == kIc0Pending) v = ld_relaxed_u64(p);
+    return __longlong_as_double(v);
+}
+// Gather up to 8 dependency values at once (one round trip when they are ready), in order.
+template <class Idx>
+__device__ __forceinline__ int ic0_gather8(const double* src, Idx idx, int cnt, double (&v)[8]) {
+    unsigned long long raw[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (k < cnt) raw[k] = ld_relaxed_u64(src + idx(k));
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (k < cnt) {
+            while (raw[k] == kIc0Pending) raw[k] = ld_relaxed_u64(src + idx(k));
+            v[k] = __longlong_as_double(raw[k]);
+        }
+    return cnt;
 }
 
 // Forward sweep: y = L^{-1} rin.
-__device__ __forceinline__ void ic0_forward_row(const Ic0Dev& d, const double* rin, uint64_t i, unsigned e) {
+__device__ __forceinline__ void ic0_forward_row(const Ic0Dev& d, const double* rin, uint64_t i) {
     const uint64_t beg = d.lro[i], end = d.lro[i + 1] - 1;
     double s = rin[i];
-    for (uint64_t p = beg; p < end; ++p) {
-        const uint32_t j = d.lci[p];
-        ic0_wait(&d.fflag[j], e);
-        s = __dsub_rn(s, __dmul_rn(d.lv[p], __ldcg(&d.y[j])));  // the reference build does not contract this one
+    for (uint64_t p0 = beg; p0 < end; p0 += 8) {
+        const int cnt = int(end - p0 < 8 ? end - p0 : 8);
+        double v[8];
+        ic0_gather8(d.y, [&](int k) { return d.lci[p0 + k]; }, cnt, v);
+        for (int k = 0; k < cnt; ++k)
+            s = __dsub_rn(s, __dmul_rn(d.lv[p0 + k], v[k]));  // the reference build does not contract this one
     }
-    const double yi = s / d.lv[end];
-    __stcg(&d.y[i], yi);
-    st_release_u32(&d.fflag[i], e);
+    st_relaxed_f64(&d.y[i], s / d.lv[end]);
 }
 // Backward sweep: z = L^{-T} y.
-__device__ __forceinline__ double ic0_backward_row(const Ic0Dev& d, double* z, uint64_t j, unsigned e) {
+__device__ __forceinline__ double ic0_backward_row(const Ic0Dev& d, double* z, uint64_t j) {
     double s = __ldcg(&d.y[j]);
-    for (uint64_t q = d.tro[j]; q < d.tro[j + 1]; ++q) {
-        const uint32_t i = d.tci[q];
-        ic0_wait(&d.bflag[i], e);
-        s = fma(-d.tv[q], __ldcg(&z[i]), s);
+    const uint64_t q0 = d.tro[j], q1 = d.tro[j + 1];
+    for (uint64_t q = q0; q < q1; q += 8) {
+        const int cnt = int(q1 - q < 8 ? q1 - q : 8);
+        double v[8];
+        ic0_gather8(z, [&](int k) { return d.tci[q + k]; }, cnt, v);
+        for (int k = 0; k < cnt; ++k) s = fma(-d.tv[q + k], v[k], s);
     }
     const double zj = s / d.lv[d.lro[j + 1] - 1];
-    __stcg(&z[j], zj);
-    st_release_u32(&d.bflag[j], e);
+    st_relaxed_f64(&z[j], zj);
     return zj;
 }
 
-__global__ void k_ic0_bump(Ic0Dev d) { *d.epoch += 1u; }
+// Mark y and z pending (before a pair of sweeps).
+__device__ __forceinline__ void ic0_mark_pending(const Ic0Dev& d, double* z, uint64_t n) {
+    const double pend = __longlong_as_double((long long)kIc0Pending);
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        d.y[i] = pend;
+        z[i] = pend;
+    }
+}
+__global__ void k_ic0_pending(Ic0Dev d, double* z, uint64_t n) { ic0_mark_pending(d, z, n); }
+
 
 // PCG with IC(0), stage 1: x += alpha p, r -= alpha Ap and |r|^2 (pcg.cpp:97-101; k_simple's
-// arithmetic), r0 at init; the last CTA finishes the residual bookkeeping and opens the next
-// apply's epoch.
+// arithmetic), r0 at init, y and z marked pending; the last CTA finishes the residual
+// bookkeeping.
 __global__ void __launch_bounds__(256) k_ic0_update(DevSys s, Ic0Dev d, int mode) {
     if (s.sc->done) return;
     const double alpha = mode == kLoop ? s.sc->alpha : 0.0;
@@ -85,18 +117,16 @@ __global__ void __launch_bounds__(256) k_ic0_update(DevSys s, Ic0Dev d, int mode
         const double rv = mode == kLoop ? update_row(s, pcur, alpha, i) : s.r[i];
         v[0] = fma(rv, rv, v[0]);
     }
+    ic0_mark_pending(d, s.z, s.n);
     double tot[1];
-    if (grid_reduce_last<1>(v, s.partials, &s.counters[3], tot) && threadIdx.x == 0) {
+    if (grid_reduce_last<1>(v, s.partials, &s.counters[3], tot) && threadIdx.x == 0)
         leaf_epilogue(s, mode, tot[0]);  // r0 (init) or rel / history / stop
-        *d.epoch += 1u;
-    }
 }
 
 __global__ void __launch_bounds__(kIc0Threads) k_ic0_forward(DevSys s, Ic0Dev d, const double* rin, int mode) {
     if (mode != kApply && s.sc->done) return;
-    const unsigned e = *d.epoch;
-    const uint64_t i = uint64_t(blockIdx.x) * kIc0Threads + threadIdx.x;
-    if (i < s.n) ic0_forward_row(d, rin, i, e);
+    const uint64_t t = uint64_t(blockIdx.x) * kIc0Threads + threadIdx.x;
+    if (t < s.n) ic0_forward_row(d, rin, d.fperm[t]);
 }
 
 // Stage 3 (and the standalone apply): the backward sweep into z, then r.z, beta and the
@@ -104,12 +134,11 @@ __global__ void __launch_bounds__(kIc0Threads) k_ic0_forward(DevSys s, Ic0Dev d,
 __global__ void __launch_bounds__(kIc0Threads) k_ic0_backward(DevSys s, Ic0Dev d, const double* rin, double* zout,
                                                               int mode) {
     if (prolong_skip(s, mode)) return;
-    const unsigned e = *d.epoch;
     const uint64_t t = uint64_t(blockIdx.x) * kIc0Threads + threadIdx.x;
     double v[1] = {0.0};
     if (t < s.n) {
-        const uint64_t j = s.n - 1 - t;
-        const double zj = ic0_backward_row(d, zout, j, e);
+        const uint64_t j = d.bperm[t];
+        const double zj = ic0_backward_row(d, zout, j);
         v[0] = rin[j] * zj;
     }
     if (mode == kApply) return;

@@ -101,4 +101,39 @@ void ic0_transpose_host(uint64_t n, const std::vector<uint64_t>& lro, const std:
         }
 }
 
+// Level schedules of the two sweeps: perm lists the rows by dependency level (stable in row
+// order). Forward: level(i) = 1 + max level(j) over the strictly-lower entries j of row i.
+// Backward: level(j) = 1 + max level(i) over the rows i > j with L_ij != 0. A sync-free sweep
+// that hands out rows in this order has every dependency earlier in the list, so a row's
+// producers are dispatched before it and the wait per row is one hand-off, not a CTA turnover.
+void ic0_levels_host(uint64_t n, const std::vector<uint64_t>& lro, const std::vector<uint32_t>& lci,
+                     const std::vector<uint64_t>& tro, const std::vector<uint32_t>& tci,
+                     std::vector<uint32_t>& fperm, std::vector<uint32_t>& bperm, uint32_t& flevels,
+                     uint32_t& blevels) {
+    std::vector<uint32_t> lev(n, 0);
+    flevels = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        uint32_t l = 0;
+        for (uint64_t p = lro[i]; p + 1 < lro[i + 1]; ++p) l = std::max(l, lev[lci[p]] + 1);
+        lev[i] = l;
+        flevels = std::max(flevels, l + 1);
+    }
+    auto order = [&](std::vector<uint32_t>& perm, uint32_t nlev) {
+        std::vector<uint64_t> cnt(uint64_t(nlev) + 1, 0);
+        for (uint64_t i = 0; i < n; ++i) ++cnt[lev[i] + 1];
+        for (uint32_t l = 0; l < nlev; ++l) cnt[l + 1] += cnt[l];
+        perm.assign(n, 0);
+        for (uint64_t i = 0; i < n; ++i) perm[cnt[lev[i]]++] = uint32_t(i);
+    };
+    order(fperm, flevels);
+    blevels = 0;
+    for (uint64_t j = n; j-- > 0;) {
+        uint32_t l = 0;
+        for (uint64_t q = tro[j]; q < tro[j + 1]; ++q) l = std::max(l, lev[tci[q]] + 1);
+        lev[j] = l;  // rows i > j already hold their backward levels
+        blevels = std::max(blevels, l + 1);
+    }
+    order(bperm, blevels);
+}
+
 }  // namespace hfpg

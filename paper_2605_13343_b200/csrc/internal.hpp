@@ -33,6 +33,10 @@ void ic0_factorize_host(uint64_t n, const uint64_t* ro, const uint32_t* ci, cons
 void ic0_transpose_host(uint64_t n, const std::vector<uint64_t>& lro, const std::vector<uint32_t>& lci,
                         const std::vector<double>& lv, std::vector<uint64_t>& tro, std::vector<uint32_t>& tci,
                         std::vector<double>& tv);
+void ic0_levels_host(uint64_t n, const std::vector<uint64_t>& lro, const std::vector<uint32_t>& lci,
+                     const std::vector<uint64_t>& tro, const std::vector<uint32_t>& tci,
+                     std::vector<uint32_t>& fperm, std::vector<uint32_t>& bperm, uint32_t& flevels,
+                     uint32_t& blevels);
 
 // Runs f(), maps exceptions to status codes and records the message.
 template <class F>
