@@ -211,6 +211,34 @@ int hfpg_get_trace(hfpg_handle* h, uint64_t* out, uint32_t cap);
 
 /* apply.cpp:79-174 apply<float>: z = M r with the loaded factors and diag(A). */
 int hfpg_apply(hfpg_handle* h, const double* r, double* z, int where);
+/* ---- on-disk formats (mppf.hpp / checkpoint.hpp) ----
+ * zlib crc32 of `bytes` at data: HFPG_DEVICE computes it on the GPU (parallel CRC by
+ * polynomial combination, bit-identical to zlib), HFPG_HOST with zlib. */
+int hfpg_crc32(hfpg_handle* h, const void* data, uint64_t bytes, int where, uint32_t* out);
+/* checkpoint.cpp:45-85 read_checkpoint straight into the handle's factor tensor: the payload is
+ * streamed through pinned buffers into device memory and its crc32 checked on the GPU. Same
+ * errors as hfpg_read_checkpoint; afterwards as hfpg_load_factors. */
+int hfpg_load_checkpoint(hfpg_handle* h, const char* path);
+/* A host frame from arrays (e.g. to write one): barriers as in hfpg_frame_meta; cell_order may
+ * be NULL. Free with hfpg_frame_free. */
+int hfpg_frame_create(uint64_t n, uint64_t width, uint64_t height, uint64_t depth, uint64_t master_seed,
+                      uint64_t frame_index, double rho_heavy, uint32_t nbarriers, const double* barriers,
+                      const uint32_t* cell_order, const double* rho, const uint64_t* row_offsets,
+                      const uint32_t* col_indices, const double* values, const double* b, hfpg_frame** out);
+/* mppf.cpp:48-100 write_mppf of a host frame (2D frames only, as MPPF v1). */
+int hfpg_write_mppf(const hfpg_frame* f, const char* path);
+/* mppf.cpp:102-177 read_mppf into a host frame: checksums, CSR invariants incl. symmetry
+ * (std::invalid_argument -> HFPG_EINVAL), section sizes, Morton cell order. */
+int hfpg_read_mppf(const char* path, hfpg_frame** out);
+/* The frame's seeds and barriers (frame.hpp:34-37): barriers[4i..4i+3] = orientation, center,
+ * thickness, gap for i < min(*nbarriers, cap). */
+int hfpg_frame_meta(const hfpg_frame* f, uint64_t* master_seed, uint64_t* frame_index, uint32_t* nbarriers,
+                    double* barriers, uint32_t cap);
+/* read_mppf on the device: sections streamed into device memory through pinned buffers, every
+ * checksum and the CSR invariants (symmetry included) checked on the GPU, Morton order on the GPU;
+ * the frame becomes the handle's system and GPU frame (hfpg_frame_gpu_view / _copy). */
+int hfpg_load_mppf(hfpg_handle* h, const char* path);
+
 /* ---- IC(0) baseline (ic0.hpp / ic0.cpp) ----
  * ic0.cpp:10-69 ic0_factorize on the host (no device needed): the lower factor L of A (pattern =
  * lower triangle of A, diagonal last; policy 0 = Ic0Shift::none, 1 = Ic0Shift::scaled, shift

@@ -188,6 +188,30 @@ class Ref(_Base):
         h = self.lib.ref_frame_create(n, seed, frame_index)
         if not h:
             raise ValueError(self.lib.ref_last_error().decode())
+        return self._frame_dict(h)
+
+    def write_mppf(self, n: int, seed: int, frame_index: int, path: str) -> None:
+        """mppf.cpp:48 write_mppf(make_frame(n, seed, frame_index), path)."""
+        f = self._f("write_mppf")
+        f.argtypes = [_u64, _u64, _u64, C.c_char_p]
+        _check(f(n, seed, frame_index, path.encode()), self.lib, "write_mppf")
+
+    def read_mppf(self, path: str) -> dict:
+        """mppf.cpp:102 read_mppf -> dict of numpy arrays (+ seeds, barriers)."""
+        self.lib.ref_read_mppf.restype = _p
+        self.lib.ref_read_mppf.argtypes = [C.c_char_p]
+        h = self.lib.ref_read_mppf(path.encode())
+        if not h:
+            raise ValueError(self.lib.ref_last_error().decode())
+        seed, fidx, nb = _u64(), _u64(), C.c_uint32()
+        bars = np.zeros(12)
+        self.lib.ref_frame_meta(_p(h), C.byref(seed), C.byref(fidx), C.byref(nb), _ptr(bars))
+        fr = self._frame_dict(h)
+        fr.update(master_seed=seed.value, frame_index=fidx.value,
+                  barriers=[tuple(bars[4 * i:4 * i + 4]) for i in range(nb.value)])
+        return fr
+
+    def _frame_dict(self, h) -> dict:
         nn, nnz, w, hh = _u64(), _u64(), _u64(), _u64()
         rh = C.c_double()
         self.lib.ref_frame_sizes(_p(h), C.byref(nn), C.byref(nnz), C.byref(w), C.byref(hh),

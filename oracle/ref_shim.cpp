@@ -15,6 +15,7 @@
 #include "hfp/factor_tensor.hpp"
 #include "hfp/frame.hpp"
 #include "hfp/ic0.hpp"
+#include "hfp/mppf.hpp"
 #include "hfp/morton.hpp"
 #include "hfp/partition.hpp"
 #include "hfp/pcg.hpp"
@@ -153,6 +154,29 @@ void ref_frame_fill(void* h, uint32_t* cell_order, double* rho, uint64_t* row_of
     if (b) std::memcpy(b, f.b.data(), f.n * 8);
 }
 void ref_frame_free(void* h) { delete static_cast<RefFrame*>(h); }
+
+// mppf.cpp:48 write_mppf of make_frame(n, seed, frame_index); mppf.cpp:102 read_mppf -> a frame
+// handle for ref_frame_sizes / ref_frame_fill / ref_frame_barriers.
+int ref_write_mppf(uint64_t n, uint64_t seed, uint64_t frame_index, const char* path) {
+    return guard([&] { write_mppf(make_frame(n, seed, frame_index), path); });
+}
+void* ref_read_mppf(const char* path) {
+    RefFrame* r = nullptr;
+    int rc = guard([&] { r = new RefFrame{read_mppf(path)}; });
+    return rc == 0 ? r : nullptr;
+}
+void ref_frame_meta(void* h, uint64_t* seed, uint64_t* frame_index, uint32_t* nbar, double* bars) {
+    auto* r = static_cast<RefFrame*>(h);
+    *seed = r->f.master_seed;
+    *frame_index = r->f.frame_index;
+    *nbar = uint32_t(r->f.barriers.size());
+    for (size_t i = 0; i < r->f.barriers.size() && i < 3; ++i) {
+        bars[4 * i + 0] = double(static_cast<int>(r->f.barriers[i].orientation));
+        bars[4 * i + 1] = r->f.barriers[i].center;
+        bars[4 * i + 2] = r->f.barriers[i].thickness;
+        bars[4 * i + 3] = double(static_cast<int>(r->f.barriers[i].gap));
+    }
+}
 
 // csr.cpp:70 spmv
 int ref_spmv(uint64_t n, const uint64_t* ro, const uint32_t* ci, const double* v,

@@ -8,8 +8,8 @@ from .api import (Checkpoint, CsrMatrix, Device, FactorInit, FactorLayout, Facto
                   HPartition, Ic0Factor, Ic0Shift, PrecondApplier, RngPurpose, RngStream, SolveConfig, SolveReport,
                   SolveStatus, TileSpec, ToynetConfig, ToynetTrace, apply, build_partition, clamp_leaf_size, factor_applier,
                   ic0_applier, ic0_factorize, identity_applier, init_factors, jacobi_applier, make_factor_layout, make_frame,
-                  make_frame_3d, packed_width, pcg_solve, read_checkpoint, test_frame_id,
-                  toynet_forward, toynet_forward_gpu_frame, train_frame_id, write_checkpoint)
+                  make_frame_3d, packed_width, pcg_solve, read_checkpoint, read_mppf, test_frame_id,
+                  toynet_forward, toynet_forward_gpu_frame, train_frame_id, write_checkpoint, write_mppf)
 
 from .partition import PartitionGroup, RankSolver  # noqa: E402
 

@@ -104,6 +104,14 @@ _PROTOS = {
     "hfpg_ic0_factor_host": (C.c_int, [u64, vp, vp, vp, i32, vp, vp, vp, u64, C.POINTER(u64),
                                        C.POINTER(dbl)]),
     "hfpg_load_ic0": (C.c_int, [vp, u64, vp, vp, vp]),
+    "hfpg_crc32": (C.c_int, [vp, vp, u64, C.c_int, C.POINTER(C.c_uint32)]),
+    "hfpg_load_checkpoint": (C.c_int, [vp, C.c_char_p]),
+    "hfpg_write_mppf": (C.c_int, [vp, C.c_char_p]),
+    "hfpg_read_mppf": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "hfpg_frame_meta": (C.c_int, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(C.c_uint32), vp, C.c_uint32]),
+    "hfpg_frame_create": (C.c_int, [u64, u64, u64, u64, u64, u64, dbl, C.c_uint32, vp, vp, vp, vp, vp, vp, vp,
+                                    C.POINTER(vp)]),
+    "hfpg_load_mppf": (C.c_int, [vp, C.c_char_p]),
     "hfpg_ic0_apply": (C.c_int, [vp, vp, vp, C.c_int]),
     "hfpg_pcg_solve": (C.c_int, [vp, vp, C.POINTER(SolveConfigC), vp, vp, C.POINTER(ReportC),
                                  C.c_int]),

@@ -257,6 +257,7 @@ class Frame:
     rho_heavy: float
     master_seed: int = 0
     frame_index: int = 0
+    barriers: list = field(default_factory=list)  # frame.hpp:37: (orientation, center, thickness, gap)
 
 
 def _frame_from_handle(h, seed, fidx) -> Frame:
@@ -272,9 +273,43 @@ def _frame_from_handle(h, seed, fidx) -> Frame:
     b = np.empty(n.value)
     check(lib.hfpg_frame_copy(h, co.ctypes.data, rho.ctypes.data, ro.ctypes.data,
                               ci.ctypes.data, v.ctypes.data, b.ctypes.data))
+    sd, fi, nb = N.u64(), N.u64(), C.c_uint32()
+    bars = np.zeros(4 * 8)
+    check(lib.hfpg_frame_meta(h, C.byref(sd), C.byref(fi), C.byref(nb), bars.ctypes.data, 8))
     lib.hfpg_frame_free(h)
+    seed = sd.value if seed is None else seed
+    fidx = fi.value if fidx is None else fidx
     return Frame(n.value, w.value, hh.value, d.value, co, rho,
-                 CsrMatrix(n.value, n.value, ro, ci, v), b, rh.value, seed, fidx)
+                 CsrMatrix(n.value, n.value, ro, ci, v), b, rh.value, seed, fidx,
+                 [tuple(float(x) for x in bars[4 * i:4 * i + 4]) for i in range(min(nb.value, 8))])
+
+
+def write_mppf(frame: Frame, path: str) -> None:
+    """mppf.cpp:48-100 (MPPF v1; per-section zlib crc32; 2D frames)."""
+    bars = np.array([x for bar in frame.barriers for x in bar], np.float64) if frame.barriers else np.zeros(1)
+    co = np.ascontiguousarray(frame.cell_order, np.uint32)
+    rho = np.ascontiguousarray(frame.rho, np.float64)
+    ro = np.ascontiguousarray(frame.A.row_offsets, np.uint64)
+    ci = np.ascontiguousarray(frame.A.col_indices, np.uint32)
+    v = np.ascontiguousarray(frame.A.values, np.float64)
+    b = np.ascontiguousarray(frame.b, np.float64)
+    h = N.vp()
+    check(lib.hfpg_frame_create(frame.n, frame.width, frame.height, frame.depth, frame.master_seed,
+                                frame.frame_index, frame.rho_heavy, len(frame.barriers), bars.ctypes.data,
+                                co.ctypes.data, rho.ctypes.data, ro.ctypes.data, ci.ctypes.data, v.ctypes.data,
+                                b.ctypes.data, C.byref(h)))
+    try:
+        check(lib.hfpg_write_mppf(h, str(path).encode()))
+    finally:
+        lib.hfpg_frame_free(h)
+
+
+def read_mppf(path: str) -> Frame:
+    """mppf.cpp:102-177: checksums, CSR invariants (ValueError, like std::invalid_argument),
+    format errors (RuntimeError), Morton cell order recomputed."""
+    h = N.vp()
+    check(lib.hfpg_read_mppf(str(path).encode(), C.byref(h)))
+    return _frame_from_handle(h, None, None)
 
 
 def make_frame(n: int, master_seed: int, frame_index: int) -> Frame:
@@ -381,6 +416,29 @@ class Device:
 
     def load_csr_device(self, n, ro_ptr, ci_ptr, v_ptr):
         check(lib.hfpg_load_csr(self.h, n, ro_ptr, ci_ptr, v_ptr, N.DEVICE))
+
+    def load_mppf(self, path: str) -> "GpuFrame":
+        """read_mppf on the device (pinned streaming, GPU crc32 and CSR checks); the frame becomes
+        this handle's system and GPU frame."""
+        check(lib.hfpg_load_mppf(self.h, str(path).encode()))
+        g = self._gpu_frame(None, None)
+        self.csr_id = ("mppf", str(path))
+        return g
+
+    def load_checkpoint(self, path: str):
+        """read_checkpoint straight into device memory (pinned streaming, GPU crc32)."""
+        check(lib.hfpg_load_checkpoint(self.h, str(path).encode()))
+
+    def crc32(self, data, where: int | None = None) -> int:
+        """zlib crc32 of a numpy array (host, zlib) or a device pointer + size (GPU)."""
+        out = C.c_uint32()
+        if isinstance(data, np.ndarray):
+            a = np.ascontiguousarray(data)
+            check(lib.hfpg_crc32(self.h, a.ctypes.data, a.nbytes, N.HOST, C.byref(out)))
+        else:
+            ptr, nbytes = data
+            check(lib.hfpg_crc32(self.h, ptr, nbytes, N.DEVICE if where is None else where, C.byref(out)))
+        return out.value
 
     def load_factors(self, f: FactorTensor):
         L = f.layout

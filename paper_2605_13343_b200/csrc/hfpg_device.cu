@@ -5,8 +5,13 @@
 #include "partition_host.hpp"
 #include "framegen.cuh"
 #include "ic0.cuh"
+#include "crc32.cuh"
+#include "io_device.cuh"
 
 #include <algorithm>
+#include <cstdio>
+#include <memory>
+#include <zlib.h>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -67,6 +72,11 @@ struct hfpg_handle {
     cudaStream_t stream = nullptr;
     cudaStream_t lstream = nullptr;  // stream the launch_* helpers use (a group capture redirects it)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // file -> device streaming (HFTC / MPPF loaders): two pinned staging buffers + their events
+    unsigned char* pin[2] = {nullptr, nullptr};
+    cudaEvent_t pin_ev[2] = {nullptr, nullptr};
+    uint32_t* crc_scratch = nullptr;
+    uint64_t crc_cap = 0;
 
     // factors
     bool have_factors = false;
@@ -849,6 +859,204 @@ void frame_gpu(hfpg_handle* h, const FrameParams& FP) {
     ensure_workspace(h);
 }
 
+// ---- file -> device ------------------------------------------------------
+constexpr uint64_t kPinBytes = 32ull << 20;
+// Copy `bytes` of the open file starting at `off` into device memory `dst`: 32 MB pieces through
+// two pinned buffers, the read of one piece overlapping the H2D copy of the other.
+void stream_to_device(hfpg_handle* h, std::FILE* fp, uint64_t off, uint64_t bytes, void* dst, const char* what) {
+    for (int q = 0; q < 2; ++q)
+        if (!h->pin[q]) {
+            CK(cudaMallocHost(reinterpret_cast<void**>(&h->pin[q]), kPinBytes));
+            CK(cudaEventCreateWithFlags(&h->pin_ev[q], cudaEventDisableTiming));
+            CK(cudaEventRecord(h->pin_ev[q], h->stream));
+        }
+    if (std::fseek(fp, long(off), SEEK_SET) != 0) throw IoError(std::string(what) + ": seek failed");
+    unsigned char* d = static_cast<unsigned char*>(dst);
+    for (uint64_t done = 0, k = 0; done < bytes; ++k) {
+        const int q = int(k & 1);
+        const uint64_t piece = std::min<uint64_t>(kPinBytes, bytes - done);
+        CK(cudaEventSynchronize(h->pin_ev[q]));  // this buffer's previous copy has landed
+        if (std::fread(h->pin[q], 1, piece, fp) != piece) throw IoError(std::string(what) + ": truncated payload");
+        CK(cudaMemcpyAsync(d + done, h->pin[q], piece, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaEventRecord(h->pin_ev[q], h->stream));
+        done += piece;
+    }
+}
+// zlib crc32 of device memory, on the handle's stream (crc32.cuh); synchronous.
+uint32_t device_crc(hfpg_handle* h, const void* d, uint64_t bytes) {
+    const uint64_t need = crc_scratch_words(bytes);
+    if (h->crc_cap < need) {
+        dalloc(h->crc_scratch, need);
+        h->crc_cap = need;
+    }
+    crc32_device(d, bytes, h->crc_scratch, h->stream);
+    CK(cudaGetLastError());
+    uint32_t out = 0;
+    CK(cudaMemcpyAsync(&out, h->crc_scratch, 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return out;
+}
+struct FileCloser {
+    void operator()(std::FILE* f) const {
+        if (f) std::fclose(f);
+    }
+};
+
+// mppf.cpp:102-177 read_mppf on the device: sections streamed into the handle's GPU-frame arrays,
+// every checksum computed on the GPU, the CSR validated on the GPU with the reference's rules,
+// Morton order by k_fg_rank, then the operator state upload_csr leaves (SELL-32, diagonal,
+// exact |A|_F) — the frame is the handle's system, as after hfpg_frame_gpu_2d.
+void frame_from_mppf(hfpg_handle* h, const char* path) {
+    set_device(h);
+    if (h->part.G > 1) reset_partition(h);
+    const MppfHeader m = mppf_read_header(path);
+    uint64_t nnz = 0, got = 0;
+    for (const MppfSection& sc : m.sections) {
+        if (sc.name == "col_indices") nnz = sc.bytes / 4;
+        got |= sc.name == "rho" ? 1 : sc.name == "row_offsets" ? 2 : sc.name == "col_indices" ? 4 : sc.name == "values" ? 8 : 16;
+    }
+    if (got != 31) throw IoError(std::string("read_mppf: missing section in ") + path);
+    const uint64_t n = m.n;
+    if (n < 1 || m.width * m.height < n || m.width >= (1u << 16) || m.height >= (1u << 16))
+        throw InvalidArgument("morton_cell_order: grid does not hold n cells");
+    auto& F = h->fr;
+    FgParams P{};
+    P.dims = 2;
+    P.nb = int(std::min<size_t>(m.bars.size(), 3));
+    for (int k = 0; k < P.nb; ++k) P.bars[k] = {int(m.bars[k].axis), int(m.bars[k].gap), m.bars[k].center, m.bars[k].thickness};
+    P.n = n;
+    P.W = m.width;
+    P.H = m.height;
+    P.D = 1;
+    P.rho_heavy = m.rho_heavy;
+    const uint64_t big = std::max(P.W, P.H);
+    P.levels = 0;
+    while ((1ULL << P.levels) < big) ++P.levels;
+    const uint64_t cells = P.W * P.H, ns = (n + 31) / 32;
+    if (!F.side[0]) {
+        for (auto& st : F.side) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        for (auto& e : F.ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaMallocHost(reinterpret_cast<void**>(&F.tail_host), 8 * sizeof(unsigned long long)));
+        dalloc(F.sums, 2);
+        dalloc(F.tail, 8);
+    }
+    if (cells > F.cap_cells || !F.rank_of) {
+        dalloc(F.rank_of, cells);
+        F.cap_cells = cells;
+    }
+    if (n + 1 > F.cap_n || !F.order) {
+        for (uint32_t** p : {&F.order, &F.len, &F.slice_len}) dalloc(*p, n + 1);
+        for (double** p : {&F.rho, &F.b}) dalloc(*p, n + 1);
+        for (unsigned long long** p : {&F.ro, &F.tot}) dalloc(*p, n + 1);
+        F.cap_n = n + 1;
+    }
+    if (nnz + 1 > F.cap_nnz || !F.ci) {
+        dalloc(F.ci, nnz + 1);
+        dalloc(F.vals, nnz + 1);
+        F.cap_nnz = nnz + 1;
+    }
+    F.valid = false;
+    // stream the sections, then check every checksum on the device (mppf.cpp:139-141)
+    std::unique_ptr<std::FILE, FileCloser> fp(std::fopen(path, "rb"));
+    if (!fp) throw IoError(std::string("read_mppf: cannot open ") + path);
+    struct Dst { void* p; uint64_t cap; };
+    auto dst_of = [&](const std::string& nm) -> Dst {
+        if (nm == "rho") return {F.rho, n * 8};
+        if (nm == "row_offsets") return {F.ro, (n + 1) * 8};
+        if (nm == "col_indices") return {F.ci, nnz * 4};
+        if (nm == "values") return {F.vals, nnz * 8};
+        return {F.b, n * 8};
+    };
+    for (const MppfSection& sc : m.sections) {
+        const Dst d = dst_of(sc.name);
+        if (sc.bytes > d.cap) {
+            if (sc.name == "rho" || sc.name == "b") throw IoError("read_mppf: section sizes inconsistent with n");
+            throw InvalidArgument(sc.name == "row_offsets" ? "csr: row_offsets length != n_rows+1" : "csr: nnz mismatch");
+        }
+        stream_to_device(h, fp.get(), m.payload_offset + sc.offset, sc.bytes, d.p, "read_mppf");
+    }
+    for (const MppfSection& sc : m.sections)
+        if (device_crc(h, dst_of(sc.name).p, sc.bytes) != sc.crc)
+            throw IoError("read_mppf: checksum mismatch in section " + sc.name);
+    // csr.cpp:9-53 in the reference's order of checks
+    for (const MppfSection& sc : m.sections) {
+        if (sc.name == "row_offsets" && sc.bytes != (n + 1) * 8) throw InvalidArgument("csr: row_offsets length != n_rows+1");
+        if (sc.name == "values" && sc.bytes != nnz * 8) throw InvalidArgument("csr: nnz mismatch");
+    }
+    const bool realloc_op = ns * 32 * 8 > h->sell_cap || ns + 1 > h->slice_cap || n > h->diag_cap ||
+                            !h->sell_cols || !h->slice_off || !h->a_diag;
+    cudaStream_t st = h->stream;
+    CK(cudaMemsetAsync(F.tail, 0, 8 * sizeof(unsigned long long), st));
+    if (n > h->diag_cap || !h->a_diag) {
+        invalidate_graph(h);
+        dalloc(h->a_diag, n);
+        h->diag_cap = n;
+    }
+    k_mppf_rows<<<unsigned((n + 255) / 256), 256, 0, st>>>(F.ro, F.ci, F.vals, n, nnz, F.len, h->a_diag,
+                                                          reinterpret_cast<unsigned*>(F.tail + 1));
+    CK(cudaGetLastError());
+    unsigned err = 0;
+    CK(cudaMemcpyAsync(&err, F.tail + 1, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (err & kCsrFirst) throw InvalidArgument("csr: row_offsets[0] != 0");
+    if (err & kCsrLast) throw InvalidArgument("csr: nnz mismatch");
+    if (err & kCsrNondecreasing) throw InvalidArgument("csr: row_offsets not nondecreasing");
+    if (err & kCsrColRange) throw InvalidArgument("csr: column index out of range");
+    if (err & kCsrColOrder) throw InvalidArgument("csr: column indices not strictly increasing");
+    if (err & kCsrSymmetric) throw InvalidArgument("csr: values not symmetric");
+    // SELL-32 width per slice, then the operator arrays (sized by this frame's widest slice)
+    if (realloc_op && (ns + 1 > h->slice_cap || !h->slice_off)) {
+        invalidate_graph(h);
+        dalloc(h->slice_off, ns + 1);
+        h->slice_cap = ns + 1;
+    }
+    k_sell_widths<<<unsigned((ns + 7) / 8), 256, 0, st>>>(F.len, n, ns, F.slice_len);
+    scan_counts(h, st, F.slice_len, ns, h->slice_off);
+    unsigned long long sell_n = 0;
+    CK(cudaMemcpyAsync(&sell_n, h->slice_off + ns, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (sell_n > h->sell_cap || !h->sell_cols || !h->sell_vals) {
+        invalidate_graph(h);
+        dalloc(h->sell_cols, std::max<uint64_t>(sell_n, 1));
+        dalloc(h->sell_vals, std::max<uint64_t>(sell_n, 1));
+        h->sell_cap = std::max<uint64_t>(sell_n, 1);
+    }
+    k_sell_fill<<<unsigned((ns + 7) / 8), 256, 0, st>>>(F.ro, F.ci, F.vals, n, ns, h->slice_off, h->sell_cols,
+                                                         h->sell_vals);
+    k_sell_chunks<<<unsigned((ns + 8 * 256 - 1) / (8 * 256)), 256, 0, st>>>(h->slice_off, ns, F.tail + 2);
+    k_fg_rank<<<fg_blocks(h, cells), 256, 0, st>>>(P, F.order, F.rank_of);  // frame.cpp:24-41 order
+    CK(cudaGetLastError());
+    seq_sum(st, F.vals, nnz, nullptr, nnz, true, F.sums + 1, F.seq[1]);  // csr.cpp:64-68, exactly
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(F.tail + 4, F.sums, 16, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(F.tail_host, F.tail, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const unsigned long long* T = F.tail_host;
+    double sums[2];
+    std::memcpy(sums, T + 4, 16);
+    F.nnz = nnz;
+    F.P = P;
+    F.gen_ms = 0.f;
+    F.valid = true;
+    h->fro = std::sqrt(sums[1]);
+    std::vector<double> dg(n);
+    CK(cudaMemcpy(dg.data(), h->a_diag, n * 8, cudaMemcpyDeviceToHost));
+    h->diag_positive = std::all_of(dg.begin(), dg.end(), [](double d) { return d > 0.0; });
+    uint64_t maxch = (T[2] + 1023) & ~uint64_t(1023);
+    const uint32_t sb = (maxch > 0 && (maxch + kSpmvHdr) * spmv_stages() + 128 <= 110 * 1024) ? uint32_t(maxch) : 0;
+    const uint64_t maxch16 = (T[3] + 127) & ~uint64_t(127);
+    const uint32_t psb = (maxch16 > 0 && 2 * maxch16 <= sizeof(PStage)) ? uint32_t(maxch16) : 0;
+    const bool no_tma = std::getenv("HFPG_NO_SPMV_TMA") != nullptr;
+    const uint32_t sb2 = no_tma ? 0 : sb, psb2 = no_tma ? 0 : psb;
+    if (h->n != n || sb2 != h->spmv_stage_bytes || psb2 != h->pspmv_stage_bytes) invalidate_graph(h);
+    h->spmv_stage_bytes = sb2;
+    h->pspmv_stage_bytes = psb2;
+    h->n = n;
+    h->have_csr = true;
+    h->have_diag = true;
+    ensure_workspace(h);
+}
+
 }  // namespace
 
 extern "C" {
@@ -918,6 +1126,11 @@ int hfpg_destroy(hfpg_handle* h) {
         if (h->toynet) toynet_model_destroy(h->toynet);
         if (h->ev0) cudaEventDestroy(h->ev0);
         if (h->ev1) cudaEventDestroy(h->ev1);
+        for (int q = 0; q < 2; ++q) {
+            if (h->pin[q]) cudaFreeHost(h->pin[q]);
+            if (h->pin_ev[q]) cudaEventDestroy(h->pin_ev[q]);
+        }
+        dfree(h->crc_scratch);
         if (h->stream) cudaStreamDestroy(h->stream);
         delete h;
     });
@@ -1714,6 +1927,59 @@ int hfpg_ic0_apply(hfpg_handle* h, const double* r, double* z, int where) {
         if (where == HFPG_HOST) copy_out(h, z, h->z, h->n, HFPG_HOST);
         CK(cudaStreamSynchronize(h->stream));
     });
+}
+
+
+// ---- on-disk formats on the device --------------------------------------
+int hfpg_crc32(hfpg_handle* h, const void* data, uint64_t bytes, int where, uint32_t* out) {
+    return guarded([&] {
+        set_device(h);
+        if (where == HFPG_DEVICE) {
+            *out = device_crc(h, data, bytes);
+        } else {
+            uLong c = ::crc32(0L, Z_NULL, 0);
+            const Bytef* b = static_cast<const Bytef*>(data);
+            for (uint64_t left = bytes; left;) {
+                const uInt chunk = static_cast<uInt>(std::min<uint64_t>(left, 1u << 30));
+                c = ::crc32(c, b, chunk);
+                b += chunk;
+                left -= chunk;
+            }
+            *out = uint32_t(c);
+        }
+    });
+}
+
+// checkpoint.cpp:45-85 read_checkpoint straight into the handle's factor tensor: header on the
+// host, payload streamed through pinned buffers into device memory, crc32 on the GPU.
+int hfpg_load_checkpoint(hfpg_handle* h, const char* path) {
+    return guarded([&] {
+        set_device(h);
+        const HftcHeader H = hftc_read_header(path);
+        const Layout& L = H.L;
+        if (h->have_csr && h->n != L.n) throw InvalidArgument("load_factors: length mismatch");
+        std::unique_ptr<std::FILE, FileCloser> fp(std::fopen(path, "rb"));
+        if (!fp) throw IoError(std::string("read_checkpoint: cannot open ") + path);
+        invalidate_graph(h);
+        if (!h->have_factors || h->L.total != L.total) dalloc(h->F, L.total);
+        h->have_factors = false;
+        stream_to_device(h, fp.get(), H.payload_offset, L.total * 4, h->F, "read_checkpoint");
+        if (device_crc(h, h->F, L.total * 4) != H.crc) throw IoError("read_checkpoint: payload checksum mismatch");
+        h->L = L;
+        h->have_factors = true;
+        h->spd_enabled = H.spd_enabled;
+        h->spd_raw = H.spd_raw;
+        h->fast = (L.l == kL && L.ls == kLs && std::getenv("HFPG_FORCE_GENERIC") == nullptr);
+        if (!h->have_csr && !h->have_diag) h->n = L.n;
+        ensure_workspace(h);
+        const double shift = H.spd_enabled ? std::log1p(std::exp(H.spd_raw)) : 0.0;  // factor_tensor.hpp:64
+        CK(cudaMemcpyAsync(&h->sc->shift, &shift, 8, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int hfpg_load_mppf(hfpg_handle* h, const char* path) {
+    return guarded([&] { frame_from_mppf(h, path); });
 }
 
 }  // extern "C"

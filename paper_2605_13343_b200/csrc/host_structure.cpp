@@ -9,6 +9,7 @@
 #include <zlib.h>
 
 #include <algorithm>
+#include <memory>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -273,6 +274,9 @@ static hfpg_frame* frame_2d(uint64_t n, uint64_t seed, uint64_t fidx) {
     f->width = w;
     f->height = h;
     f->rho_heavy = P.rho_heavy;
+    f->master_seed = seed;
+    f->frame_index = fidx;
+    f->bars = P.bars;
     // frame.cpp:24-41: Morton codes are unique per cell, so a key sort equals the reference's
     // comparator sort.
     std::vector<std::pair<uint32_t, uint32_t>> keyed(w * h);
@@ -322,6 +326,9 @@ static hfpg_frame* frame_3d(uint64_t nx, uint64_t ny, uint64_t nz, uint64_t seed
     f->height = ny;
     f->depth = nz;
     f->rho_heavy = P.rho_heavy;
+    f->master_seed = seed;
+    f->frame_index = fidx;
+    f->bars = P.bars;
     std::vector<std::pair<uint64_t, uint32_t>> keyed(n);
     parallel_for(n, [&](uint64_t lo, uint64_t hi) {
         for (uint64_t id = lo; id < hi; ++id) {
@@ -456,7 +463,170 @@ uint32_t crc_of(const float* p, uint64_t n) {
     }
     return static_cast<uint32_t>(c);
 }
+// Elements of a JSON array's raw text ("[a, b, ...]").
+std::vector<std::string> split_array(const std::string& s) {
+    std::vector<std::string> out;
+    size_t i = 0;
+    skip_ws(s, i);
+    if (i >= s.size() || s[i] != '[') throw IoError("read_mppf: malformed header");
+    ++i;
+    for (;;) {
+        skip_ws(s, i);
+        if (i < s.size() && s[i] == ']') break;
+        const size_t b = i;
+        i = skip_value(s, i);
+        out.push_back(s.substr(b, i - b));
+        skip_ws(s, i);
+        if (i < s.size() && s[i] == ',') {
+            ++i;
+            continue;
+        }
+        if (i < s.size() && s[i] == ']') break;
+        throw IoError("read_mppf: malformed header");
+    }
+    return out;
+}
+const std::string& need(const JsonHeader& h, const char* k) {
+    const std::string* v = h.get(k);
+    if (!v) throw IoError(std::string("read_mppf: missing key ") + k);
+    return *v;
+}
+const char kMppfMagic[8] = {'M', 'P', 'P', 'F', '0', '0', '0', '1'};
+uint32_t crc_bytes(const void* p, uint64_t bytes) {
+    uLong c = ::crc32(0L, Z_NULL, 0);
+    const Bytef* b = static_cast<const Bytef*>(p);
+    while (bytes) {
+        const uInt chunk = static_cast<uInt>(std::min<uint64_t>(bytes, 1u << 30));
+        c = ::crc32(c, b, chunk);
+        b += chunk;
+        bytes -= chunk;
+    }
+    return static_cast<uint32_t>(c);
+}
+std::string fmt_double(double v) {
+    char num[64];
+    std::snprintf(num, sizeof(num), "%.17g", v);
+    return num;
+}
 }  // namespace
+
+// checkpoint.cpp:45-66: magic, header length, JSON header, layout checks (no payload).
+HftcHeader hftc_read_header(const char* path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw IoError(std::string("read_checkpoint: cannot open ") + path);
+    char magic[8];
+    in.read(magic, 8);
+    if (!in || std::memcmp(magic, kMagic, 8) != 0) throw IoError("read_checkpoint: bad magic");
+    uint64_t len = 0;
+    in.read(reinterpret_cast<char*>(&len), 8);
+    if (!in || len == 0 || len > (1ULL << 30)) throw IoError("read_checkpoint: bad header length");
+    std::string hs(len, '\0');
+    in.read(hs.data(), std::streamsize(len));
+    if (!in) throw IoError("read_checkpoint: truncated header");
+    JsonHeader h = parse_header(hs);
+    if (need_u64(h, "layout_version") != 1) throw IoError("read_checkpoint: unsupported layout version");
+    HftcHeader out;
+    out.L = make_layout(need_u64(h, "n"), need_u64(h, "leaf_size"), need_u64(h, "coarse_size"));
+    if (out.L.total != need_u64(h, "packed_width")) throw IoError("read_checkpoint: packed width mismatch");
+    const std::string* e = h.get("spd_shift_enabled");
+    out.spd_enabled = (e && *e == "true") ? 1 : 0;
+    const std::string* r = h.get("spd_shift_raw");
+    out.spd_raw = r ? std::stod(*r) : 0.0;
+    out.crc = uint32_t(need_u64(h, "payload_crc32"));
+    out.payload_offset = 16 + len;
+    return out;
+}
+
+// mppf.cpp:104-141: magic, header length, JSON header (version, dims, seeds, barriers, sections).
+MppfHeader mppf_read_header(const char* path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw IoError(std::string("read_mppf: cannot open ") + path);
+    char magic[8];
+    in.read(magic, 8);
+    if (!in || std::memcmp(magic, kMppfMagic, 8) != 0) throw IoError(std::string("read_mppf: bad magic in ") + path);
+    uint64_t len = 0;
+    in.read(reinterpret_cast<char*>(&len), 8);
+    if (!in || len == 0 || len > (1ULL << 30)) throw IoError(std::string("read_mppf: bad header length in ") + path);
+    std::string hs(len, '\0');
+    in.read(hs.data(), std::streamsize(len));
+    if (!in) throw IoError(std::string("read_mppf: truncated header in ") + path);
+    const JsonHeader h = parse_header(hs);
+    if (std::stoll(need(h, "version")) != 1) throw IoError("read_mppf: unsupported version");
+    MppfHeader m;
+    m.n = std::stoull(need(h, "n"));
+    m.width = std::stoull(need(h, "width"));
+    m.height = std::stoull(need(h, "height"));
+    const JsonHeader seeds = parse_header(need(h, "seeds"));
+    m.seed = std::stoull(need(seeds, "master"));
+    m.frame = std::stoull(need(seeds, "frame"));
+    m.rho_heavy = std::stod(need(h, "rho_heavy"));
+    for (const std::string& e : split_array(need(h, "barriers"))) {
+        const JsonHeader b = parse_header(e);
+        FrameBarrier fb;
+        fb.axis = std::stoull(need(b, "orientation"));
+        fb.center = std::stod(need(b, "center"));
+        fb.thickness = std::stod(need(b, "thickness"));
+        fb.gap = std::stoull(need(b, "gap"));
+        m.bars.push_back(fb);
+    }
+    for (const std::string& e : split_array(need(h, "sections"))) {
+        const JsonHeader sh = parse_header(e);
+        MppfSection sec;
+        std::string nm = need(sh, "name");
+        if (nm.size() >= 2 && nm.front() == '"') nm = nm.substr(1, nm.size() - 2);
+        sec.name = nm;
+        sec.offset = std::stoull(need(sh, "offset"));
+        sec.bytes = std::stoull(need(sh, "bytes"));
+        sec.crc = uint32_t(std::stoull(need(sh, "crc32")));
+        if (nm != "rho" && nm != "row_offsets" && nm != "col_indices" && nm != "values" && nm != "b")
+            throw IoError("read_mppf: unknown section " + nm);
+        m.sections.push_back(sec);
+    }
+    m.payload_offset = 16 + len;
+    return m;
+}
+
+// csr.cpp:9-53 CsrMatrix::validate(check_symmetric = true), the reference's messages.
+void validate_csr_symmetric(const Csr& A, uint64_t n) {
+    if (A.row_offsets.size() != n + 1) throw InvalidArgument("csr: row_offsets length != n_rows+1");
+    if (A.row_offsets.front() != 0) throw InvalidArgument("csr: row_offsets[0] != 0");
+    if (A.row_offsets.back() != A.cols.size() || A.cols.size() != A.vals.size())
+        throw InvalidArgument("csr: nnz mismatch");
+    for (uint64_t i = 0; i < n; ++i) {
+        if (A.row_offsets[i] > A.row_offsets[i + 1]) throw InvalidArgument("csr: row_offsets not nondecreasing");
+        for (uint64_t p = A.row_offsets[i]; p < A.row_offsets[i + 1]; ++p) {
+            if (A.cols[p] >= n) throw InvalidArgument("csr: column index out of range");
+            if (p > A.row_offsets[i] && A.cols[p] <= A.cols[p - 1])
+                throw InvalidArgument("csr: column indices not strictly increasing in row " + std::to_string(i));
+        }
+    }
+    auto entry = [&](uint64_t r, uint32_t c) -> double {
+        uint64_t lo = A.row_offsets[r], hi = A.row_offsets[r + 1];
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) / 2;
+            if (A.cols[mid] < c) lo = mid + 1;
+            else hi = mid;
+        }
+        return (lo < A.row_offsets[r + 1] && A.cols[lo] == c) ? A.vals[lo] : 0.0;
+    };
+    for (uint64_t i = 0; i < n; ++i)
+        for (uint64_t p = A.row_offsets[i]; p < A.row_offsets[i + 1]; ++p)
+            if (A.vals[p] != entry(A.cols[p], uint32_t(i))) throw InvalidArgument("csr: values not symmetric");
+}
+
+// frame.cpp:24-41 morton_cell_order (2D).
+std::vector<uint32_t> morton_order_2d(uint64_t w, uint64_t h, uint64_t n) {
+    if (w >= (1u << 16) || h >= (1u << 16)) throw InvalidArgument("morton_cell_order: grid dimension >= 2^16");
+    std::vector<std::pair<uint32_t, uint32_t>> keyed(w * h);
+    for (uint64_t y = 0; y < h; ++y)
+        for (uint64_t x = 0; x < w; ++x)
+            keyed[y * w + x] = {spread2(uint32_t(x)) | (spread2(uint32_t(y)) << 1), uint32_t(y * w + x)};
+    std::sort(keyed.begin(), keyed.end());
+    if (n > keyed.size()) throw InvalidArgument("morton_cell_order: n exceeds the grid");
+    std::vector<uint32_t> order(n);
+    for (uint64_t i = 0; i < n; ++i) order[i] = keyed[i].second;
+    return order;
+}
 
 }  // namespace hfpg
 
@@ -618,4 +788,142 @@ int hfpg_frame_copy(const hfpg_frame* f, uint32_t* cell_order, double* rho,
 
 void hfpg_frame_free(hfpg_frame* f) { delete f; }
 
+
+int hfpg_frame_meta(const hfpg_frame* f, uint64_t* master_seed, uint64_t* frame_index, uint32_t* nbarriers,
+                    double* barriers, uint32_t cap) {
+    return guarded([&] {
+        if (!f) throw InvalidArgument("frame_meta: null frame");
+        if (master_seed) *master_seed = f->master_seed;
+        if (frame_index) *frame_index = f->frame_index;
+        if (nbarriers) *nbarriers = uint32_t(f->bars.size());
+        for (uint32_t i = 0; barriers && i < f->bars.size() && i < cap; ++i) {
+            barriers[4 * i + 0] = double(f->bars[i].axis);
+            barriers[4 * i + 1] = f->bars[i].center;
+            barriers[4 * i + 2] = f->bars[i].thickness;
+            barriers[4 * i + 3] = double(f->bars[i].gap);
+        }
+    });
+}
+
+// mppf.cpp:48-100 write_mppf: MPPF v1 ("MPPF0001" | u64 header length | JSON | sections
+// rho f64 | row_offsets u64 | col_indices u32 | values f64 | b f64), per-section zlib crc32.
+// Keys in nlohmann's sorted order. MPPF frames are 2D (width x height), as the reference's.
+int hfpg_write_mppf(const hfpg_frame* f, const char* path) {
+    return guarded([&] {
+        if (!f) throw InvalidArgument("write_mppf: null frame");
+        if (f->depth != 1) throw InvalidArgument("write_mppf: MPPF frames are 2D");
+        const uint64_t n = f->n, nnz = f->A.row_offsets.back();
+        struct Sec { const char* name; const char* dtype; const void* p; uint64_t bytes; };
+        const Sec secs[5] = {{"rho", "f64", f->rho.data(), n * 8},
+                             {"row_offsets", "u64", f->A.row_offsets.data(), (n + 1) * 8},
+                             {"col_indices", "u32", f->A.cols.data(), nnz * 4},
+                             {"values", "f64", f->A.vals.data(), nnz * 8},
+                             {"b", "f64", f->b.data(), n * 8}};
+        std::string bars = "[";
+        for (size_t i = 0; i < f->bars.size(); ++i) {
+            const FrameBarrier& b = f->bars[i];
+            bars += std::string(i ? "," : "") + "{\"center\":" + fmt_double(b.center) + ",\"gap\":" +
+                    std::to_string(b.gap) + ",\"orientation\":" + std::to_string(b.axis) + ",\"thickness\":" +
+                    fmt_double(b.thickness) + "}";
+        }
+        bars += "]";
+        std::string sj = "[";
+        uint64_t cursor = 0;
+        for (int i = 0; i < 5; ++i) {
+            sj += std::string(i ? "," : "") + "{\"bytes\":" + std::to_string(secs[i].bytes) + ",\"crc32\":" +
+                  std::to_string(crc_bytes(secs[i].p, secs[i].bytes)) + ",\"dtype\":\"" + secs[i].dtype +
+                  "\",\"name\":\"" + secs[i].name + "\",\"offset\":" + std::to_string(cursor) + "}";
+            cursor += secs[i].bytes;
+        }
+        sj += "]";
+        const std::string hdr = "{\"barriers\":" + bars + ",\"format\":\"MPPF\",\"height\":" +
+                                std::to_string(f->height) + ",\"n\":" + std::to_string(n) +
+                                ",\"rho_heavy\":" + fmt_double(f->rho_heavy) + ",\"sections\":" + sj +
+                                ",\"seeds\":{\"frame\":" + std::to_string(f->frame_index) + ",\"master\":" +
+                                std::to_string(f->master_seed) + "},\"version\":1,\"width\":" +
+                                std::to_string(f->width) + "}";
+        std::ofstream out(path, std::ios::binary | std::ios::trunc);
+        if (!out) throw IoError(std::string("write_mppf: cannot open ") + path);
+        const uint64_t len = hdr.size();
+        out.write(kMppfMagic, 8);
+        out.write(reinterpret_cast<const char*>(&len), 8);
+        out.write(hdr.data(), std::streamsize(len));
+        for (const Sec& sc : secs) out.write(static_cast<const char*>(sc.p), std::streamsize(sc.bytes));
+        if (!out) throw IoError(std::string("write_mppf: write failed for ") + path);
+    });
+}
+
+// mppf.cpp:102-177 read_mppf: every checksum, the CSR invariants (symmetric), section sizes,
+// then the Morton cell order of the grid.
+int hfpg_read_mppf(const char* path, hfpg_frame** out) {
+    return guarded([&] {
+        const MppfHeader m = mppf_read_header(path);
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw IoError(std::string("read_mppf: cannot open ") + path);
+        auto* f = new hfpg_frame;
+        std::unique_ptr<hfpg_frame> guard_f(f);
+        f->n = m.n;
+        f->width = m.width;
+        f->height = m.height;
+        f->master_seed = m.seed;
+        f->frame_index = m.frame;
+        f->rho_heavy = m.rho_heavy;
+        f->bars = m.bars;
+        for (const MppfSection& sc : m.sections) {
+            void* dst = nullptr;
+            if (sc.name == "rho") { f->rho.resize(sc.bytes / 8); dst = f->rho.data(); }
+            else if (sc.name == "row_offsets") { f->A.row_offsets.resize(sc.bytes / 8); dst = f->A.row_offsets.data(); }
+            else if (sc.name == "col_indices") { f->A.cols.resize(sc.bytes / 4); dst = f->A.cols.data(); }
+            else if (sc.name == "values") { f->A.vals.resize(sc.bytes / 8); dst = f->A.vals.data(); }
+            else { f->b.resize(sc.bytes / 8); dst = f->b.data(); }
+            in.seekg(std::streamoff(m.payload_offset + sc.offset));
+            in.read(static_cast<char*>(dst), std::streamsize(sc.bytes));
+            if (!in) throw IoError(std::string("read_mppf: truncated section in ") + path);
+            if (crc_bytes(dst, sc.bytes) != sc.crc)
+                throw IoError("read_mppf: checksum mismatch in section " + sc.name);
+        }
+        f->A.n = m.n;
+        if (f->A.row_offsets.empty()) throw InvalidArgument("csr: row_offsets length != n_rows+1");
+        validate_csr_symmetric(f->A, m.n);
+        if (f->rho.size() != m.n || f->b.size() != m.n)
+            throw IoError("read_mppf: section sizes inconsistent with n");
+        f->cell_order = morton_order_2d(m.width, m.height, m.n);
+        *out = guard_f.release();
+    });
+}
+
+
+int hfpg_frame_create(uint64_t n, uint64_t width, uint64_t height, uint64_t depth, uint64_t master_seed,
+                      uint64_t frame_index, double rho_heavy, uint32_t nbarriers, const double* barriers,
+                      const uint32_t* cell_order, const double* rho, const uint64_t* row_offsets,
+                      const uint32_t* col_indices, const double* values, const double* b, hfpg_frame** out) {
+    return guarded([&] {
+        if (n == 0 || !row_offsets) throw InvalidArgument("frame_create: empty frame");
+        auto f = std::make_unique<hfpg_frame>();
+        f->n = n;
+        f->width = width;
+        f->height = height;
+        f->depth = depth ? depth : 1;
+        f->master_seed = master_seed;
+        f->frame_index = frame_index;
+        f->rho_heavy = rho_heavy;
+        for (uint32_t i = 0; i < nbarriers; ++i) {
+            FrameBarrier fb;
+            fb.axis = uint64_t(barriers[4 * i + 0]);
+            fb.center = barriers[4 * i + 1];
+            fb.thickness = barriers[4 * i + 2];
+            fb.gap = uint64_t(barriers[4 * i + 3]);
+            f->bars.push_back(fb);
+        }
+        const uint64_t nnz = row_offsets[n];
+        if (cell_order) f->cell_order.assign(cell_order, cell_order + n);
+        f->rho.assign(rho, rho + n);
+        f->b.assign(b, b + n);
+        f->A.n = n;
+        f->A.row_offsets.assign(row_offsets, row_offsets + n + 1);
+        f->A.cols.assign(col_indices, col_indices + nnz);
+        f->A.vals.assign(values, values + nnz);
+        *out = f.release();
+    });
+}
 }  // extern "C"

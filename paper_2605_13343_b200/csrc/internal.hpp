@@ -160,11 +160,36 @@ struct ToynetDeviceFrame {
 void toynet_forward_device_frame(ToynetModel* m, cudaStream_t st, const ToynetDeviceFrame& f, float* out,
                                  hfpg_toynet_trace* trace);
 
+// HFTC / MPPF headers (host_structure.cpp), for the device loaders in hfpg_device.cu.
+struct HftcHeader {
+    Layout L;
+    int spd_enabled = 0;
+    double spd_raw = 0.0;
+    uint32_t crc = 0;
+    uint64_t payload_offset = 0;
+};
+HftcHeader hftc_read_header(const char* path);
+struct MppfSection {
+    std::string name;
+    uint64_t offset = 0, bytes = 0;
+    uint32_t crc = 0;
+};
+struct MppfHeader {
+    uint64_t n = 0, width = 0, height = 0, seed = 0, frame = 0;
+    double rho_heavy = 0.0;
+    std::vector<FrameBarrier> bars;
+    std::vector<MppfSection> sections;
+    uint64_t payload_offset = 0;
+};
+MppfHeader mppf_read_header(const char* path);
+
 }  // namespace hfpg
 
 struct hfpg_frame {
     uint64_t n = 0, width = 0, height = 0, depth = 1;
     double rho_heavy = 0.0;
+    uint64_t master_seed = 0, frame_index = 0;
+    std::vector<hfpg::FrameBarrier> bars;  // frame.hpp:37 (MPPF header)
     std::vector<uint32_t> cell_order;
     std::vector<double> rho, b;
     hfpg::Csr A;
