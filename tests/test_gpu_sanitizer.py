@@ -14,7 +14,8 @@ CS = "/usr/local/cuda/bin/compute-sanitizer"
 
 @pytest.mark.skipif(not os.path.exists(CS), reason="compute-sanitizer not installed")
 @pytest.mark.parametrize("tool,case", [("memcheck", "apply_fast"), ("memcheck", "solve_persistent"),
-                                       ("racecheck", "iteration_kernels")])
+                                       ("racecheck", "iteration_kernels"), ("memcheck", "solve_graph"),
+                                       ("memcheck", "ic0"), ("memcheck", "io")])
 def test_sanitizer_clean(tool, case):
     r = subprocess.run([CS, "--tool", tool, "--error-exitcode", "9", sys.executable,
                         os.path.join(ROOT, "tools", "sanitize_driver.py"), "--only", case],

@@ -1,6 +1,7 @@
 """Small invocations of every device path, for compute-sanitizer (memcheck / racecheck /
 synccheck): fast + generic apply, SpMV, graph and persistent PCG, a 2-rank partitioned group
-solve, the toy-network forward (tcgen05 GEMMs + attention).
+solve, the toy-network forward (tcgen05 GEMMs + attention), the IC(0) sweeps, the GPU crc32 and
+the MPPF / HFTC device loaders.
 
     compute-sanitizer --tool memcheck python tools/sanitize_driver.py [--only NAME]
 """
@@ -89,6 +90,29 @@ def toynet():
                      trace=H.ToynetTrace())
 
 
+def ic0():
+    fr = H.make_frame(4096, 7, 8)
+    ap_ = H.ic0_applier(H.ic0_factorize(fr.A))
+    ap_.bind(fr.A)
+    ap_(fr.b)
+    H.pcg_solve(fr.A, fr.b, ap_, H.SolveConfig(max_iters=5))
+
+
+def io():
+    import tempfile
+    import torch
+    d = H.Device(0)
+    x = torch.arange(100000, dtype=torch.uint8, device="cuda")
+    d.crc32((x.data_ptr() + 3, 99990))
+    fr = H.make_frame(4096, 7, 9)
+    with tempfile.TemporaryDirectory() as t:
+        H.write_mppf(fr, os.path.join(t, "f.mppf"))
+        d.load_mppf(os.path.join(t, "f.mppf"))
+        f = seeded(4096, frame=9)
+        H.write_checkpoint(f, os.path.join(t, "m.hftc"))
+        d.load_checkpoint(os.path.join(t, "m.hftc"))
+
+
 run("apply_fast", apply_fast)
 run("apply_generic", apply_generic)
 run("solve_graph", solve(N.SOLVER_GRAPH))
@@ -97,3 +121,5 @@ run("iteration_kernels", iteration_kernels)
 run("group_apply", group_apply)
 run("group", group)
 run("toynet", toynet)
+run("ic0", ic0)
+run("io", io)
