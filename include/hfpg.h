@@ -239,6 +239,27 @@ int hfpg_frame_meta(const hfpg_frame* f, uint64_t* master_seed, uint64_t* frame_
  * the frame becomes the handle's system and GPU frame (hfpg_frame_gpu_view / _copy). */
 int hfpg_load_mppf(hfpg_handle* h, const char* path);
 
+/* ---- training of the factor tensor (adjoint.hpp, loss.hpp, train.cpp) ----
+ * Double-precision parameters (PackedFactors<double>, packed width of make_factor_layout(n, 128,
+ * 32)); batches are kz columns, row-major n x kz; diag(A) is the loaded system's. shift = the
+ * tensor's spd_shift() (0 when disabled). where = HFPG_HOST / HFPG_DEVICE for every pointer.
+ * adjoint.cpp:44-127 factor_apply_batch: y = M x, every stage stashed on the handle. */
+int hfpg_batch_apply(hfpg_handle* h, const double* params, uint64_t leaf, uint64_t ls, double shift,
+                     const double* x, uint64_t kz, double* y, int where);
+/* adjoint.cpp:129-248 factor_apply_batch_adjoint for the handle's last forward batch:
+ * grad = d(loss)/d(params) for the upstream adjoint bar_y (grad is overwritten). */
+int hfpg_batch_adjoint(hfpg_handle* h, const double* params, const double* bar_y, double* grad, int where);
+/* adjoint.cpp:250-292 loss_gradient on the loaded system: kind 0 cosine (Y = M A Z, 1 - cos),
+ * 1 sai (|(1/norm_a) A M Z - Z|_F^2). A zero image sets *degenerate and a zero gradient. */
+int hfpg_loss_gradient(hfpg_handle* h, const double* params, uint64_t leaf, uint64_t ls, double shift,
+                       const double* z, uint64_t kz, int32_t kind, double norm_a, double* loss,
+                       int32_t* degenerate, double* grad, int where);
+/* train.cpp:136-160: global clip of grad to clip_norm, then AdamW with decoupled weight decay;
+ * device pointers; updates params, m1, m2 (and grad, clipped) in place. */
+int hfpg_adamw_step(hfpg_handle* h, double* params, double* grad, double* m1, double* m2, uint64_t count,
+                    uint64_t step, double lr, double beta1, double beta2, double eps, double weight_decay,
+                    double clip_norm, double* gnorm_out);
+
 /* ---- IC(0) baseline (ic0.hpp / ic0.cpp) ----
  * ic0.cpp:10-69 ic0_factorize on the host (no device needed): the lower factor L of A (pattern =
  * lower triangle of A, diagonal last; policy 0 = Ic0Shift::none, 1 = Ic0Shift::scaled, shift

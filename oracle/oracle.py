@@ -148,6 +148,32 @@ class Ref(_Base):
 
     prefix = "ref_"
 
+    def apply_batch_adjoint(self, n, packed64, a_diag, x, kz, bar_y=None, spd_enabled=0, spd_raw=0.0):
+        """adjoint.cpp:44 factor_apply_batch (+ :129 adjoint when bar_y is given) -> (y, grad)."""
+        y = np.empty(n * kz)
+        grad = np.empty(len(packed64))
+        f = self._f("apply_batch_adjoint")
+        f.argtypes = [_u64, _u64, _u64, _p, C.c_int, C.c_double, _p, _p, _u64, _p, _p, _p]
+        _check(f(n, 128, 32, _ptr(np.ascontiguousarray(packed64, np.float64)), spd_enabled, spd_raw,
+                 _ptr(np.ascontiguousarray(a_diag, np.float64)), _ptr(np.ascontiguousarray(x, np.float64)), kz,
+                 _ptr(np.ascontiguousarray(bar_y, np.float64)) if bar_y is not None else None, _ptr(y),
+                 _ptr(grad)), self.lib, "apply_batch_adjoint")
+        return y, (grad if bar_y is not None else None)
+
+    def loss_gradient(self, csr, packed64, z, kz, kind, norm_a=1.0):
+        """adjoint.cpp:250 loss_gradient -> (loss, degenerate, grad)."""
+        ro, ci, v = csr
+        n = len(ro) - 1
+        grad = np.empty(len(packed64))
+        loss = C.c_double()
+        deg = C.c_int()
+        f = self._f("loss_gradient")
+        f.argtypes = [_u64, _p, _p, _p, _u64, _u64, _p, _p, _u64, C.c_int, C.c_double, _p, _p, _p]
+        _check(f(n, _ptr(ro), _ptr(ci), _ptr(v), 128, 32, _ptr(np.ascontiguousarray(packed64, np.float64)),
+                 _ptr(np.ascontiguousarray(z, np.float64)), kz, kind, norm_a, C.byref(loss), C.byref(deg),
+                 _ptr(grad)), self.lib, "loss_gradient")
+        return loss.value, bool(deg.value), grad
+
     def ic0_factorize(self, csr, policy=1):
         """ic0.cpp:10 -> (lro u64[n+1], lci u32[nnz], lv f64[nnz], shift)."""
         ro, ci, v = csr

@@ -16,6 +16,7 @@
 #include "hfp/frame.hpp"
 #include "hfp/ic0.hpp"
 #include "hfp/mppf.hpp"
+#include "hfp/adjoint.hpp"
 #include "hfp/morton.hpp"
 #include "hfp/partition.hpp"
 #include "hfp/pcg.hpp"
@@ -235,6 +236,40 @@ int ref_assemble_dense_f32(uint64_t n, uint64_t leaf, uint64_t ls, const float* 
         auto f = make_factors<float>(n, leaf, ls, packed, spd_enabled, spd_raw);
         DenseMat M = assemble_dense(f, std::span<const double>(a_diag, n));
         std::memcpy(out, M.data.data(), n * n * 8);
+    });
+}
+
+// adjoint.cpp:44 factor_apply_batch then :129 factor_apply_batch_adjoint on the same context.
+int ref_apply_batch_adjoint(uint64_t n, uint64_t leaf, uint64_t ls, const double* packed, int spd_enabled,
+                            double spd_raw, const double* a_diag, const double* x, uint64_t kz,
+                            const double* bar_y, double* y_out, double* grad_out) {
+    return guard([&] {
+        PackedFactors<double> f = make_factors<double>(n, leaf, ls, packed, spd_enabled, spd_raw);
+        BatchApplyContext ctx(f.layout, kz);
+        std::vector<double> y(n * kz), grad(f.layout.total, 0.0);
+        factor_apply_batch(f, std::span<const double>(a_diag, n), std::span<const double>(x, n * kz), ctx, y);
+        std::memcpy(y_out, y.data(), n * kz * 8);
+        if (bar_y) {
+            factor_apply_batch_adjoint(f, std::span<const double>(a_diag, n), std::span<const double>(bar_y, n * kz),
+                                       ctx, grad);
+            std::memcpy(grad_out, grad.data(), grad.size() * 8);
+        }
+    });
+}
+
+// adjoint.cpp:250 loss_gradient (kind 0 cosine, 1 sai).
+int ref_loss_gradient(uint64_t n, const uint64_t* ro, const uint32_t* ci, const double* v, uint64_t leaf,
+                      uint64_t ls, const double* packed, const double* z, uint64_t kz, int kind, double norm_a,
+                      double* loss, int* degenerate, double* grad_out) {
+    return guard([&] {
+        CsrMatrix A = make_csr(n, ro, ci, v);
+        PackedFactors<double> f = make_factors<double>(n, leaf, ls, packed, 0, 0.0);
+        BatchApplyContext ctx(f.layout, kz);
+        LossGradResult r = loss_gradient(f, A, std::span<const double>(z, n * kz), kz,
+                                         kind ? LossKind::sai : LossKind::cosine, norm_a, ctx);
+        *loss = r.loss;
+        *degenerate = r.degenerate ? 1 : 0;
+        std::memcpy(grad_out, r.grad.data(), r.grad.size() * 8);
     });
 }
 

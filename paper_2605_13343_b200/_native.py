@@ -112,6 +112,12 @@ _PROTOS = {
     "hfpg_frame_create": (C.c_int, [u64, u64, u64, u64, u64, u64, dbl, C.c_uint32, vp, vp, vp, vp, vp, vp, vp,
                                     C.POINTER(vp)]),
     "hfpg_load_mppf": (C.c_int, [vp, C.c_char_p]),
+    "hfpg_batch_apply": (C.c_int, [vp, vp, u64, u64, dbl, vp, u64, vp, C.c_int]),
+    "hfpg_batch_adjoint": (C.c_int, [vp, vp, vp, vp, C.c_int]),
+    "hfpg_loss_gradient": (C.c_int, [vp, vp, u64, u64, dbl, vp, u64, i32, dbl, C.POINTER(dbl),
+                                     C.POINTER(i32), vp, C.c_int]),
+    "hfpg_adamw_step": (C.c_int, [vp, vp, vp, vp, vp, u64, u64, dbl, dbl, dbl, dbl, dbl, dbl,
+                                  C.POINTER(dbl)]),
     "hfpg_ic0_apply": (C.c_int, [vp, vp, vp, C.c_int]),
     "hfpg_pcg_solve": (C.c_int, [vp, vp, C.POINTER(SolveConfigC), vp, vp, C.POINTER(ReportC),
                                  C.c_int]),

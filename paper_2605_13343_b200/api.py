@@ -593,6 +593,68 @@ class _Factor(PrecondApplier):
         return self.dev.apply(r)
 
 
+# ------------------------------------------------------------------ adjoint.hpp / train.cpp
+
+
+class LossKind(enum.IntEnum):
+    """loss.hpp: cosine (1 - cos(Z, M A Z)) or sai (|(1/normA) A M Z - Z|_F^2)."""
+    cosine = 0
+    sai = 1
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, np.float64)
+
+
+def factor_apply_batch(params, x, kz: int, device: "Device", shift: float = 0.0) -> np.ndarray:
+    """adjoint.cpp:44-127: Y = M X (row-major n x kz, double precision, stages stashed on the
+    device for factor_apply_batch_adjoint). diag(A) is the device's loaded system's."""
+    x = _f64(x)
+    y = np.empty_like(x)
+    p = _f64(params)
+    check(lib.hfpg_batch_apply(device.h, p.ctypes.data, 128, 32, float(shift), x.ctypes.data, kz,
+                               y.ctypes.data, N.HOST))
+    return y
+
+
+def factor_apply_batch_adjoint(params, bar_y, device: "Device") -> np.ndarray:
+    """adjoint.cpp:129-248: d(loss)/d(params) for the upstream adjoint bar_y of the last batch."""
+    p = _f64(params)
+    by = _f64(bar_y)
+    g = np.empty_like(p)
+    check(lib.hfpg_batch_adjoint(device.h, p.ctypes.data, by.ctypes.data, g.ctypes.data, N.HOST))
+    return g
+
+
+@dataclass
+class LossGradResult:
+    loss: float
+    degenerate: bool
+    grad: np.ndarray
+
+
+def loss_gradient(params, z, kz: int, kind: LossKind, device: "Device", norm_a: float = 1.0,
+                  shift: float = 0.0) -> LossGradResult:
+    """adjoint.cpp:250-292 on the device's loaded system."""
+    p = _f64(params)
+    z = _f64(z)
+    g = np.empty_like(p)
+    loss, deg = N.dbl(), N.i32()
+    check(lib.hfpg_loss_gradient(device.h, p.ctypes.data, 128, 32, float(shift), z.ctypes.data, kz,
+                                 int(kind), float(norm_a), C.byref(loss), C.byref(deg), g.ctypes.data, N.HOST))
+    return LossGradResult(float(loss.value), bool(deg.value), g)
+
+
+def adamw_step(device: "Device", params_ptr: int, grad_ptr: int, m1_ptr: int, m2_ptr: int, count: int,
+               step: int, lr: float, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+               weight_decay: float = 0.0, clip_norm: float = float("inf")) -> float:
+    """train.cpp:136-160 on device buffers (global clip, AdamW); returns the gradient norm."""
+    gn = N.dbl()
+    check(lib.hfpg_adamw_step(device.h, params_ptr, grad_ptr, m1_ptr, m2_ptr, count, step, lr, beta1, beta2,
+                              eps, weight_decay, clip_norm, C.byref(gn)))
+    return float(gn.value)
+
+
 class Ic0Shift(enum.IntEnum):
     """ic0.hpp:7: scaled factors A + 1e-8 max(diag) I."""
     none = 0

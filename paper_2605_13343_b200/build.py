@@ -16,7 +16,7 @@ SO = os.path.join(HERE, "libhfpg.so")
 SRCS = ["csrc/hfpg_device.cu", "csrc/toynet.cu", "csrc/host_structure.cpp", "csrc/partition_host.cpp",
         "csrc/ic0_host.cpp"]
 DEPS = SRCS + ["csrc/kernels.cuh", "csrc/device_common.cuh", "csrc/internal.hpp",
-               "csrc/gemm_tcgen05.cuh", "csrc/attention_tcgen05.cuh", "csrc/solve_persistent.cuh", "csrc/comm.cuh", "csrc/partition_host.hpp", "csrc/framegen.cuh", "csrc/crmath.cuh", "csrc/toynet_kernels.cuh", "csrc/ic0.cuh", "csrc/crc32.cuh", "csrc/io_device.cuh",
+               "csrc/gemm_tcgen05.cuh", "csrc/attention_tcgen05.cuh", "csrc/solve_persistent.cuh", "csrc/comm.cuh", "csrc/partition_host.hpp", "csrc/framegen.cuh", "csrc/crmath.cuh", "csrc/toynet_kernels.cuh", "csrc/ic0.cuh", "csrc/crc32.cuh", "csrc/io_device.cuh", "csrc/train.cuh",
                "../include/hfpg.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -32,7 +32,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return SO
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
-           "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O3,-march=x86-64-v3,-ffp-contract=fast",
+           "-std=c++17", "--extended-lambda", "-shared", "-Xcompiler", "-fPIC,-O3,-march=x86-64-v3,-ffp-contract=fast",
            "-o", SO + ".tmp", *[os.path.join(HERE, s) for s in SRCS], "-lz", "-lpthread"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")

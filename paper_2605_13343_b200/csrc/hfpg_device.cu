@@ -7,6 +7,7 @@
 #include "ic0.cuh"
 #include "crc32.cuh"
 #include "io_device.cuh"
+#include "train.cuh"
 
 #include <algorithm>
 #include <cstdio>
@@ -77,6 +78,15 @@ struct hfpg_handle {
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     uint32_t* crc_scratch = nullptr;
     uint64_t crc_cap = 0;
+    // training batch state (train.cuh): stashes for (n, kz), params / grad / bar_y staging
+    struct Train {
+        uint64_t n = 0, kz = 0;
+        std::vector<double*> bufs;
+        TrainDev T{};
+        double *P = nullptr, *G = nullptr, *BY = nullptr, *Z = nullptr, *part = nullptr;
+        uint64_t pcap = 0;
+        bool have_fwd = false;
+    } tr;
 
     // factors
     bool have_factors = false;
@@ -1057,6 +1067,99 @@ void frame_from_mppf(hfpg_handle* h, const char* path) {
     ensure_workspace(h);
 }
 
+// ---- training (train.cuh) ---------------------------------------------------------------------
+// Size the batch state for (n, kz) and the packed width; point T at the loaded system.
+void train_prepare(hfpg_handle* h, uint64_t leaf, uint64_t ls, uint64_t kz, double shift) {
+    if (!h->have_diag || h->n == 0) throw InvalidArgument("factor_apply_batch: no system loaded (diag(A))");
+    if (leaf != 128 || ls != 32) throw InvalidArgument("factor_apply_batch: the GPU path implements L = 128, L_s = 32");
+    if (kz == 0) throw InvalidArgument("factor_apply_batch: kz must be positive");
+    const Layout L = make_layout(h->n, leaf, ls);
+    auto& R = h->tr;
+    if (R.n != h->n || R.kz != kz) {
+        for (double* b : R.bufs) dfree(b);
+        R.bufs.clear();
+        const uint64_t nk = h->n * kz, kk = L.k * 32 * kz, mk = L.m * 32 * kz, mq = L.m * 16 * kz;
+        auto mk_buf = [&](uint64_t cnt) {
+            double* p = nullptr;
+            dalloc(p, std::max<uint64_t>(cnt, 1));
+            R.bufs.push_back(p);
+            return p;
+        };
+        TrainDev& T = R.T;
+        T.X = mk_buf(nk); T.H = mk_buf(nk); T.Y = mk_buf(nk); T.W = mk_buf(nk);
+        T.Rr = mk_buf(kk); T.Rc = mk_buf(kk); T.Gr = mk_buf(kk); T.Gc = mk_buf(kk);
+        T.BGr = mk_buf(kk); T.BGc = mk_buf(kk); T.BRr = mk_buf(kk); T.BRc = mk_buf(kk);
+        T.Sr = mk_buf(mk); T.Sc = mk_buf(mk); T.Crow = mk_buf(mk); T.Ccol = mk_buf(mk);
+        T.BCr = mk_buf(mk); T.BCc = mk_buf(mk); T.BSr = mk_buf(mk); T.BSc = mk_buf(mk);
+        T.Pu = mk_buf(mq); T.Qv = mk_buf(mq); T.Bc1 = mk_buf(mq); T.Bc2 = mk_buf(mq);
+        dfree(R.BY); dfree(R.Z);
+        dalloc(R.BY, nk);
+        dalloc(R.Z, nk);
+        R.n = h->n;
+        R.kz = kz;
+        R.have_fwd = false;
+    }
+    if (R.pcap < L.total) {
+        dfree(R.P); dfree(R.G);
+        dalloc(R.P, L.total);
+        dalloc(R.G, L.total);
+        R.pcap = L.total;
+    }
+    if (!R.part) dalloc(R.part, 4096 * 3);
+    TrainDev& T = R.T;
+    T.n = h->n; T.K = L.k; T.D = L.depth; T.M = L.m; T.kz = kz;
+    T.tile_base = L.tile_base; T.bridge_base = L.bridge_base; T.gate_base = L.gate_base;
+    T.a_diag = h->a_diag;
+    T.shift = shift;
+}
+const double* train_params(hfpg_handle* h, const double* params, uint64_t total, int where) {
+    if (where == HFPG_DEVICE) return params;
+    CK(cudaMemcpyAsync(h->tr.P, params, total * 8, cudaMemcpyHostToDevice, h->stream));
+    return h->tr.P;
+}
+// Y = A X for a kz-wide row-major batch (csr.cpp:87-100 spmm; SELL slots in column order).
+void train_spmm(hfpg_handle* h, const double* X, double* Y, uint64_t kz) {
+    const unsigned long long* so = h->slice_off;
+    const uint32_t* sc = h->sell_cols;
+    const double* sv = h->sell_vals;
+    const uint64_t n = h->n;
+    each(h->stream, n * kz, [=] __device__(uint64_t t) {
+        const uint64_t row = t / kz, j = t % kz, sl = row >> 5, lane = row & 31;
+        const uint64_t b = so[sl], w = (so[sl + 1] - b) >> 5;
+        double y = 0.0;
+        for (uint64_t q = 0; q < w; ++q) {
+            const uint64_t idx = b + q * 32 + lane;
+            y = fma(sv[idx], X[uint64_t(sc[idx]) * kz + j], y);
+        }
+        Y[t] = y;
+    });
+}
+// Deterministic sums of NV per-element functions over cnt elements: block partials on the
+// device, then the blocks' partials added in block order on the host.
+template <int NV, class F>
+void train_sums(hfpg_handle* h, uint64_t cnt, F f, double (&out)[NV]) {
+    const unsigned blocks = unsigned(std::min<uint64_t>((cnt + 255) / 256, 4096 / NV));
+    double* part = h->tr.part;
+    auto kern = [=] __device__(uint64_t b) {
+        double acc[NV];
+        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+        for (uint64_t t = b; t < cnt; t += blocks) {
+            double e[NV];
+            f(t, e);
+            for (int v = 0; v < NV; ++v) acc[v] += e[v];
+        }
+        for (int v = 0; v < NV; ++v) part[b * NV + v] = acc[v];
+    };
+    each(h->stream, blocks, kern);
+    std::vector<double> hp(size_t(blocks) * NV);
+    CK(cudaMemcpyAsync(hp.data(), part, hp.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    for (int v = 0; v < NV; ++v) {
+        out[v] = 0.0;
+        for (unsigned b = 0; b < blocks; ++b) out[v] += hp[size_t(b) * NV + v];
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -1131,6 +1234,8 @@ int hfpg_destroy(hfpg_handle* h) {
             if (h->pin_ev[q]) cudaEventDestroy(h->pin_ev[q]);
         }
         dfree(h->crc_scratch);
+        for (double* b : h->tr.bufs) dfree(b);
+        dfree(h->tr.P); dfree(h->tr.G); dfree(h->tr.BY); dfree(h->tr.Z); dfree(h->tr.part);
         if (h->stream) cudaStreamDestroy(h->stream);
         delete h;
     });
@@ -1980,6 +2085,140 @@ int hfpg_load_checkpoint(hfpg_handle* h, const char* path) {
 
 int hfpg_load_mppf(hfpg_handle* h, const char* path) {
     return guarded([&] { frame_from_mppf(h, path); });
+}
+
+
+// ---- training (adjoint.cpp, loss.cpp, train.cpp) ---------------------------
+int hfpg_batch_apply(hfpg_handle* h, const double* params, uint64_t leaf, uint64_t ls, double shift,
+                     const double* x, uint64_t kz, double* y, int where) {
+    return guarded([&] {
+        set_device(h);
+        train_prepare(h, leaf, ls, kz, shift);
+        const Layout L = make_layout(h->n, leaf, ls);
+        const double* P = train_params(h, params, L.total, where);
+        auto& T = h->tr.T;
+        CK(cudaMemcpyAsync(T.X, x, h->n * kz * 8, where == HFPG_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                           h->stream));
+        train_forward(h->stream, T, P);
+        CK(cudaGetLastError());
+        if (y) CK(cudaMemcpyAsync(y, T.Y, h->n * kz * 8, where == HFPG_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                                  h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        h->tr.have_fwd = true;
+    });
+}
+
+int hfpg_batch_adjoint(hfpg_handle* h, const double* params, const double* bar_y, double* grad, int where) {
+    return guarded([&] {
+        set_device(h);
+        auto& R = h->tr;
+        if (!R.have_fwd) throw InvalidArgument("factor_apply_batch_adjoint: no forward batch on this handle");
+        const Layout L = make_layout(h->n, 128, 32);
+        const double* P = train_params(h, params, L.total, where);
+        const uint64_t nk = h->n * R.kz;
+        const double* BY = bar_y;
+        if (where == HFPG_HOST) {
+            CK(cudaMemcpyAsync(R.BY, bar_y, nk * 8, cudaMemcpyHostToDevice, h->stream));
+            BY = R.BY;
+        }
+        double* G = where == HFPG_HOST ? R.G : grad;
+        CK(cudaMemsetAsync(G, 0, L.total * 8, h->stream));
+        train_adjoint(h->stream, R.T, P, BY, G);
+        CK(cudaGetLastError());
+        if (where == HFPG_HOST) CK(cudaMemcpyAsync(grad, R.G, L.total * 8, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+// adjoint.cpp:250-292 loss_gradient (kind 0 cosine, 1 sai) on the handle's system.
+int hfpg_loss_gradient(hfpg_handle* h, const double* params, uint64_t leaf, uint64_t ls, double shift,
+                       const double* z, uint64_t kz, int32_t kind, double norm_a, double* loss,
+                       int32_t* degenerate, double* grad, int where) {
+    return guarded([&] {
+        set_device(h);
+        if (kind != 0 && kind != 1) throw InvalidArgument("loss_gradient: unknown loss kind");
+        if (kind == 1 && !(norm_a > 0.0)) throw InvalidArgument("sai_loss: norm_a must be positive");
+        train_prepare(h, leaf, ls, kz, shift);
+        const Layout L = make_layout(h->n, leaf, ls);
+        const double* P = train_params(h, params, L.total, where);
+        auto& R = h->tr;
+        auto& T = R.T;
+        const uint64_t nk = h->n * kz;
+        double* Z = R.Z;
+        CK(cudaMemcpyAsync(Z, z, nk * 8, where == HFPG_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, h->stream));
+        double* G = where == HFPG_HOST ? R.G : grad;
+        CK(cudaMemsetAsync(G, 0, L.total * 8, h->stream));
+        double* BY = R.BY;
+        *degenerate = 0;
+        if (kind == 0) {  // Y = M (A Z), 1 - cos(Z, Y)
+            train_spmm(h, Z, T.X, kz);
+            train_forward(h->stream, T, P);
+            const double* Y = T.Y;
+            double s3[3];
+            train_sums<3>(h, nk, [=] __device__(uint64_t i, double (&e)[3]) {
+                e[0] = Z[i] * Y[i];
+                e[1] = Z[i] * Z[i];
+                e[2] = Y[i] * Y[i];
+            }, s3);
+            const double zy = s3[0], zz = s3[1], yy = s3[2];
+            if (zz == 0.0 || yy == 0.0) {
+                *degenerate = 1;
+                *loss = 0.0;
+            } else {
+                const double nz = std::sqrt(zz), ny = std::sqrt(yy);
+                *loss = 1.0 - zy / (nz * ny);
+                const double c1 = 1.0 / (nz * ny), c2 = zy / (nz * ny * ny * ny);
+                each(h->stream, nk, [=] __device__(uint64_t i) { BY[i] = -(Z[i] * c1 - Y[i] * c2); });
+                train_adjoint(h->stream, T, P, BY, G);
+            }
+        } else {  // W = M Z; |(1/normA) A W - Z|^2
+            CK(cudaMemcpyAsync(T.X, Z, nk * 8, cudaMemcpyDeviceToDevice, h->stream));
+            train_forward(h->stream, T, P);
+            double* Q = T.W;  // scratch until the adjoint (which rewrites W)
+            train_spmm(h, T.Y, Q, kz);
+            each(h->stream, nk, [=] __device__(uint64_t i) { Q[i] = Q[i] / norm_a - Z[i]; });
+            double s1[1];
+            train_sums<1>(h, nk, [=] __device__(uint64_t i, double (&e)[1]) { e[0] = Q[i] * Q[i]; }, s1);
+            *loss = s1[0];
+            train_spmm(h, Q, BY, kz);
+            const double scale = 2.0 / norm_a;
+            each(h->stream, nk, [=] __device__(uint64_t i) { BY[i] *= scale; });
+            train_adjoint(h->stream, T, P, BY, G);
+        }
+        CK(cudaGetLastError());
+        if (where == HFPG_HOST) CK(cudaMemcpyAsync(grad, R.G, L.total * 8, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        R.have_fwd = true;
+    });
+}
+
+// train.cpp:136-160: global clip of g to clip_norm, then AdamW with decoupled weight decay
+// (device pointers, count elements, step >= 1).
+int hfpg_adamw_step(hfpg_handle* h, double* params, double* grad, double* m1, double* m2, uint64_t count,
+                    uint64_t step, double lr, double beta1, double beta2, double eps, double weight_decay,
+                    double clip_norm, double* gnorm_out) {
+    return guarded([&] {
+        set_device(h);
+        if (step == 0) throw InvalidArgument("adamw: step counts from 1");
+        if (!h->tr.part) dalloc(h->tr.part, 4096 * 3);
+        const double* g = grad;
+        double s1[1];
+        train_sums<1>(h, count, [=] __device__(uint64_t i, double (&e)[1]) { e[0] = g[i] * g[i]; }, s1);
+        const double gnorm = std::sqrt(s1[0]);
+        if (gnorm_out) *gnorm_out = gnorm;
+        const double s = (gnorm > clip_norm && gnorm > 0.0) ? clip_norm / gnorm : 1.0;
+        const double bc1 = 1.0 - std::pow(beta1, double(step)), bc2 = 1.0 - std::pow(beta2, double(step));
+        each(h->stream, count, [=] __device__(uint64_t i) {
+            const double gi = s == 1.0 ? grad[i] : grad[i] * s;
+            grad[i] = gi;
+            m1[i] = beta1 * m1[i] + (1.0 - beta1) * gi;
+            m2[i] = beta2 * m2[i] + (1.0 - beta2) * gi * gi;
+            const double mhat = m1[i] / bc1, vhat = m2[i] / bc2;
+            params[i] -= lr * (mhat / (sqrt(vhat) + eps) + weight_decay * params[i]);
+        });
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(h->stream));
+    });
 }
 
 }  // extern "C"
