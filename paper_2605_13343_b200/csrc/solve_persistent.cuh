@@ -409,78 +409,86 @@ __device__ __forceinline__ void p_tile(const DevSys& s, uint64_t m, double sr_p,
 // lane q holds leaf q, and a shuffle butterfly builds the pairwise f64 up-sweep (after the step
 // of distance d every lane holds its (2d)-group's sum = left child + right child, exactly the
 // heap sums node[u] = node[2u+1] + node[2u+2]); the first lane of each group writes the node.
-// No shared memory, no block barrier. The last CTA to finish among S2 sibling subtrees
-// (arrival counter) continues one level up with their roots as its leaves, to the tree root.
+// No shared memory, no block barrier, no arrival hop: the levels above the group roots are never
+// materialised (R <= 32 groups in the persistent regime); the tiles phase sums the roots it needs.
 __device__ __forceinline__ void p_sums_phase(const DevSys& s, PSmem& sm) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t K = s.K, D = s.D;
-    const uint64_t S0 = K < kCoarseS0 ? K : kCoarseS0, R = K / S0;
+    const uint64_t S = K < kCoarseS0 ? K : kCoarseS0, R = K / S;
+    int logS = 0;
+    while ((1ULL << logS) < S) ++logS;
+    const uint64_t dr = D - logS;
     const int side = warp >> 3, c0 = 4 * (warp & 7);  // side 0: u columns, 1: v columns
     double* node = side ? s.node_v : s.node_u;
-    for (uint64_t task0 = blockIdx.x; task0 < R; task0 += gridDim.x) {
-        uint64_t task = task0, dlo = D;
-        for (int level = 0;; ++level) {
-            const bool pr = task0 == blockIdx.x && level < 3;
-            if (pr) PROBE(44 + 4 * level);
-            const uint64_t cnt = 1ULL << dlo;
-            const uint64_t S = cnt < kCoarseS0 ? cnt : kCoarseS0;
-            int logS = 0;
-            while ((1ULL << logS) < S) ++logS;
-            const uint64_t dr = dlo - logS;
-            double v[4] = {0.0, 0.0, 0.0, 0.0};
-            if (uint64_t(lane) < S) {
-                if (level == 0) {
-                    const float4 f = __ldcg(reinterpret_cast<const float4*>(
-                        &s.restrict_[(task * S + lane) * 64 + 32 * side + c0]));
-                    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-                } else {
-                    const uint64_t g = (1ULL << dlo) - 1 + task * S + lane;
-                    const double2 a = __ldcg(reinterpret_cast<const double2*>(&node[g * 32 + c0]));
-                    const double2 bb = __ldcg(reinterpret_cast<const double2*>(&node[g * 32 + c0 + 2]));
-                    v[0] = a.x; v[1] = a.y; v[2] = bb.x; v[3] = bb.y;
-                }
-            }
-            for (int l2 = 0; l2 < logS; ++l2) {  // step 2^l2 -> nodes at local depth logS-1-l2
-                const int d = 1 << l2;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) v[c] += __shfl_xor_sync(0xffffffffu, v[c], d);
-                const int ld = logS - 1 - l2;
-                if (uint64_t(lane) < S && (lane & (2 * d - 1)) == 0) {
-                    const uint64_t g = (1ULL << (dr + ld)) - 1 + task * (1ULL << ld) + uint64_t(lane >> (l2 + 1));
-                    __stcg(reinterpret_cast<double2*>(&node[g * 32 + c0]), make_double2(v[0], v[1]));
-                    __stcg(reinterpret_cast<double2*>(&node[g * 32 + c0 + 2]), make_double2(v[2], v[3]));
-                }
-            }
-            if (pr) PROBE(45 + 4 * level);
-            if (dr == 0) break;
-            __threadfence();
-            __syncthreads();
-            const uint64_t cnt2 = 1ULL << dr;
-            const uint64_t S2 = cnt2 < kCoarseS0 ? cnt2 : kCoarseS0;
-            int logS2 = 0;
-            while ((1ULL << logS2) < S2) ++logS2;
-            if (tid == 0) {
-                const uint64_t parent = (1ULL << (dr - logS2)) - 1 + task / S2;
-                const unsigned t = atomicAdd(&s.tree_counters[parent], 1u);
-                sm.last = (t == S2 - 1);
-                if (sm.last) s.tree_counters[parent] = 0u;
-            }
-            __syncthreads();
-            if (pr) PROBE(46 + 4 * level);
-            if (!sm.last) break;
-            __threadfence();
-            task /= S2;
-            dlo = dr;
+    (void)sm;
+    for (uint64_t task = blockIdx.x; task < R; task += gridDim.x) {
+        const bool pr = task == blockIdx.x;
+        if (pr) PROBE(44);
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
+        if (uint64_t(lane) < S) {
+            const float4 f = __ldcg(reinterpret_cast<const float4*>(&s.restrict_[(task * S + lane) * 64 + 32 * side + c0]));
+            v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
         }
+        for (int l2 = 0; l2 < logS; ++l2) {  // step 2^l2 -> nodes at local depth logS-1-l2
+            const int d = 1 << l2;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[c] += __shfl_xor_sync(0xffffffffu, v[c], d);
+            const int ld = logS - 1 - l2;
+            if (uint64_t(lane) < S && (lane & (2 * d - 1)) == 0) {
+                const uint64_t g = (1ULL << (dr + ld)) - 1 + task * (1ULL << ld) + uint64_t(lane >> (l2 + 1));
+                __stcg(reinterpret_cast<double2*>(&node[g * 32 + c0]), make_double2(v[0], v[1]));
+                __stcg(reinterpret_cast<double2*>(&node[g * 32 + c0 + 2]), make_double2(v[2], v[3]));
+            }
+        }
+        if (pr) PROBE(45);
     }
+}
+
+// Pairwise (heap-order) sum of W (a power of two) consecutive group roots at depth dr, lane =
+// column: the value the up-sweep would have stored in their common ancestor. Blocks of 8 are
+// summed in registers; block sums merge through a binary-counter stack (the same tree).
+__device__ __forceinline__ double p_root_sum(const double* node, uint64_t dr, uint64_t g0, uint64_t W, int lane) {
+    const double* base = node + ((1ULL << dr) - 1 + g0) * 32 + lane;
+    if (W <= 8) {
+        double v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (uint64_t(i) < W) v[i] = __ldcg(base + i * 32);
+#pragma unroll
+        for (int w = 1; w < 8; w *= 2)
+#pragma unroll
+            for (int i = 0; i + w < 8; i += 2 * w)
+                if (uint64_t(i + w) < W) v[i] = v[i] + v[i + w];
+        return v[0];
+    }
+    double stack[24];
+    int top = 0;
+    for (uint64_t b = 0; b < W / 8; ++b) {
+        double v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = __ldcg(base + (b * 8 + i) * 32);
+#pragma unroll
+        for (int w = 1; w < 8; w *= 2)
+#pragma unroll
+            for (int i = 0; i + w < 8; i += 2 * w) v[i] = v[i] + v[i + w];
+        double x = v[0];
+        for (uint64_t c = b + 1; (c & 1) == 0; c >>= 1) x = stack[--top] + x;  // merge equal subtrees
+        stack[top++] = x;
+    }
+    return stack[0];
 }
 
 // Tile couplings (apply.cpp:121-138): every tile in parallel, one warp each, dealt across CTAs
 // first (tile order t -> CTA t mod grid). Children sums come from the node arrays (leaf children:
-// the restrictions themselves).
+// the restrictions themselves); tiles above the 32-leaf groups sum their children's group roots
+// pairwise themselves (p_root_sum), so the strip-sum phase needs no arrival hop.
 __device__ __forceinline__ void p_tiles_phase(const DevSys& s, PSmem& sm, PTileScratch* ws, uint64_t pol) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t K = s.K, G = gridDim.x;
+    const uint64_t S0 = K < kCoarseS0 ? K : kCoarseS0, R = K / S0;
+    int logS0 = 0;
+    while ((1ULL << logS0) < S0) ++logS0;
+    const uint64_t dr = s.D - logS0;  // depth of the group roots (R <= 32 in the persistent regime)
     for (uint64_t m = uint64_t(wid) * G + blockIdx.x; m < K - 1; m += G * kPWarps) {
         if (m == 0) PROBE(56);
         const uint64_t l = 2 * m + 1, r = 2 * m + 2;  // children (heap)
@@ -488,6 +496,12 @@ __device__ __forceinline__ void p_tiles_phase(const DevSys& s, PSmem& sm, PTileS
         if (l >= K - 1) {
             a = double(__ldcg(&s.restrict_[(l - (K - 1)) * 64 + lane]));
             bb = double(__ldcg(&s.restrict_[(r - (K - 1)) * 64 + 32 + lane]));
+        } else if (m + 1 < R) {  // above the 32-leaf groups: the children's sums from the group roots
+            int d = 0;
+            while ((2ULL << d) <= m + 1) ++d;
+            const uint64_t wg = R >> d, g0 = (m + 1 - (1ULL << d)) * wg, W = wg / 2;
+            a = p_root_sum(s.node_u, dr, g0, W, lane);
+            bb = p_root_sum(s.node_v, dr, g0 + W, W, lane);
         } else {
             a = __ldcg(&s.node_u[l * 32 + lane]);
             bb = __ldcg(&s.node_v[r * 32 + lane]);
