@@ -1093,6 +1093,9 @@ __global__ void __launch_bounds__(kSumsThreads) k_sums_tree(DevSys s, int mode) 
     while ((1ULL << logS0) < S0) ++logS0;
     // level 0: subtrees of S0 leaves, dealt round-robin
     for (uint64_t task = blockIdx.x; task < R; task += gridDim.x) sweep_leaves(s, D, task, S0);
+    // single rank: no levels above the group roots — k_tiles_all's upper tiles sum the roots
+    // they need themselves (tile_root_sums), so there is no arrival hop or serial sweep here
+    if (s.G == 1) return;
     // upper levels: groups of up to 512 nodes; the last CTA of each level continues
     uint64_t dlo = D - logS0, cnt = R;  // current level: cnt nodes at depth dlo
     unsigned* counter = s.tree_counters;
@@ -1149,6 +1152,78 @@ __global__ void __launch_bounds__(kSumsThreads) k_sums_tree(DevSys s, int mode) 
 // residual bookkeeping with the rank-ordered |r|^2 (r0 at init, rel / history / stop in the
 // loop — pcg.cpp:73-112) and computes the G-1 top tiles from the rank-root sums (same pairwise
 // order as a single-rank up-sweep), identically on every rank.
+// Pairwise (heap-order) sum of n (a power of two) consecutive nodes at depth d, lane = column:
+// blocks of 8 in registers, block sums merged through a binary-counter stack (the same tree).
+__device__ __forceinline__ double pairwise_nodes(const double* node, uint64_t d, uint64_t p0, uint64_t n, int lane) {
+    const double* base = node + ((1ULL << d) - 1 + p0) * 32 + lane;
+    if (n <= 8) {
+        double v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (uint64_t(i) < n) v[i] = __ldcg(base + i * 32);
+#pragma unroll
+        for (int w = 1; w < 8; w *= 2)
+#pragma unroll
+            for (int i = 0; i + w < 8; i += 2 * w)
+                if (uint64_t(i + w) < n) v[i] = v[i] + v[i + w];
+        return v[0];
+    }
+    double stack[24];
+    int top = 0;
+    for (uint64_t b = 0; b < n / 8; ++b) {
+        double v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = __ldcg(base + (b * 8 + i) * 32);
+#pragma unroll
+        for (int w = 1; w < 8; w *= 2)
+#pragma unroll
+            for (int i = 0; i + w < 8; i += 2 * w) v[i] = v[i] + v[i + w];
+        double x = v[0];
+        for (uint64_t c = b + 1; (c & 1) == 0; c >>= 1) x = stack[--top] + x;
+        stack[top++] = x;
+    }
+    return stack[0];
+}
+// The strip sums of tile m < R - 1 (above the 32-leaf groups) from the group roots, by all 8
+// warps of the CTA: each sums an aligned eighth of each child's roots pairwise, warp 0 merges the
+// eight partials pairwise — the heap-order tree of the up-sweep, so the sums equal the node sums
+// a full sweep would have stored. All threads call it (contains block barriers).
+constexpr int kTileRootWarps = 8;
+__device__ __forceinline__ void tile_root_sums(const DevSys& s, uint64_t m, uint64_t R, uint64_t dr,
+                                               double* sr_out, double* sc_out) {
+    __shared__ double part[2][kTileRootWarps][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int d = 0;
+    while ((2ULL << d) <= m + 1) ++d;
+    const uint64_t wg = R >> d, g0 = (m + 1 - (1ULL << d)) * wg, W = wg / 2;  // W roots per child
+    const uint64_t per = W >= kTileRootWarps ? W / kTileRootWarps : 1;
+    const uint64_t nw = W >= kTileRootWarps ? kTileRootWarps : 1;
+    if (uint64_t(wid) < nw) {
+        part[0][wid][lane] = pairwise_nodes(s.node_u, dr, g0 + wid * per, nw == 1 ? W : per, lane);
+        part[1][wid][lane] = pairwise_nodes(s.node_v, dr, g0 + W + wid * per, nw == 1 ? W : per, lane);
+    }
+    __syncthreads();
+    if (wid == 0) {
+        double u[kTileRootWarps], v[kTileRootWarps];
+#pragma unroll
+        for (int q = 0; q < kTileRootWarps; ++q) {
+            u[q] = uint64_t(q) < nw ? part[0][q][lane] : 0.0;
+            v[q] = uint64_t(q) < nw ? part[1][q][lane] : 0.0;
+        }
+#pragma unroll
+        for (int w = 1; w < kTileRootWarps; w *= 2)
+#pragma unroll
+            for (int q = 0; q + w < kTileRootWarps; q += 2 * w)
+                if (uint64_t(q + w) < nw) {
+                    u[q] = u[q] + u[q + w];
+                    v[q] = v[q] + v[q + w];
+                }
+        sr_out[lane] = u[0];
+        sc_out[lane] = v[0];
+    }
+    __syncthreads();
+}
+
 constexpr int kTilesThreads = 256;  // 98 registers: two CTAs per SM
 __global__ void __launch_bounds__(kTilesThreads) k_tiles_all(DevSys s, int mode) {
     if (mode != kApply && s.sc->done) return;
@@ -1199,7 +1274,24 @@ __global__ void __launch_bounds__(kTilesThreads) k_tiles_all(DevSys s, int mode)
         }
     }
     const uint64_t K = s.K, G = gridDim.x;
-    for (uint64_t m = uint64_t(wid) * G + blockIdx.x; m < K - 1; m += G * (kTilesThreads / 32)) {
+    const uint64_t S0 = K < kCoarseS0 ? K : kCoarseS0, R = K / S0;
+    int logS0 = 0;
+    while ((1ULL << logS0) < S0) ++logS0;
+    const uint64_t dr = s.D - logS0;  // depth of the group roots
+    // single rank: the R - 1 tiles above the 32-leaf groups first, one per CTA at a time, their
+    // children's sums from the group roots by all 8 warps (tile_root_sums); then the group-internal
+    // tiles, one per warp. Partitioned ranks: every tile from the node sums of k_sums_tree.
+    const uint64_t first = s.G == 1 ? R - 1 : 0;
+    if (s.G == 1) {
+        __shared__ double up_sr[32], up_sc[32];
+        for (uint64_t m = blockIdx.x; m + 1 < R; m += G) {
+            tile_root_sums(s, m, R, dr, up_sr, up_sc);
+            if (wid == 0)
+                tile_couple(s.F + s.tile_base + m * (kLs * kLs), up_sr[lane], up_sc[lane], ws[0], lane, pol,
+                            s.coupled + m * 64);
+        }
+    }
+    for (uint64_t m = first + uint64_t(wid) * G + blockIdx.x; m < K - 1; m += G * (kTilesThreads / 32)) {
         const uint64_t l = 2 * m + 1, r = 2 * m + 2;  // children (heap)
         double a, bb;
         if (l >= K - 1) {
