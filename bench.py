@@ -157,9 +157,15 @@ def max_over_ranks(v: float, world: int, local: int) -> float:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+    dev = "cpu" if dist.get_backend() == "gloo" else f"cuda:{local}"  # gloo: the CPU multi-process tests
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def frames_of(rank: int, world: int, frames: int) -> list:
+    """configs[3]'s sharding: frame i on rank i mod N (no collective on the solve path)."""
+    return list(range(rank, frames, world))
 
 
 def barrier(world):
@@ -359,7 +365,7 @@ def run_batch(args, cfg):
     torch.cuda.set_device(local)
     import paper_2605_13343_b200 as H
     from paper_2605_13343_b200 import _native as N
-    mine = list(range(rank, cfg["frames"], world))
+    mine = frames_of(rank, world, cfg["frames"])
     devs, bs, xs, its = [], [], [], []
     for i in mine:
         fr, f = make_inputs(cfg, i)
