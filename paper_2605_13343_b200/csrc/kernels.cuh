@@ -726,194 +726,6 @@ __global__ void __launch_bounds__(256) k_leaf_generic(DevSys s, int mode, const 
 // computes its internal tiles, publishes its root sums, and the last-arriving CTA of each
 // group of siblings carries on one level up — one launch covers the whole tree.
 // ============================================================================================
-// Sum 16 per-lane values over the warp: afterwards lane L holds the total of column L >> 1
-// (recursive halving; 16 shuffles instead of 16 x 5).
-__device__ __forceinline__ float transpose_reduce16(const float (&a)[16], int lane) {
-    float t8[8], t4[4], t2[2];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const bool hi = lane & 16;
-        t8[i] = (hi ? a[i + 8] : a[i]) + __shfl_xor_sync(0xffffffffu, hi ? a[i] : a[i + 8], 16);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const bool hi = lane & 8;
-        t4[i] = (hi ? t8[i + 4] : t8[i]) + __shfl_xor_sync(0xffffffffu, hi ? t8[i] : t8[i + 4], 8);
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const bool hi = lane & 4;
-        t2[i] = (hi ? t4[i + 2] : t4[i]) + __shfl_xor_sync(0xffffffffu, hi ? t4[i] : t4[i + 2], 4);
-    }
-    const bool hi = lane & 2;
-    float t1 = (hi ? t2[1] : t2[0]) + __shfl_xor_sync(0xffffffffu, hi ? t2[0] : t2[1], 2);
-    return t1 + __shfl_xor_sync(0xffffffffu, t1, 1);
-}
-
-// One tile (L_s = 32, rank 16) per warp. Lane p holds row p of U_m and V_m (registers) and
-// stages them in the warp's shared scratch; lanes q < 16 then run the fp32 chain
-// coef_r[q] = sum_p U[p][q] float(s_r[p]) and lanes 16 + q the chain for V^T float(s_c), in
-// p order exactly like matvec_t; lane j finishes coupled_col[j] = float(sum_q V[j][q] coef_r[q])
-// and coupled_row[j] = float(sum_q U[j][q] coef_c[q]) in f64 like matvec (apply.cpp:125-137).
-__device__ __forceinline__ void tile_warp32(const float4 (&u4)[4], const float4 (&v4)[4],
-                                            const double* sr, const double* sc, int lane,
-                                            float* scratch, float* ccol, float* crow) {
-    float4* T4 = reinterpret_cast<float4*>(scratch);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        T4[lane * 4 + i] = u4[i];
-        T4[132 + lane * 4 + i] = v4[i];  // V at +528 floats: the two half-warps hit disjoint banks
-    }
-    __syncwarp();
-    const int q = lane & 15;
-    const float* col = scratch + (lane < 16 ? 0 : 528) + q;
-    const double* st = lane < 16 ? sr : sc;
-    float coef = 0.f;
-#pragma unroll
-    for (int p = 0; p < 32; ++p) coef = fmaf(col[p * 16], float(st[p]), coef);
-    double acc_c = 0.0, acc_r = 0.0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float uu[4] = {u4[i].x, u4[i].y, u4[i].z, u4[i].w};
-        const float vv[4] = {v4[i].x, v4[i].y, v4[i].z, v4[i].w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int qq = 4 * i + t;
-            const float cr = __shfl_sync(0xffffffffu, coef, qq);       // (U^T s_r)[qq]
-            const float cc = __shfl_sync(0xffffffffu, coef, 16 + qq);  // (V^T s_c)[qq]
-            acc_c += double(vv[t]) * double(cr);
-            acc_r += double(uu[t]) * double(cc);
-        }
-    }
-    ccol[lane] = float(acc_c);
-    crow[lane] = float(acc_r);
-    __syncwarp();
-}
-
-// Tile factors are re-read every iteration and total 4 (K-1) L_s^2 bytes (33.5 MB at N=1M):
-// load them with an evict_last policy so they stay L2-resident while F streams past.
-__device__ __forceinline__ void load_tile32(const DevSys& s, uint64_t m, int lane, float4 (&u4)[4],
-                                            float4 (&v4)[4], uint64_t pol) {
-    const float4* U = reinterpret_cast<const float4*>(s.F + s.tile_base + m * 1024) + lane * 4;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        u4[i] = ldg_hint(U + i, pol);
-        v4[i] = ldg_hint(U + 128 + i, pol);  // V_m = U_m + 32 x 16 floats
-    }
-}
-
-// Coarse stage, fast path (L_s = 32), part 1 — strip sums. Each CTA owns an aligned subtree of
-// up to 32 leaves, loads their restrictions (û | v̂, fp32) and runs the f64 up-sweep in shared
-// memory; every internal node's sums (root included) go to the heap-indexed node arrays.
-__global__ void __launch_bounds__(256) k_coarse_sums(DevSys s, int mode) {
-    if (mode != kApply && s.sc->done) return;
-    __shared__ double SU[63 * 32], SV[63 * 32];
-    const int tid = threadIdx.x;
-    const uint64_t task = blockIdx.x, D = s.D;
-    const uint64_t S = s.K < kCoarseS0 ? s.K : kCoarseS0;
-    int logS = 0;
-    while ((1ULL << logS) < S) ++logS;
-    const uint64_t dr = D - logS;
-    {   // all loads issued before any store
-        double bu[4], bv[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const uint64_t e = uint64_t(tid) + 256u * t, q = e >> 5, j = e & 31;
-            if (e < S * 32) {
-                bu[t] = double(__ldg(&s.restrict_[(task * S + q) * 64 + j]));
-                bv[t] = double(__ldg(&s.restrict_[(task * S + q) * 64 + 32 + j]));
-            }
-        }
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const uint64_t e = uint64_t(tid) + 256u * t;
-            if (e < S * 32) {
-                SU[(S - 1) * 32 + e] = bu[t];
-                SV[(S - 1) * 32 + e] = bv[t];
-            }
-        }
-    }
-    __syncthreads();
-    for (int ld = logS - 1; ld >= 0; --ld) {
-        const uint64_t u0 = (1ULL << ld) - 1;
-        for (uint64_t e = tid; e < (1ULL << ld) * 32; e += blockDim.x) {
-            const uint64_t u = u0 + (e >> 5), j = e & 31;
-            const double a = SU[(2 * u + 1) * 32 + j] + SU[(2 * u + 2) * 32 + j];
-            const double b = SV[(2 * u + 1) * 32 + j] + SV[(2 * u + 2) * 32 + j];
-            SU[u * 32 + j] = a;
-            SV[u * 32 + j] = b;
-            const uint64_t g = (1ULL << (dr + ld)) - 1 + task * (1ULL << ld) + (u - u0);
-            s.node_u[g * 32 + j] = a;
-            s.node_v[g * 32 + j] = b;
-        }
-        __syncthreads();
-    }
-}
-
-// Coarse stage, fast path, part 2 — every tile in parallel. Tiles whose children lie inside the
-// 32-leaf subtrees take one warp each and read the children's sums directly (leaf children:
-// the restrictions themselves); each tile above them takes a whole CTA whose 8 warps split the
-// sum over the subtree roots of its halves. Then the exact-order tile chain (tile_warp32).
-constexpr int kTileWarps = 8;
-__global__ void __launch_bounds__(32 * kTileWarps) k_coarse_tiles(DevSys s, int mode) {
-    if (mode != kApply && s.sc->done) return;
-    __shared__ __align__(16) float scratch[kTileWarps][1056];
-    __shared__ double sr[kTileWarps][32], sc[kTileWarps][32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t K = s.K, D = s.D;
-    const uint64_t S = K < kCoarseS0 ? K : kCoarseS0;
-    const uint64_t R = K / S;            // subtree roots, at depth dr
-    const uint64_t upper = R - 1;        // tiles above the roots: one CTA each
-    const uint64_t pol_keep = policy_evict_last();
-    uint64_t m;
-    if (blockIdx.x < upper) {
-        m = blockIdx.x;
-        int d = 0;
-        while ((2ULL << d) <= m + 1) ++d;
-        const uint64_t w = R >> d, a = (m + 1 - (1ULL << d)) * w, g0 = R - 1;
-        double pu = 0.0, pv = 0.0;
-        for (uint64_t t = warp; t < w / 2; t += kTileWarps) {
-            pu += __ldg(&s.node_u[(g0 + a + t) * 32 + lane]);
-            pv += __ldg(&s.node_v[(g0 + a + w / 2 + t) * 32 + lane]);
-        }
-        sr[warp][lane] = pu;
-        sc[warp][lane] = pv;
-        __syncthreads();
-        if (warp != 0) return;
-        float4 u4[4], v4[4];
-        load_tile32(s, m, lane, u4, v4, pol_keep);
-        double tu = 0.0, tv = 0.0;
-#pragma unroll
-        for (int q = 0; q < kTileWarps; ++q) {
-            tu += sr[q][lane];
-            tv += sc[q][lane];
-        }
-        __syncwarp();
-        sr[0][lane] = tu;
-        sc[0][lane] = tv;
-        __syncwarp();
-        tile_warp32(u4, v4, sr[0], sc[0], lane, scratch[0], s.coupled + m * 64 + 32, s.coupled + m * 64);
-        return;
-    }
-    m = upper + (uint64_t(blockIdx.x) - upper) * kTileWarps + warp;
-    if (m >= K - 1) return;
-    float4 u4[4], v4[4];
-    load_tile32(s, m, lane, u4, v4, pol_keep);
-    const uint64_t l = 2 * m + 1, r = 2 * m + 2;  // children (heap)
-    double a, b;
-    if (l >= K - 1) {  // leaf children: their restrictions
-        a = double(__ldg(&s.restrict_[(l - (K - 1)) * 64 + lane]));
-        b = double(__ldg(&s.restrict_[(r - (K - 1)) * 64 + 32 + lane]));
-    } else {
-        a = __ldg(&s.node_u[l * 32 + lane]);
-        b = __ldg(&s.node_v[r * 32 + lane]);
-    }
-    sr[warp][lane] = a;
-    sc[warp][lane] = b;
-    __syncwarp();
-    tile_warp32(u4, v4, sr[warp], sc[warp], lane, scratch[warp], s.coupled + m * 64 + 32, s.coupled + m * 64);
-}
-
 
 // ============================================================================================
 // Coarse stage, graph path (also the row-partitioned solve): strip sums, then every tile.

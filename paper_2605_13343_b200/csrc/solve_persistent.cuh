@@ -345,7 +345,7 @@ __device__ __forceinline__ double p_leaf_phase(const DevSys& s, PSmem& sm, PLeaf
     return rr;
 }
 
-// One tile (L_s = 32, rank 16) per warp, like tile_warp32 without the shared transpose:
+// One tile (L_s = 32, rank 16) per warp:
 // lanes q < 16 read column q of U_m (lanes 16 + q: of V_m) straight from L2 (64 contiguous
 // bytes per half-warp per row) and run the fp32 chain coef = sum_p U[p][q] float(s_r[p]) in p
 // order (matvec_t); lane j then forms coupled_col[j] = float(sum_q V[j][q] coef_r[q]) and
