@@ -719,12 +719,13 @@ __global__ void __launch_bounds__(256) k_leaf_generic(DevSys s, int mode, const 
 }
 
 // ============================================================================================
-// Coarse kernel: apply stage 4 (apply.cpp:110-138) over the bisection tree in heap order
+// Coarse stage (apply stage 4, apply.cpp:110-138) over the bisection tree in heap order
 // (tile m = heap node m; its rows are the left child's leaves, its columns the right child's).
 // s_r(m) = Σ û over the left child, s_c(m) = Σ v̂ over the right child: an f64 up-sweep. Each
 // CTA owns an aligned subtree of up to 32 leaves (or of 32 subtree roots at higher levels),
 // computes its internal tiles, publishes its root sums, and the last-arriving CTA of each
-// group of siblings carries on one level up — one launch covers the whole tree.
+// group of siblings carries on one level up — one launch covers the whole tree (k_coarse, the
+// generic path, below); the fast path splits it into k_sums_tree and k_tiles_all.
 // ============================================================================================
 
 // ============================================================================================
