@@ -115,8 +115,39 @@ __global__ void k_tn_layernorm(uint64_t rows, uint32_t d, const float* x, float*
 struct EdgeMlp {
     float w1[4 * 8], b1[8], w2[8 * 8], b2[8];
 };
+// Fixed-size form (the production config: edge_hidden = heads = 8): fully unrolled, so the
+// hidden layer and outputs stay in registers (the runtime-bounded loops below put them, and the
+// indexed weights, in local memory — 374 us for the 8.4 M leaf pairs at N=65,536).
+template <int EH, int HD>
+__device__ __forceinline__ void edge_mlp_t(const EdgeMlp& m, float dx, float dy, float dist, float c,
+                                           float (&out)[8]) {
+    float hid[EH];
+#pragma unroll
+    for (int k = 0; k < EH; ++k) {
+        float a = m.b1[k];
+        a = fmaf(dx, m.w1[0 * EH + k], a);
+        a = fmaf(dy, m.w1[1 * EH + k], a);
+        a = fmaf(dist, m.w1[2 * EH + k], a);
+        a = fmaf(c, m.w1[3 * EH + k], a);
+        hid[k] = gelu_f(a);
+    }
+#pragma unroll
+    for (int h = 0; h < HD; ++h) {
+        float a = m.b2[h];
+#pragma unroll
+        for (int k = 0; k < EH; ++k) a = fmaf(hid[k], m.w2[k * HD + h], a);
+        out[h] = a;
+    }
+}
 __device__ __forceinline__ void edge_mlp(const EdgeMlp& m, uint32_t eh, uint32_t heads, float dx,
                                          float dy, float dist, float c, float* out) {
+    if (eh == 8 && heads == 8) {
+        float o[8];
+        edge_mlp_t<8, 8>(m, dx, dy, dist, c, o);
+#pragma unroll
+        for (int h = 0; h < 8; ++h) out[h] = o[h];
+        return;
+    }
     float hid[8];
     for (uint32_t k = 0; k < eh; ++k) {
         float a = m.b1[k];
@@ -150,6 +181,12 @@ __global__ void k_tn_leaf_bias(TnDims g, const uint32_t* order, const unsigned l
     for (unsigned long long p = ro[base + i]; p < ro[base + i + 1]; ++p)
         if (ci[p] == base + j) c = v[p];
     float out[8];
+    if (g.eh == 8 && g.heads == 8) {
+        edge_mlp_t<8, 8>(mlp, float(dx), float(dy), float(dist), float(c), out);
+#pragma unroll
+        for (int h = 0; h < 8; ++h) bias[((k * 8 + h) * g.L + j) * g.L + i] = out[h];
+        return;
+    }
     edge_mlp(mlp, g.eh, g.heads, float(dx), float(dy), float(dist), float(c), out);
     for (uint32_t h = 0; h < g.heads; ++h) bias[((k * g.heads + h) * g.L + j) * g.L + i] = out[h];
 }
