@@ -171,11 +171,26 @@ __global__ void k_tn_leaf_bias(TnDims g, const uint32_t* order, const unsigned l
                                const uint32_t* ci, const double* v, EdgeMlp mlp, float* bias) {
     const uint64_t k = blockIdx.y;
     const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // j * L + i
+    const uint64_t base = k * g.L;
+    // the leaf's node coordinates (frame.cpp cell centres, f64), once per CTA instead of four f64
+    // divisions per pair
+    __shared__ double cx[128], cy[128];
+    for (uint64_t q = threadIdx.x; q < g.L && q < 128; q += blockDim.x) {
+        const uint32_t a = order[base + q];
+        cx[q] = (double(a % g.width) + 0.5) / double(g.width);
+        cy[q] = (double(a / g.width) + 0.5) / double(g.height);
+    }
+    __syncthreads();
     if (idx >= g.L * g.L) return;
-    const uint64_t j = idx / g.L, i = idx % g.L, base = k * g.L;
-    const uint32_t a = order[base + i], b = order[base + j];
-    const double xa = (double(a % g.width) + 0.5) / double(g.width), ya = (double(a / g.width) + 0.5) / double(g.height);
-    const double xb = (double(b % g.width) + 0.5) / double(g.width), yb = (double(b / g.width) + 0.5) / double(g.height);
+    const uint64_t j = idx / g.L, i = idx % g.L;
+    double xa, ya, xb, yb;
+    if (g.L <= 128) {
+        xa = cx[i]; ya = cy[i]; xb = cx[j]; yb = cy[j];
+    } else {
+        const uint32_t a = order[base + i], b = order[base + j];
+        xa = (double(a % g.width) + 0.5) / double(g.width); ya = (double(a / g.width) + 0.5) / double(g.height);
+        xb = (double(b % g.width) + 0.5) / double(g.width); yb = (double(b / g.width) + 0.5) / double(g.height);
+    }
     const double dx = xa - xb, dy = ya - yb, dist = sqrt(dx * dx + dy * dy);
     double c = 0.0;
     for (unsigned long long p = ro[base + i]; p < ro[base + i + 1]; ++p)
