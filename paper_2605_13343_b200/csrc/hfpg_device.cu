@@ -110,6 +110,7 @@ struct hfpg_handle {
         double *lv = nullptr, *tv = nullptr, *y = nullptr;
         uint32_t *fperm = nullptr, *bperm = nullptr;
         uint32_t flevels = 0, blevels = 0;
+        uint16_t *flev = nullptr, *blev = nullptr, *fmax = nullptr, *bmax = nullptr;
     } ic0;
     unsigned long long* slice_off = nullptr;
     uint32_t* sell_cols = nullptr;
@@ -407,15 +408,23 @@ void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
 
 Ic0Dev ic0_dev(const hfpg_handle* h) {
     const auto& c = h->ic0;
-    return Ic0Dev{c.lro, c.lci, c.lv, c.tro, c.tci, c.tv, c.y, c.fperm, c.bperm};
+    static const bool rows = std::getenv("HFPG_IC0_ROWS") != nullptr;  // A/B: per-row sweeps
+    return Ic0Dev{c.lro, c.lci, c.lv, c.tro, c.tci, c.tv, c.y, c.fperm, c.bperm, c.flev, c.blev, c.fmax, c.bmax,
+                  rows ? 0 : 1};
 }
 // The two sync-free sweeps (ic0.cuh): z = (L L^T)^{-1} rin; mode kApply leaves the scalars alone.
 void launch_ic0_sweeps(hfpg_handle* h, const DevSys& s, int mode, const double* rin, double* zout) {
     const unsigned g = unsigned((h->n + kIc0Threads - 1) / kIc0Threads);
     const Ic0Dev d = ic0_dev(h);
-    k_ic0_forward<<<g, kIc0Threads, 0, h->lstream>>>(s, d, rin, mode);
-    CK(cudaGetLastError());
-    k_ic0_backward<<<g, kIc0Threads, 0, h->lstream>>>(s, d, rin, zout, mode);
+    if (d.chunked) {
+        k_ic0_forward_chunk<<<g, kIc0ChunkThreads, 0, h->lstream>>>(s, d, rin, mode);
+        CK(cudaGetLastError());
+        k_ic0_backward_chunk<<<g, kIc0ChunkThreads, 0, h->lstream>>>(s, d, rin, zout, mode);
+    } else {
+        k_ic0_forward<<<g, kIc0Threads, 0, h->lstream>>>(s, d, rin, mode);
+        CK(cudaGetLastError());
+        k_ic0_backward<<<g, kIc0Threads, 0, h->lstream>>>(s, d, rin, zout, mode);
+    }
     CK(cudaGetLastError());
 }
 void launch_ic0_step(hfpg_handle* h, const DevSys& s, int mode) {
@@ -1215,6 +1224,7 @@ int hfpg_destroy(hfpg_handle* h) {
         dfree(h->ic0.lro); dfree(h->ic0.lci); dfree(h->ic0.lv); dfree(h->ic0.tro); dfree(h->ic0.tci);
         dfree(h->ic0.tv); dfree(h->ic0.y);
         dfree(h->ic0.fperm); dfree(h->ic0.bperm);
+        dfree(h->ic0.flev); dfree(h->ic0.blev); dfree(h->ic0.fmax); dfree(h->ic0.bmax);
         if (h->sc_host) cudaFreeHost(h->sc_host);
         {
             auto& F = h->fr;
@@ -1984,6 +1994,8 @@ int hfpg_load_ic0(hfpg_handle* h, uint64_t n, const uint64_t* lro, const uint32_
         std::vector<uint32_t> fperm, bperm;
         uint32_t fl = 0, bl = 0;
         ic0_levels_host(n, vr, vc, tro, tci, fperm, bperm, fl, bl);
+        std::vector<uint16_t> flev, blev, fmx, bmx;
+        ic0_chunk_levels_host(n, kIc0Threads, vr, vc, tro, tci, flev, blev, fmx, bmx);
         invalidate_graph(h);
         auto& c = h->ic0;
         dalloc(c.lro, n + 1);
@@ -1995,6 +2007,14 @@ int hfpg_load_ic0(hfpg_handle* h, uint64_t n, const uint64_t* lro, const uint32_
         dalloc(c.y, n);
         dalloc(c.fperm, n);
         dalloc(c.bperm, n);
+        dalloc(c.flev, n);
+        dalloc(c.blev, n);
+        dalloc(c.fmax, fmx.size());
+        dalloc(c.bmax, bmx.size());
+        CK(cudaMemcpy(c.flev, flev.data(), n * 2, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c.blev, blev.data(), n * 2, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c.fmax, fmx.data(), fmx.size() * 2, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c.bmax, bmx.data(), bmx.size() * 2, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(c.fperm, fperm.data(), n * 4, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(c.bperm, bperm.data(), n * 4, cudaMemcpyHostToDevice));
         c.flevels = fl;

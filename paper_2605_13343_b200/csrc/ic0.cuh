@@ -27,6 +27,12 @@ struct Ic0Dev {
     double* y;                      // forward-sweep result
     const uint32_t* fperm;          // rows in forward / backward dependency-level order
     const uint32_t* bperm;
+    // chunked sweeps: rows in chunks of kIc0Threads consecutive (Morton) rows, one CTA each
+    const uint16_t* flev;           // level of a row among its chunk's rows (forward / backward)
+    const uint16_t* blev;
+    const uint16_t* fmax;           // deepest level per chunk
+    const uint16_t* bmax;
+    int chunked;
 };
 constexpr int kIc0Threads = 128;
 // "Not yet computed": a NaN payload no arithmetic produces (a computed value with these bits is
@@ -121,6 +127,153 @@ __global__ void __launch_bounds__(256) k_ic0_update(DevSys s, Ic0Dev d, int mode
     double tot[1];
     if (grid_reduce_last<1>(v, s.partials, &s.counters[3], tot) && threadIdx.x == 0)
         leaf_epilogue(s, mode, tot[0]);  // r0 (init) or rel / history / stop
+}
+
+// Chunked sweeps (the default): CTA c owns the kIc0Threads consecutive rows of chunk c (a Morton
+// brick), one thread per row, plus one helper warp. Every row thread loads its row's (up to 8)
+// off-diagonal columns and values, right-hand side and diagonal into registers and registers each
+// dependency outside the chunk (earlier chunks forward; later chunks backward, whose CTAs are
+// numbered from the end) in a shared slot list. The helper warp polls all slots from global
+// memory concurrently and drops each value into shared memory as soon as it is published; the
+// row threads meanwhile resolve the chunk level by level (flev / blev, ic0_chunk_levels_host),
+// one named barrier per level, reading in-chunk values and external slots from shared memory.
+// The global hand-off latency thus overlaps the chunk's own levels: the wavefront pipelines
+// across bricks and pays about one L2 round trip per brick crossing. Accumulation order and
+// rounding are the per-row kernels' (bit-identical to the reference).
+constexpr int kIc0ChunkThreads = kIc0Threads + 32;
+constexpr int kIc0Slots = 256;  // external dependencies per chunk served by the helper warp
+
+__device__ __forceinline__ unsigned long long ld_volatile_shared_u64(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+template <bool FWD>
+__device__ __forceinline__ double ic0_chunk_sweep(const Ic0Dev& d, const double* rhs, double* out, uint64_t n,
+                                                  uint64_t ch) {
+    __shared__ double sh[kIc0Threads];
+    __shared__ unsigned long long ext[kIc0Slots];
+    __shared__ uint32_t ext_col[kIc0Slots];
+    __shared__ int nslot;
+    const uint64_t c0 = ch * kIc0Threads, c1 = c0 + kIc0Threads, i = c0 + threadIdx.x;
+    const bool helper = threadIdx.x >= kIc0Threads;
+    if (threadIdx.x == 0) nslot = 0;
+    __syncthreads();
+    uint64_t beg = 0, end = 0;
+    uint32_t col[8];
+    double val[8];
+    int slot[8];
+    double rv = 0.0, diag = 1.0;
+    int lev = -1;
+    if (!helper && i < n) {
+        if (FWD) {
+            beg = d.lro[i];
+            end = d.lro[i + 1] - 1;
+            lev = d.flev[i];
+            diag = d.lv[end];
+        } else {
+            beg = d.tro[i];
+            end = d.tro[i + 1];
+            lev = d.blev[i];
+            diag = d.lv[d.lro[i + 1] - 1];
+        }
+        rv = FWD ? rhs[i] : __ldcg(&rhs[i]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            slot[k] = -1;
+            if (beg + k < end) {
+                col[k] = FWD ? d.lci[beg + k] : d.tci[beg + k];
+                val[k] = FWD ? d.lv[beg + k] : d.tv[beg + k];
+                if (FWD ? col[k] < c0 : col[k] >= c1) {
+                    const int t = atomicAdd(&nslot, 1);
+                    if (t < kIc0Slots) {  // beyond kIc0Slots the row polls global memory itself
+                        slot[k] = t;
+                        ext_col[t] = col[k];
+                        ext[t] = kIc0Pending;
+                    } else {
+                        slot[k] = -2;
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (helper) {  // poll every registered slot until all are published
+        const int ns = min(nslot, kIc0Slots), lane = threadIdx.x & 31;
+        for (int base = 0; base < ns; base += 32 * 8) {
+            unsigned long long raw[8];
+            bool pend = true;
+            while (pend) {
+                pend = false;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int t = base + k * 32 + lane;
+                    if (t < ns && ext[t] == kIc0Pending) raw[k] = ld_relaxed_u64(&out[ext_col[t]]);
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int t = base + k * 32 + lane;
+                    if (t < ns && ext[t] == kIc0Pending) {
+                        if (raw[k] != kIc0Pending) *reinterpret_cast<volatile unsigned long long*>(&ext[t]) = raw[k];
+                        else pend = true;
+                    }
+                }
+            }
+        }
+        return 0.0;
+    }
+    const int maxl = FWD ? d.fmax[ch] : d.bmax[ch];
+    double res = 0.0;
+    for (int l = 0; l <= maxl; ++l) {
+        if (lev == l) {
+            double acc = rv;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (beg + k < end) {
+                    double v;
+                    if (slot[k] == -1) {
+                        v = sh[col[k] - c0];
+                    } else if (slot[k] >= 0) {
+                        unsigned long long r = ld_volatile_shared_u64(&ext[slot[k]]);
+                        while (r == kIc0Pending) r = ld_volatile_shared_u64(&ext[slot[k]]);
+                        v = __longlong_as_double(r);
+                    } else {
+                        v = ic0_get(&out[col[k]]);
+                    }
+                    // forward: vmulsd + vsubsd as the reference build; backward: its vfnmadd
+                    acc = FWD ? __dsub_rn(acc, __dmul_rn(val[k], v)) : fma(-val[k], v, acc);
+                }
+            for (uint64_t p = beg + 8; p < end; ++p) {  // rows with more than 8 couplings
+                const uint32_t j = FWD ? d.lci[p] : d.tci[p];
+                const double a = FWD ? d.lv[p] : d.tv[p];
+                const double v = (FWD ? j >= c0 : j < c1) ? sh[j - c0] : ic0_get(&out[j]);
+                acc = FWD ? __dsub_rn(acc, __dmul_rn(a, v)) : fma(-a, v, acc);
+            }
+            res = acc / diag;
+            sh[threadIdx.x] = res;
+            st_relaxed_f64(&out[i], res);
+        }
+        named_bar_sync(1, kIc0Threads);
+    }
+    return res;
+}
+
+__global__ void __launch_bounds__(kIc0ChunkThreads) k_ic0_forward_chunk(DevSys s, Ic0Dev d, const double* rin,
+                                                                        int mode) {
+    if (mode != kApply && s.sc->done) return;
+    ic0_chunk_sweep<true>(d, rin, d.y, s.n, blockIdx.x);
+}
+
+__global__ void __launch_bounds__(kIc0ChunkThreads) k_ic0_backward_chunk(DevSys s, Ic0Dev d, const double* rin,
+                                                                         double* zout, int mode) {
+    if (prolong_skip(s, mode)) return;
+    const uint64_t nch = (s.n + kIc0Threads - 1) / kIc0Threads, ch = nch - 1 - blockIdx.x;
+    const double zj = ic0_chunk_sweep<false>(d, d.y, zout, s.n, ch);
+    const uint64_t j = ch * kIc0Threads + threadIdx.x;
+    double v[1] = {threadIdx.x < kIc0Threads && j < s.n ? rin[j] * zj : 0.0};
+    if (mode == kApply) return;
+    double tot[1];
+    if (grid_reduce_last<1>(v, s.partials, &s.counters[2], tot) && threadIdx.x == 0)
+        prolong_epilogue(s, mode, tot[0]);
 }
 
 __global__ void __launch_bounds__(kIc0Threads) k_ic0_forward(DevSys s, Ic0Dev d, const double* rin, int mode) {

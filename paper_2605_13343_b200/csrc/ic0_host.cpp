@@ -136,4 +136,36 @@ void ic0_levels_host(uint64_t n, const std::vector<uint64_t>& lro, const std::ve
     order(bperm, blevels);
 }
 
+// Levels of the rows inside their chunk of `chunk` consecutive rows (the chunked sweeps):
+// forward, a row's level counts only the dependencies in its own chunk; backward likewise over
+// the transposed lists. Per-chunk maxima bound the kernels' level loops.
+void ic0_chunk_levels_host(uint64_t n, uint64_t chunk, const std::vector<uint64_t>& lro,
+                           const std::vector<uint32_t>& lci, const std::vector<uint64_t>& tro,
+                           const std::vector<uint32_t>& tci, std::vector<uint16_t>& flev,
+                           std::vector<uint16_t>& blev, std::vector<uint16_t>& fmax, std::vector<uint16_t>& bmax) {
+    const uint64_t nch = (n + chunk - 1) / chunk;
+    flev.assign(n, 0);
+    blev.assign(n, 0);
+    fmax.assign(nch, 0);
+    bmax.assign(nch, 0);
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t c0 = (i / chunk) * chunk;
+        uint32_t l = 0;
+        for (uint64_t p = lro[i]; p + 1 < lro[i + 1]; ++p)
+            if (lci[p] >= c0) l = std::max<uint32_t>(l, uint32_t(flev[lci[p]]) + 1);
+        if (l > 65535) throw InvalidArgument("ic0: chunk level overflow");
+        flev[i] = uint16_t(l);
+        fmax[i / chunk] = std::max<uint16_t>(fmax[i / chunk], uint16_t(l));
+    }
+    for (uint64_t j = n; j-- > 0;) {
+        const uint64_t c1 = (j / chunk + 1) * chunk;
+        uint32_t l = 0;
+        for (uint64_t q = tro[j]; q < tro[j + 1]; ++q)
+            if (tci[q] < c1) l = std::max<uint32_t>(l, uint32_t(blev[tci[q]]) + 1);
+        if (l > 65535) throw InvalidArgument("ic0: chunk level overflow");
+        blev[j] = uint16_t(l);
+        bmax[j / chunk] = std::max<uint16_t>(bmax[j / chunk], uint16_t(l));
+    }
+}
+
 }  // namespace hfpg

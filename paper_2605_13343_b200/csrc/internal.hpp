@@ -37,6 +37,10 @@ void ic0_levels_host(uint64_t n, const std::vector<uint64_t>& lro, const std::ve
                      const std::vector<uint64_t>& tro, const std::vector<uint32_t>& tci,
                      std::vector<uint32_t>& fperm, std::vector<uint32_t>& bperm, uint32_t& flevels,
                      uint32_t& blevels);
+void ic0_chunk_levels_host(uint64_t n, uint64_t chunk, const std::vector<uint64_t>& lro,
+                           const std::vector<uint32_t>& lci, const std::vector<uint64_t>& tro,
+                           const std::vector<uint32_t>& tci, std::vector<uint16_t>& flev,
+                           std::vector<uint16_t>& blev, std::vector<uint16_t>& fmax, std::vector<uint16_t>& bmax);
 
 // Runs f(), maps exceptions to status codes and records the message.
 template <class F>
