@@ -1143,23 +1143,34 @@ void train_spmm(hfpg_handle* h, const double* X, double* Y, uint64_t kz) {
         Y[t] = y;
     });
 }
-// Deterministic sums of NV per-element functions over cnt elements: block partials on the
-// device, then the blocks' partials added in block order on the host.
+// Deterministic sums of NV per-element functions over cnt elements: a fixed grid of 256-thread
+// CTAs, each thread a fixed strided subset, a fixed shared-memory tree per CTA, then the CTAs'
+// partials added in CTA order on the host — the same bits on every run.
+template <int NV, class F>
+__global__ void __launch_bounds__(256) k_train_sums(uint64_t cnt, F f, double* part) {
+    __shared__ double red[NV][256];
+    double acc[NV];
+    for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+    for (uint64_t t = uint64_t(blockIdx.x) * 256 + threadIdx.x; t < cnt; t += uint64_t(gridDim.x) * 256) {
+        double e[NV];
+        f(t, e);
+        for (int v = 0; v < NV; ++v) acc[v] += e[v];
+    }
+    for (int v = 0; v < NV; ++v) red[v][threadIdx.x] = acc[v];
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (int(threadIdx.x) < w)
+            for (int v = 0; v < NV; ++v) red[v][threadIdx.x] += red[v][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x < NV) part[blockIdx.x * NV + threadIdx.x] = red[threadIdx.x][0];
+}
 template <int NV, class F>
 void train_sums(hfpg_handle* h, uint64_t cnt, F f, double (&out)[NV]) {
-    const unsigned blocks = unsigned(std::min<uint64_t>((cnt + 255) / 256, 4096 / NV));
+    const unsigned blocks = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((cnt + 255) / 256, 4096 / NV)));
     double* part = h->tr.part;
-    auto kern = [=] __device__(uint64_t b) {
-        double acc[NV];
-        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
-        for (uint64_t t = b; t < cnt; t += blocks) {
-            double e[NV];
-            f(t, e);
-            for (int v = 0; v < NV; ++v) acc[v] += e[v];
-        }
-        for (int v = 0; v < NV; ++v) part[b * NV + v] = acc[v];
-    };
-    each(h->stream, blocks, kern);
+    k_train_sums<NV><<<blocks, 256, 0, h->stream>>>(cnt, f, part);
+    CK(cudaGetLastError());
     std::vector<double> hp(size_t(blocks) * NV);
     CK(cudaMemcpyAsync(hp.data(), part, hp.size() * 8, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));

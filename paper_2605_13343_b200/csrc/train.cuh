@@ -27,6 +27,86 @@ void each(cudaStream_t st, uint64_t n, F f) {
     k_each<<<unsigned(g), 256, 0, st>>>(n, f);
 }
 
+// Batched small GEMMs through shared memory: out(r, j) = sum_p a(r, p) b(p, j) per batch entry
+// (blockIdx.z), a 64 x 64 output tile per CTA, 4 x 4 outputs per thread, p staged 16 at a time.
+// Each output still accumulates over p in ascending order with the reference's rounding — fused
+// (DOT = false: gemm_nn / gemm_tn) or dot_ref's products-then-sums with a fused odd tail
+// (DOT = true: gemm_nt, the parameter gradients) — so tiling changes only the data reuse. NP = 2
+// runs a second operand pair over the same output index (two accumulators, one epilogue).
+struct BgOp {
+    const double* a;
+    uint64_t sa, ar, ap;  // a(r, p) = a[batch sa + r ar + p ap]
+    const double* b;
+    uint64_t sb, bp, bj;  // b(p, j) = b[batch sb + p bp + j bj]
+};
+constexpr int kBgT = 64, kBgP = 16;
+
+template <bool DOT, int NP, class Epi>
+__global__ void __launch_bounds__(256) k_bgemm(uint64_t R, uint64_t J, uint64_t P, BgOp o0, BgOp o1, Epi epi) {
+    __shared__ double As[NP][kBgP][kBgT + 1], Bs[NP][kBgP][kBgT + 1];
+    const uint64_t bz = blockIdx.z, r0 = uint64_t(blockIdx.y) * kBgT, j0 = uint64_t(blockIdx.x) * kBgT;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    double acc[NP][4][4];
+#pragma unroll
+    for (int n = 0; n < NP; ++n)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[n][i][q] = 0.0;
+    for (uint64_t p0 = 0; p0 < P; p0 += kBgP) {
+#pragma unroll
+        for (int n = 0; n < NP; ++n) {
+            const BgOp& o = n ? o1 : o0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int idx = tid + 256 * e;
+                int r, pp;
+                if (o.ap == 1) { pp = idx & 15; r = idx >> 4; } else { r = idx & 63; pp = idx >> 6; }
+                const uint64_t gr = r0 + r, gp = p0 + pp;
+                As[n][pp][r] = gr < R && gp < P ? o.a[bz * o.sa + gr * o.ar + gp * o.ap] : 0.0;
+                int j;
+                if (o.bj == 1) { j = idx & 63; pp = idx >> 6; } else { pp = idx & 15; j = idx >> 4; }
+                const uint64_t gj = j0 + j, gq = p0 + pp;
+                Bs[n][pp][j] = gj < J && gq < P ? o.b[bz * o.sb + gq * o.bp + gj * o.bj] : 0.0;
+            }
+        }
+        __syncthreads();
+        const int pl = int(P - p0 < kBgP ? P - p0 : kBgP);
+        const bool odd_tail = DOT && (P & 1) && p0 + kBgP >= P;  // the fused last element
+        for (int pp = 0; pp < pl; ++pp) {
+            const bool fused = !DOT || (odd_tail && pp == pl - 1);
+#pragma unroll
+            for (int n = 0; n < NP; ++n) {
+                double a[4], b[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = As[n][pp][ty + 16 * i];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) b[q] = Bs[n][pp][tx + 16 * q];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        acc[n][i][q] = fused ? fma(a[i], b[q], acc[n][i][q])
+                                             : __dadd_rn(acc[n][i][q], __dmul_rn(a[i], b[q]));
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint64_t r = r0 + ty + 16 * i, j = j0 + tx + 16 * q;
+            if (r < R && j < J) epi(bz, r, j, acc[0][i][q], acc[NP - 1][i][q]);
+        }
+}
+template <bool DOT, int NP, class Epi>
+void bgemm(cudaStream_t st, uint64_t batch, uint64_t R, uint64_t J, uint64_t P, BgOp o0, BgOp o1, Epi epi) {
+    if (!batch || !R || !J) return;
+    const dim3 g(unsigned((J + kBgT - 1) / kBgT), unsigned((R + kBgT - 1) / kBgT), unsigned(batch));
+    k_bgemm<DOT, NP><<<g, 256, 0, st>>>(R, J, P, o0, o1, epi);
+}
+
 // Device views of the batch state (all f64). L = 128, Ls = 32, rank 16 (the fast layout).
 struct TrainDev {
     uint64_t n, K, D, M, kz;
@@ -63,32 +143,20 @@ __device__ __forceinline__ void tile_span(uint64_t K, uint64_t m, uint64_t& span
 inline void train_forward(cudaStream_t st, const TrainDev T, const double* P) {
     const uint64_t kz = T.kz, K = T.K, M = T.M, D = T.D;
     // diagonal blocks: H_k = F_k^T X_k (gemm_tn), Y_k = F_k H_k (gemm_nn)
-    each(st, T.n * kz, [=] __device__(uint64_t t) {
-        const uint64_t row = t / kz, j = t % kz, k = row >> 7, r = row & 127;
-        const double* F = P + k * 16384;
-        const double* Xk = T.X + k * 128 * kz + j;
-        double acc = 0.0;
-        for (int p = 0; p < 128; ++p) acc = fma(F[p * 128 + r], Xk[p * kz], acc);
-        T.H[t] = acc;
+    const BgOp ft{P, 16384, 1, 128, T.X, 128 * kz, kz, 1};  // F^T X
+    bgemm<false, 1>(st, K, 128, kz, 128, ft, ft, [=] __device__(uint64_t k, uint64_t r, uint64_t j, double a, double) {
+        T.H[(k * 128 + r) * kz + j] = a;
     });
-    each(st, T.n * kz, [=] __device__(uint64_t t) {
-        const uint64_t row = t / kz, j = t % kz, k = row >> 7, r = row & 127;
-        const double* F = P + k * 16384 + r * 128;
-        const double* Hk = T.H + k * 128 * kz + j;
-        double acc = 0.0;
-        for (int p = 0; p < 128; ++p) acc = fma(F[p], Hk[p * kz], acc);
-        T.Y[t] = acc;
+    const BgOp fh{P, 16384, 128, 1, T.H, 128 * kz, kz, 1};  // F H
+    bgemm<false, 1>(st, K, 128, kz, 128, fh, fh, [=] __device__(uint64_t k, uint64_t r, uint64_t j, double a, double) {
+        T.Y[(k * 128 + r) * kz + j] = a;
     });
     // restriction (gemm_tn with the bridges)
-    each(st, K * 32 * kz, [=] __device__(uint64_t t) {
-        const uint64_t row = t / kz, j = t % kz, k = row >> 5, c = row & 31;
-        const double* Bu = P + T.bridge_base + k * 8192;
-        const double* Xk = T.X + k * 128 * kz + j;
-        double au = 0.0, av = 0.0;
-        for (int p = 0; p < 128; ++p) au = fma(Bu[p * 32 + c], Xk[p * kz], au);
-        for (int p = 0; p < 128; ++p) av = fma(Bu[4096 + p * 32 + c], Xk[p * kz], av);
-        T.Rr[t] = au;
-        T.Rc[t] = av;
+    const BgOp ru{P + T.bridge_base, 8192, 1, 32, T.X, 128 * kz, kz, 1}, rv{P + T.bridge_base + 4096, 8192, 1, 32,
+                                                                          T.X, 128 * kz, kz, 1};
+    bgemm<false, 2>(st, K, 32, kz, 128, ru, rv, [=] __device__(uint64_t k, uint64_t c, uint64_t j, double au, double av) {
+        T.Rr[(k * 32 + c) * kz + j] = au;
+        T.Rc[(k * 32 + c) * kz + j] = av;
     });
     // strip aggregation (leaf order)
     each(st, M * 32 * kz, [=] __device__(uint64_t t) {
@@ -159,44 +227,30 @@ inline void train_adjoint(cudaStream_t st, const TrainDev T, const double* P, co
         const double acc = dot_ref(BY + i * kz, T.X + i * kz, kz);
         G[T.gate_base + i] += acc / T.a_diag[i];
     });
-    each(st, T.n * kz, [=] __device__(uint64_t t) {  // W = F^T bar_Y
-        const uint64_t row = t / kz, j = t % kz, k = row >> 7, c = row & 127;
-        const double* F = P + k * 16384;
-        const double* by = BY + k * 128 * kz + j;
-        double acc = 0.0;
-        for (int p = 0; p < 128; ++p) acc = fma(F[p * 128 + c], by[p * kz], acc);
-        T.W[t] = acc;
+    const BgOp fb{P, 16384, 1, 128, BY, 128 * kz, kz, 1};  // W = F^T bar_Y
+    bgemm<false, 1>(st, K, 128, kz, 128, fb, fb, [=] __device__(uint64_t k, uint64_t c, uint64_t j, double a, double) {
+        T.W[(k * 128 + c) * kz + j] = a;
     });
-    each(st, K * 16384, [=] __device__(uint64_t t) {  // bar_F += bar_Y H^T; bar_F += X W^T
-        const uint64_t k = t >> 14, r = (t >> 7) & 127, c = t & 127;
-        const double* by = BY + (k * 128 + r) * kz;
-        const double* h = T.H + (k * 128 + c) * kz;
-        const double* x = T.X + (k * 128 + r) * kz;
-        const double* w = T.W + (k * 128 + c) * kz;
-        const double a1 = dot_ref(by, h, kz), a2 = dot_ref(x, w, kz);
-        double g = G[t];
-        g = g + a1;
-        G[t] = g + a2;
+    // bar_F += bar_Y H^T; bar_F += X W^T (dot products over the probes)
+    const BgOp yh{BY, 128 * kz, kz, 1, T.H, 128 * kz, 1, kz}, xw{T.X, 128 * kz, kz, 1, T.W, 128 * kz, 1, kz};
+    bgemm<true, 2>(st, K, 128, 128, kz, yh, xw, [=] __device__(uint64_t k, uint64_t r, uint64_t c, double a1, double a2) {
+        double* g = G + k * 16384 + r * 128 + c;
+        const double t = *g + a1;
+        *g = t + a2;
     });
-    each(st, K * 128 * 32, [=] __device__(uint64_t t) {  // bridges: bar_Y G^T (prolongation)
-        const uint64_t k = t >> 12, r = (t >> 5) & 127, c = t & 31;
-        const double* by = BY + (k * 128 + r) * kz;
-        const double* gr = T.Gr + (k * 32 + c) * kz;
-        const double* gc = T.Gc + (k * 32 + c) * kz;
-        const double a1 = dot_ref(by, gr, kz), a2 = dot_ref(by, gc, kz);
+    // bridges: bar_Y G^T (prolongation)
+    const BgOp yr{BY, 128 * kz, kz, 1, T.Gr, 32 * kz, 1, kz}, yc{BY, 128 * kz, kz, 1, T.Gc, 32 * kz, 1, kz};
+    bgemm<true, 2>(st, K, 128, 32, kz, yr, yc, [=] __device__(uint64_t k, uint64_t r, uint64_t c, double a1, double a2) {
         double* gb = G + T.bridge_base + k * 8192 + r * 32 + c;
         gb[0] = gb[0] + a1;
         gb[4096] = gb[4096] + a2;
     });
-    each(st, K * 32 * kz, [=] __device__(uint64_t t) {  // bar_gather = bridge^T bar_Y
-        const uint64_t row = t / kz, j = t % kz, k = row >> 5, c = row & 31;
-        const double* Bu = P + T.bridge_base + k * 8192;
-        const double* by = BY + k * 128 * kz + j;
-        double au = 0.0, av = 0.0;
-        for (int p = 0; p < 128; ++p) au = fma(Bu[p * 32 + c], by[p * kz], au);
-        for (int p = 0; p < 128; ++p) av = fma(Bu[4096 + p * 32 + c], by[p * kz], av);
-        T.BGr[t] = au;
-        T.BGc[t] = av;
+    // bar_gather = bridge^T bar_Y
+    const BgOp gu{P + T.bridge_base, 8192, 1, 32, BY, 128 * kz, kz, 1}, gv{P + T.bridge_base + 4096, 8192, 1, 32,
+                                                                           BY, 128 * kz, kz, 1};
+    bgemm<false, 2>(st, K, 32, kz, 128, gu, gv, [=] __device__(uint64_t k, uint64_t c, uint64_t j, double au, double av) {
+        T.BGr[(k * 32 + c) * kz + j] = au;
+        T.BGc[(k * 32 + c) * kz + j] = av;
     });
     each(st, M * 32 * kz, [=] __device__(uint64_t t) {  // gather adjoint: member leaves' bar-gathers
         const uint64_t m = t / (32 * kz), e = t % (32 * kz);
@@ -263,12 +317,9 @@ inline void train_adjoint(cudaStream_t st, const TrainDev T, const double* P, co
         T.BRr[t] = rr;
         T.BRc[t] = rc;
     });
-    each(st, K * 128 * 32, [=] __device__(uint64_t t) {  // restriction adjoint: X bar_r^T
-        const uint64_t k = t >> 12, r = (t >> 5) & 127, c = t & 31;
-        const double* x = T.X + (k * 128 + r) * kz;
-        const double* br = T.BRr + (k * 32 + c) * kz;
-        const double* bc = T.BRc + (k * 32 + c) * kz;
-        const double a1 = dot_ref(x, br, kz), a2 = dot_ref(x, bc, kz);
+    // restriction adjoint: X bar_r^T
+    const BgOp xr{T.X, 128 * kz, kz, 1, T.BRr, 32 * kz, 1, kz}, xc{T.X, 128 * kz, kz, 1, T.BRc, 32 * kz, 1, kz};
+    bgemm<true, 2>(st, K, 128, 32, kz, xr, xc, [=] __device__(uint64_t k, uint64_t r, uint64_t c, double a1, double a2) {
         double* gb = G + T.bridge_base + k * 8192 + r * 32 + c;
         gb[0] = gb[0] + a1;
         gb[4096] = gb[4096] + a2;

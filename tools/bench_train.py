@@ -39,11 +39,29 @@ reps = 3
 for _ in range(reps):
     r = H.loss_gradient(P, Z, kz, H.LossKind(a.kind), dev, norm_a=8.0)
 gpu_ms = (time.perf_counter() - t) * 1e3 / reps
+# the same call on device-resident arrays (where = DEVICE): the kernels alone, no PCIe copies
+import ctypes as C  # noqa: E402
+from paper_2605_13343_b200 import _native as N  # noqa: E402
+dP, dZ = torch.from_numpy(P).cuda(), torch.from_numpy(Z).cuda()
+dG = torch.empty_like(dP)
+lo, dg = N.dbl(), N.i32()
+def dev_call():
+    rc = N.lib.hfpg_loss_gradient(dev.h, dP.data_ptr(), 128, 32, 0.0, dZ.data_ptr(), kz, a.kind, 8.0,
+                                  C.byref(lo), C.byref(dg), dG.data_ptr(), N.DEVICE)
+    assert rc == 0, rc
+dev_call()
+torch.cuda.synchronize()
+t = time.perf_counter()
+for _ in range(reps):
+    dev_call()
+torch.cuda.synchronize()
+dev_ms = (time.perf_counter() - t) * 1e3 / reps
+assert np.array_equal(dG.cpu().numpy(), r.grad)
 # forward-pass FLOPs (2 per multiply-add): leaf 2 x 2 L^2 n/L kz... summed per stage
 K = n // 128
 fwd = 2 * kz * (2 * K * 128 * 128 + 2 * 2 * K * 128 * 32 + 4 * (K - 1) * 32 * 16)
 line = {"metric": "loss_gradient ms per probe batch (host arrays in/out)", "n": n, "kz": kz, "kind": a.kind,
-        "gpu_ms": gpu_ms, "loss": r.loss, "approx_gflop": 3 * fwd / 1e9}
+        "gpu_ms": gpu_ms, "gpu_device_ms": dev_ms, "loss": r.loss, "approx_gflop": 3 * fwd / 1e9}
 if a.cpu:
     try:
         from oracle.oracle import Ref
