@@ -281,6 +281,13 @@ int hfpg_spmv(hfpg_handle* h, const double* x, double* y, int where);
  * x (n) and history (max_iters entries, may be NULL) are written in `where` memory. */
 int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg, double* x,
                    double* history, hfpg_report* report, int where);
+/* pcg.cpp:53-126 pcg_solve bit for bit: the same loop driven from the host with every dot
+ * product evaluated exactly as the reference's sequential loop (its pinned build: in-order sums
+ * of the products, fused remainder), so x, the residual history, the iteration count and the
+ * status are identical to the reference's for the loaded preconditioner (factor, IC(0), Jacobi,
+ * identity). A verification mode: several host round trips per iteration. */
+int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg, double* x,
+                         double* history, hfpg_report* report, int where);
 
 /* ---- row-partitioned solve (north star: N=16.7M over 8 GPUs) ------------------------------
  * The system is split along the bisection tree (partition.cpp:9-46): rank r of G (a power of

@@ -121,6 +121,8 @@ _PROTOS = {
     "hfpg_ic0_apply": (C.c_int, [vp, vp, vp, C.c_int]),
     "hfpg_pcg_solve": (C.c_int, [vp, vp, C.POINTER(SolveConfigC), vp, vp, C.POINTER(ReportC),
                                  C.c_int]),
+    "hfpg_pcg_solve_exact": (C.c_int, [vp, vp, C.POINTER(SolveConfigC), vp, vp, C.POINTER(ReportC),
+                                       C.c_int]),
     "hfpg_set_solver": (C.c_int, [vp, C.c_int]),
     "hfpg_solver_in_use": (C.c_int, [vp, C.POINTER(i32)]),
     "hfpg_set_trace": (C.c_int, [vp, C.c_uint32]),

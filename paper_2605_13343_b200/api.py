@@ -471,10 +471,11 @@ class Device:
     def spmv_ptr(self, x_ptr: int, y_ptr: int, where: int = N.DEVICE):
         check(lib.hfpg_spmv(self.h, x_ptr, y_ptr, where))
 
-    def solve_ptr(self, b_ptr, x_ptr, cfg: "SolveConfig", hist_ptr=None, where=N.DEVICE):
+    def solve_ptr(self, b_ptr, x_ptr, cfg: "SolveConfig", hist_ptr=None, where=N.DEVICE, exact: bool = False):
         rep = N.ReportC()
         c = N.SolveConfigC(cfg.rtol, cfg.max_iters)
-        check(lib.hfpg_pcg_solve(self.h, b_ptr, C.byref(c), x_ptr, hist_ptr, C.byref(rep), where))
+        fn = lib.hfpg_pcg_solve_exact if exact else lib.hfpg_pcg_solve
+        check(fn(self.h, b_ptr, C.byref(c), x_ptr, hist_ptr, C.byref(rep), where))
         return rep
 
     def solve_async(self, b_ptr, x_ptr, cfg: "SolveConfig", where=N.DEVICE):
@@ -743,9 +744,11 @@ def factor_applier(factors: FactorTensor, A: CsrMatrix) -> PrecondApplier:
 
 
 def pcg_solve(A: CsrMatrix, b, precond: PrecondApplier, cfg: SolveConfig | None = None,
-              x_out: list | None = None) -> SolveReport:
+              x_out: list | None = None, exact: bool = False) -> SolveReport:
     """pcg.cpp:53-126, whole loop in one CUDA graph. If x_out is a list, the solution is
-    appended to it (the reference's optional std::vector<double>* out-parameter)."""
+    appended to it (the reference's optional std::vector<double>* out-parameter).
+    exact=True: every dot product as the reference's sequential loop (hfpg_pcg_solve_exact), so
+    x, the history and the iteration count are the reference's bit for bit (slower)."""
     cfg = cfg or SolveConfig()
     if cfg.rtol <= 0.0:
         raise ValueError("pcg_solve: rtol must be positive")
@@ -755,7 +758,7 @@ def pcg_solve(A: CsrMatrix, b, precond: PrecondApplier, cfg: SolveConfig | None 
     dev = precond.bind(A)
     x = np.empty(A.n_rows)
     hist = np.empty(max(cfg.max_iters, 1))
-    rep = dev.solve_ptr(b.ctypes.data, x.ctypes.data, cfg, hist.ctypes.data, N.HOST)
+    rep = dev.solve_ptr(b.ctypes.data, x.ctypes.data, cfg, hist.ctypes.data, N.HOST, exact=exact)
     if x_out is not None:
         x_out.append(x)
     return SolveReport(method=getattr(precond, "method", ""), n=int(rep.n),

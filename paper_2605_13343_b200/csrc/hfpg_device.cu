@@ -8,6 +8,7 @@
 #include "crc32.cuh"
 #include "io_device.cuh"
 #include "train.cuh"
+#include "pcg_exact.cuh"
 
 #include <algorithm>
 #include <cstdio>
@@ -1537,6 +1538,157 @@ int hfpg_pcg_solve_async(hfpg_handle* h, const double* b, const hfpg_solve_confi
 
 int hfpg_pcg_solve_wait(hfpg_handle* h, double* history, hfpg_report* report, int where) {
     return guarded([&] { solve_finish(h, history, report, where); });
+}
+
+// pcg.cpp:53-126 bit for bit (pcg_exact.cuh): a host-driven loop over the solve path's SpMV and
+// preconditioner kernels with every dot product as the reference's sequential loop.
+int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg_in, double* x,
+                         double* history, hfpg_report* report, int where) {
+    return guarded([&] {
+        set_device(h);
+        if (h->part.G > 1) throw InvalidArgument("pcg_solve_exact: partitioned handle");
+        if (!h->have_csr) throw InvalidArgument("pcg_solve: no matrix loaded");
+        if (h->pending) throw InvalidArgument("pcg_solve_exact: a solve is in flight");
+        if (h->precond == HFPG_PRECOND_FACTOR) require_apply_ready(h);
+        if (h->precond == HFPG_PRECOND_IC0 && (!h->ic0.have || h->ic0.n != h->n))
+            throw InvalidArgument("pcg_solve: no IC(0) factor loaded");
+        const hfpg_solve_config cfg = cfg_in ? *cfg_in : hfpg_solve_config{1e-8, 20000};
+        ensure_workspace(h);
+        fill_sys(h);
+        h->lstream = h->stream;
+        cudaStream_t st = h->stream;
+        const uint64_t n = h->n, n4 = n & ~uint64_t(3);
+        double *dx = h->x, *dr = h->r, *dz = h->z, *dp = h->p0, *dap = h->ap, *prod = nullptr, *dsum = nullptr,
+               *hsum = nullptr;
+        dalloc(prod, n + 2);  // seq_sum reads to the next 16-byte boundary
+        dalloc(dsum, 4);
+        CK(cudaMallocHost(&hsum, 4 * sizeof(double)));
+        SeqScratch sc;
+        auto cleanup = [&] {
+            dfree(prod);
+            dfree(dsum);
+            if (hsum) cudaFreeHost(hsum);
+            sc.release();
+        };
+        try {
+            const unsigned g = unsigned(simple_grid(h));
+            // one dot into dsum[slot] (device); fused_each: the |r0|^2 site's remainder form
+            auto dot = [&](const double* a, const double* c, int slot, int fused_each) {
+                if (n4 >= 4) {
+                    k_ex_prod<<<g, 256, 0, st>>>(a, c, n4, prod);
+                    seq_sum(st, prod, n4, nullptr, n4, false, dsum + slot, sc);
+                } else {
+                    CK(cudaMemsetAsync(dsum + slot, 0, 8, st));
+                }
+                // n <= 2: the whole vector is the remainder (the vector body needs n > 2)
+                k_ex_tail<<<1, 1, 0, st>>>(a, c, n, n <= 2 ? 0 : n4, fused_each, dsum + slot);
+                CK(cudaGetLastError());
+            };
+            auto fetch = [&](int cnt) {
+                CK(cudaMemcpyAsync(hsum, dsum, cnt * 8, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+            };
+            auto precond = [&] {  // z = M r
+                if (h->precond == HFPG_PRECOND_FACTOR) {
+                    const double shift = h->spd_enabled ? std::log1p(std::exp(h->spd_raw)) : 0.0;
+                    CK(cudaMemcpyAsync(&h->sc->shift, &shift, 8, cudaMemcpyHostToDevice, st));
+                    launch_apply(h, kApply, dr, dz);
+                } else if (h->precond == HFPG_PRECOND_IC0) {
+                    k_ic0_pending<<<g, 256, 0, st>>>(ic0_dev(h), dz, n);
+                    launch_ic0_sweeps(h, h->sys, kApply, dr, dz);
+                } else if (h->precond == HFPG_PRECOND_JACOBI) {
+                    k_ex_jacobi<<<g, 256, 0, st>>>(dr, h->a_diag, dz, n);
+                } else {
+                    CK(cudaMemcpyAsync(dz, dr, n * 8, cudaMemcpyDeviceToDevice, st));
+                }
+                CK(cudaGetLastError());
+            };
+            cudaEvent_t e0, e1;
+            CK(cudaEventCreate(&e0));
+            CK(cudaEventCreate(&e1));
+            CK(cudaEventRecord(e0, st));
+            CK(cudaMemsetAsync(dx, 0, n * 8, st));
+            copy_in(h, dr, b, n, where);
+            std::vector<double> hist;
+            uint64_t iterations = 0, breakdown_iter = 0;
+            int status = HFPG_MAX_ITERS, converged = 0;
+            dot(dr, dr, 0, 1);
+            fetch(1);
+            const double r0 = std::sqrt(hsum[0]);
+            if (r0 == 0.0) {
+                status = HFPG_CONVERGED;
+                converged = 1;
+            } else {
+                const double breakdown_tol = 1e-12 * h->fro;
+                precond();
+                CK(cudaMemcpyAsync(dp, dz, n * 8, cudaMemcpyDeviceToDevice, st));
+                dot(dr, dz, 0, 0);
+                fetch(1);
+                double rz = hsum[0];
+                for (uint64_t k = 1; k <= cfg.max_iters; ++k) {
+                    launch_spmv<kApply>(h, h->sys, dp, dap);
+                    CK(cudaGetLastError());
+                    dot(dp, dap, 0, 0);
+                    dot(dp, dp, 1, 0);
+                    fetch(2);
+                    const double pap = hsum[0], p2 = hsum[1];
+                    if (pap < -breakdown_tol * p2 || pap == 0.0) {
+                        status = HFPG_BREAKDOWN;
+                        breakdown_iter = k;
+                        iterations = k;
+                        break;
+                    }
+                    const double alpha = rz / pap;
+                    k_ex_xr<<<g, 256, 0, st>>>(dx, dr, dp, dap, alpha, n);
+                    dot(dr, dr, 0, 0);
+                    fetch(1);
+                    const double rel = std::sqrt(hsum[0]) / r0;
+                    hist.push_back(rel);
+                    if (rel <= cfg.rtol) {
+                        status = HFPG_CONVERGED;
+                        converged = 1;
+                        iterations = k;
+                        break;
+                    }
+                    if (k == cfg.max_iters) {
+                        iterations = k;
+                        break;
+                    }
+                    precond();
+                    dot(dr, dz, 0, 0);
+                    fetch(1);
+                    const double rz_next = hsum[0];
+                    const double beta = rz_next / rz;
+                    rz = rz_next;
+                    k_ex_p<<<g, 256, 0, st>>>(dp, dz, beta, n);
+                    CK(cudaGetLastError());
+                }
+            }
+            CK(cudaEventRecord(e1, st));
+            copy_out(h, x, dx, n, where);
+            if (history && !hist.empty())
+                CK(cudaMemcpyAsync(history, hist.data(), hist.size() * 8,
+                                   where == HFPG_HOST ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice, st));
+            CK(cudaStreamSynchronize(st));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            if (report) {
+                report->n = n;
+                report->iterations = iterations;
+                report->converged = converged;
+                report->status = status;
+                report->breakdown_iter = breakdown_iter;
+                report->history_len = hist.size();
+                report->wall_ms = ms;
+            }
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
+    });
 }
 
 int hfpg_launch_counts(hfpg_handle* h, uint32_t* per_iteration, uint32_t* per_apply) {
