@@ -288,6 +288,9 @@ int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg
  * identity). A verification mode: several host round trips per iteration. */
 int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg, double* x,
                          double* history, hfpg_report* report, int where);
+/* apply.cpp:80-173 apply<float> bit for bit (the pinned build's float accumulation and
+ * contractions, stage by stage): the factor preconditioner of hfpg_pcg_solve_exact. */
+int hfpg_apply_exact(hfpg_handle* h, const double* r, double* z, int where);
 
 /* ---- row-partitioned solve (north star: N=16.7M over 8 GPUs) ------------------------------
  * The system is split along the bisection tree (partition.cpp:9-46): rank r of G (a power of

@@ -119,6 +119,7 @@ _PROTOS = {
     "hfpg_adamw_step": (C.c_int, [vp, vp, vp, vp, vp, u64, u64, dbl, dbl, dbl, dbl, dbl, dbl,
                                   C.POINTER(dbl)]),
     "hfpg_ic0_apply": (C.c_int, [vp, vp, vp, C.c_int]),
+    "hfpg_apply_exact": (C.c_int, [vp, vp, vp, C.c_int]),
     "hfpg_pcg_solve": (C.c_int, [vp, vp, C.POINTER(SolveConfigC), vp, vp, C.POINTER(ReportC),
                                  C.c_int]),
     "hfpg_pcg_solve_exact": (C.c_int, [vp, vp, C.POINTER(SolveConfigC), vp, vp, C.POINTER(ReportC),

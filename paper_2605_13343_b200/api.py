@@ -462,6 +462,13 @@ class Device:
     def apply_ptr(self, r_ptr: int, z_ptr: int, where: int = N.DEVICE):
         check(lib.hfpg_apply(self.h, r_ptr, z_ptr, where))
 
+    def apply_exact(self, r: np.ndarray) -> np.ndarray:
+        """apply<float> bit for bit (hfpg_apply_exact; the exact PCG's factor preconditioner)."""
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.empty_like(r)
+        check(lib.hfpg_apply_exact(self.h, r.ctypes.data, z.ctypes.data, N.HOST))
+        return z
+
     def spmv(self, x: np.ndarray) -> np.ndarray:
         x = np.ascontiguousarray(x, np.float64)
         y = np.empty_like(x)

@@ -1540,6 +1540,51 @@ int hfpg_pcg_solve_wait(hfpg_handle* h, double* history, hfpg_report* report, in
     return guarded([&] { solve_finish(h, history, report, where); });
 }
 
+// Device scratch for apply_exact_f32 (one float buffer carved into the stage arrays).
+struct ExApplyBuf {
+    float* buf = nullptr;
+    ExApplyWs w{};
+    void alloc(const Layout& L) {
+        const uint64_t n = L.n, K = L.k, M = K ? K - 1 : 0, ls = L.ls, rk = L.rk;
+        const uint64_t sizes[12] = {n, n, K * ls, K * ls, M * ls, M * ls, M * rk, M * rk, M * ls, M * ls, K * ls, K * ls};
+        uint64_t tot = 0;
+        for (uint64_t v : sizes) tot += v + 4;
+        dalloc(buf, tot);
+        float** dst[12] = {&w.rin, &w.coef, &w.rr, &w.rc, &w.scr, &w.scc, &w.cc1, &w.cc2, &w.crow, &w.ccol, &w.gr, &w.gc};
+        uint64_t off = 0;
+        for (int i = 0; i < 12; ++i) {
+            *dst[i] = buf + off;
+            off += sizes[i] + 4;
+        }
+    }
+    ~ExApplyBuf() { dfree(buf); }
+};
+double factor_shift(const hfpg_handle* h) {
+    return h->spd_enabled ? std::log1p(std::exp(h->spd_raw)) : 0.0;  // factor_tensor.hpp:64
+}
+
+// apply<float> bit for bit (pcg_exact.cuh): z = M r.
+int hfpg_apply_exact(hfpg_handle* h, const double* r, double* z, int where) {
+    return guarded([&] {
+        set_device(h);
+        if (h->part.G > 1) throw InvalidArgument("apply: partitioned handle");
+        require_apply_ready(h);
+        const uint64_t n = h->n;
+        double *dr = nullptr, *dz = nullptr;
+        dalloc(dr, n);
+        dalloc(dz, n);
+        ExApplyBuf eb;
+        eb.alloc(h->L);
+        CK(cudaMemcpyAsync(dr, r, n * 8, where == HFPG_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, h->stream));
+        apply_exact_f32(h->stream, h->L, h->F, h->a_diag, factor_shift(h), dr, dz, eb.w);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(z, dz, n * 8, where == HFPG_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        dfree(dr);
+        dfree(dz);
+    });
+}
+
 // pcg.cpp:53-126 bit for bit (pcg_exact.cuh): a host-driven loop over the solve path's SpMV and
 // preconditioner kernels with every dot product as the reference's sequential loop.
 int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg_in, double* x,
@@ -1564,6 +1609,8 @@ int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_confi
         dalloc(dsum, 4);
         CK(cudaMallocHost(&hsum, 4 * sizeof(double)));
         SeqScratch sc;
+        ExApplyBuf eb;
+        if (h->precond == HFPG_PRECOND_FACTOR) eb.alloc(h->L);
         auto cleanup = [&] {
             dfree(prod);
             dfree(dsum);
@@ -1590,9 +1637,7 @@ int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_confi
             };
             auto precond = [&] {  // z = M r
                 if (h->precond == HFPG_PRECOND_FACTOR) {
-                    const double shift = h->spd_enabled ? std::log1p(std::exp(h->spd_raw)) : 0.0;
-                    CK(cudaMemcpyAsync(&h->sc->shift, &shift, 8, cudaMemcpyHostToDevice, st));
-                    launch_apply(h, kApply, dr, dz);
+                    apply_exact_f32(st, h->L, h->F, h->a_diag, factor_shift(h), dr, dz, eb.w);
                 } else if (h->precond == HFPG_PRECOND_IC0) {
                     k_ic0_pending<<<g, 256, 0, st>>>(ic0_dev(h), dz, n);
                     launch_ic0_sweeps(h, h->sys, kApply, dr, dz);
