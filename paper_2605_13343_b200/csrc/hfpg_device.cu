@@ -417,10 +417,17 @@ Ic0Dev ic0_dev(const hfpg_handle* h) {
 void launch_ic0_sweeps(hfpg_handle* h, const DevSys& s, int mode, const double* rin, double* zout) {
     const unsigned g = unsigned((h->n + kIc0Threads - 1) / kIc0Threads);
     const Ic0Dev d = ic0_dev(h);
-    if (d.chunked) {
-        k_ic0_forward_chunk<<<g, kIc0ChunkThreads, 0, h->lstream>>>(s, d, rin, mode);
+    // the larger register budget wins while the wavefront is short next to the chunk count
+    // (2D 65K / 262K: 512 / 2,048 chunks); the higher residency once chunks far outnumber the
+    // slots (3D 1M: 8,192 chunks)
+    if (d.chunked && g <= unsigned(h->num_sms) * kIc0MinBlocksResident * 4) {
+        k_ic0_forward_chunk<kIc0MinBlocksResident><<<g, kIc0ChunkThreads, 0, h->lstream>>>(s, d, rin, mode);
         CK(cudaGetLastError());
-        k_ic0_backward_chunk<<<g, kIc0ChunkThreads, 0, h->lstream>>>(s, d, rin, zout, mode);
+        k_ic0_backward_chunk<kIc0MinBlocksResident><<<g, kIc0ChunkThreads, 0, h->lstream>>>(s, d, rin, zout, mode);
+    } else if (d.chunked) {
+        k_ic0_forward_chunk<kIc0MinBlocksWide><<<g, kIc0ChunkThreads, 0, h->lstream>>>(s, d, rin, mode);
+        CK(cudaGetLastError());
+        k_ic0_backward_chunk<kIc0MinBlocksWide><<<g, kIc0ChunkThreads, 0, h->lstream>>>(s, d, rin, zout, mode);
     } else {
         k_ic0_forward<<<g, kIc0Threads, 0, h->lstream>>>(s, d, rin, mode);
         CK(cudaGetLastError());

@@ -142,6 +142,12 @@ __global__ void __launch_bounds__(256) k_ic0_update(DevSys s, Ic0Dev d, int mode
 // rounding are the per-row kernels' (bit-identical to the reference).
 constexpr int kIc0ChunkThreads = kIc0Threads + 32;
 constexpr int kIc0Slots = 256;  // external dependencies per chunk served by the helper warp
+// Two register budgets: 4 CTAs per SM (96 registers, no spills) and 6 (64 registers). When the
+// chunks far outnumber the resident slots the sweep is a wavefront over CTAs dispatched in index
+// order and the number of chunks in flight bounds it (3D 1M: 1.38 -> 1.21 ms per IC(0)-PCG
+// iteration with 6); on the 2D grids the per-level latency dominates and the larger budget wins
+// (2D 65K: 0.65 vs 0.71 ms; 2D 262K: 1.42 vs 1.47 ms).
+constexpr int kIc0MinBlocksWide = 6, kIc0MinBlocksResident = 4;
 
 __device__ __forceinline__ unsigned long long ld_volatile_shared_u64(const unsigned long long* p) {
     return *reinterpret_cast<const volatile unsigned long long*>(p);
@@ -257,13 +263,15 @@ __device__ __forceinline__ double ic0_chunk_sweep(const Ic0Dev& d, const double*
     return res;
 }
 
-__global__ void __launch_bounds__(kIc0ChunkThreads) k_ic0_forward_chunk(DevSys s, Ic0Dev d, const double* rin,
+template <int MINB>
+__global__ void __launch_bounds__(kIc0ChunkThreads, MINB) k_ic0_forward_chunk(DevSys s, Ic0Dev d, const double* rin,
                                                                         int mode) {
     if (mode != kApply && s.sc->done) return;
     ic0_chunk_sweep<true>(d, rin, d.y, s.n, blockIdx.x);
 }
 
-__global__ void __launch_bounds__(kIc0ChunkThreads) k_ic0_backward_chunk(DevSys s, Ic0Dev d, const double* rin,
+template <int MINB>
+__global__ void __launch_bounds__(kIc0ChunkThreads, MINB) k_ic0_backward_chunk(DevSys s, Ic0Dev d, const double* rin,
                                                                          double* zout, int mode) {
     if (prolong_skip(s, mode)) return;
     const uint64_t nch = (s.n + kIc0Threads - 1) / kIc0Threads, ch = nch - 1 - blockIdx.x;
