@@ -28,7 +28,7 @@ void each(cudaStream_t st, uint64_t n, F f) {
 }
 
 // Batched small GEMMs through shared memory: out(r, j) = sum_p a(r, p) b(p, j) per batch entry
-// (blockIdx.z), a 64 x 64 output tile per CTA, 4 x 4 outputs per thread, p staged 16 at a time.
+// (blockIdx.z), 4 x 4 outputs per thread, p staged 16 at a time through shared memory.
 // Each output still accumulates over p in ascending order with the reference's rounding — fused
 // (DOT = false: gemm_nn / gemm_tn) or dot_ref's products-then-sums with a fused odd tail
 // (DOT = true: gemm_nt, the parameter gradients) — so tiling changes only the data reuse. NP = 2
@@ -39,13 +39,17 @@ struct BgOp {
     const double* b;
     uint64_t sb, bp, bj;  // b(p, j) = b[batch sb + p bp + j bj]
 };
-constexpr int kBgT = 64, kBgP = 16;
+constexpr int kBgP = 16;
 
-template <bool DOT, int NP, class Epi>
+// TM x TN output tile per CTA (TM * TN = 4096): 64 x 64, or 128 x 32 / 32 x 128 when one output
+// dimension is 32 (the bridge and restriction stages), so no thread idles on padding.
+template <bool DOT, int NP, int TM, int TN, class Epi>
 __global__ void __launch_bounds__(256) k_bgemm(uint64_t R, uint64_t J, uint64_t P, BgOp o0, BgOp o1, Epi epi) {
-    __shared__ double As[NP][kBgP][kBgT + 1], Bs[NP][kBgP][kBgT + 1];
-    const uint64_t bz = blockIdx.z, r0 = uint64_t(blockIdx.y) * kBgT, j0 = uint64_t(blockIdx.x) * kBgT;
-    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    constexpr int TX = TN / 4, TY = 256 / TX;
+    static_assert(TY * 4 == TM, "tile shape");
+    __shared__ double As[NP][kBgP][TM + 1], Bs[NP][kBgP][TN + 1];
+    const uint64_t bz = blockIdx.z, r0 = uint64_t(blockIdx.y) * TM, j0 = uint64_t(blockIdx.x) * TN;
+    const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
     double acc[NP][4][4];
 #pragma unroll
     for (int n = 0; n < NP; ++n)
@@ -58,14 +62,18 @@ __global__ void __launch_bounds__(256) k_bgemm(uint64_t R, uint64_t J, uint64_t 
         for (int n = 0; n < NP; ++n) {
             const BgOp& o = n ? o1 : o0;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
+            for (int e = 0; e < TM * kBgP / 256; ++e) {
                 const int idx = tid + 256 * e;
                 int r, pp;
-                if (o.ap == 1) { pp = idx & 15; r = idx >> 4; } else { r = idx & 63; pp = idx >> 6; }
+                if (o.ap == 1) { pp = idx % kBgP; r = idx / kBgP; } else { r = idx % TM; pp = idx / TM; }
                 const uint64_t gr = r0 + r, gp = p0 + pp;
                 As[n][pp][r] = gr < R && gp < P ? o.a[bz * o.sa + gr * o.ar + gp * o.ap] : 0.0;
-                int j;
-                if (o.bj == 1) { j = idx & 63; pp = idx >> 6; } else { pp = idx & 15; j = idx >> 4; }
+            }
+#pragma unroll
+            for (int e = 0; e < TN * kBgP / 256; ++e) {
+                const int idx = tid + 256 * e;
+                int j, pp;
+                if (o.bj == 1) { j = idx % TN; pp = idx / TN; } else { pp = idx % kBgP; j = idx / kBgP; }
                 const uint64_t gj = j0 + j, gq = p0 + pp;
                 Bs[n][pp][j] = gj < J && gq < P ? o.b[bz * o.sb + gq * o.bp + gj * o.bj] : 0.0;
             }
@@ -79,9 +87,9 @@ __global__ void __launch_bounds__(256) k_bgemm(uint64_t R, uint64_t J, uint64_t 
             for (int n = 0; n < NP; ++n) {
                 double a[4], b[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) a[i] = As[n][pp][ty + 16 * i];
+                for (int i = 0; i < 4; ++i) a[i] = As[n][pp][ty + TY * i];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) b[q] = Bs[n][pp][tx + 16 * q];
+                for (int q = 0; q < 4; ++q) b[q] = Bs[n][pp][tx + TX * q];
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -96,15 +104,21 @@ __global__ void __launch_bounds__(256) k_bgemm(uint64_t R, uint64_t J, uint64_t 
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const uint64_t r = r0 + ty + 16 * i, j = j0 + tx + 16 * q;
+            const uint64_t r = r0 + ty + TY * i, j = j0 + tx + TX * q;
             if (r < R && j < J) epi(bz, r, j, acc[0][i][q], acc[NP - 1][i][q]);
         }
+}
+template <bool DOT, int NP, int TM, int TN, class Epi>
+void bgemm_shape(cudaStream_t st, uint64_t batch, uint64_t R, uint64_t J, uint64_t P, BgOp o0, BgOp o1, Epi epi) {
+    const dim3 g(unsigned((J + TN - 1) / TN), unsigned((R + TM - 1) / TM), unsigned(batch));
+    k_bgemm<DOT, NP, TM, TN><<<g, 256, 0, st>>>(R, J, P, o0, o1, epi);
 }
 template <bool DOT, int NP, class Epi>
 void bgemm(cudaStream_t st, uint64_t batch, uint64_t R, uint64_t J, uint64_t P, BgOp o0, BgOp o1, Epi epi) {
     if (!batch || !R || !J) return;
-    const dim3 g(unsigned((J + kBgT - 1) / kBgT), unsigned((R + kBgT - 1) / kBgT), unsigned(batch));
-    k_bgemm<DOT, NP><<<g, 256, 0, st>>>(R, J, P, o0, o1, epi);
+    if (J <= 32) bgemm_shape<DOT, NP, 128, 32>(st, batch, R, J, P, o0, o1, epi);
+    else if (R <= 32) bgemm_shape<DOT, NP, 32, 128>(st, batch, R, J, P, o0, o1, epi);
+    else bgemm_shape<DOT, NP, 64, 64>(st, batch, R, J, P, o0, o1, epi);
 }
 
 // Device views of the batch state (all f64). L = 128, Ls = 32, rank 16 (the fast layout).
