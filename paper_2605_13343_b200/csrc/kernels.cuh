@@ -276,6 +276,9 @@ __global__ void __launch_bounds__(256) k_spmv(DevSys s, const double* xin, doubl
 // flight), then gather z / p_prev (L1/L2-resident neighbours) and accumulate. No CTA-wide
 // barrier inside the loop. Same arithmetic as k_spmv (bit-identical to the reference spmv).
 // Used when every chunk fits a stage (host-checked); k_spmv covers the general case.
+#ifndef HFPG_SPMV_MINB
+#define HFPG_SPMV_MINB 3
+#endif
 constexpr int kSpmvStages = 3;
 constexpr int kSpmvThreads = 288;  // 8 consumer warps + 1 producer warp
 constexpr uint32_t kSpmvHdr = 128; // per stage: 9 slice offsets (u64)
@@ -310,7 +313,7 @@ __device__ __forceinline__ double sell_row_release(const double* vals, const uin
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kSpmvThreads, 3) k_spmv_tma(DevSys s, const double* xin, double* yout) {
+__global__ void __launch_bounds__(kSpmvThreads, HFPG_SPMV_MINB) k_spmv_tma(DevSys s, const double* xin, double* yout) {
     if (MODE == kLoop && s.sc->done) return;
     extern __shared__ __align__(128) unsigned char sraw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(sraw);
