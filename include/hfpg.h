@@ -288,6 +288,10 @@ int hfpg_pcg_solve(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg
  * identity). A verification mode: several host round trips per iteration. */
 int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg, double* x,
                          double* history, hfpg_report* report, int where);
+/* pcg.cpp:56,102 residual_vectors: hfpg_pcg_solve_exact calls fn(user, k, r_k, n) after every
+ * iteration's residual update (r_k in host memory, valid during the call). NULL disables. */
+typedef void (*hfpg_residual_fn)(void* user, uint64_t k, const double* r, uint64_t n);
+int hfpg_set_residual_callback(hfpg_handle* h, hfpg_residual_fn fn, void* user);
 /* apply.cpp:80-173 apply<float> bit for bit (the pinned build's float accumulation and
  * contractions, stage by stage): the factor preconditioner of hfpg_pcg_solve_exact. */
 int hfpg_apply_exact(hfpg_handle* h, const double* r, double* z, int where);

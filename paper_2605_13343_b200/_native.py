@@ -120,6 +120,7 @@ _PROTOS = {
                                   C.POINTER(dbl)]),
     "hfpg_ic0_apply": (C.c_int, [vp, vp, vp, C.c_int]),
     "hfpg_apply_exact": (C.c_int, [vp, vp, vp, C.c_int]),
+    "hfpg_set_residual_callback": (C.c_int, [vp, vp, vp]),
     "hfpg_pcg_solve": (C.c_int, [vp, vp, C.POINTER(SolveConfigC), vp, vp, C.POINTER(ReportC),
                                  C.c_int]),
     "hfpg_pcg_solve_exact": (C.c_int, [vp, vp, C.POINTER(SolveConfigC), vp, vp, C.POINTER(ReportC),
@@ -183,3 +184,6 @@ def check(rc: int) -> None:
     if rc == HFPG_ECUDA:
         raise CudaError(msg)
     raise RuntimeError(msg)  # std::runtime_error (I/O, format, checksum)
+
+# pcg.cpp:102 residual_vectors callback (hfpg_residual_fn)
+RESIDUAL_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.POINTER(C.c_double), C.c_uint64)

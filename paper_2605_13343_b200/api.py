@@ -751,11 +751,14 @@ def factor_applier(factors: FactorTensor, A: CsrMatrix) -> PrecondApplier:
 
 
 def pcg_solve(A: CsrMatrix, b, precond: PrecondApplier, cfg: SolveConfig | None = None,
-              x_out: list | None = None, exact: bool = False) -> SolveReport:
+              x_out: list | None = None, exact: bool = False,
+              residual_vectors: list | None = None) -> SolveReport:
     """pcg.cpp:53-126, whole loop in one CUDA graph. If x_out is a list, the solution is
     appended to it (the reference's optional std::vector<double>* out-parameter).
     exact=True: every dot product as the reference's sequential loop (hfpg_pcg_solve_exact), so
-    x, the history and the iteration count are the reference's bit for bit (slower)."""
+    x, the history and the iteration count are the reference's bit for bit (slower).
+    residual_vectors: a list receiving r_k after every iteration (pcg.cpp:102); delivered by the
+    host-driven exact loop, so it implies exact=True."""
     cfg = cfg or SolveConfig()
     if cfg.rtol <= 0.0:
         raise ValueError("pcg_solve: rtol must be positive")
@@ -765,7 +768,15 @@ def pcg_solve(A: CsrMatrix, b, precond: PrecondApplier, cfg: SolveConfig | None 
     dev = precond.bind(A)
     x = np.empty(A.n_rows)
     hist = np.empty(max(cfg.max_iters, 1))
-    rep = dev.solve_ptr(b.ctypes.data, x.ctypes.data, cfg, hist.ctypes.data, N.HOST, exact=exact)
+    if residual_vectors is not None:
+        exact = True
+        cb = N.RESIDUAL_FN(lambda _u, _k, r, n: residual_vectors.append(np.ctypeslib.as_array(r, (n,)).copy()))
+        check(lib.hfpg_set_residual_callback(dev.h, C.cast(cb, C.c_void_p), None))
+    try:
+        rep = dev.solve_ptr(b.ctypes.data, x.ctypes.data, cfg, hist.ctypes.data, N.HOST, exact=exact)
+    finally:
+        if residual_vectors is not None:
+            check(lib.hfpg_set_residual_callback(dev.h, None, None))
     if x_out is not None:
         x_out.append(x)
     return SolveReport(method=getattr(precond, "method", ""), n=int(rep.n),

@@ -94,6 +94,8 @@ struct hfpg_handle {
     Layout L;
     float* F = nullptr;
     int spd_enabled = 0;
+    hfpg_residual_fn res_fn = nullptr;  // pcg.cpp:102 residual_vectors (exact loop only)
+    void* res_user = nullptr;
     double spd_raw = 0.0;
     bool fast = false;
 
@@ -1547,6 +1549,13 @@ int hfpg_pcg_solve_wait(hfpg_handle* h, double* history, hfpg_report* report, in
     return guarded([&] { solve_finish(h, history, report, where); });
 }
 
+int hfpg_set_residual_callback(hfpg_handle* h, hfpg_residual_fn fn, void* user) {
+    return guarded([&] {
+        h->res_fn = fn;
+        h->res_user = fn ? user : nullptr;
+    });
+}
+
 // Device scratch for apply_exact_f32 (one float buffer carved into the stage arrays).
 struct ExApplyBuf {
     float* buf = nullptr;
@@ -1661,7 +1670,7 @@ int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_confi
             CK(cudaEventRecord(e0, st));
             CK(cudaMemsetAsync(dx, 0, n * 8, st));
             copy_in(h, dr, b, n, where);
-            std::vector<double> hist;
+            std::vector<double> hist, rbuf;
             uint64_t iterations = 0, breakdown_iter = 0;
             int status = HFPG_MAX_ITERS, converged = 0;
             dot(dr, dr, 0, 1);
@@ -1696,6 +1705,12 @@ int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_confi
                     fetch(1);
                     const double rel = std::sqrt(hsum[0]) / r0;
                     hist.push_back(rel);
+                    if (h->res_fn) {  // residual_vectors->push_back(r) (pcg.cpp:102)
+                        if (rbuf.size() != n) rbuf.resize(n);
+                        CK(cudaMemcpyAsync(rbuf.data(), dr, n * 8, cudaMemcpyDeviceToHost, st));
+                        CK(cudaStreamSynchronize(st));
+                        h->res_fn(h->res_user, k, rbuf.data(), n);
+                    }
                     if (rel <= cfg.rtol) {
                         status = HFPG_CONVERGED;
                         converged = 1;

@@ -133,3 +133,14 @@ def test_exact_full_size_matches_reference_runs(H, name):
         assert rep.iterations == want[kind]["iterations"], (kind, rep.iterations)
         assert rep.status.name == want[kind]["status"]
         assert rep.residual_history[-1] == want[kind]["final_rel"], (kind, rep.residual_history[-1])
+
+
+def test_residual_vectors(H):
+    # pcg.cpp:102: one r_k per iteration, the last one the returned solution's residual
+    fr = H.make_frame(1024, 7, 3)
+    rv, xs = [], []
+    rep = H.pcg_solve(fr.A, fr.b, H.jacobi_applier(fr.A), H.SolveConfig(), xs, residual_vectors=rv)
+    assert rep.converged and len(rv) == rep.iterations == len(rep.residual_history)
+    r0 = np.linalg.norm(fr.b)
+    for k in (0, len(rv) // 2, len(rv) - 1):
+        assert np.sqrt(np.dot(rv[k], rv[k])) / r0 == pytest.approx(rep.residual_history[k], rel=1e-12)
