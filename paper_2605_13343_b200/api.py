@@ -547,6 +547,16 @@ class SolveReport:
     frame_id: str = ""
     breakdown_iter: int = 0
 
+    def to_json(self) -> str:
+        """pcg.cpp:12-26 (same keys; breakdown_iter only on breakdown)."""
+        import json
+        j = {"method": self.method, "n": self.n, "iterations": self.iterations, "converged": self.converged,
+             "status": self.status.name, "wall_ms": self.wall_ms, "frame_id": self.frame_id}
+        if self.status == SolveStatus.breakdown:
+            j["breakdown_iter"] = self.breakdown_iter
+        j["residual_history"] = list(self.residual_history)
+        return json.dumps(j, separators=(",", ":"))
+
 
 class PrecondApplier:
     """pcg.hpp:36: callable z = M r (host arrays; H2D -> device apply -> D2H, for parity and

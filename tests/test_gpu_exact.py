@@ -144,3 +144,20 @@ def test_residual_vectors(H):
     r0 = np.linalg.norm(fr.b)
     for k in (0, len(rv) // 2, len(rv) - 1):
         assert np.sqrt(np.dot(rv[k], rv[k])) / r0 == pytest.approx(rep.residual_history[k], rel=1e-12)
+
+
+def test_cli_solve(tmp_path):
+    # the hfp solve front end with the hfactor-gpu method tag
+    import json
+    import subprocess
+    import sys
+    from conftest import ROOT
+    rep = tmp_path / "rep.json"
+    r = subprocess.run([sys.executable, "-m", "paper_2605_13343_b200", "solve", "--n", "1024", "--seed", "7",
+                        "--frame-index", "3", "--method", "hfactor-gpu", "--report", str(rep)],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.startswith("hfactor-gpu: converged in ")
+    j = json.loads(rep.read_text())
+    assert j["method"] == "hfactor-gpu" and j["converged"] and j["status"] == "converged"
+    assert len(j["residual_history"]) == j["iterations"]
