@@ -338,6 +338,27 @@ def run_ours(args, cfg):
         "gpu_launches": args.steps * launches_per_solve(dev, iters[-1]),
         "clocks": clk.summary(),
     }
+    if rank == 0 and not args.no_parity:
+        # outside the timed region: the bit-exact loop (hfpg_pcg_solve_exact) on the same system,
+        # against the reference's own run at this size (tests/golden/ref_iterations.json)
+        want = None
+        try:
+            want = json.load(open(ITERS))[cfg["ref_key"]]["factor"]
+        except Exception:
+            pass
+        hist_d = torch.empty(sc.max_iters, dtype=torch.float64, device=f"cuda:{local}")
+        xr = torch.empty_like(b_d)
+        rx = dev.solve_ptr(b_d.data_ptr(), xr.data_ptr(), sc, hist_d.data_ptr(), N.DEVICE, exact=True)
+        last = float(hist_d[int(rx.history_len) - 1].item()) if rx.history_len else None
+        line["parity"] = {
+            "graph_iterations": iters[-1], "exact_iterations": int(rx.iterations),
+            "reference_iterations": want["iterations"] if want else None,
+            "exact_final_rel": last, "reference_final_rel": want["final_rel"] if want else None,
+            "exact_bit_identical_to_reference": bool(want) and int(rx.iterations) == want["iterations"]
+                                               and last == want["final_rel"],
+            "exact_ms": float(rx.wall_ms),
+            "how": "hfpg_pcg_solve_exact (sequential dots emulated exactly, apply<float> bit for bit) "
+                   "vs the reference's own pcg_solve run at this size"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ms_it, n_it = cpu_sample(cfg, fr, f, args.ref_budget)
         its = ref_iterations(cfg["ref_key"]) or iters[-1]
@@ -583,6 +604,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-budget", type=float, default=10.0, help="CPU seconds per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the bit-exact parity solve")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
