@@ -113,7 +113,8 @@ def test_exact_dot_remainders(H, ref, n):
         assert same(rep.residual_history, hist) and same(xs[0], xr)
 
 
-@pytest.mark.parametrize("name", ["2d_8192", "2d_65536", "3d_1m_s1e-3", "2d_262144_t0_s1e-3"])
+@pytest.mark.parametrize("name", ["2d_8192", "2d_65536", "3d_1m_s1e-3", "2d_262144_t0_s1e-3",
+                                  "2d_262144_t0_s1e-2"])
 def test_exact_full_size_matches_reference_runs(H, name):
     # the reference's own runs at BASELINE sizes (tests/golden/ref_iterations.json, made by
     # running oracle/_ref): the exact solve reproduces the iteration count and the final
