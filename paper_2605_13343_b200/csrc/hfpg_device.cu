@@ -1686,6 +1686,71 @@ int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_confi
                 dot(dr, dz, 0, 0);
                 fetch(1);
                 double rz = hsum[0];
+                if (!h->res_fn && cfg.max_iters > 0 && !std::getenv("HFPG_EXACT_HOSTLOOP")) {
+                    // one captured CUDA graph per iteration, the scalar decisions on the device
+                    // (ExState); the host polls the state every kBatch iterations
+                    constexpr uint64_t kBatch = 8;
+                    ExState* S = nullptr;
+                    double* dhist = nullptr;
+                    dalloc(S, 1);
+                    dalloc(dhist, cfg.max_iters);
+                    ExState hs{rz, 0.0, 0.0, r0, breakdown_tol, cfg.rtol, 1ULL, 0ULL, 0, 0};
+                    CK(cudaMemcpyAsync(S, &hs, sizeof(ExState), cudaMemcpyHostToDevice, st));
+                    CK(cudaStreamSynchronize(st));
+                    cudaGraph_t gr = nullptr;
+                    cudaGraphExec_t ge = nullptr;
+                    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                    try {
+                        launch_spmv<kApply>(h, h->sys, dp, dap);
+                        dot(dp, dap, 0, 0);
+                        dot(dp, dp, 1, 0);
+                        k_exg_alpha<<<1, 1, 0, st>>>(S, dsum);
+                        k_exg_xr<<<g, 256, 0, st>>>(S, dx, dr, dp, dap, n);
+                        dot(dr, dr, 2, 0);
+                        k_exg_rel<<<1, 1, 0, st>>>(S, dsum + 2, dhist);
+                        precond();
+                        dot(dr, dz, 3, 0);
+                        k_exg_beta<<<1, 1, 0, st>>>(S, dsum + 3);
+                        k_exg_p<<<g, 256, 0, st>>>(S, dp, dz, n);
+                        CK(cudaGetLastError());
+                    } catch (...) {
+                        cudaStreamEndCapture(st, &gr);
+                        if (gr) cudaGraphDestroy(gr);
+                        dfree(S);
+                        dfree(dhist);
+                        throw;
+                    }
+                    CK(cudaStreamEndCapture(st, &gr));
+                    CK(cudaGraphInstantiate(&ge, gr, 0));
+                    uint64_t launched = 0;
+                    while (launched < cfg.max_iters) {
+                        const uint64_t batch = std::min<uint64_t>(kBatch, cfg.max_iters - launched);
+                        for (uint64_t q = 0; q < batch; ++q) CK(cudaGraphLaunch(ge, st));
+                        launched += batch;
+                        CK(cudaMemcpyAsync(&hs, S, sizeof(ExState), cudaMemcpyDeviceToHost, st));
+                        CK(cudaStreamSynchronize(st));
+                        if (hs.stop) break;
+                    }
+                    uint64_t hlen = cfg.max_iters;
+                    if (hs.stop == 1) {
+                        status = HFPG_CONVERGED;
+                        converged = 1;
+                        iterations = hlen = hs.iters;
+                    } else if (hs.stop == 2) {
+                        status = HFPG_BREAKDOWN;
+                        breakdown_iter = iterations = hs.iters;
+                        hlen = hs.iters - 1;
+                    } else {
+                        iterations = cfg.max_iters;
+                    }
+                    hist.resize(hlen);
+                    if (hlen) CK(cudaMemcpyAsync(hist.data(), dhist, hlen * 8, cudaMemcpyDeviceToHost, st));
+                    CK(cudaStreamSynchronize(st));
+                    cudaGraphExecDestroy(ge);
+                    cudaGraphDestroy(gr);
+                    dfree(S);
+                    dfree(dhist);
+                } else
                 for (uint64_t k = 1; k <= cfg.max_iters; ++k) {
                     launch_spmv<kApply>(h, h->sys, dp, dap);
                     CK(cudaGetLastError());

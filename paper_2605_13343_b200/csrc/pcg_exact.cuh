@@ -58,7 +58,21 @@ inline void apply_exact_f32(cudaStream_t st, const Layout L, const float* P, con
         uint64_t span, rb, cb;
         tile_span(K, m, span, rb, cb);
         double sr = 0.0, sc = 0.0;
-        for (uint64_t q = 0; q < span; ++q) {
+        uint64_t q = 0;
+        for (; q + 8 <= span; q += 8) {  // 8 loads in flight, then the in-order adds
+            float a[8], b[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                a[e] = w.rr[(rb + q + e) * ls + j];
+                b[e] = w.rc[(cb + q + e) * ls + j];
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                sr = __dadd_rn(sr, double(a[e]));
+                sc = __dadd_rn(sc, double(b[e]));
+            }
+        }
+        for (; q < span; ++q) {
             sr = __dadd_rn(sr, double(w.rr[(rb + q) * ls + j]));
             sc = __dadd_rn(sc, double(w.rc[(cb + q) * ls + j]));
         }
@@ -146,6 +160,57 @@ __global__ void k_ex_jacobi(const double* __restrict__ r, const double* __restri
                             uint64_t n) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
         z[i] = __ddiv_rn(r[i], d[i]);
+}
+
+// Device-resident loop state for the captured iteration (hfpg_pcg_solve_exact without a
+// residual callback): the scalar decisions of pcg.cpp:86-119 taken on the device, so one CUDA
+// graph per iteration runs without host round trips; once `stop` is set every later step is a
+// no-op for x, r, p and the history.
+struct ExState {
+    double rz, alpha, beta, r0, tol_bd, rtol;
+    unsigned long long k, iters;  // current iteration (1-based); the stopping iteration
+    int stop, pad;                // 0 running, 1 converged, 2 breakdown
+};
+__global__ void k_exg_alpha(ExState* S, const double* dsum) {  // pcg.cpp:88-96
+    if (S->stop) return;
+    const double pap = dsum[0], p2 = dsum[1];
+    if (pap < -S->tol_bd * p2 || pap == 0.0) {
+        S->stop = 2;
+        S->iters = S->k;
+        return;
+    }
+    S->alpha = S->rz / pap;
+}
+__global__ void k_exg_xr(const ExState* S, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                         const double* __restrict__ ap, uint64_t n) {
+    if (S->stop) return;
+    const double alpha = S->alpha;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        x[i] = __fma_rn(alpha, p[i], x[i]);
+        r[i] = __fma_rn(-alpha, ap[i], r[i]);
+    }
+}
+__global__ void k_exg_rel(ExState* S, const double* rr, double* hist) {  // pcg.cpp:100-107
+    if (S->stop) return;
+    const double rel = sqrt(*rr) / S->r0;
+    hist[S->k - 1] = rel;
+    if (rel <= S->rtol) {
+        S->stop = 1;
+        S->iters = S->k;
+    }
+}
+__global__ void k_exg_beta(ExState* S, const double* rzn) {  // pcg.cpp:115-117
+    if (!S->stop) {
+        S->beta = *rzn / S->rz;
+        S->rz = *rzn;
+    }
+    S->k += 1;
+}
+__global__ void k_exg_p(const ExState* S, double* __restrict__ p, const double* __restrict__ z, uint64_t n) {
+    if (S->stop) return;
+    const double beta = S->beta;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        p[i] = __fma_rn(beta, p[i], z[i]);
 }
 
 }  // namespace hfpg

@@ -178,7 +178,21 @@ inline void train_forward(cudaStream_t st, const TrainDev T, const double* P) {
         uint64_t span, rb, cb;
         tile_span(K, m, span, rb, cb);
         double sr = 0.0, sc = 0.0;
-        for (uint64_t s = 0; s < span; ++s) {
+        uint64_t s = 0;
+        for (; s + 8 <= span; s += 8) {  // 8 loads in flight, then the in-order adds
+            double a[8], b[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                a[q] = T.Rr[(rb + s + q) * 32 * kz + e];
+                b[q] = T.Rc[(cb + s + q) * 32 * kz + e];
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                sr += a[q];
+                sc += b[q];
+            }
+        }
+        for (; s < span; ++s) {
             sr += T.Rr[(rb + s) * 32 * kz + e];
             sc += T.Rc[(cb + s) * 32 * kz + e];
         }
@@ -271,7 +285,21 @@ inline void train_adjoint(cudaStream_t st, const TrainDev T, const double* P, co
         uint64_t span, rb, cb;
         tile_span(K, m, span, rb, cb);
         double br = 0.0, bc = 0.0;
-        for (uint64_t s = 0; s < span; ++s) {
+        uint64_t s = 0;
+        for (; s + 8 <= span; s += 8) {
+            double a[8], b[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                a[q] = T.BGr[(rb + s + q) * 32 * kz + e];
+                b[q] = T.BGc[(cb + s + q) * 32 * kz + e];
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                br += a[q];
+                bc += b[q];
+            }
+        }
+        for (; s < span; ++s) {
             br += T.BGr[(rb + s) * 32 * kz + e];
             bc += T.BGc[(cb + s) * 32 * kz + e];
         }
