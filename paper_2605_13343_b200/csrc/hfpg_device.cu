@@ -1,4 +1,6 @@
 // Device handle, CUDA-graph PCG driver and the device half of the C ABI (include/hfpg.h).
+#include <atomic>
+
 #include "internal.hpp"
 #include "kernels.cuh"
 #include "solve_persistent.cuh"
@@ -732,11 +734,14 @@ void scan_counts(hfpg_handle* h, cudaStream_t st, const uint32_t* in, uint64_t n
 // loop, HFPG_FG_NOSUMM=1 the emulation without tile summaries (A/B checks).
 void seq_sum(cudaStream_t st, const double* src, uint64_t cnt, const unsigned long long* cnt_dev,
              uint64_t cnt_max, bool squares, double* out, SeqScratch& sc) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr_set{0};  // one bit per device (function attributes are per device)
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const uint64_t bit = 1ULL << (dev & 63);
+    if (!(attr_set.load() & bit)) {
         CK(cudaFuncSetAttribute(k_seq_sum<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSeqSmem)));
         CK(cudaFuncSetAttribute(k_seq_sum<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSeqSmem)));
-        attr = true;
+        attr_set.fetch_or(bit);
     }
     if (std::getenv("HFPG_FG_SERIAL")) {
         k_fg_chain<<<1, kFgChainThreads, 0, st>>>(src, cnt, cnt_dev, squares ? 1 : 0, out);
