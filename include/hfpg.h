@@ -215,6 +215,10 @@ int hfpg_apply(hfpg_handle* h, const double* r, double* z, int where);
  * zlib crc32 of `bytes` at data: HFPG_DEVICE computes it on the GPU (parallel CRC by
  * polynomial combination, bit-identical to zlib), HFPG_HOST with zlib. */
 int hfpg_crc32(hfpg_handle* h, const void* data, uint64_t bytes, int where, uint32_t* out);
+/* The checksum an HFTC payload / MPPF section stores (checkpoint.cpp:28-30, mppf.cpp:21-24):
+ * the reference casts the byte length to zlib's uInt, so it covers the first (bytes mod 2^32)
+ * bytes. Host memory. */
+int hfpg_payload_crc32(const void* data, uint64_t bytes, uint32_t* out);
 /* checkpoint.cpp:45-85 read_checkpoint straight into the handle's factor tensor: the payload is
  * streamed through pinned buffers into device memory and its crc32 checked on the GPU. Same
  * errors as hfpg_read_checkpoint; afterwards as hfpg_load_factors. */

@@ -105,6 +105,7 @@ _PROTOS = {
                                        C.POINTER(dbl)]),
     "hfpg_load_ic0": (C.c_int, [vp, u64, vp, vp, vp]),
     "hfpg_crc32": (C.c_int, [vp, vp, u64, C.c_int, C.POINTER(C.c_uint32)]),
+    "hfpg_payload_crc32": (C.c_int, [vp, u64, C.POINTER(C.c_uint32)]),
     "hfpg_load_checkpoint": (C.c_int, [vp, C.c_char_p]),
     "hfpg_write_mppf": (C.c_int, [vp, C.c_char_p]),
     "hfpg_read_mppf": (C.c_int, [C.c_char_p, C.POINTER(vp)]),

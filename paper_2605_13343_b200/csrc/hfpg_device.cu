@@ -1010,7 +1010,7 @@ void frame_from_mppf(hfpg_handle* h, const char* path) {
         stream_to_device(h, fp.get(), m.payload_offset + sc.offset, sc.bytes, d.p, "read_mppf");
     }
     for (const MppfSection& sc : m.sections)
-        if (device_crc(h, dst_of(sc.name).p, sc.bytes) != sc.crc)
+        if (device_crc(h, dst_of(sc.name).p, ref_crc_len(sc.bytes)) != sc.crc)
             throw IoError("read_mppf: checksum mismatch in section " + sc.name);
     // csr.cpp:9-53 in the reference's order of checks
     for (const MppfSection& sc : m.sections) {
@@ -2389,7 +2389,7 @@ int hfpg_load_checkpoint(hfpg_handle* h, const char* path) {
         if (!h->have_factors || h->L.total != L.total) dalloc(h->F, L.total);
         h->have_factors = false;
         stream_to_device(h, fp.get(), H.payload_offset, L.total * 4, h->F, "read_checkpoint");
-        if (device_crc(h, h->F, L.total * 4) != H.crc) throw IoError("read_checkpoint: payload checksum mismatch");
+        if (device_crc(h, h->F, ref_crc_len(L.total * 4)) != H.crc) throw IoError("read_checkpoint: payload checksum mismatch");
         h->L = L;
         h->have_factors = true;
         h->spd_enabled = H.spd_enabled;

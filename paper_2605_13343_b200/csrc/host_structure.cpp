@@ -450,11 +450,12 @@ uint64_t need_u64(const JsonHeader& h, const char* k) {
     return std::stoull(*v);
 }
 uint32_t crc_of(const float* p, uint64_t n) {
-    // zlib's crc32 takes uInt lengths; the reference passes the whole payload at once
-    // (checkpoint.cpp:28-30), which is the same as chaining for payloads < 4 GiB.
+    // The reference passes the whole payload to zlib in one call with the length cast to uInt
+    // (checkpoint.cpp:28-30, 79-81): it checksums the first (bytes mod 2^32) bytes only, which
+    // matters from 4 GiB payloads on (N >= ~5.6M). Same prefix here, chained in 1 GiB pieces.
     uLong c = ::crc32(0L, Z_NULL, 0);
     const Bytef* b = reinterpret_cast<const Bytef*>(p);
-    uint64_t left = n * sizeof(float);
+    uint64_t left = ref_crc_len(n * sizeof(float));
     while (left) {
         const uInt chunk = static_cast<uInt>(std::min<uint64_t>(left, 1u << 30));
         c = ::crc32(c, b, chunk);
@@ -493,6 +494,8 @@ const std::string& need(const JsonHeader& h, const char* k) {
 }
 const char kMppfMagic[8] = {'M', 'P', 'P', 'F', '0', '0', '0', '1'};
 uint32_t crc_bytes(const void* p, uint64_t bytes) {
+    // mppf.cpp:21-24 casts the section length to uInt as well: first (bytes mod 2^32) bytes
+    bytes = ref_crc_len(bytes);
     uLong c = ::crc32(0L, Z_NULL, 0);
     const Bytef* b = static_cast<const Bytef*>(p);
     while (bytes) {
@@ -633,6 +636,12 @@ std::vector<uint32_t> morton_order_2d(uint64_t w, uint64_t h, uint64_t n) {
 using namespace hfpg;
 
 extern "C" {
+
+// The checksum HFTC payloads and MPPF sections carry (checkpoint.cpp:28-30, mppf.cpp:21-24):
+// zlib crc32 of the first (bytes mod 2^32) bytes.
+int hfpg_payload_crc32(const void* data, uint64_t bytes, uint32_t* out) {
+    return guarded([&] { *out = crc_bytes(data, bytes); });
+}
 
 int hfpg_packed_width(uint64_t n, uint64_t leaf, uint64_t ls, uint64_t* out) {
     return guarded([&] {

@@ -26,6 +26,11 @@ struct CudaError : std::runtime_error {
 
 void set_error(const std::string& msg);
 
+// The reference hands zlib a whole payload / section with its byte length cast to uInt
+// (checkpoint.cpp:28-30, 79-81; mppf.cpp:21-24), so its stored crc32 covers only the first
+// (bytes mod 2^32) bytes. Every HFTC / MPPF checksum here covers the same prefix.
+inline uint64_t ref_crc_len(uint64_t bytes) { return bytes & 0xFFFFFFFFull; }
+
 // ic0_host.cpp (ic0.cpp:10-69): lower IC(0) factor of A (policy 0 none, 1 scaled); its transpose.
 void ic0_factorize_host(uint64_t n, const uint64_t* ro, const uint32_t* ci, const double* v, int policy,
                         std::vector<uint64_t>& lro, std::vector<uint32_t>& lci, std::vector<double>& lv,

@@ -81,3 +81,31 @@ def test_errors(H, ref, tmp_path):
     with pytest.raises(ValueError):
         H.write_mppf(H.make_frame_3d(4, 4, 4, 1, 0), path)
     os.remove(path)
+
+
+def test_payload_crc_covers_length_mod_2_32():
+    """checkpoint.cpp:28-30 / mppf.cpp:21-24 pass the byte length to zlib as uInt: a payload of
+    2^32 + k bytes is checksummed over its first k bytes only. An anonymous mapping keeps the
+    4 GiB region virtual (untouched zero pages)."""
+    import ctypes
+    import mmap
+    import zlib
+
+    from paper_2605_13343_b200 import _native as N
+    size = (1 << 32) + 4096
+    m = mmap.mmap(-1, size)
+    try:
+        m[:4096] = bytes(range(256)) * 16
+        m[size - 8:] = b"tailtail"  # beyond 2^32: not covered, like the reference
+        base = ctypes.addressof(ctypes.c_char.from_buffer(m))
+        out = ctypes.c_uint32()
+        N.check(N.lib.hfpg_payload_crc32(base, size, ctypes.byref(out)))
+        assert out.value == zlib.crc32(m[:4096])
+        N.check(N.lib.hfpg_payload_crc32(base, 4096, ctypes.byref(out)))
+        assert out.value == zlib.crc32(m[:4096])
+        del base
+    finally:
+        try:
+            m.close()
+        except BufferError:
+            pass
