@@ -58,6 +58,10 @@ CONFIGS = {
                             "tensor (RngStream(2024, frame_id, factor_init); sigma=1e-2 leaves "
                             "frames at max_iters, DESIGN.md), sharded over the GPUs",
                        n=262144, sigma=1e-3, ref_key="2d_262144_t0_s1e-3"),
+    "2d_65536_infer": dict(kind="infer", n=65536,
+                           desc="BASELINE configs[1]: N=65,536 (make_frame(65536, 2024, 0) generated on the GPU), "
+                                "full toynet d128_L3_hw inference into the packed factor tensor + graph PCG; "
+                                "step = generate + forward + solve (device times)"),
     "part_16m": dict(kind="part",
                      desc="BASELINE configs[4]: N=16,777,216 3D 256^3 7-point pressure-Poisson, "
                           "seeded sigma=1e-3 tensor, row-partitioned over the GPUs along the "
@@ -216,6 +220,88 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------ configs[1]: inference + graph PCG
+
+
+def toynet_flops(n: int, L: int = 128, Ls: int = 32, d: int = 128, layers: int = 3, feat: int = 19) -> int:
+    """Dense-contraction FLOPs of one toynet forward as the reference computes it
+    (toy_net.cpp:225-586): encoder MLP + GCN, per layer QKV / QK^T / PV / O-projection / 4d FFN
+    (K = 4d, the glob slice included) for both streams, decoder heads. 2 FLOPs per MAC."""
+    K = n // L
+    mt = (K - 1) * Ls  # tile tokens
+
+    def stream(rows, T):
+        return rows * (d * 3 * d + 2 * T * d + d * d + 4 * d * 4 * d + 4 * d * d)
+
+    macs = n * (feat * d + d * d) + 2 * n * d * d  # encoder + 2 GCN layers
+    macs += layers * (stream(n, L) + stream(mt, Ls))
+    macs += n * (d * d + d * L + d * (2 * Ls + 1)) + mt * d * Ls  # decoder heads
+    return 2 * macs
+
+
+def run_inference(local: int, steps: int, warmup: int, n: int = 65536, solve: bool = True) -> dict:
+    """BASELINE configs[1]: the N=65,536 frame generated on the GPU (make_frame(n, 2024, 0)),
+    the d128_L3_hw toy network (seeded weights, toy_net.cpp:170-223) writing the packed factor
+    tensor straight into the handle, then the graph PCG on that tensor. Device times (CUDA
+    events on the handle's stream)."""
+    import paper_2605_13343_b200 as H
+    from paper_2605_13343_b200 import _native as N
+    import torch
+    dev = H.Device(local)
+    gen_ms, inf_ms = [], []
+    for i in range(warmup + steps):
+        gf = dev.frame_gpu(n, 2024, 0)
+        tr = H.ToynetTrace()
+        H.toynet_forward_gpu_frame(gf, 32, trace=tr, load=True)
+        if i >= warmup:
+            gen_ms.append(gf.generate_ms)
+            inf_ms.append(tr.ms)
+    fl = toynet_flops(n)
+    peak_bf16 = None
+    try:
+        peak_bf16 = float(json.load(open(PEAKS))["bf16_tflops_sustained"])
+        peak_src = "0.5 x MEASURED_PEAKS.json bf16_tflops_sustained (kind::tf32 runs at half the bf16 rate)"
+    except Exception:
+        peak_bf16 = 2250.0 * 0.85
+        peak_src = "0.5 x fallback bf16 dense (B200_PROFILING.md)"
+    peak = 0.5 * peak_bf16
+    ms = statistics.median(inf_ms)
+    out = {"workload": "BASELINE configs[1]: make_frame(65536, 2024, 0) generated on the GPU, toynet "
+                       "d128_L3_hw (d=128, 3 layers, 8 heads, L=128, L_s=32, weight seed 0) -> packed "
+                       "factor tensor on the device -> graph PCG",
+           "n": n, "generate_ms": statistics.median(gen_ms), "inference_ms": ms,
+           "inference_ms_all": inf_ms, "inference_flops": fl,
+           "roofline": {"bound": "tensor", "achieved": fl / (ms * 1e-3) / 1e12, "peak": peak,
+                        "unit": "TFLOP/s", "frac": fl / (ms * 1e-3) / 1e12 / peak,
+                        "peak_source": peak_src, "precision": "kind::tf32 products, fp32 accumulation"}}
+    if solve:
+        dev.set_precond(2)
+        x = torch.empty(n, dtype=torch.float64, device=f"cuda:{local}")
+        rep = dev.solve_ptr(gf.b, x.data_ptr(), H.SolveConfig(), None, N.DEVICE)
+        out.update({"solve_ms": float(rep.wall_ms), "solve_iterations": int(rep.iterations),
+                    "solve_status": H.SolveStatus(int(rep.status)).name,
+                    "solve_note": "the seeded-weight tensor is not a convergent preconditioner "
+                                  "(SURVEY.md section 0 fact 2: the reference stagnates / NaNs), so the "
+                                  "solve runs to max_iters exactly as the reference's does"})
+    return out
+
+
+def run_infer_config(args, cfg):
+    world, rank, local = dist_init()
+    import torch
+    torch.cuda.set_device(local)
+    with Clocks(local) as clk:
+        res = run_inference(local, args.steps, args.warmup, cfg["n"], solve=True)
+    step_ms = res["generate_ms"] + res["inference_ms"] + res["solve_ms"]
+    line = {"metric": METRIC, "value": step_ms, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (tf32 MMA) / f64", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "n": cfg["n"]},
+            "roofline": res.pop("roofline"), "inference": res, "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------------------- our arm
 
 
@@ -232,6 +318,8 @@ def run_ours(args, cfg):
         return run_batch(args, cfg)
     if cfg.get("kind") == "part":
         return run_part(args, cfg)
+    if cfg.get("kind") == "infer":
+        return run_infer_config(args, cfg)
     world, rank, local = dist_init()
     import torch
     torch.cuda.set_device(local)
@@ -359,6 +447,9 @@ def run_ours(args, cfg):
             "exact_ms": float(rx.wall_ms),
             "how": "hfpg_pcg_solve_exact (sequential dots emulated exactly, apply<float> bit for bit) "
                    "vs the reference's own pcg_solve run at this size"}
+    if rank == 0 and not args.no_inference:
+        # BASELINE configs[1] (N=65,536 inference + graph PCG), outside the timed region
+        line["inference"] = run_inference(local, 3, 1, 65536, solve=True)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ms_it, n_it = cpu_sample(cfg, fr, f, args.ref_budget)
         its = ref_iterations(cfg["ref_key"]) or iters[-1]
@@ -605,6 +696,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=10.0, help="CPU seconds per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the bit-exact parity solve")
+    ap.add_argument("--no-inference", action="store_true", help="skip the configs[1] inference object")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -17,6 +17,7 @@
 #include "hfpg.h"
 
 #include <cstdint>
+#include <cstring>
 #include <functional>
 #include <memory>
 #include <span>
@@ -80,11 +81,45 @@ std::function<void(std::span<const double>, std::span<double>)> factor_applier(
     };
 }
 
+// 64-bit content fingerprint of a CSR operator (structure and value bits), so gpu::pcg_solve can
+// tell whether the device operator is still the A it is handed (pcg.cpp:53 always uses its A).
+template <class Csr>
+uint64_t csr_fingerprint(const Csr& A) {
+    uint64_t h = 0x9E3779B97F4A7C15ull ^ (uint64_t(A.n_rows) * 0x100000001B3ull);
+    auto mix = [&h](const void* p, std::size_t bytes) {
+        const unsigned char* c = static_cast<const unsigned char*>(p);
+        std::size_t i = 0;
+        for (; i + 8 <= bytes; i += 8) {
+            uint64_t w;
+            std::memcpy(&w, c + i, 8);
+            h = (h ^ w) * 0x100000001B3ull;
+            h ^= h >> 29;
+        }
+        for (; i < bytes; ++i) h = (h ^ c[i]) * 0x100000001B3ull;
+        h ^= bytes;
+    };
+    mix(A.row_offsets.data(), A.row_offsets.size() * sizeof(A.row_offsets[0]));
+    mix(A.col_indices.data(), A.col_indices.size() * sizeof(A.col_indices[0]));
+    mix(A.values.data(), A.values.size() * sizeof(A.values[0]));
+    return h;
+}
+
 // Device-side description of the preconditioner for gpu::pcg_solve (pcg.cpp:28-51).
 struct Precond {
     std::shared_ptr<Device> dev;
     int kind = HFPG_PRECOND_FACTOR;
     std::string method;
+    std::shared_ptr<uint64_t> operator_fp = std::make_shared<uint64_t>(0);  // A on the device
+
+    // Make the device operator A (reload it when A's content differs from what was loaded).
+    template <class Csr>
+    void bind(const Csr& A) const {
+        const uint64_t fp = csr_fingerprint(A);
+        if (fp == *operator_fp) return;
+        dev->load_csr(A);
+        dev->set_precond(kind);
+        *operator_fp = fp;
+    }
 
     template <class Csr>
     static Precond identity(const Csr& A) {
@@ -110,6 +145,7 @@ struct Precond {
         p.dev->set_precond(kind);
         p.kind = kind;
         p.method = method;
+        *p.operator_fp = csr_fingerprint(A);
         return p;
     }
 };
@@ -136,6 +172,7 @@ Report pcg_solve(const Csr& A, std::span<const double> b, const Precond& M, cons
                  std::vector<double>* x_out = nullptr) {
     if (!(cfg.rtol > 0.0)) throw std::invalid_argument("pcg_solve: rtol must be positive");
     if (b.size() != A.n_rows) throw std::invalid_argument("pcg_solve: rhs length mismatch");
+    M.bind(A);  // solve with the A handed in, as pcg.cpp:53 does
     std::vector<double> x(A.n_rows), hist(cfg.max_iters ? cfg.max_iters : 1);
     hfpg_solve_config c{cfg.rtol, static_cast<uint64_t>(cfg.max_iters)};
     hfpg_report r{};

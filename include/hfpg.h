@@ -211,6 +211,10 @@ int hfpg_get_trace(hfpg_handle* h, uint64_t* out, uint32_t cap);
 
 /* apply.cpp:79-174 apply<float>: z = M r with the loaded factors and diag(A). */
 int hfpg_apply(hfpg_handle* h, const double* r, double* z, int where);
+/* pcg.cpp:28-51 PrecondApplier of the handle's current kind (hfpg_set_precond): identity
+ * (z = r), jacobi (z = r / a_ii, IEEE division, pcg.cpp:34-42), factor (hfpg_apply) or IC(0)
+ * (hfpg_ic0_apply), on the device. */
+int hfpg_precond_apply(hfpg_handle* h, const double* r, double* z, int where);
 /* ---- on-disk formats (mppf.hpp / checkpoint.hpp) ----
  * zlib crc32 of `bytes` at data: HFPG_DEVICE computes it on the GPU (parallel CRC by
  * polynomial combination, bit-identical to zlib), HFPG_HOST with zlib. */

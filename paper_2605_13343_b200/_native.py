@@ -100,6 +100,7 @@ _PROTOS = {
     "hfpg_set_diag": (C.c_int, [vp, u64, vp, C.c_int]),
     "hfpg_set_precond": (C.c_int, [vp, C.c_int]),
     "hfpg_apply": (C.c_int, [vp, vp, vp, C.c_int]),
+    "hfpg_precond_apply": (C.c_int, [vp, vp, vp, C.c_int]),
     "hfpg_spmv": (C.c_int, [vp, vp, vp, C.c_int]),
     "hfpg_ic0_factor_host": (C.c_int, [u64, vp, vp, vp, i32, vp, vp, vp, u64, C.POINTER(u64),
                                        C.POINTER(dbl)]),

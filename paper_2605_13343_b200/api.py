@@ -395,11 +395,23 @@ class Device:
         check(lib.hfpg_load_csr(self.h, A.n_rows, A.row_offsets.ctypes.data,
                                 A.col_indices.ctypes.data, A.values.ctypes.data, N.HOST))
         self.csr_id = id(A)
+        # content snapshot: a solve must use the A it is handed (pcg.cpp:53), even if the caller
+        # edited the arrays in place or a new matrix reuses a freed object's id
+        self._csr_snap = (A.n_rows, A.row_offsets.copy(), A.col_indices.copy(), A.values.view(np.uint64).copy())
+
+    def holds_csr(self, A: CsrMatrix) -> bool:
+        """True when the device operator is bit-identical to A (structure and values)."""
+        snap = getattr(self, "_csr_snap", None)
+        if snap is None or snap[0] != A.n_rows or len(snap[3]) != len(A.values):
+            return False
+        return (np.array_equal(snap[1], A.row_offsets) and np.array_equal(snap[2], A.col_indices)
+                and np.array_equal(snap[3], A.values.view(np.uint64)))
 
     def _gpu_frame(self, seed, fidx) -> GpuFrame:
         v = N.FrameDeviceC()
         check(lib.hfpg_frame_gpu_view(self.h, C.byref(v)))
         self.csr_id = ("gpu_frame", seed, fidx)
+        self._csr_snap = None
         return GpuFrame(v.n, v.nnz, v.width, v.height, v.depth, v.rho_heavy, v.cell_order or 0,
                         v.rho or 0, v.row_offsets or 0, v.col_indices or 0, v.values or 0, v.b or 0,
                         v.a_diag or 0, float(v.generate_ms), float(v.frobenius), seed, fidx, self)
@@ -416,6 +428,8 @@ class Device:
 
     def load_csr_device(self, n, ro_ptr, ci_ptr, v_ptr):
         check(lib.hfpg_load_csr(self.h, n, ro_ptr, ci_ptr, v_ptr, N.DEVICE))
+        self.csr_id = ("device", ro_ptr, ci_ptr, v_ptr)
+        self._csr_snap = None
 
     def load_mppf(self, path: str) -> "GpuFrame":
         """read_mppf on the device (pinned streaming, GPU crc32 and CSR checks); the frame becomes
@@ -570,7 +584,7 @@ class PrecondApplier:
     def bind(self, A: CsrMatrix) -> Device:
         if self.dev is None:
             self.dev = Device(0)
-        if self.dev.csr_id != id(A):
+        if not self.dev.holds_csr(A):
             self.dev.load_csr(A)
         self.dev.set_precond(self.kind)
         return self.dev
@@ -592,10 +606,19 @@ class _Jacobi(PrecondApplier):
         super().__init__(Device(0))
         self.dev.load_csr(A)
         self.dev.set_precond(1)  # throws ValueError on a nonpositive diagonal (pcg.cpp:36-38)
-        self.diag = A.diagonal()
 
     def __call__(self, r):
-        return np.asarray(r, np.float64) / self.diag
+        """pcg.cpp:40: z_i = r_i / a_ii, on the device (hfpg_precond_apply)."""
+        r = np.ascontiguousarray(r, np.float64)
+        if len(r) != self.dev_n():
+            raise ValueError("apply: length mismatch")
+        z = np.empty_like(r)
+        self.dev.set_precond(self.kind)
+        check(lib.hfpg_precond_apply(self.dev.h, r.ctypes.data, z.ctypes.data, N.HOST))
+        return z
+
+    def dev_n(self) -> int:
+        return len(self.dev._csr_snap[1]) - 1
 
 
 class _Factor(PrecondApplier):
@@ -721,7 +744,7 @@ class _Ic0(PrecondApplier):
             self.bind(A)
 
     def bind(self, A: "CsrMatrix") -> Device:
-        if self.dev.csr_id != id(A):
+        if not self.dev.holds_csr(A):
             self.dev.load_csr(A)
         L = self.factor.lower
         lro = np.ascontiguousarray(L.row_offsets, np.uint64)

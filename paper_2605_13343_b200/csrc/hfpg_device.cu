@@ -37,6 +37,16 @@ static void dfree(T*& p) {
     if (p) cudaFree(const_cast<void*>(static_cast<const void*>(p)));
     p = nullptr;
 }
+// Runs its callable when the scope ends, on every exit path.
+template <class F>
+struct ScopeExit {
+    F f;
+    ~ScopeExit() { f(); }
+};
+template <class F>
+ScopeExit<F> on_scope_exit(F f) {
+    return ScopeExit<F>{f};
+}
 template <class T>
 static void dalloc(T*& p, size_t count) {
     dfree(p);
@@ -158,6 +168,9 @@ struct hfpg_handle {
 
     DevSys sys{};
     ToynetModel* toynet = nullptr;
+    // exact-mode apply<float> scratch (apply_exact_f32's stage arrays), grown once, reused
+    float* exbuf = nullptr;
+    uint64_t exbuf_cap = 0;
 
     // row partition (G > 1): this handle holds rank `rank`'s share of a system
     struct Part {
@@ -1270,6 +1283,7 @@ int hfpg_destroy(hfpg_handle* h) {
             if (h->pin_ev[q]) cudaEventDestroy(h->pin_ev[q]);
         }
         dfree(h->crc_scratch);
+        dfree(h->exbuf);
         for (double* b : h->tr.bufs) dfree(b);
         dfree(h->tr.P); dfree(h->tr.G); dfree(h->tr.BY); dfree(h->tr.Z); dfree(h->tr.part);
         if (h->stream) cudaStreamDestroy(h->stream);
@@ -1460,6 +1474,29 @@ int hfpg_apply(hfpg_handle* h, const double* r, double* z, int where) {
     });
 }
 
+int hfpg_precond_apply(hfpg_handle* h, const double* r, double* z, int where) {
+    if (h && h->precond == HFPG_PRECOND_FACTOR) return hfpg_apply(h, r, z, where);
+    if (h && h->precond == HFPG_PRECOND_IC0) return hfpg_ic0_apply(h, r, z, where);
+    return guarded([&] {
+        set_device(h);
+        if (h->part.G > 1) throw InvalidArgument("precond_apply: partitioned handle");
+        if (!h->have_csr) throw InvalidArgument("precond_apply: no matrix loaded");
+        ensure_workspace(h);
+        const double* rin = r;
+        double* zout = z;
+        if (where == HFPG_HOST) {
+            copy_in(h, h->scratch, r, h->n, HFPG_HOST);
+            rin = h->scratch;
+            zout = h->z;
+        }
+        k_diag_apply<<<unsigned(simple_grid(h)), 256, 0, h->stream>>>(h->n, rin, h->a_diag, zout,
+                                                                      h->precond == HFPG_PRECOND_JACOBI);
+        CK(cudaGetLastError());
+        if (where == HFPG_HOST) copy_out(h, z, h->z, h->n, HFPG_HOST);
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
 int hfpg_spmv(hfpg_handle* h, const double* x, double* y, int where) {
     return guarded([&] {
         set_device(h);
@@ -1485,6 +1522,9 @@ int hfpg_spmv(hfpg_handle* h, const double* x, double* y, int where) {
 // handle's pinned report buffer; x (n) is copied to `where` memory.
 static void solve_enqueue(hfpg_handle* h, const double* b, const hfpg_solve_config* cfg_in, double* x, int where) {
     set_device(h);
+    // the report buffer doubles as the config staging buffer: a second solve before the first
+    // one's report is collected would read back that solve's scalars as its config
+    if (h->pending) throw InvalidArgument("pcg_solve: a solve is in flight (hfpg_pcg_solve_wait first)");
     hfpg_solve_config cfg = cfg_in ? *cfg_in : hfpg_solve_config{1e-8, 20000};
     if (!(cfg.rtol > 0.0)) throw InvalidArgument("pcg_solve: rtol must be positive");
     if (!h->have_csr) throw InvalidArgument("pcg_solve: no matrix loaded");
@@ -1561,25 +1601,27 @@ int hfpg_set_residual_callback(hfpg_handle* h, hfpg_residual_fn fn, void* user) 
     });
 }
 
-// Device scratch for apply_exact_f32 (one float buffer carved into the stage arrays).
-struct ExApplyBuf {
-    float* buf = nullptr;
-    ExApplyWs w{};
-    void alloc(const Layout& L) {
-        const uint64_t n = L.n, K = L.k, M = K ? K - 1 : 0, ls = L.ls, rk = L.rk;
-        const uint64_t sizes[12] = {n, n, K * ls, K * ls, M * ls, M * ls, M * rk, M * rk, M * ls, M * ls, K * ls, K * ls};
-        uint64_t tot = 0;
-        for (uint64_t v : sizes) tot += v + 4;
-        dalloc(buf, tot);
-        float** dst[12] = {&w.rin, &w.coef, &w.rr, &w.rc, &w.scr, &w.scc, &w.cc1, &w.cc2, &w.crow, &w.ccol, &w.gr, &w.gc};
-        uint64_t off = 0;
-        for (int i = 0; i < 12; ++i) {
-            *dst[i] = buf + off;
-            off += sizes[i] + 4;
-        }
+// Device scratch for apply_exact_f32: one float buffer on the handle, carved into the stage
+// arrays; allocated on first use and kept (apply allocates nothing per call, test_apply.cpp:262).
+ExApplyWs exact_ws(hfpg_handle* h) {
+    const Layout& L = h->L;
+    const uint64_t n = L.n, K = L.k, M = K ? K - 1 : 0, ls = L.ls, rk = L.rk;
+    const uint64_t sizes[12] = {n, n, K * ls, K * ls, M * ls, M * ls, M * rk, M * rk, M * ls, M * ls, K * ls, K * ls};
+    uint64_t tot = 0;
+    for (uint64_t v : sizes) tot += v + 4;
+    if (h->exbuf_cap < tot) {
+        dalloc(h->exbuf, tot);
+        h->exbuf_cap = tot;
     }
-    ~ExApplyBuf() { dfree(buf); }
-};
+    ExApplyWs w{};
+    float** dst[12] = {&w.rin, &w.coef, &w.rr, &w.rc, &w.scr, &w.scc, &w.cc1, &w.cc2, &w.crow, &w.ccol, &w.gr, &w.gc};
+    uint64_t off = 0;
+    for (int i = 0; i < 12; ++i) {
+        *dst[i] = h->exbuf + off;
+        off += sizes[i] + 4;
+    }
+    return w;
+}
 double factor_shift(const hfpg_handle* h) {
     return h->spd_enabled ? std::log1p(std::exp(h->spd_raw)) : 0.0;  // factor_tensor.hpp:64
 }
@@ -1591,18 +1633,14 @@ int hfpg_apply_exact(hfpg_handle* h, const double* r, double* z, int where) {
         if (h->part.G > 1) throw InvalidArgument("apply: partitioned handle");
         require_apply_ready(h);
         const uint64_t n = h->n;
-        double *dr = nullptr, *dz = nullptr;
-        dalloc(dr, n);
-        dalloc(dz, n);
-        ExApplyBuf eb;
-        eb.alloc(h->L);
+        ensure_workspace(h);
+        double *dr = h->scratch, *dz = h->z;  // handle-owned (no allocation per call)
+        const ExApplyWs ws = exact_ws(h);
         CK(cudaMemcpyAsync(dr, r, n * 8, where == HFPG_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, h->stream));
-        apply_exact_f32(h->stream, h->L, h->F, h->a_diag, factor_shift(h), dr, dz, eb.w);
+        apply_exact_f32(h->stream, h->L, h->F, h->a_diag, factor_shift(h), dr, dz, ws);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(z, dz, n * 8, where == HFPG_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, h->stream));
         CK(cudaStreamSynchronize(h->stream));
-        dfree(dr);
-        dfree(dz);
     });
 }
 
@@ -1630,8 +1668,8 @@ int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_confi
         dalloc(dsum, 4);
         CK(cudaMallocHost(&hsum, 4 * sizeof(double)));
         SeqScratch sc;
-        ExApplyBuf eb;
-        if (h->precond == HFPG_PRECOND_FACTOR) eb.alloc(h->L);
+        ExApplyWs ews{};
+        if (h->precond == HFPG_PRECOND_FACTOR) ews = exact_ws(h);
         auto cleanup = [&] {
             dfree(prod);
             dfree(dsum);
@@ -1658,7 +1696,7 @@ int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_confi
             };
             auto precond = [&] {  // z = M r
                 if (h->precond == HFPG_PRECOND_FACTOR) {
-                    apply_exact_f32(st, h->L, h->F, h->a_diag, factor_shift(h), dr, dz, eb.w);
+                    apply_exact_f32(st, h->L, h->F, h->a_diag, factor_shift(h), dr, dz, ews);
                 } else if (h->precond == HFPG_PRECOND_IC0) {
                     k_ic0_pending<<<g, 256, 0, st>>>(ic0_dev(h), dz, n);
                     launch_ic0_sweeps(h, h->sys, kApply, dr, dz);
@@ -1669,7 +1707,11 @@ int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_confi
                 }
                 CK(cudaGetLastError());
             };
-            cudaEvent_t e0, e1;
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            auto ev_guard = on_scope_exit([&] {
+                if (e0) cudaEventDestroy(e0);
+                if (e1) cudaEventDestroy(e1);
+            });
             CK(cudaEventCreate(&e0));
             CK(cudaEventCreate(&e1));
             CK(cudaEventRecord(e0, st));
@@ -1697,13 +1739,19 @@ int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_confi
                     constexpr uint64_t kBatch = 8;
                     ExState* S = nullptr;
                     double* dhist = nullptr;
+                    cudaGraph_t gr = nullptr;
+                    cudaGraphExec_t ge = nullptr;
+                    auto loop_guard = on_scope_exit([&] {  // every exit path, throws included
+                        if (ge) cudaGraphExecDestroy(ge);
+                        if (gr) cudaGraphDestroy(gr);
+                        dfree(S);
+                        dfree(dhist);
+                    });
                     dalloc(S, 1);
                     dalloc(dhist, cfg.max_iters);
                     ExState hs{rz, 0.0, 0.0, r0, breakdown_tol, cfg.rtol, 1ULL, 0ULL, 0, 0};
                     CK(cudaMemcpyAsync(S, &hs, sizeof(ExState), cudaMemcpyHostToDevice, st));
                     CK(cudaStreamSynchronize(st));
-                    cudaGraph_t gr = nullptr;
-                    cudaGraphExec_t ge = nullptr;
                     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
                     try {
                         launch_spmv<kApply>(h, h->sys, dp, dap);
@@ -1719,10 +1767,7 @@ int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_confi
                         k_exg_p<<<g, 256, 0, st>>>(S, dp, dz, n);
                         CK(cudaGetLastError());
                     } catch (...) {
-                        cudaStreamEndCapture(st, &gr);
-                        if (gr) cudaGraphDestroy(gr);
-                        dfree(S);
-                        dfree(dhist);
+                        cudaStreamEndCapture(st, &gr);  // gr (if any) freed by loop_guard
                         throw;
                     }
                     CK(cudaStreamEndCapture(st, &gr));
@@ -1751,10 +1796,6 @@ int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_confi
                     hist.resize(hlen);
                     if (hlen) CK(cudaMemcpyAsync(hist.data(), dhist, hlen * 8, cudaMemcpyDeviceToHost, st));
                     CK(cudaStreamSynchronize(st));
-                    cudaGraphExecDestroy(ge);
-                    cudaGraphDestroy(gr);
-                    dfree(S);
-                    dfree(dhist);
                 } else
                 for (uint64_t k = 1; k <= cfg.max_iters; ++k) {
                     launch_spmv<kApply>(h, h->sys, dp, dap);
@@ -1809,8 +1850,6 @@ int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_confi
             CK(cudaStreamSynchronize(st));
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, e0, e1));
-            cudaEventDestroy(e0);
-            cudaEventDestroy(e1);
             if (report) {
                 report->n = n;
                 report->iterations = iterations;

@@ -1567,6 +1567,13 @@ __global__ void __launch_bounds__(256) k_simple(DevSys s, int mode, int jacobi) 
     }
 }
 
+// pcg.cpp:28-42 standalone: z = r / a_ii (jacobi) or z = r (identity), IEEE division.
+__global__ void k_diag_apply(uint64_t n, const double* __restrict__ r, const double* __restrict__ a_diag,
+                             double* __restrict__ z, int jacobi) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        z[i] = jacobi ? r[i] / a_diag[i] : r[i];
+}
+
 // Solve initialisation: x = 0, r = b, p_prev = 0 and the state words (pcg.cpp:65-80).
 __global__ void k_init(DevSys s, const double* b) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < s.n;

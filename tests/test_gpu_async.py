@@ -33,3 +33,22 @@ def test_concurrent_solves_match_sequential(H):
         assert (x.cpu().numpy() == xw).all()
     with pytest.raises(ValueError):
         devs[0].wait()  # nothing in flight
+
+
+def test_second_solve_while_one_is_in_flight_is_refused(H):
+    # the handle's pinned report buffer also stages the config: a second enqueue before the
+    # wait would upload the first solve's scalars as its config
+    from paper_2605_13343_b200 import _native as N
+    fr = H.make_frame(4096, 2024, 0)
+    d = H.Device(0)
+    d.load_csr(fr.A)
+    d.set_precond(1)
+    x = np.empty(fr.n)
+    d.solve_async(fr.b.ctypes.data, x.ctypes.data, H.SolveConfig(), N.HOST)
+    with pytest.raises(ValueError):
+        d.solve_async(fr.b.ctypes.data, x.ctypes.data, H.SolveConfig(rtol=1e-3), N.HOST)
+    with pytest.raises(ValueError):
+        d.solve_ptr(fr.b.ctypes.data, x.ctypes.data, H.SolveConfig(), None, N.HOST)
+    rep = d.wait()
+    ref = H.pcg_solve(fr.A, fr.b, H.jacobi_applier(fr.A))
+    assert int(rep.iterations) == ref.iterations

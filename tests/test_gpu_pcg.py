@@ -147,3 +147,32 @@ def test_iteration_parity_large(H, name):
         assert lo <= rep.iterations <= hi, (rep.iterations, ref_its, band)
     else:
         assert abs(rep.iterations - ref_its) <= 2, (rep.iterations, want)
+
+
+def test_solve_uses_the_matrix_it_is_handed(H):
+    # pcg.cpp:53 always multiplies by the A passed in: a matrix edited in place after the applier
+    # was bound, or a different matrix, must be reloaded (no id() caching)
+    fr = H.make_frame(2048, 11, 0)
+    ap = H.jacobi_applier(fr.A)
+    r1 = H.pcg_solve(fr.A, fr.b, ap)
+    fr.A.values *= 2.5  # in place: same object, same id()
+    r2 = H.pcg_solve(fr.A, fr.b, ap)
+    r2_fresh = H.pcg_solve(fr.A, fr.b, H.jacobi_applier(fr.A))
+    assert r2.iterations == r2_fresh.iterations
+    assert np.array_equal(r2.residual_history, r2_fresh.residual_history)
+    xs, xs2 = [], []
+    H.pcg_solve(fr.A, fr.b, ap, H.SolveConfig(), xs)
+    H.pcg_solve(fr.A, fr.b, H.jacobi_applier(fr.A), H.SolveConfig(), xs2)
+    assert np.array_equal(xs[0], xs2[0])
+    assert r1.iterations >= 1
+
+
+def test_jacobi_applier_call_on_device_bit_exact(H):
+    # pcg.cpp:34-42 z_i = r_i / a_ii: the plug-compatible call runs on the device (IEEE division)
+    fr = H.make_frame(4096, 5, 2)
+    ap = H.jacobi_applier(fr.A)
+    r = np.random.default_rng(4).standard_normal(fr.n)
+    z = ap(r)
+    assert np.array_equal(z.view(np.uint64), (r / fr.A.diagonal()).view(np.uint64))
+    with pytest.raises(ValueError):
+        ap(r[:-1])

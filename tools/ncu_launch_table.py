@@ -24,7 +24,7 @@ def load(path):
             continue
         v = float(r[vi].replace(",", ""))
         unit = r[ui]
-        us = v / 1e3 if unit == "nsecond" else v * 1e3 if unit == "msecond" else v
+        us = v / 1e3 if unit in ("nsecond", "ns") else v * 1e3 if unit in ("msecond", "ms") else v
         out.append((r[ki], us))
     return out
 
