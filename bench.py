@@ -82,6 +82,30 @@ def make_inputs(cfg: dict, frame_index: int):
     return fr, f
 
 
+def make_ref_inputs(cfg: dict, frame_index: int):
+    """The reference arm's inputs, built without the product library: the reference's own
+    make_frame (frame.cpp:161-181) / the oracle-side 3D frame (oracle/frame3d_ref.cpp, reference
+    RngStream + sample_rhs) and the reference's init_factors (factor_tensor.cpp:30-39), all from
+    oracle/_ref. Returns (csr tuple, b, packed factors, n)."""
+    from oracle.oracle import Ref
+    r = Ref()
+    if "dims" in cfg:
+        fr = r.make_frame_3d(*cfg["dims"], 2024, frame_index)
+        fid = frame_index
+    else:
+        n = cfg["n"]
+        fid = ((n << 24) | (1 << 20) | frame_index) if cfg.get("test_frame") or cfg.get("kind") == "batch" \
+            else frame_index  # frame.hpp:88-90 test_frame_id
+        fr = r.make_frame(n, 2024, fid)
+    packed = r.init_factors(fr["n"], 128, 32, cfg["sigma"], 2024, fid)
+    return (fr["row_offsets"], fr["col_indices"], fr["values"]), fr["b"], packed, fr["n"]
+
+
+def config_of(cfg: dict, n: int, nnz: int) -> dict:
+    """The `config` object both arms print (same keys, same values)."""
+    return {"workload": cfg["desc"], "n": int(n), "nnz": int(nnz)}
+
+
 def peaks():
     try:
         p = json.load(open(PEAKS))
@@ -181,27 +205,34 @@ def barrier(world):
 # ------------------------------------------------------------------------- reference arm
 
 
-def cpu_sample(cfg, fr, f, budget_s: float):
+def cpu_sample_raw(csr, b, packed, budget_s: float):
     """Time the reference's own pcg_solve loop (oracle/_ref) for a bounded number of
     iterations; returns (ms per iteration, iterations run)."""
     from oracle.oracle import Ref
     r = Ref()
-    csr = (fr.A.row_offsets, fr.A.col_indices, fr.A.values)
-    ms = r.pcg_time_iters(csr, fr.b, 128, 32, f.data, 3) / 3.0
+    ms = r.pcg_time_iters(csr, b, 128, 32, packed, 3) / 3.0
     iters = max(3, int(budget_s * 1000.0 / max(ms, 1e-3)))
-    total = r.pcg_time_iters(csr, fr.b, 128, 32, f.data, iters)
+    total = r.pcg_time_iters(csr, b, 128, 32, packed, iters)
     return total / iters, iters
+
+
+def cpu_sample(cfg, fr, f, budget_s: float):
+    return cpu_sample_raw((fr.A.row_offsets, fr.A.col_indices, fr.A.values), fr.b, f.data, budget_s)
 
 
 def run_reference(args, cfg):
     world, rank, local = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
     if rank != 0:
         return
-    fr, f = make_inputs(cfg, 0)
+    if cfg.get("kind") in ("part", "infer"):
+        print(json.dumps({"impl": "reference", "unavailable": f"--config {args.config}: the reference "
+                          "has no row-partitioned solve / its forward is timed in the parity tests"}), flush=True)
+        return
+    csr, b, packed, n = make_ref_inputs(cfg, 0)
     its = ref_iterations(cfg["ref_key"])
     vals = []
     for step in range(args.warmup + args.steps):
-        ms_it, n_it = cpu_sample(cfg, fr, f, args.ref_budget)
+        ms_it, n_it = cpu_sample_raw(csr, b, packed, args.ref_budget)
         if step >= args.warmup:
             vals.append(ms_it)
     ms_it = statistics.median(vals)
@@ -213,7 +244,9 @@ def run_reference(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_it * n_it,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32/f64", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "n": fr.n, "nnz": int(fr.A.nnz())},
+            "config": config_of(cfg, n, len(csr[2])),
+            "config_details": {"inputs": "built by oracle/_ref (reference make_frame / oracle-side 3D "
+                                         "frame, reference init_factors); the product library is not loaded"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
                              "sample": sample, "ms_per_iteration": ms_it, "nproc": os.cpu_count()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -296,7 +329,7 @@ def run_infer_config(args, cfg):
     line = {"metric": METRIC, "value": step_ms, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 (tf32 MMA) / f64", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "n": cfg["n"]},
+            "config": config_of(cfg, cfg["n"], 0),
             "roofline": res.pop("roofline"), "inference": res, "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -357,7 +390,9 @@ def run_ours(args, cfg):
     barrier(world)
     t_ms = e0.elapsed_time(e1)
     t_max = max_over_ranks(t_ms, world, local)
-    value = t_max / (args.steps * world)
+    # every rank solves its own independent system (weak scaling): the metric is the per-solve
+    # latency, max over ranks; the aggregate rate across GPUs is reported beside it
+    value = t_max / args.steps
     status = rep.status
 
     # end to end through the public C ABI with pinned host buffers (H2D b, D2H x + report)
@@ -403,7 +438,8 @@ def run_ours(args, cfg):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "n": n, "nnz": nnz, "leaf": 128, "coarse": 32,
+        "config": config_of(cfg, n, nnz),
+        "config_details": {"leaf": 128, "coarse": 32,
                    "iterations": iters[-1], "status": status, "rtol": 1e-8,
                    "ref_iterations": ref_iterations(cfg["ref_key"]),
                    "l2": "inputs larger than L2 (4P = %.0f MB of factors streamed per iteration)"
@@ -421,7 +457,8 @@ def run_ours(args, cfg):
                      "prolong_GBps": prol_bytes / (ms_prol * 1e-3) / 1e9,
                      "iteration_ms": iter_ms,
                      "solve_ms_per_iteration": (t_max / args.steps) / max(iters[-1], 1)},
-        "e2e": {"value": e2e_max / (e2e_steps * world), "unit": UNIT,
+        "aggregate_solves_per_s": world * args.steps / (t_max * 1e-3),
+        "e2e": {"value": e2e_max / e2e_steps, "unit": UNIT,
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 96},
         "gpu_launches": args.steps * launches_per_solve(dev, iters[-1]),
         "clocks": clk.summary(),
@@ -479,6 +516,7 @@ def run_batch(args, cfg):
     from paper_2605_13343_b200 import _native as N
     mine = frames_of(rank, world, cfg["frames"])
     devs, bs, xs, its = [], [], [], []
+    fr0 = f0 = None
     for i in mine:
         fr, f = make_inputs(cfg, i)
         d = H.Device(local)
@@ -554,7 +592,8 @@ def run_batch(args, cfg):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "n": n, "frames": cfg["frames"], "frames_per_gpu": len(mine),
+        "config": config_of(cfg, n, int(fr0.A.nnz()) if fr0 is not None else 0),
+        "config_details": {"frames": cfg["frames"], "frames_per_gpu": len(mine),
                    "iterations_mean": float(np.mean(all_its)), "iterations_min": int(min(all_its)),
                    "iterations_max": int(max(all_its)), "ref_iterations_frame0": ref_iterations(cfg["ref_key"]),
                    "solver": "persistent" if devs[0].solver_in_use() == N.SOLVER_PERSISTENT else "graph",
@@ -668,7 +707,8 @@ def run_part(args, cfg):
             "metric": METRIC, "value": t_ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "n": n, "nnz": nnz, "rows_per_gpu": nl, "iterations": its,
+            "config": config_of(cfg, n, nnz),
+            "config_details": {"rows_per_gpu": nl, "iterations": its,
                        "status": int(rep.status), "rtol": 1e-8, "setup_s": setup_s,
                        "parallelism": f"row partition over {world} GPU(s)" + (
                            ", mailboxes + z halo over CUDA IPC (NVLink P2P)" if world > 1 else ""),

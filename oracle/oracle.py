@@ -216,6 +216,28 @@ class Ref(_Base):
             raise ValueError(self.lib.ref_last_error().decode())
         return self._frame_dict(h)
 
+    def make_frame_3d(self, nx: int, ny: int, nz: int, seed: int, frame_index: int) -> dict:
+        """The 3D benchmark frame built from the reference's RngStream / sample_rhs / stencil
+        rules (oracle/frame3d_ref.cpp) -> dict of numpy arrays."""
+        L = self.lib
+        L.ref_frame3d_create.restype = _p
+        L.ref_frame3d_create.argtypes = [_u64] * 5
+        L.ref_frame3d_last_error.restype = C.c_char_p
+        h = L.ref_frame3d_create(nx, ny, nz, seed, frame_index)
+        if not h:
+            raise ValueError(L.ref_frame3d_last_error().decode())
+        nn, nnz, rh = _u64(), _u64(), C.c_double()
+        L.ref_frame3d_sizes(_p(h), C.byref(nn), C.byref(nnz), C.byref(rh))
+        fr = dict(n=nn.value, width=nx, height=ny, depth=nz, rho_heavy=rh.value,
+                  cell_order=np.empty(nn.value, np.uint32), rho=np.empty(nn.value),
+                  row_offsets=np.empty(nn.value + 1, np.uint64),
+                  col_indices=np.empty(nnz.value, np.uint32), values=np.empty(nnz.value),
+                  b=np.empty(nn.value))
+        L.ref_frame3d_fill(_p(h), _ptr(fr["cell_order"]), _ptr(fr["rho"]), _ptr(fr["row_offsets"]),
+                           _ptr(fr["col_indices"]), _ptr(fr["values"]), _ptr(fr["b"]))
+        L.ref_frame3d_free(_p(h))
+        return fr
+
     def write_mppf(self, n: int, seed: int, frame_index: int, path: str) -> None:
         """mppf.cpp:48 write_mppf(make_frame(n, seed, frame_index), path)."""
         f = self._f("write_mppf")

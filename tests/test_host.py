@@ -121,3 +121,17 @@ def test_checkpoint_roundtrip_and_interop(H, ref):
         open(path, "wb").write(b"NOTHFTC0" + bytes(16))
         with pytest.raises(RuntimeError):
             H.read_checkpoint(path)
+
+
+@pytest.mark.parametrize("dims", [(16, 12, 8), (5, 7, 3), (32, 16, 24)])
+def test_oracle_3d_frame_matches_product_generator(H, ref, dims):
+    """bench.py's reference arm builds the 3D benchmark frame on the oracle side
+    (oracle/frame3d_ref.cpp, the reference's RngStream / sample_rhs / stencil rules) without the
+    product library; it must be the product's make_frame_3d bit for bit."""
+    a = ref.make_frame_3d(*dims, 2024, 1)
+    b = H.make_frame_3d(*dims, 2024, 1)
+    assert np.array_equal(a["cell_order"], b.cell_order)
+    for k, v in (("rho", b.rho), ("values", b.A.values), ("b", b.b)):
+        assert np.array_equal(a[k].view(np.uint64), np.asarray(v).view(np.uint64)), k
+    assert np.array_equal(a["row_offsets"], b.A.row_offsets)
+    assert np.array_equal(a["col_indices"], b.A.col_indices)
