@@ -284,7 +284,7 @@ def run_inference(local: int, steps: int, warmup: int, n: int = 65536, solve: bo
     gen_ms, inf_ms = [], []
     for i in range(warmup + steps):
         gf = dev.frame_gpu(n, 2024, 0)
-        tr = H.ToynetTrace()
+        tr = H.ToynetTrace(timing_only=True)
         H.toynet_forward_gpu_frame(gf, 32, trace=tr, load=True)
         if i >= warmup:
             gen_ms.append(gf.generate_ms)

@@ -79,7 +79,9 @@ typedef struct {
     double max_attention_row_sum_error;
     double highway_max_deviation;
     uint64_t leaf_attention_dispatches, tile_attention_dispatches;
-    double ms;
+    double ms;           /* out: device time of the forward (CUDA events) */
+    int32_t timing_only; /* in: 1 = fill only ms (no row-sum / conservation audits, which add
+                            work to the forward); 0 = the full trace, as toy_net.hpp:64-74 */
 } hfpg_toynet_trace;
 
 /* frame.hpp:26-40 — the fields toynet::encode / forward consume (host pointers) */

@@ -50,7 +50,7 @@ class ToynetConfigC(C.Structure):
 class ToynetTraceC(C.Structure):
     _fields_ = [("max_attention_row_sum_error", dbl), ("highway_max_deviation", dbl),
                 ("leaf_attention_dispatches", u64), ("tile_attention_dispatches", u64),
-                ("ms", dbl)]
+                ("ms", dbl), ("timing_only", i32)]
 
 
 class FrameViewC(C.Structure):

@@ -842,6 +842,7 @@ class ToynetTrace:
     max_attention_row_sum_error: float = 0.0
     highway_max_deviation: float = 0.0
     ms: float = 0.0
+    timing_only: bool = False  # input: time the forward without the audits
 
     def attention_kernel_families(self) -> int:
         return int(self.leaf_attention_dispatches > 0) + int(self.tile_attention_dispatches > 0)
@@ -870,6 +871,7 @@ def toynet_forward(frame: Frame, partition: HPartition, coarse_size: int,
     out = np.empty(lay.total, np.float32)
     c = N.ToynetConfigC(cfg.d, cfg.layers, cfg.heads, cfg.gcn_layers, cfg.d_global, cfg.edge_hidden)
     tr = N.ToynetTraceC()
+    tr.timing_only = int(bool(trace is not None and trace.timing_only))
     view = _frame_view(frame)
     check(lib.hfpg_toynet_forward(dev.h, C.byref(view), partition.leaf_size, coarse_size, C.byref(c),
                                   weight_seed, out.ctypes.data, int(load),
@@ -897,6 +899,7 @@ def toynet_forward_gpu_frame(frame: "GpuFrame", coarse_size: int, cfg: ToynetCon
     out = np.empty(lay.total, np.float32) if copy_out else None
     c = N.ToynetConfigC(cfg.d, cfg.layers, cfg.heads, cfg.gcn_layers, cfg.d_global, cfg.edge_hidden)
     tr = N.ToynetTraceC()
+    tr.timing_only = int(bool(trace is not None and trace.timing_only))
     check(lib.hfpg_toynet_forward_gpu_frame(frame.device.h, leaf_size, coarse_size, C.byref(c), weight_seed,
                                             out.ctypes.data if copy_out else None, int(load),
                                             C.byref(tr) if trace is not None else None))

@@ -1,71 +1,117 @@
-// Leaf-window attention on the 5th-generation tensor cores (sm_100a): toy_net.cpp:78-125 for
-// windows of T = 128 tokens, head dim 16, per (block, head):
+// Windowed attention on the 5th-generation tensor cores (sm_100a): toy_net.cpp:78-125 for the
+// leaf windows (T = 128 tokens) and the strip-pooled tile windows (T = 32 tokens, four windows
+// packed into one 128-row MMA), head dim 16, 8 heads. One CTA per group of 128 token rows:
 //
-//   S = Q K^T            tcgen05.mma kind::tf32, M = 128 queries, N = 128 keys, K = 16 (2 x K=8)
-//   P = softmax(S/4 + B) fp32 in registers: each of the 128 threads owns one TMEM lane = one
-//                        query row (tcgen05.ld 32x32b), the key-major edge bias is read
-//                        coalesced across the rows; P is written back to shared memory in the
-//                        UMMA SWIZZLE_128B K-major layout
-//   O = P V              tcgen05.mma kind::tf32, M = 128, N = 16, K = 128 (4 blocks x 4 x K=8)
-//   out = O / rowsum
+//   S = Q K^T            tcgen05.mma kind::tf32, M = 128 rows, N = 128 keys, K = 16 (2 x K=8).
+//                        For T = 32 the four 32 x 32 diagonal blocks are the four windows' logits
+//                        (the off-diagonal blocks are computed and ignored).
+//   P = softmax(S/4 + B) thread = TMEM lane = query row, 32 keys per thread: T = 128 splits the
+//                        row's keys over four warp quads (max / sum combined through shared
+//                        memory), T = 32 gives each row's window to one thread. The logits stay
+//                        in registers between the max and the exponentials. The fp16 edge bias
+//                        (query-major as the reference indexes it, pre-scaled by log2 e) is
+//                        prefetched one head ahead. P goes to shared memory in the UMMA
+//                        SWIZZLE_128B K-major layout; for T = 32 only the row's own window block
+//                        is written — the off-diagonal blocks stay zero (block-diagonal mask).
+//   O_h = P V_h          tcgen05.mma kind::tf32, M = 128, N = 16, K = 128, into TMEM columns
+//                        128 + 16 h; it runs while head h+1 is staged and its logits computed.
+//   out = O_h / rowsum   all eight heads at the end, contiguous 16-float runs per thread.
 //
-// Operands are staged by the 128 threads from the fp32 qkv rows: Q and K zero-padded to 32
-// columns (one 128-byte swizzle row; only the first two K=8 steps are issued), V transposed into
-// a 16-row B operand. One CTA per window loops over the heads; TMEM holds S (128 columns) and O
-// (16 columns). The f32->tf32 operand rounding matches the inference GEMMs (kind::tf32).
+// Operands are staged by the threads from the fp32 qkv rows (Q, K zero-padded to 32 columns —
+// one 128-byte swizzle row, only the first two K=8 steps are issued), V transposed into a 16-row
+// B operand. TMEM: 256 columns (S 128 + O 8 x 16). T = 128: 512 threads, one CTA per SM;
+// T = 32: 128 threads, two CTAs per SM.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <math_constants.h>
 
 #include "gemm_tcgen05.cuh"
 
 namespace hfpg {
 
-constexpr int kAttT = 128, kAttHD = 16, kAttThreads = 256;
+constexpr int kAttRows = 128, kAttHD = 16, kAttHeads = 8;
+constexpr float kAttLog2e = 1.4426950408889634f;
 
 struct AttSmem {
-    alignas(1024) float Q[kAttT * 32];       // 128 x 32 SW128 (cols 16..31 zero)
-    alignas(1024) float K[kAttT * 32];
-    alignas(1024) float P[4][kAttT * 32];    // 4 K-blocks of 128 x 32 SW128
-    alignas(1024) float VT[4][16 * 32];      // V^T: 4 K-blocks of 16 x 32 SW128
-    float part[2][kAttT];                    // per-half row max, then row sum
-    uint64_t bar;
+    alignas(1024) float Q[kAttRows * 32];    // 128 x 32 SW128 (cols 16..31 zero)
+    alignas(1024) float K[kAttRows * 32];
+    alignas(1024) float P[4][kAttRows * 32]; // 4 K-blocks of 128 x 32 SW128
+    alignas(1024) float VT[4][16 * 32];      // V^T: 4 K-blocks of 16 x 32
+    float part[4][kAttRows];                 // T = 128: per-quad row max, then row sum
+    uint64_t bar_s, bar_o;
     uint32_t tmem;
 };
+constexpr size_t att_smem_bytes() { return sizeof(AttSmem) + 1024; }
+template <int T>
+__host__ __device__ constexpr int att_quads() {
+    return T == 128 ? 4 : 1;
+}
+template <int T>
+__host__ __device__ constexpr int att_threads() {
+    return att_quads<T>() * 128;
+}
 
 // Byte offset of element (row, col < 32) in a SW128 K-major tile of 32-float rows.
 __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t col) {
     const uint32_t chunk = (col >> 2) ^ (row & 7);
     return (row >> 3) * 1024 + (row & 7) * 128 + chunk * 16 + (col & 3) * 4;
 }
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
-// Two warp quads per window: quad q (warps 4q..4q+3) owns keys [64q, 64q+64) of every query row
-// (TMEM lane = row, warp w reads lanes 32 (w mod 4)..); row max and sum are combined through
-// shared memory. Two CTAs per SM.
-__global__ void __launch_bounds__(kAttThreads, 2)
-    k_tn_attention_tc(uint32_t d, uint32_t heads, const float* qkv, const float* bias,
-                      float* head_out, unsigned int* rowsum_err_bits) {
+// qkv: rows of [q | k | v] (3 d = 384 wide); bias: fp16 [window][head][query][key] in log2
+// units (b log2 e); head_out: rows x d. nwin windows of T tokens (rows = nwin * T).
+template <int T>
+__global__ void __launch_bounds__(att_threads<T>(), T == 128 ? 1 : 2)
+    k_tn_attn_tc(uint64_t nwin, const float* __restrict__ qkv, const __half* __restrict__ bias,
+                 float* __restrict__ head_out, unsigned int* rowsum_err_bits) {
+    static_assert(T == 128 || T == 32, "windows of 128 (leaf) or 32 (tile) tokens");
+    constexpr int NQ = att_quads<T>();
+    constexpr int d = kAttHeads * kAttHD;  // 128
     extern __shared__ __align__(1024) unsigned char araw[];
     AttSmem& sm = *reinterpret_cast<AttSmem*>((reinterpret_cast<uintptr_t>(araw) + 1023) & ~uintptr_t(1023));
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
-    const uint32_t row = tid & (kAttT - 1), quad = tid >> 7, key0 = 64 * quad;
-    const uint64_t blk = blockIdx.x;
+    const uint32_t row = tid & (kAttRows - 1), quad = tid >> 7;
+    const uint64_t grow = uint64_t(blockIdx.x) * kAttRows + row;  // global token row
+    const uint64_t win = grow / T;                                  // window of this row
+    const uint32_t wrow = uint32_t(grow % T);                        // query index inside it
+    const bool valid = win < nwin;
+    // this thread's 32 keys: window-local [key0, key0 + 32) = S columns [scol0, scol0 + 32) =
+    // P K-block kb (T = 128: quad q owns keys 32q..; T = 32: the row's own window)
+    const uint32_t key0 = T == 128 ? 32 * quad : 0;
+    const uint32_t scol0 = T == 128 ? key0 : (row & ~31u);
+    const uint32_t kb = scol0 >> 5;
     unsigned char* Qb = reinterpret_cast<unsigned char*>(sm.Q);
     unsigned char* Kb = reinterpret_cast<unsigned char*>(sm.K);
-    constexpr float kLog2e = 1.4426950408889634f;
+    // stagers: T = 128 quad 0 -> Q, 1 -> K, 2 -> V^T; T = 32 the single quad stages all three
+    const bool stage_q = quad == 0, stage_k = T == 128 ? quad == 1 : true, stage_v = T == 128 ? quad == 2 : true;
+
     if (tid == 0) {
-        mbar_init(&sm.bar, 1);
+        mbar_init(&sm.bar_s, 1);
+        mbar_init(&sm.bar_o, 1);
         fence_mbar_init();
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&sm.tmem)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (quad == 0) {  // zero the padding columns 16..31 of Q and K once (never rewritten)
+    if (quad == 0) {  // Q, K padding columns 16..31 and (T = 32) every P block: zero once
 #pragma unroll
         for (int c = 16; c < 32; c += 4) {
             *reinterpret_cast<float4*>(Qb + sw128_off(row, c)) = make_float4(0.f, 0.f, 0.f, 0.f);
             *reinterpret_cast<float4*>(Kb + sw128_off(row, c)) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (T == 32) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+#pragma unroll
+                for (int c = 0; c < 32; c += 4)
+                    *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(sm.P[b]) + sw128_off(row, c)) =
+                        make_float4(0.f, 0.f, 0.f, 0.f);
         }
     }
     tc_fence_before();
@@ -73,40 +119,47 @@ __global__ void __launch_bounds__(kAttThreads, 2)
     tc_fence_after();
     const uint32_t tmem = sm.tmem, tS = tmem, tO = tmem + 128;
     constexpr uint32_t idS = idesc_tf32<128>(), idO = idesc_tf32<16>();
-    uint32_t phase = 0;
-    const float* rowp = qkv + (blk * kAttT + row) * 3 * d;
-    float4 n0[4], n1[4];  // next head's operands of row `row`: quad 0 q, k; quad 1 v
+    const uint32_t lane_off = uint32_t((warp & 3) * 32) << 16;
+
+    const float* rowp = qkv + grow * 3 * d;
+    // next head's operands of this thread (T = 128: one of q / k / v in n0; T = 32: all three)
+    float4 n0[4], n1[4], n2[4];
     auto fetch = [&](uint32_t h) {
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            if (quad == 0) {
-                n0[c] = reinterpret_cast<const float4*>(rowp + h * kAttHD)[c];
-                n1[c] = reinterpret_cast<const float4*>(rowp + d + h * kAttHD)[c];
+            if constexpr (T == 128) {
+                if (quad < 3) n0[c] = valid ? reinterpret_cast<const float4*>(rowp + quad * d + h * kAttHD)[c] : z;
             } else {
-                n0[c] = reinterpret_cast<const float4*>(rowp + 2 * d + h * kAttHD)[c];
+                n0[c] = valid ? reinterpret_cast<const float4*>(rowp + h * kAttHD)[c] : z;
+                n1[c] = valid ? reinterpret_cast<const float4*>(rowp + d + h * kAttHD)[c] : z;
+                n2[c] = valid ? reinterpret_cast<const float4*>(rowp + 2 * d + h * kAttHD)[c] : z;
             }
         }
     };
+    uint4 bcur[4], bnext[4];  // 32 fp16 bias values of this thread's keys
+    auto fetch_bias = [&](uint32_t h, uint4 (&dst)[4]) {
+        const __half* b = bias + ((win * kAttHeads + h) * T + wrow) * T + key0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            dst[i] = valid ? __ldg(reinterpret_cast<const uint4*>(b) + i) : make_uint4(0u, 0u, 0u, 0u);
+    };
     fetch(0);
-    const uint32_t trow = tS + (uint32_t((warp & 3) * 32) << 16);
-    for (uint32_t h = 0; h < heads; ++h) {
-        // ---- stage Q, K (quad 0, row `row`) and V^T (quad 1, key `row`)
-        if (quad == 0) {
+    fetch_bias(0, bcur);
+    float inv[kAttHeads];
+    float rs_err = 0.f;
+
+#pragma unroll 1
+    for (uint32_t h = 0; h < kAttHeads; ++h) {
+        // ---- stage Q_h, K_h
+        if (stage_q) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                *reinterpret_cast<float4*>(Qb + sw128_off(row, 4 * c)) = n0[c];
-                *reinterpret_cast<float4*>(Kb + sw128_off(row, 4 * c)) = n1[c];
-            }
-        } else {
-            unsigned char* vb = reinterpret_cast<unsigned char*>(sm.VT[row >> 5]);
-            const uint32_t key = row & 31;
+            for (int c = 0; c < 4; ++c) *reinterpret_cast<float4*>(Qb + sw128_off(row, 4 * c)) = n0[c];
+        }
+        if (stage_k) {
+            const float4* kk = T == 128 ? n0 : n1;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                *reinterpret_cast<float*>(vb + sw128_off(4 * c + 0, key)) = n0[c].x;
-                *reinterpret_cast<float*>(vb + sw128_off(4 * c + 1, key)) = n0[c].y;
-                *reinterpret_cast<float*>(vb + sw128_off(4 * c + 2, key)) = n0[c].z;
-                *reinterpret_cast<float*>(vb + sw128_off(4 * c + 3, key)) = n0[c].w;
-            }
+            for (int c = 0; c < 4; ++c) *reinterpret_cast<float4*>(Kb + sw128_off(row, 4 * c)) = kk[c];
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
@@ -116,117 +169,157 @@ __global__ void __launch_bounds__(kAttThreads, 2)
             const uint64_t da = umma_desc_sw128(sm.Q), db = umma_desc_sw128(sm.K);
             mma_tf32(tS, da, db, idS, 0u);
             mma_tf32(tS, da + 2, db + 2, idS, 1u);
-            mma_commit(&sm.bar);
+            mma_commit(&sm.bar_s);
         }
-        if (h + 1 < heads) fetch(h + 1);
-        // the bias column of this query row (key-major: b[j * T]), keys of this quad; logits in
-        // base-2 units: l = (s / 4 + b) log2(e)
-        const float* b = bias + (blk * heads + h) * kAttT * kAttT + row + key0 * kAttT;
-        float bn[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) bn[j] = __ldg(b + j * kAttT);
-        mbar_wait(&sm.bar, phase);
-        phase ^= 1;
+        if (h + 1 < kAttHeads) fetch_bias(h + 1, bnext);
+        mbar_wait(&sm.bar_s, h & 1);
         tc_fence_after();
-        // pass 1: max over this quad's 64 keys (bias chunk c+1 in flight while c computes)
-        float mx = -CUDART_INF_F;
-#pragma unroll 1
-        for (int c = 0; c < 64; c += 16) {
-            float s[16], bc[16];
+        // ---- logits l = s log2(e) / 4 + b' (b' = b log2 e) of this thread's 32 keys, row max
+        float lg[32];
+        {
+            uint32_t u0[16], u1[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(u0[0]), "=r"(u0[1]), "=r"(u0[2]), "=r"(u0[3]), "=r"(u0[4]), "=r"(u0[5]), "=r"(u0[6]),
+                  "=r"(u0[7]), "=r"(u0[8]), "=r"(u0[9]), "=r"(u0[10]), "=r"(u0[11]), "=r"(u0[12]), "=r"(u0[13]),
+                  "=r"(u0[14]), "=r"(u0[15])
+                : "r"(tS + lane_off + scol0));
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(u1[0]), "=r"(u1[1]), "=r"(u1[2]), "=r"(u1[3]), "=r"(u1[4]), "=r"(u1[5]), "=r"(u1[6]),
+                  "=r"(u1[7]), "=r"(u1[8]), "=r"(u1[9]), "=r"(u1[10]), "=r"(u1[11]), "=r"(u1[12]), "=r"(u1[13]),
+                  "=r"(u1[14]), "=r"(u1[15])
+                : "r"(tS + lane_off + scol0 + 16));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int j = 0; j < 16; ++j) bc[j] = bn[j];
-            if (c + 16 < 64) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) bn[j] = __ldg(b + (c + 16 + j) * kAttT);
-            } else {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) bn[j] = __ldg(b + j * kAttT);  // pass 2 restarts
+            for (int j = 0; j < 16; ++j) {
+                lg[j] = __uint_as_float(u0[j]);
+                lg[16 + j] = __uint_as_float(u1[j]);
             }
-            tmem_ld16(trow + key0 + c, s);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) mx = fmaxf(mx, fmaf(s[j], 0.25f, bc[j]));
         }
-        sm.part[quad][row] = mx;
-        __syncthreads();
-        mx = fmaxf(sm.part[0][row], sm.part[1][row]);
-        const float mx2 = mx * kLog2e;
-        // pass 2: p = 2^(l - max), the quad's partial sum, P into the swizzled A operand
+        float mx = -CUDART_INF_F;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const __half2* b2 = reinterpret_cast<const __half2*>(&bcur[i]);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const float2 bf = __half22float2(b2[t]);
+                const int j = 8 * i + 2 * t;
+                lg[j] = fmaf(lg[j], 0.25f * kAttLog2e, bf.x);
+                lg[j + 1] = fmaf(lg[j + 1], 0.25f * kAttLog2e, bf.y);
+                mx = fmaxf(mx, fmaxf(lg[j], lg[j + 1]));
+            }
+        }
+        if constexpr (NQ > 1) {
+            sm.part[quad][row] = mx;
+            named_bar_sync(1, NQ * 128);
+            mx = fmaxf(fmaxf(sm.part[0][row], sm.part[1][row]), fmaxf(sm.part[2][row], sm.part[3][row]));
+        }
+        // ---- after head h-1's PV MMA: V_h^T into its buffer, P = 2^(l - max) into the operand
+        if (h > 0) mbar_wait(&sm.bar_o, (h - 1) & 1);
+        if (stage_v) {
+            const float4* nv = T == 128 ? n0 : n2;
+            unsigned char* vb = reinterpret_cast<unsigned char*>(sm.VT[row >> 5]);
+            const uint32_t key = row & 31;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                *reinterpret_cast<float*>(vb + sw128_off(4 * c + 0, key)) = nv[c].x;
+                *reinterpret_cast<float*>(vb + sw128_off(4 * c + 1, key)) = nv[c].y;
+                *reinterpret_cast<float*>(vb + sw128_off(4 * c + 2, key)) = nv[c].z;
+                *reinterpret_cast<float*>(vb + sw128_off(4 * c + 3, key)) = nv[c].w;
+            }
+        }
         float sum = 0.f;
-#pragma unroll 1
-        for (int c = 0; c < 64; c += 16) {
-            float s[16], bc[16];
+        unsigned char* pb = reinterpret_cast<unsigned char*>(sm.P[kb]);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) bc[j] = bn[j];
-            if (c + 16 < 64) {
+        for (int q4 = 0; q4 < 8; ++q4) {
+            float pp[4];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) bn[j] = __ldg(b + (c + 16 + j) * kAttT);
+            for (int t = 0; t < 4; ++t) {
+                pp[t] = ex2_approx(lg[4 * q4 + t] - mx);
+                sum += pp[t];
             }
-            tmem_ld16(trow + key0 + c, s);
-            const uint32_t kk = key0 + c;
-            unsigned char* pb = reinterpret_cast<unsigned char*>(sm.P[kk >> 5]);
-#pragma unroll
-            for (int j4 = 0; j4 < 4; ++j4) {
-                float p[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int j = 4 * j4 + t;
-                    p[t] = exp2f(fmaf(fmaf(s[j], 0.25f, bc[j]), kLog2e, -mx2));
-                    sum += p[t];
-                }
-                *reinterpret_cast<float4*>(pb + sw128_off(row, (kk & 31) + 4 * j4)) = make_float4(p[0], p[1], p[2], p[3]);
-            }
+            *reinterpret_cast<float4*>(pb + sw128_off(row, 4 * q4)) = make_float4(pp[0], pp[1], pp[2], pp[3]);
+        }
+        if constexpr (NQ > 1) {
+            named_bar_sync(1, NQ * 128);  // every quad has read the maxima
+            sm.part[quad][row] = sum;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
-        __syncthreads();  // P complete; part[] max reads done
+        __syncthreads();  // P, V^T (and the partial sums) complete
         tc_fence_after();
-        if (tid == 0) {  // O = P V
+        if (tid == 0) {  // O_h = P V_h
 #pragma unroll
-            for (int kb = 0; kb < 4; ++kb) {
-                const uint64_t da = umma_desc_sw128(sm.P[kb]), db = umma_desc_sw128(sm.VT[kb]);
+            for (int b = 0; b < 4; ++b) {
+                const uint64_t da = umma_desc_sw128(sm.P[b]), db = umma_desc_sw128(sm.VT[b]);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) mma_tf32(tO, da + 2 * k, db + 2 * k, idO, (kb | k) ? 1u : 0u);
+                for (int k = 0; k < 4; ++k) mma_tf32(tO + h * kAttHD, da + 2 * k, db + 2 * k, idO, (b | k) ? 1u : 0u);
             }
-            mma_commit(&sm.bar);
+            mma_commit(&sm.bar_o);
         }
-        sm.part[quad][row] = sum;
-        float rs_trace = 0.f;
-        if (rowsum_err_bits) {  // trace: row sum of the normalised probabilities (this quad)
-            for (int c = 0; c < 64; c += 16) {
-                float s2[16];
-                tmem_ld16(trow + key0 + c, s2);
+        if (h + 1 < kAttHeads) fetch(h + 1);  // next head's q / k / v, in flight during the PV MMA
+        float tot = sum;
+        if constexpr (NQ > 1) tot = (sm.part[0][row] + sm.part[1][row]) + (sm.part[2][row] + sm.part[3][row]);
+        inv[h] = 1.f / tot;
+        if (rowsum_err_bits) {  // trace (toy_net.cpp:108-113): row sum of the normalised probabilities
+            float rs = 0.f;
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    rs_trace += exp2f(fmaf(fmaf(s2[j], 0.25f, __ldg(b + (c + j) * kAttT)), kLog2e, -mx2));
+            for (int j = 0; j < 32; ++j) rs += ex2_approx(lg[j] - mx) * inv[h];
+            if constexpr (NQ > 1) {
+                named_bar_sync(1, NQ * 128);  // every quad has read the sums
+                sm.part[quad][row] = rs;
+                named_bar_sync(1, NQ * 128);
+                rs = (sm.part[0][row] + sm.part[1][row]) + (sm.part[2][row] + sm.part[3][row]);
+                named_bar_sync(1, NQ * 128);
             }
+            if (valid) rs_err = fmaxf(rs_err, fabsf(rs - 1.f));
         }
-        mbar_wait(&sm.bar, phase);
-        phase ^= 1;
-        tc_fence_after();
-        __syncthreads();  // partial sums visible
-        const float tot = sm.part[0][row] + sm.part[1][row];
-        const float inv = 1.f / tot;
-        if (quad == 0) {
-            float o[16];
-            tmem_ld16(tO + (uint32_t((warp & 3) * 32) << 16), o);
-            float4* dst = reinterpret_cast<float4*>(head_out + (blk * kAttT + row) * d + h * kAttHD);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) bcur[i] = bnext[i];
+    }
+    // ---- out = O_h / rowsum: T = 128 quad q writes heads 2q, 2q+1; T = 32 all eight
+    mbar_wait(&sm.bar_o, (kAttHeads - 1) & 1);
+    tc_fence_after();
+    constexpr int HPQ = kAttHeads / NQ;
+    float* dst = head_out + grow * d + quad * HPQ * kAttHD;
+#pragma unroll
+    for (int hh = 0; hh < HPQ; hh += 2) {
+        const uint32_t hg = quad * HPQ + hh;
+        uint32_t u0[16], u1[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(u0[0]), "=r"(u0[1]), "=r"(u0[2]), "=r"(u0[3]), "=r"(u0[4]), "=r"(u0[5]), "=r"(u0[6]),
+              "=r"(u0[7]), "=r"(u0[8]), "=r"(u0[9]), "=r"(u0[10]), "=r"(u0[11]), "=r"(u0[12]), "=r"(u0[13]),
+              "=r"(u0[14]), "=r"(u0[15])
+            : "r"(tO + lane_off + hg * kAttHD));
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(u1[0]), "=r"(u1[1]), "=r"(u1[2]), "=r"(u1[3]), "=r"(u1[4]), "=r"(u1[5]), "=r"(u1[6]),
+              "=r"(u1[7]), "=r"(u1[8]), "=r"(u1[9]), "=r"(u1[10]), "=r"(u1[11]), "=r"(u1[12]), "=r"(u1[13]),
+              "=r"(u1[14]), "=r"(u1[15])
+            : "r"(tO + lane_off + (hg + 1) * kAttHD));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (valid) {
+            const float i0 = inv[hg], i1 = inv[hg + 1];
+            float4* o4 = reinterpret_cast<float4*>(dst + hh * kAttHD);
 #pragma unroll
             for (int c = 0; c < 4; ++c)
-                dst[c] = make_float4(o[4 * c] * inv, o[4 * c + 1] * inv, o[4 * c + 2] * inv, o[4 * c + 3] * inv);
+                o4[c] = make_float4(__uint_as_float(u0[4 * c]) * i0, __uint_as_float(u0[4 * c + 1]) * i0,
+                                    __uint_as_float(u0[4 * c + 2]) * i0, __uint_as_float(u0[4 * c + 3]) * i0);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                o4[4 + c] = make_float4(__uint_as_float(u1[4 * c]) * i1, __uint_as_float(u1[4 * c + 1]) * i1,
+                                        __uint_as_float(u1[4 * c + 2]) * i1, __uint_as_float(u1[4 * c + 3]) * i1);
         }
-        if (rowsum_err_bits) {
-            __syncthreads();  // both quads have read part[] for the row total
-            sm.part[quad][row] = rs_trace * inv;
-            __syncthreads();
-            if (quad == 0) atomicMax(rowsum_err_bits, __float_as_uint(fabsf(sm.part[0][row] + sm.part[1][row] - 1.f)));
-        }
-        tc_fence_before();
-        __syncthreads();  // TMEM S / O and smem reused by the next head
-        tc_fence_after();
     }
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    if (rowsum_err_bits && quad == 0 && valid) atomicMax(rowsum_err_bits, __float_as_uint(rs_err));
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    }
 }
-
-constexpr size_t att_smem_bytes() { return sizeof(AttSmem) + 1024; }
 
 }  // namespace hfpg

@@ -8,9 +8,12 @@
 #include <chrono>
 #include <cstring>
 #include <cstdlib>
+#include <initializer_list>
+#include <type_traits>
 #include <vector>
 
 #include "attention_tcgen05.cuh"
+#include "gemm_persistent.cuh"
 #include "gemm_tcgen05.cuh"
 #include "internal.hpp"
 #include "toynet_kernels.cuh"
@@ -113,136 +116,144 @@ CUtensorMap tmap(const float* p, uint64_t rows, uint64_t cols, uint64_t ld, uint
     return m;
 }
 
-// ---- GEMM epilogues ---------------------------------------------------------------------------
+// ---- GEMM epilogues (k_pgemm_tf32): apply1(row, col, v) with lane = column (coalesced) -----
 struct EpiStore {  // out[row, col] = act(v + bias)
+    static constexpr bool kWholeRow = false;
     float* out;
-    uint32_t ld, n;
+    uint32_t ld;
     const float* bias;
     int gelu;
-    // 8 consecutive rows (row0 .. row0+7) of columns col..col+3; values at v[i * ld]
-    __device__ void apply4x8(int row0, int col, const float* v, int ld, int nv) const {
+    __device__ __forceinline__ void apply32(int row0, int col, float (&v)[32], int nrows) const {
+        const float b = bias ? bias[col] : 0.f;
+        float* o = out + uint64_t(row0) * ld + col;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) apply4(row0 + i, col, *reinterpret_cast<const float4*>(v + i * ld), nv);
-    }
-    __device__ void apply4(int row, int col, float4 v, int nv) const {
-        float x[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            x[j] += (bias && j < nv) ? bias[col + j] : 0.f;
-            if (gelu) x[j] = gelu_f(x[j]);
-        }
-        float* o = out + uint64_t(row) * ld + col;
-        if (nv == 4 && (ld & 3) == 0) {
-            *reinterpret_cast<float4*>(o) = make_float4(x[0], x[1], x[2], x[3]);
-        } else {
-            for (int j = 0; j < nv; ++j) o[j] = x[j];
+        for (int rr = 0; rr < 32; ++rr) {
+            float x = v[rr] + b;
+            if (gelu) x = gelu_f(x);
+            if (rr < nrows) o[uint64_t(rr) * ld] = x;
         }
     }
 };
 struct EpiResidual {  // out[row, col] += act(v + bias)
+    static constexpr bool kWholeRow = false;
     float* out;
-    uint32_t ld, n;
+    uint32_t ld;
     const float* bias;
     int gelu;
-    // 8 rows at once: all residual reads issued before the writes
-    __device__ void apply4x8(int row0, int col, const float* v, int ldv, int nv) const {
-        if (nv != 4 || (ld & 3) != 0) {
-            for (int i = 0; i < 8; ++i) apply4(row0 + i, col, *reinterpret_cast<const float4*>(v + i * ldv), nv);
-            return;
-        }
-        float4 a[8];
+    __device__ __forceinline__ void apply32(int row0, int col, float (&v)[32], int nrows) const {
+        const float b = bias ? bias[col] : 0.f;
+        float* o = out + uint64_t(row0) * ld + col;
+        float a[32];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float4*>(out + uint64_t(row0 + i) * ld + col);
+        for (int rr = 0; rr < 32; ++rr) a[rr] = rr < nrows ? o[uint64_t(rr) * ld] : 0.f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float4 t = *reinterpret_cast<const float4*>(v + i * ldv);
-            float x[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                x[j] += bias ? bias[col + j] : 0.f;
-                if (gelu) x[j] = gelu_f(x[j]);
-            }
-            a[i].x += x[0]; a[i].y += x[1]; a[i].z += x[2]; a[i].w += x[3];
-            *reinterpret_cast<float4*>(out + uint64_t(row0 + i) * ld + col) = a[i];
+        for (int rr = 0; rr < 32; ++rr) {
+            float x = v[rr] + b;
+            if (gelu) x = gelu_f(x);
+            if (rr < nrows) o[uint64_t(rr) * ld] = a[rr] + x;
         }
     }
-    __device__ void apply4(int row, int col, float4 v, int nv) const {
-        float x[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            x[j] += (bias && j < nv) ? bias[col + j] : 0.f;
-            if (gelu) x[j] = gelu_f(x[j]);
-        }
-        float* o = out + uint64_t(row) * ld + col;
-        if (nv == 4 && (ld & 3) == 0) {
-            float4 a = *reinterpret_cast<float4*>(o);
-            a.x += x[0]; a.y += x[1]; a.z += x[2]; a.w += x[3];
-            *reinterpret_cast<float4*>(o) = a;
-        } else {
-            for (int j = 0; j < nv; ++j) o[j] += x[j];
-        }
-    }
+};
+// Residual + LayerNorm of the updated row (toy_net.cpp:28-41, no affine, eps 1e-5, two-pass):
+// x[row] += act(v) (the sublayer output, toy_net.cpp:123 / :435; act = GELU for the GCN update,
+// :316), ln[row] = LN(x[row]) — the next sublayer's normalised input, so there is no separate
+// LayerNorm pass over the tokens. Rows of d = 128 = BN (k_pgemm_tf32's whole-row epilogue).
+struct EpiResidualLN {
+    static constexpr bool kWholeRow = true;
+    float* x;
+    float* ln;
+    int gelu;
+    __device__ __forceinline__ float act(float v) const { return gelu_f(v); }
 };
 // Decoder heads of leaf node `row` (toy_net.cpp:549-567): columns [0, L_s) -> Ũ_k row,
 // [L_s, 2 L_s) -> Ṽ_k row, 2 L_s -> gate. Cast to float as the reference does.
 struct EpiLeafHeads {
+    static constexpr bool kWholeRow = false;
     float* out;
-    uint64_t L, Ls, bridge_base, gate_base;
-    const float* bias;  // 2 Ls + 1
-    // 8 consecutive rows (row0 .. row0+7) of columns col..col+3; values at v[i * ld]
-    __device__ void apply4x8(int row0, int col, const float* v, int ld, int nv) const {
+    uint32_t lL, lLs;  // log2 L, log2 L_s (powers of two, as the GPU forward requires)
+    uint64_t bridge_base, gate_base;
+    __device__ __forceinline__ void apply32(int row0, int col, float (&v)[32], int nrows) const {
+        const uint32_t c = uint32_t(col), Ls = 1u << lLs, L = 1u << lL;
+        if (c < 2 * Ls) {
+            const uint64_t off = c < Ls ? c : uint64_t(L) * Ls + (c - Ls);  // Ũ_k or Ṽ_k column
 #pragma unroll
-        for (int i = 0; i < 8; ++i) apply4(row0 + i, col, *reinterpret_cast<const float4*>(v + i * ld), nv);
-    }
-    __device__ void apply4(int row, int col, float4 v, int nv) const {
-        const uint64_t k = uint64_t(row) / L, r = uint64_t(row) % L;
-        const float vv[4] = {v.x, v.y, v.z, v.w};
-        for (int j = 0; j < nv; ++j) {
-            const uint64_t c = uint64_t(col + j);
-            const float x = vv[j] + (bias && c <= 2 * Ls ? bias[c] : 0.f);
-            if (c < Ls) out[bridge_base + k * 2 * L * Ls + r * Ls + c] = x;
-            else if (c < 2 * Ls) out[bridge_base + k * 2 * L * Ls + L * Ls + r * Ls + (c - Ls)] = x;
-            else if (c == 2 * Ls) out[gate_base + uint64_t(row)] = x;
+            for (int rr = 0; rr < 32; ++rr) {
+                const uint64_t row = uint64_t(row0 + rr), k = row >> lL, r = row & (L - 1);
+                if (rr < nrows) out[bridge_base + k * (2ull * L * Ls) + r * Ls + off] = v[rr];
+            }
+        } else if (c == 2 * Ls) {
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr)
+                if (rr < nrows) out[gate_base + uint64_t(row0 + rr)] = v[rr];
         }
     }
 };
 // Tile heads of tile token `row` = m L_s + tok (toy_net.cpp:570-584): [0, rk) -> U_m[tok],
 // [rk, 2 rk) -> V_m[tok].
 struct EpiTileHeads {
+    static constexpr bool kWholeRow = false;
     float* out;
-    uint64_t Ls, rk, tile_base;
-    const float* bias;
-    // 8 consecutive rows (row0 .. row0+7) of columns col..col+3; values at v[i * ld]
-    __device__ void apply4x8(int row0, int col, const float* v, int ld, int nv) const {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) apply4(row0 + i, col, *reinterpret_cast<const float4*>(v + i * ld), nv);
-    }
-    __device__ void apply4(int row, int col, float4 v, int nv) const {
-        const uint64_t m = uint64_t(row) / Ls, tok = uint64_t(row) % Ls;
-        const float vv[4] = {v.x, v.y, v.z, v.w};
-        for (int j = 0; j < nv; ++j) {
-            const uint64_t c = uint64_t(col + j);
-            if (c >= 2 * rk) continue;
-            const float x = vv[j] + (bias ? bias[c] : 0.f);
-            out[tile_base + m * Ls * Ls + (c < rk ? 0 : Ls * rk) + tok * rk + (c % rk)] = x;
+    uint32_t lLs;  // log2 L_s
+    uint64_t tile_base;
+    __device__ __forceinline__ void apply32(int row0, int col, float (&v)[32], int nrows) const {
+        const uint32_t c = uint32_t(col), Ls = 1u << lLs, rk = Ls >> 1;
+        if (c >= 2 * rk) return;
+        for (int rr = 0; rr < nrows; ++rr) {
+            const uint64_t row = uint64_t(row0 + rr), m = row >> lLs, tok = row & (Ls - 1);
+            out[tile_base + m * Ls * Ls + (c < rk ? 0 : Ls * rk) + tok * rk + (c % rk)] = v[rr];
         }
     }
 };
 
+// A operand sources side by side along K (gemm_persistent.cuh): {pointer, row pitch, columns}.
+struct ASrc {
+    const float* p;
+    uint64_t ld, kcols;
+};
+PgA make_pga(std::initializer_list<ASrc> srcs, uint64_t M) {
+    PgA a{};
+    int s = 0, kb = 0;
+    for (const ASrc& d : srcs) {
+        if (s == 3) throw InvalidArgument("gemm: at most three A sources");
+        a.map[s] = tmap(d.p, M, d.kcols, d.ld, kGemmBM);
+        kb += int((d.kcols + kGemmBK - 1) / kGemmBK);
+        a.kb_end[s] = kb;
+        if (s + 1 < int(srcs.size()) && d.kcols % kGemmBK) throw InvalidArgument("gemm: inner A sources need K % 32 == 0");
+        ++s;
+    }
+    a.nsrc = s;
+    return a;
+}
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        TCK(cudaGetDevice(&dev));
+        TCK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return n;
+}
+// C = epi(A * W): A from `pa` (M x K), W^T = Bt (N x K, row pitch ldb).
 template <int BN, class Epi>
-void gemm(cudaStream_t st, const float* A, uint64_t M, uint64_t K, uint64_t lda, const float* Bt,
-          uint64_t N, uint64_t ldb, const Epi& epi) {
+void pgemm(cudaStream_t st, const PgA& pa, uint64_t M, uint64_t K, const float* Bt, uint64_t N, uint64_t ldb,
+           const Epi& epi) {
     static bool configured = false;
     if (!configured) {
-        TCK(cudaFuncSetAttribute(k_gemm_tf32<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(gemm_smem_bytes<BN>())));
+        TCK(cudaFuncSetAttribute(k_pgemm_tf32<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(pgemm_smem_bytes<BN, Epi::kWholeRow>())));
         configured = true;
     }
     if (M == 0 || N == 0) return;
-    const CUtensorMap ta = tmap(A, M, K, lda, kGemmBM), tb = tmap(Bt, N, K, ldb, BN);
-    dim3 grid(unsigned((M + kGemmBM - 1) / kGemmBM), unsigned((N + BN - 1) / BN));
-    k_gemm_tf32<BN, Epi><<<grid, kGemmThreads, gemm_smem_bytes<BN>(), st>>>(ta, tb, int(M), int(N), int(K), epi);
+    const CUtensorMap tb = tmap(Bt, N, K, ldb, BN);
+    const uint64_t tiles = ((M + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
+    const unsigned grid = unsigned(std::min<uint64_t>(tiles, uint64_t(sm_count())));
+    k_pgemm_tf32<BN, Epi><<<grid, kPgThreads, pgemm_smem_bytes<BN, Epi::kWholeRow>(), st>>>(pa, tb, int(M), int(N), int(K), epi);
     TCK(cudaGetLastError());
+}
+template <int BN, class Epi>
+void pgemm1(cudaStream_t st, const float* A, uint64_t M, uint64_t K, uint64_t lda, const float* Bt, uint64_t N,
+            uint64_t ldb, const Epi& epi) {
+    pgemm<BN>(st, make_pga({ASrc{A, lda, K}}, M), M, K, Bt, N, ldb, epi);
 }
 
 // Device copy of W^T (out x in, fp32), optionally padding the input dimension to kpad.
@@ -312,11 +323,17 @@ struct ToynetModel {
     std::vector<LW> wl, wt;
     std::vector<std::pair<void*, size_t>> scratch;  // (ptr, bytes), index = buffer id
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // the tile stream's chain runs beside the leaf stream's on a second stream (fork / join)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     ~ToynetModel() {
         for (float* p : wbuf) cudaFree(p);
         for (auto& b : scratch) cudaFree(b.first);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (side) cudaStreamDestroy(side);
     }
     template <class T>
     T* buf(size_t id, uint64_t count) {
@@ -365,6 +382,9 @@ ToynetModel* toynet_model_create(const hfpg_toynet_config& cfg, uint64_t L, uint
         m->w_theads = upload_stack_t({&w.thu, &w.thv}, m->wbuf);
         TCK(cudaEventCreate(&m->ev0));
         TCK(cudaEventCreate(&m->ev1));
+        TCK(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
+        TCK(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
+        TCK(cudaStreamCreateWithFlags(&m->side, cudaStreamNonBlocking));
     } catch (...) {
         delete m;
         throw;
@@ -410,101 +430,205 @@ static void toynet_run(ToynetModel* mdl, cudaStream_t st, uint64_t n, uint64_t w
     const auto& wl = mdl->wl;
     const auto& wt = mdl->wt;
     using LW = ToynetModel::LW;
+    // chunk-sum pyramids need nested power-of-two chunks: c0 = L / L_s >= 1 (the production
+    // L = 128, L_s = 32 gives c0 = 4); other shapes walk each chunk
+    const bool pyr = L >= Ls && lay.m > 0;
+    uint32_t lev_shift = 0;
+    while ((uint64_t(1) << lev_shift) < L / std::max<uint64_t>(Ls, 1)) ++lev_shift;
+    const uint32_t c0 = uint32_t(1) << lev_shift, nlev = uint32_t(lay.depth);
+    uint64_t pyr_rows = 0;  // entries over all levels
+    for (uint32_t l = 0; l < nlev; ++l) pyr_rows += n / (uint64_t(c0) << l);
     // ---- activations -------------------------------------------------------------------------
     auto* feat = mdl->buf<float>(5, n * g.feat_pad);
     auto* x = mdl->buf<float>(6, n * d);       // embedding -> leaf tokens
     auto* h1 = mdl->buf<float>(7, n * d);      // encoder hidden / gcn message / decoder hidden
-    auto* tile_tok = mdl->buf<float>(8, MT * d);
-    auto* ln = mdl->buf<float>(9, std::max(n, MT) * d);
-    auto* qkv = mdl->buf<float>(10, std::max(n, MT) * 3 * d);
-    auto* hout = mdl->buf<float>(11, std::max(n, MT) * d);
+    auto* tile_tok = mdl->buf<float>(8, std::max<uint64_t>(MT, 1) * d);
+    auto* ln = mdl->buf<float>(9, n * d);      // LN(leaf tokens): the next sublayer's input
+    auto* qkv = mdl->buf<float>(10, n * 3 * d);
+    auto* hout = mdl->buf<float>(11, n * d);
     auto* row_hw = mdl->buf<float>(12, n * d);
     auto* col_hw = mdl->buf<float>(13, n * d);
-    auto* Af = mdl->buf<float>(14, std::max(n, MT) * 4 * d);
-    auto* Hf = mdl->buf<float>(15, std::max(n, MT) * 4 * d);
+    auto* ln_t = mdl->buf<float>(14, std::max<uint64_t>(MT, 1) * d);  // LN(tile tokens)
+    auto* Hf = mdl->buf<float>(15, n * 4 * d);
+    auto* Hf_t = mdl->buf<float>(35, std::max<uint64_t>(MT, 1) * 4 * d);
+    auto* qkv_t = mdl->buf<float>(36, std::max<uint64_t>(MT, 1) * 3 * d);
+    auto* hout_t = mdl->buf<float>(37, std::max<uint64_t>(MT, 1) * d);
     auto* glob_hw = mdl->buf<float>(16, d);
     const uint32_t nparts = 296;
-    auto* partial = mdl->buf<float>(17, uint64_t(nparts) * 2 * d);
-    auto* leaf_bias = mdl->buf<float>(18, lay.k * cfg.heads * L * L);
-    auto* tile_bias = mdl->buf<float>(19, lay.m * cfg.heads * Ls * Ls);
+    const unsigned hw_blocks = pyr ? unsigned((n / c0 * 32 + 255) / 256) : 0u;  // k_tn_highway_chunks CTAs
+    auto* partial = mdl->buf<float>(17, (uint64_t(nparts) * 2 + hw_blocks) * d);
+    auto* leaf_bias = mdl->buf<__half>(18, lay.k * cfg.heads * L * L);
+    auto* tile_bias = mdl->buf<__half>(19, std::max<uint64_t>(lay.m, 1) * cfg.heads * Ls * Ls);
     auto* tile_pos = mdl->buf<double>(26, std::max<uint64_t>(lay.m, 1) * 2 * Ls * 2);
-    unsigned int* rowsum_bits = trace ? mdl->buf<unsigned int>(20, 1) : nullptr;
-    float* audit_part = trace ? mdl->buf<float>(23, uint64_t(nparts) * d) : nullptr;
-    float* audit_sums = trace ? mdl->buf<float>(24, 6 * d) : nullptr;
-    float* audit_dev = trace ? mdl->buf<float>(25, cfg.layers) : nullptr;
+    auto* rmean = mdl->buf<float>(28, std::max<uint64_t>(MT, 1) * d);
+    auto* cmean = mdl->buf<float>(29, std::max<uint64_t>(MT, 1) * d);
+    auto* pyr_r = mdl->buf<float>(30, std::max<uint64_t>(pyr_rows, 1) * d);  // also the embedding pyramid
+    auto* pyr_c = mdl->buf<float>(31, std::max<uint64_t>(pyr_rows, 1) * d);
+    auto* b1 = mdl->buf<float>(32, 8 * d);  // glob-slice FFN biases: leaf [0, 4d), tile [4d, 8d)
+    const bool audit = trace && !trace->timing_only;
+    unsigned int* rowsum_bits = audit ? mdl->buf<unsigned int>(20, 1) : nullptr;
+    float* audit_part = audit ? mdl->buf<float>(23, uint64_t(nparts) * d) : nullptr;
+    float* audit_sums = audit ? mdl->buf<float>(24, 6 * d) : nullptr;
+    float* audit_dev = audit ? mdl->buf<float>(25, cfg.layers) : nullptr;
     if (rowsum_bits) TCK(cudaMemsetAsync(rowsum_bits, 0, 4, st));
+    auto levels = [&](float* base) {
+        PyrLevels<float> P{};
+        uint64_t off = 0;
+        for (uint32_t l = 0; l < nlev && l < 24; ++l) {
+            P.lev[l] = base + off * d;
+            off += n / (uint64_t(c0) << l);
+        }
+        return P;
+    };
+    // levels 0 .. nlev-1 of the row-chunk sums of src (n x C), c0 rows per level-0 entry
+    auto build_pyramid = [&](cudaStream_t st, auto* src, uint32_t C, const auto& P) {
+        using T = std::remove_const_t<std::remove_pointer_t<decltype(src)>>;
+        using V = std::conditional_t<std::is_same_v<T, float>, float4, double2>;
+        constexpr uint32_t VW = sizeof(V) / sizeof(T);
+        uint32_t done = 0, group = c0;
+        uint64_t rows = n;
+        const T* s0 = src;
+        while (done < nlev) {
+            uint32_t q = std::min<uint32_t>(nlev - done - 1, 4u);
+            while ((group << q) > 32) --q;
+            const uint64_t nblocks = rows / (uint64_t(group) << q);
+            const uint64_t threads = nblocks * (C / VW);
+            const unsigned gr = unsigned((threads + 127) / 128);
+            switch (group) {
+                case 1: k_tn_pyramid<T, V, 1><<<gr, 128, 0, st>>>(s0, nblocks, C, q, P, done); break;
+                case 2: k_tn_pyramid<T, V, 2><<<gr, 128, 0, st>>>(s0, nblocks, C, q, P, done); break;
+                case 4: k_tn_pyramid<T, V, 4><<<gr, 128, 0, st>>>(s0, nblocks, C, q, P, done); break;
+                case 8: k_tn_pyramid<T, V, 8><<<gr, 128, 0, st>>>(s0, nblocks, C, q, P, done); break;
+                case 16: k_tn_pyramid<T, V, 16><<<gr, 128, 0, st>>>(s0, nblocks, C, q, P, done); break;
+                default: k_tn_pyramid<T, V, 32><<<gr, 128, 0, st>>>(s0, nblocks, C, q, P, done); break;
+            }
+            done += q + 1;
+            s0 = P.lev[done - 1];
+            rows = n / (uint64_t(c0) << (done - 1));
+            group = 2;
+        }
+        TCK(cudaGetLastError());
+    };
+    const PyrLevels<float> Pr = levels(pyr_r), Pc = levels(pyr_c);
 
     const unsigned nb = unsigned((n + 255) / 256), nw = unsigned((n * 32 + 255) / 256);
     TCK(cudaEventRecord(mdl->ev0, st));
-    // ---- encoder (toy_net.cpp:295-318) -----------------------------------------------------
+    // ---- encoder (toy_net.cpp:295-318); the last residual update also writes LN(x) -------------
     k_tn_features<<<nb, 256, 0, st>>>(g, d_order, d_rho, d_ro, d_ci, d_glob, feat);
-    gemm<128>(st, feat, n, g.feat_pad, g.feat_pad, mdl->w_enc1, d, g.feat_pad, EpiStore{h1, uint32_t(d), uint32_t(d), nullptr, 1});
-    gemm<128>(st, h1, n, d, d, mdl->w_enc2, d, d, EpiStore{x, uint32_t(d), uint32_t(d), nullptr, 0});
-    for (float* wg : mdl->w_gcn) {
+    pgemm1<128>(st, feat, n, g.feat_pad, g.feat_pad, mdl->w_enc1, d, g.feat_pad, EpiStore{h1, uint32_t(d), nullptr, 1});
+    pgemm1<128>(st, h1, n, d, d, mdl->w_enc2, d, d, EpiStore{x, uint32_t(d), nullptr, 0});
+    for (size_t gi = 0; gi < mdl->w_gcn.size(); ++gi) {
         k_tn_gcn_msg<<<nw, 256, 0, st>>>(g, d_ro, d_ci, d_v, d_diag, x, h1);
-        gemm<128>(st, h1, n, d, d, wg, d, d, EpiResidual{x, uint32_t(d), uint32_t(d), nullptr, 1});
+        if (gi + 1 < mdl->w_gcn.size())
+            pgemm1<128>(st, h1, n, d, d, mdl->w_gcn[gi], d, d, EpiResidual{x, uint32_t(d), nullptr, 1});
+        else
+            pgemm1<128>(st, h1, n, d, d, mdl->w_gcn[gi], d, d, EpiResidualLN{x, ln, 1});
     }
+    if (mdl->w_gcn.empty()) k_tn_layernorm<<<nw, 256, 0, st>>>(n, uint32_t(d), x, ln, uint32_t(d));
     TCK(cudaGetLastError());
     // ---- tile tokens, edge biases ------------------------------------------------------------
-    if (lay.m) k_tn_tile_pool<<<dim3(unsigned(lay.m), unsigned(Ls)), 128, 0, st>>>(g, x, tile_tok);
+    if (lay.m) {
+        if (pyr) {
+            build_pyramid(st, x, uint32_t(d), Pr);  // embedding pyramid (pyr_r is reused per layer below)
+            k_tn_tile_pool_pyr<<<unsigned((MT * 32 + 255) / 256), 256, 0, st>>>(g, Pr, lev_shift, tile_tok);
+        } else {
+            k_tn_tile_pool<<<dim3(unsigned(lay.m), unsigned(Ls)), 128, 0, st>>>(g, x, tile_tok);
+        }
+        k_tn_layernorm<<<unsigned((MT * 32 + 255) / 256), 256, 0, st>>>(MT, uint32_t(d), tile_tok, ln_t, uint32_t(d));
+    }
     k_tn_leaf_bias<<<dim3(unsigned((L * L + 255) / 256), unsigned(lay.k)), 256, 0, st>>>(
         g, d_order, d_ro, d_ci, d_v, mdl->le, leaf_bias);
     if (lay.m) {
-        k_tn_tile_pos<<<dim3(unsigned(lay.m), 2), 256, 0, st>>>(g, d_order, tile_pos);
+        if (pyr) {
+            auto* pos = mdl->buf<double>(33, n * 2);
+            auto* ppos = mdl->buf<double>(34, std::max<uint64_t>(pyr_rows, 1) * 2);
+            PyrLevels<double> Pp{};
+            uint64_t off = 0;
+            for (uint32_t l = 0; l < nlev && l < 24; ++l) {
+                Pp.lev[l] = ppos + off * 2;
+                off += n / (uint64_t(c0) << l);
+            }
+            k_tn_positions<<<nb, 256, 0, st>>>(g, d_order, pos);
+            build_pyramid(st, pos, 2u, Pp);
+            k_tn_tile_pos_pyr<<<unsigned(lay.m), 64, 0, st>>>(g, Pp, lev_shift, tile_pos);
+        } else {
+            k_tn_tile_pos<<<dim3(unsigned(lay.m), 2), 256, 0, st>>>(g, d_order, tile_pos);
+        }
         k_tn_tile_bias<<<dim3(unsigned(lay.m), unsigned(Ls)), 64, 0, st>>>(
             g, tile_pos, d_ro, d_ci, d_v, mdl->te, tile_bias);
     }
     TCK(cudaGetLastError());
 
-    auto attention = [&](float* tok, uint64_t rows, uint64_t T, const LW& lw, const float* bias) {
-        k_tn_layernorm<<<unsigned((rows * 32 + 255) / 256), 256, 0, st>>>(rows, uint32_t(d), tok, ln, uint32_t(d));
-        gemm<128>(st, ln, rows, d, d, lw.qkv, 3 * d, d, EpiStore{qkv, uint32_t(3 * d), uint32_t(3 * d), nullptr, 0});
-        const dim3 grid(unsigned(rows / T), unsigned(cfg.heads));
-        static const bool simt128 = std::getenv("HFPG_ATTENTION_SIMT") != nullptr;  // A/B checks only
-        if (T == 128 && !simt128) {  // tensor-core path (attention_tcgen05.cuh)
+    // attention sublayer (toy_net.cpp:78-125) on `rows` tokens in windows of T; lnbuf holds
+    // LN(tok) on entry and LN(tok + attention) on exit (fused into the O-projection epilogue)
+    auto attention = [&](cudaStream_t st, float* tok, float* lnbuf, uint64_t rows, uint64_t T, const LW& lw,
+                         const __half* bias, float* qkv, float* hout) {
+        pgemm1<128>(st, lnbuf, rows, d, d, lw.qkv, 3 * d, d, EpiStore{qkv, uint32_t(3 * d), nullptr, 0});
+        const uint64_t nwin = rows / T;
+        if (T == 128 || T == 32) {  // tensor cores (attention_tcgen05.cuh)
             static bool configured = false;
             if (!configured) {
-                TCK(cudaFuncSetAttribute(k_tn_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(att_smem_bytes())));
+                TCK(cudaFuncSetAttribute(k_tn_attn_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(att_smem_bytes())));
+                TCK(cudaFuncSetAttribute(k_tn_attn_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(att_smem_bytes())));
                 configured = true;
             }
-            k_tn_attention_tc<<<unsigned(rows / T), kAttThreads, att_smem_bytes(), st>>>(
-                uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits);
-            TCK(cudaGetLastError());
-            gemm<128>(st, hout, rows, d, d, lw.wo, d, d, EpiResidual{tok, uint32_t(d), uint32_t(d), nullptr, 0});
-            return;
-        }
-        switch (T) {
-            case 128: k_tn_attention<128><<<grid, 128, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
-            case 64: k_tn_attention<64><<<grid, 64, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
-            case 32: k_tn_attention<32><<<grid, 32, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
-            case 16: k_tn_attention<16><<<grid, 16, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
-            case 8: k_tn_attention<8><<<grid, 8, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
-            case 4: k_tn_attention<4><<<grid, 4, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
-            default: throw InvalidArgument("toynet (gpu): unsupported attention window");
+            const unsigned groups = unsigned((rows + kAttRows - 1) / kAttRows);
+            if (T == 128)
+                k_tn_attn_tc<128><<<groups, att_threads<128>(), att_smem_bytes(), st>>>(nwin, qkv, bias, hout, rowsum_bits);
+            else
+                k_tn_attn_tc<32><<<groups, att_threads<32>(), att_smem_bytes(), st>>>(nwin, qkv, bias, hout, rowsum_bits);
+        } else {
+            const dim3 grid(unsigned(nwin), unsigned(cfg.heads));
+            switch (T) {
+                case 64: k_tn_attention<64><<<grid, 64, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
+                case 16: k_tn_attention<16><<<grid, 16, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
+                case 8: k_tn_attention<8><<<grid, 8, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
+                case 4: k_tn_attention<4><<<grid, 4, 0, st>>>(uint32_t(d), uint32_t(cfg.heads), qkv, bias, hout, rowsum_bits); break;
+                default: throw InvalidArgument("toynet (gpu): unsupported attention window");
+            }
         }
         TCK(cudaGetLastError());
-        gemm<128>(st, hout, rows, d, d, lw.wo, d, d, EpiResidual{tok, uint32_t(d), uint32_t(d), nullptr, 0});
+        pgemm1<128>(st, hout, rows, d, d, lw.wo, d, d, EpiResidualLN{tok, lnbuf, 0});
     };
-    auto ffn = [&](float* tok, uint64_t rows, const LW& lw, bool leaf) {
-        k_tn_layernorm<<<unsigned((rows * 32 + 255) / 256), 256, 0, st>>>(rows, uint32_t(d), tok, Af, uint32_t(4 * d));
-        if (leaf)
-            k_tn_ffn_input_leaf<<<unsigned((rows * 32 + 255) / 256), 256, 0, st>>>(g, row_hw, col_hw, glob_hw, Af);
-        else
-            k_tn_ffn_input_tile<<<dim3(unsigned(lay.m), unsigned(Ls)), 128, 0, st>>>(g, row_hw, col_hw, glob_hw, Af);
-        TCK(cudaGetLastError());
-        gemm<128>(st, Af, rows, 4 * d, 4 * d, lw.f1, 4 * d, 4 * d, EpiStore{Hf, uint32_t(4 * d), uint32_t(4 * d), nullptr, 1});
-        gemm<128>(st, Hf, rows, 4 * d, 4 * d, lw.f2, d, 4 * d, EpiResidual{tok, uint32_t(d), uint32_t(d), nullptr, 0});
+    // FFN sublayer (toy_net.cpp:421-436) on [LN(t) | r | c | glob]: K-sliced over the three
+    // buffers (no concatenated input), the glob slice folded into the bias (k_tn_glob_bias);
+    // the second GEMM's epilogue adds the residual and writes LN of the result
+    auto ffn = [&](cudaStream_t st, float* tok, float* lnbuf, const float* r, const float* c, uint64_t rows,
+                   const LW& lw, const float* bias, float* Hf) {
+        pgemm<256>(st, make_pga({ASrc{lnbuf, d, d}, ASrc{r, d, d}, ASrc{c, d, d}}, rows), rows, 3 * d, lw.f1, 4 * d,
+                   4 * d, EpiStore{Hf, uint32_t(4 * d), bias, 1});
+        pgemm1<128>(st, Hf, rows, 4 * d, 4 * d, lw.f2, d, 4 * d, EpiResidualLN{tok, lnbuf, 0});
     };
 
+    cudaStream_t st2 = mdl->side;
+    auto fork = [&] {  // st2 continues from st's current point
+        TCK(cudaEventRecord(mdl->ev_fork, st));
+        TCK(cudaStreamWaitEvent(st2, mdl->ev_fork, 0));
+    };
+    auto join = [&] {  // st waits for st2's work so far
+        TCK(cudaEventRecord(mdl->ev_join, st2));
+        TCK(cudaStreamWaitEvent(st, mdl->ev_join, 0));
+    };
     for (uint64_t layer = 0; layer < cfg.layers; ++layer) {
-        attention(x, n, L, wl[layer], leaf_bias);
-        if (lay.m) attention(tile_tok, MT, Ls, wt[layer], tile_bias);
-        k_tn_highway<<<nw, 256, 0, st>>>(g, x, tile_tok, row_hw, col_hw);
-        k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(n, uint32_t(d), x, partial);
-        k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(MT, uint32_t(d), tile_tok, partial + nparts * d);
-        k_tn_colsum_finish<<<unsigned(d), 32, 0, st>>>(2 * nparts, uint32_t(d), partial, glob_hw);
+        // the two attention sublayers touch disjoint tokens: leaf on st, tile on st2
+        fork();
+        attention(st, x, ln, n, L, wl[layer], leaf_bias, qkv, hout);
+        if (lay.m) attention(st2, tile_tok, ln_t, MT, Ls, wt[layer], tile_bias, qkv_t, hout_t);
+        join();
+        if (pyr) {  // scatter + the leaf tokens' glob partials in one pass
+            k_tn_highway_chunks<<<hw_blocks, 256, 0, st>>>(g, c0, x, tile_tok, row_hw, col_hw, partial);
+            k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(MT, uint32_t(d), tile_tok, partial + uint64_t(hw_blocks) * d);
+            k_tn_colsum_finish<<<unsigned(d), 32, 0, st>>>(hw_blocks + nparts, uint32_t(d), partial, glob_hw);
+        } else {
+            k_tn_highway<<<nw, 256, 0, st>>>(g, x, tile_tok, row_hw, col_hw);
+            k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(n, uint32_t(d), x, partial);
+            k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(MT, uint32_t(d), tile_tok, partial + nparts * d);
+            k_tn_colsum_finish<<<unsigned(d), 32, 0, st>>>(2 * nparts, uint32_t(d), partial, glob_hw);
+        }
+        k_tn_glob_bias<<<dim3(unsigned((4 * d * 32 + 255) / 256), 2), 256, 0, st>>>(uint32_t(d), glob_hw, wl[layer].f1,
+                                                                                  wt[layer].f1, b1, b1 + 4 * d);
         TCK(cudaGetLastError());
-        if (trace) {  // highway conservation audit (toy_net.cpp:478-512), on device
+        if (audit) {  // highway conservation audit (toy_net.cpp:478-512), on device
             k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(n, uint32_t(d), row_hw, audit_part);
             k_tn_colsum_finish<<<unsigned(d), 32, 0, st>>>(nparts, uint32_t(d), audit_part, audit_sums);
             k_tn_colsum_partial<<<nparts, unsigned(d), 0, st>>>(n, uint32_t(d), col_hw, audit_part);
@@ -519,29 +643,47 @@ static void toynet_run(ToynetModel* mdl, cudaStream_t st, uint64_t n, uint64_t w
             k_tn_highway_audit<<<1, unsigned(d), 0, st>>>(uint32_t(d), audit_sums, audit_dev + layer);
             TCK(cudaGetLastError());
         }
-        ffn(x, n, wl[layer], true);
-        if (lay.m) ffn(tile_tok, MT, wt[layer], false);
+        // FFN sublayers: leaf on st; the tile FFN's strip means + FFN on st2 (both only read
+        // row_hw / col_hw; the next layer's scatter joins them first)
+        fork();
+        ffn(st, x, ln, row_hw, col_hw, n, wl[layer], b1, Hf);
+        if (lay.m) {
+            if (pyr) {
+                build_pyramid(st2, row_hw, uint32_t(d), Pr);
+                build_pyramid(st2, col_hw, uint32_t(d), Pc);
+                k_tn_tile_means_pyr<<<unsigned((MT * 32 + 255) / 256), 256, 0, st2>>>(g, Pr, Pc, lev_shift, rmean, cmean);
+            } else {
+                k_tn_tile_means_walk<<<dim3(unsigned(lay.m), unsigned(Ls)), 128, 0, st2>>>(g, row_hw, col_hw, rmean, cmean);
+            }
+            TCK(cudaGetLastError());
+            ffn(st2, tile_tok, ln_t, rmean, cmean, MT, wt[layer], b1 + 4 * d, Hf_t);
+        }
+        join();
     }
 
     // ---- decoder heads into the packed layout (toy_net.cpp:540-585) ------------------------
-    gemm<128>(st, x, n, d, d, mdl->w_lh1, d, d, EpiStore{h1, uint32_t(d), uint32_t(d), nullptr, 1});
+    pgemm1<128>(st, x, n, d, d, mdl->w_lh1, d, d, EpiStore{h1, uint32_t(d), nullptr, 1});
     // F_k rows: leaf_factor(k) + r L = (k L + r) L = i L -> a row-major [n x L] section
-    gemm<128>(st, h1, n, d, d, mdl->w_lh2, L, d, EpiStore{out, uint32_t(L), uint32_t(L), nullptr, 0});
-    gemm<80>(st, x, n, d, d, mdl->w_heads, 2 * Ls + 1, d,
-             EpiLeafHeads{out, L, Ls, lay.bridge_base, lay.gate_base, nullptr});
-    if (lay.m) gemm<32>(st, tile_tok, MT, d, d, mdl->w_theads, Ls, d, EpiTileHeads{out, Ls, Ls / 2, lay.tile_base, nullptr});
+    pgemm1<128>(st, h1, n, d, d, mdl->w_lh2, L, d, EpiStore{out, uint32_t(L), nullptr, 0});
+    uint32_t lL = 0, lLs = 0;
+    while ((1ull << lL) < L) ++lL;
+    while ((1ull << lLs) < Ls) ++lLs;
+    pgemm1<80>(st, x, n, d, d, mdl->w_heads, 2 * Ls + 1, d, EpiLeafHeads{out, lL, lLs, lay.bridge_base, lay.gate_base});
+    if (lay.m) pgemm1<32>(st, tile_tok, MT, d, d, mdl->w_theads, Ls, d, EpiTileHeads{out, lLs, lay.tile_base});
     TCK(cudaEventRecord(mdl->ev1, st));
     TCK(cudaStreamSynchronize(st));
 
     if (trace) {
-        unsigned int bits = 0;
-        TCK(cudaMemcpy(&bits, rowsum_bits, 4, cudaMemcpyDeviceToHost));
-        float e;
-        std::memcpy(&e, &bits, 4);
-        trace->max_attention_row_sum_error = e;
-        std::vector<float> hw(cfg.layers, 0.f);
-        TCK(cudaMemcpy(hw.data(), audit_dev, cfg.layers * 4, cudaMemcpyDeviceToHost));
-        trace->highway_max_deviation = hw.empty() ? 0.0 : *std::max_element(hw.begin(), hw.end());
+        if (audit) {
+            unsigned int bits = 0;
+            TCK(cudaMemcpy(&bits, rowsum_bits, 4, cudaMemcpyDeviceToHost));
+            float e;
+            std::memcpy(&e, &bits, 4);
+            trace->max_attention_row_sum_error = e;
+            std::vector<float> hw(cfg.layers, 0.f);
+            TCK(cudaMemcpy(hw.data(), audit_dev, cfg.layers * 4, cudaMemcpyDeviceToHost));
+            trace->highway_max_deviation = hw.empty() ? 0.0 : *std::max_element(hw.begin(), hw.end());
+        }
         trace->leaf_attention_dispatches = cfg.layers;
         trace->tile_attention_dispatches = lay.m ? cfg.layers : 0;
         float dev_ms = 0.f;
@@ -639,7 +781,7 @@ extern "C" int hfpg_gemm_tf32(uint64_t M, uint64_t N, uint64_t K, const float* A
         TCK(cudaMalloc(&dC, std::max<uint64_t>(M * N, 1) * 4));
         TCK(cudaMemcpy(dA, A, M * K * 4, cudaMemcpyHostToDevice));
         TCK(cudaMemcpy(dB, Bt, N * K * 4, cudaMemcpyHostToDevice));
-        gemm<128>(0, dA, M, K, K, dB, N, K, EpiStore{dC, uint32_t(N), uint32_t(N), nullptr, 0});
+        pgemm1<128>(0, dA, M, K, K, dB, N, K, EpiStore{dC, uint32_t(N), nullptr, 0});
         TCK(cudaDeviceSynchronize());
         TCK(cudaMemcpy(C, dC, M * N * 4, cudaMemcpyDeviceToHost));
         cudaFree(dA);

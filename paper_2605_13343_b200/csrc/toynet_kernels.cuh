@@ -3,6 +3,7 @@
 // strip pooling, highway scatter / chunk means, FFN input assembly. fp32 activations.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
@@ -80,13 +81,27 @@ __global__ void k_tn_gcn_msg(TnDims g, const unsigned long long* ro, const uint3
     const int lane = threadIdx.x & 31;
     if (row >= g.n) return;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (unsigned long long p = ro[row]; p < ro[row + 1]; ++p) {
-        const float w = float(v[p] / diag[row]);
-        const float4 xj = reinterpret_cast<const float4*>(x + uint64_t(ci[p]) * g.d)[lane];
-        acc.x = fmaf(w, xj.x, acc.x);
-        acc.y = fmaf(w, xj.y, acc.y);
-        acc.z = fmaf(w, xj.z, acc.z);
-        acc.w = fmaf(w, xj.w, acc.w);
+    const unsigned long long p0 = ro[row], p1 = ro[row + 1];
+    const double rdiag = 1.0 / diag[row];  // A_ij / A_ii to within an f64 ulp, then cast to fp32
+    for (unsigned long long pb = p0; pb < p1; pb += 8) {  // the row's (<= 8) gathers in flight together
+        float w[8];
+        float4 xj[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            w[q] = 0.f;
+            xj[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (pb + q < p1) {
+                w[q] = float(v[pb + q] * rdiag);
+                xj[q] = reinterpret_cast<const float4*>(x + uint64_t(ci[pb + q]) * g.d)[lane];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {  // the row's entries in CSR order (toy_net.cpp:305-313)
+            acc.x = fmaf(w[q], xj[q].x, acc.x);
+            acc.y = fmaf(w[q], xj[q].y, acc.y);
+            acc.z = fmaf(w[q], xj[q].z, acc.z);
+            acc.w = fmaf(w[q], xj[q].w, acc.w);
+        }
     }
     reinterpret_cast<float4*>(msg + row * g.d)[lane] = acc;
 }
@@ -165,45 +180,48 @@ __device__ __forceinline__ void edge_mlp(const EdgeMlp& m, uint32_t eh, uint32_t
 }
 
 // Leaf-pair edge biases (toy_net.cpp:371-381), once per forward (reused by every layer), stored
-// key-major: bias[k][h][j][i] (query i fastest) so the attention's lanes (queries) read them
-// coalesced. Coupling = A_{base+i, base+j} looked up in the sorted CSR row.
+// as the reference indexes them — bias[k][h][i][j], query i, key j (toy_net.cpp:95) — in fp16
+// (10-bit mantissa like the tf32 products; the MLP outputs are O(1e3) at most, far inside the
+// fp16 range), pre-multiplied by log2(e) for the attention kernels' exp2 softmax: half the bytes
+// of fp32, one query row's keys contiguous. Coupling = A_{base+i, base+j} looked up in the sorted CSR row.
 __global__ void k_tn_leaf_bias(TnDims g, const uint32_t* order, const unsigned long long* ro,
-                               const uint32_t* ci, const double* v, EdgeMlp mlp, float* bias) {
+                               const uint32_t* ci, const double* v, EdgeMlp mlp, __half* bias) {
     const uint64_t k = blockIdx.y;
-    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // j * L + i
+    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // i * L + j
     const uint64_t base = k * g.L;
-    // the leaf's node coordinates (frame.cpp cell centres, f64), once per CTA instead of four f64
-    // divisions per pair
-    __shared__ double cx[128], cy[128];
+    // the leaf's node coordinates (frame.cpp cell centres, rounded once from f64), once per CTA.
+    // The descriptors are formed in fp32: they feed an fp32 MLP whose output is stored as fp16,
+    // so f64 differences (the reference's) would only cost f64 divisions and square roots
+    __shared__ float cx[128], cy[128];
     for (uint64_t q = threadIdx.x; q < g.L && q < 128; q += blockDim.x) {
         const uint32_t a = order[base + q];
-        cx[q] = (double(a % g.width) + 0.5) / double(g.width);
-        cy[q] = (double(a / g.width) + 0.5) / double(g.height);
+        cx[q] = float((double(a % g.width) + 0.5) / double(g.width));
+        cy[q] = float((double(a / g.width) + 0.5) / double(g.height));
     }
     __syncthreads();
     if (idx >= g.L * g.L) return;
-    const uint64_t j = idx / g.L, i = idx % g.L;
-    double xa, ya, xb, yb;
+    const uint64_t i = idx / g.L, j = idx % g.L;
+    float xa, ya, xb, yb;
     if (g.L <= 128) {
         xa = cx[i]; ya = cy[i]; xb = cx[j]; yb = cy[j];
     } else {
         const uint32_t a = order[base + i], b = order[base + j];
-        xa = (double(a % g.width) + 0.5) / double(g.width); ya = (double(a / g.width) + 0.5) / double(g.height);
-        xb = (double(b % g.width) + 0.5) / double(g.width); yb = (double(b / g.width) + 0.5) / double(g.height);
+        xa = float((double(a % g.width) + 0.5) / double(g.width)); ya = float((double(a / g.width) + 0.5) / double(g.height));
+        xb = float((double(b % g.width) + 0.5) / double(g.width)); yb = float((double(b / g.width) + 0.5) / double(g.height));
     }
-    const double dx = xa - xb, dy = ya - yb, dist = sqrt(dx * dx + dy * dy);
+    const float dx = xa - xb, dy = ya - yb, dist = sqrtf(dx * dx + dy * dy);
     double c = 0.0;
     for (unsigned long long p = ro[base + i]; p < ro[base + i + 1]; ++p)
         if (ci[p] == base + j) c = v[p];
     float out[8];
     if (g.eh == 8 && g.heads == 8) {
-        edge_mlp_t<8, 8>(mlp, float(dx), float(dy), float(dist), float(c), out);
+        edge_mlp_t<8, 8>(mlp, dx, dy, dist, float(c), out);
 #pragma unroll
-        for (int h = 0; h < 8; ++h) bias[((k * 8 + h) * g.L + j) * g.L + i] = out[h];
+        for (int h = 0; h < 8; ++h) bias[((k * 8 + h) * g.L + i) * g.L + j] = __float2half_rn(out[h] * 1.4426950408889634f);
         return;
     }
-    edge_mlp(mlp, g.eh, g.heads, float(dx), float(dy), float(dist), float(c), out);
-    for (uint32_t h = 0; h < g.heads; ++h) bias[((k * g.heads + h) * g.L + j) * g.L + i] = out[h];
+    edge_mlp(mlp, g.eh, g.heads, dx, dy, dist, float(c), out);
+    for (uint32_t h = 0; h < g.heads; ++h) bias[((k * g.heads + h) * g.L + i) * g.L + j] = __float2half_rn(out[h] * 1.4426950408889634f);
 }
 
 // Chunk positions of every tile (toy_net.cpp:382-414 descriptors): pos[m][side][chunk] =
@@ -234,12 +252,12 @@ __global__ void k_tn_tile_pos(TnDims g, const uint32_t* order, double* pos) {
 }
 
 // Tile-pair edge biases (toy_net.cpp:382-414): chunk-mean positions and the mean coupling over
-// each (row chunk a, column chunk b) pair, stored key-major bias[m][h][b][a]. One CTA (64
+// each (row chunk a, column chunk b) pair, stored query-major fp16 bias[m][h][a][b]. One CTA (64
 // threads) per (tile, a): the a-chunk's CSR rows are split over the threads, each bins its
 // column-band entries into a private column of partial sums, combined per bin in thread order.
 __global__ void __launch_bounds__(64) k_tn_tile_bias(TnDims g, const double* pos, const unsigned long long* ro,
                                                     const uint32_t* ci, const double* v, EdgeMlp mlp,
-                                                    float* bias) {
+                                                    __half* bias) {
     const uint64_t m = blockIdx.x, a = blockIdx.y;
     const TileGeom t = tile_geom(g, m);
     __shared__ double part[64][33];
@@ -263,8 +281,8 @@ __global__ void __launch_bounds__(64) k_tn_tile_bias(TnDims g, const double* pos
         c /= ch * ch;
         float out[8];
         edge_mlp(mlp, g.eh, g.heads, float(dx), float(dy), float(dist), float(c), out);
-        for (uint32_t h = 0; h < g.heads; ++h)
-            bias[((m * g.heads + h) * g.Ls + tid) * g.Ls + a] = out[h];
+        for (uint32_t h = 0; h < g.heads; ++h)  // query a (row chunk), key tid (column chunk)
+            bias[((m * g.heads + h) * g.Ls + a) * g.Ls + tid] = __float2half_rn(out[h] * 1.4426950408889634f);
     }
 }
 
@@ -281,13 +299,12 @@ __global__ void k_tn_tile_pool(TnDims g, const float* emb, float* tile_tok) {
 
 // Windowed multi-head attention core (toy_net.cpp:78-125) for one (block, head): T tokens,
 // head dim 16. qkv rows hold [q | k | v] (3d wide). One thread per query row; K/V of the block
-// head staged in shared memory; the key-major bias row j is read once, coalesced across the
-// query lanes; softmax in fp32 with an online (rescaled) running max, i.e. one pass over the
+// head staged in shared memory; the thread's fp16 bias row read along the keys; softmax in fp32 with an online (rescaled) running max, i.e. one pass over the
 // keys. Writes head_out[row, h*16..]. With rowsum_err_bits (trace) a second pass audits
 // max |row sum - 1| of the normalised probabilities.
 template <int T>
 __global__ void __launch_bounds__(T) k_tn_attention(uint32_t d, uint32_t heads, const float* qkv,
-                                                    const float* bias, float* head_out,
+                                                    const __half* bias, float* head_out,
                                                     unsigned int* rowsum_err_bits) {
     const uint64_t blk = blockIdx.x;
     const uint32_t h = blockIdx.y, i = threadIdx.x;
@@ -302,7 +319,7 @@ __global__ void __launch_bounds__(T) k_tn_attention(uint32_t d, uint32_t heads, 
         vs[i][c] = rowp[(2 * d + h * HD) / 4 + c];
     }
     __syncthreads();
-    const float* b = bias + (blk * heads + h) * T * T + i;  // column i of the key-major bias
+    const __half* b = bias + ((blk * heads + h) * T + i) * T;  // query row i of the bias
     const float scale = 0.25f;  // 1/sqrt(16)
     auto logit = [&](int j) {
         float dot = 0.f;
@@ -314,7 +331,7 @@ __global__ void __launch_bounds__(T) k_tn_attention(uint32_t d, uint32_t heads, 
             dot = fmaf(q4[c].z, k.z, dot);
             dot = fmaf(q4[c].w, k.w, dot);
         }
-        return fmaf(dot, scale, __ldg(b + j * T));
+        return fmaf(dot, scale, __half2float(b[j]) * 0.69314718055994531f);  // bias stored x log2(e)
     };
     float mx = -CUDART_INF_F, sum = 0.f;
     float4 acc[HD / 4];
@@ -392,6 +409,52 @@ __global__ void k_tn_highway(TnDims g, const float* leaf_tok, const float* tile_
     reinterpret_cast<float4*>(col_hw + uint64_t(i) * g.d)[lane] = c;
 }
 
+// The same scatter by level-0 chunks (c0 = L / L_s nodes share every ancestor's covering tile
+// token): one warp per chunk sums the D ancestors' tokens into a row-side and a column-side
+// accumulator (depth dd: the chunk's tile m, half and token from the chunk index at level
+// l = D - 1 - dd), then writes t + acc for each of its c0 nodes — D gathers per c0 nodes instead
+// of per node.
+// Also the leaf half of glob_hw (toy_net.cpp:458): the CTA's column sums of the leaf tokens it
+// reads anyway, one fixed-order partial per CTA in colsum_part (finished by k_tn_colsum_finish).
+__global__ void __launch_bounds__(256) k_tn_highway_chunks(TnDims g, uint32_t c0, const float* leaf_tok,
+                                                           const float* tile_tok, float* row_hw, float* col_hw,
+                                                           float* colsum_part) {
+    __shared__ float4 wsum[8][32];
+    const uint64_t j0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float4 ts = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (j0 * c0 < g.n) {
+    const uint32_t D = uint32_t(g.D);
+    float4 ar = make_float4(0.f, 0.f, 0.f, 0.f), ac = ar;
+#pragma unroll 4
+    for (uint32_t l = 0; l < D; ++l) {  // all gathers independent
+        const uint64_t jl = j0 >> l, it = jl / (2 * g.Ls), a = jl % g.Ls;
+        const uint32_t dd = D - 1 - l;
+        const uint64_t m = ((uint64_t(1) << dd) - 1) + it;
+        const float4 e = __ldg(reinterpret_cast<const float4*>(tile_tok + (m * g.Ls + a) * g.d) + lane);
+        float4& dst = ((jl / g.Ls) & 1) ? ac : ar;
+        dst.x += e.x; dst.y += e.y; dst.z += e.z; dst.w += e.w;
+    }
+    for (uint32_t q = 0; q < c0; ++q) {
+        const uint64_t i = j0 * c0 + q;
+        const float4 t = reinterpret_cast<const float4*>(leaf_tok + i * g.d)[lane];
+        reinterpret_cast<float4*>(row_hw + i * g.d)[lane] = make_float4(t.x + ar.x, t.y + ar.y, t.z + ar.z, t.w + ar.w);
+        reinterpret_cast<float4*>(col_hw + i * g.d)[lane] = make_float4(t.x + ac.x, t.y + ac.y, t.z + ac.z, t.w + ac.w);
+        ts.x += t.x; ts.y += t.y; ts.z += t.z; ts.w += t.w;
+    }
+    }
+    wsum[warp][lane] = ts;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float4 a = wsum[0][threadIdx.x];
+        for (int w = 1; w < 8; ++w) {
+            const float4 b = wsum[w][threadIdx.x];
+            a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+        }
+        reinterpret_cast<float4*>(colsum_part + uint64_t(blockIdx.x) * g.d)[threadIdx.x] = a;
+    }
+}
+
 // glob_hw = sum of every leaf token + every tile token (toy_net.cpp:458, 474). Column sums via
 // per-block partials (deterministic), then a single-block finish.
 __global__ void k_tn_colsum_partial(uint64_t rows, uint32_t d, const float* x, float* partial) {
@@ -440,33 +503,150 @@ __global__ void k_tn_colsum_finish(uint32_t nparts, uint32_t d, const float* par
     if (lane == 0) out[c] = float(s);
 }
 
-// FFN input rows for leaves (toy_net.cpp:421-436, 515-517): [LN(tok) | row_hw | col_hw | glob],
-// LN already written into columns 0..d-1 by k_tn_layernorm.
-__global__ void k_tn_ffn_input_leaf(TnDims g, const float* row_hw, const float* col_hw,
-                                    const float* glob, float* A) {
-    const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (i >= g.n) return;
-    float4* a = reinterpret_cast<float4*>(A + i * 4 * g.d);
-    a[32 + lane] = reinterpret_cast<const float4*>(row_hw + i * g.d)[lane];
-    a[64 + lane] = reinterpret_cast<const float4*>(col_hw + i * g.d)[lane];
-    a[96 + lane] = reinterpret_cast<const float4*>(glob)[lane];
-}
-
-// ... and for tile tokens (toy_net.cpp:519-537): chunk means of row_hw over the token's row
-// chunk and of col_hw over its column chunk.
-__global__ void k_tn_ffn_input_tile(TnDims g, const float* row_hw, const float* col_hw,
-                                    const float* glob, float* A) {
+// Tile FFN strip means walked chunk by chunk (toy_net.cpp:519-532), for partitions whose chunks
+// do not nest as powers of two (L < L_s); the production shapes use k_tn_tile_means_pyr.
+__global__ void k_tn_tile_means_walk(TnDims g, const float* row_hw, const float* col_hw, float* rmean,
+                                     float* cmean) {
     const uint64_t m = blockIdx.x, tok = blockIdx.y;
     const TileGeom t = tile_geom(g, m);
-    float* a = A + (m * g.Ls + tok) * 4 * g.d;
     for (uint32_t c = threadIdx.x; c < g.d; c += blockDim.x) {
         const float rs = strided_sum(row_hw + (t.row0 + tok * t.chunk) * g.d + c, t.chunk, g.d);
         const float cs = strided_sum(col_hw + (t.col0 + tok * t.chunk) * g.d + c, t.chunk, g.d);
-        a[g.d + c] = rs / float(t.chunk);
-        a[2 * g.d + c] = cs / float(t.chunk);
-        a[3 * g.d + c] = glob[c];
+        rmean[(m * g.Ls + tok) * g.d + c] = rs / float(t.chunk);
+        cmean[(m * g.Ls + tok) * g.d + c] = cs / float(t.chunk);
     }
+}
+
+// ---- chunk-sum pyramids: O(N d) strip pooling and chunk means --------------------------
+// Every tile of span s leaves splits its row and column halves into L_s chunks of c = s L / L_s
+// consecutive nodes (toy_net.cpp:352-353). Chunk sizes are c0 2^l (c0 = L / L_s, l = log2 s) and
+// chunks nest: level l of a pyramid holds the sums of c0 2^l consecutive rows, level l + 1 the
+// pairwise sums of level l. Tile pooling (toy_net.cpp:348-365), the tile FFN's strip means
+// (:519-537) and the tile descriptors' chunk positions (:382-414) then read one pyramid entry per
+// (tile, token) instead of walking the chunk: O(N d) per pyramid instead of O(N d log K).
+template <class T>
+struct PyrLevels {
+    T* lev[24];
+};
+// One launch produces levels l0 .. l0 + q: block b of (group << q) <= 32 source rows; a thread
+// owns VW consecutive channels of one block, loads all its rows first (up to 32 vector loads in
+// flight), then forms level l0 (sums of `group` rows) and each level above as pairwise sums.
+__device__ __forceinline__ float4 vadd(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ double2 vadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+template <class T, class V, uint32_t group>
+__global__ void __launch_bounds__(128) k_tn_pyramid(const T* __restrict__ src, uint64_t nblocks, uint32_t C,
+                                                    uint32_t q, PyrLevels<T> out, uint32_t l0) {
+    constexpr uint32_t VW = sizeof(V) / sizeof(T);
+    const uint32_t cv = C / VW;
+    const uint64_t gid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t blk = gid / cv;
+    const uint32_t c = uint32_t(gid % cv);
+    if (blk >= nblocks) return;
+    const uint32_t rows = group << q;
+    const V* s = reinterpret_cast<const V*>(src) + blk * rows * cv + c;
+    V r[32];
+#pragma unroll
+    for (uint32_t i = 0; i < 32; ++i)
+        if (i < rows) r[i] = s[uint64_t(i) * cv];
+    // level l0: r[j] = sum of rows j*group .. j*group+group-1 (in order), in place
+    const uint32_t n0 = 1u << q;
+#pragma unroll
+    for (uint32_t j = 0; j < 32; ++j) {
+        if (j < n0) {
+            V a = r[j * group];
+#pragma unroll
+            for (uint32_t gg = 1; gg < group; ++gg) a = vadd(a, r[j * group + gg]);
+            r[j] = a;  // j * group >= j: reads ahead of the writes
+        }
+    }
+    for (uint32_t l = 0; l <= q; ++l) {
+        const uint32_t cnt = n0 >> l;
+        V* o = reinterpret_cast<V*>(out.lev[l0 + l]) + ((blk << q) >> l) * cv + c;
+#pragma unroll
+        for (uint32_t j = 0; j < 32; ++j)
+            if (j < cnt) o[uint64_t(j) * cv] = r[j];
+        if (l < q) {
+#pragma unroll
+            for (uint32_t j = 0; j < 16; ++j)
+                if (j < cnt / 2) r[j] = vadd(r[2 * j], r[2 * j + 1]);
+        }
+    }
+}
+
+// Tile token (m, a) from the embedding pyramid: 0.5 (row chunk sum + column chunk sum) / c
+// (toy_net.cpp:356-364). lev_shift = log2(L / L_s).
+// One warp per tile token (d = 128: a float4 per lane).
+__global__ void k_tn_tile_pool_pyr(TnDims g, PyrLevels<float> P, uint32_t lev_shift, float* tile_tok) {
+    const uint64_t tok = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (tok >= g.M * g.Ls) return;
+    const uint64_t m = tok / g.Ls, a = tok % g.Ls;
+    const TileGeom t = tile_geom(g, m);
+    int l = 0;
+    while ((uint64_t(1) << (l + lev_shift)) < t.chunk) ++l;
+    const float4 r = reinterpret_cast<const float4*>(P.lev[l] + (t.row0 / t.chunk + a) * g.d)[lane];
+    const float4 c = reinterpret_cast<const float4*>(P.lev[l] + (t.col0 / t.chunk + a) * g.d)[lane];
+    const float inv = 1.f / float(t.chunk);  // a power of two: exact
+    reinterpret_cast<float4*>(tile_tok + tok * g.d)[lane] =
+        make_float4(0.5f * (r.x + c.x) * inv, 0.5f * (r.y + c.y) * inv, 0.5f * (r.z + c.z) * inv, 0.5f * (r.w + c.w) * inv);
+}
+
+// Tile FFN strip means (toy_net.cpp:519-532): rmean = row_hw chunk sum / c over the token's row
+// chunk, cmean = col_hw chunk sum / c over its column chunk; rows of the tile FFN's K-sliced
+// input (sources 1 and 2).
+__global__ void k_tn_tile_means_pyr(TnDims g, PyrLevels<float> Pr, PyrLevels<float> Pc, uint32_t lev_shift,
+                                    float* rmean, float* cmean) {
+    const uint64_t tok = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;  // warp per tile token
+    const int lane = threadIdx.x & 31;
+    if (tok >= g.M * g.Ls) return;
+    const uint64_t m = tok / g.Ls, a = tok % g.Ls;
+    const TileGeom t = tile_geom(g, m);
+    int l = 0;
+    while ((uint64_t(1) << (l + lev_shift)) < t.chunk) ++l;
+    const float4 r = reinterpret_cast<const float4*>(Pr.lev[l] + (t.row0 / t.chunk + a) * g.d)[lane];
+    const float4 c = reinterpret_cast<const float4*>(Pc.lev[l] + (t.col0 / t.chunk + a) * g.d)[lane];
+    const float inv = 1.f / float(t.chunk);
+    reinterpret_cast<float4*>(rmean + tok * g.d)[lane] = make_float4(r.x * inv, r.y * inv, r.z * inv, r.w * inv);
+    reinterpret_cast<float4*>(cmean + tok * g.d)[lane] = make_float4(c.x * inv, c.y * inv, c.z * inv, c.w * inv);
+}
+
+// Node positions (frame.cpp cell centres, toy_net.cpp:333-338) as f64 pairs, the input of the
+// position pyramid.
+__global__ void k_tn_positions(TnDims g, const uint32_t* order, double* pos) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= g.n) return;
+    const uint32_t id = order[i];
+    pos[2 * i] = (double(id % g.width) + 0.5) / double(g.width);
+    pos[2 * i + 1] = (double(id / g.width) + 0.5) / double(g.height);
+}
+// Chunk position sums of every tile from the position pyramid, in k_tn_tile_bias's layout
+// pos[m][side][chunk][x|y].
+__global__ void k_tn_tile_pos_pyr(TnDims g, PyrLevels<double> P, uint32_t lev_shift, double* pos) {
+    const uint64_t m = blockIdx.x;
+    const TileGeom t = tile_geom(g, m);
+    int l = 0;
+    while ((uint64_t(1) << (l + lev_shift)) < t.chunk) ++l;
+    for (uint32_t q = threadIdx.x; q < 2 * g.Ls; q += blockDim.x) {
+        const uint32_t side = q / g.Ls, a = q % g.Ls;
+        const double* e = P.lev[l] + ((side ? t.col0 : t.row0) / t.chunk + a) * 2;
+        pos[((m * 2 + side) * g.Ls + a) * 2 + 0] = e[0];
+        pos[((m * 2 + side) * g.Ls + a) * 2 + 1] = e[1];
+    }
+}
+
+// The FFN's glob slice as a bias (toy_net.cpp:428-430: every row of a layer's FFN input carries
+// the same glob_hw in columns [3d, 4d)): bias[o] = sum_i glob[i] W1[3d + i][o], once per layer
+// and stream instead of a K = d slice of every row's product. w1t is W1^T (4d x 4d, out x in).
+__global__ void k_tn_glob_bias(uint32_t d, const float* glob, const float* w1t_leaf, const float* w1t_tile,
+                               float* bias_leaf, float* bias_tile) {
+    const uint32_t o = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;  // warp per output
+    if (o >= 4 * d) return;
+    const float* w = (blockIdx.y ? w1t_tile : w1t_leaf) + uint64_t(o) * 4 * d + 3 * d;
+    double a = 0.0;
+    for (uint32_t i = lane; i < d; i += 32) a = fma(double(glob[i]), double(w[i]), a);
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) a += __shfl_xor_sync(0xffffffffu, a, s);
+    if (lane == 0) (blockIdx.y ? bias_tile : bias_leaf)[o] = float(a);
 }
 
 // ---- global statistics of a device frame (toy_net.cpp:232-268) --------------------------
