@@ -13,9 +13,10 @@
 //    streams the operands ahead.
 //  * Epilogue, eight warps: warp e reads TMEM lanes 32 (e mod 4) .. +31 and every other 32-column
 //    chunk; each 32 x 32 chunk is transposed through shared memory so the functor's stores are
-//    coalesced rows (Epi::apply32(row0, col, v[32], nrows): lane = column, 32 rows at once so
-//    read-modify-write functors keep all their loads in flight). Epi::kWholeRow (BN = N = 128):
-//    warps 0-3 hold whole rows — residual add + LayerNorm of the new row, written coalesced.
+//    coalesced rows (Epi::apply8(row0, col, v[8], ncols, M): lane = 4 columns of rows row0 + 4 i,
+//    eight rows at once so read-modify-write functors keep all their loads in flight). Epi::kWholeRow (BN = N = 128):
+//    residual add + LayerNorm of the new row; a warp pair splits each row's columns, the residual
+//    rows arrive by cp.async while the MMAs run, the row statistics meet in shared memory.
 #pragma once
 
 #include "gemm_tcgen05.cuh"
@@ -28,7 +29,7 @@ constexpr int kPgThreads = (kPgEpiWarps + 2) * 32;  // + TMA producer + MMA issu
 template <int BN, bool WHOLE>
 struct PgCfg {
     static constexpr int kABytes = kGemmBM * kGemmBK * 4, kBBytes = BN * kGemmBK * 4;
-    static constexpr int kStgFloats = WHOLE ? 4 * 32 * 129 : kPgEpiWarps * 32 * 33;
+    static constexpr int kStgFloats = WHOLE ? kPgEpiWarps * 32 * 65 + 2 * 4 * 2 * 32 : kPgEpiWarps * 32 * 32;
     static constexpr int kBudget = 200 * 1024 - kStgFloats * 4;
     static constexpr int kStages0 = kBudget / (kABytes + kBBytes);
     static constexpr int kStages = kStages0 > 6 ? 6 : kStages0;
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(kPgThreads, 1)
     constexpr bool WHOLE = Epi::kWholeRow;
     using Cfg = PgCfg<BN, WHOLE>;
     constexpr int S = Cfg::kStages;
-    constexpr int kEpiActive = WHOLE ? 4 : kPgEpiWarps;  // warps arriving on tempty
+    constexpr int kEpiActive = kPgEpiWarps;  // warps arriving on tempty
     extern __shared__ __align__(1024) unsigned char praw[];
     PgSmem<BN, WHOLE>& sm = *reinterpret_cast<PgSmem<BN, WHOLE>*>((reinterpret_cast<uintptr_t>(praw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -142,27 +143,44 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                 mma_commit(&sm.tfull[b]);
             }
         }
-    } else if (!WHOLE || warp < 4) {
-        // epilogue: warp e owns TMEM lanes (rows) 32 (e mod 4) .. +31, column chunks e / 4 + 2 i
-        const int quad = warp & 3, half = WHOLE ? 0 : warp >> 2;
-        float* stg = sm.stg + (WHOLE ? quad * 32 * 129 : warp * 32 * 33);
+    } else {
+        // epilogue: warp e owns TMEM lanes (rows) 32 (e mod 4) .. +31; chunked: column chunks
+        // e / 4 + 2 i; whole-row: columns [64 (e / 4), +64)
+        const int quad = warp & 3, half = warp >> 2;
+        float* stg = sm.stg + (WHOLE ? warp * 32 * 65 : warp * 32 * 32);
         uint32_t tl = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
             const uint32_t b = tl & 1, use = tl >> 1;
             const int m0 = (t / ntl) * kGemmBM, n0 = (t % ntl) * BN;
             const int rbase = m0 + quad * 32;  // first row of this warp's 32
-            mbar_wait(&sm.tfull[b], use & 1);
-            tc_fence_after();
             const uint32_t tacc = tmem + b * Cfg::kAccCols + (uint32_t(quad * 32) << 16);
             if constexpr (WHOLE) {
                 static_assert(BN == 128, "whole-row epilogues need the full 128-column row in one tile");
-                // thread = row rbase + lane: its 128 accumulator columns
-                float v[128];
+                // the warp pair (quad, half 0 / 1) splits each row's 128 columns; row statistics
+                // are combined through `red` with a 64-thread named barrier per quad
+                float* red = sm.stg + kPgEpiWarps * 32 * 65 + quad * 2 * 2 * 32;  // [stat][half][row]
+                const int c0 = 64 * half;
+                // residual rows of this tile -> staging, asynchronously (cp.async 4 B, coalesced),
+                // while the accumulator is still being computed
+                for (int rr = 0; rr < 32; ++rr) {
+                    const int row = rbase + rr;
+                    if (row < M) {
 #pragma unroll
-                for (int c = 0; c < 128; c += 32) {
+                        for (int q = 0; q < 2; ++q)
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(stg + rr * 65 + 32 * q + lane)),
+                                         "l"(epi.x + uint64_t(row) * 128 + c0 + 32 * q + lane)
+                                         : "memory");
+                    }
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                mbar_wait(&sm.tfull[b], use & 1);
+                tc_fence_after();
+                float v[64];  // thread = row rbase + lane, columns c0 .. c0 + 63
+#pragma unroll
+                for (int c = 0; c < 64; c += 32) {
                     uint32_t u0[16], u1[16];
-                    tmem_ld16_nowait(tacc + uint32_t(c), u0);
-                    tmem_ld16_nowait(tacc + uint32_t(c + 16), u1);
+                    tmem_ld16_nowait(tacc + uint32_t(c0 + c), u0);
+                    tmem_ld16_nowait(tacc + uint32_t(c0 + c + 16), u1);
                     tmem_wait_ld();
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
@@ -175,58 +193,51 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                 if (lane == 0) mbar_arrive(&sm.tempty[b]);
                 if (epi.gelu) {
 #pragma unroll
-                    for (int j = 0; j < 128; ++j) v[j] = epi.act(v[j]);
+                    for (int j = 0; j < 64; ++j) v[j] = epi.act(v[j]);
                 }
-                // 1. the accumulator rows into the staging rows (thread = row, conflict-free pitch)
-#pragma unroll
-                for (int j = 0; j < 128; ++j) stg[lane * 129 + j] = v[j];
+                asm volatile("cp.async.wait_all;" ::: "memory");
                 __syncwarp();
-                // 2. residual rows in, coalesced (lane = column), eight rows of loads in flight
-#pragma unroll 1
-                for (int r0 = 0; r0 < 32; r0 += 8) {
-                    float xr[8][4];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int row = rbase + r0 + i;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            xr[i][q] = row < M ? epi.x[uint64_t(row) * 128 + 32 * q + lane] : 0.f;
-                    }
-#pragma unroll
-                    for (int i = 0; i < 8; ++i)
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) stg[(r0 + i) * 129 + 32 * q + lane] += xr[i][q];
-                }
-                __syncwarp();
-                // 3. row statistics, thread = row (two-pass, toy_net.cpp:28-41)
                 float s = 0.f;
 #pragma unroll
-                for (int j = 0; j < 128; j += 4)
-                    s += (stg[lane * 129 + j] + stg[lane * 129 + j + 1]) + (stg[lane * 129 + j + 2] + stg[lane * 129 + j + 3]);
-                const float mean = s * (1.f / 128.f);
+                for (int j = 0; j < 64; j += 4) {
+                    v[j] += stg[lane * 65 + j];
+                    v[j + 1] += stg[lane * 65 + j + 1];
+                    v[j + 2] += stg[lane * 65 + j + 2];
+                    v[j + 3] += stg[lane * 65 + j + 3];
+                    s += (v[j] + v[j + 1]) + (v[j + 2] + v[j + 3]);
+                }
+                red[half * 32 + lane] = s;
+                named_bar_sync(1 + quad, 64);
+                const float mean = (red[lane] + red[32 + lane]) * (1.f / 128.f);
                 float qs = 0.f;
 #pragma unroll
-                for (int j = 0; j < 128; ++j) {
-                    const float c = stg[lane * 129 + j] - mean;
-                    qs = fmaf(c, c, qs);
+                for (int j = 0; j < 64; ++j) {
+                    const float cdev = v[j] - mean;
+                    qs = fmaf(cdev, cdev, qs);
+                    stg[lane * 65 + j] = v[j];
                 }
-                const float inv = 1.f / sqrtf(qs * (1.f / 128.f) + 1e-5f);
-                // 4. new rows and their LayerNorm out, coalesced
+                red[64 + half * 32 + lane] = qs;
+                named_bar_sync(1 + quad, 64);
+                const float inv = 1.f / sqrtf((red[64 + lane] + red[96 + lane]) * (1.f / 128.f) + 1e-5f);
+                __syncwarp();
+                // new rows and their LayerNorm out, coalesced
 #pragma unroll 4
                 for (int rr = 0; rr < 32; ++rr) {
                     const int row = rbase + rr;
                     const float mr = __shfl_sync(0xffffffffu, mean, rr), ir = __shfl_sync(0xffffffffu, inv, rr);
                     if (row < M) {
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const float xv = stg[rr * 129 + 32 * q + lane];
-                            epi.x[uint64_t(row) * 128 + 32 * q + lane] = xv;
-                            epi.ln[uint64_t(row) * 128 + 32 * q + lane] = (xv - mr) * ir;
+                        for (int q = 0; q < 2; ++q) {
+                            const float xv = stg[rr * 65 + 32 * q + lane];
+                            epi.x[uint64_t(row) * 128 + c0 + 32 * q + lane] = xv;
+                            epi.ln[uint64_t(row) * 128 + c0 + 32 * q + lane] = (xv - mr) * ir;
                         }
                     }
                 }
-                __syncwarp();
+                named_bar_sync(1 + quad, 64);  // red[] reads done before the next tile writes it
             } else {
+                mbar_wait(&sm.tfull[b], use & 1);
+                tc_fence_after();
                 constexpr int nch = (BN + 31) / 32;
 #pragma unroll 1
                 for (int ch = half; ch < nch; ch += 2) {
@@ -240,18 +251,32 @@ __global__ void __launch_bounds__(kPgThreads, 1)
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&sm.tempty[b]);
                     }
+                    // 32 x 32 chunk through shared memory, 16-byte granules XOR-swizzled by row
+                    // (conflict-free float4 writes by rows and reads by columns): thread = row
+                    // writes its 32 columns; lane l then holds columns 4 (l mod 8) .. +3 of rows
+                    // l / 8 + 4 i, so each warp store covers four full 128-byte row segments
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        stg[lane * 33 + j] = __uint_as_float(u0[j]);
-                        stg[lane * 33 + 16 + j] = c + 16 < BN ? __uint_as_float(u1[j]) : 0.f;
+                    for (int q = 0; q < 4; ++q) {
+                        *reinterpret_cast<float4*>(stg + lane * 32 + ((q ^ (lane & 7)) << 2)) =
+                            make_float4(__uint_as_float(u0[4 * q]), __uint_as_float(u0[4 * q + 1]),
+                                        __uint_as_float(u0[4 * q + 2]), __uint_as_float(u0[4 * q + 3]));
+                        *reinterpret_cast<float4*>(stg + lane * 32 + (((q + 4) ^ (lane & 7)) << 2)) =
+                            c + 16 < BN ? make_float4(__uint_as_float(u1[4 * q]), __uint_as_float(u1[4 * q + 1]),
+                                                      __uint_as_float(u1[4 * q + 2]), __uint_as_float(u1[4 * q + 3]))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
                     __syncwarp();
-                    const int col = n0 + c + lane;
-                    float cv[32];  // column `col` of this warp's 32 rows
+                    const int cq = lane & 7, r0 = lane >> 3;
+                    float4 cv[8];
 #pragma unroll
-                    for (int rr = 0; rr < 32; ++rr) cv[rr] = stg[rr * 33 + lane];
+                    for (int i = 0; i < 8; ++i) {
+                        const int rr = r0 + 4 * i;
+                        cv[i] = *reinterpret_cast<const float4*>(stg + rr * 32 + ((cq ^ (rr & 7)) << 2));
+                    }
                     __syncwarp();
-                    if (col < N && c + lane < BN) epi.apply32(rbase, col, cv, M - rbase < 32 ? M - rbase : 32);
+                    const int col = n0 + c + 4 * cq;
+                    const int ncv = min(min(N - col, BN - (c + 4 * cq)), 4);  // valid columns of the float4
+                    if (ncv > 0) epi.apply8(rbase + r0, col, cv, ncv, M);
                 }
                 if (half >= nch) {  // no chunk of this parity (BN <= 32): still release the buffer
                     __syncwarp();

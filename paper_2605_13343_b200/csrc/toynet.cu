@@ -116,41 +116,74 @@ CUtensorMap tmap(const float* p, uint64_t rows, uint64_t cols, uint64_t ld, uint
     return m;
 }
 
-// ---- GEMM epilogues (k_pgemm_tf32): apply1(row, col, v) with lane = column (coalesced) -----
-struct EpiStore {  // out[row, col] = act(v + bias)
+// ---- GEMM epilogues (k_pgemm_tf32): apply8(row0, col, v[8], ncols, M) — columns col .. col+3
+// (ncols valid) of rows row0 + 4 i, i < 8 (rows >= M skipped); coalesced across the warp ---------
+__device__ __forceinline__ float4 f4_act(float4 v, float4 b, bool gelu) {
+    v = make_float4(v.x + b.x, v.y + b.y, v.z + b.z, v.w + b.w);
+    if (gelu) v = make_float4(gelu_fast(v.x), gelu_fast(v.y), gelu_fast(v.z), gelu_fast(v.w));
+    return v;
+}
+__device__ __forceinline__ float4 f4_bias(const float* bias, int col, int ncols) {
+    if (!bias) return make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ncols == 4) return *reinterpret_cast<const float4*>(bias + col);
+    float b[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < ncols; ++j) b[j] = bias[col + j];
+    return make_float4(b[0], b[1], b[2], b[3]);
+}
+__device__ __forceinline__ void f4_store(float* o, float4 v, int ncols) {
+    if (ncols == 4) {
+        *reinterpret_cast<float4*>(o) = v;
+    } else {
+        const float e[4] = {v.x, v.y, v.z, v.w};
+        for (int j = 0; j < ncols; ++j) o[j] = e[j];
+    }
+}
+template <bool GELU>
+struct EpiStore {  // out[row, col] = act(v + bias); ld a multiple of 4
     static constexpr bool kWholeRow = false;
     float* out;
     uint32_t ld;
     const float* bias;
-    int gelu;
-    __device__ __forceinline__ void apply32(int row0, int col, float (&v)[32], int nrows) const {
-        const float b = bias ? bias[col] : 0.f;
-        float* o = out + uint64_t(row0) * ld + col;
+    __device__ __forceinline__ void apply8(int row0, int col, float4 (&v)[8], int ncols, int M) const {
+        const float4 b = f4_bias(bias, col, ncols);
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) {
-            float x = v[rr] + b;
-            if (gelu) x = gelu_f(x);
-            if (rr < nrows) o[uint64_t(rr) * ld] = x;
+        for (int i = 0; i < 8; ++i) {
+            const int row = row0 + 4 * i;
+            if (row < M) f4_store(out + uint64_t(row) * ld + col, f4_act(v[i], b, GELU), ncols);
         }
     }
 };
+template <bool GELU>
 struct EpiResidual {  // out[row, col] += act(v + bias)
     static constexpr bool kWholeRow = false;
     float* out;
     uint32_t ld;
     const float* bias;
-    int gelu;
-    __device__ __forceinline__ void apply32(int row0, int col, float (&v)[32], int nrows) const {
-        const float b = bias ? bias[col] : 0.f;
-        float* o = out + uint64_t(row0) * ld + col;
-        float a[32];
+    __device__ __forceinline__ void apply8(int row0, int col, float4 (&v)[8], int ncols, int M) const {
+        const float4 b = f4_bias(bias, col, ncols);
+        float4 a[8];
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) a[rr] = rr < nrows ? o[uint64_t(rr) * ld] : 0.f;
+        for (int i = 0; i < 8; ++i) {  // all residual loads first
+            const int row = row0 + 4 * i;
+            a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (row < M) {
+                const float* o = out + uint64_t(row) * ld + col;
+                if (ncols == 4) {
+                    a[i] = *reinterpret_cast<const float4*>(o);
+                } else {
+                    float e[4] = {0.f, 0.f, 0.f, 0.f};
+                    for (int j = 0; j < ncols; ++j) e[j] = o[j];
+                    a[i] = make_float4(e[0], e[1], e[2], e[3]);
+                }
+            }
+        }
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) {
-            float x = v[rr] + b;
-            if (gelu) x = gelu_f(x);
-            if (rr < nrows) o[uint64_t(rr) * ld] = a[rr] + x;
+        for (int i = 0; i < 8; ++i) {
+            const int row = row0 + 4 * i;
+            const float4 x = f4_act(v[i], b, GELU);
+            if (row < M)
+                f4_store(out + uint64_t(row) * ld + col, make_float4(a[i].x + x.x, a[i].y + x.y, a[i].z + x.z, a[i].w + x.w),
+                         ncols);
         }
     }
 };
@@ -163,7 +196,7 @@ struct EpiResidualLN {
     float* x;
     float* ln;
     int gelu;
-    __device__ __forceinline__ float act(float v) const { return gelu_f(v); }
+    __device__ __forceinline__ float act(float v) const { return gelu_fast(v); }
 };
 // Decoder heads of leaf node `row` (toy_net.cpp:549-567): columns [0, L_s) -> Ũ_k row,
 // [L_s, 2 L_s) -> Ṽ_k row, 2 L_s -> gate. Cast to float as the reference does.
@@ -172,19 +205,20 @@ struct EpiLeafHeads {
     float* out;
     uint32_t lL, lLs;  // log2 L, log2 L_s (powers of two, as the GPU forward requires)
     uint64_t bridge_base, gate_base;
-    __device__ __forceinline__ void apply32(int row0, int col, float (&v)[32], int nrows) const {
-        const uint32_t c = uint32_t(col), Ls = 1u << lLs, L = 1u << lL;
-        if (c < 2 * Ls) {
-            const uint64_t off = c < Ls ? c : uint64_t(L) * Ls + (c - Ls);  // Ũ_k or Ṽ_k column
+    __device__ __forceinline__ void apply8(int row0, int col, float4 (&v)[8], int ncols, int M) const {
+        const uint32_t Ls = 1u << lLs, L = 1u << lL;
 #pragma unroll
-            for (int rr = 0; rr < 32; ++rr) {
-                const uint64_t row = uint64_t(row0 + rr), k = row >> lL, r = row & (L - 1);
-                if (rr < nrows) out[bridge_base + k * (2ull * L * Ls) + r * Ls + off] = v[rr];
+        for (int i = 0; i < 8; ++i) {
+            const uint64_t row = uint64_t(row0 + 4 * i), k = row >> lL, r = row & (L - 1);
+            if (row >= uint64_t(M)) continue;
+            const float e[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+            float* bu = out + bridge_base + k * (2ull * L * Ls) + r * Ls;
+            for (int j = 0; j < ncols; ++j) {
+                const uint32_t c = uint32_t(col + j);
+                if (c < Ls) bu[c] = e[j];
+                else if (c < 2 * Ls) bu[uint64_t(L) * Ls + (c - Ls)] = e[j];
+                else if (c == 2 * Ls) out[gate_base + row] = e[j];
             }
-        } else if (c == 2 * Ls) {
-#pragma unroll
-            for (int rr = 0; rr < 32; ++rr)
-                if (rr < nrows) out[gate_base + uint64_t(row0 + rr)] = v[rr];
         }
     }
 };
@@ -195,12 +229,17 @@ struct EpiTileHeads {
     float* out;
     uint32_t lLs;  // log2 L_s
     uint64_t tile_base;
-    __device__ __forceinline__ void apply32(int row0, int col, float (&v)[32], int nrows) const {
-        const uint32_t c = uint32_t(col), Ls = 1u << lLs, rk = Ls >> 1;
-        if (c >= 2 * rk) return;
-        for (int rr = 0; rr < nrows; ++rr) {
-            const uint64_t row = uint64_t(row0 + rr), m = row >> lLs, tok = row & (Ls - 1);
-            out[tile_base + m * Ls * Ls + (c < rk ? 0 : Ls * rk) + tok * rk + (c % rk)] = v[rr];
+    __device__ __forceinline__ void apply8(int row0, int col, float4 (&v)[8], int ncols, int M) const {
+        const uint32_t Ls = 1u << lLs, rk = Ls >> 1;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint64_t row = uint64_t(row0 + 4 * i), m = row >> lLs, tok = row & (Ls - 1);
+            if (row >= uint64_t(M)) continue;
+            const float e[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+            for (int j = 0; j < ncols; ++j) {
+                const uint32_t c = uint32_t(col + j);
+                if (c < 2 * rk) out[tile_base + m * Ls * Ls + (c < rk ? 0 : Ls * rk) + tok * rk + (c % rk)] = e[j];
+            }
         }
     }
 };
@@ -512,15 +551,51 @@ static void toynet_run(ToynetModel* mdl, cudaStream_t st, uint64_t n, uint64_t w
     const PyrLevels<float> Pr = levels(pyr_r), Pc = levels(pyr_c);
 
     const unsigned nb = unsigned((n + 255) / 256), nw = unsigned((n * 32 + 255) / 256);
+    cudaStream_t st2 = mdl->side;
+    auto fork = [&] {  // st2 continues from st's current point
+        TCK(cudaEventRecord(mdl->ev_fork, st));
+        TCK(cudaStreamWaitEvent(st2, mdl->ev_fork, 0));
+    };
+    auto join = [&] {  // st waits for st2's work so far
+        TCK(cudaEventRecord(mdl->ev_join, st2));
+        TCK(cudaStreamWaitEvent(st, mdl->ev_join, 0));
+    };
+    uint32_t lL = 0, lLs = 0;
+    while ((1ull << lL) < L) ++lL;
+    while ((1ull << lLs) < Ls) ++lLs;
     TCK(cudaEventRecord(mdl->ev0, st));
+    // ---- edge biases (toy_net.cpp:367-415) depend on the frame only: on st2, beside the encoder
+    fork();
+    k_tn_leaf_bias<<<dim3(unsigned((L * L + 255) / 256), unsigned(lay.k)), 256, 0, st2>>>(
+        g, lL, d_order, d_ro, d_ci, d_v, mdl->le, leaf_bias);
+    if (lay.m) {
+        if (pyr) {
+            auto* pos = mdl->buf<double>(33, n * 2);
+            auto* ppos = mdl->buf<double>(34, std::max<uint64_t>(pyr_rows, 1) * 2);
+            PyrLevels<double> Pp{};
+            uint64_t off = 0;
+            for (uint32_t l = 0; l < nlev && l < 24; ++l) {
+                Pp.lev[l] = ppos + off * 2;
+                off += n / (uint64_t(c0) << l);
+            }
+            k_tn_positions<<<nb, 256, 0, st2>>>(g, d_order, pos);
+            build_pyramid(st2, pos, 2u, Pp);
+            k_tn_tile_pos_pyr<<<unsigned(lay.m), 64, 0, st2>>>(g, Pp, lev_shift, tile_pos);
+        } else {
+            k_tn_tile_pos<<<dim3(unsigned(lay.m), 2), 256, 0, st2>>>(g, d_order, tile_pos);
+        }
+        k_tn_tile_bias<<<dim3(unsigned(lay.m), unsigned(Ls)), 64, 0, st2>>>(
+            g, tile_pos, d_ro, d_ci, d_v, mdl->te, tile_bias);
+    }
+    TCK(cudaGetLastError());
     // ---- encoder (toy_net.cpp:295-318); the last residual update also writes LN(x) -------------
     k_tn_features<<<nb, 256, 0, st>>>(g, d_order, d_rho, d_ro, d_ci, d_glob, feat);
-    pgemm1<128>(st, feat, n, g.feat_pad, g.feat_pad, mdl->w_enc1, d, g.feat_pad, EpiStore{h1, uint32_t(d), nullptr, 1});
-    pgemm1<128>(st, h1, n, d, d, mdl->w_enc2, d, d, EpiStore{x, uint32_t(d), nullptr, 0});
+    pgemm1<128>(st, feat, n, g.feat_pad, g.feat_pad, mdl->w_enc1, d, g.feat_pad, EpiStore<true>{h1, uint32_t(d), nullptr});
+    pgemm1<128>(st, h1, n, d, d, mdl->w_enc2, d, d, EpiStore<false>{x, uint32_t(d), nullptr});
     for (size_t gi = 0; gi < mdl->w_gcn.size(); ++gi) {
         k_tn_gcn_msg<<<nw, 256, 0, st>>>(g, d_ro, d_ci, d_v, d_diag, x, h1);
         if (gi + 1 < mdl->w_gcn.size())
-            pgemm1<128>(st, h1, n, d, d, mdl->w_gcn[gi], d, d, EpiResidual{x, uint32_t(d), nullptr, 1});
+            pgemm1<128>(st, h1, n, d, d, mdl->w_gcn[gi], d, d, EpiResidual<true>{x, uint32_t(d), nullptr});
         else
             pgemm1<128>(st, h1, n, d, d, mdl->w_gcn[gi], d, d, EpiResidualLN{x, ln, 1});
     }
@@ -536,34 +611,13 @@ static void toynet_run(ToynetModel* mdl, cudaStream_t st, uint64_t n, uint64_t w
         }
         k_tn_layernorm<<<unsigned((MT * 32 + 255) / 256), 256, 0, st>>>(MT, uint32_t(d), tile_tok, ln_t, uint32_t(d));
     }
-    k_tn_leaf_bias<<<dim3(unsigned((L * L + 255) / 256), unsigned(lay.k)), 256, 0, st>>>(
-        g, d_order, d_ro, d_ci, d_v, mdl->le, leaf_bias);
-    if (lay.m) {
-        if (pyr) {
-            auto* pos = mdl->buf<double>(33, n * 2);
-            auto* ppos = mdl->buf<double>(34, std::max<uint64_t>(pyr_rows, 1) * 2);
-            PyrLevels<double> Pp{};
-            uint64_t off = 0;
-            for (uint32_t l = 0; l < nlev && l < 24; ++l) {
-                Pp.lev[l] = ppos + off * 2;
-                off += n / (uint64_t(c0) << l);
-            }
-            k_tn_positions<<<nb, 256, 0, st>>>(g, d_order, pos);
-            build_pyramid(st, pos, 2u, Pp);
-            k_tn_tile_pos_pyr<<<unsigned(lay.m), 64, 0, st>>>(g, Pp, lev_shift, tile_pos);
-        } else {
-            k_tn_tile_pos<<<dim3(unsigned(lay.m), 2), 256, 0, st>>>(g, d_order, tile_pos);
-        }
-        k_tn_tile_bias<<<dim3(unsigned(lay.m), unsigned(Ls)), 64, 0, st>>>(
-            g, tile_pos, d_ro, d_ci, d_v, mdl->te, tile_bias);
-    }
-    TCK(cudaGetLastError());
+    join();  // the biases are ready before the first attention
 
     // attention sublayer (toy_net.cpp:78-125) on `rows` tokens in windows of T; lnbuf holds
     // LN(tok) on entry and LN(tok + attention) on exit (fused into the O-projection epilogue)
     auto attention = [&](cudaStream_t st, float* tok, float* lnbuf, uint64_t rows, uint64_t T, const LW& lw,
                          const __half* bias, float* qkv, float* hout) {
-        pgemm1<128>(st, lnbuf, rows, d, d, lw.qkv, 3 * d, d, EpiStore{qkv, uint32_t(3 * d), nullptr, 0});
+        pgemm1<128>(st, lnbuf, rows, d, d, lw.qkv, 3 * d, d, EpiStore<false>{qkv, uint32_t(3 * d), nullptr});
         const uint64_t nwin = rows / T;
         if (T == 128 || T == 32) {  // tensor cores (attention_tcgen05.cuh)
             static bool configured = false;
@@ -596,19 +650,10 @@ static void toynet_run(ToynetModel* mdl, cudaStream_t st, uint64_t n, uint64_t w
     auto ffn = [&](cudaStream_t st, float* tok, float* lnbuf, const float* r, const float* c, uint64_t rows,
                    const LW& lw, const float* bias, float* Hf) {
         pgemm<256>(st, make_pga({ASrc{lnbuf, d, d}, ASrc{r, d, d}, ASrc{c, d, d}}, rows), rows, 3 * d, lw.f1, 4 * d,
-                   4 * d, EpiStore{Hf, uint32_t(4 * d), bias, 1});
+                   4 * d, EpiStore<true>{Hf, uint32_t(4 * d), bias});
         pgemm1<128>(st, Hf, rows, 4 * d, 4 * d, lw.f2, d, 4 * d, EpiResidualLN{tok, lnbuf, 0});
     };
 
-    cudaStream_t st2 = mdl->side;
-    auto fork = [&] {  // st2 continues from st's current point
-        TCK(cudaEventRecord(mdl->ev_fork, st));
-        TCK(cudaStreamWaitEvent(st2, mdl->ev_fork, 0));
-    };
-    auto join = [&] {  // st waits for st2's work so far
-        TCK(cudaEventRecord(mdl->ev_join, st2));
-        TCK(cudaStreamWaitEvent(st, mdl->ev_join, 0));
-    };
     for (uint64_t layer = 0; layer < cfg.layers; ++layer) {
         // the two attention sublayers touch disjoint tokens: leaf on st, tile on st2
         fork();
@@ -662,12 +707,9 @@ static void toynet_run(ToynetModel* mdl, cudaStream_t st, uint64_t n, uint64_t w
     }
 
     // ---- decoder heads into the packed layout (toy_net.cpp:540-585) ------------------------
-    pgemm1<128>(st, x, n, d, d, mdl->w_lh1, d, d, EpiStore{h1, uint32_t(d), nullptr, 1});
+    pgemm1<128>(st, x, n, d, d, mdl->w_lh1, d, d, EpiStore<true>{h1, uint32_t(d), nullptr});
     // F_k rows: leaf_factor(k) + r L = (k L + r) L = i L -> a row-major [n x L] section
-    pgemm1<128>(st, h1, n, d, d, mdl->w_lh2, L, d, EpiStore{out, uint32_t(L), nullptr, 0});
-    uint32_t lL = 0, lLs = 0;
-    while ((1ull << lL) < L) ++lL;
-    while ((1ull << lLs) < Ls) ++lLs;
+    pgemm1<128>(st, h1, n, d, d, mdl->w_lh2, L, d, EpiStore<false>{out, uint32_t(L), nullptr});
     pgemm1<80>(st, x, n, d, d, mdl->w_heads, 2 * Ls + 1, d, EpiLeafHeads{out, lL, lLs, lay.bridge_base, lay.gate_base});
     if (lay.m) pgemm1<32>(st, tile_tok, MT, d, d, mdl->w_theads, Ls, d, EpiTileHeads{out, lLs, lay.tile_base});
     TCK(cudaEventRecord(mdl->ev1, st));
@@ -774,14 +816,14 @@ extern "C" int hfpg_gemm_tf32(uint64_t M, uint64_t N, uint64_t K, const float* A
                               float* C) {
     using namespace hfpg;
     return guarded([&] {
-        if (K % 4) throw InvalidArgument("gemm: K must be a multiple of 4 (16-byte rows)");
+        if (K % 4 || N % 4) throw InvalidArgument("gemm: K and N must be multiples of 4 (16-byte rows)");
         float *dA = nullptr, *dB = nullptr, *dC = nullptr;
         TCK(cudaMalloc(&dA, std::max<uint64_t>(M * K, 1) * 4));
         TCK(cudaMalloc(&dB, std::max<uint64_t>(N * K, 1) * 4));
         TCK(cudaMalloc(&dC, std::max<uint64_t>(M * N, 1) * 4));
         TCK(cudaMemcpy(dA, A, M * K * 4, cudaMemcpyHostToDevice));
         TCK(cudaMemcpy(dB, Bt, N * K * 4, cudaMemcpyHostToDevice));
-        pgemm1<128>(0, dA, M, K, K, dB, N, K, EpiStore{dC, uint32_t(N), nullptr, 0});
+        pgemm1<128>(0, dA, M, K, K, dB, N, K, EpiStore<false>{dC, uint32_t(N), nullptr});
         TCK(cudaDeviceSynchronize());
         TCK(cudaMemcpy(C, dC, M * N * 4, cudaMemcpyDeviceToHost));
         cudaFree(dA);

@@ -16,6 +16,21 @@ struct TnDims {
 };
 
 __device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
+// GELU with erf from Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7 absolute, below the fp32
+// rounding of the GELU's inputs after tf32 products): one reciprocal, one exp2 and a degree-5
+// polynomial instead of erff's branchy evaluation. The GEMM epilogues and the edge-bias MLPs use it.
+__device__ __forceinline__ float gelu_fast(float x) {
+    const float z = fabsf(x) * 0.70710678118654752f;
+    const float t = __frcp_rn(fmaf(0.3275911f, z, 1.f));
+    float p = fmaf(1.061405429f, t, -1.453152027f);
+    p = fmaf(p, t, 1.421413741f);
+    p = fmaf(p, t, -0.284496736f);
+    p = fmaf(p, t, 0.254829592f);
+    p *= t;
+    const float e = exp2f(-z * z * 1.4426950408889634f);
+    const float erf_abs = fmaf(-p, e, 1.f);
+    return 0.5f * x * (1.f + copysignf(erf_abs, x));
+}
 
 // Tile heap index m -> (span in leaves, row0 node, col0 node, chunk rows per token)
 struct TileGeom {
@@ -144,7 +159,7 @@ __device__ __forceinline__ void edge_mlp_t(const EdgeMlp& m, float dx, float dy,
         a = fmaf(dy, m.w1[1 * EH + k], a);
         a = fmaf(dist, m.w1[2 * EH + k], a);
         a = fmaf(c, m.w1[3 * EH + k], a);
-        hid[k] = gelu_f(a);
+        hid[k] = gelu_fast(a);
     }
 #pragma unroll
     for (int h = 0; h < HD; ++h) {
@@ -170,7 +185,7 @@ __device__ __forceinline__ void edge_mlp(const EdgeMlp& m, uint32_t eh, uint32_t
         a = fmaf(dy, m.w1[1 * eh + k], a);
         a = fmaf(dist, m.w1[2 * eh + k], a);
         a = fmaf(c, m.w1[3 * eh + k], a);
-        hid[k] = gelu_f(a);
+        hid[k] = gelu_fast(a);
     }
     for (uint32_t h = 0; h < heads; ++h) {
         float a = m.b2[h];
@@ -184,11 +199,11 @@ __device__ __forceinline__ void edge_mlp(const EdgeMlp& m, uint32_t eh, uint32_t
 // (10-bit mantissa like the tf32 products; the MLP outputs are O(1e3) at most, far inside the
 // fp16 range), pre-multiplied by log2(e) for the attention kernels' exp2 softmax: half the bytes
 // of fp32, one query row's keys contiguous. Coupling = A_{base+i, base+j} looked up in the sorted CSR row.
-__global__ void k_tn_leaf_bias(TnDims g, const uint32_t* order, const unsigned long long* ro,
+__global__ void k_tn_leaf_bias(TnDims g, uint32_t lL, const uint32_t* order, const unsigned long long* ro,
                                const uint32_t* ci, const double* v, EdgeMlp mlp, __half* bias) {
     const uint64_t k = blockIdx.y;
-    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // i * L + j
-    const uint64_t base = k * g.L;
+    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;  // i * L + j (L = 2^lL <= 128)
+    const uint64_t base = k << lL;
     // the leaf's node coordinates (frame.cpp cell centres, rounded once from f64), once per CTA.
     // The descriptors are formed in fp32: they feed an fp32 MLP whose output is stored as fp16,
     // so f64 differences (the reference's) would only cost f64 divisions and square roots
@@ -199,8 +214,8 @@ __global__ void k_tn_leaf_bias(TnDims g, const uint32_t* order, const unsigned l
         cy[q] = float((double(a / g.width) + 0.5) / double(g.height));
     }
     __syncthreads();
-    if (idx >= g.L * g.L) return;
-    const uint64_t i = idx / g.L, j = idx % g.L;
+    if (idx >= (1u << (2 * lL))) return;
+    const uint32_t i = idx >> lL, j = idx & ((1u << lL) - 1u);
     float xa, ya, xb, yb;
     if (g.L <= 128) {
         xa = cx[i]; ya = cy[i]; xb = cx[j]; yb = cy[j];
@@ -211,17 +226,20 @@ __global__ void k_tn_leaf_bias(TnDims g, const uint32_t* order, const unsigned l
     }
     const float dx = xa - xb, dy = ya - yb, dist = sqrtf(dx * dx + dy * dy);
     double c = 0.0;
-    for (unsigned long long p = ro[base + i]; p < ro[base + i + 1]; ++p)
-        if (ci[p] == base + j) c = v[p];
+    const uint32_t col = uint32_t(base) + j;
+    for (unsigned long long p = ro[base + i], pe = ro[base + i + 1]; p < pe; ++p)
+        if (ci[p] == col) c = v[p];
     float out[8];
+    const uint64_t L2 = uint64_t(1) << (2 * lL);
+    __half* bk = bias + (k * g.heads) * L2 + idx;  // + h L^2: [k][h][i][j]
     if (g.eh == 8 && g.heads == 8) {
         edge_mlp_t<8, 8>(mlp, dx, dy, dist, float(c), out);
 #pragma unroll
-        for (int h = 0; h < 8; ++h) bias[((k * 8 + h) * g.L + i) * g.L + j] = __float2half_rn(out[h] * 1.4426950408889634f);
+        for (int h = 0; h < 8; ++h) bk[h * L2] = __float2half_rn(out[h] * 1.4426950408889634f);
         return;
     }
     edge_mlp(mlp, g.eh, g.heads, dx, dy, dist, float(c), out);
-    for (uint32_t h = 0; h < g.heads; ++h) bias[((k * g.heads + h) * g.L + i) * g.L + j] = __float2half_rn(out[h] * 1.4426950408889634f);
+    for (uint32_t h = 0; h < g.heads; ++h) bk[h * L2] = __float2half_rn(out[h] * 1.4426950408889634f);
 }
 
 // Chunk positions of every tile (toy_net.cpp:382-414 descriptors): pos[m][side][chunk] =

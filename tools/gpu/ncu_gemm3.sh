@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+bash tools/gpu/toynet_r02.sh
+for spec in "ffn1:pgemm_tf32<\(int\)256:0" "qkv:pgemm_tf32<\(int\)128, hfpg::.*EpiStore:2" "oproj:EpiResidualLN:1" "att128:k_tn_attn_tc<\(int\)128:0" "lbias:k_tn_leaf_bias:0"; do
+  name=${spec%%:*}; rest=${spec#*:}; rx=${rest%:*}; skip=${rest##*:}
+  timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$rx" -s $skip -c 1 -o gpurun_out/prof_$name python tools/bench_toynet.py --n 65536 --reps 0 > gpurun_out/ncu_$name.log 2>&1
+  echo "$name: $(grep -c 'Report' gpurun_out/ncu_$name.log)"
+done
