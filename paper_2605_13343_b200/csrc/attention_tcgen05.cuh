@@ -19,8 +19,10 @@
 //
 // Operands are staged by the threads from the fp32 qkv rows (Q, K zero-padded to 32 columns —
 // one 128-byte swizzle row, only the first two K=8 steps are issued), V transposed into a 16-row
-// B operand. TMEM: 256 columns (S 128 + O 8 x 16). T = 128: 512 threads, one CTA per SM;
-// T = 32: 128 threads, two CTAs per SM.
+// B operand. Pipelined over the heads: Q, K and S are double-buffered (smem, TMEM columns
+// 0 / 128), so head h+1's S MMA is issued with head h's PV MMA and is ready when its softmax
+// starts; operands are fetched two heads ahead. One block barrier + one named barrier per head.
+// TMEM: 512 columns (S 2 x 128 + O 8 x 16), one CTA per SM; T = 128: 512 threads, T = 32: 128.
 #pragma once
 
 #include <cuda_fp16.h>
@@ -34,11 +36,12 @@ constexpr int kAttRows = 128, kAttHD = 16, kAttHeads = 8;
 constexpr float kAttLog2e = 1.4426950408889634f;
 
 struct AttSmem {
-    alignas(1024) float Q[kAttRows * 32];    // 128 x 32 SW128 (cols 16..31 zero)
-    alignas(1024) float K[kAttRows * 32];
+    alignas(1024) float Q[2][kAttRows * 32]; // 128 x 32 SW128 (cols 16..31 zero), by head parity
+    alignas(1024) float K[2][kAttRows * 32];
     alignas(1024) float P[4][kAttRows * 32]; // 4 K-blocks of 128 x 32 SW128
     alignas(1024) float VT[4][16 * 32];      // V^T: 4 K-blocks of 16 x 32
-    float part[4][kAttRows];                 // T = 128: per-quad row max, then row sum
+    float part[4][kAttRows];                 // T = 128: per-quad row max (trace: row sums)
+    float psum[4][kAttRows];                 // T = 128: per-quad row sum
     uint64_t bar_s, bar_o;
     uint32_t tmem;
 };
@@ -66,14 +69,16 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // qkv: rows of [q | k | v] (3 d = 384 wide); bias: fp16 [window][head][query][key] in log2
 // units (b log2 e); head_out: rows x d. nwin windows of T tokens (rows = nwin * T).
 template <int T>
-__global__ void __launch_bounds__(att_threads<T>(), T == 128 ? 1 : 2)
+__global__ void __launch_bounds__(att_threads<T>(), 1)
     k_tn_attn_tc(uint64_t nwin, const float* __restrict__ qkv, const __half* __restrict__ bias,
                  float* __restrict__ head_out, unsigned int* rowsum_err_bits) {
     static_assert(T == 128 || T == 32, "windows of 128 (leaf) or 32 (tile) tokens");
     constexpr int NQ = att_quads<T>();
     constexpr int d = kAttHeads * kAttHD;  // 128
     extern __shared__ __align__(1024) unsigned char araw[];
-    AttSmem& sm = *reinterpret_cast<AttSmem*>((reinterpret_cast<uintptr_t>(araw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment by an offset into the shared array (a uintptr_t round trip would turn
+    // every shared-memory access into a generic one)
+    AttSmem& sm = *reinterpret_cast<AttSmem*>(araw + ((1024u - (smem_u32(araw) & 1023u)) & 1023u));
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
     const uint32_t row = tid & (kAttRows - 1), quad = tid >> 7;
     const uint64_t grow = uint64_t(blockIdx.x) * kAttRows + row;  // global token row
@@ -85,8 +90,6 @@ __global__ void __launch_bounds__(att_threads<T>(), T == 128 ? 1 : 2)
     const uint32_t key0 = T == 128 ? 32 * quad : 0;
     const uint32_t scol0 = T == 128 ? key0 : (row & ~31u);
     const uint32_t kb = scol0 >> 5;
-    unsigned char* Qb = reinterpret_cast<unsigned char*>(sm.Q);
-    unsigned char* Kb = reinterpret_cast<unsigned char*>(sm.K);
     // stagers: T = 128 quad 0 -> Q, 1 -> K, 2 -> V^T; T = 32 the single quad stages all three
     const bool stage_q = quad == 0, stage_k = T == 128 ? quad == 1 : true, stage_v = T == 128 ? quad == 2 : true;
 
@@ -96,15 +99,17 @@ __global__ void __launch_bounds__(att_threads<T>(), T == 128 ? 1 : 2)
         fence_mbar_init();
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&sm.tmem)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.tmem)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (quad == 0) {  // Q, K padding columns 16..31 and (T = 32) every P block: zero once
 #pragma unroll
-        for (int c = 16; c < 32; c += 4) {
-            *reinterpret_cast<float4*>(Qb + sw128_off(row, c)) = make_float4(0.f, 0.f, 0.f, 0.f);
-            *reinterpret_cast<float4*>(Kb + sw128_off(row, c)) = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        for (int bq = 0; bq < 2; ++bq)
+#pragma unroll
+            for (int c = 16; c < 32; c += 4) {
+                *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(sm.Q[bq]) + sw128_off(row, c)) = make_float4(0.f, 0.f, 0.f, 0.f);
+                *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(sm.K[bq]) + sw128_off(row, c)) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         if (T == 32) {
 #pragma unroll
             for (int b = 0; b < 4; ++b)
@@ -117,25 +122,47 @@ __global__ void __launch_bounds__(att_threads<T>(), T == 128 ? 1 : 2)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = sm.tmem, tS = tmem, tO = tmem + 128;
+    const uint32_t tmem = sm.tmem, tO = tmem + 256;  // S(h) in columns 128 (h & 1) .. +127
     constexpr uint32_t idS = idesc_tf32<128>(), idO = idesc_tf32<16>();
     const uint32_t lane_off = uint32_t((warp & 3) * 32) << 16;
 
     const float* rowp = qkv + grow * 3 * d;
     // next head's operands of this thread (T = 128: one of q / k / v in n0; T = 32: all three)
-    float4 n0[4], n1[4], n2[4];
-    auto fetch = [&](uint32_t h) {
+    struct Ops {
+        float4 q[4], k[4], v[4];  // T = 128 uses q only (this quad's one of q / k / v)
+    };
+    Ops cur, nxt;
+    auto fetch = [&](uint32_t h, Ops& o) {
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             if constexpr (T == 128) {
-                if (quad < 3) n0[c] = valid ? reinterpret_cast<const float4*>(rowp + quad * d + h * kAttHD)[c] : z;
+                if (quad < 3) o.q[c] = valid ? reinterpret_cast<const float4*>(rowp + quad * d + h * kAttHD)[c] : z;
             } else {
-                n0[c] = valid ? reinterpret_cast<const float4*>(rowp + h * kAttHD)[c] : z;
-                n1[c] = valid ? reinterpret_cast<const float4*>(rowp + d + h * kAttHD)[c] : z;
-                n2[c] = valid ? reinterpret_cast<const float4*>(rowp + 2 * d + h * kAttHD)[c] : z;
+                o.q[c] = valid ? reinterpret_cast<const float4*>(rowp + h * kAttHD)[c] : z;
+                o.k[c] = valid ? reinterpret_cast<const float4*>(rowp + d + h * kAttHD)[c] : z;
+                o.v[c] = valid ? reinterpret_cast<const float4*>(rowp + 2 * d + h * kAttHD)[c] : z;
             }
         }
+    };
+    auto stage_qk = [&](const Ops& o, int bq) {  // Q_h, K_h into buffer bq
+        if (stage_q) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(sm.Q[bq]) + sw128_off(row, 4 * c)) = o.q[c];
+        }
+        if (stage_k) {
+            const float4* kk = T == 128 ? o.q : o.k;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(sm.K[bq]) + sw128_off(row, 4 * c)) = kk[c];
+        }
+    };
+    auto issue_s = [&](int bq) {  // S = Q K^T into TMEM columns 128 bq
+        const uint64_t da = umma_desc_sw128(sm.Q[bq]), db = umma_desc_sw128(sm.K[bq]);
+        mma_tf32(tmem + 128 * bq, da, db, idS, 0u);
+        mma_tf32(tmem + 128 * bq, da + 2, db + 2, idS, 1u);
+        mma_commit(&sm.bar_s);
     };
     uint4 bcur[4], bnext[4];  // 32 fp16 bias values of this thread's keys
     auto fetch_bias = [&](uint32_t h, uint4 (&dst)[4]) {
@@ -144,34 +171,28 @@ __global__ void __launch_bounds__(att_threads<T>(), T == 128 ? 1 : 2)
         for (int i = 0; i < 4; ++i)
             dst[i] = valid ? __ldg(reinterpret_cast<const uint4*>(b) + i) : make_uint4(0u, 0u, 0u, 0u);
     };
-    fetch(0);
+    // prologue: head 0's S in flight, head 1's operands loading
+    fetch(0, cur);
     fetch_bias(0, bcur);
+    stage_qk(cur, 0);
+    fetch(1, nxt);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) issue_s(0);
     float inv[kAttHeads];
     float rs_err = 0.f;
 
 #pragma unroll 1
     for (uint32_t h = 0; h < kAttHeads; ++h) {
-        // ---- stage Q_h, K_h
-        if (stage_q) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) *reinterpret_cast<float4*>(Qb + sw128_off(row, 4 * c)) = n0[c];
+        const uint32_t tS = tmem + 128 * (h & 1);
+        if (h + 1 < kAttHeads) {
+            fetch_bias(h + 1, bnext);
+            // the next head's Q, K into the other buffer now (its last reader, head h-1's S MMA,
+            // completed before head h-1's softmax), so S(h+1) can be issued ahead of PV(h)
+            stage_qk(nxt, (h + 1) & 1);
         }
-        if (stage_k) {
-            const float4* kk = T == 128 ? n0 : n1;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) *reinterpret_cast<float4*>(Kb + sw128_off(row, 4 * c)) = kk[c];
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tc_fence_before();
-        __syncthreads();
-        tc_fence_after();
-        if (tid == 0) {  // S = Q K^T
-            const uint64_t da = umma_desc_sw128(sm.Q), db = umma_desc_sw128(sm.K);
-            mma_tf32(tS, da, db, idS, 0u);
-            mma_tf32(tS, da + 2, db + 2, idS, 1u);
-            mma_commit(&sm.bar_s);
-        }
-        if (h + 1 < kAttHeads) fetch_bias(h + 1, bnext);
         mbar_wait(&sm.bar_s, h & 1);
         tc_fence_after();
         // ---- logits l = s log2(e) / 4 + b' (b' = b log2 e) of this thread's 32 keys, row max
@@ -218,7 +239,7 @@ __global__ void __launch_bounds__(att_threads<T>(), T == 128 ? 1 : 2)
         // ---- after head h-1's PV MMA: V_h^T into its buffer, P = 2^(l - max) into the operand
         if (h > 0) mbar_wait(&sm.bar_o, (h - 1) & 1);
         if (stage_v) {
-            const float4* nv = T == 128 ? n0 : n2;
+            const float4* nv = T == 128 ? cur.q : cur.v;
             unsigned char* vb = reinterpret_cast<unsigned char*>(sm.VT[row >> 5]);
             const uint32_t key = row & 31;
 #pragma unroll
@@ -241,15 +262,13 @@ __global__ void __launch_bounds__(att_threads<T>(), T == 128 ? 1 : 2)
             }
             *reinterpret_cast<float4*>(pb + sw128_off(row, 4 * q4)) = make_float4(pp[0], pp[1], pp[2], pp[3]);
         }
-        if constexpr (NQ > 1) {
-            named_bar_sync(1, NQ * 128);  // every quad has read the maxima
-            sm.part[quad][row] = sum;
-        }
+        if constexpr (NQ > 1) sm.psum[quad][row] = sum;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
-        __syncthreads();  // P, V^T (and the partial sums) complete
+        __syncthreads();  // P, V^T, the partial sums and the next Q, K complete
         tc_fence_after();
-        if (tid == 0) {  // O_h = P V_h
+        if (tid == 0) {  // S for head h+1 first (the next softmax waits on it), then O_h = P V_h
+            if (h + 1 < kAttHeads) issue_s((h + 1) & 1);
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
                 const uint64_t da = umma_desc_sw128(sm.P[b]), db = umma_desc_sw128(sm.VT[b]);
@@ -258,17 +277,19 @@ __global__ void __launch_bounds__(att_threads<T>(), T == 128 ? 1 : 2)
             }
             mma_commit(&sm.bar_o);
         }
-        if (h + 1 < kAttHeads) fetch(h + 1);  // next head's q / k / v, in flight during the PV MMA
+        if (h + 1 < kAttHeads) {
+            cur = nxt;
+            if (h + 2 < kAttHeads) fetch(h + 2, nxt);  // two heads ahead, in flight over a whole head
+        }
         float tot = sum;
-        if constexpr (NQ > 1) tot = (sm.part[0][row] + sm.part[1][row]) + (sm.part[2][row] + sm.part[3][row]);
+        if constexpr (NQ > 1) tot = (sm.psum[0][row] + sm.psum[1][row]) + (sm.psum[2][row] + sm.psum[3][row]);
         inv[h] = 1.f / tot;
         if (rowsum_err_bits) {  // trace (toy_net.cpp:108-113): row sum of the normalised probabilities
             float rs = 0.f;
 #pragma unroll
             for (int j = 0; j < 32; ++j) rs += ex2_approx(lg[j] - mx) * inv[h];
             if constexpr (NQ > 1) {
-                named_bar_sync(1, NQ * 128);  // every quad has read the sums
-                sm.part[quad][row] = rs;
+                sm.part[quad][row] = rs;  // the maxima were read before the block barrier
                 named_bar_sync(1, NQ * 128);
                 rs = (sm.part[0][row] + sm.part[1][row]) + (sm.part[2][row] + sm.part[3][row]);
                 named_bar_sync(1, NQ * 128);
@@ -318,7 +339,7 @@ __global__ void __launch_bounds__(att_threads<T>(), T == 128 ? 1 : 2)
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
     }
 }
 

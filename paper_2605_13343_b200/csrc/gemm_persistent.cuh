@@ -78,7 +78,9 @@ __global__ void __launch_bounds__(kPgThreads, 1)
     constexpr int S = Cfg::kStages;
     constexpr int kEpiActive = kPgEpiWarps;  // warps arriving on tempty
     extern __shared__ __align__(1024) unsigned char praw[];
-    PgSmem<BN, WHOLE>& sm = *reinterpret_cast<PgSmem<BN, WHOLE>*>((reinterpret_cast<uintptr_t>(praw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment by an offset into the shared array (a uintptr_t round trip would turn
+    // every shared-memory access into a generic one)
+    PgSmem<BN, WHOLE>& sm = *reinterpret_cast<PgSmem<BN, WHOLE>*>(praw + ((1024u - (smem_u32(praw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = (K + kGemmBK - 1) / kGemmBK;
     const int mt = (M + kGemmBM - 1) / kGemmBM, ntl = (N + BN - 1) / BN, tiles = mt * ntl;

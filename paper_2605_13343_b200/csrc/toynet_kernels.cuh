@@ -21,14 +21,15 @@ __device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.f + erff
 // polynomial instead of erff's branchy evaluation. The GEMM epilogues and the edge-bias MLPs use it.
 __device__ __forceinline__ float gelu_fast(float x) {
     const float z = fabsf(x) * 0.70710678118654752f;
-    const float t = __frcp_rn(fmaf(0.3275911f, z, 1.f));
+    float t, e;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.f)));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-z * z * 1.4426950408889634f));
     float p = fmaf(1.061405429f, t, -1.453152027f);
     p = fmaf(p, t, 1.421413741f);
     p = fmaf(p, t, -0.284496736f);
     p = fmaf(p, t, 0.254829592f);
     p *= t;
-    const float e = exp2f(-z * z * 1.4426950408889634f);
-    const float erf_abs = fmaf(-p, e, 1.f);
+    const float erf_abs = fmaf(-p, e, 1.f);  // erf(|x| / sqrt 2)
     return 0.5f * x * (1.f + copysignf(erf_abs, x));
 }
 
