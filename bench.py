@@ -726,6 +726,40 @@ def run_part(args, cfg):
         dist.destroy_process_group()
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run with N ranks
+    (one per GPU, rendezvous on 127.0.0.1), the driver's own launch line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def check_launch(args):
+    """--check-launch: the N-rank plumbing only (rendezvous, barrier, max over ranks, the
+    configs[3] frame sharding) — one JSON line from rank 0; runs on CPU with HFPG_BENCH_GLOO=1."""
+    world, rank, local = dist_init()
+    barrier(world)
+    t = max_over_ranks(float(rank + 1), world, local)
+    frames = frames_of(rank, world, 64)
+    if world > 1:
+        import torch.distributed as dist
+        got = [None] * world
+        dist.all_gather_object(got, frames)
+        frames = sorted(f for g in got for f in g)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"check_launch": True, "n_gpus": world, "gpus_requested": args.gpus,
+                          "max_over_ranks": t, "frames_covered": frames == list(range(64))}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -737,7 +771,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the bit-exact parity solve")
     ap.add_argument("--no-inference", action="store_true", help="skip the configs[1] inference object")
+    ap.add_argument("--check-launch", action="store_true", help="N-rank plumbing only (no solve)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
+    if args.check_launch:
+        return check_launch(args)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         args.ref_budget = min(args.ref_budget, 4.0)

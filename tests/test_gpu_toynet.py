@@ -14,7 +14,13 @@ import pytest
 from conftest import ROOT, rel_l2
 
 pytestmark = pytest.mark.gpu
-SECTION_TOL = 3e-2  # tf32 products through 3 layers of attention + FFN
+# Per packed section, relative l2 against the reference's f64 forward. tf32 products carry a
+# 10-bit mantissa (2^-11 relative each); through the encoder, 3 layers of attention + 4d FFN
+# (K up to 512) and the heads the measured error is 4e-3 .. 5.4e-3 for the leaf / tile / bridge
+# sections and 2e-3 .. 1.2e-2 for the gate (one d -> 1 projection of the final tokens, the most
+# cancellation-prone section) at N = 256 .. 65,536 (profiles/r02_toynet_parity.jsonl): the
+# bounds keep ~2x headroom over those.
+SECTION_TOL = {"leaf": 1e-2, "tile": 1e-2, "bridge": 1e-2, "gate": 2.5e-2}
 
 
 def sections(lay, data):
@@ -59,7 +65,7 @@ def test_forward_matches_reference(H, ref, n):
             "ref_forward_ms": ref_ms, "max_abs_ref": float(np.abs(want).max()),
             "row_sum_err": tr.max_attention_row_sum_error, "highway_dev": tr.highway_max_deviation})
     assert all(np.isfinite(f.data)), "non-finite factors"
-    assert max(errs.values()) <= SECTION_TOL, errs
+    assert all(errs[k] <= SECTION_TOL[k] for k in errs), errs
     # trace (toy_net.hpp:64-74): two attention families, normalised rows, conservation
     assert tr.attention_kernel_families() == 2
     assert tr.max_attention_row_sum_error <= 1e-5
