@@ -270,6 +270,53 @@ int hfpg_adamw_step(hfpg_handle* h, double* params, double* grad, double* m1, do
                     uint64_t step, double lr, double beta1, double beta2, double eps, double weight_decay,
                     double clip_norm, double* gnorm_out);
 
+/* probes.cpp:14-44 on the device for large batches: z (device, n * kz) = the normals of draws
+ * counter0 .. of the RngStream with key `key` (rng.hpp; correctly rounded log / cos), then
+ * `steps` damped-Jacobi sweeps with omega on the handle's operator. */
+int hfpg_probes_device(hfpg_handle* h, uint64_t key, uint64_t counter0, uint64_t kz, double omega, uint64_t steps,
+                       double* z);
+/* train.hpp:12-52 — a training frame (frame.hpp fields + rhs + its frame index, which keys the
+ * power-iteration and evaluation-probe streams), TrainConfig, one log entry, the run summary. */
+typedef struct {
+    hfpg_frame_view view;
+    const double* b;
+    uint64_t frame_index;
+} hfpg_train_frame;
+typedef struct {
+    double lr, weight_decay, clip_norm;
+    double plateau_factor;
+    uint64_t plateau_patience;
+    double plateau_rel_threshold;
+    uint64_t max_steps, autostop_window;
+    double probe_omega;
+    uint64_t probe_smooth_steps, contexts_per_step;
+    int32_t loss; /* 0 cosine, 1 sai */
+    uint64_t log_every;
+    double init_sigma;
+    uint64_t leaf_size, coarse_size, eval_every_logs;
+    double solve_rtol;
+    uint64_t solve_max_iters, stop_at_iters;
+} hfpg_train_config;
+typedef struct {
+    uint64_t step;
+    double train_loss, sai_heldout;
+    uint64_t pcg_iters_heldout;
+    double lr, wall_s;
+} hfpg_train_log;
+typedef struct {
+    uint64_t total_steps;
+    int32_t auto_stopped, aborted_divergence, reached_target;
+    uint64_t n_entries;  /* log entries produced (entries beyond log_cap are not stored) */
+    uint64_t leaf_size;  /* after clamp_leaf_size (partition.hpp:48-50) */
+    uint64_t packed_width;
+} hfpg_train_summary;
+/* train.cpp:29-217 train_factors on `device`: frames share N; eval NULL = frames[0]. Writes the
+ * final float tensor (packed_width floats, may be NULL) and up to log_cap log entries. The
+ * held-out PCG iterations use hfpg_pcg_solve_exact (the reference's count exactly). */
+int hfpg_train_factors(const hfpg_train_frame* frames, uint64_t nframes, const hfpg_train_frame* eval,
+                       const hfpg_train_config* cfg, uint64_t seed, int device, float* factors_out,
+                       hfpg_train_log* log_out, uint64_t log_cap, hfpg_train_summary* summary);
+
 /* ---- IC(0) baseline (ic0.hpp / ic0.cpp) ----
  * ic0.cpp:10-69 ic0_factorize on the host (no device needed): the lower factor L of A (pattern =
  * lower triangle of A, diagonal last; policy 0 = Ic0Shift::none, 1 = Ic0Shift::scaled, shift

@@ -333,6 +333,24 @@ class Ref(_Base):
                  _ptr(out)), self.lib, "read_checkpoint")
         return dict(n=n.value, leaf=leaf.value, ls=ls.value), out
 
+    def train_factors(self, n, frame_seed, frame_indices, eval_index, cfg_c, seed, log_cap=4096):
+        """train.cpp:29 train_factors on make_frame(n, frame_seed, i) frames; cfg_c is the
+        product's TrainConfigC (same C layout). Returns (factors, [log dicts], summary dict)."""
+        from paper_2605_13343_b200 import _native as PN  # struct layouts only
+        idx = np.asarray(frame_indices, np.uint64)
+        summ = PN.TrainSummaryC()
+        logs = (PN.TrainLogC * log_cap)()
+        width = self.packed_width(n, n // 2 if n < 2 * cfg_c.leaf_size else cfg_c.leaf_size, cfg_c.coarse_size)
+        out = np.empty(width, np.float32)
+        f = self.lib.ref_train_factors
+        f.argtypes = [_u64, _u64, _p, _u64, _u64, _p, _u64, _p, _p, _u64, _p]
+        _check(f(n, frame_seed, _ptr(idx), len(idx), eval_index, C.byref(cfg_c), seed, _ptr(out), logs, log_cap,
+                 C.byref(summ)), self.lib, "train_factors")
+        ents = [dict(step=e.step, train_loss=e.train_loss, sai_heldout=e.sai_heldout,
+                     pcg_iters_heldout=e.pcg_iters_heldout, lr=e.lr) for e in logs[: summ.n_entries]]
+        return out, ents, dict(total_steps=summ.total_steps, auto_stopped=summ.auto_stopped,
+                               aborted_divergence=summ.aborted_divergence, reached_target=summ.reached_target)
+
     def toynet_forward(self, n, seed, frame_index, leaf=128, ls=32, d=128, layers=3, heads=8,
                        gcn_layers=2, d_global=12, edge_hidden=8, weight_seed=0):
         out = np.empty(self.packed_width(n, leaf, ls), np.float32)

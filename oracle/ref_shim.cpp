@@ -22,6 +22,9 @@
 #include "hfp/pcg.hpp"
 #include "hfp/rng.hpp"
 #include "hfp/toy_net.hpp"
+#include "hfp/train.hpp"
+
+#include "../include/hfpg.h"  // plain C structs of the training run (layout only)
 
 #include <chrono>
 #include <cstring>
@@ -397,6 +400,59 @@ int ref_toynet_forward(uint64_t n, uint64_t seed, uint64_t frame_index, uint64_t
             trace_out[2] = double(tr.leaf_attention_dispatches);
             trace_out[3] = double(tr.tile_attention_dispatches);
         }
+    });
+}
+
+// train.cpp:29 train_factors on make_frame(n, frame_seed, idx[i]) (eval: make_frame(n, frame_seed,
+// eval_index)); the same hfpg_train_config / log / summary layout as the product's ABI.
+int ref_train_factors(uint64_t n, uint64_t frame_seed, const uint64_t* idx, uint64_t nframes,
+                      uint64_t eval_index, const hfpg_train_config* c, uint64_t seed, float* factors_out,
+                      hfpg_train_log* log_out, uint64_t log_cap, hfpg_train_summary* summary) {
+    return guard([&] {
+        std::vector<Frame> fr;
+        for (uint64_t i = 0; i < nframes; ++i) fr.push_back(make_frame(n, frame_seed, idx[i]));
+        Frame ev = make_frame(n, frame_seed, eval_index);
+        std::vector<const Frame*> fp;
+        for (auto& f : fr) fp.push_back(&f);
+        TrainConfig cfg;
+        cfg.lr = c->lr;
+        cfg.weight_decay = c->weight_decay;
+        cfg.clip_norm = c->clip_norm;
+        cfg.plateau.factor = c->plateau_factor;
+        cfg.plateau.patience = c->plateau_patience;
+        cfg.plateau.rel_threshold = c->plateau_rel_threshold;
+        cfg.max_steps = c->max_steps;
+        cfg.autostop_window = c->autostop_window;
+        cfg.probe_omega = c->probe_omega;
+        cfg.probe_smooth_steps = c->probe_smooth_steps;
+        cfg.contexts_per_step = c->contexts_per_step;
+        cfg.loss = c->loss == 1 ? LossKind::sai : LossKind::cosine;
+        cfg.log_every = c->log_every;
+        cfg.init_sigma = c->init_sigma;
+        cfg.leaf_size = c->leaf_size;
+        cfg.coarse_size = c->coarse_size;
+        cfg.eval_every_logs = c->eval_every_logs;
+        cfg.solve_rtol = c->solve_rtol;
+        cfg.solve_max_iters = c->solve_max_iters;
+        cfg.stop_at_iters = c->stop_at_iters;
+        TrainResult r = train_factors(fp, cfg, seed, &ev);
+        if (factors_out) std::memcpy(factors_out, r.factors.data.data(), r.factors.data.size() * 4);
+        const auto& E = r.history.entries;
+        for (size_t i = 0; i < E.size() && i < log_cap; ++i) {
+            log_out[i].step = E[i].step;
+            log_out[i].train_loss = E[i].train_loss;
+            log_out[i].sai_heldout = E[i].sai_heldout;
+            log_out[i].pcg_iters_heldout = E[i].pcg_iters_heldout;
+            log_out[i].lr = E[i].lr;
+            log_out[i].wall_s = E[i].wall_s;
+        }
+        summary->total_steps = r.history.total_steps;
+        summary->auto_stopped = r.history.auto_stopped;
+        summary->aborted_divergence = r.history.aborted_divergence;
+        summary->reached_target = r.history.reached_target;
+        summary->n_entries = E.size();
+        summary->leaf_size = r.factors.layout.leaf_size;
+        summary->packed_width = r.factors.data.size();
     });
 }
 

@@ -9,7 +9,8 @@ from .api import (Checkpoint, CsrMatrix, Device, FactorInit, FactorLayout, Facto
                   SolveStatus, TileSpec, ToynetConfig, ToynetTrace, adamw_step, apply, build_partition, factor_apply_batch, factor_apply_batch_adjoint, loss_gradient, clamp_leaf_size, factor_applier,
                   ic0_applier, ic0_factorize, identity_applier, init_factors, jacobi_applier, make_factor_layout, make_frame,
                   make_frame_3d, packed_width, pcg_solve, read_checkpoint, read_mppf, test_frame_id,
-                  toynet_forward, toynet_forward_gpu_frame, train_frame_id, write_checkpoint, write_mppf)
+                  toynet_forward, toynet_forward_gpu_frame, train_frame_id, write_checkpoint, write_mppf,
+                  PlateauConfig, TrainConfig, TrainHistory, TrainLogEntry, TrainResult, train_factors)
 
 from .partition import PartitionGroup, RankSolver  # noqa: E402
 

@@ -58,6 +58,29 @@ class FrameViewC(C.Structure):
                 ("rho_heavy", dbl), ("row_offsets", vp), ("col_indices", vp), ("values", vp)]
 
 
+class TrainFrameC(C.Structure):
+    _fields_ = [("view", FrameViewC), ("b", vp), ("frame_index", u64)]
+
+
+class TrainConfigC(C.Structure):
+    _fields_ = [("lr", dbl), ("weight_decay", dbl), ("clip_norm", dbl), ("plateau_factor", dbl),
+                ("plateau_patience", u64), ("plateau_rel_threshold", dbl), ("max_steps", u64),
+                ("autostop_window", u64), ("probe_omega", dbl), ("probe_smooth_steps", u64),
+                ("contexts_per_step", u64), ("loss", i32), ("log_every", u64), ("init_sigma", dbl),
+                ("leaf_size", u64), ("coarse_size", u64), ("eval_every_logs", u64), ("solve_rtol", dbl),
+                ("solve_max_iters", u64), ("stop_at_iters", u64)]
+
+
+class TrainLogC(C.Structure):
+    _fields_ = [("step", u64), ("train_loss", dbl), ("sai_heldout", dbl), ("pcg_iters_heldout", u64),
+                ("lr", dbl), ("wall_s", dbl)]
+
+
+class TrainSummaryC(C.Structure):
+    _fields_ = [("total_steps", u64), ("auto_stopped", i32), ("aborted_divergence", i32),
+                ("reached_target", i32), ("n_entries", u64), ("leaf_size", u64), ("packed_width", u64)]
+
+
 class FrameDeviceC(C.Structure):
     _fields_ = [("n", u64), ("nnz", u64), ("width", u64), ("height", u64), ("depth", u64),
                 ("rho_heavy", dbl), ("cell_order", vp), ("rho", vp), ("row_offsets", vp),
@@ -101,6 +124,8 @@ _PROTOS = {
     "hfpg_set_precond": (C.c_int, [vp, C.c_int]),
     "hfpg_apply": (C.c_int, [vp, vp, vp, C.c_int]),
     "hfpg_precond_apply": (C.c_int, [vp, vp, vp, C.c_int]),
+    "hfpg_train_factors": (C.c_int, [C.POINTER(TrainFrameC), u64, C.POINTER(TrainFrameC), C.POINTER(TrainConfigC),
+                                     u64, C.c_int, vp, C.POINTER(TrainLogC), u64, C.POINTER(TrainSummaryC)]),
     "hfpg_spmv": (C.c_int, [vp, vp, vp, C.c_int]),
     "hfpg_ic0_factor_host": (C.c_int, [u64, vp, vp, vp, i32, vp, vp, vp, u64, C.POINTER(u64),
                                        C.POINTER(dbl)]),

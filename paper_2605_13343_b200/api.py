@@ -21,6 +21,7 @@ layout / seeded initialisation / frame generation in the library's native host c
 from __future__ import annotations
 
 import ctypes as C
+import json
 import enum
 import math
 from dataclasses import dataclass, field
@@ -694,6 +695,115 @@ def adamw_step(device: "Device", params_ptr: int, grad_ptr: int, m1_ptr: int, m2
     check(lib.hfpg_adamw_step(device.h, params_ptr, grad_ptr, m1_ptr, m2_ptr, count, step, lr, beta1, beta2,
                               eps, weight_decay, clip_norm, C.byref(gn)))
     return float(gn.value)
+
+
+@dataclass
+class PlateauConfig:
+    """train.hpp:12-17."""
+    factor: float = 0.5
+    patience: int = 5
+    rel_threshold: float = 5e-3
+
+
+@dataclass
+class TrainConfig:
+    """train.hpp:19-40 (defaults as the reference's)."""
+    lr: float = 2e-4
+    weight_decay: float = 1e-4
+    clip_norm: float = 1.0
+    plateau: PlateauConfig = field(default_factory=PlateauConfig)
+    max_steps: int = 100000
+    autostop_window: int = 10
+    probe_omega: float = 0.6
+    probe_smooth_steps: int = 2
+    contexts_per_step: int = 4
+    loss: LossKind = LossKind.cosine
+    log_every: int = 100
+    init_sigma: float = 1e-2
+    leaf_size: int = 128
+    coarse_size: int = 32
+    eval_every_logs: int = 1
+    solve_rtol: float = 1e-8
+    solve_max_iters: int = 20000
+    stop_at_iters: int = 0
+
+    def to_c(self) -> "N.TrainConfigC":
+        return N.TrainConfigC(self.lr, self.weight_decay, self.clip_norm, self.plateau.factor, self.plateau.patience,
+                              self.plateau.rel_threshold, self.max_steps, self.autostop_window, self.probe_omega,
+                              self.probe_smooth_steps, self.contexts_per_step, int(self.loss), self.log_every,
+                              self.init_sigma, self.leaf_size, self.coarse_size, self.eval_every_logs,
+                              self.solve_rtol, self.solve_max_iters, self.stop_at_iters)
+
+
+@dataclass
+class TrainLogEntry:
+    """train.hpp:42-49."""
+    step: int = 0
+    train_loss: float = 0.0
+    sai_heldout: float = 0.0
+    pcg_iters_heldout: int = 0
+    lr: float = 0.0
+    wall_s: float = 0.0
+
+
+@dataclass
+class TrainHistory:
+    """train.hpp:51-58; to_jsonl as train.cpp:13-27."""
+    entries: list = field(default_factory=list)
+    auto_stopped: bool = False
+    aborted_divergence: bool = False
+    reached_target: bool = False
+    total_steps: int = 0
+
+    def to_jsonl(self) -> str:
+        return "".join(json.dumps({"step": e.step, "train_loss": e.train_loss, "sai_heldout": e.sai_heldout,
+                                   "pcg_iters_heldout": e.pcg_iters_heldout, "lr": e.lr, "wall_s": e.wall_s},
+                                  separators=(",", ":")) + "\n" for e in self.entries)
+
+
+@dataclass
+class TrainResult:
+    """train.hpp:60-63."""
+    factors: "FactorTensor"
+    history: TrainHistory
+
+
+def _train_frame(fr: Frame) -> "N.TrainFrameC":
+    v = _frame_view(fr)
+    t = N.TrainFrameC(v, fr.b.ctypes.data, int(fr.frame_index))
+    t._keep = (v, fr)
+    return t
+
+
+def train_factors(frames, cfg: TrainConfig | None = None, seed: int = 0, eval_frame: Frame | None = None,
+                  device: int = 0) -> TrainResult:
+    """train.cpp:29-217 on the GPU (train_loop.cu): AdamW with decoupled weight decay, global
+    clip, reduce-on-plateau, min-lr auto-stop, divergence abort; each step averages
+    contexts_per_step fresh smoothed probe batches; the held-out evaluation runs the exact PCG."""
+    cfg = cfg or TrainConfig()
+    frames = list(frames)
+    if not frames:
+        raise ValueError("train_factors: no frames")
+    tf = (N.TrainFrameC * len(frames))(*[_train_frame(f) for f in frames])
+    keep = [f for f in frames]
+    ev = _train_frame(eval_frame) if eval_frame is not None else None
+    n = frames[0].n
+    leaf = clamp_leaf_size(n, cfg.leaf_size)
+    lay = make_factor_layout(build_partition(n, leaf), cfg.coarse_size)
+    out = np.empty(lay.total, np.float32)
+    cap = max(1, cfg.max_steps // max(cfg.log_every, 1) + 1)
+    logs = (N.TrainLogC * cap)()
+    summ = N.TrainSummaryC()
+    c = cfg.to_c()
+    check(lib.hfpg_train_factors(tf, len(frames), C.byref(ev) if ev is not None else None, C.byref(c), seed,
+                                 device, out.ctypes.data, logs, cap, C.byref(summ)))
+    del keep
+    hist = TrainHistory([TrainLogEntry(int(e.step), float(e.train_loss), float(e.sai_heldout),
+                                       int(e.pcg_iters_heldout), float(e.lr), float(e.wall_s))
+                         for e in logs[: min(int(summ.n_entries), cap)]],
+                        bool(summ.auto_stopped), bool(summ.aborted_divergence), bool(summ.reached_target),
+                        int(summ.total_steps))
+    return TrainResult(FactorTensor(lay, out), hist)
 
 
 class Ic0Shift(enum.IntEnum):

@@ -171,6 +171,9 @@ struct hfpg_handle {
     // exact-mode apply<float> scratch (apply_exact_f32's stage arrays), grown once, reused
     float* exbuf = nullptr;
     uint64_t exbuf_cap = 0;
+    // probe smoothing scratch (hfpg_probes_device): A z of one batch
+    double* probe_tmp = nullptr;
+    uint64_t probe_cap = 0;
 
     // row partition (G > 1): this handle holds rank `rank`'s share of a system
     struct Part {
@@ -1284,6 +1287,7 @@ int hfpg_destroy(hfpg_handle* h) {
         }
         dfree(h->crc_scratch);
         dfree(h->exbuf);
+        dfree(h->probe_tmp);
         for (double* b : h->tr.bufs) dfree(b);
         dfree(h->tr.P); dfree(h->tr.G); dfree(h->tr.BY); dfree(h->tr.Z); dfree(h->tr.part);
         if (h->stream) cudaStreamDestroy(h->stream);
@@ -1493,6 +1497,39 @@ int hfpg_precond_apply(hfpg_handle* h, const double* r, double* z, int where) {
                                                                       h->precond == HFPG_PRECOND_JACOBI);
         CK(cudaGetLastError());
         if (where == HFPG_HOST) copy_out(h, z, h->z, h->n, HFPG_HOST);
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+// probes.cpp:14-44 on the device, for batches too large to draw and smooth on the host: z_i is
+// the normal of draw counter0 + i of the stream `key` (rng.hpp, with correctly rounded log / cos —
+// crmath.cuh; libm differs by <= 1 ulp on ~0.2% of draws), then `steps` damped-Jacobi sweeps
+// z -= (omega / a_ii) (A z) with the reference build's fused update (probes.cpp:36-41).
+int hfpg_probes_device(hfpg_handle* h, uint64_t key, uint64_t counter0, uint64_t kz, double omega, uint64_t steps,
+                       double* z) {
+    return guarded([&] {
+        set_device(h);
+        if (!h->have_csr) throw InvalidArgument("smooth_probes: no matrix loaded");
+        if (!h->diag_positive) throw InvalidArgument("smooth_probes: nonpositive diagonal");
+        const uint64_t n = h->n, nk = n * kz;
+        each(h->stream, nk, [=] __device__(uint64_t i) { z[i] = crm::normal_of_cr(fg_mix64(key ^ (counter0 + i))); });
+        if (steps) {
+            if (h->probe_cap < nk) {
+                dalloc(h->probe_tmp, nk);
+                h->probe_cap = nk;
+            }
+            double* az = h->probe_tmp;
+            const double* d = h->a_diag;
+            for (uint64_t s = 0; s < steps; ++s) {
+                train_spmm(h, z, az, kz);
+                each(h->stream, nk, [=] __device__(uint64_t t) {
+                    const uint64_t i = t / kz;
+                    const double scale = omega / d[i];
+                    z[t] = fma(-scale, az[t], z[t]);
+                });
+            }
+        }
+        CK(cudaGetLastError());
         CK(cudaStreamSynchronize(h->stream));
     });
 }
