@@ -308,8 +308,8 @@ void ensure_workspace(hfpg_handle* h) {
         CK(cudaMemsetAsync(h->dpart, 0, kPartLen * sizeof(double), h->stream));
     }
     if (!h->counters) {
-        dalloc(h->counters, 8);
-        CK(cudaMemsetAsync(h->counters, 0, 8 * sizeof(unsigned), h->stream));
+        dalloc(h->counters, 16);  // [0..3] grid reductions, [4..11] k_leaf_coarse tickets
+        CK(cudaMemsetAsync(h->counters, 0, 16 * sizeof(unsigned), h->stream));
     }
     if (!h->gbar) dalloc(h->gbar, 1);
     if (!h->sc) {
@@ -369,6 +369,9 @@ void fill_sys(hfpg_handle* h) {
     // deferred reductions on the single-rank factor fast path (HFPG_NO_DEFER=1: last-CTA tails)
     s.defer = h->part.G == 1 && h->precond == HFPG_PRECOND_FACTOR && h->fast && h->have_factors &&
               !std::getenv("HFPG_NO_DEFER");
+    // apply stages 1-4 in one kernel (leaf_coarse.cuh) with HFPG_LEAF_COARSE=1 — measured slower
+    // than the staged kernels, so opt-in only
+    s.fused_leaf = s.defer && std::getenv("HFPG_LEAF_COARSE") && std::getenv("HFPG_LEAF_COARSE")[0] == '1';
     s.sc = h->sc;
     s.history = h->history;
     s.use_cond = 0;
@@ -413,13 +416,15 @@ void launch_coarse(hfpg_handle* h, const DevSys& s, int mode) {
 void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
     const DevSys& s = h->sys;
     const Layout& L = h->L;
-    if (h->fast) {
+    if (h->fast && s.fused_leaf) {  // stages 1-4 in one launch
+        k_leaf_coarse<<<unsigned(leaf_grid(h)), kLeafThreads, sizeof(LcSmem), h->lstream>>>(s, mode, rin);
+    } else if (h->fast) {
         k_leaf_fast<<<unsigned(leaf_grid(h)), kLeafThreads, sizeof(LeafSmem), h->lstream>>>(s, mode, rin);
     } else {
         k_leaf_generic<<<unsigned(L.k), 256, 2 * L.l * sizeof(float), h->lstream>>>(s, mode, rin);
     }
     CK(cudaGetLastError());
-    launch_coarse(h, s, mode);
+    if (!(h->fast && s.fused_leaf)) launch_coarse(h, s, mode);
     if (h->fast)
         k_prolong_fast<<<unsigned(prolong_grid(h)), 256, 0, h->lstream>>>(s, mode, rin, zout);
     else
@@ -494,6 +499,8 @@ void configure_kernels() {
     std::call_once(once, [] {
         CK(cudaFuncSetAttribute(k_leaf_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(sizeof(LeafSmem))));
+        CK(cudaFuncSetAttribute(k_leaf_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(sizeof(LcSmem))));
         CK(cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         CK(cudaFuncSetAttribute(k_spmv_tma<kLoop>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         CK(cudaFuncSetAttribute(k_spmv_tma<kApply>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
@@ -1906,7 +1913,8 @@ int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_confi
 
 int hfpg_launch_counts(hfpg_handle* h, uint32_t* per_iteration, uint32_t* per_apply) {
     return guarded([&] {
-        const uint32_t apply = (h->have_factors && h->fast) ? 4 : 3;
+        fill_sys(h);
+        const uint32_t apply = (h->have_factors && h->fast) ? (h->sys.fused_leaf ? 2 : 4) : 3;
         *per_apply = apply;
         *per_iteration = h->precond == HFPG_PRECOND_FACTOR ? apply + 1 : h->precond == HFPG_PRECOND_IC0 ? 4 : 2;
         if (use_persistent(h)) {  // one k_solve launch per solve
@@ -1974,12 +1982,14 @@ int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out) {
             CK(cudaEventRecord(ev[0], h->stream));
             launch_spmv<kLoop>(h, h->sys, nullptr, nullptr);
             CK(cudaEventRecord(ev[1], h->stream));
-            if (h->fast)
+            if (h->fast && h->sys.fused_leaf)  // leaf + coarse in one kernel: "coarse" reads 0
+                k_leaf_coarse<<<unsigned(leaf_grid(h)), kLeafThreads, sizeof(LcSmem), h->stream>>>(h->sys, kLoop, nullptr);
+            else if (h->fast)
                 k_leaf_fast<<<unsigned(leaf_grid(h)), kLeafThreads, sizeof(LeafSmem), h->stream>>>(h->sys, kLoop, nullptr);
             else
                 k_leaf_generic<<<unsigned(L.k), 256, 2 * L.l * sizeof(float), h->stream>>>(h->sys, kLoop, nullptr);
             CK(cudaEventRecord(ev[2], h->stream));
-            launch_coarse(h, h->sys, kLoop);
+            if (!(h->fast && h->sys.fused_leaf)) launch_coarse(h, h->sys, kLoop);
             CK(cudaEventRecord(ev[3], h->stream));
             if (h->fast)
                 k_prolong_fast<<<unsigned(prolong_grid(h)), 256, 0, h->stream>>>(h->sys, kLoop, nullptr, nullptr);

@@ -67,6 +67,9 @@ struct DevSys {
     int defer;
     double* dpart;
     uint32_t grid_spmv, grid_leaf, grid_prol;
+    // k_leaf_coarse (leaf_coarse.cuh) runs apply stages 1-4: r' = r - alpha Ap is then stored by
+    // the prolongation (which re-forms it with the same fma) instead of the leaf kernel
+    int fused_leaf;
 };
 constexpr uint32_t kPartSpmv = 0, kPartLeaf = 2048, kPartProl = 3072, kPartLen = 4096;
 
@@ -1444,11 +1447,17 @@ __global__ void __launch_bounds__(256, 2) k_prolong_fast(DevSys s, int mode, con
         }
         double yl[4], rv[4], ad[4];
         float gt[4];
+        const bool form_r = mode == kLoop && s.fused_leaf;  // r' = r - alpha Ap (pcg.cpp:98) lands here
+        const double alpha = form_r ? s.sc->alpha : 0.0;
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             const uint64_t i = base + lane + 32 * t;
             yl[t] = __ldcg(&s.y_loc[i]);
             rv[t] = __ldcg(&rsrc[i]);
+            if (form_r) {
+                rv[t] = fma(-alpha, __ldcg(&s.ap[i]), rv[t]);
+                s.r[i] = rv[t];
+            }
             ad[t] = __ldg(&s.a_diag[i]);
             gt[t] = __ldg(&s.F[s.gate_base + i]);
         }
@@ -1600,3 +1609,6 @@ __global__ void k_init(DevSys s, const double* b) {
 }
 
 }  // namespace hfpg
+
+#include "leaf_coarse.cuh"
+
