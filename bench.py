@@ -319,6 +319,47 @@ def run_inference(local: int, steps: int, warmup: int, n: int = 65536, solve: bo
     return out
 
 
+TRAINED = os.path.join(ROOT, "tests", "golden", "trained_8192.hftc")
+
+
+def run_trained(local: int, reps: int = 5) -> dict:
+    """BASELINE configs[0]'s system (make_frame(8192, 2024, 0)) with a TRAINED factor tensor —
+    tests/golden/trained_8192.hftc, produced by the GPU train_factors on the reference's
+    acceptance recipe (acceptance.cpp:378-420; tools/train_tensor.py --acceptance --n 8192) — next
+    to Jacobi on the same graph: graph-PCG device times, the exact solver's count against the
+    reference's own pcg_solve with the same checkpoint (tests/golden/ref_iterations.json)."""
+    import paper_2605_13343_b200 as H
+    from paper_2605_13343_b200 import _native as N
+    import torch
+    fr = H.make_frame(8192, 2024, 0)
+    dev = H.Device(local)
+    dev.load_csr(fr.A)
+    dev.load_checkpoint(TRAINED)
+    b = torch.from_numpy(fr.b).to(f"cuda:{local}")
+    x = torch.empty_like(b)
+    sc = H.SolveConfig()
+    out = {"workload": "make_frame(8192, 2024, 0) (BASELINE configs[0]) with the trained tensor "
+                       "tests/golden/trained_8192.hftc vs Jacobi, graph PCG to 1e-8"}
+    for name, kind in (("trained", 2), ("jacobi", 1)):
+        dev.set_precond(kind)
+        ms, its = [], 0
+        for _ in range(reps + 1):
+            rep = dev.solve_ptr(b.data_ptr(), x.data_ptr(), sc, None, N.DEVICE)
+            ms.append(float(rep.wall_ms))
+            its = int(rep.iterations)
+        out[name] = {"iterations": its, "ms": statistics.median(ms[1:])}
+    dev.set_precond(2)
+    rx = dev.solve_ptr(b.data_ptr(), x.data_ptr(), sc, None, N.DEVICE, exact=True)
+    want = None
+    try:
+        want = json.load(open(ITERS))["2d_8192_trained"]
+    except Exception:
+        pass
+    out["trained"]["exact_iterations"] = int(rx.iterations)
+    out["reference_iterations"] = {"trained": want["factor"]["iterations"], "jacobi": want["jacobi"]["iterations"]} if want else None
+    return out
+
+
 def run_infer_config(args, cfg):
     world, rank, local = dist_init()
     import torch
@@ -512,6 +553,9 @@ def run_ours(args, cfg):
     if rank == 0 and not args.no_inference:
         # BASELINE configs[1] (N=65,536 inference + graph PCG), outside the timed region
         line["inference"] = run_inference(local, 3, 1, 65536, solve=True)
+        # a trained tensor (GPU train_factors) on configs[0]'s system, against Jacobi
+        if os.path.exists(TRAINED):
+            line["trained"] = run_trained(local)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ms_it, n_it = cpu_sample(cfg, fr, f, args.ref_budget)
         its = ref_iterations(cfg["ref_key"]) or iters[-1]

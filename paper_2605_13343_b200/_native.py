@@ -124,6 +124,7 @@ _PROTOS = {
     "hfpg_set_precond": (C.c_int, [vp, C.c_int]),
     "hfpg_apply": (C.c_int, [vp, vp, vp, C.c_int]),
     "hfpg_precond_apply": (C.c_int, [vp, vp, vp, C.c_int]),
+    "hfpg_probes_device": (C.c_int, [vp, u64, u64, u64, dbl, u64, vp]),
     "hfpg_train_factors": (C.c_int, [C.POINTER(TrainFrameC), u64, C.POINTER(TrainFrameC), C.POINTER(TrainConfigC),
                                      u64, C.c_int, vp, C.POINTER(TrainLogC), u64, C.POINTER(TrainSummaryC)]),
     "hfpg_spmv": (C.c_int, [vp, vp, vp, C.c_int]),

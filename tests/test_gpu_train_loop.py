@@ -45,3 +45,25 @@ def test_plateau_schedule_and_autostop_match_reference(H, ref):
     assert res.history.total_steps == summ["total_steps"]
     assert res.history.auto_stopped == bool(summ["auto_stopped"])
     assert [e.lr for e in res.history.entries] == [w["lr"] for w in want]
+
+
+def test_trained_checkpoint_beats_jacobi_like_reference(H):
+    """tests/golden/trained_8192.hftc (GPU train_factors on the reference's acceptance recipe,
+    tools/train_tensor.py --acceptance --n 8192) on BASELINE configs[0]'s system: the reference's
+    own pcg_solve with this checkpoint takes 221 iterations against Jacobi's 513
+    (tests/golden/ref_iterations.json); the graph solve is within +-2 and the exact solve equal."""
+    import json
+    import os
+    from conftest import ROOT
+    want = json.load(open(os.path.join(ROOT, "tests", "golden", "ref_iterations.json")))["2d_8192_trained"]
+    fr = H.make_frame(8192, 2024, 0)
+    dev = H.Device(0)
+    dev.load_csr(fr.A)
+    dev.load_checkpoint(os.path.join(ROOT, "tests", "golden", "trained_8192.hftc"))
+    dev.set_precond(2)
+    x = np.empty(fr.n)
+    rep = dev.solve_ptr(fr.b.ctypes.data, x.ctypes.data, H.SolveConfig(), None, 0)
+    assert rep.converged and abs(int(rep.iterations) - want["factor"]["iterations"]) <= 2
+    rex = dev.solve_ptr(fr.b.ctypes.data, x.ctypes.data, H.SolveConfig(), None, 0, exact=True)
+    assert int(rex.iterations) == want["factor"]["iterations"]
+    assert want["factor"]["iterations"] < want["jacobi"]["iterations"] / 2
