@@ -396,15 +396,33 @@ void fill_sys(hfpg_handle* h) {
 }
 
 
+// Coarse-stage launch shapes. The tile kernel keeps its free register budget (98 registers,
+// two CTAs per SM); HFPG_COARSE_MINB=4 is the 64-register variant (four CTAs per SM, spills) kept
+// for A/B runs. The strip-sum sweep: up to two CTAs per SM, one 32-leaf group each.
+int tiles_minb() {
+    static const int v = [] {
+        const char* e = std::getenv("HFPG_COARSE_MINB");
+        return (e && e[0] == '4') ? 4 : 1;
+    }();
+    return v;
+}
+uint64_t sums_ctas_per_sm() { return 2; }
+void launch_tiles(hfpg_handle* h, const DevSys& s, int mode, uint64_t tw) {
+    const uint64_t cap = uint64_t(h->num_sms) * uint64_t(tiles_minb() == 4 ? 4 : 2);
+    const unsigned g = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(tw, cap)));
+    if (tiles_minb() == 4) k_tiles_all<4><<<g, kTilesThreads, 0, h->lstream>>>(s, mode);
+    else k_tiles_all<1><<<g, kTilesThreads, 0, h->lstream>>>(s, mode);
+}
+
 // Apply stage 4: subtree kernel + (above 32 leaves) the parallel top-of-tree kernel.
 void launch_coarse(hfpg_handle* h, const DevSys& s, int mode) {
     const Layout& L = h->L;
     if (h->fast) {
         const uint64_t R = L.k / std::min<uint64_t>(L.k, kCoarseS0);
-        k_sums_tree<<<unsigned(std::min<uint64_t>(R, uint64_t(h->num_sms))), kSumsThreads, 0, h->lstream>>>(s, mode);
+        k_sums_tree<<<unsigned(std::min<uint64_t>(R, uint64_t(h->num_sms) * sums_ctas_per_sm())), kSumsThreads, 0, h->lstream>>>(s, mode);
         CK(cudaGetLastError());
         const uint64_t tw = (L.k - 1 + kTilesThreads / 32 - 1) / (kTilesThreads / 32);
-        k_tiles_all<<<unsigned(std::max<uint64_t>(1, std::min<uint64_t>(tw, uint64_t(h->num_sms) * 2))), kTilesThreads, 0, h->lstream>>>(s, mode);
+        launch_tiles(h, s, mode, tw);
     } else {
         const uint64_t S0 = std::min<uint64_t>(L.k, coarse_width(L));
         k_coarse<<<unsigned(L.k / S0), kCoarseThreads, coarse_smem(L), h->lstream>>>(s, mode);
@@ -705,12 +723,12 @@ void stage_prolong(hfpg_handle* h, int mode, const double* rin, double* zout) {
 }
 void stage_sums(hfpg_handle* h, int mode) {
     const uint64_t R = h->L.k / std::min<uint64_t>(h->L.k, kCoarseS0);
-    k_sums_tree<<<unsigned(std::min<uint64_t>(R, uint64_t(h->num_sms))), kSumsThreads, 0, h->lstream>>>(h->sys, mode);
+    k_sums_tree<<<unsigned(std::min<uint64_t>(R, uint64_t(h->num_sms) * sums_ctas_per_sm())), kSumsThreads, 0, h->lstream>>>(h->sys, mode);
     CK(cudaGetLastError());
 }
 void stage_tiles(hfpg_handle* h, int mode) {
     const uint64_t tw = (h->L.k - 1 + kTilesThreads / 32 - 1) / (kTilesThreads / 32);
-    k_tiles_all<<<unsigned(std::max<uint64_t>(1, std::min<uint64_t>(tw, uint64_t(h->num_sms) * 2))), kTilesThreads, 0, h->lstream>>>(h->sys, mode);
+    launch_tiles(h, h->sys, mode, tw);
     CK(cudaGetLastError());
 }
 

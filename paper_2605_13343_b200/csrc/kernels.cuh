@@ -1043,8 +1043,10 @@ __device__ __forceinline__ void tile_root_sums(const DevSys& s, uint64_t m, uint
     __syncthreads();
 }
 
-constexpr int kTilesThreads = 256;  // 98 registers: two CTAs per SM
-__global__ void __launch_bounds__(kTilesThreads) k_tiles_all(DevSys s, int mode) {
+constexpr int kTilesThreads = 256;
+// MINB = resident CTAs per SM the register budget is fitted to (2: 98 registers; 4: 64)
+template <int MINB>
+__global__ void __launch_bounds__(kTilesThreads, MINB) k_tiles_all(DevSys s, int mode) {
     if (mode != kApply && s.sc->done) return;
     __shared__ TileScratch ws[kTilesThreads / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

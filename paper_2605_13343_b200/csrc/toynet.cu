@@ -364,7 +364,7 @@ struct ToynetModel {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // the tile stream's chain runs beside the leaf stream's on a second stream (fork / join)
     cudaStream_t side = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_lbias = nullptr;
     ~ToynetModel() {
         for (float* p : wbuf) cudaFree(p);
         for (auto& b : scratch) cudaFree(b.first);
@@ -372,6 +372,7 @@ struct ToynetModel {
         if (ev1) cudaEventDestroy(ev1);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
+        if (ev_lbias) cudaEventDestroy(ev_lbias);
         if (side) cudaStreamDestroy(side);
     }
     template <class T>
@@ -423,6 +424,7 @@ ToynetModel* toynet_model_create(const hfpg_toynet_config& cfg, uint64_t L, uint
         TCK(cudaEventCreate(&m->ev1));
         TCK(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
         TCK(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
+        TCK(cudaEventCreateWithFlags(&m->ev_lbias, cudaEventDisableTiming));
         TCK(cudaStreamCreateWithFlags(&m->side, cudaStreamNonBlocking));
     } catch (...) {
         delete m;
@@ -568,6 +570,7 @@ static void toynet_run(ToynetModel* mdl, cudaStream_t st, uint64_t n, uint64_t w
     fork();
     k_tn_leaf_bias<<<dim3(unsigned((L * L + 255) / 256), unsigned(lay.k)), 256, 0, st2>>>(
         g, lL, d_order, d_ro, d_ci, d_v, mdl->le, leaf_bias);
+    TCK(cudaEventRecord(mdl->ev_lbias, st2));  // the leaf attention waits for this one only
     if (lay.m) {
         if (pyr) {
             auto* pos = mdl->buf<double>(33, n * 2);
@@ -611,7 +614,9 @@ static void toynet_run(ToynetModel* mdl, cudaStream_t st, uint64_t n, uint64_t w
         }
         k_tn_layernorm<<<unsigned((MT * 32 + 255) / 256), 256, 0, st>>>(MT, uint32_t(d), tile_tok, ln_t, uint32_t(d));
     }
-    join();  // the biases are ready before the first attention
+    // the leaf stream's first attention needs the leaf biases; the tile biases stay queued on
+    // st2 ahead of the tile stream's attention
+    TCK(cudaStreamWaitEvent(st, mdl->ev_lbias, 0));
 
     // attention sublayer (toy_net.cpp:78-125) on `rows` tokens in windows of T; lnbuf holds
     // LN(tok) on entry and LN(tok + attention) on exit (fused into the O-projection epilogue)
@@ -712,6 +717,7 @@ static void toynet_run(ToynetModel* mdl, cudaStream_t st, uint64_t n, uint64_t w
     pgemm1<128>(st, h1, n, d, d, mdl->w_lh2, L, d, EpiStore<false>{out, uint32_t(L), nullptr});
     pgemm1<80>(st, x, n, d, d, mdl->w_heads, 2 * Ls + 1, d, EpiLeafHeads{out, lL, lLs, lay.bridge_base, lay.gate_base});
     if (lay.m) pgemm1<32>(st, tile_tok, MT, d, d, mdl->w_theads, Ls, d, EpiTileHeads{out, lLs, lay.tile_base});
+    join();  // nothing of this forward is left on st2
     TCK(cudaEventRecord(mdl->ev1, st));
     TCK(cudaStreamSynchronize(st));
 
