@@ -16,7 +16,7 @@ SO = os.path.join(HERE, "libhfpg.so")
 SRCS = ["csrc/hfpg_device.cu", "csrc/toynet.cu", "csrc/train_loop.cu", "csrc/host_structure.cpp",
         "csrc/partition_host.cpp", "csrc/ic0_host.cpp"]
 DEPS = SRCS + ["csrc/kernels.cuh", "csrc/device_common.cuh", "csrc/internal.hpp", "csrc/pcg_exact.cuh",
-               "csrc/gemm_tcgen05.cuh", "csrc/gemm_persistent.cuh", "csrc/attention_tcgen05.cuh", "csrc/solve_persistent.cuh", "csrc/comm.cuh", "csrc/partition_host.hpp", "csrc/framegen.cuh", "csrc/crmath.cuh", "csrc/toynet_kernels.cuh", "csrc/ic0.cuh", "csrc/crc32.cuh", "csrc/io_device.cuh", "csrc/train.cuh",
+               "csrc/gemm_tcgen05.cuh", "csrc/gemm_persistent.cuh", "csrc/attention_tcgen05.cuh", "csrc/leaf_coarse.cuh", "csrc/solve_persistent.cuh", "csrc/comm.cuh", "csrc/partition_host.hpp", "csrc/framegen.cuh", "csrc/crmath.cuh", "csrc/toynet_kernels.cuh", "csrc/ic0.cuh", "csrc/crc32.cuh", "csrc/io_device.cuh", "csrc/train.cuh",
                "../include/hfpg.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

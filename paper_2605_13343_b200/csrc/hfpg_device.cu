@@ -226,9 +226,27 @@ void invalidate_graph(hfpg_handle* h) {
 uint64_t leaf_grid(const hfpg_handle* h) {
     return h->fast ? std::min<uint64_t>(h->L.k, uint64_t(h->num_sms)) : h->L.k;
 }
-uint64_t prolong_grid(const hfpg_handle* h) {
-    return h->fast ? std::min<uint64_t>((h->L.k + kProlWarps - 1) / kProlWarps, uint64_t(h->num_sms) * 2)
-                   : h->L.k;
+// k_prolong_tma is the fast path's prolongation; HFPG_PROLONG_WARP=1 selects the register-
+// staged k_prolong_fast (A/B), which also serves apply calls whose vectors are not 16-byte
+// aligned (cp.async.bulk needs 16-byte aligned sources).
+bool prolong_tma_on() {
+    static const bool v = std::getenv("HFPG_PROLONG_WARP") == nullptr;
+    return v;
+}
+bool prolong_tma(const hfpg_handle* h, const double* rin, const double* zout) {
+    return h->fast && prolong_tma_on() && (reinterpret_cast<uintptr_t>(rin) & 15u) == 0 &&
+           (reinterpret_cast<uintptr_t>(zout) & 15u) == 0;
+}
+uint64_t prolong_grid(const hfpg_handle* h, bool tma = true) {
+    if (!h->fast) return h->L.k;
+    if (tma && prolong_tma_on()) return std::min<uint64_t>(h->L.k, uint64_t(h->num_sms));
+    return std::min<uint64_t>((h->L.k + kProlWarps - 1) / kProlWarps, uint64_t(h->num_sms) * 2);
+}
+void launch_prolong(hfpg_handle* h, const DevSys& s, cudaStream_t st, int mode, const double* rin, double* zout) {
+    if (prolong_tma(h, rin, zout))
+        k_prolong_tma<<<unsigned(prolong_grid(h)), kPtThreads, sizeof(ProlSmem), st>>>(s, mode, rin, zout);
+    else
+        k_prolong_fast<<<unsigned(prolong_grid(h, false)), 256, 0, st>>>(s, mode, rin, zout);
 }
 uint32_t spmv_stages() {
     static const uint32_t v = [] {
@@ -372,6 +390,7 @@ void fill_sys(hfpg_handle* h) {
     // apply stages 1-4 in one kernel (leaf_coarse.cuh) with HFPG_LEAF_COARSE=1 — measured slower
     // than the staged kernels, so opt-in only
     s.fused_leaf = s.defer && std::getenv("HFPG_LEAF_COARSE") && std::getenv("HFPG_LEAF_COARSE")[0] == '1';
+    s.bridge_first = std::getenv("HFPG_BRIDGE_FIRST") && std::getenv("HFPG_BRIDGE_FIRST")[0] == '1';
     s.sc = h->sc;
     s.history = h->history;
     s.use_cond = 0;
@@ -444,7 +463,7 @@ void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
     CK(cudaGetLastError());
     if (!(h->fast && s.fused_leaf)) launch_coarse(h, s, mode);
     if (h->fast)
-        k_prolong_fast<<<unsigned(prolong_grid(h)), 256, 0, h->lstream>>>(s, mode, rin, zout);
+        launch_prolong(h, s, h->lstream, mode, rin, zout);
     else
         k_prolong_generic<<<unsigned(L.k), 256, 2 * L.ls * sizeof(float), h->lstream>>>(s, mode, rin, zout);
     CK(cudaGetLastError());
@@ -520,6 +539,8 @@ void configure_kernels() {
         CK(cudaFuncSetAttribute(k_leaf_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(sizeof(LcSmem))));
         CK(cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CK(cudaFuncSetAttribute(k_prolong_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(sizeof(ProlSmem))));
         CK(cudaFuncSetAttribute(k_spmv_tma<kLoop>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         CK(cudaFuncSetAttribute(k_spmv_tma<kApply>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         CK(cudaFuncSetAttribute(k_leaf_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
@@ -718,7 +739,7 @@ void stage_leaf(hfpg_handle* h, int mode, const double* rin) {
     CK(cudaGetLastError());
 }
 void stage_prolong(hfpg_handle* h, int mode, const double* rin, double* zout) {
-    k_prolong_fast<<<unsigned(prolong_grid(h)), 256, 0, h->lstream>>>(h->sys, mode, rin, zout);
+    launch_prolong(h, h->sys, h->lstream, mode, rin, zout);
     CK(cudaGetLastError());
 }
 void stage_sums(hfpg_handle* h, int mode) {
@@ -2010,7 +2031,7 @@ int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out) {
             if (!(h->fast && h->sys.fused_leaf)) launch_coarse(h, h->sys, kLoop);
             CK(cudaEventRecord(ev[3], h->stream));
             if (h->fast)
-                k_prolong_fast<<<unsigned(prolong_grid(h)), 256, 0, h->stream>>>(h->sys, kLoop, nullptr, nullptr);
+                launch_prolong(h, h->sys, h->stream, kLoop, nullptr, nullptr);
             else
                 k_prolong_generic<<<unsigned(L.k), 256, 2 * L.ls * sizeof(float), h->stream>>>(h->sys, kLoop, nullptr, nullptr);
             CK(cudaEventRecord(ev[4], h->stream));

@@ -70,6 +70,7 @@ struct DevSys {
     // k_leaf_coarse (leaf_coarse.cuh) runs apply stages 1-4: r' = r - alpha Ap is then stored by
     // the prolongation (which re-forms it with the same fma) instead of the leaf kernel
     int fused_leaf;
+    int bridge_first;  // HFPG_BRIDGE_FIRST=1: the leaf kernel streams the bridges evict_first (A/B)
 };
 constexpr uint32_t kPartSpmv = 0, kPartLeaf = 2048, kPartProl = 3072, kPartLen = 4096;
 
@@ -544,8 +545,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mod
                         &sm.full[st], pol_stream);
         // bridges: evict_last — the prolongation walks the leaves in reverse and finds the
         // most recently streamed ones still in L2 (measured: evict_first makes it 10% slower)
-        tma_load_1d(&sm.B[st][0], b, kBBytes / 2, &sm.full[st], pol_keep);
-        tma_load_1d(&sm.B[st][kL * kLs], b + kL * kLs, kBBytes / 2, &sm.full[st], pol_keep);
+        const uint64_t pol_b = s.bridge_first ? pol_stream : pol_keep;
+        tma_load_1d(&sm.B[st][0], b, kBBytes / 2, &sm.full[st], pol_b);
+        tma_load_1d(&sm.B[st][kL * kLs], b + kL * kLs, kBBytes / 2, &sm.full[st], pol_b);
         tma_load_1d(sm.vec[st][0], rsrc + leaf * kL, kL * 8, &sm.full[st], pol_keep);
         if (mode == kLoop) {
             tma_load_1d(sm.vec[st][1], s.ap + leaf * kL, kL * 8, &sm.full[st], pol_stream);
@@ -1504,6 +1506,193 @@ __global__ void __launch_bounds__(256, 2) k_prolong_fast(DevSys s, int mode, con
     }
 }
 
+
+// Prolongation, TMA ring (the default fast path): one persistent CTA per SM, four producer warps
+// and sixteen consumer warps. Per leaf a producer streams Ũ_k | Ṽ_k (32 KB) and the leaf's
+// epilogue operands (y_loc, r, diag(A), Ap, gate: 4.5 KB) by cp.async.bulk into a 6-stage
+// shared-memory ring, then gathers the leaf's ancestor corrections g_r | g_c into the stage
+// (one L2 round trip; the four producers keep four gathers in flight, one producer alone was
+// gather-latency bound at 1.9 us per leaf) and arrives on the stage's full barrier; five leaves
+// stay in flight while the consumers compute one, which is what
+// k_prolong_fast's register-staged loads (two 4 KB chunks per warp) could not sustain; sixteen
+// consumer warps (eight rows each) hide the F2F / f64 / shuffle latencies (eight were issue-
+// latency bound at 0.34 IPC per scheduler). The
+// consumer arithmetic is k_prolong_fast's, lane for lane (same 8-lanes-per-row float4 split, same
+// f64 fma order and xor tree), so z is bit-identical to it; only the r.z partial's summation
+// order differs (rows are owned per warp here).
+constexpr int kPtStages = 6;
+constexpr int kPtCons = 16;  // consumer warps: warp w owns rows kPtRows w .. kPtRows w + kPtRows - 1
+constexpr int kPtRows = kL / kPtCons;
+constexpr int kPtProd = 4;  // producer warps: warp kPtCons + j stages the leaves k = j (mod kPtProd)
+constexpr int kPtThreads = (kPtCons + kPtProd) * 32;
+struct ProlSmem {
+    float B[kPtStages][2 * kL * kLs];  // Ũ_k | Ṽ_k
+    double vec[kPtStages][4][kL];       // y_loc, r, diag(A), Ap (form_r only)
+    float gate[kPtStages][kL];
+    double g[kPtStages][2 * kLs];       // g_r | g_c, rounded to fp32 as apply.cpp:154 does
+    uint64_t full[kPtStages], empty[kPtStages];
+};
+
+__global__ void __launch_bounds__(kPtThreads, 1) k_prolong_tma(DevSys s, int mode, const double* rin_ext,
+                                                               double* zout) {
+    if (prolong_skip(s, mode)) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    ProlSmem& sm = *reinterpret_cast<ProlSmem*>(smem_raw);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint64_t K = s.K, D = s.D, grid = gridDim.x;
+    const double* rsrc = mode == kApply ? rin_ext : s.r;
+    double* zdst = mode == kApply ? zout : s.z;
+    const bool form_r = mode == kLoop && s.fused_leaf;  // r' = r - alpha Ap (pcg.cpp:98) lands here
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < kPtStages; ++q) {
+            mbar_init(&sm.full[q], 2);  // the producer's expect_tx arrival + its gather arrival
+            mbar_init(&sm.empty[q], kPtCons);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    double rz = 0.0;
+    if (wid >= kPtCons) {  // ---- producer warps: several ancestor gathers in flight at once
+        const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+        const uint32_t bytes = 2 * kL * kLs * 4 + (form_r ? 4 : 3) * kL * 8 + kL * 4;
+        const uint32_t Du = uint32_t(D);
+        uint32_t k = uint32_t(wid - kPtCons);
+        for (uint64_t w = blockIdx.x + uint64_t(k) * grid; w < K; w += kPtProd * grid, k += kPtProd) {
+            const int st = int(k % kPtStages);
+            if (k >= kPtStages) mbar_wait(&sm.empty[st], (k / kPtStages - 1) & 1);
+            const uint64_t leaf = K - 1 - w, base = leaf * kL;  // reverse walk: see k_prolong_fast
+            if (lane == 0) {
+                mbar_expect_tx(&sm.full[st], bytes);
+                const float* b = s.F + s.bridge_base + leaf * (2 * kL * kLs);
+                tma_load_1d(&sm.B[st][0], b, kL * kLs * 4, &sm.full[st], pol_stream);
+                tma_load_1d(&sm.B[st][kL * kLs], b + kL * kLs, kL * kLs * 4, &sm.full[st], pol_stream);
+                tma_load_1d(sm.vec[st][0], s.y_loc + base, kL * 8, &sm.full[st], pol_stream);
+                tma_load_1d(sm.vec[st][1], rsrc + base, kL * 8, &sm.full[st], pol_keep);
+                tma_load_1d(sm.vec[st][2], s.a_diag + base, kL * 8, &sm.full[st], pol_keep);
+                if (form_r) tma_load_1d(sm.vec[st][3], s.ap + base, kL * 8, &sm.full[st], pol_stream);
+                tma_load_1d(sm.gate[st], s.F + s.gate_base + base, kL * 4, &sm.full[st], pol_keep);
+            }
+            // ancestor gather (apply.cpp:140-154), exactly k_prolong_fast's: all loads up front,
+            // partitioned top tiles first, then root -> leaf in f64
+            const uint32_t hl = uint32_t(K + leaf), lf = uint32_t(leaf);
+            float ga[kMaxDepth];
+#pragma unroll
+            for (int d = 0; d < kMaxDepth; ++d) {
+                ga[d] = 0.f;
+                if (uint32_t(d) < Du) {
+                    const uint32_t m = (hl >> (Du - d)) - 1u, right = (lf >> (Du - 1 - d)) & 1u;
+                    ga[d] = __ldcg(&s.coupled[m * 64u + right * 32u + lane]);
+                }
+            }
+            double gr = 0.0, gc = 0.0;
+            for (uint32_t d = 0; d < s.glog; ++d) {
+                const uint32_t t = ((s.G + s.rank) >> (s.glog - d)) - 1u, right = (s.rank >> (s.glog - 1 - d)) & 1u;
+                const double gv = double(__ldcg(&s.top_coupled[t * 64u + right * 32u + lane]));
+                if (right) gc += gv;
+                else gr += gv;
+            }
+#pragma unroll
+            for (int d = 0; d < kMaxDepth; ++d)
+                if (uint32_t(d) < Du) {
+                    if ((lf >> (Du - 1 - d)) & 1u) gc += double(ga[d]);
+                    else gr += double(ga[d]);
+                }
+            sm.g[st][lane] = double(float(gr));
+            sm.g[st][kLs + lane] = double(float(gc));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.full[st]);  // release: the gather is visible to the waiters
+        }
+    } else {  // ---- consumer warps
+        const int l8 = lane & 7, rsub = lane >> 3;
+        const double shift = s.sc->shift;
+        const double alpha = form_r ? s.sc->alpha : 0.0;
+        uint32_t k = 0;
+        for (uint64_t w = blockIdx.x; w < K; w += grid, ++k) {
+            const int st = int(k % kPtStages);
+            mbar_wait(&sm.full[st], (k / kPtStages) & 1);
+            const uint64_t base = (K - 1 - w) * kL;
+            double g4[4], h4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                g4[q] = sm.g[st][4 * l8 + q];
+                h4[q] = sm.g[st][kLs + 4 * l8 + q];
+            }
+            const float4* Bu = reinterpret_cast<const float4*>(sm.B[st]);
+            const float4* Bv = Bu + kL * kLs / 4;
+            // rows 8w + rsub (i = 0) and 8w + 4 + rsub (i = 1): four partial dot products per lane
+            // (Ũ, Ṽ x two rows), reduced over the row's 8 lanes by a transpose-reduce — 4 f64
+            // shuffles instead of 12, and the same pairing tree as the xor butterfly
+            // ((a0+a4)+(a2+a6))+((a1+a5)+(a3+a7)), so each sum is bit-identical to k_prolong_fast's
+            static_assert(kPtRows == 8, "two 4-row passes per warp");
+            double v[4];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int row = kPtRows * wid + 4 * i + rsub;
+                const float4 u = Bu[row * (kLs / 4) + l8], w4 = Bv[row * (kLs / 4) + l8];
+                v[2 * i] = fma(double(u.w), g4[3], fma(double(u.z), g4[2], fma(double(u.y), g4[1], double(u.x) * g4[0])));
+                v[2 * i + 1] = fma(double(w4.w), h4[3], fma(double(w4.z), h4[2], fma(double(w4.y), h4[1], double(w4.x) * h4[0])));
+            }
+            {
+                const bool hi = lane & 4;  // bit 2 keeps row pass i = 1
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const double send = hi ? v[q] : v[q + 2];
+                    const double keep = hi ? v[q + 2] : v[q];
+                    v[q] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+                }
+            }
+            {
+                const bool hi = lane & 2;  // bit 1 keeps the Ṽ sum
+                const double send = hi ? v[0] : v[1];
+                const double keep = hi ? v[1] : v[0];
+                v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+            }
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+            const double vsum = __shfl_xor_sync(0xffffffffu, v[0], 2);  // lanes with bit 1 clear: + the Ṽ sum
+            if ((lane & 3) == 0) {  // epilogue (apply.cpp:169-173): row 8w + 4 (bit 2) + rsub
+                const int row = kPtRows * wid + ((lane >> 2) & 1) * 4 + rsub;
+                double rv = sm.vec[st][1][row];
+                if (form_r) {
+                    rv = fma(-alpha, sm.vec[st][3][row], rv);
+                    s.r[base + row] = rv;
+                }
+                double y = sm.vec[st][0][row];
+                y += v[0];
+                y += vsum;
+                y += double(sm.gate[st][row]) * rv / sm.vec[st][2][row] + shift * rv;
+                zdst[base + row] = y;
+                rz = fma(rv, y, rz);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.empty[st]);
+        }
+    }
+    if (mode == kApply) return;
+    double v[1] = {rz}, tot[1];
+    if (s.defer) {  // r.z is summed by the next SpMV (beta); CTA 0 keeps the books
+        publish_partials<1>(v, s.dpart + kPartProl);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            Scalars* sc = s.sc;
+            if (mode == kInit) {
+                sc->beta = 0.0;
+                sc->k = 1;
+                if (sc->max_iters == 0) {
+                    sc->iterations = 0;
+                    sc->status = 1;
+                    sc->done = 1;
+                }
+            } else {
+                sc->k += 1;
+            }
+            if (s.use_cond) cudaGraphSetConditional(s.cond, sc->done ? 0u : 1u);
+        }
+        return;
+    }
+    if (grid_reduce_last<1>(v, s.partials, &s.counters[2], tot)) {
+        if (s.G > 1) part_prolong_epilogue(s, mode, tot[0]);
+        else if (threadIdx.x == 0) prolong_epilogue(s, mode, tot[0]);
+    }
+}
 
 __global__ void __launch_bounds__(256) k_prolong_generic(DevSys s, int mode,
                                                          const double* rin_ext, double* zout) {

@@ -24,7 +24,8 @@
 
 namespace hfpg {
 
-constexpr int kLcStages1 = 3;  // phase 1 ring: bridges + vector slices
+constexpr int kLcStages1 = 5;  // phase 1 ring: bridges + vector slices (36 KB stages)
+constexpr int kLcStages2 = 3;  // phase 2 ring: F_k + r_k, Ap_k (66 KB stages): two in flight while one computes
 struct LcSmem {
     union {
         struct {
@@ -32,14 +33,14 @@ struct LcSmem {
             double vec[kLcStages1][4][kL];
         } p1;
         struct {
-            float F[2][kL * kL];
-            double r[2][2][kL];  // r_k, Ap_k of the staged leaf
+            float F[kLcStages2][kL * kL];
+            double r[kLcStages2][2][kL];  // r_k, Ap_k of the staged leaf
         } p2;
     } u;
     float rin[kL];
     float c[kL];
     TileScratch ws[kLeafThreads / 32];
-    uint64_t full[kLcStages1];
+    uint64_t full[kLcStages1 > kLcStages2 ? kLcStages1 : kLcStages2];
 };
 
 // Tickets / arrivals of one launch (DevSys::counters[4 ..]): zero between launches.
@@ -56,8 +57,23 @@ __device__ __forceinline__ unsigned atom_add_relaxed(unsigned* p, unsigned v) {
     return old;
 }
 
+__device__ __forceinline__ unsigned long long lc_clock() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_coarse(DevSys s, int mode, const double* rin_ext) {
     if (mode != kApply && s.sc->done) return;
+    // hfpg_set_trace(h, >= 4 grid): per-CTA %globaltimer at start / end of phase 1 / end, units
+    // (>= 8 grid: + ns spent in F / sum / tile / wait units)
+    unsigned long long* tr = (s.trace && s.trace_cap >= 4 * gridDim.x) ? s.trace + (s.trace_cap >= 12 * gridDim.x ? 12 : s.trace_cap >= 8 * gridDim.x ? 8 : 4) * blockIdx.x : nullptr;
+    const bool tr8 = tr && s.trace_cap >= 8 * gridDim.x;
+    unsigned long long t_unit[4] = {0, 0, 0, 0}, t_mark = 0;
+    const bool tr12 = tr && s.trace_cap >= 12 * gridDim.x;  // + F-unit sub-phase clock64 cycles
+    long long t_sub[3] = {0, 0, 0};
+    const long long clk0 = clock64();
+    if (tr && threadIdx.x == 0) tr[0] = lc_clock();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     LcSmem& sm = *reinterpret_cast<LcSmem*>(smem_raw);
     unsigned* ctr = s.counters + 4;
@@ -163,6 +179,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_coarse(DevSys s, int m
         publish_partials<1>(v, s.dpart + kPartLeaf);
     }
     __shared__ int is_last_p1;
+    if (tr && threadIdx.x == 0) tr[1] = lc_clock();
     __syncthreads();  // restrictions / partials of this CTA before its release
     if (tid == 0) is_last_p1 = atom_add_acq_rel_gpu(&ctr[kLcP1], 1u) == grid - 1;
     // the phase-1 ring's last copies have all been consumed (every issued stage was waited on)
@@ -195,12 +212,12 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_coarse(DevSys s, int m
     // in flight, so they are simply re-initialised
     __syncthreads();
     if (tid == 0) {
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < kLcStages2; ++q) {
             asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&sm.full[q])) : "memory");
             mbar_init(&sm.full[q], 1);
         }
         fence_mbar_init();
-        for (int q = 0; q < 2; ++q)
+        for (int q = 0; q < kLcStages2; ++q)
             if (blockIdx.x + uint64_t(q) * grid < K) issue2(blockIdx.x + uint64_t(q) * grid, q);
         p1_done = epi_taken = sums_out = sums_ready = tiles_out = 0;
         epi_taken = want_epi ? 0 : 1;
@@ -209,8 +226,18 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_coarse(DevSys s, int m
     uint64_t fleaf = blockIdx.x;  // next F leaf of this CTA
     uint32_t fit = 0;
     unsigned peek_p1 = 0, peek_sums = 0;  // relaxed loads issued a unit ahead of their use
+    int last_act = -1;
+    if (tr8 && tid == 0) t_mark = lc_clock();
     for (;;) {
         if (tid == 0) {
+            if (tr8) {
+                const unsigned long long now = lc_clock();
+                if (last_act == kActF) t_unit[0] += now - t_mark;
+                else if (last_act == kActSum) t_unit[1] += now - t_mark;
+                else if (last_act == kActTile) t_unit[2] += now - t_mark;
+                // (other units' time is not recorded: slot 3 holds the F units' mbarrier waits)
+                t_mark = now;
+            }
             // the loads issued at the end of the previous unit have landed by now
             if (!p1_done && peek_p1 == grid) {
                 asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -245,6 +272,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_coarse(DevSys s, int m
                 else act = kActWait;  // tiles still blocked on sums held by running CTAs
             }
             action = act;
+            last_act = act;
             unit = u;
             // peek ahead: overlapped with the unit about to run
             if (!p1_done) peek_p1 = *reinterpret_cast<volatile unsigned*>(&ctr[kLcP1]);
@@ -258,15 +286,22 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_coarse(DevSys s, int m
             continue;
         }
         if (act == kActF) {
-            const int st = int(fit & 1);
+            const int st = int(fit % kLcStages2);
             const uint64_t leaf = fleaf;
-            mbar_wait(&sm.full[st], (fit >> 1) & 1);
+            if (tr8 && tid == 0) {
+                const unsigned long long w0 = lc_clock();
+                mbar_wait(&sm.full[st], (fit / kLcStages2) & 1);
+                t_unit[3] += lc_clock() - w0;
+            }
+            mbar_wait(&sm.full[st], (fit / kLcStages2) & 1);
             if (tid < kL) {  // r'_k exactly as phase 1 formed it
                 double rv = sm.u.p2.r[st][0][tid];
                 if (mode == kLoop) rv = fma(-alpha, sm.u.p2.r[st][1][tid], rv);
                 sm.rin[tid] = static_cast<float>(rv);
             }
+            long long c0 = clock64();
             __syncthreads();
+            long long c1 = clock64();
             const float* F = sm.u.p2.F[st];
             if (tid < kL) {  // c = F^T r: matvec_t order (apply.cpp:25-35)
                 float acc = 0.f;
@@ -275,6 +310,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_coarse(DevSys s, int m
                 sm.c[tid] = acc;
             }
             __syncthreads();
+            long long c2 = clock64();
             {   // y = F c with f64 accumulation (k_leaf_fast's transpose-reduce)
                 const float4 c4 = reinterpret_cast<const float4*>(sm.c)[lane];
                 const double c0 = c4.x, c1 = c4.y, c2 = c4.z, c3 = c4.w;
@@ -312,10 +348,20 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_coarse(DevSys s, int m
                 }
             }
             __syncthreads();  // stage consumed
+            if (tr12 && tid == 0) {
+                const long long c3 = clock64();
+                (void)c0;
+                t_sub[1] += c2 - c1;
+                t_sub[2] += c3 - c2;
+            }
             ++fit;
             fleaf += grid;
-            const uint64_t nxt = fleaf + grid;  // two leaves ahead
-            if (tid == 0 && nxt < K) issue2(nxt, st);
+            const uint64_t nxt = fleaf + uint64_t(kLcStages2 - 1) * grid;  // kLcStages2 leaves ahead
+            if (tid == 0 && nxt < K) {
+                const long long i0 = clock64();
+                issue2(nxt, st);
+                if (tr12) t_sub[0] += clock64() - i0;
+            }
             continue;
         }
         if (act == kActEpi) {  // |r|^2 over every CTA's phase-1 partial -> r0 / rel / history / stop
@@ -358,6 +404,15 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_coarse(DevSys s, int m
             }
         }
         __syncthreads();
+    }
+    if (tr && threadIdx.x == 0) {
+        tr[2] = lc_clock();
+        tr[3] = fit;
+        if (tr8)
+            for (int q = 0; q < 4; ++q) tr[4 + q] = t_unit[q];
+        if (tr12)
+            for (int q = 0; q < 3; ++q) tr[8 + q] = t_sub[q];
+        if (tr12) tr[11] = clock64() - clk0;
     }
     // leaving: the last CTA out resets the tickets for the next launch
     if (tid == 0 && atom_add_acq_rel_gpu(&ctr[kLcExit], 1u) == grid - 1)
