@@ -543,8 +543,11 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mod
         for (int q = 0; q < 4; ++q)
             tma_load_1d(&sm.F[st][q * kL * kL / 4], f + q * kL * kL / 4, kFBytes / 4,
                         &sm.full[st], pol_stream);
-        // bridges: evict_last — the prolongation walks the leaves in reverse and finds the
-        // most recently streamed ones still in L2 (measured: evict_first makes it 10% slower)
+        // bridges: evict_last, meant for the prolongation's reverse walk to find the last-
+        // streamed ones in L2. Measured (r02): no reuse — the prolongation reads all 268 MB of
+        // bridges from DRAM, and the solve time is the same with evict_first (HFPG_BRIDGE_FIRST=1,
+        // 224.9 vs 223.6 ms); an 80 MB persisting carve-out plus an access-policy window over
+        // the bridge tail did not help either (229-230 ms: the carve-out slows the SpMV).
         const uint64_t pol_b = s.bridge_first ? pol_stream : pol_keep;
         tma_load_1d(&sm.B[st][0], b, kBBytes / 2, &sm.full[st], pol_b);
         tma_load_1d(&sm.B[st][kL * kLs], b + kL * kLs, kBBytes / 2, &sm.full[st], pol_b);
