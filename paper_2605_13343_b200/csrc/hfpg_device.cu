@@ -434,9 +434,30 @@ void launch_tiles(hfpg_handle* h, const DevSys& s, int mode, uint64_t tw) {
 }
 
 // Apply stage 4: subtree kernel + (above 32 leaves) the parallel top-of-tree kernel.
+// k_coarse_coop (one cooperative launch) is the single-rank fast path's coarse stage for K >= 64;
+// HFPG_COARSE_SPLIT=1 selects k_sums_tree + k_tiles_all (A/B; also the partitioned path).
+bool coarse_coop(const hfpg_handle* h, const DevSys& s) {
+    static const bool split = std::getenv("HFPG_COARSE_SPLIT") != nullptr;
+    return h->fast && !split && s.G == 1 && h->L.k >= 64 && h->L.ls == 32;
+}
+unsigned coarse_coop_grid(const hfpg_handle* h) {
+    static const int occ = [] {
+        int o = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_coarse_coop, kTilesThreads, 0));
+        return o;
+    }();
+    if (occ < 1) throw CudaError("k_coarse_coop: no resident CTA fits an SM");
+    return unsigned(h->num_sms) * unsigned(std::min(occ, 2));
+}
 void launch_coarse(hfpg_handle* h, const DevSys& s, int mode) {
     const Layout& L = h->L;
-    if (h->fast) {
+    if (coarse_coop(h, s)) {
+        DevSys sc = s;
+        int md = mode;
+        void* args[] = {&sc, &md};
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_coarse_coop), dim3(coarse_coop_grid(h)),
+                                       dim3(kTilesThreads), args, 0, h->lstream));
+    } else if (h->fast) {
         const uint64_t R = L.k / std::min<uint64_t>(L.k, kCoarseS0);
         k_sums_tree<<<unsigned(std::min<uint64_t>(R, uint64_t(h->num_sms) * sums_ctas_per_sm())), kSumsThreads, 0, h->lstream>>>(s, mode);
         CK(cudaGetLastError());

@@ -754,8 +754,11 @@ struct alignas(16) TileScratch {
     float fr[32], fc[32];
     double coef[32];
 };
-__device__ __forceinline__ void tile_couple(const float* T, double sr_p, double sc_p, TileScratch& ws,
-                                            int lane, uint64_t pol, float* out) {
+// `sums(sr_p, sc_p)` yields the strip sums; it runs after the tile's loads are issued, so loads
+// it makes itself (k_coarse_coop) are in flight together with the tile's.
+template <class Sums>
+__device__ __forceinline__ void tile_couple_f(const float* T, Sums sums, TileScratch& ws, int lane, uint64_t pol,
+                                              float* out) {
     const float* colp = T + (lane < 16 ? 0 : kLs * 16) + (lane & 15);
     float cv[32];
 #pragma unroll
@@ -767,6 +770,8 @@ __device__ __forceinline__ void tile_couple(const float* T, double sr_p, double 
         u4[i] = ldg_hint(U + i, pol);
         v4[i] = ldg_hint(U + 128 + i, pol);
     }
+    double sr_p, sc_p;
+    sums(sr_p, sc_p);
     ws.fr[lane] = float(sr_p);  // apply.cpp:121-124 (strip sums cast to T)
     ws.fc[lane] = float(sc_p);
     __syncwarp();
@@ -797,6 +802,10 @@ __device__ __forceinline__ void tile_couple(const float* T, double sr_p, double 
     __stcg(&out[32 + lane], float(acc_c));
     __stcg(&out[lane], float(acc_r));
     __syncwarp();
+}
+__device__ __forceinline__ void tile_couple(const float* T, double sr_p, double sc_p, TileScratch& ws,
+                                            int lane, uint64_t pol, float* out) {
+    tile_couple_f(T, [&](double& a, double& b) { a = sr_p; b = sc_p; }, ws, lane, pol, out);
 }
 
 // Strip sums (apply.cpp:110-120) over this rank's bisection tree in one launch.
@@ -1128,6 +1137,109 @@ __global__ void __launch_bounds__(kTilesThreads, MINB) k_tiles_all(DevSys s, int
             bb = __ldcg(&s.node_v[r * 32 + lane]);
         }
         tile_couple(s.F + s.tile_base + m * (kLs * kLs), a, bb, ws[wid], lane, pol, s.coupled + m * 64);
+    }
+}
+
+// Coarse stage in one cooperative launch (single rank, K >= 64): replaces k_sums_tree +
+// k_tiles_all and the launch between them.
+//   A. CTA t < R sums group t's 32 restrictions pairwise into the group roots (the up-sweep's
+//      depth-dr nodes; nothing below them is stored — nothing reads it), then every CTA arrives
+//      on one counter (release).
+//   B. the group-internal tiles, one per warp: their children's strip sums are pairwise sums of
+//      at most 16 consecutive leaves' restrictions, read directly (the same left + right tree
+//      as the up-sweep, so bit-identical to the node sums k_sums_tree stores).
+//   C. the R - 1 tiles above the groups, after waiting for the counter to reach the grid size
+//      (acquire; the launch is cooperative, so every CTA is resident and the wait cannot hang),
+//      exactly as k_tiles_all does them (tile_root_sums + tile_couple).
+// CTA 0 finishes |r|^2 (deferred mode) only after the wait, i.e. after every CTA has read
+// sc->done at entry, so all CTAs agree on whether to run. The last CTA out resets the counters.
+template <int N>
+__device__ __forceinline__ double leaf_run_sum(const float* p) {  // p: first leaf's column, stride 64
+    double v[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = double(__ldcg(p + i * 64));
+#pragma unroll
+    for (int w = 1; w < N; w *= 2)
+#pragma unroll
+        for (int i = 0; i + w < N; i += 2 * w) v[i] = v[i] + v[i + w];  // heap sum: left + right
+    return v[0];
+}
+__device__ __forceinline__ double child_strip_sum(const DevSys& s, uint64_t c, int side, int lane) {
+    const uint64_t K = s.K, D = s.D;
+    if (c >= K - 1) return double(__ldcg(&s.restrict_[(c - (K - 1)) * 64 + 32 * side + lane]));
+    int dc = 0;
+    while ((2ULL << dc) <= c + 1) ++dc;
+    const uint64_t n = 1ULL << (D - dc), leaf0 = (c + 1 - (1ULL << dc)) * n;
+    const float* p = s.restrict_ + leaf0 * 64 + 32 * side + lane;
+    switch (n) {
+        case 2: return leaf_run_sum<2>(p);
+        case 4: return leaf_run_sum<4>(p);
+        case 8: return leaf_run_sum<8>(p);
+        default: return leaf_run_sum<16>(p);
+    }
+}
+
+__global__ void __launch_bounds__(kTilesThreads, 2) k_coarse_coop(DevSys s, int mode) {
+    if (mode != kApply && s.sc->done) return;  // every CTA reads the same value (see above)
+    __shared__ TileScratch ws[kTilesThreads / 32];
+    __shared__ double half[2][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint64_t pol = policy_evict_last();
+    const uint64_t K = s.K, G = gridDim.x, R = K / kCoarseS0;
+    const uint64_t dr = s.D - 5;  // depth of the group roots (32 = 2^5 leaves per group)
+    unsigned* ctr = s.counters + 12;
+    // A. group roots: warps 0-3 = (side, half of the group), lane = column
+    for (uint64_t g = blockIdx.x; g < R; g += G) {
+        double r = 0.0;
+        if (wid < 4) {
+            const int side = wid >> 1, h = wid & 1;
+            r = leaf_run_sum<16>(s.restrict_ + (g * 32 + 16 * h) * 64 + 32 * side + lane);
+            if (h) half[side][lane] = r;
+        }
+        __syncthreads();
+        if (wid == 0 || wid == 2) {
+            const int side = wid >> 1;
+            (side ? s.node_v : s.node_u)[((1ULL << dr) - 1 + g) * 32 + lane] = r + half[side][lane];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) atom_add_acq_rel_gpu(&ctr[0], 1u);
+    // B. group-internal tiles
+    for (uint64_t m = (R - 1) + uint64_t(wid) * G + blockIdx.x; m < K - 1; m += G * (kTilesThreads / 32)) {
+        tile_couple_f(
+            s.F + s.tile_base + m * (kLs * kLs),
+            [&](double& a, double& bb) {
+                a = child_strip_sum(s, 2 * m + 1, 0, lane);
+                bb = child_strip_sum(s, 2 * m + 2, 1, lane);
+            },
+            ws[wid], lane, pol, s.coupled + m * 64);
+    }
+    // C. the tiles above the groups (and CTA 0's |r|^2 epilogue) once every group root is out
+    if (blockIdx.x + 1 < R || blockIdx.x == 0) {
+        if (threadIdx.x == 0) {
+            unsigned v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&ctr[0]) : "memory");
+            } while (v < G);
+        }
+        __syncthreads();
+        __shared__ double up_sr[32], up_sc[32];
+        for (uint64_t m = blockIdx.x; m + 1 < R; m += G) {
+            tile_root_sums(s, m, R, dr, up_sr, up_sc);
+            if (wid == 0)
+                tile_couple(s.F + s.tile_base + m * (kLs * kLs), up_sr[lane], up_sc[lane], ws[0], lane, pol,
+                            s.coupled + m * 64);
+        }
+        if (s.defer && mode != kApply && blockIdx.x == 0 && wid == 0) {  // |r|^2 of the leaf kernel
+            double rr[1];
+            sum_partials<1>(s.dpart + kPartLeaf, s.grid_leaf, rr);
+            if (lane == 0) leaf_epilogue(s, mode, rr[0]);  // r0 (init) or rel / history / stop
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && atom_add_acq_rel_gpu(&ctr[1], 1u) == G - 1) {
+        ctr[0] = 0u;
+        ctr[1] = 0u;
     }
 }
 
