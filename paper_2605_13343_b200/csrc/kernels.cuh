@@ -756,22 +756,37 @@ struct alignas(16) TileScratch {
 };
 // `sums(sr_p, sc_p)` yields the strip sums; it runs after the tile's loads are issued, so loads
 // it makes itself (k_coarse_coop) are in flight together with the tile's.
-template <class Sums>
-__device__ __forceinline__ void tile_couple_f(const float* T, Sums sums, TileScratch& ws, int lane, uint64_t pol,
-                                              float* out) {
-    const float* colp = T + (lane < 16 ? 0 : kLs * 16) + (lane & 15);
+struct TileRegs {
     float cv[32];
-#pragma unroll
-    for (int p = 0; p < 32; ++p) cv[p] = ldg_f32_hint(colp + p * 16, pol);
     float4 u4[4], v4[4];
+};
+__device__ __forceinline__ void tile_load(const float* T, int lane, uint64_t pol, TileRegs& t) {
+    const float* colp = T + (lane < 16 ? 0 : kLs * 16) + (lane & 15);
+#pragma unroll
+    for (int p = 0; p < 32; ++p) t.cv[p] = ldg_f32_hint(colp + p * 16, pol);
     const float4* U = reinterpret_cast<const float4*>(T) + lane * 4;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        u4[i] = ldg_hint(U + i, pol);
-        v4[i] = ldg_hint(U + 128 + i, pol);
+        t.u4[i] = ldg_hint(U + i, pol);
+        t.v4[i] = ldg_hint(U + 128 + i, pol);
     }
+}
+__device__ __forceinline__ void tile_finish(const TileRegs& t, double sr_p, double sc_p, TileScratch& ws, int lane,
+                                            float* out);
+template <class Sums>
+__device__ __forceinline__ void tile_couple_f(const float* T, Sums sums, TileScratch& ws, int lane, uint64_t pol,
+                                              float* out) {
+    TileRegs t;
+    tile_load(T, lane, pol, t);
     double sr_p, sc_p;
     sums(sr_p, sc_p);
+    tile_finish(t, sr_p, sc_p, ws, lane, out);
+}
+__device__ __forceinline__ void tile_finish(const TileRegs& t, double sr_p, double sc_p, TileScratch& ws, int lane,
+                                            float* out) {
+    const float* cv = t.cv;
+    const float4* u4 = t.u4;
+    const float4* v4 = t.v4;
     ws.fr[lane] = float(sr_p);  // apply.cpp:121-124 (strip sums cast to T)
     ws.fc[lane] = float(sc_p);
     __syncwarp();
@@ -1120,10 +1135,10 @@ __global__ void __launch_bounds__(kTilesThreads, MINB) k_tiles_all(DevSys s, int
     if (s.G == 1) {
         __shared__ double up_sr[32], up_sc[32];
         for (uint64_t m = blockIdx.x; m + 1 < R; m += G) {
+            TileRegs t;  // warp 0's tile loads in flight during the root sums
+            if (wid == 0) tile_load(s.F + s.tile_base + m * (kLs * kLs), lane, pol, t);
             tile_root_sums(s, m, R, dr, up_sr, up_sc);
-            if (wid == 0)
-                tile_couple(s.F + s.tile_base + m * (kLs * kLs), up_sr[lane], up_sc[lane], ws[0], lane, pol,
-                            s.coupled + m * 64);
+            if (wid == 0) tile_finish(t, up_sr[lane], up_sc[lane], ws[0], lane, s.coupled + m * 64);
         }
     }
     for (uint64_t m = first + uint64_t(wid) * G + blockIdx.x; m < K - 1; m += G * (kTilesThreads / 32)) {
