@@ -122,6 +122,16 @@ __device__ __forceinline__ double ldg_stream_f64(const double* p) {
     return r;
 }
 
+// ---- programmatic dependent launch (PDL) -------------------------------------------------------
+// The solve's kernels are launched with programmatic stream serialisation (hfpg_device.cu
+// launch_k): each lets its dependent grid launch at once (launch_dependents), so the next kernel's
+// CTAs are placed and set up as this one's CTAs drain, and then waits for its own predecessor to
+// complete and flush (griddepcontrol.wait) before reading anything — a no-op without PDL.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ---- deterministic reductions ----------------------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -223,6 +223,39 @@ void invalidate_graph(hfpg_handle* h) {
     h->graph_valid = false;
 }
 
+// Kernel launch with programmatic stream serialisation (PDL, see pdl_enter in device_common.cuh)
+// for the fast path's solve kernels when HFPG_PDL=1. Off by default: measured (r02, 3D 1M, same
+// box, A/B twice) 222.7 ms per solve with PDL vs 220.9 ms without — the graph's kernel-to-kernel
+// gaps are not launch-bound. `coop` adds the cooperative attribute (k_coarse_coop).
+bool pdl_on() {
+    static const bool v = std::getenv("HFPG_PDL") && std::getenv("HFPG_PDL")[0] == '1';
+    return v;
+}
+template <class... KArgs, class... Args>
+void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool coop,
+              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    unsigned na = 0;
+    if (pdl_on()) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (coop) {
+        at[na].id = cudaLaunchAttributeCooperative;
+        at[na].val.cooperative = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    CK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 uint64_t leaf_grid(const hfpg_handle* h) {
     return h->fast ? std::min<uint64_t>(h->L.k, uint64_t(h->num_sms)) : h->L.k;
 }
@@ -244,7 +277,8 @@ uint64_t prolong_grid(const hfpg_handle* h, bool tma = true) {
 }
 void launch_prolong(hfpg_handle* h, const DevSys& s, cudaStream_t st, int mode, const double* rin, double* zout) {
     if (prolong_tma(h, rin, zout))
-        k_prolong_tma<<<unsigned(prolong_grid(h)), kPtThreads, sizeof(ProlSmem), st>>>(s, mode, rin, zout);
+        launch_k(k_prolong_tma, dim3(unsigned(prolong_grid(h))), dim3(kPtThreads), sizeof(ProlSmem), st, false, s,
+                 mode, rin, zout);
     else
         k_prolong_fast<<<unsigned(prolong_grid(h, false)), 256, 0, st>>>(s, mode, rin, zout);
 }
@@ -270,7 +304,8 @@ uint64_t spmv_grid(const hfpg_handle* h) {
 template <int MODE>
 void launch_spmv(hfpg_handle* h, const DevSys& s, const double* x, double* y) {
     if (h->spmv_stage_bytes)
-        k_spmv_tma<MODE><<<unsigned(spmv_grid(h)), kSpmvThreads, spmv_smem(h), h->lstream>>>(s, x, y);
+        launch_k(k_spmv_tma<MODE>, dim3(unsigned(spmv_grid(h))), dim3(kSpmvThreads), spmv_smem(h), h->lstream, false,
+                 s, x, y);
     else
         k_spmv<MODE><<<unsigned(spmv_grid(h)), 256, 0, h->lstream>>>(s, x, y);
 }
@@ -452,11 +487,7 @@ unsigned coarse_coop_grid(const hfpg_handle* h) {
 void launch_coarse(hfpg_handle* h, const DevSys& s, int mode) {
     const Layout& L = h->L;
     if (coarse_coop(h, s)) {
-        DevSys sc = s;
-        int md = mode;
-        void* args[] = {&sc, &md};
-        CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_coarse_coop), dim3(coarse_coop_grid(h)),
-                                       dim3(kTilesThreads), args, 0, h->lstream));
+        launch_k(k_coarse_coop, dim3(coarse_coop_grid(h)), dim3(kTilesThreads), 0, h->lstream, true, s, mode);
     } else if (h->fast) {
         const uint64_t R = L.k / std::min<uint64_t>(L.k, kCoarseS0);
         k_sums_tree<<<unsigned(std::min<uint64_t>(R, uint64_t(h->num_sms) * sums_ctas_per_sm())), kSumsThreads, 0, h->lstream>>>(s, mode);
@@ -477,7 +508,8 @@ void launch_apply(hfpg_handle* h, int mode, const double* rin, double* zout) {
     if (h->fast && s.fused_leaf) {  // stages 1-4 in one launch
         k_leaf_coarse<<<unsigned(leaf_grid(h)), kLeafThreads, sizeof(LcSmem), h->lstream>>>(s, mode, rin);
     } else if (h->fast) {
-        k_leaf_fast<<<unsigned(leaf_grid(h)), kLeafThreads, sizeof(LeafSmem), h->lstream>>>(s, mode, rin);
+        launch_k(k_leaf_fast, dim3(unsigned(leaf_grid(h))), dim3(kLeafThreads), sizeof(LeafSmem), h->lstream, false, s,
+                 mode, rin);
     } else {
         k_leaf_generic<<<unsigned(L.k), 256, 2 * L.l * sizeof(float), h->lstream>>>(s, mode, rin);
     }

@@ -318,6 +318,7 @@ __device__ __forceinline__ double sell_row_release(const double* vals, const uin
 
 template <int MODE>
 __global__ void __launch_bounds__(kSpmvThreads, HFPG_SPMV_MINB) k_spmv_tma(DevSys s, const double* xin, double* yout) {
+    pdl_enter();  // programmatic dependent launch: see device_common.cuh
     if (MODE == kLoop && s.sc->done) return;
     extern __shared__ __align__(128) unsigned char sraw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(sraw);
@@ -512,6 +513,7 @@ constexpr uint64_t kCoarseS0 = 32;  // leaves per bottom subtree (group) of the 
 
 __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf_fast(DevSys s, int mode,
                                                                const double* rin_ext) {
+    pdl_enter();  // programmatic dependent launch: see device_common.cuh
     if (mode != kApply && s.sc->done) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     LeafSmem& sm = *reinterpret_cast<LeafSmem*>(smem_raw);
@@ -1195,6 +1197,7 @@ __device__ __forceinline__ double child_strip_sum(const DevSys& s, uint64_t c, i
 }
 
 __global__ void __launch_bounds__(kTilesThreads, 2) k_coarse_coop(DevSys s, int mode) {
+    pdl_enter();  // programmatic dependent launch: see device_common.cuh
     if (mode != kApply && s.sc->done) return;  // every CTA reads the same value (see above)
     __shared__ TileScratch ws[kTilesThreads / 32];
     __shared__ double half[2][32];
@@ -1665,6 +1668,7 @@ struct ProlSmem {
 
 __global__ void __launch_bounds__(kPtThreads, 1) k_prolong_tma(DevSys s, int mode, const double* rin_ext,
                                                                double* zout) {
+    pdl_enter();  // programmatic dependent launch: see device_common.cuh
     if (prolong_skip(s, mode)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     ProlSmem& sm = *reinterpret_cast<ProlSmem*>(smem_raw);
