@@ -485,7 +485,7 @@ def run_ours(args, cfg):
     try:
         tj = json.load(open(TRAFFIC)).get(args.config, {})
         traffic = tj.get("k_leaf_fast")
-        parts = [tj.get(k) for k in ("k_leaf_fast", "k_sums_tree", "k_tiles_all", "k_prolong_fast")]
+        parts = [tj.get(k) for k in ("k_leaf_fast", "k_coarse_coop", "k_prolong_tma")]
         apply_traffic = sum(parts) if all(p is not None for p in parts) else None
     except Exception:
         pass
@@ -505,16 +505,16 @@ def run_ours(args, cfg):
                    "parallelism": f"replicas x{world} (one independent system per GPU)"},
         # headline: the whole preconditioner apply (the metric's "precond-apply HBM GB/s vs
         # peak"): B_apply = 4P + 24N algorithmic bytes over the summed device time
-        # of its launches (leaf + strip sums + tiles + prolongation); the dominant kernel below
-        "roofline": {"bound": "hbm", "kernel": "apply (k_leaf_fast + k_sums_tree + k_tiles_all + k_prolong_fast)",
+        # of its launches (leaf + coarse + prolongation); the dominant kernel below
+        "roofline": {"bound": "hbm", "kernel": "apply (k_leaf_fast + k_coarse_coop + k_prolong_tma)",
                      "achieved": apply_gbps, "peak": peak, "unit": "GB/s", "frac": apply_gbps / peak,
                      "traffic": apply_traffic, "peak_source": peak_src, "algorithmic_bytes_per_launch": b_apply,
-                     "traffic_note": "ncu DRAM read+write bytes of the apply's four launches (cold-cache standalone "
+                     "traffic_note": "ncu DRAM read+write bytes of the apply's three launches (cold-cache standalone "
                                      "launches: the bridges are read twice, once per side of the coarse stage)",
                      "dominant_kernel": {"kernel": "k_leaf_fast", "achieved": achieved, "frac": achieved / peak,
                                          "algorithmic_bytes_per_launch": leaf_bytes, "traffic": traffic},
                      "kernel_ms": {"k_spmv": ms_spmv, "k_leaf_fast": ms_leaf,
-                                   "k_coarse": ms_coarse, "k_prolong_fast": ms_prol},
+                                   "k_coarse": ms_coarse, "k_prolong": ms_prol},
                      "apply_GBps": apply_gbps,
                      "spmv_GBps": spmv_bytes / (ms_spmv * 1e-3) / 1e9,
                      "prolong_GBps": prol_bytes / (ms_prol * 1e-3) / 1e9,
@@ -685,7 +685,7 @@ def run_batch(args, cfg):
         achieved = leaf_bytes / (float(ms4[1]) * 1e-3) / 1e9
         line["roofline"].update({"kernel": "k_leaf_fast", "achieved": achieved, "frac": achieved / peak,
                                  "traffic": None, "algorithmic_bytes_per_launch": leaf_bytes,
-                                 "kernel_ms": dict(zip(["k_spmv", "k_leaf_fast", "k_coarse", "k_prolong_fast"],
+                                 "kernel_ms": dict(zip(["k_spmv", "k_leaf_fast", "k_coarse", "k_prolong"],
                                                        map(float, ms4)))})
         if world == 1 and not args.no_cpu_baseline:
             ms_it, n_it = cpu_sample(cfg, fr0, f0, args.ref_budget)

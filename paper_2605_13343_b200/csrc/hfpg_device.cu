@@ -2006,7 +2006,9 @@ int hfpg_pcg_solve_exact(hfpg_handle* h, const double* b, const hfpg_solve_confi
 int hfpg_launch_counts(hfpg_handle* h, uint32_t* per_iteration, uint32_t* per_apply) {
     return guarded([&] {
         fill_sys(h);
-        const uint32_t apply = (h->have_factors && h->fast) ? (h->sys.fused_leaf ? 2 : 4) : 3;
+        const uint32_t apply = (h->have_factors && h->fast)
+                                   ? (h->sys.fused_leaf ? 2 : coarse_coop(h, h->sys) ? 3 : 4)
+                                   : 3;
         *per_apply = apply;
         *per_iteration = h->precond == HFPG_PRECOND_FACTOR ? apply + 1 : h->precond == HFPG_PRECOND_IC0 ? 4 : 2;
         if (use_persistent(h)) {  // one k_solve launch per solve

@@ -1,6 +1,6 @@
 """Small driver for ncu: builds the bench workload, runs one short solve (max_iters=4) and
 then `reps` standalone factor-PCG iterations (hfpg_profile_iteration), so a profiler sees
-k_spmv / k_leaf_fast / k_coarse / k_prolong_fast launches in isolation.
+k_spmv_tma / k_leaf_fast / k_coarse_coop / k_prolong_tma launches in isolation.
 
     python tools/iter_driver.py [--config 3d_1m] [--reps 3]
 """
