@@ -1243,10 +1243,10 @@ __global__ void __launch_bounds__(kTilesThreads, 2) k_coarse_coop(DevSys s, int 
         __syncthreads();
         __shared__ double up_sr[32], up_sc[32];
         for (uint64_t m = blockIdx.x; m + 1 < R; m += G) {
+            TileRegs t;  // warp 0's tile loads in flight during the root sums
+            if (wid == 0) tile_load(s.F + s.tile_base + m * (kLs * kLs), lane, pol, t);
             tile_root_sums(s, m, R, dr, up_sr, up_sc);
-            if (wid == 0)
-                tile_couple(s.F + s.tile_base + m * (kLs * kLs), up_sr[lane], up_sc[lane], ws[0], lane, pol,
-                            s.coupled + m * 64);
+            if (wid == 0) tile_finish(t, up_sr[lane], up_sc[lane], ws[0], lane, s.coupled + m * 64);
         }
         if (s.defer && mode != kApply && blockIdx.x == 0 && wid == 0) {  // |r|^2 of the leaf kernel
             double rr[1];
