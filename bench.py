@@ -481,12 +481,13 @@ def run_ours(args, cfg):
     achieved = leaf_bytes / (ms_leaf * 1e-3) / 1e9
     apply_ms = ms_leaf + ms_coarse + ms_prol
     apply_gbps = b_apply / (apply_ms * 1e-3) / 1e9
-    traffic = apply_traffic = None
+    traffic = apply_traffic = spmv_traffic = None
     try:
         tj = json.load(open(TRAFFIC)).get(args.config, {})
         traffic = tj.get("k_leaf_fast")
         parts = [tj.get(k) for k in ("k_leaf_fast", "k_coarse_coop", "k_prolong_tma")]
         apply_traffic = sum(parts) if all(p is not None for p in parts) else None
+        spmv_traffic = tj.get("k_spmv_tma")
     except Exception:
         pass
     iter_ms = ms_spmv + ms_leaf + ms_coarse + ms_prol
@@ -517,6 +518,10 @@ def run_ours(args, cfg):
                                    "k_coarse": ms_coarse, "k_prolong": ms_prol},
                      "apply_GBps": apply_gbps,
                      "spmv_GBps": spmv_bytes / (ms_spmv * 1e-3) / 1e9,
+                     # sustained DRAM rate: the ncu bytes the launches actually move (the apply reads
+                     # the bridges twice, which B_apply does not count) over the same device times
+                     "apply_dram_GBps": apply_traffic / (apply_ms * 1e-3) / 1e9 if apply_traffic else None,
+                     "spmv_dram_GBps": spmv_traffic / (ms_spmv * 1e-3) / 1e9 if spmv_traffic else None,
                      "prolong_GBps": prol_bytes / (ms_prol * 1e-3) / 1e9,
                      "iteration_ms": iter_ms,
                      "solve_ms_per_iteration": (t_max / args.steps) / max(iters[-1], 1)},
