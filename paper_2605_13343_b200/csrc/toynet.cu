@@ -568,7 +568,7 @@ static void toynet_run(ToynetModel* mdl, cudaStream_t st, uint64_t n, uint64_t w
     TCK(cudaEventRecord(mdl->ev0, st));
     // ---- edge biases (toy_net.cpp:367-415) depend on the frame only: on st2, beside the encoder
     fork();
-    k_tn_leaf_bias<<<dim3(unsigned((L * L + 255) / 256), unsigned(lay.k)), 256, 0, st2>>>(
+    k_tn_leaf_bias<<<unsigned(lay.k), 256, 0, st2>>>(
         g, lL, d_order, d_ro, d_ci, d_v, mdl->le, leaf_bias);
     TCK(cudaEventRecord(mdl->ev_lbias, st2));  // the leaf attention waits for this one only
     if (lay.m) {

@@ -200,22 +200,10 @@ __device__ __forceinline__ void edge_mlp(const EdgeMlp& m, uint32_t eh, uint32_t
 // (10-bit mantissa like the tf32 products; the MLP outputs are O(1e3) at most, far inside the
 // fp16 range), pre-multiplied by log2(e) for the attention kernels' exp2 softmax: half the bytes
 // of fp32, one query row's keys contiguous. Coupling = A_{base+i, base+j} looked up in the sorted CSR row.
-__global__ void k_tn_leaf_bias(TnDims g, uint32_t lL, const uint32_t* order, const unsigned long long* ro,
-                               const uint32_t* ci, const double* v, EdgeMlp mlp, __half* bias) {
-    const uint64_t k = blockIdx.y;
-    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;  // i * L + j (L = 2^lL <= 128)
-    const uint64_t base = k << lL;
-    // the leaf's node coordinates (frame.cpp cell centres, rounded once from f64), once per CTA.
-    // The descriptors are formed in fp32: they feed an fp32 MLP whose output is stored as fp16,
-    // so f64 differences (the reference's) would only cost f64 divisions and square roots
-    __shared__ float cx[128], cy[128];
-    for (uint64_t q = threadIdx.x; q < g.L && q < 128; q += blockDim.x) {
-        const uint32_t a = order[base + q];
-        cx[q] = float((double(a % g.width) + 0.5) / double(g.width));
-        cy[q] = float((double(a / g.width) + 0.5) / double(g.height));
-    }
-    __syncthreads();
-    if (idx >= (1u << (2 * lL))) return;
+__device__ __forceinline__ void leaf_bias_pair(TnDims g, uint32_t lL, uint64_t k, uint64_t base, uint32_t idx,
+                                               const float* cx, const float* cy, const uint32_t* order,
+                                               const unsigned long long* ro, const uint32_t* ci, const double* v,
+                                               const EdgeMlp& mlp, __half* bias) {
     const uint32_t i = idx >> lL, j = idx & ((1u << lL) - 1u);
     float xa, ya, xb, yb;
     if (g.L <= 128) {
@@ -243,6 +231,27 @@ __global__ void k_tn_leaf_bias(TnDims g, uint32_t lL, const uint32_t* order, con
     for (uint32_t h = 0; h < g.heads; ++h) bk[h * L2] = __float2half_rn(out[h] * 1.4426950408889634f);
 }
 
+// One CTA per leaf, each thread walking pairs idx = i L + j with a stride of the block (so a
+// warp's stores stay contiguous in j): the coordinate prologue runs once per leaf (with a CTA per
+// 256 pairs it ran 64 times per leaf, and 32,768 short CTAs took 165 us at N = 65,536).
+__global__ void __launch_bounds__(256) k_tn_leaf_bias(TnDims g, uint32_t lL, const uint32_t* order,
+                                                      const unsigned long long* ro, const uint32_t* ci,
+                                                      const double* v, EdgeMlp mlp, __half* bias) {
+    const uint64_t k = blockIdx.x;
+    const uint64_t base = k << lL;
+    // the leaf's node coordinates (frame.cpp cell centres, rounded once from f64), once per CTA.
+    // The descriptors are formed in fp32: they feed an fp32 MLP whose output is stored as fp16,
+    // so f64 differences (the reference's) would only cost f64 divisions and square roots
+    __shared__ float cx[128], cy[128];
+    for (uint64_t q = threadIdx.x; q < g.L && q < 128; q += blockDim.x) {
+        const uint32_t a = order[base + q];
+        cx[q] = float((double(a % g.width) + 0.5) / double(g.width));
+        cy[q] = float((double(a / g.width) + 0.5) / double(g.height));
+    }
+    __syncthreads();
+    for (uint32_t idx = threadIdx.x; idx < (1u << (2 * lL)); idx += blockDim.x)  // i * L + j (L = 2^lL)
+        leaf_bias_pair(g, lL, k, base, idx, cx, cy, order, ro, ci, v, mlp, bias);
+}
 // Chunk positions of every tile (toy_net.cpp:382-414 descriptors): pos[m][side][chunk] =
 // (sum x, sum y) over the chunk's nodes (side 0: row chunks, 1: column chunks), f64. One CTA per
 // (tile, side), one warp per chunk, lanes over the chunk's nodes, fixed-order reduction.
