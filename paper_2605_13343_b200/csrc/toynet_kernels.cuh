@@ -231,27 +231,105 @@ __device__ __forceinline__ void leaf_bias_pair(TnDims g, uint32_t lL, uint64_t k
     for (uint32_t h = 0; h < g.heads; ++h) bk[h * L2] = __float2half_rn(out[h] * 1.4426950408889634f);
 }
 
-// One CTA per leaf, each thread walking pairs idx = i L + j with a stride of the block (so a
-// warp's stores stay contiguous in j): the coordinate prologue runs once per leaf (with a CTA per
-// 256 pairs it ran 64 times per leaf, and 32,768 short CTAs took 165 us at N = 65,536).
+// One CTA per leaf. Production shape (L = 128, edge_hidden = heads = 8): a pair's descriptors
+// are its cell offset (dx, dy) = (Δcol / width, Δrow / height), |d| and the coupling A_ij, and
+// A_ij = 0 for every pair but the row's few stencil neighbours. So the MLP runs once per distinct
+// offset inside the leaf's bounding box (a 16 x 8 Morton block has 31 x 15 = 465 of them, against
+// 16,384 pairs) into a shared-memory table of the 8 fp16 outputs, every pair copies its entry
+// (one 16-byte shared load, coalesced fp16 stores), and the A_ij != 0 pairs are then recomputed
+// with their coupling and overwritten (after a barrier, so the later store wins). The offsets are
+// formed as Δ/width rounded once from f64 — the reference's f64 difference of the two centres,
+// correctly rounded — instead of the difference of two rounded fp32 centres. Other shapes, or a
+// box whose table would not fit, take the per-pair path below. (Per pair, 452 instructions
+// issued at 0.83 IPC held this kernel at 151 us for the 8.4 M pairs at N = 65,536.)
+constexpr int kBiasLutCap = 2048;  // 32 KB of fp16 x 8 entries
 __global__ void __launch_bounds__(256) k_tn_leaf_bias(TnDims g, uint32_t lL, const uint32_t* order,
                                                       const unsigned long long* ro, const uint32_t* ci,
                                                       const double* v, EdgeMlp mlp, __half* bias) {
     const uint64_t k = blockIdx.x;
     const uint64_t base = k << lL;
-    // the leaf's node coordinates (frame.cpp cell centres, rounded once from f64), once per CTA.
-    // The descriptors are formed in fp32: they feed an fp32 MLP whose output is stored as fp16,
-    // so f64 differences (the reference's) would only cost f64 divisions and square roots
     __shared__ float cx[128], cy[128];
+    __shared__ int ax[128], ay[128];
+    __shared__ uint4 lut[kBiasLutCap];
+    __shared__ int box[4];
+    const bool fast = lL == 7 && g.eh == 8 && g.heads == 8;
+    if (threadIdx.x < 4) box[threadIdx.x] = (threadIdx.x & 1) ? -1 : 0x7fffffff;
+    __syncthreads();
     for (uint64_t q = threadIdx.x; q < g.L && q < 128; q += blockDim.x) {
         const uint32_t a = order[base + q];
+        // the leaf's node coordinates (frame.cpp cell centres, rounded once from f64) for the
+        // per-pair path; its cell indices for the table
         cx[q] = float((double(a % g.width) + 0.5) / double(g.width));
         cy[q] = float((double(a / g.width) + 0.5) / double(g.height));
+        ax[q] = int(a % g.width);
+        ay[q] = int(a / g.width);
+        if (fast) {
+            atomicMin(&box[0], ax[q]);
+            atomicMax(&box[1], ax[q]);
+            atomicMin(&box[2], ay[q]);
+            atomicMax(&box[3], ay[q]);
+        }
     }
     __syncthreads();
-    for (uint32_t idx = threadIdx.x; idx < (1u << (2 * lL)); idx += blockDim.x)  // i * L + j (L = 2^lL)
-        leaf_bias_pair(g, lL, k, base, idx, cx, cy, order, ro, ci, v, mlp, bias);
+    const int ex = box[1] - box[0], ey = box[3] - box[2], W = 2 * ex + 1, H = 2 * ey + 1;
+    if (!fast || W * H > kBiasLutCap) {
+        for (uint32_t idx = threadIdx.x; idx < (1u << (2 * lL)); idx += blockDim.x)  // i * L + j (L = 2^lL)
+            leaf_bias_pair(g, lL, k, base, idx, cx, cy, order, ro, ci, v, mlp, bias);
+        return;
+    }
+    auto mlp8 = [&](int ddx, int ddy, float c) {  // the 8 outputs x log2(e), packed fp16
+        const float dx = float(double(ddx) / double(g.width)), dy = float(double(ddy) / double(g.height));
+        const float dist = sqrtf(dx * dx + dy * dy);
+        float out[8];
+        edge_mlp_t<8, 8>(mlp, dx, dy, dist, c, out);
+        uint4 p;
+        __half2 h2[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            h2[t] = __floats2half2_rn(out[2 * t] * 1.4426950408889634f, out[2 * t + 1] * 1.4426950408889634f);
+        p.x = *reinterpret_cast<uint32_t*>(&h2[0]);
+        p.y = *reinterpret_cast<uint32_t*>(&h2[1]);
+        p.z = *reinterpret_cast<uint32_t*>(&h2[2]);
+        p.w = *reinterpret_cast<uint32_t*>(&h2[3]);
+        return p;
+    };
+    for (int e = threadIdx.x; e < W * H; e += blockDim.x) lut[e] = mlp8(e % W - ex, e / W - ey, 0.f);
+    __syncthreads();
+    constexpr uint64_t L2 = 1u << 14;
+    __half* bk = bias + (k * 8) * L2;  // [k][h][i][j]
+    for (uint32_t idx = 8 * threadIdx.x; idx < L2; idx += 8 * blockDim.x) {  // keys j .. j + 7 of query i
+        const uint32_t i = idx >> 7, j0 = idx & 127u;
+        __half hv[8][8];  // [key][head]
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const uint4 p = lut[(ax[i] - ax[j0 + t] + ex) + (ay[i] - ay[j0 + t] + ey) * W];
+            const __half* hp = reinterpret_cast<const __half*>(&p);
+#pragma unroll
+            for (int h = 0; h < 8; ++h) hv[t][h] = hp[h];
+        }
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {  // one 16-byte store per head: the 8 keys' fp16 biases
+            __half o[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) o[t] = hv[t][h];
+            *reinterpret_cast<uint4*>(bk + h * L2 + idx) = *reinterpret_cast<const uint4*>(o);
+        }
+    }
+    __syncthreads();  // the coupled pairs below overwrite their table entries
+    if (threadIdx.x < 128) {
+        const uint32_t i = threadIdx.x;
+        for (unsigned long long p = ro[base + i], pe = ro[base + i + 1]; p < pe; ++p) {
+            const uint32_t col = ci[p];
+            if (col < base || col >= base + 128) continue;
+            const uint32_t j = col - uint32_t(base);
+            const uint4 q = mlp8(ax[i] - ax[j], ay[i] - ay[j], float(v[p]));
+            const __half* hp = reinterpret_cast<const __half*>(&q);
+#pragma unroll
+            for (int h = 0; h < 8; ++h) bk[h * L2 + i * 128 + j] = hp[h];
+        }
+    }
 }
+
 // Chunk positions of every tile (toy_net.cpp:382-414 descriptors): pos[m][side][chunk] =
 // (sum x, sum y) over the chunk's nodes (side 0: row chunks, 1: column chunks), f64. One CTA per
 // (tile, side), one warp per chunk, lanes over the chunk's nodes, fixed-order reduction.
