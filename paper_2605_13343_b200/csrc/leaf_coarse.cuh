@@ -1,4 +1,8 @@
-// Apply stages 1-4 in one persistent kernel (single-rank fast path, L = 128, L_s = 32):
+// EXPERIMENTAL, opt-in (HFPG_LEAF_COARSE=1; not the product path): apply stages 1-4 in one
+// persistent kernel (single-rank fast path, L = 128, L_s = 32). Parity-green, but measured
+// slower than k_leaf_fast + k_coarse_coop (232 vs 171 us at 3D 1M: its F phase is compute-
+// latency bound); kept as the A/B arm behind that finding, with a per-CTA phase
+// trace (hfpg_set_trace, tools/lc_trace.py).
 //
 //   phase 1  every CTA streams the bridge pairs Ũ_k | Ṽ_k (and the leaf's PCG vector slices)
 //            of its static share of leaves: x += alpha p, r' = r - alpha Ap, |r'|^2
