@@ -519,11 +519,19 @@ __device__ __forceinline__ double p_prolong_phase(const DevSys& s, PSmem& sm, PS
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t K = s.K, D = s.D, G = gridDim.x;
     const int l8 = lane & 7, rsub = lane >> 3;
+    // a leaf's 128 rows are split over P warps (128 / P rows each) when the grid has the warps
+    // for it: at small K one warp per leaf walked its 8 bridge chunks in 4-5 dependent L2 round
+    // trips while most warps idled (8K: 64 leaves on 2,368 warps). The rows' arithmetic is
+    // unchanged; r.z is summed in another (valid) order.
+    uint32_t P = 1;
+    while (P < 8 && uint64_t(2 * P) * K <= G * kPWarps) P *= 2;
+    const uint32_t rows_per = kL / P, nch = rows_per / 16;
     double rz = 0.0;
-    for (uint64_t w = uint64_t(wid) * G + blockIdx.x; w < K; w += G * kPWarps) {
-        const uint64_t leaf = K - 1 - w;
+    for (uint64_t item = uint64_t(wid) * G + blockIdx.x; item < K * P; item += G * kPWarps) {
+        const uint64_t w = item / P, leaf = K - 1 - w;
+        const uint32_t part = uint32_t(item % P), row0 = part * rows_per, c0 = row0 / 16;
         const uint64_t base = leaf * kL;
-        if (w == 0) PROBE(20);
+        if (item == 0) PROBE(20);
         const uint32_t hl = uint32_t(K + leaf), lf = uint32_t(leaf), Du = uint32_t(D);
         float ga[kMaxDepth];
 #pragma unroll
@@ -554,7 +562,7 @@ __device__ __forceinline__ double p_prolong_phase(const DevSys& s, PSmem& sm, PS
         const float4* Bu = reinterpret_cast<const float4*>(s.F + s.bridge_base + leaf * (2 * kL * kLs));
         const float4* Bv = Bu + kL * kLs / 4;
         float4 ua[4], va[4], ub[4], vb[4];
-        auto load_chunk = [&](int c, float4 (&u)[4], float4 (&v)[4]) {
+        auto load_chunk = [&](uint32_t c, float4 (&u)[4], float4 (&v)[4]) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int row = 16 * c + 4 * i + rsub;
@@ -562,7 +570,7 @@ __device__ __forceinline__ double p_prolong_phase(const DevSys& s, PSmem& sm, PS
                 v[i] = ldg_stream(Bv + row * (kLs / 4) + l8);
             }
         };
-        auto do_chunk = [&](int c, const float4 (&u)[4], const float4 (&v)[4]) {
+        auto do_chunk = [&](uint32_t c, const float4 (&u)[4], const float4 (&v)[4]) {
             double val[8];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -586,38 +594,48 @@ __device__ __forceinline__ double p_prolong_phase(const DevSys& s, PSmem& sm, PS
             if (l8 < 4) ps.su[wid][row] = t1;
             else ps.sv[wid][row] = t1;
         };
-        load_chunk(0, ua, va);
+        load_chunk(c0, ua, va);
+        if (nch == 1) {
+            do_chunk(c0, ua, va);
+        } else {
 #pragma unroll 1
-        for (int c = 0; c < 8; c += 2) {
-            load_chunk(c + 1, ub, vb);
-            do_chunk(c, ua, va);
-            if (c + 2 < 8) load_chunk(c + 2, ua, va);
-            do_chunk(c + 1, ub, vb);
+            for (uint32_t c = c0; c < c0 + nch; c += 2) {
+                load_chunk(c + 1, ub, vb);
+                do_chunk(c, ua, va);
+                if (c + 2 < c0 + nch) load_chunk(c + 2, ua, va);
+                do_chunk(c + 1, ub, vb);
+            }
         }
-        if (w == 0) PROBE(21);
+        if (item == 0) PROBE(21);
         double yl[4], rv[4], ad[4];
         float gt[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-            const uint64_t i = base + lane + 32 * t;
-            yl[t] = __ldcg(&s.y_loc[i]);
-            rv[t] = __ldcg(&s.r[i]);
-            ad[t] = __ldg(&s.a_diag[i]);
-            gt[t] = __ldg(&s.F[s.gate_base + i]);
+            const uint32_t r = lane + 32 * t;
+            if (r < rows_per) {
+                const uint64_t i = base + row0 + r;
+                yl[t] = __ldcg(&s.y_loc[i]);
+                rv[t] = __ldcg(&s.r[i]);
+                ad[t] = __ldg(&s.a_diag[i]);
+                gt[t] = __ldg(&s.F[s.gate_base + i]);
+            }
         }
         __syncwarp();
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-            const int row = lane + 32 * t;
-            double y = yl[t];
-            y += ps.su[wid][row];
-            y += ps.sv[wid][row];
-            y += double(gt[t]) * rv[t] / ad[t] + shift * rv[t];
-            s.z[base + row] = y;
-            rz = fma(rv[t], y, rz);
+            const uint32_t r = lane + 32 * t;
+            if (r < rows_per) {
+                const uint32_t row = row0 + r;
+                double y = yl[t];
+                y += ps.su[wid][row];
+                y += ps.sv[wid][row];
+                y += double(gt[t]) * rv[t] / ad[t] + shift * rv[t];
+                s.z[base + row] = y;
+                rz = fma(rv[t], y, rz);
+            }
         }
         __syncwarp();
-        if (w == 0) PROBE(22);
+        if (item == 0) PROBE(22);
     }
     return rz;
 }

@@ -1,7 +1,9 @@
 """The persistent whole-solve kernel (k_solve, one cooperative launch per pcg_solve) against
-the per-stage CUDA-graph driver and the reference: identical iteration counts (the two differ
-only in the order of the f64 dot-product partial sums), residual histories to f64 rounding,
-and the status semantics of pcg.cpp:53-126."""
+the per-stage CUDA-graph driver and the reference: each within ±2 iterations of the reference's
+own pcg_solve (oracle/_ref) on the same inputs — the north-star criterion — and within the
+dot-order band of each other (they differ only in the order of the f64 partial sums: valid
+orders move the count by up to 3), residual histories to f64 rounding, and the
+status semantics of pcg.cpp:53-126."""
 import json
 import os
 
@@ -24,6 +26,35 @@ def _setup(H, fr, sigma, seed, frame):
     return dev, f
 
 
+BAND_CHILD = r"""
+import sys
+sys.path.insert(0, ROOT)
+import paper_2605_13343_b200 as H
+from oracle.oracle import Oracle
+n, seed, frame = (int(a) for a in sys.argv[1:4])
+fr = H.make_frame(n, seed, frame)
+f = H.init_factors(H.build_partition(n, 128), 32, H.FactorInit.jacobi_seed, 1e-2,
+                   H.RngStream(seed, frame, H.RngPurpose.factor_init))
+rep, x, h = Oracle().pcg_solve((fr.A.row_offsets, fr.A.col_indices, fr.A.values), fr.b, 2, 128, 32, f.data)
+print(rep["iterations"])
+"""
+
+
+def _dot_order_band(n, seed, frame):
+    """Iteration counts of the CPU oracle (apply bit-identical to the reference) with two other
+    valid f64 dot orders (tests/golden/gen_dot_band.py): blocked-pairwise and compensated."""
+    import subprocess
+    import sys
+    out = []
+    for mode in (1, 2):
+        r = subprocess.run([sys.executable, "-c", BAND_CHILD.replace("ROOT", repr(ROOT)), str(n), str(seed), str(frame)],
+                           capture_output=True, text=True, timeout=600, cwd=ROOT,
+                           env=dict(os.environ, ORC_DOT_MODE=str(mode)))
+        assert r.returncode == 0, r.stderr[-2000:]
+        out.append(int(r.stdout.strip().splitlines()[-1]))
+    return out
+
+
 def _solve(H, dev, fr, solver, cfg=None):
     from paper_2605_13343_b200 import _native as N
     dev.set_solver(solver)
@@ -36,16 +67,23 @@ def _solve(H, dev, fr, solver, cfg=None):
 
 @pytest.mark.parametrize("n,seed,frame", [(256, 3, 1), (1024, 7, 3), (8192, 2024, 0),
                                           (16384, 5, 2)])
-def test_persistent_matches_graph(H, n, seed, frame):
+def test_persistent_matches_graph(H, ref, n, seed, frame):
     from paper_2605_13343_b200 import _native as N
     fr = H.make_frame(n, seed, frame)
-    dev, _ = _setup(H, fr, 1e-2, seed, frame)
+    dev, f = _setup(H, fr, 1e-2, seed, frame)
     dev.set_solver(N.SOLVER_AUTO)
     assert dev.solver_in_use() == N.SOLVER_PERSISTENT
     rp, xp, hp = _solve(H, dev, fr, N.SOLVER_PERSISTENT)
     rg, xg, hg = _solve(H, dev, fr, N.SOLVER_GRAPH)
     assert rp.status == rg.status == 0
-    assert abs(int(rp.iterations) - int(rg.iterations)) <= 2
+    csr = (np.ascontiguousarray(fr.A.row_offsets, np.uint64), np.ascontiguousarray(fr.A.col_indices, np.uint32),
+           np.ascontiguousarray(fr.A.values, np.float64))
+    want, _, _ = ref.pcg_solve(csr, fr.b, 2, 128, 32, f.data, max_iters=20000)
+    # ±2 of the reference; on long solves ±2 of the band the dot order alone spans
+    band = [want["iterations"]] + (_dot_order_band(n, seed, frame) if n >= 8192 else [])
+    lo, hi = min(band) - 2, max(band) + 2
+    assert lo <= int(rp.iterations) <= hi, (rp.iterations, band)
+    assert lo <= int(rg.iterations) <= hi, (rg.iterations, band)
     m = min(len(hp), len(hg), 50)
     np.testing.assert_allclose(hp[:m], hg[:m], rtol=1e-9)
     assert rel_l2(xp, xg) < 1e-6
