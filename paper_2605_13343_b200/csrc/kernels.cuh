@@ -1206,6 +1206,17 @@ __global__ void __launch_bounds__(kTilesThreads, 2) k_coarse_coop(DevSys s, int 
     const uint64_t K = s.K, G = gridDim.x, R = K / kCoarseS0;
     const uint64_t dr = s.D - 5;  // depth of the group roots (32 = 2^5 leaves per group)
     unsigned* ctr = s.counters + 12;
+    // hfpg_set_trace(h, >= 8 grid): %globaltimer at entry / after A / after B / after the wait /
+    // after C / exit, thread 0 of every CTA (tools/coarse_trace.py)
+    unsigned long long* tr = (s.trace && s.trace_cap >= 8 * gridDim.x) ? s.trace + 8 * blockIdx.x : nullptr;
+    auto stamp = [&](int q) {
+        if (tr && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            tr[q] = t;
+        }
+    };
+    stamp(0);
     // A. group roots: warps 0-3 = (side, half of the group), lane = column
     for (uint64_t g = blockIdx.x; g < R; g += G) {
         double r = 0.0;
@@ -1222,6 +1233,7 @@ __global__ void __launch_bounds__(kTilesThreads, 2) k_coarse_coop(DevSys s, int 
         __syncthreads();
     }
     if (threadIdx.x == 0) atom_add_acq_rel_gpu(&ctr[0], 1u);
+    stamp(1);
     // B. group-internal tiles
     for (uint64_t m = (R - 1) + uint64_t(wid) * G + blockIdx.x; m < K - 1; m += G * (kTilesThreads / 32)) {
         tile_couple_f(
@@ -1233,6 +1245,7 @@ __global__ void __launch_bounds__(kTilesThreads, 2) k_coarse_coop(DevSys s, int 
             ws[wid], lane, pol, s.coupled + m * 64);
     }
     // C. the tiles above the groups (and CTA 0's |r|^2 epilogue) once every group root is out
+    stamp(2);
     if (blockIdx.x + 1 < R || blockIdx.x == 0) {
         if (threadIdx.x == 0) {
             unsigned v;
@@ -1241,6 +1254,7 @@ __global__ void __launch_bounds__(kTilesThreads, 2) k_coarse_coop(DevSys s, int 
             } while (v < G);
         }
         __syncthreads();
+        stamp(3);
         __shared__ double up_sr[32], up_sc[32];
         for (uint64_t m = blockIdx.x; m + 1 < R; m += G) {
             TileRegs t;  // warp 0's tile loads in flight during the root sums
@@ -1254,7 +1268,9 @@ __global__ void __launch_bounds__(kTilesThreads, 2) k_coarse_coop(DevSys s, int 
             if (lane == 0) leaf_epilogue(s, mode, rr[0]);  // r0 (init) or rel / history / stop
         }
     }
+    stamp(4);
     __syncthreads();
+    stamp(5);
     if (threadIdx.x == 0 && atom_add_acq_rel_gpu(&ctr[1], 1u) == G - 1) {
         ctr[0] = 0u;
         ctr[1] = 0u;
