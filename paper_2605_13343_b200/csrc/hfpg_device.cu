@@ -2058,8 +2058,12 @@ int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out) {
         require_apply_ready(h);
         ensure_workspace(h);
         fill_sys(h);
-        cudaEvent_t ev[5];
-        for (auto& e : ev) CK(cudaEventCreate(&e));
+        // every rep enqueued before one synchronisation (a per-rep host sync let the first
+        // kernel's interval absorb the host's launch latency: ~4 us per kernel at 3D 1M), the
+        // first rep a warm-up
+        const uint32_t R = std::max(reps, 1u) + 1;
+        std::vector<cudaEvent_t> evs(5 * size_t(R));
+        for (auto& e : evs) CK(cudaEventCreate(&e));
         double acc[4] = {0, 0, 0, 0};
         Scalars prof{};
         prof.rtol = 0.0;
@@ -2071,7 +2075,8 @@ int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out) {
         prof.shift = h->spd_enabled ? std::log1p(std::exp(h->spd_raw)) : 0.0;
         const Layout& L = h->L;
         const uint64_t S0 = std::min<uint64_t>(L.k, coarse_width(L));
-        for (uint32_t rep = 0; rep < std::max(reps, 1u); ++rep) {
+        for (uint32_t rep = 0; rep < R; ++rep) {
+            cudaEvent_t* ev = evs.data() + 5 * size_t(rep);
             CK(cudaMemcpyAsync(h->sc, &prof, sizeof(Scalars), cudaMemcpyHostToDevice, h->stream));
             CK(cudaEventRecord(ev[0], h->stream));
             launch_spmv<kLoop>(h, h->sys, nullptr, nullptr);
@@ -2091,15 +2096,16 @@ int hfpg_profile_iteration(hfpg_handle* h, uint32_t reps, float* ms_out) {
                 k_prolong_generic<<<unsigned(L.k), 256, 2 * L.ls * sizeof(float), h->stream>>>(h->sys, kLoop, nullptr, nullptr);
             CK(cudaEventRecord(ev[4], h->stream));
             CK(cudaGetLastError());
-            CK(cudaEventSynchronize(ev[4]));
+        }
+        CK(cudaEventSynchronize(evs.back()));
+        for (uint32_t rep = 1; rep < R; ++rep)
             for (int i = 0; i < 4; ++i) {
                 float ms = 0.f;
-                CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+                CK(cudaEventElapsedTime(&ms, evs[5 * size_t(rep) + i], evs[5 * size_t(rep) + i + 1]));
                 acc[i] += ms;
             }
-        }
-        for (int i = 0; i < 4; ++i) ms_out[i] = float(acc[i] / std::max(reps, 1u));
-        for (auto& e : ev) cudaEventDestroy(e);
+        for (int i = 0; i < 4; ++i) ms_out[i] = float(acc[i] / (R - 1));
+        for (auto& e : evs) cudaEventDestroy(e);
     });
 }
 
