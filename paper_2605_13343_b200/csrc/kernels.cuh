@@ -824,6 +824,69 @@ __device__ __forceinline__ void tile_couple(const float* T, double sr_p, double 
                                             int lane, uint64_t pol, float* out) {
     tile_couple_f(T, [&](double& a, double& b) { a = sr_p; b = sc_p; }, ws, lane, pol, out);
 }
+// Row-only variant (k_coarse_coop): a tile's 1,024 floats are loaded once, lane = row (8
+// float4 loads instead of 8 + 32 scalar column loads), and the coefficient chains read the
+// column view from a per-warp shared copy. The copy is XOR-swizzled by 16-byte chunk
+// (chunk ^ ((row >> 1) & 3)), so both the row stores and the column reads are conflict-free;
+// V sits 16 floats after U's 512 so the two half-warps' columns use different banks. Same
+// arithmetic as tile_finish, so the couplings are bit-identical.
+struct TileRows {
+    float4 u4[4], v4[4];
+};
+constexpr int kTileColFloats = 2 * 512 + 16;
+__device__ __forceinline__ int tile_sw(int row, int col) {  // swizzled offset of (row, col < 16)
+    return row * 16 + 4 * ((col >> 2) ^ ((row >> 1) & 3)) + (col & 3);
+}
+__device__ __forceinline__ void tile_load_rows(const float* T, int lane, uint64_t pol, TileRows& t) {
+    const float4* U = reinterpret_cast<const float4*>(T) + lane * 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        t.u4[i] = ldg_hint(U + i, pol);
+        t.v4[i] = ldg_hint(U + 128 + i, pol);
+    }
+}
+__device__ __forceinline__ void tile_finish_rows(const TileRows& t, double sr_p, double sc_p, TileScratch& ws,
+                                                 float* col, int lane, float* out) {
+    float* cu = col;
+    float* cvv = col + 512 + 16;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        *reinterpret_cast<float4*>(cu + tile_sw(lane, 4 * i)) = t.u4[i];
+        *reinterpret_cast<float4*>(cvv + tile_sw(lane, 4 * i)) = t.v4[i];
+    }
+    ws.fr[lane] = float(sr_p);  // apply.cpp:121-124 (strip sums cast to T)
+    ws.fc[lane] = float(sc_p);
+    __syncwarp();
+    const float* cb = lane < 16 ? cu : cvv;
+    const int q = lane & 15;
+    const float4* st4 = reinterpret_cast<const float4*>(lane < 16 ? ws.fr : ws.fc);
+    float coef = 0.f;
+#pragma unroll
+    for (int p4 = 0; p4 < 8; ++p4) {
+        const float4 sv = st4[p4];
+        coef = fmaf(cb[tile_sw(4 * p4 + 0, q)], sv.x, coef);
+        coef = fmaf(cb[tile_sw(4 * p4 + 1, q)], sv.y, coef);
+        coef = fmaf(cb[tile_sw(4 * p4 + 2, q)], sv.z, coef);
+        coef = fmaf(cb[tile_sw(4 * p4 + 3, q)], sv.w, coef);
+    }
+    ws.coef[lane] = double(coef);  // [0,16): U^T s_r, [16,32): V^T s_c
+    __syncwarp();
+    double acc_c = 0.0, acc_r = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float uu[4] = {t.u4[i].x, t.u4[i].y, t.u4[i].z, t.u4[i].w};
+        const float vv[4] = {t.v4[i].x, t.v4[i].y, t.v4[i].z, t.v4[i].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int qq = 4 * i + k;
+            acc_c += double(vv[k]) * ws.coef[qq];
+            acc_r += double(uu[k]) * ws.coef[16 + qq];
+        }
+    }
+    __stcg(&out[32 + lane], float(acc_c));
+    __stcg(&out[lane], float(acc_r));
+    __syncwarp();
+}
 
 // Strip sums (apply.cpp:110-120) over this rank's bisection tree in one launch.
 // Level 0: a CTA takes an aligned subtree of S0 = min(K, 32) leaves; warp w owns 4 of the 64 sum
@@ -1235,14 +1298,13 @@ __global__ void __launch_bounds__(kTilesThreads, 2) k_coarse_coop(DevSys s, int 
     if (threadIdx.x == 0) atom_add_acq_rel_gpu(&ctr[0], 1u);
     stamp(1);
     // B. group-internal tiles
+    __shared__ __align__(16) float colv[kTilesThreads / 32][kTileColFloats];
     for (uint64_t m = (R - 1) + uint64_t(wid) * G + blockIdx.x; m < K - 1; m += G * (kTilesThreads / 32)) {
-        tile_couple_f(
-            s.F + s.tile_base + m * (kLs * kLs),
-            [&](double& a, double& bb) {
-                a = child_strip_sum(s, 2 * m + 1, 0, lane);
-                bb = child_strip_sum(s, 2 * m + 2, 1, lane);
-            },
-            ws[wid], lane, pol, s.coupled + m * 64);
+        TileRows t;  // the tile's loads and its children's sums in flight together
+        tile_load_rows(s.F + s.tile_base + m * (kLs * kLs), lane, pol, t);
+        const double a = child_strip_sum(s, 2 * m + 1, 0, lane);
+        const double bb = child_strip_sum(s, 2 * m + 2, 1, lane);
+        tile_finish_rows(t, a, bb, ws[wid], colv[wid], lane, s.coupled + m * 64);
     }
     // C. the tiles above the groups (and CTA 0's |r|^2 epilogue) once every group root is out
     stamp(2);
