@@ -357,7 +357,7 @@ struct alignas(16) PTileScratch {
     float fr[32], fc[32];
     double coef[32];
 };
-static_assert(kPWarps * sizeof(PTileScratch) <= sizeof(PStage), "tile scratch");
+static_assert(kPWarps * sizeof(PTileScratch) + 64 * 32 * sizeof(double) <= sizeof(PStage), "tile scratch");
 __device__ __forceinline__ void p_tile(const DevSys& s, uint64_t m, double sr_p, double sc_p,
                                        PTileScratch& ws, int lane, uint64_t pol) {
     const float* T = s.F + s.tile_base + m * (kLs * kLs);
@@ -508,6 +508,62 @@ __device__ __forceinline__ void p_tiles_phase(const DevSys& s, PSmem& sm, PTileS
         }
         p_tile(s, m, a, bb, ws[wid], lane, pol);
         if (m == 0) PROBE(57);
+    }
+}
+
+// The coarse stage (apply.cpp:110-138) in ONE phase — no strip-sum pass and one grid barrier
+// less per iteration. Nothing below the group roots is stored any more:
+//   * a tile above the 32-leaf groups (m < R - 1 <= 31: one per CTA) has its CTA's 16 warps sum
+//     its children's groups straight from the restrictions, in half-groups of 16 leaves
+//     (leaf_run_sum<16>: the up-sweep's tree), then warp 0 forms each group root as the two
+//     halves' sum and the child's strip sum as the pairwise tree over its W groups — the values
+//     the up-sweep + p_root_sum produced;
+//   * a group-internal tile sums its children's <= 16 leaves itself (child_strip_sum).
+// Bit-identical couplings to p_sums_phase + p_tiles_phase (same trees, same tile arithmetic).
+__device__ __forceinline__ void p_coarse_phase(const DevSys& s, PSmem& sm, unsigned char* scr, uint64_t pol) {
+    PTileScratch* ws = reinterpret_cast<PTileScratch*>(scr);
+    double* hs = reinterpret_cast<double*>(scr + kPWarps * sizeof(PTileScratch));  // [64][32]
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint64_t K = s.K, G = gridDim.x, b = blockIdx.x;
+    const uint64_t S0 = K < kCoarseS0 ? K : kCoarseS0, R = K / S0;
+    if (R > 1 && b + 1 < R) {  // R <= 32 (the caller's condition): at most one such tile per CTA
+        const uint64_t m = b;
+        if (m == 0) PROBE(56);
+        int d = 0;
+        while ((2ULL << d) <= m + 1) ++d;
+        const uint64_t wg = R >> d, g0 = (m + 1 - (1ULL << d)) * wg, W = wg / 2;
+        for (uint64_t u = uint64_t(wid); u < 4 * W; u += kPWarps) {  // (group, half) units
+            const uint64_t gi = u >> 1, side = gi < W ? 0 : 1;
+            const float* p = s.restrict_ + ((g0 + gi) * 32 + 16 * (u & 1)) * 64 + 32 * side + lane;
+            hs[u * 32 + lane] = leaf_run_sum<16>(p);
+        }
+        __syncthreads();
+        if (wid == 0) {
+            double ga[16], gb[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                ga[i] = gb[i] = 0.0;
+                if (uint64_t(i) < W) {
+                    ga[i] = hs[(2 * i) * 32 + lane] + hs[(2 * i + 1) * 32 + lane];
+                    gb[i] = hs[(2 * (W + i)) * 32 + lane] + hs[(2 * (W + i) + 1) * 32 + lane];
+                }
+            }
+#pragma unroll
+            for (int w = 1; w < 16; w *= 2)
+#pragma unroll
+                for (int i = 0; i + w < 16; i += 2 * w)
+                    if (uint64_t(i + w) < W) {
+                        ga[i] = ga[i] + ga[i + w];
+                        gb[i] = gb[i] + gb[i + w];
+                    }
+            p_tile(s, m, ga[0], gb[0], ws[0], lane, pol);
+        }
+        if (m == 0) PROBE(57);
+    }
+    for (uint64_t m = (R - 1) + uint64_t(wid) * G + b; m < K - 1; m += G * kPWarps) {
+        const double a = child_strip_sum(s, 2 * m + 1, 0, lane);
+        const double bb = child_strip_sum(s, 2 * m + 2, 1, lane);
+        p_tile(s, m, a, bb, ws[wid], lane, pol);
     }
 }
 
@@ -750,9 +806,13 @@ __global__ void __launch_bounds__(kPThreads, 1) k_solve(DevSys s, const double* 
         return t[0];
     };
     auto apply_tail = [&]() -> double {  // apply stages 4-7 after the leaf phase's barrier
-        p_sums_phase(s, sm);
-        grid_barrier(s, bar);
-        p_tiles_phase(s, sm, reinterpret_cast<PTileScratch*>(scratch()), policy_evict_last());
+        if (s.K <= 32 * kCoarseS0) {  // R <= 32 group roots: one phase (p_coarse_phase)
+            p_coarse_phase(s, sm, scratch(), policy_evict_last());
+        } else {  // larger (forced persistent): strip sums, then every tile
+            p_sums_phase(s, sm);
+            grid_barrier(s, bar);
+            p_tiles_phase(s, sm, reinterpret_cast<PTileScratch*>(scratch()), policy_evict_last());
+        }
         grid_barrier(s, bar);
         double v[1] = {p_prolong_phase(s, sm, *reinterpret_cast<PScratchProlong*>(scratch()), __ldg(&cfg->shift))};
         double t[1];

@@ -38,15 +38,18 @@ for _ in range(2):
 t = np.zeros(cap, np.uint64)
 N.check(N.lib.hfpg_get_trace(dev.h, t.ctypes.data, cap))
 its = int(rep.iterations)
-NI, NP = 4, 5  # barriers: init [leaf, sums, tiles, prolong]; per iteration [spmv, leaf, sums, tiles, prolong]
+# barriers: init [leaf, (sums,) coarse, prolong]; per iteration [spmv, leaf, (sums,) coarse, prolong] —
+# K <= 1024 leaves run the coarse stage as one phase (p_coarse_phase), larger K as sums + tiles
+merged = fr.n // 128 <= 1024
+NI, NP = (3, 4) if merged else (4, 5)
 n_bar = min(NI + NP * (its - 1) + 2, cap - 1)
 t = t[: n_bar + 1].astype(np.float64)
 d = np.diff(t) / 1e3  # us
 init = d[:NI]
 loop = d[NI: NI + NP * ((n_bar - NI) // NP)].reshape(-1, NP)
-names = ["spmv", "leaf", "sums", "tiles", "prolong"]
+names = ["spmv", "leaf", "coarse", "prolong"] if merged else ["spmv", "leaf", "sums", "tiles", "prolong"]
 out = {"config": a.config, "n": fr.n, "iterations": its, "solve_ms": rep.wall_ms,
-       "init_us": dict(zip(["leaf", "sums", "tiles", "prolong"], init.round(2).tolist())),
+       "init_us": dict(zip(names[1:], init.round(2).tolist())),
        "loop_us_median": dict(zip(names, np.median(loop, 0).round(2).tolist())),
        "loop_us_mean": dict(zip(names, loop.mean(0).round(2).tolist())),
        "iteration_us_median": float(np.median(loop.sum(1)))}
