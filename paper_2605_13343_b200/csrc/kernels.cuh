@@ -1757,7 +1757,7 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_prolong_tma(DevSys s, int mod
     const bool form_r = mode == kLoop && s.fused_leaf;  // r' = r - alpha Ap (pcg.cpp:98) lands here
     if (threadIdx.x == 0) {
         for (int q = 0; q < kPtStages; ++q) {
-            mbar_init(&sm.full[q], 2);  // the producer's expect_tx arrival + its gather arrival
+            mbar_init(&sm.full[q], 1 + 32);  // the producer's expect_tx arrival + one per gathering lane
             mbar_init(&sm.empty[q], kPtCons);
         }
         fence_mbar_init();
@@ -1811,8 +1811,7 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_prolong_tma(DevSys s, int mod
                 }
             sm.g[st][lane] = double(float(gr));
             sm.g[st][kLs + lane] = double(float(gc));
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.full[st]);  // release: the gather is visible to the waiters
+            mbar_arrive(&sm.full[st]);  // every lane releases its own gather writes
         }
     } else {  // ---- consumer warps
         const int l8 = lane & 7, rsub = lane >> 3;
