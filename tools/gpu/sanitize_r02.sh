@@ -6,7 +6,7 @@ out=gpurun_out/sanitizer_r02.txt
 : > $out
 for spec in memcheck:apply_fast memcheck:solve_graph memcheck:solve_persistent memcheck:iteration_kernels \
             memcheck:group_apply memcheck:toynet racecheck:iteration_kernels racecheck:apply_fast \
-            synccheck:iteration_kernels synccheck:apply_fast initcheck:iteration_kernels; do
+            synccheck:iteration_kernels synccheck:apply_fast initcheck:solve_graph initcheck:solve_persistent initcheck:apply_fast; do
   tool=${spec%%:*}; case=${spec#*:}
   timeout 900 $CS --tool $tool --error-exitcode 9 python tools/sanitize_driver.py --only $case > gpurun_out/san_${tool}_${case}.log 2>&1
   rc=$?
