@@ -426,6 +426,7 @@ void fill_sys(hfpg_handle* h) {
     // than the staged kernels, so opt-in only
     s.fused_leaf = s.defer && std::getenv("HFPG_LEAF_COARSE") && std::getenv("HFPG_LEAF_COARSE")[0] == '1';
     s.bridge_first = std::getenv("HFPG_BRIDGE_FIRST") && std::getenv("HFPG_BRIDGE_FIRST")[0] == '1';
+    s.ksolve_pipe = !(std::getenv("HFPG_KSOLVE_PIPE") && std::getenv("HFPG_KSOLVE_PIPE")[0] == '0');
     s.sc = h->sc;
     s.history = h->history;
     s.use_cond = 0;

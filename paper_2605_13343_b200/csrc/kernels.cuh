@@ -71,6 +71,7 @@ struct DevSys {
     // the prolongation (which re-forms it with the same fma) instead of the leaf kernel
     int fused_leaf;
     int bridge_first;  // HFPG_BRIDGE_FIRST=1: the leaf kernel streams the bridges evict_first (A/B)
+    int ksolve_pipe;   // k_solve pipelines a CTA's leaves (default; HFPG_KSOLVE_PIPE=0: sequential, A/B)
 };
 constexpr uint32_t kPartSpmv = 0, kPartLeaf = 2048, kPartProl = 3072, kPartLen = 4096;
 

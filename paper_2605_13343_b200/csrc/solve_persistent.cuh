@@ -48,6 +48,8 @@ struct PSmem {
     double vec[2][4][kL];    // r_k, Ap_k, p_k, x_k of the staged leaf (or b_k at init)
     float rin[kL];
     float c[kL];
+    float rin2[2][kL];       // p_leaf_phase_pipe: double-buffered by leaf parity
+    float c2[2][kL];
     double red[4][kPWarps];
     double bc[4];
     uint64_t full[2];        // factors of stage s landed
@@ -341,6 +343,133 @@ __device__ __forceinline__ double p_leaf_phase(const DevSys& s, PSmem& sm, PLeaf
         }
         if (j < 4) PROBE(j * 4 + 3);
     }
+    __syncthreads();  // the last leaf's stage becomes scratch
+    return rr;
+}
+
+// Leaf phase, pipelined across the CTA's leaves (>= 2 of them): warps 0-3 (the chain group:
+// x/r update, the F^T r chains on warps 0-1, the restrictions on warp 2) run leaf j+1 while warps
+// 8-15 (the F c group, two 8-row blocks each) finish leaf j, so a leaf costs max(chains, F c)
+// instead of their sum. Stage handoff: leaf j lives in stage st_j = (it + j) & 1; the F c group
+// issues leaf j+2 (factors + vectors; for j+2 = count the next iteration's first leaf, factors
+// only) into st_j once its F c of leaf j is done; at entry leaf 1 (or, with one leaf, the wrap)
+// goes into the other stage, which the entry contract leaves free. Same entry / exit contract
+// and the same arithmetic per leaf as p_leaf_phase (rr summed by the same threads in the same
+// leaf order), so the result is bit-identical.
+//   named barriers 3 / 6 (384, by leaf parity): the chain group arrives when c(j) is written,
+//   the F c group syncs
+//   named barrier 4 (256): the F c group, after its F c of leaf j (then one thread issues)
+//   named barrier 5 (128): the chain group, rin(j) complete before the chains
+__device__ __forceinline__ double p_leaf_phase_pipe(const DevSys& s, PSmem& sm, PLeafSched& ls, int mode,
+                                                    const double* b, const double* pcur, double alpha,
+                                                    uint64_t pol_f, uint64_t pol_b, uint64_t pol_v) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t G = gridDim.x, n = ls.count;
+    double rr = 0.0;
+    const uint32_t it0 = ls.it;
+    if (tid == 0) {
+        fence_proxy_async_global();
+        p_issue_vectors(s, sm, ls.first, int(it0 & 1), mode, b, pcur, pol_v);
+        // item 1 into the other (free) stage: leaf 1 (n >= 2 here)
+        p_issue_factors(s, sm, ls.first + G, int((it0 + 1) & 1), pol_f, pol_b);
+        p_issue_vectors(s, sm, ls.first + G, int((it0 + 1) & 1), mode, b, pcur, pol_v);
+    }
+    __syncthreads();
+    if (warp < 4) {  // ---- chain group
+        for (uint64_t j = 0; j < n; ++j) {
+            const uint64_t leaf = ls.first + j * G;
+            const uint32_t itj = it0 + uint32_t(j);
+            const int st = int(itj & 1), pb = int(j & 1);
+            const uint32_t par = (itj >> 1) & 1;
+            {
+                mbar_wait(&sm.vfull[st], par);
+                const uint64_t i = leaf * kL + tid;
+                double rv = sm.vec[st][0][tid];
+                if (mode == kLoop) {  // pcg.cpp:97-98, fused
+                    s.x[i] = fma(alpha, sm.vec[st][2][tid], sm.vec[st][3][tid]);
+                    rv = fma(-alpha, sm.vec[st][1][tid], rv);
+                }
+                s.r[i] = rv;
+                rr = fma(rv, rv, rr);
+                sm.rin2[pb][tid] = static_cast<float>(rv);  // apply.cpp:90
+            }
+            mbar_wait(&sm.full[st], par);
+            named_bar_sync(5, 128);
+            const float* F = sm.st[st].F;
+            const float* B = sm.st[st].B;
+            const float4* r4 = reinterpret_cast<const float4*>(sm.rin2[pb]);
+            if (warp < 2) {
+                const int j0 = 64 * warp + 2 * lane;
+                *reinterpret_cast<float2*>(&sm.c2[pb][j0]) = chain2<kL>(F + j0, r4);
+            } else if (warp == 2) {
+                const int o = lane < 16 ? 2 * lane : kLs + 2 * (lane - 16);
+                const float* Bo = B + (lane < 16 ? 0 : kL * kLs) + 2 * (lane & 15);
+                __stcg(reinterpret_cast<float2*>(&s.restrict_[leaf * (2 * kLs) + o]), chain2<kLs>(Bo, r4));
+            }
+            // c(j) written (warps 0-1), restrictions out. Two barriers by leaf parity: the chain
+            // group may reach leaf j+1 before the F c group has synchronised on leaf j (leaf 1
+            // is staged at entry), and a hardware barrier counts arrivals, not leaves
+            if (j & 1) asm volatile("bar.arrive 6, 384;" ::: "memory");
+            else asm volatile("bar.arrive 3, 384;" ::: "memory");
+        }
+    } else if (warp >= 8) {  // ---- F c group
+        const int fw = warp - 8;
+        for (uint64_t j = 0; j < n; ++j) {
+            const uint64_t leaf = ls.first + j * G;
+            const uint32_t itj = it0 + uint32_t(j);
+            const int st = int(itj & 1), pb = int(j & 1);
+            named_bar_sync((j & 1) ? 6 : 3, 384);  // c(j) complete
+            const float* F = sm.st[st].F;
+            const float4 c4 = reinterpret_cast<const float4*>(sm.c2[pb])[lane];
+            const double c0 = c4.x, c1 = c4.y, c2 = c4.z, c3 = c4.w;
+#pragma unroll 1
+            for (int blk = fw; blk < 16; blk += 8) {  // two 8-row blocks: rows 8 blk .. 8 blk + 7
+                double v[8];
+#pragma unroll
+                for (int rI = 0; rI < 8; ++rI) {
+                    const float4 f4 = reinterpret_cast<const float4*>(F + (8 * blk + rI) * kL)[lane];
+                    v[rI] = fma(double(f4.w), c3, fma(double(f4.z), c2, fma(double(f4.y), c1, double(f4.x) * c0)));
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const bool hi = lane & 16;
+                    const double send = hi ? v[q] : v[q + 4];
+                    const double keep = hi ? v[q + 4] : v[q];
+                    v[q] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                }
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const bool hi = lane & 8;
+                    const double send = hi ? v[q] : v[q + 2];
+                    const double keep = hi ? v[q + 2] : v[q];
+                    v[q] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                }
+                {
+                    const bool hi = lane & 4;
+                    const double send = hi ? v[0] : v[1];
+                    const double keep = hi ? v[1] : v[0];
+                    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+                }
+                v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+                v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+                if ((lane & 3) == 0) {
+                    const int row = 8 * blk + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+                    __stcg(&s.y_loc[leaf * kL + row], v[0]);
+                }
+            }
+            named_bar_sync(4, 256);  // every F c read of stage st done
+            if (fw == 0 && lane == 0 && j + 2 <= n) {
+                if (j + 2 < n) {
+                    fence_proxy_async_global();
+                    p_issue_factors(s, sm, leaf + 2 * G, st, pol_f, pol_b);
+                    p_issue_vectors(s, sm, leaf + 2 * G, st, mode, b, pcur, pol_v);
+                } else {  // the next iteration's first leaf: factors only (its vectors are not out yet)
+                    p_issue_factors(s, sm, ls.first, st, pol_f, pol_b);
+                }
+            }
+        }
+    }
+    ls.it = it0 + uint32_t(n);
     __syncthreads();  // the last leaf's stage becomes scratch
     return rr;
 }
@@ -800,7 +929,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_solve(DevSys s, const double* 
     auto leaf = [&](int mode, const double* pcur, double alpha) -> double {
         const uint64_t keep = policy_evict_last();
         const uint64_t pf = s.l2_resident ? keep : policy_evict_first();
-        double v[1] = {p_leaf_phase(s, sm, ls, mode, b, pcur, alpha, pf, keep, keep)};
+        double v[1] = {ls.count >= 2 && s.ksolve_pipe ? p_leaf_phase_pipe(s, sm, ls, mode, b, pcur, alpha, pf, keep, keep)
+                                                      : p_leaf_phase(s, sm, ls, mode, b, pcur, alpha, pf, keep, keep)};
         double t[1];
         grid_reduce<1>(s, sm, bar, v, s.partials + 2 * gridDim.x, t);
         return t[0];

@@ -47,12 +47,12 @@ def apply_generic():
     H.factor_applier(f, fr.A)(fr.b)
 
 
-def solve(kind):
+def solve(kind, n=8192):
     def go():
-        fr = H.make_frame(8192, 7, 2)
+        fr = H.make_frame(n, 7, 2)
         d = H.Device(0)
         d.load_csr(fr.A)
-        d.load_factors(seeded(8192, frame=2))
+        d.load_factors(seeded(n, frame=2))
         d.set_precond(2)
         d.set_solver(kind)
         x = np.empty(fr.n)
@@ -117,6 +117,7 @@ run("apply_fast", apply_fast)
 run("apply_generic", apply_generic)
 run("solve_graph", solve(N.SOLVER_GRAPH))
 run("solve_persistent", solve(N.SOLVER_PERSISTENT))
+run("solve_persistent_pipe", solve(N.SOLVER_PERSISTENT, 65536))  # 3-4 leaves per CTA: the pipelined leaf phase
 run("iteration_kernels", iteration_kernels)
 run("group_apply", group_apply)
 run("group", group)
