@@ -1281,22 +1281,19 @@ __global__ void __launch_bounds__(kTilesThreads, 2) k_coarse_coop(DevSys s, int 
         }
     };
     stamp(0);
-    // A. group roots: warps 0-3 = (side, half of the group), lane = column
-    for (uint64_t g = blockIdx.x; g < R; g += G) {
-        double r = 0.0;
-        if (wid < 4) {
+    // A. group roots: warps 0-3 = (side, half of the group), lane = column; warps 4-7 go
+    // straight to their tiles (B), so part of the tile-factor burst starts at entry
+    if (wid < 4) {
+        for (uint64_t g = blockIdx.x; g < R; g += G) {
             const int side = wid >> 1, h = wid & 1;
-            r = leaf_run_sum<16>(s.restrict_ + (g * 32 + 16 * h) * 64 + 32 * side + lane);
+            const double r = leaf_run_sum<16>(s.restrict_ + (g * 32 + 16 * h) * 64 + 32 * side + lane);
             if (h) half[side][lane] = r;
+            named_bar_sync(1, 128);
+            if (!h) (side ? s.node_v : s.node_u)[((1ULL << dr) - 1 + g) * 32 + lane] = r + half[side][lane];
+            named_bar_sync(1, 128);  // the roots are stored (and half[] free) before the next group / the release
         }
-        __syncthreads();
-        if (wid == 0 || wid == 2) {
-            const int side = wid >> 1;
-            (side ? s.node_v : s.node_u)[((1ULL << dr) - 1 + g) * 32 + lane] = r + half[side][lane];
-        }
-        __syncthreads();
+        if (threadIdx.x == 0) atom_add_acq_rel_gpu(&ctr[0], 1u);
     }
-    if (threadIdx.x == 0) atom_add_acq_rel_gpu(&ctr[0], 1u);
     stamp(1);
     // B. group-internal tiles
     __shared__ __align__(16) float colv[kTilesThreads / 32][kTileColFloats];
